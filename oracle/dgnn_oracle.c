@@ -1,0 +1,427 @@
+/*
+ * dgnn_oracle.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain, slow, obviously-correct CPU implementation of the DiskGNN offline
+ * hot path (arXiv 2405.05231), written from the paper and from the
+ * readings fixed in DESIGN.md ("Readings of the paper").  It is the parity
+ * oracle for the CUDA path in paper_2405_05231_b200/csrc and shares NO code,
+ * header, table or helper with it.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.
+ *
+ * Citations: "P:n" = /root/reference/PAPER.md line n, "S:n" = SPEC.md line n.
+ *
+ * Every step is written in the order the method states it; library
+ * primitives used: qsort (sorting), bsearch (set membership), memcpy (row copy).
+ *
+ * Pinning (tests/test_oracle_*.py): Philox against Random123 known-answer
+ * vectors and against curand_Philox4x32_10 compiled on the host; Floyd by
+ * exhaustive enumeration of draw tuples; the sampler by the paper's Fig. 1
+ * worked example, full-fanout == BFS ball, star graph
+ * (S:58), fanout [0]; counts by S:128/S:129; tier selection by Fig. 3
+ * and by the tie-break-free optimality statement of P:226; pack and
+ * assemble by row identity with the closed-form feature generator.
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define OR_OK 0
+#define OR_EINVAL 1
+#define OR_ERANGE 2
+#define OR_ENOMEM 3
+
+#define TIER_GPU 0u
+#define TIER_HOST 1u
+#define TIER_DISK 2u
+#define TIER_SHIFT 30
+#define SLOT_MASK ((1u << TIER_SHIFT) - 1u)
+
+/* ------------------------------------------------------------------------ */
+/* Philox4x32-10 (Salmon, Moraes, Dror, Shaw, SC'11).  DESIGN.md reading c5. */
+/* ------------------------------------------------------------------------ */
+static void philox_round(uint32_t c[4], const uint32_t k[2])
+{
+    uint64_t p0 = (uint64_t)0xD2511F53u * (uint64_t)c[0];
+    uint64_t p1 = (uint64_t)0xCD9E8D57u * (uint64_t)c[2];
+    uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+    uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    uint32_t n0 = hi1 ^ c[1] ^ k[0];
+    uint32_t n1 = lo1;
+    uint32_t n2 = hi0 ^ c[3] ^ k[1];
+    uint32_t n3 = lo0;
+    c[0] = n0; c[1] = n1; c[2] = n2; c[3] = n3;
+}
+
+void oracle_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4])
+{
+    uint32_t c[4] = {ctr_in[0], ctr_in[1], ctr_in[2], ctr_in[3]};
+    uint32_t k[2] = {key_in[0], key_in[1]};
+    for (int r = 0; r < 10; ++r) {
+        if (r > 0) { k[0] += 0x9E3779B9u; k[1] += 0xBB67AE85u; }
+        philox_round(c, k);
+    }
+    out[0] = c[0]; out[1] = c[1]; out[2] = c[2]; out[3] = c[3];
+}
+
+/* One 64-bit draw keyed by (rng_seed, node v, batch bid, hop h, slot s).
+ * Counter packing = DESIGN.md reading c5/c8: ctr = {v, lo32(bid), h<<16|s, hi32(bid)},
+ * key = {lo32(seed), hi32(seed)}, result = out.y << 32 | out.x. */
+uint64_t oracle_draw64(uint64_t rng_seed, uint32_t v, uint64_t bid, uint32_t h, uint32_t s)
+{
+    uint32_t ctr[4] = {v, (uint32_t)bid, (h << 16) | (s & 0xFFFFu), (uint32_t)(bid >> 32)};
+    uint32_t key[2] = {(uint32_t)rng_seed, (uint32_t)(rng_seed >> 32)};
+    uint32_t out[4];
+    oracle_philox4x32_10(ctr, key, out);
+    return ((uint64_t)out[1] << 32) | (uint64_t)out[0];
+}
+
+/* Uniform integer in [0, n) from a 64-bit draw: floor(x * n / 2^64) (reading c6). */
+static uint64_t mulhi64(uint64_t x, uint64_t n)
+{
+    return (uint64_t)(((unsigned __int128)x * (unsigned __int128)n) >> 64);
+}
+
+static int cmp_i64(const void* a, const void* b)
+{
+    int64_t x = *(const int64_t*)a, y = *(const int64_t*)b;
+    return (x > y) - (x < y);
+}
+
+static int cmp_i32(const void* a, const void* b)
+{
+    int32_t x = *(const int32_t*)a, y = *(const int32_t*)b;
+    return (x > y) - (x < y);
+}
+
+/* Floyd's algorithm (Bentley & Floyd, CACM 30(9) 1987): a uniform k-subset of
+ * [0, d) from exactly k draws, then sorted ascending (readings c2, c7).
+ *   for s = 0..k-1: i = d-k+s; t = draw_s in [0, i]; S += (t in S) ? i : t
+ * oracle_floyd_core takes the k draws t[s] (each already in [0, d-k+s]). */
+void oracle_floyd_core(int64_t d, int32_t k, const int64_t* t, int64_t* out)
+{
+    for (int32_t s = 0; s < k; ++s) {
+        int64_t i = d - k + s;
+        int present = 0;
+        for (int32_t r = 0; r < s; ++r)
+            if (out[r] == t[s]) { present = 1; break; }
+        out[s] = present ? i : t[s];
+    }
+    qsort(out, (size_t)k, sizeof(int64_t), cmp_i64);
+}
+
+void oracle_floyd(int64_t d, int32_t k, uint64_t rng_seed, uint32_t v, uint64_t bid,
+                  uint32_t h, int64_t* out)
+{
+    int64_t* t = (int64_t*)malloc((size_t)(k > 0 ? k : 1) * sizeof(int64_t));
+    for (int32_t s = 0; s < k; ++s) {
+        int64_t i = d - k + s;
+        t[s] = (int64_t)mulhi64(oracle_draw64(rng_seed, v, bid, h, (uint32_t)s), (uint64_t)(i + 1));
+    }
+    oracle_floyd_core(d, k, t, out);
+    free(t);
+}
+
+/* ------------------------------------------------------------------------ */
+/* One graph sample (P:205 node-wise sampling).           */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+    int32_t status;
+    int32_t num_hops;
+    int64_t num_nodes;   /* n_i                                             */
+    int32_t* nodes;      /* [n_i] global IDs: seeds, then per hop new ascending (c10) */
+    int32_t* hop_off;    /* [H+2] local boundaries: 0, |seeds|, ..., n_i      */
+    int64_t num_edges;
+    int32_t* eptr;       /* [hop_off[H]+1] edges of frontier node j: eptr[j]..eptr[j+1] */
+    int32_t* src_local;  /* [num_edges] local index of the sampled neighbour (c11) */
+} oracle_batch;
+
+typedef struct { int32_t id; int32_t local; } id_local;
+
+static int cmp_id_local(const void* a, const void* b)
+{
+    int32_t x = ((const id_local*)a)->id, y = ((const id_local*)b)->id;
+    return (x > y) - (x < y);
+}
+
+static int cmp_id_only(const void* key, const void* elem)
+{
+    int32_t x = *(const int32_t*)key, y = ((const id_local*)elem)->id;
+    return (x > y) - (x < y);
+}
+
+void oracle_batch_free(oracle_batch* b)
+{
+    if (!b) return;
+    free(b->nodes); free(b->hop_off); free(b->eptr); free(b->src_local);
+    free(b);
+}
+
+/* Sample batch `bid` with seeds seeds[0..ns).  Oracle algorithm steps 2-3
+ * of DESIGN.md: the frontier at hop h is the set of nodes first discovered
+ * at hop h-1 (reading c4, following Fig. 1 P:205 where v0 does not resample). */
+oracle_batch* oracle_sample_batch(const int64_t* indptr, const int32_t* indices, int64_t num_nodes,
+                                  const int32_t* seeds, int64_t ns, const int32_t* fanout,
+                                  int32_t num_hops, uint64_t rng_seed, uint64_t bid)
+{
+    oracle_batch* B = (oracle_batch*)calloc(1, sizeof(oracle_batch));
+    if (!B) return NULL;
+    B->num_hops = num_hops;
+    B->hop_off = (int32_t*)calloc((size_t)num_hops + 2, sizeof(int32_t));
+
+    /* capacity for nodes: grows as needed */
+    int64_t cap_nodes = ns > 0 ? ns : 1;
+    B->nodes = (int32_t*)malloc((size_t)cap_nodes * sizeof(int32_t));
+    int64_t cap_edges = 16;
+    B->src_local = (int32_t*)malloc((size_t)cap_edges * sizeof(int32_t));
+    if (!B->hop_off || !B->nodes || !B->src_local) { B->status = OR_ENOMEM; return B; }
+
+    /* step 2: nodes = seeds (in input order); seeds must be valid and distinct (c12) */
+    for (int64_t i = 0; i < ns; ++i) {
+        if (seeds[i] < 0 || (int64_t)seeds[i] >= num_nodes) { B->status = OR_EINVAL; return B; }
+        B->nodes[i] = seeds[i];
+    }
+    {
+        int32_t* tmp = (int32_t*)malloc((size_t)(ns > 0 ? ns : 1) * sizeof(int32_t));
+        memcpy(tmp, seeds, (size_t)ns * sizeof(int32_t));
+        qsort(tmp, (size_t)ns, sizeof(int32_t), cmp_i32);
+        for (int64_t i = 1; i < ns; ++i)
+            if (tmp[i] == tmp[i - 1]) { free(tmp); B->status = OR_EINVAL; return B; }
+        free(tmp);
+    }
+    int64_t n = ns;
+    B->hop_off[0] = 0;
+    B->hop_off[1] = (int32_t)ns;
+
+    /* eptr is indexed by frontier local index; every node with local index
+     * < hop_off[H] is a frontier node of exactly one hop. */
+    int64_t cap_eptr = ns + 1;
+    B->eptr = (int32_t*)malloc((size_t)cap_eptr * sizeof(int32_t));
+    B->eptr[0] = 0;
+    int64_t ne = 0;
+
+    int64_t lo = 0, hi = ns; /* frontier = local [lo, hi) */
+    for (int32_t h = 0; h < num_hops; ++h) {
+        int32_t k = fanout[h];
+        /* eptr must cover frontier nodes lo..hi-1 */
+        if (hi + 1 > cap_eptr) {
+            cap_eptr = hi + 1;
+            B->eptr = (int32_t*)realloc(B->eptr, (size_t)cap_eptr * sizeof(int32_t));
+        }
+        int64_t cand_begin = ne;
+        /* step 3: per frontier node, ascending local j */
+        for (int64_t j = lo; j < hi; ++j) {
+            int32_t v = B->nodes[j];
+            int64_t start = indptr[v];
+            int64_t d = indptr[(int64_t)v + 1] - start;
+            int64_t take = (k >= d) ? d : k;
+            if (ne + take > cap_edges) {
+                while (ne + take > cap_edges) cap_edges *= 2;
+                B->src_local = (int32_t*)realloc(B->src_local, (size_t)cap_edges * sizeof(int32_t));
+            }
+            if (k >= d) {
+                for (int64_t p = 0; p < d; ++p) B->src_local[ne++] = indices[start + p]; /* c3: all positions */
+            } else {
+                int64_t* P = (int64_t*)malloc((size_t)k * sizeof(int64_t));
+                oracle_floyd(d, k, rng_seed, (uint32_t)v, bid, (uint32_t)h, P);
+                for (int32_t s = 0; s < k; ++s) B->src_local[ne++] = indices[start + P[s]];
+                free(P);
+            }
+            B->eptr[j + 1] = (int32_t)ne;
+        }
+        /* new = sorted(set(candidates) - set(nodes)) ascending global ID (c10) */
+        int64_t nc = ne - cand_begin;
+        int32_t* cs = (int32_t*)malloc((size_t)(nc > 0 ? nc : 1) * sizeof(int32_t));
+        memcpy(cs, B->src_local + cand_begin, (size_t)nc * sizeof(int32_t));
+        qsort(cs, (size_t)nc, sizeof(int32_t), cmp_i32);
+        id_local* known = (id_local*)malloc((size_t)(n > 0 ? n : 1) * sizeof(id_local));
+        for (int64_t i = 0; i < n; ++i) { known[i].id = B->nodes[i]; known[i].local = (int32_t)i; }
+        qsort(known, (size_t)n, sizeof(id_local), cmp_id_local);
+        int64_t nnew = 0;
+        for (int64_t i = 0; i < nc; ++i) {
+            if (i > 0 && cs[i] == cs[i - 1]) continue;
+            if (bsearch(&cs[i], known, (size_t)n, sizeof(id_local), cmp_id_only)) continue;
+            cs[nnew++] = cs[i]; /* compaction in place keeps ascending order */
+        }
+        free(known);
+        if (n + nnew > cap_nodes) {
+            cap_nodes = n + nnew;
+            B->nodes = (int32_t*)realloc(B->nodes, (size_t)cap_nodes * sizeof(int32_t));
+        }
+        memcpy(B->nodes + n, cs, (size_t)nnew * sizeof(int32_t));
+        free(cs);
+        int64_t n_before = n;
+        n += nnew;
+        B->hop_off[h + 2] = (int32_t)n;
+
+        /* remap this hop's candidates to local indices: local[u] = index in nodes */
+        id_local* all = (id_local*)malloc((size_t)(n > 0 ? n : 1) * sizeof(id_local));
+        for (int64_t i = 0; i < n; ++i) { all[i].id = B->nodes[i]; all[i].local = (int32_t)i; }
+        qsort(all, (size_t)n, sizeof(id_local), cmp_id_local);
+        for (int64_t e = cand_begin; e < ne; ++e) {
+            id_local* hit = (id_local*)bsearch(&B->src_local[e], all, (size_t)n, sizeof(id_local), cmp_id_only);
+            if (!hit) { free(all); B->status = OR_ERANGE; return B; }
+            B->src_local[e] = hit->local;
+        }
+        free(all);
+        lo = n_before;
+        hi = n;
+    }
+    B->num_nodes = n;
+    B->num_edges = ne;
+    return B;
+}
+
+/* Partition seeds in order into ceil(S/B) batches (reading c24) and
+ * sample batches t in [t_lo, t_hi); out[t - t_lo] receives each sample. */
+int oracle_sample_range(const int64_t* indptr, const int32_t* indices, int64_t num_nodes,
+                        const int32_t* seeds, int64_t num_seeds, int32_t batch_size,
+                        int64_t batch_id_base, const int32_t* fanout, int32_t num_hops,
+                        uint64_t rng_seed, int64_t t_lo, int64_t t_hi, int32_t threads,
+                        oracle_batch** out)
+{
+    if (batch_size <= 0 || num_hops < 1) return OR_EINVAL;
+    (void)threads;
+#pragma omp parallel for schedule(dynamic, 1) num_threads(threads > 0 ? threads : 1)
+    for (int64_t t = t_lo; t < t_hi; ++t) {
+        int64_t a = t * batch_size;
+        int64_t b = a + batch_size < num_seeds ? a + batch_size : num_seeds;
+        out[t - t_lo] = oracle_sample_batch(indptr, indices, num_nodes, seeds + a, b - a, fanout,
+                                            num_hops, rng_seed, (uint64_t)(batch_id_base + t));
+    }
+    for (int64_t t = t_lo; t < t_hi; ++t) {
+        if (!out[t - t_lo]) return OR_ENOMEM;
+        if (out[t - t_lo]->status) return out[t - t_lo]->status;
+    }
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Access frequency: counts[v] = #batches whose node set contains v          */
+/* ("keeps a counter for each node and streams the graph samples";    */
+/*  S:125; reading c14).                                                     */
+/* ------------------------------------------------------------------------ */
+void oracle_count_add(const int32_t* nodes, int64_t n, uint32_t* counts)
+{
+    for (int64_t i = 0; i < n; ++i) counts[nodes[i]] += 1u;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Tier selection ("rank the nodes by their access frequencies and     */
+/* cache more popular nodes in faster memory"; P:275-277 GPU cache = most    */
+/* popular, CPU cache = second most popular; readings c15-c17).             */
+/* ------------------------------------------------------------------------ */
+typedef struct { uint32_t count; int32_t id; } count_id;
+
+static int cmp_rank(const void* a, const void* b)
+{
+    const count_id* x = (const count_id*)a;
+    const count_id* y = (const count_id*)b;
+    if (x->count != y->count) return x->count > y->count ? -1 : 1; /* count descending */
+    return (x->id > y->id) - (x->id < y->id);                      /* then ID ascending */
+}
+
+int oracle_select_tiers(const uint32_t* counts, int64_t num_nodes, int64_t gpu_rows, int64_t host_rows,
+                        uint32_t* tier_map, int32_t* gpu_ids, int32_t* host_ids,
+                        int64_t* k_gpu, int64_t* k_host)
+{
+    if (num_nodes >= ((int64_t)1 << TIER_SHIFT) || gpu_rows < 0 || host_rows < 0) return OR_EINVAL;
+    int64_t nnz = 0;
+    for (int64_t v = 0; v < num_nodes; ++v) nnz += counts[v] > 0;
+    count_id* order = (count_id*)malloc((size_t)(nnz > 0 ? nnz : 1) * sizeof(count_id));
+    if (!order) return OR_ENOMEM;
+    int64_t m = 0;
+    for (int64_t v = 0; v < num_nodes; ++v)
+        if (counts[v] > 0) { order[m].count = counts[v]; order[m].id = (int32_t)v; ++m; }
+    qsort(order, (size_t)nnz, sizeof(count_id), cmp_rank);
+    int64_t kg = gpu_rows < nnz ? gpu_rows : nnz;
+    int64_t kh = host_rows < nnz - kg ? host_rows : nnz - kg;
+    for (int64_t i = 0; i < kg; ++i) gpu_ids[i] = order[i].id;
+    for (int64_t i = 0; i < kh; ++i) host_ids[i] = order[kg + i].id;
+    free(order);
+    /* slots: position in the tier's ascending-ID list (c17) */
+    qsort(gpu_ids, (size_t)kg, sizeof(int32_t), cmp_i32);
+    qsort(host_ids, (size_t)kh, sizeof(int32_t), cmp_i32);
+    for (int64_t v = 0; v < num_nodes; ++v) tier_map[v] = TIER_DISK << TIER_SHIFT;
+    for (int64_t s = 0; s < kg; ++s) tier_map[gpu_ids[s]] = (TIER_GPU << TIER_SHIFT) | (uint32_t)s;
+    for (int64_t s = 0; s < kh; ++s) tier_map[host_ids[s]] = (TIER_HOST << TIER_SHIFT) | (uint32_t)s;
+    *k_gpu = kg;
+    *k_host = kh;
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Address table of one batch ("interpreted address tables"):  */
+/* addr[j] = tier<<30 | slot; DISK slot = rank among the batch's DISK nodes  */
+/* in local order; P = the DISK nodes in local order (reading c21).          */
+/* Returns |P|.                                                              */
+/* ------------------------------------------------------------------------ */
+int64_t oracle_classify(const int32_t* nodes, int64_t n, const uint32_t* tier_map,
+                        uint32_t* addr, int32_t* packed)
+{
+    int64_t p = 0;
+    for (int64_t j = 0; j < n; ++j) {
+        uint32_t t = tier_map[nodes[j]];
+        if ((t >> TIER_SHIFT) == TIER_DISK) {
+            addr[j] = (TIER_DISK << TIER_SHIFT) | (uint32_t)p;
+            packed[p++] = nodes[j];
+        } else {
+            addr[j] = t;
+        }
+    }
+    return p;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Batched packing of one packing group ("collect all node features   */
+/* it requires and store them contiguously"): chunk i starts at   */
+/* chunk_off[i], chunk_off[i+1] = roundup(chunk_off[i] + |P_i|*row_bytes,    */
+/* 4096) (reading c20); padding bytes are zero.                             */
+/* ------------------------------------------------------------------------ */
+void oracle_chunk_offsets(const int64_t* packed_rows, int64_t nb, int64_t row_bytes, int64_t* chunk_off)
+{
+    chunk_off[0] = 0;
+    for (int64_t i = 0; i < nb; ++i) {
+        int64_t end = chunk_off[i] + packed_rows[i] * row_bytes;
+        chunk_off[i + 1] = (end + 4095) / 4096 * 4096;
+    }
+}
+
+void oracle_pack(const uint8_t* features, int64_t row_bytes, const int32_t* packed_concat,
+                 const int64_t* packed_rows, int64_t nb, const int64_t* chunk_off, uint8_t* group_buf)
+{
+    memset(group_buf, 0, (size_t)chunk_off[nb]);
+    int64_t r0 = 0;
+    for (int64_t i = 0; i < nb; ++i) {
+        for (int64_t r = 0; r < packed_rows[i]; ++r)
+            memcpy(group_buf + chunk_off[i] + r * row_bytes,
+                   features + (int64_t)packed_concat[r0 + r] * row_bytes, (size_t)row_bytes);
+        r0 += packed_rows[i];
+    }
+}
+
+/* out[s] = features[ids[s]] (tier buffers as "special mini-batches", P:443;
+ * direct-gather assembly out[j] = features[nodes[j]]). */
+void oracle_gather_rows(const uint8_t* features, int64_t row_bytes, const int32_t* ids, int64_t n,
+                        uint8_t* out)
+{
+    for (int64_t s = 0; s < n; ++s)
+        memcpy(out + s * row_bytes, features + (int64_t)ids[s] * row_bytes, (size_t)row_bytes);
+}
+
+/* Three-source reconstruction (Fig. 3): the GPU reads the GPU
+ * cache, the CPU cache and the partial input (this batch's chunk). */
+int oracle_assemble_tiers(const uint32_t* addr, int64_t n, const uint8_t* gpu_buf, int64_t k_gpu,
+                          const uint8_t* host_buf, int64_t k_host, const uint8_t* chunk, int64_t chunk_rows,
+                          int64_t row_bytes, uint8_t* out)
+{
+    for (int64_t j = 0; j < n; ++j) {
+        uint32_t t = addr[j] >> TIER_SHIFT, s = addr[j] & SLOT_MASK;
+        const uint8_t* src;
+        if (t == TIER_GPU && s < k_gpu) src = gpu_buf + (int64_t)s * row_bytes;
+        else if (t == TIER_HOST && s < k_host) src = host_buf + (int64_t)s * row_bytes;
+        else if (t == TIER_DISK && s < chunk_rows) src = chunk + (int64_t)s * row_bytes;
+        else return OR_ERANGE; /* unresolvable address */
+        memcpy(out + j * row_bytes, src, (size_t)row_bytes);
+    }
+    return OR_OK;
+}
