@@ -1,0 +1,272 @@
+/*
+ * dgnn.h -- C ABI of the B200-native DiskGNN offline hot path (libdgnn.so).
+ *
+ * The path (DiskGNN, arXiv 2405.05231; PAPER.md cited as P:n, SPEC.md as S:n):
+ *   a1-a3  dgnn_sample       offline K-hop node-wise neighbour sampling of many
+ *                             mini-batches (Sec. 2; Sec. 3) with the
+ *                             per-node access counter fused in (Sec. 4).
+ *   a4-a5  dgnn_build_cache  popularity ranking: most popular nodes -> GPU cache, next
+ *                             most popular -> CPU (host) cache.
+ *   a6     dgnn_classify     per-batch "interpreted address tables" (Sec. 6) and
+ *                             the list of each batch's disk-resident features.
+ *   a7     dgnn_pack         batched feature packing into per-batch contiguous chunks,
+ *                             and the tier buffers as "special mini-batches" (P:228-230,
+ *                             P:437-443 Sec. 5.2).
+ *   a8     dgnn_stage_*      moving chunks to/from the disk tier (pinned host memory or a
+ *                             file) on a side stream.
+ *   a9     dgnn_assemble     feature assembly from GPU cache, CPU cache (UVA) and the
+ *                             staged partial input (Sec. 4, Fig. 3).
+ * The exact semantics (RNG keying, node order, tie-breaks, chunk layout) are the
+ * readings c1-c26 listed in DESIGN.md; the CPU oracle in oracle/ implements them
+ * independently and the GPU results are required to be byte-identical to it.
+ *
+ * Conventions
+ *  - Every call returns dgnn_status; nothing throws across the boundary.  On a non-OK
+ *    status, dgnn_last_error() returns a thread-local message.
+ *  - "device" pointers are CUDA device pointers of the ctx's device; "host" pointers are
+ *    ordinary CPU memory; "UVA" pointers may be either device memory or pinned host
+ *    memory mapped into the device address space (cudaHostAlloc / cudaHostRegister).
+ *  - All work is enqueued on the ctx stream (see dgnn_ctx_create) unless stated;
+ *    inputs are borrowed and must stay valid until that stream has passed the call.
+ *  - Variable-size outputs (dgnn_samples, dgnn_cache_plan) are library-owned, allocated
+ *    with the ctx allocator and released by *_free; they must not outlive their ctx.
+ *    Fixed-size outputs are caller-allocated.
+ *  - Node IDs are int32, N < 2^30 (the address encoding keeps 30 slot bits).
+ *  - Feature rows are opaque bytes: row_bytes > 0 and a multiple of 4; rows are copied,
+ *    never combined, so every result is bit-exact.
+ */
+#ifndef DGNN_H
+#define DGNN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    DGNN_OK = 0,
+    DGNN_EINVAL = 1,       /* argument / precondition violation                    */
+    DGNN_ERANGE = 2,       /* unresolvable node address                    */
+    DGNN_ENOMEM = 3,       /* allocation failed                                           */
+    DGNN_ECUDA = 4,        /* CUDA runtime error                                          */
+    DGNN_ECOMM = 5,        /* collective failure (reserved for the sharded tier)          */
+    DGNN_EIO = 6,          /* file staging I/O error                                      */
+    DGNN_EUNSUPPORTED = 7  /* configuration outside the implemented envelope              */
+} dgnn_status;
+
+/* Address encoding (reading c18): addr = tier << 30 | slot. */
+#define DGNN_TIER_GPU 0u
+#define DGNN_TIER_HOST 1u
+#define DGNN_TIER_DISK 2u
+#define DGNN_TIER_SHIFT 30
+#define DGNN_SLOT_MASK ((1u << DGNN_TIER_SHIFT) - 1u)
+
+/* Kernel families, for dgnn_ctx_kernel_stats (per-launch CUDA-event timing). */
+typedef enum {
+    DGNN_K_SCAN = 0,        /* decoupled look-back prefix scan (all scans)             */
+    DGNN_K_SAMPLE_SEED,     /* seed insertion / validation                             */
+    DGNN_K_SAMPLE_HOP,      /* a2: Philox + Floyd draw, CSR gather, dedup insert, count */
+    DGNN_K_SAMPLE_ORDER,    /* a3: bucket order of new nodes (hist, scatter, sort)      */
+    DGNN_K_SAMPLE_REMAP,    /* a3: global -> local remap of sampled edges               */
+    DGNN_K_SAMPLE_COMPACT,  /* a3: batch-major output compaction                        */
+    DGNN_K_SAMPLE_SETUP,    /* per-hop bookkeeping (1-block kernels)                    */
+    DGNN_K_CACHE_HIST,      /* a4: count histogram                                      */
+    DGNN_K_CACHE_SELECT,    /* a5: tier membership + slots                              */
+    DGNN_K_CLASSIFY,        /* a6: address tables + packed lists                        */
+    DGNN_K_PACK,            /* a7: batched pack gather (the HBM-bound kernel)           */
+    DGNN_K_GATHER,          /* a7: tier-buffer gather ("special mini-batches")          */
+    DGNN_K_ASSEMBLE,        /* a9: three-source assembly                                */
+    DGNN_K_MISC,            /* memsets and small helpers                                */
+    DGNN_K_NUM
+} dgnn_kernel_id;
+
+typedef struct dgnn_ctx dgnn_ctx;
+typedef struct dgnn_samples dgnn_samples;
+typedef struct dgnn_cache_plan dgnn_cache_plan;
+
+/* Optional device allocator (e.g. a framework's caching allocator).  alloc must return
+ * device memory usable on `stream` (a cudaStream_t) or NULL; free receives the same
+ * pointer and size.  When NULL is passed to dgnn_ctx_create, cudaMallocAsync /
+ * cudaFreeAsync on the ctx stream are used. */
+typedef void* (*dgnn_alloc_fn)(size_t bytes, void* stream, void* user);
+typedef void (*dgnn_free_fn)(void* ptr, size_t bytes, void* stream, void* user);
+typedef struct {
+    dgnn_alloc_fn alloc;
+    dgnn_free_fn free;
+    void* user;
+} dgnn_allocator;
+
+/* ------------------------------------------------------------------ context ---- */
+/* Create a context on CUDA device `device` enqueuing on `stream` (a cudaStream_t;
+ * NULL = the context creates its own non-blocking stream).  A second, internal side
+ * stream carries staging copies (a8).  One ctx per host thread. */
+dgnn_status dgnn_ctx_create(int device, void* stream, const dgnn_allocator* allocator, dgnn_ctx** out);
+void dgnn_ctx_destroy(dgnn_ctx* ctx);
+dgnn_status dgnn_ctx_set_stream(dgnn_ctx* ctx, void* stream);
+void* dgnn_ctx_stream(const dgnn_ctx* ctx);
+void* dgnn_ctx_side_stream(const dgnn_ctx* ctx);
+/* Synchronize the ctx stream and report deferred device-side errors (e.g. an
+ * unresolvable address seen by dgnn_assemble -> DGNN_ERANGE). */
+dgnn_status dgnn_ctx_sync(dgnn_ctx* ctx);
+/* Thread-local message for the last non-OK status returned on this thread. */
+const char* dgnn_last_error(void);
+/* Tuning knob: batches sampled concurrently per sampling group (0 = automatic). */
+dgnn_status dgnn_ctx_set_sample_group(dgnn_ctx* ctx, int32_t batches);
+
+/* Statistics: number of kernels this ctx has launched; optional per-launch CUDA-event
+ * timing on the ctx stream (enable before the region of interest). */
+int64_t dgnn_ctx_launches(const dgnn_ctx* ctx);
+dgnn_status dgnn_ctx_set_timing(dgnn_ctx* ctx, int enable);
+typedef struct {
+    int64_t launches;  /* timed launches of this family                          */
+    double ms;         /* summed CUDA-event durations (ms)                        */
+    double bytes;      /* summed algorithmic bytes, 0 if n/a */
+} dgnn_kernel_stat;
+/* Synchronizes the ctx stream, folds pending events into the totals. */
+dgnn_status dgnn_ctx_kernel_stats(dgnn_ctx* ctx, int32_t kernel_id, dgnn_kernel_stat* out);
+dgnn_status dgnn_ctx_reset_stats(dgnn_ctx* ctx);
+const char* dgnn_kernel_name(int32_t kernel_id);
+
+/* ----------------------------------------------------------- a1-a3 sampling ---- */
+typedef struct {
+    int64_t num_nodes;       /* N (< 2^30)                                                */
+    int64_t num_edges;       /* E = indptr[N]                                             */
+    const int64_t* indptr;   /* device [N+1], non-decreasing, indptr[0] = 0               */
+    const int32_t* indices;  /* device [E], neighbour IDs in [0, N)                       */
+} dgnn_csr;
+
+/* Sample mini-batches t = 0 .. ceil(num_seeds/batch_size)-1: batch t has
+ * seeds[t*B .. min((t+1)*B, S)) and batch id bid = batch_id_base + t (reading c9).
+ * Per batch, hop h = 0..H-1 with k = fanout[h] (reading c1): every node first
+ * discovered at hop h-1 (the seeds at h = 0; reading c4) with out-degree d takes all d
+ * CSR positions if k >= d, else the k positions chosen by Floyd's algorithm from
+ * Philox4x32-10 draws keyed (rng_seed, v, bid, h, slot) (readings c2, c3, c5-c8),
+ * in ascending position order.  New nodes of a hop are appended in ascending global
+ * ID (c10); edges are (frontier node j -> local id of the neighbour), grouped by j,
+ * then by CSR position (c11).
+ *   seeds        device [num_seeds]; distinct within a batch (c12), in [0, N).
+ *   fanout       HOST [num_hops], each in [0, 65535]; num_hops in [1, 65535].
+ *   counts       device uint32 [N] or NULL: counts[v] += 1 for every sampled batch whose
+ *                node set contains v (the access-frequency counter, c14).
+ *   out          receives a library-owned dgnn_samples (free with dgnn_samples_free).
+ * Blocking: returns after the samples are complete (it synchronizes the ctx stream
+ * once per sampling group to size the outputs).  num_seeds == 0 returns OK with zero
+ * batches.  Errors: DGNN_EINVAL for bad arguments, a seed outside [0, N) or a
+ * seed repeated within one batch (in the last two cases `counts` is unspecified). */
+dgnn_status dgnn_sample(dgnn_ctx* ctx, const dgnn_csr* csr, const int32_t* seeds, int64_t num_seeds,
+                        int32_t batch_size, int64_t batch_id_base, const int32_t* fanout, int32_t num_hops,
+                        uint64_t rng_seed, uint32_t* counts, dgnn_samples** out);
+
+/* Concatenated, batch-major layout of all samples (device unless *_host). */
+typedef struct {
+    int64_t num_batches;
+    int32_t num_hops;
+    int64_t batch_id_base;
+    int64_t total_nodes;
+    int64_t total_edges;
+    int64_t total_eptr;
+    const int64_t* node_off;      /* [nb+1]: batch b's nodes are nodes[node_off[b] .. node_off[b+1]) */
+    const int32_t* nodes;         /* [total_nodes] global IDs, seeds first, then per hop ascending   */
+    const int32_t* hop_off;       /* [nb*(H+2)]: local boundaries 0, |seeds|, ..., n_b per batch      */
+    const int64_t* eptr_off;      /* [nb+1]: batch b's eptr starts at eptr[eptr_off[b]]               */
+    const int32_t* eptr;          /* per batch hop_off[b][H]+1 entries: edges of frontier node j are  */
+                                  /* src_local[edge_off[b] + eptr[j] .. edge_off[b] + eptr[j+1])      */
+    const int64_t* edge_off;      /* [nb+1]                                                           */
+    const int32_t* src_local;     /* [total_edges] local index (within the batch) of each neighbour   */
+    const int64_t* node_off_host; /* host mirrors of the offset arrays                                */
+    const int64_t* edge_off_host;
+    const int64_t* eptr_off_host;
+    const int32_t* hop_off_host;
+} dgnn_samples_info;
+dgnn_status dgnn_samples_get_info(const dgnn_samples* s, dgnn_samples_info* info);
+void dgnn_samples_free(dgnn_samples* s);
+
+/* ------------------------------------------------------- a4-a5 cache plan ---- */
+/* Rank nodes by (counts desc, ID asc), excluding zero counts (c15); the first
+ * K_g = min(gpu_rows, nnz) form the GPU tier, the next K_h = min(host_rows, nnz-K_g)
+ * the host tier; every other node is DISK (c18, c19).  Slots inside a tier follow
+ * ascending node ID (c17); tier_map[v] = tier << 30 | slot (DISK slot 0).
+ *   counts   device uint32 [num_nodes]; must already be summed over ranks when the
+ *            offline pass is sharded (the Python layer all-reduces it).
+ * Blocking (one small histogram read-back).  DGNN_EUNSUPPORTED if max(counts) >= 2^24. */
+dgnn_status dgnn_build_cache(dgnn_ctx* ctx, const uint32_t* counts, int64_t num_nodes, int64_t gpu_rows,
+                             int64_t host_rows, dgnn_cache_plan** out);
+typedef struct {
+    int64_t num_nodes;
+    int64_t k_gpu;
+    int64_t k_host;
+    const uint32_t* tier_map;  /* device [num_nodes]               */
+    const int32_t* gpu_ids;    /* device [k_gpu], ascending IDs     */
+    const int32_t* host_ids;   /* device [k_host], ascending IDs    */
+    uint32_t gpu_min_count;    /* smallest count inside the GPU tier (0 if empty)  */
+    uint32_t host_min_count;   /* smallest count inside the host tier (0 if empty) */
+} dgnn_plan_info;
+dgnn_status dgnn_cache_plan_get_info(const dgnn_cache_plan* p, dgnn_plan_info* info);
+void dgnn_cache_plan_free(dgnn_cache_plan* p);
+
+/* --------------------------------------------------------- a6 classify ---- */
+/* Address tables of batches [b_lo, b_hi) (reading c18, c21):
+ * for local node j of batch b, addr = tier_map[nodes[j]] if that tier is GPU/HOST,
+ * else DISK << 30 | (rank of j among the batch's DISK nodes, in local order).
+ * The DISK nodes of each batch, in local order, are that batch's packed list P_b.
+ *   addr        device uint32 [node_off[b_hi] - node_off[b_lo]] (caller-owned).
+ *   packed_ids  device int32, same capacity: P_{b_lo} .. P_{b_hi-1} concatenated.
+ *   packed_off  device int64 [b_hi-b_lo+1]: exclusive prefix of |P_b| (packed_off[0]=0).
+ *   packed_off_host  host int64 [b_hi-b_lo+1] or NULL; when non-NULL the call
+ *               synchronizes and copies packed_off there. */
+dgnn_status dgnn_classify(dgnn_ctx* ctx, const dgnn_cache_plan* plan, const dgnn_samples* samples,
+                          int64_t b_lo, int64_t b_hi, uint32_t* addr, int32_t* packed_ids, int64_t* packed_off,
+                          int64_t* packed_off_host);
+
+/* ------------------------------------------------------------- a7 pack ---- */
+/* Host arithmetic of the chunk layout (reading c20): chunk_off[0] = 0,
+ * chunk_off[i+1] = roundup(chunk_off[i] + (packed_off[i+1]-packed_off[i]) * row_bytes, 4096). */
+dgnn_status dgnn_chunk_layout(const int64_t* packed_off_host, int64_t nb, int64_t row_bytes,
+                              int64_t* chunk_off_host);
+
+/* Batched pack of one packing group: for every batch i < nb and r <
+ * |P_i|, group_buf[chunk_off[i] + r*row_bytes ..] = features[P_i[r]] (raw bytes), and
+ * the tail of each chunk up to chunk_off[i+1] is zeroed.
+ *   features    UVA [num_rows * row_bytes] (device HBM, or pinned host for tables that
+ *               exceed HBM).
+ *   packed_ids, packed_off (device, as produced by dgnn_classify), chunk_off (device
+ *   int64 [nb+1]); total_rows = packed_off[nb] and group_bytes = chunk_off[nb] (host
+ *   values, used for grid sizing).  group_buf: device or pinned [group_bytes]. */
+dgnn_status dgnn_pack(dgnn_ctx* ctx, const void* features, int64_t num_rows, int64_t row_bytes,
+                      const int32_t* packed_ids, const int64_t* packed_off, const int64_t* chunk_off, int64_t nb,
+                      int64_t total_rows, int64_t group_bytes, void* group_buf);
+
+/* Tier buffers as special mini-batches: out[s] = features[ids[s]], s < n.
+ * out: device or pinned host (UVA). */
+dgnn_status dgnn_gather_rows(dgnn_ctx* ctx, const void* features, int64_t num_rows, int64_t row_bytes,
+                             const int32_t* ids, int64_t n, void* out);
+
+/* ----------------------------------------------------------- a8 staging ---- */
+/* Copies on the ctx side stream, ordered after all work already enqueued on the ctx
+ * stream.  Each returns a ticket; dgnn_stage_wait makes the ctx stream wait for that
+ * copy (and all earlier ones); dgnn_stage_sync blocks the host until it completes.
+ * kind: 0 = device -> host, 1 = host -> device, 2 = device -> device. */
+dgnn_status dgnn_stage_copy(dgnn_ctx* ctx, void* dst, const void* src, int64_t bytes, int32_t kind,
+                            int64_t* ticket);
+dgnn_status dgnn_stage_wait(dgnn_ctx* ctx, int64_t ticket);
+dgnn_status dgnn_stage_sync(dgnn_ctx* ctx, int64_t ticket);
+/* Pinned, device-mapped host memory for the host tier and the disk-tier arena. */
+dgnn_status dgnn_host_alloc(int64_t bytes, void** out);
+dgnn_status dgnn_host_free(void* p);
+
+/* --------------------------------------------------------- a9 assemble ---- */
+/* out[j] = row(addr[j]) for j < n (Fig. 3): tier GPU -> gpu_tier[slot]
+ * (device), HOST -> host_tier[slot] (pinned host, read over PCIe through UVA), DISK ->
+ * chunk[slot] (the batch's staged chunk: device or pinned host).  Slots must be below
+ * k_gpu / k_host / chunk_rows; an unresolvable address writes a zero row and is
+ * reported as DGNN_ERANGE by the next dgnn_ctx_sync.  out: device [n * row_bytes]. */
+dgnn_status dgnn_assemble(dgnn_ctx* ctx, const uint32_t* addr, int64_t n, const void* gpu_tier, int64_t k_gpu,
+                          const void* host_tier, int64_t k_host, const void* chunk, int64_t chunk_rows,
+                          int64_t row_bytes, void* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DGNN_H */

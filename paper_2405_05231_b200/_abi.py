@@ -1,0 +1,400 @@
+"""ctypes binding of libdgnn.so (include/dgnn.h) -- argument marshalling only.
+
+Every function here has the name of the C entry point it calls and does no
+computation of its own: torch tensors are turned into raw pointers and sizes,
+the status is checked, library-owned results are wrapped so that they are
+freed with the matching ``*_free``.  If the shared library is missing or
+cannot be loaded the import fails loudly; there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+import weakref
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libdgnn.so")
+
+P = ctypes.c_void_p
+i32, i64, u32, u64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint64
+
+DGNN_OK, DGNN_EINVAL, DGNN_ERANGE, DGNN_ENOMEM, DGNN_ECUDA, DGNN_ECOMM, DGNN_EIO, DGNN_EUNSUPPORTED = range(8)
+STATUS_NAMES = ["OK", "EINVAL", "ERANGE", "ENOMEM", "ECUDA", "ECOMM", "EIO", "EUNSUPPORTED"]
+TIER_GPU, TIER_HOST, TIER_DISK = 0, 1, 2
+TIER_SHIFT = 30
+SLOT_MASK = (1 << TIER_SHIFT) - 1
+KERNELS = ["scan", "sample_seed", "sample_hop", "sample_order", "sample_remap", "sample_compact", "sample_setup",
+           "cache_hist", "cache_select", "classify", "pack_gather", "tier_gather", "assemble", "misc"]
+K = {name: i for i, name in enumerate(KERNELS)}
+
+# every symbol include/dgnn.h declares (checked by tests/test_abi_symbols.py)
+EXPORTS = [
+    "dgnn_ctx_create", "dgnn_ctx_destroy", "dgnn_ctx_set_stream", "dgnn_ctx_stream", "dgnn_ctx_side_stream",
+    "dgnn_ctx_sync", "dgnn_last_error", "dgnn_ctx_set_sample_group", "dgnn_ctx_launches", "dgnn_ctx_set_timing",
+    "dgnn_ctx_kernel_stats", "dgnn_ctx_reset_stats", "dgnn_kernel_name", "dgnn_sample", "dgnn_samples_get_info",
+    "dgnn_samples_free", "dgnn_build_cache", "dgnn_cache_plan_get_info", "dgnn_cache_plan_free", "dgnn_classify",
+    "dgnn_chunk_layout", "dgnn_pack", "dgnn_gather_rows", "dgnn_stage_copy", "dgnn_stage_wait", "dgnn_stage_sync",
+    "dgnn_host_alloc", "dgnn_host_free", "dgnn_assemble",
+]
+
+
+class DgnnError(RuntimeError):
+    def __init__(self, status: int, fn: str, msg: str):
+        name = STATUS_NAMES[status] if 0 <= status < len(STATUS_NAMES) else str(status)
+        super().__init__(f"{fn} -> DGNN_{name}: {msg}")
+        self.status = status
+
+
+class _CSR(ctypes.Structure):
+    _fields_ = [("num_nodes", i64), ("num_edges", i64), ("indptr", P), ("indices", P)]
+
+
+class _SamplesInfo(ctypes.Structure):
+    _fields_ = [("num_batches", i64), ("num_hops", i32), ("batch_id_base", i64), ("total_nodes", i64),
+                ("total_edges", i64), ("total_eptr", i64), ("node_off", P), ("nodes", P), ("hop_off", P),
+                ("eptr_off", P), ("eptr", P), ("edge_off", P), ("src_local", P), ("node_off_host", P),
+                ("edge_off_host", P), ("eptr_off_host", P), ("hop_off_host", P)]
+
+
+class _PlanInfo(ctypes.Structure):
+    _fields_ = [("num_nodes", i64), ("k_gpu", i64), ("k_host", i64), ("tier_map", P), ("gpu_ids", P),
+                ("host_ids", P), ("gpu_min_count", u32), ("host_min_count", u32)]
+
+
+class _KStat(ctypes.Structure):
+    _fields_ = [("launches", i64), ("ms", ctypes.c_double), ("bytes", ctypes.c_double)]
+
+
+_ALLOC_FN = ctypes.CFUNCTYPE(P, ctypes.c_size_t, P, P)
+_FREE_FN = ctypes.CFUNCTYPE(None, P, ctypes.c_size_t, P, P)
+
+
+class _Allocator(ctypes.Structure):
+    _fields_ = [("alloc", _ALLOC_FN), ("free", _FREE_FN), ("user", P)]
+
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libdgnn.so and declare its signatures (no GPU needed)."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise ImportError(f"{path} is missing: build it with `python -m paper_2405_05231_b200.build` "
+                              "(there is no CPU fallback)")
+        L = ctypes.CDLL(path)
+        sig = {
+            "dgnn_ctx_create": (i32, [ctypes.c_int, P, P, ctypes.POINTER(P)]),
+            "dgnn_ctx_destroy": (None, [P]),
+            "dgnn_ctx_set_stream": (i32, [P, P]),
+            "dgnn_ctx_stream": (P, [P]),
+            "dgnn_ctx_side_stream": (P, [P]),
+            "dgnn_ctx_sync": (i32, [P]),
+            "dgnn_last_error": (ctypes.c_char_p, []),
+            "dgnn_ctx_set_sample_group": (i32, [P, i32]),
+            "dgnn_ctx_launches": (i64, [P]),
+            "dgnn_ctx_set_timing": (i32, [P, ctypes.c_int]),
+            "dgnn_ctx_kernel_stats": (i32, [P, i32, ctypes.POINTER(_KStat)]),
+            "dgnn_ctx_reset_stats": (i32, [P]),
+            "dgnn_kernel_name": (ctypes.c_char_p, [i32]),
+            "dgnn_sample": (i32, [P, ctypes.POINTER(_CSR), P, i64, i32, i64, P, i32, u64, P, ctypes.POINTER(P)]),
+            "dgnn_samples_get_info": (i32, [P, ctypes.POINTER(_SamplesInfo)]),
+            "dgnn_samples_free": (None, [P]),
+            "dgnn_build_cache": (i32, [P, P, i64, i64, i64, ctypes.POINTER(P)]),
+            "dgnn_cache_plan_get_info": (i32, [P, ctypes.POINTER(_PlanInfo)]),
+            "dgnn_cache_plan_free": (None, [P]),
+            "dgnn_classify": (i32, [P, P, P, i64, i64, P, P, P, P]),
+            "dgnn_chunk_layout": (i32, [P, i64, i64, P]),
+            "dgnn_pack": (i32, [P, P, i64, i64, P, P, P, i64, i64, i64, P]),
+            "dgnn_gather_rows": (i32, [P, P, i64, i64, P, i64, P]),
+            "dgnn_stage_copy": (i32, [P, P, P, i64, i32, ctypes.POINTER(i64)]),
+            "dgnn_stage_wait": (i32, [P, i64]),
+            "dgnn_stage_sync": (i32, [P, i64]),
+            "dgnn_host_alloc": (i32, [i64, ctypes.POINTER(P)]),
+            "dgnn_host_free": (i32, [P]),
+            "dgnn_assemble": (i32, [P, P, i64, P, i64, P, i64, P, i64, i64, P]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+        return L
+
+
+def _check(status: int, fn: str):
+    if status != DGNN_OK:
+        msg = load_library().dgnn_last_error()
+        raise DgnnError(status, fn, msg.decode() if msg else "")
+
+
+def _ptr(t) -> P:
+    if t is None:
+        return P(0)
+    if isinstance(t, int):
+        return P(t)
+    if isinstance(t, torch.Tensor):
+        if t.numel() and not t.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return P(t.data_ptr() if t.numel() else 0)
+    raise TypeError(type(t))
+
+
+def _need_cuda(t: torch.Tensor, name: str, dtype=None):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if dtype is not None and t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+
+
+# ---------------------------------------------------------------- views
+class _DevView:
+    """Zero-copy __cuda_array_interface__ over library-owned memory; keeps the owner alive."""
+
+    _TYPESTR = {torch.int32: "<i4", torch.int64: "<i8", torch.uint32: "<u4", torch.uint8: "|u1"}
+
+    def __init__(self, ptr: int, n: int, dtype, owner):
+        self.owner = owner
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": self._TYPESTR[dtype],
+                                         "data": (int(ptr) if n else 0, False), "version": 3, "strides": None,
+                                         "stream": None}
+
+
+def _view(ptr: int, n: int, dtype, owner, device) -> torch.Tensor:
+    if n == 0:
+        return torch.empty(0, dtype=dtype, device=device)
+    return torch.as_tensor(_DevView(ptr, n, dtype, owner), device=device)
+
+
+def _host_array(ptr: int, n: int, ctype):
+    import numpy as np
+    if n == 0:
+        return np.zeros(0, dtype=np.dtype(ctype))
+    return np.ctypeslib.as_array(ctypes.cast(ptr, ctypes.POINTER(ctype)), (n,)).copy()
+
+
+# ------------------------------------------------------------------ context
+class Ctx:
+    """A dgnn_ctx bound to one device and a CUDA stream (default: torch's current stream).
+
+    Library-owned buffers are allocated from torch's caching allocator unless
+    ``torch_allocator=False`` (then cudaMallocAsync).
+    """
+
+    def __init__(self, device=None, stream: torch.cuda.Stream | None = None, torch_allocator: bool = True):
+        L = load_library()
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else
+                                   torch.device(device).index or 0)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        self._alloc = None
+        alloc_p = P(0)
+        if torch_allocator:
+            dev = self.device.index
+
+            def _a(nbytes, stream, user):
+                try:
+                    return torch.cuda.caching_allocator_alloc(int(nbytes), dev, int(stream or 0))
+                except Exception:
+                    return None
+
+            def _f(ptr, nbytes, stream, user):
+                try:
+                    torch.cuda.caching_allocator_delete(int(ptr))
+                except Exception:
+                    pass
+
+            self._alloc = _Allocator(_ALLOC_FN(_a), _FREE_FN(_f), P(0))
+            alloc_p = ctypes.cast(ctypes.pointer(self._alloc), P)
+        h = P()
+        _check(L.dgnn_ctx_create(self.device.index, P(self.stream.cuda_stream), alloc_p, ctypes.byref(h)),
+               "dgnn_ctx_create")
+        self.handle = h
+        self._finalizer = weakref.finalize(self, L.dgnn_ctx_destroy, h)
+
+    def close(self):
+        self._finalizer()
+
+    # statistics -------------------------------------------------------
+    def launches(self) -> int:
+        return int(load_library().dgnn_ctx_launches(self.handle))
+
+    def set_timing(self, on: bool):
+        _check(load_library().dgnn_ctx_set_timing(self.handle, int(bool(on))), "dgnn_ctx_set_timing")
+
+    def kernel_stats(self) -> dict:
+        out = {}
+        for name, kid in K.items():
+            s = _KStat()
+            _check(load_library().dgnn_ctx_kernel_stats(self.handle, kid, ctypes.byref(s)), "dgnn_ctx_kernel_stats")
+            out[name] = {"launches": int(s.launches), "ms": float(s.ms), "bytes": float(s.bytes)}
+        return out
+
+    def reset_stats(self):
+        _check(load_library().dgnn_ctx_reset_stats(self.handle), "dgnn_ctx_reset_stats")
+
+    def sync(self):
+        _check(load_library().dgnn_ctx_sync(self.handle), "dgnn_ctx_sync")
+
+    def set_sample_group(self, batches: int):
+        _check(load_library().dgnn_ctx_set_sample_group(self.handle, int(batches)), "dgnn_ctx_set_sample_group")
+
+    @property
+    def side_stream_ptr(self) -> int:
+        return int(load_library().dgnn_ctx_side_stream(self.handle) or 0)
+
+
+# ------------------------------------------------------------------ samples
+class Samples:
+    """Library-owned result of dgnn_sample (batch-major concatenated layout)."""
+
+    def __init__(self, ctx: Ctx, handle):
+        L = load_library()
+        self.ctx = ctx
+        self.handle = handle
+        self._finalizer = weakref.finalize(self, L.dgnn_samples_free, handle)
+        info = _SamplesInfo()
+        _check(L.dgnn_samples_get_info(handle, ctypes.byref(info)), "dgnn_samples_get_info")
+        self.num_batches = int(info.num_batches)
+        self.num_hops = int(info.num_hops)
+        self.batch_id_base = int(info.batch_id_base)
+        self.total_nodes = int(info.total_nodes)
+        self.total_edges = int(info.total_edges)
+        nb, H = self.num_batches, self.num_hops
+        dev = ctx.device
+        self.node_off = _view(info.node_off, nb + 1, torch.int64, self, dev)
+        self.nodes = _view(info.nodes, self.total_nodes, torch.int32, self, dev)
+        self.hop_off = _view(info.hop_off, nb * (H + 2), torch.int32, self, dev)
+        self.eptr_off = _view(info.eptr_off, nb + 1, torch.int64, self, dev)
+        self.eptr = _view(info.eptr, int(info.total_eptr), torch.int32, self, dev)
+        self.edge_off = _view(info.edge_off, nb + 1, torch.int64, self, dev)
+        self.src_local = _view(info.src_local, self.total_edges, torch.int32, self, dev)
+        self.node_off_host = _host_array(info.node_off_host, nb + 1, ctypes.c_int64)
+        self.edge_off_host = _host_array(info.edge_off_host, nb + 1, ctypes.c_int64)
+        self.eptr_off_host = _host_array(info.eptr_off_host, nb + 1, ctypes.c_int64)
+        self.hop_off_host = _host_array(info.hop_off_host, nb * (H + 2), ctypes.c_int32).reshape(nb, H + 2)
+
+    def batch(self, b: int) -> dict:
+        """Device views of batch b: nodes, hop_off (host), eptr, src_local."""
+        n0, n1 = int(self.node_off_host[b]), int(self.node_off_host[b + 1])
+        e0, e1 = int(self.edge_off_host[b]), int(self.edge_off_host[b + 1])
+        p0, p1 = int(self.eptr_off_host[b]), int(self.eptr_off_host[b + 1])
+        return {"bid": self.batch_id_base + b, "nodes": self.nodes[n0:n1], "hop_off": self.hop_off_host[b],
+                "eptr": self.eptr[p0:p1], "src_local": self.src_local[e0:e1]}
+
+
+def dgnn_sample(ctx: Ctx, indptr: torch.Tensor, indices: torch.Tensor, seeds: torch.Tensor, batch_size: int,
+                fanout, rng_seed: int, batch_id_base: int = 0, counts: torch.Tensor | None = None) -> Samples:
+    _need_cuda(indptr, "indptr", torch.int64)
+    _need_cuda(indices, "indices", torch.int32)
+    _need_cuda(seeds, "seeds", torch.int32)
+    if counts is not None:
+        _need_cuda(counts, "counts")
+        if counts.dtype not in (torch.int32, torch.uint32) or counts.numel() != indptr.numel() - 1:
+            raise ValueError("counts must be a 32-bit tensor of length num_nodes")
+    fan = (ctypes.c_int32 * max(len(fanout), 1))(*[int(k) for k in fanout])
+    csr = _CSR(indptr.numel() - 1, indices.numel(), _ptr(indptr), _ptr(indices))
+    h = P()
+    _check(load_library().dgnn_sample(ctx.handle, ctypes.byref(csr), _ptr(seeds), seeds.numel(), int(batch_size),
+                                      int(batch_id_base), fan, len(fanout), int(rng_seed) & ((1 << 64) - 1),
+                                      _ptr(counts), ctypes.byref(h)), "dgnn_sample")
+    return Samples(ctx, h)
+
+
+# --------------------------------------------------------------- cache plan
+class CachePlan:
+    def __init__(self, ctx: Ctx, handle):
+        L = load_library()
+        self.ctx = ctx
+        self.handle = handle
+        self._finalizer = weakref.finalize(self, L.dgnn_cache_plan_free, handle)
+        info = _PlanInfo()
+        _check(L.dgnn_cache_plan_get_info(handle, ctypes.byref(info)), "dgnn_cache_plan_get_info")
+        self.num_nodes = int(info.num_nodes)
+        self.k_gpu = int(info.k_gpu)
+        self.k_host = int(info.k_host)
+        self.gpu_min_count = int(info.gpu_min_count)
+        self.host_min_count = int(info.host_min_count)
+        dev = ctx.device
+        self.tier_map = _view(info.tier_map, self.num_nodes, torch.int32, self, dev)
+        self.gpu_ids = _view(info.gpu_ids, self.k_gpu, torch.int32, self, dev)
+        self.host_ids = _view(info.host_ids, self.k_host, torch.int32, self, dev)
+
+
+def dgnn_build_cache(ctx: Ctx, counts: torch.Tensor, gpu_rows: int, host_rows: int) -> CachePlan:
+    _need_cuda(counts, "counts")
+    h = P()
+    _check(load_library().dgnn_build_cache(ctx.handle, _ptr(counts), counts.numel(), int(gpu_rows), int(host_rows),
+                                           ctypes.byref(h)), "dgnn_build_cache")
+    return CachePlan(ctx, h)
+
+
+# ------------------------------------------------------------ classify / pack
+def dgnn_classify(ctx: Ctx, plan: CachePlan, samples: Samples, b_lo: int, b_hi: int, addr: torch.Tensor,
+                  packed_ids: torch.Tensor, packed_off: torch.Tensor, want_host: bool = True):
+    import numpy as np
+    n = int(samples.node_off_host[b_hi] - samples.node_off_host[b_lo])
+    _need_cuda(addr, "addr")
+    _need_cuda(packed_ids, "packed_ids", torch.int32)
+    _need_cuda(packed_off, "packed_off", torch.int64)
+    if addr.numel() < n or packed_ids.numel() < n or packed_off.numel() < b_hi - b_lo + 1:
+        raise ValueError("dgnn_classify: output buffers too small")
+    host = np.zeros(b_hi - b_lo + 1, np.int64) if want_host else None
+    _check(load_library().dgnn_classify(ctx.handle, plan.handle, samples.handle, b_lo, b_hi, _ptr(addr),
+                                        _ptr(packed_ids), _ptr(packed_off),
+                                        P(host.ctypes.data) if host is not None else P(0)), "dgnn_classify")
+    return host
+
+
+def dgnn_chunk_layout(packed_off_host, row_bytes: int):
+    import numpy as np
+    po = np.ascontiguousarray(packed_off_host, dtype=np.int64)
+    out = np.zeros(len(po), np.int64)
+    _check(load_library().dgnn_chunk_layout(P(po.ctypes.data), len(po) - 1, int(row_bytes), P(out.ctypes.data)),
+           "dgnn_chunk_layout")
+    return out
+
+
+def dgnn_pack(ctx: Ctx, features: torch.Tensor, packed_ids: torch.Tensor, packed_off: torch.Tensor,
+              chunk_off: torch.Tensor, total_rows: int, group_bytes: int, group_buf: torch.Tensor):
+    row_bytes = features.element_size() * (features.numel() // max(features.shape[0], 1))
+    nb = chunk_off.numel() - 1
+    _check(load_library().dgnn_pack(ctx.handle, _ptr(features), features.shape[0], row_bytes, _ptr(packed_ids),
+                                    _ptr(packed_off), _ptr(chunk_off), nb, int(total_rows), int(group_bytes),
+                                    _ptr(group_buf)), "dgnn_pack")
+
+
+def dgnn_gather_rows(ctx: Ctx, features: torch.Tensor, ids: torch.Tensor, out: torch.Tensor):
+    row_bytes = features.element_size() * (features.numel() // max(features.shape[0], 1))
+    _check(load_library().dgnn_gather_rows(ctx.handle, _ptr(features), features.shape[0], row_bytes, _ptr(ids),
+                                           ids.numel(), _ptr(out)), "dgnn_gather_rows")
+
+
+# ------------------------------------------------------------------ staging
+def dgnn_stage_copy(ctx: Ctx, dst, src, nbytes: int, kind: int) -> int:
+    t = i64()
+    _check(load_library().dgnn_stage_copy(ctx.handle, _ptr(dst), _ptr(src), int(nbytes), int(kind), ctypes.byref(t)),
+           "dgnn_stage_copy")
+    return int(t.value)
+
+
+def dgnn_stage_wait(ctx: Ctx, ticket: int):
+    _check(load_library().dgnn_stage_wait(ctx.handle, int(ticket)), "dgnn_stage_wait")
+
+
+def dgnn_stage_sync(ctx: Ctx, ticket: int):
+    _check(load_library().dgnn_stage_sync(ctx.handle, int(ticket)), "dgnn_stage_sync")
+
+
+# ----------------------------------------------------------------- assemble
+def dgnn_assemble(ctx: Ctx, addr: torch.Tensor, gpu_tier, k_gpu: int, host_tier, k_host: int, chunk,
+                  chunk_rows: int, row_bytes: int, out: torch.Tensor):
+    _check(load_library().dgnn_assemble(ctx.handle, _ptr(addr), addr.numel(), _ptr(gpu_tier), int(k_gpu),
+                                        _ptr(host_tier), int(k_host), _ptr(chunk), int(chunk_rows), int(row_bytes),
+                                        _ptr(out)), "dgnn_assemble")

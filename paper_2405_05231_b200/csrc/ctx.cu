@@ -1,0 +1,266 @@
+// ctx.cu -- context, errors, allocation, statistics and the a8 staging runtime.
+#include <cstdarg>
+
+#include "internal.cuh"
+
+namespace dgnn {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+dgnn_status cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
+    set_error("CUDA error %s (%s) in %s at %s:%d", cudaGetErrorName(e), cudaGetErrorString(e), what, file, line);
+    return e == cudaErrorMemoryAllocation ? DGNN_ENOMEM : DGNN_ECUDA;
+}
+
+void* dev_alloc(dgnn_ctx* c, size_t bytes) {
+    if (c->has_alloc) return c->alloc.alloc(bytes, (void*)c->stream, c->alloc.user);
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, bytes, c->stream) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return p;
+}
+
+void dev_free(dgnn_ctx* c, void* p, size_t bytes) {
+    if (!p) return;
+    if (c->has_alloc) c->alloc.free(p, bytes, (void*)c->stream, c->alloc.user);
+    else cudaFreeAsync(p, c->stream);
+}
+
+cudaEvent_t take_event(dgnn_ctx* c) {
+    if (!c->event_pool.empty()) {
+        cudaEvent_t e = c->event_pool.back();
+        c->event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+void fold_pending(dgnn_ctx* c, bool sync) {
+    if (sync) cudaStreamSynchronize(c->stream);
+    for (auto& p : c->pending) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
+            c->stat_ms[p.kid] += ms;
+            c->stat_bytes[p.kid] += p.bytes;
+            c->stat_n[p.kid] += 1;
+        } else {
+            cudaGetLastError();
+        }
+        c->event_pool.push_back(p.a);
+        c->event_pool.push_back(p.b);
+    }
+    c->pending.clear();
+}
+
+dgnn_status memset_async(dgnn_ctx* c, void* p, int value, size_t bytes) {
+    if (!bytes) return DGNN_OK;
+    DGNN_CK(cudaMemsetAsync(p, value, bytes, c->stream));
+    return DGNN_OK;
+}
+
+dgnn_status check_dev_err(dgnn_ctx* c) {
+    int h = 0;
+    DGNN_CK(cudaMemcpyAsync(&h, c->dev_err, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    DGNN_CK(cudaStreamSynchronize(c->stream));
+    if (h) {
+        DGNN_CK(cudaMemsetAsync(c->dev_err, 0, sizeof(int), c->stream));
+        if (h & DEVERR_SEED_RANGE) { set_error("a seed is outside [0, num_nodes)"); return DGNN_EINVAL; }
+        if (h & DEVERR_SEED_DUP) { set_error("a seed appears twice within one batch (reading c12)"); return DGNN_EINVAL; }
+        if (h & DEVERR_ADDR_RANGE) { set_error("unresolvable node address (slot beyond its tier)"); return DGNN_ERANGE; }
+        if (h & DEVERR_TABLE) { set_error("internal: sampling hash table overflow"); return DGNN_ECUDA; }
+        set_error("internal: device capacity overflow (flags %d)", h);
+        return DGNN_ECUDA;
+    }
+    return DGNN_OK;
+}
+
+}  // namespace dgnn
+
+using namespace dgnn;
+
+extern "C" {
+
+const char* dgnn_last_error(void) { return g_err; }
+
+dgnn_status dgnn_ctx_create(int device, void* stream, const dgnn_allocator* allocator, dgnn_ctx** out) {
+    DGNN_REQUIRE(out != nullptr, "dgnn_ctx_create: out is NULL");
+    *out = nullptr;
+    int ndev = 0;
+    DGNN_CK(cudaGetDeviceCount(&ndev));
+    DGNN_REQUIRE(device >= 0 && device < ndev, "dgnn_ctx_create: device %d not present (%d devices)", device, ndev);
+    DGNN_CK(cudaSetDevice(device));
+    auto* c = new dgnn_ctx();
+    c->device = device;
+    cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+    if (stream) {
+        c->stream = (cudaStream_t)stream;
+    } else {
+        if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+            delete c;
+            set_error("cudaStreamCreate failed");
+            return DGNN_ECUDA;
+        }
+        c->own_stream = true;
+    }
+    if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess) {
+        delete c;
+        set_error("cudaStreamCreate (side) failed");
+        return DGNN_ECUDA;
+    }
+    if (allocator && allocator->alloc && allocator->free) {
+        c->alloc = *allocator;
+        c->has_alloc = true;
+    } else {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    }
+    for (int i = 0; i < dgnn_ctx::kStageRing; ++i) cudaEventCreateWithFlags(&c->stage_ev[i], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&c->order_ev, cudaEventDisableTiming);
+    if (cudaMalloc(&c->dev_err, sizeof(int)) != cudaSuccess || cudaMemset(c->dev_err, 0, sizeof(int)) != cudaSuccess) {
+        dgnn_ctx_destroy(c);
+        set_error("cudaMalloc of the error word failed");
+        return DGNN_ECUDA;
+    }
+    *out = c;
+    return DGNN_OK;
+}
+
+void dgnn_ctx_destroy(dgnn_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->side) cudaStreamSynchronize(c->side);
+    fold_pending(c, false);
+    for (auto e : c->event_pool) cudaEventDestroy(e);
+    for (int i = 0; i < dgnn_ctx::kStageRing; ++i)
+        if (c->stage_ev[i]) cudaEventDestroy(c->stage_ev[i]);
+    if (c->order_ev) cudaEventDestroy(c->order_ev);
+    if (c->dev_err) cudaFree(c->dev_err);
+    if (c->side) cudaStreamDestroy(c->side);
+    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+dgnn_status dgnn_ctx_set_stream(dgnn_ctx* c, void* stream) {
+    DGNN_REQUIRE(c && stream, "dgnn_ctx_set_stream: NULL argument");
+    if (c->own_stream) {
+        cudaStreamSynchronize(c->stream);
+        cudaStreamDestroy(c->stream);
+        c->own_stream = false;
+    }
+    c->stream = (cudaStream_t)stream;
+    return DGNN_OK;
+}
+
+void* dgnn_ctx_stream(const dgnn_ctx* c) { return c ? (void*)c->stream : nullptr; }
+void* dgnn_ctx_side_stream(const dgnn_ctx* c) { return c ? (void*)c->side : nullptr; }
+
+dgnn_status dgnn_ctx_sync(dgnn_ctx* c) {
+    DGNN_REQUIRE(c, "dgnn_ctx_sync: NULL ctx");
+    DGNN_CK(cudaSetDevice(c->device));
+    DGNN_CK(cudaStreamSynchronize(c->side));
+    return check_dev_err(c);
+}
+
+dgnn_status dgnn_ctx_set_sample_group(dgnn_ctx* c, int32_t batches) {
+    DGNN_REQUIRE(c && batches >= 0 && batches <= 1024, "dgnn_ctx_set_sample_group: bad argument");
+    c->sample_group = batches;
+    return DGNN_OK;
+}
+
+int64_t dgnn_ctx_launches(const dgnn_ctx* c) { return c ? c->launches : 0; }
+
+dgnn_status dgnn_ctx_set_timing(dgnn_ctx* c, int enable) {
+    DGNN_REQUIRE(c, "dgnn_ctx_set_timing: NULL ctx");
+    c->timing = enable != 0;
+    return DGNN_OK;
+}
+
+dgnn_status dgnn_ctx_kernel_stats(dgnn_ctx* c, int32_t kid, dgnn_kernel_stat* out) {
+    DGNN_REQUIRE(c && out && kid >= 0 && kid < DGNN_K_NUM, "dgnn_ctx_kernel_stats: bad argument");
+    DGNN_CK(cudaSetDevice(c->device));
+    fold_pending(c, true);
+    out->launches = c->stat_n[kid];
+    out->ms = c->stat_ms[kid];
+    out->bytes = c->stat_bytes[kid];
+    return DGNN_OK;
+}
+
+dgnn_status dgnn_ctx_reset_stats(dgnn_ctx* c) {
+    DGNN_REQUIRE(c, "dgnn_ctx_reset_stats: NULL ctx");
+    fold_pending(c, true);
+    for (int k = 0; k < DGNN_K_NUM; ++k) {
+        c->stat_ms[k] = 0;
+        c->stat_bytes[k] = 0;
+        c->stat_n[k] = 0;
+    }
+    return DGNN_OK;
+}
+
+const char* dgnn_kernel_name(int32_t kid) {
+    static const char* names[DGNN_K_NUM] = {"scan",           "sample_seed",   "sample_hop",    "sample_order",
+                                            "sample_remap",   "sample_compact", "sample_setup", "cache_hist",
+                                            "cache_select",   "classify",      "pack_gather",   "tier_gather",
+                                            "assemble",       "misc"};
+    return (kid >= 0 && kid < DGNN_K_NUM) ? names[kid] : "?";
+}
+
+// ---------------------------------------------------------------- staging
+dgnn_status dgnn_stage_copy(dgnn_ctx* c, void* dst, const void* src, int64_t bytes, int32_t kind, int64_t* ticket) {
+    DGNN_REQUIRE(c && ticket && bytes >= 0 && kind >= 0 && kind <= 2 && (bytes == 0 || (dst && src)),
+                 "dgnn_stage_copy: bad argument");
+    DGNN_CK(cudaSetDevice(c->device));
+    const int64_t t = c->stage_next++;
+    cudaEvent_t ev = c->stage_ev[t % dgnn_ctx::kStageRing];
+    if (t >= dgnn_ctx::kStageRing) DGNN_CK(cudaEventSynchronize(ev));  // slot reuse: the older copy must be done
+    // order after everything already on the ctx stream
+    DGNN_CK(cudaEventRecord(c->order_ev, c->stream));
+    DGNN_CK(cudaStreamWaitEvent(c->side, c->order_ev, 0));
+    static const cudaMemcpyKind kinds[3] = {cudaMemcpyDeviceToHost, cudaMemcpyHostToDevice, cudaMemcpyDeviceToDevice};
+    if (bytes) DGNN_CK(cudaMemcpyAsync(dst, src, (size_t)bytes, kinds[kind], c->side));
+    DGNN_CK(cudaEventRecord(ev, c->side));
+    *ticket = t;
+    return DGNN_OK;
+}
+
+dgnn_status dgnn_stage_wait(dgnn_ctx* c, int64_t ticket) {
+    DGNN_REQUIRE(c && ticket >= 0 && ticket < c->stage_next, "dgnn_stage_wait: bad ticket");
+    if (c->stage_next - ticket > dgnn_ctx::kStageRing) return DGNN_OK;  // long since complete (slot was reused)
+    DGNN_CK(cudaStreamWaitEvent(c->stream, c->stage_ev[ticket % dgnn_ctx::kStageRing], 0));
+    return DGNN_OK;
+}
+
+dgnn_status dgnn_stage_sync(dgnn_ctx* c, int64_t ticket) {
+    DGNN_REQUIRE(c && ticket >= 0 && ticket < c->stage_next, "dgnn_stage_sync: bad ticket");
+    if (c->stage_next - ticket > dgnn_ctx::kStageRing) return DGNN_OK;
+    DGNN_CK(cudaEventSynchronize(c->stage_ev[ticket % dgnn_ctx::kStageRing]));
+    return DGNN_OK;
+}
+
+dgnn_status dgnn_host_alloc(int64_t bytes, void** out) {
+    DGNN_REQUIRE(out && bytes >= 0, "dgnn_host_alloc: bad argument");
+    *out = nullptr;
+    DGNN_CK(cudaHostAlloc(out, (size_t)(bytes ? bytes : 1), cudaHostAllocPortable | cudaHostAllocMapped));
+    return DGNN_OK;
+}
+
+dgnn_status dgnn_host_free(void* p) {
+    if (p) DGNN_CK(cudaFreeHost(p));
+    return DGNN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,218 @@
+// pack.cu -- a6 address tables and a7 batched feature packing.
+// a6: P:488 (Sec. 6) "we prepare interpreted address tables during
+//     pre-processing".  Readings c18, c21.
+// a7: P:228-230 (Sec. 3) "collect all node features it requires and store them
+//     contiguously"; P:437-443 (Sec. 5.2) batched packing, and the GPU / CPU
+//     caches filled "by treating them as special mini-batches".  Chunk layout:
+//     reading c20 (dense rows, 4 KiB-aligned chunk starts, zero tail).
+//
+// On B200 the whole feature table of the single-GPU configurations is HBM
+// resident, so "batched packing" (one sequential pass over a feature partition
+// shared by many batches) becomes one gather launch per packing group: every
+// packed row of every batch in the group is an independent 16-byte-vectorized
+// row copy, HBM-bandwidth bound.
+#include <algorithm>
+
+#include "rowcopy.cuh"
+
+namespace dgnn {
+namespace {
+
+constexpr int kPackU = 4;
+constexpr int kMaxSmemSeg = 2048;
+
+struct PackRow {
+    const uint8_t* src;
+    int64_t row_bytes;
+    const int32_t* ids;
+    const int64_t* seg;  // packed_off (smem or global), nb+1
+    const int64_t* chunk_off;
+    int nb;
+    uint8_t* dst;
+    __device__ __forceinline__ bool operator()(int64_t r, const uint8_t*& s, uint8_t*& d) const {
+        const int b = segment_of(seg, nb + 1, r);
+        s = src + (int64_t)ids[r] * row_bytes;
+        d = dst + chunk_off[b] + (r - seg[b]) * row_bytes;
+        return true;
+    }
+};
+
+template <class V>
+__global__ void __launch_bounds__(256) k_pack(const uint8_t* __restrict__ src, int64_t row_bytes,
+                                              const int32_t* __restrict__ ids, const int64_t* __restrict__ packed_off,
+                                              const int64_t* __restrict__ chunk_off, int nb, int64_t R,
+                                              uint8_t* __restrict__ dst) {
+    __shared__ int64_t s_seg[kMaxSmemSeg + 1];
+    const bool in_smem = nb <= kMaxSmemSeg;
+    if (in_smem)
+        for (int i = threadIdx.x; i <= nb; i += blockDim.x) s_seg[i] = packed_off[i];
+    __syncthreads();
+    const int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    // zero tail of each chunk (reading c20): warp b handles batch b
+    for (int64_t b = warp; b < nb; b += nwarps) {
+        const int64_t rows = packed_off[b + 1] - packed_off[b];
+        uint32_t* z = reinterpret_cast<uint32_t*>(dst + chunk_off[b] + rows * row_bytes);
+        const int64_t nz = (chunk_off[b + 1] - chunk_off[b] - rows * row_bytes) >> 2;
+        for (int64_t i = threadIdx.x & 31; i < nz; i += 32) z[i] = 0u;
+    }
+    PackRow fn{src, row_bytes, ids, in_smem ? s_seg : packed_off, chunk_off, nb, dst};
+    copy_rows_warp<kPackU, V>(R, row_bytes, fn, warp, nwarps);
+}
+
+struct GatherRow {
+    const uint8_t* src;
+    int64_t row_bytes;
+    const int32_t* ids;
+    uint8_t* dst;
+    __device__ __forceinline__ bool operator()(int64_t r, const uint8_t*& s, uint8_t*& d) const {
+        s = src + (int64_t)ids[r] * row_bytes;
+        d = dst + r * row_bytes;
+        return true;
+    }
+};
+
+template <class V>
+__global__ void __launch_bounds__(256) k_gather(const uint8_t* __restrict__ src, int64_t row_bytes,
+                                                const int32_t* __restrict__ ids, int64_t R, uint8_t* __restrict__ dst) {
+    const int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    copy_rows_warp<kPackU, V>(R, row_bytes, GatherRow{src, row_bytes, ids, dst}, warp, nwarps);
+}
+
+bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
+__global__ void k_classify_fix(uint32_t* __restrict__ addr, int64_t n, const int64_t* __restrict__ seg, int nseg,
+                               int64_t n0, const int64_t* __restrict__ packed_off) {
+    __shared__ int64_t s_seg[kMaxSmemSeg + 1];
+    __shared__ int64_t s_po[kMaxSmemSeg + 1];
+    const bool in_smem = nseg <= kMaxSmemSeg;
+    if (in_smem)
+        for (int i = threadIdx.x; i <= nseg; i += blockDim.x) {
+            s_seg[i] = seg[i];
+            s_po[i] = packed_off[i];
+        }
+    __syncthreads();
+    const int64_t* sg = in_smem ? s_seg : seg;
+    const int64_t* po = in_smem ? s_po : packed_off;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t a = addr[i];
+        if ((a >> DGNN_TIER_SHIFT) == DGNN_TIER_DISK) {
+            const int b = segment_of(sg, nseg + 1, n0 + i);
+            addr[i] = a - (uint32_t)po[b];
+        }
+    }
+}
+
+}  // namespace
+}  // namespace dgnn
+
+using namespace dgnn;
+
+extern "C" dgnn_status dgnn_classify(dgnn_ctx* c, const dgnn_cache_plan* plan, const dgnn_samples* S, int64_t b_lo,
+                                     int64_t b_hi, uint32_t* addr, int32_t* packed_ids, int64_t* packed_off,
+                                     int64_t* packed_off_host) {
+    DGNN_REQUIRE(c && plan && S && addr && packed_ids && packed_off, "dgnn_classify: NULL argument");
+    DGNN_REQUIRE(0 <= b_lo && b_lo <= b_hi && b_hi <= S->nb, "dgnn_classify: batch range [%lld, %lld) outside [0, %lld)",
+                 (long long)b_lo, (long long)b_hi, (long long)S->nb);
+    DGNN_CK(cudaSetDevice(c->device));
+    const int64_t nbg = b_hi - b_lo;
+    const int64_t n0 = S->node_off_h[b_lo];
+    const int64_t n = S->node_off_h[b_hi] - n0;
+    DGNN_TRY(memset_async(c, packed_off, 0, sizeof(int64_t)));
+    if (n > 0) {
+        const int32_t* nodes = S->nodes + n0;
+        const int64_t* seg = S->node_off + b_lo;  // absolute offsets of batches b_lo..b_hi
+        const uint32_t* tm = plan->tier_map;
+        const int nseg = (int)nbg;
+        auto in = [=] __device__(int64_t i) -> int64_t {
+            return (int64_t)((tm[nodes[i]] >> DGNN_TIER_SHIFT) == DGNN_TIER_DISK);
+        };
+        // pass 1: compaction of the DISK nodes (P_b concatenated), batch starts,
+        // global packed index parked in addr
+        auto outf = [=] __device__(int64_t i, int64_t excl, int64_t val) {
+            const int b = segment_of(seg, nseg + 1, n0 + i);
+            if (n0 + i == seg[b]) packed_off[b] = excl;
+            if (val) {
+                packed_ids[excl] = nodes[i];
+                addr[i] = (DGNN_TIER_DISK << DGNN_TIER_SHIFT) | (uint32_t)excl;
+            } else {
+                addr[i] = tm[nodes[i]];
+            }
+        };
+        DGNN_TRY(scan::run(c, n, nullptr, in, outf, packed_off + nbg));
+        // pass 2: DISK slots relative to the batch (rank among the batch's DISK nodes)
+        launch(c, DGNN_K_CLASSIFY, 8.0 * n, [&] {
+            k_classify_fix<<<grid_for(c, n, 256), 256, 0, c->stream>>>(addr, n, seg, nseg, n0, packed_off);
+        });
+        DGNN_CK_LAUNCH();
+    } else {
+        DGNN_TRY(memset_async(c, packed_off, 0, sizeof(int64_t) * (nbg + 1)));
+    }
+    if (packed_off_host) {
+        DGNN_CK(cudaMemcpyAsync(packed_off_host, packed_off, sizeof(int64_t) * (nbg + 1), cudaMemcpyDeviceToHost,
+                                c->stream));
+        DGNN_CK(cudaStreamSynchronize(c->stream));
+    }
+    return DGNN_OK;
+}
+
+extern "C" dgnn_status dgnn_chunk_layout(const int64_t* packed_off_host, int64_t nb, int64_t row_bytes,
+                                         int64_t* chunk_off_host) {
+    DGNN_REQUIRE(packed_off_host && chunk_off_host && nb >= 0 && row_bytes > 0, "dgnn_chunk_layout: bad argument");
+    chunk_off_host[0] = 0;
+    for (int64_t i = 0; i < nb; ++i) {
+        const int64_t rows = packed_off_host[i + 1] - packed_off_host[i];
+        DGNN_REQUIRE(rows >= 0, "dgnn_chunk_layout: packed_off must be non-decreasing");
+        const int64_t end = chunk_off_host[i] + rows * row_bytes;
+        chunk_off_host[i + 1] = (end + 4095) / 4096 * 4096;
+    }
+    return DGNN_OK;
+}
+
+extern "C" dgnn_status dgnn_pack(dgnn_ctx* c, const void* features, int64_t num_rows, int64_t row_bytes,
+                                 const int32_t* packed_ids, const int64_t* packed_off, const int64_t* chunk_off,
+                                 int64_t nb, int64_t total_rows, int64_t group_bytes, void* group_buf) {
+    DGNN_REQUIRE(c && (features || num_rows == 0) && packed_off && chunk_off && (group_buf || group_bytes == 0),
+                 "dgnn_pack: NULL argument");
+    DGNN_REQUIRE(row_bytes > 0 && row_bytes % 4 == 0, "dgnn_pack: row_bytes must be a positive multiple of 4");
+    DGNN_REQUIRE(nb >= 0 && nb < (1 << 30) && total_rows >= 0 && (packed_ids || total_rows == 0),
+                 "dgnn_pack: bad sizes");
+    DGNN_REQUIRE(total_rows * row_bytes <= group_bytes, "dgnn_pack: group_bytes too small for the packed rows");
+    if (nb == 0) return DGNN_OK;
+    DGNN_CK(cudaSetDevice(c->device));
+    const bool v16 = row_bytes % 16 == 0 && aligned16(features) && aligned16(group_buf);
+    const int64_t work = std::max<int64_t>(total_rows * 32 / kPackU, nb * 32);
+    const int grid = grid_for(c, work, 256, 8);
+    const double bytes = (double)total_rows * (2.0 * row_bytes + 4.0);
+    launch(c, DGNN_K_PACK, bytes, [&] {
+        if (v16)
+            k_pack<uint4><<<grid, 256, 0, c->stream>>>((const uint8_t*)features, row_bytes, packed_ids, packed_off,
+                                                        chunk_off, (int)nb, total_rows, (uint8_t*)group_buf);
+        else
+            k_pack<uint32_t><<<grid, 256, 0, c->stream>>>((const uint8_t*)features, row_bytes, packed_ids,
+                                                           packed_off, chunk_off, (int)nb, total_rows,
+                                                           (uint8_t*)group_buf);
+    });
+    DGNN_CK_LAUNCH();
+    return DGNN_OK;
+}
+
+extern "C" dgnn_status dgnn_gather_rows(dgnn_ctx* c, const void* features, int64_t num_rows, int64_t row_bytes,
+                                        const int32_t* ids, int64_t n, void* out) {
+    DGNN_REQUIRE(c && (n == 0 || (features && ids && out)), "dgnn_gather_rows: NULL argument");
+    DGNN_REQUIRE(row_bytes > 0 && row_bytes % 4 == 0 && n >= 0, "dgnn_gather_rows: bad sizes");
+    if (n == 0) return DGNN_OK;
+    DGNN_CK(cudaSetDevice(c->device));
+    const bool v16 = row_bytes % 16 == 0 && aligned16(features) && aligned16(out);
+    const int grid = grid_for(c, n * 32 / kPackU, 256, 8);
+    launch(c, DGNN_K_GATHER, (double)n * (2.0 * row_bytes + 4.0), [&] {
+        if (v16)
+            k_gather<uint4><<<grid, 256, 0, c->stream>>>((const uint8_t*)features, row_bytes, ids, n, (uint8_t*)out);
+        else
+            k_gather<uint32_t><<<grid, 256, 0, c->stream>>>((const uint8_t*)features, row_bytes, ids, n,
+                                                             (uint8_t*)out);
+    });
+    DGNN_CK_LAUNCH();
+    return DGNN_OK;
+}

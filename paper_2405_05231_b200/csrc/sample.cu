@@ -1,0 +1,820 @@
+// sample.cu -- a1-a3: offline K-hop node-wise neighbour sampling of many
+// mini-batches (Sec. 2 "node-wise sampling ... uses a fan-out
+// vector"; Sec. 3 "sample many mini-batches before running their
+// model computation"), with the per-node access counter of P:271 fused into
+// the dedup step.  Semantics: DESIGN.md readings c1-c14, c24, c26.
+//
+// Design (B200): batches are processed in sampling groups of G slots; every
+// step of a hop runs over the flattened frontier / candidate / new-node sets of
+// all G batches at once, sized on the device (no host round trip inside a
+// group):
+//   hop_begin   frontier prefix over slots                        (1 block)
+//   scan        cand offsets = exclusive scan of min(k, deg(v))   (decoupled look-back)
+//   sample_hop  warp per frontier node: Philox draws (lane s = slot s), Floyd
+//               resolution with warp ballots, rank-sort of the k positions,
+//               gather of indices[], per-batch hash-set insert (CAS); first
+//               insert -> counts[u] += 1 and warp-aggregated append
+//   order       bucket sort of each batch's new IDs: histogram on (slot,
+//               id >> shift), scan, scatter, per-bucket insertion sort, and
+//               local-ID assignment into the hash set
+//   remap       cand[i] = local(cand[i])
+//   hop_end     frontier <- the new nodes                          (1 block)
+// then one host sync per group sizes the batch-major compaction into the
+// output arena.
+#include <algorithm>
+
+#include "internal.cuh"
+
+namespace dgnn {
+namespace {
+
+constexpr int kMaxGroup = 256;
+constexpr int32_t kEmpty = -1;
+constexpr unsigned kFull = 0xffffffffu;
+
+struct Grp {
+    int G;
+    int tlog;
+    uint32_t tmask;
+    int H;
+    int64_t cap_n;
+    int32_t* nodes;      // [G*cap_n]
+    int2* table;         // [G << tlog] {key, local}
+    int32_t* n;          // [G] nodes so far
+    int32_t* fr_lo;      // [G]
+    int32_t* fr_hi;      // [G]
+    int32_t* new_cnt;    // [G]
+    int64_t* fr_off;     // [G+1]
+    int64_t* cand_base;  // [G+1]
+    int64_t* new_off;    // [G+1]
+    int64_t* cand_total; // [1]
+    int32_t* hop_bound;  // [G*(H+2)]
+    int64_t* hop_fr_off; // [H*(kMaxGroup+1)]
+    int64_t* hop_cbase;  // [H*(kMaxGroup+1)]
+};
+
+__device__ __forceinline__ uint32_t slot_hash(int32_t key, int tlog) {
+    return ((uint32_t)key * 2654435761u) >> (32 - tlog);
+}
+
+// 1 = inserted, 0 = already present, -1 = table full
+__device__ __forceinline__ int table_insert(int2* tab, int tlog, uint32_t mask, int32_t key, int32_t value) {
+    uint32_t p = slot_hash(key, tlog);
+    for (uint32_t probes = 0; probes <= mask; ++probes) {
+        const int prev = atomicCAS(&tab[p].x, kEmpty, key);
+        if (prev == kEmpty) {
+            if (value >= 0) tab[p].y = value;
+            return 1;
+        }
+        if (prev == key) return 0;
+        p = (p + 1) & mask;
+    }
+    return -1;
+}
+
+__device__ __forceinline__ int2* table_find(int2* tab, int tlog, uint32_t mask, int32_t key) {
+    uint32_t p = slot_hash(key, tlog);
+    for (uint32_t probes = 0; probes <= mask; ++probes) {
+        int2* e = &tab[p];
+        const int k = e->x;
+        if (k == key) return e;
+        if (k == kEmpty) return nullptr;
+        p = (p + 1) & mask;
+    }
+    return nullptr;
+}
+
+// ----------------------------------------------------------------- seeds
+__global__ void k_seed_init(Grp g, const int32_t* __restrict__ seeds, int64_t num_seeds, int32_t B, int64_t t0,
+                            int64_t N, uint32_t* counts, int* err) {
+    const int s = blockIdx.x;
+    const int64_t a = (t0 + s) * (int64_t)B;
+    const int64_t ns = min((int64_t)B, num_seeds - a);
+    if (threadIdx.x == 0) {
+        g.n[s] = (int32_t)ns;
+        g.fr_lo[s] = 0;
+        g.fr_hi[s] = (int32_t)ns;
+        g.new_cnt[s] = 0;
+        g.hop_bound[s * (g.H + 2) + 0] = 0;
+        g.hop_bound[s * (g.H + 2) + 1] = (int32_t)ns;
+    }
+    int2* tab = g.table + ((int64_t)s << g.tlog);
+    for (int64_t i = threadIdx.x; i < ns; i += blockDim.x) {
+        const int32_t u = seeds[a + i];
+        if (u < 0 || (int64_t)u >= N) {
+            atomicOr(err, DEVERR_SEED_RANGE);
+            g.nodes[(int64_t)s * g.cap_n + i] = 0;
+            continue;
+        }
+        g.nodes[(int64_t)s * g.cap_n + i] = u;
+        const int r = table_insert(tab, g.tlog, g.tmask, u, (int32_t)i);
+        if (r == 0) atomicOr(err, DEVERR_SEED_DUP);
+        else if (r < 0) atomicOr(err, DEVERR_TABLE);
+        else if (counts) atomicAdd(&counts[u], 1u);
+    }
+}
+
+__global__ void k_seed_range(const int32_t* __restrict__ seeds, int64_t n, int64_t N, int* err) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t u = seeds[i];
+        if (u < 0 || (int64_t)u >= N) atomicOr(err, DEVERR_SEED_RANGE);
+    }
+}
+
+// ------------------------------------------------------ per-hop bookkeeping
+__global__ void k_hop_begin(Grp g, int h) {
+    if (threadIdx.x != 0) return;
+    int64_t acc = 0;
+    for (int s = 0; s < g.G; ++s) {
+        g.fr_off[s] = acc;
+        g.hop_fr_off[h * (kMaxGroup + 1) + s] = acc;
+        acc += g.fr_hi[s] - g.fr_lo[s];
+    }
+    g.fr_off[g.G] = acc;
+    g.hop_fr_off[h * (kMaxGroup + 1) + g.G] = acc;
+}
+
+__global__ void k_hop_cands(Grp g, int h, int64_t* cptr) {
+    if (threadIdx.x != 0) return;
+    const int64_t F = g.fr_off[g.G];
+    cptr[F] = *g.cand_total;
+    for (int s = 0; s <= g.G; ++s) {
+        const int64_t c = cptr[g.fr_off[s]];
+        g.cand_base[s] = c;
+        g.hop_cbase[h * (kMaxGroup + 1) + s] = c;
+    }
+}
+
+__global__ void k_new_setup(Grp g) {
+    if (threadIdx.x != 0) return;
+    int64_t acc = 0;
+    for (int s = 0; s < g.G; ++s) {
+        g.new_off[s] = acc;
+        acc += g.new_cnt[s];
+    }
+    g.new_off[g.G] = acc;
+}
+
+__global__ void k_hop_end(Grp g, int h) {
+    for (int s = threadIdx.x; s < g.G; s += blockDim.x) {
+        const int32_t n0 = g.n[s], c = g.new_cnt[s];
+        g.hop_bound[s * (g.H + 2) + h + 2] = n0 + c;
+        g.fr_lo[s] = n0;
+        g.fr_hi[s] = n0 + c;
+        g.n[s] = n0 + c;
+        g.new_cnt[s] = 0;
+    }
+}
+
+// ------------------------------------------------ a2: the sampling kernel
+struct DegIn {
+    Grp g;
+    const int64_t* indptr;
+    int k;
+    __device__ __forceinline__ int64_t operator()(int64_t t) const {
+        const int s = segment_of(g.fr_off, g.G + 1, t);
+        const int64_t j = g.fr_lo[s] + (t - g.fr_off[s]);
+        const int32_t v = g.nodes[(int64_t)s * g.cap_n + j];
+        const int64_t d = indptr[v + 1] - indptr[v];
+        return d < k ? d : k;
+    }
+};
+
+struct StoreExcl {
+    int64_t* out;
+    __device__ __forceinline__ void operator()(int64_t i, int64_t excl, int64_t) const { out[i] = excl; }
+};
+
+__device__ __forceinline__ void insert_append(int2* tab, int tlog, uint32_t mask, int32_t* new_cnt_s,
+                                              int32_t* newdst, int32_t u, bool act, uint32_t* counts, int* err,
+                                              int lane) {
+    const int r = act ? table_insert(tab, tlog, mask, u, -1) : 0;
+    if (r < 0) atomicOr(err, DEVERR_TABLE);
+    const bool nw = r > 0;
+    if (nw && counts) atomicAdd(&counts[u], 1u);
+    const unsigned m = __ballot_sync(kFull, nw);
+    if (m) {
+        const int leader = __ffs(m) - 1;
+        int pos0 = 0;
+        if (lane == leader) pos0 = atomicAdd(new_cnt_s, __popc(m));
+        pos0 = __shfl_sync(kFull, pos0, leader);
+        if (nw) newdst[pos0 + __popc(m & lanemask_lt())] = u;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_sample_hop(Grp g, const int64_t* __restrict__ indptr,
+                                                    const int32_t* __restrict__ indices, int k, uint64_t seed,
+                                                    int64_t bid0, int h, const int64_t* __restrict__ cptr,
+                                                    int32_t* __restrict__ cand, uint32_t* counts, int* err) {
+    __shared__ int64_t s_fr[kMaxGroup + 1];
+    for (int i = threadIdx.x; i <= g.G; i += blockDim.x) s_fr[i] = g.fr_off[i];
+    __syncthreads();
+    const int64_t F = s_fr[g.G];
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < F; t += nwarps) {
+        const int s = segment_of(s_fr, g.G + 1, t);
+        const int64_t j = g.fr_lo[s] + (t - s_fr[s]);
+        const int32_t v = g.nodes[(int64_t)s * g.cap_n + j];
+        const int64_t start = indptr[v];
+        const int64_t d = indptr[v + 1] - start;
+        const int64_t base = cptr[t];
+        const uint64_t bid = (uint64_t)(bid0 + s);
+        int2* tab = g.table + ((int64_t)s << g.tlog);
+        int32_t* newdst = g.nodes + (int64_t)s * g.cap_n + g.n[s];
+        int32_t* ncnt = g.new_cnt + s;
+        if (d <= k) {
+            // reading c3: take every position, in CSR order
+            for (int64_t p0 = 0; p0 < d; p0 += 32) {
+                const int64_t p = p0 + lane;
+                const bool act = p < d;
+                const int32_t u = act ? indices[start + p] : 0;
+                if (act) cand[base + p] = u;
+                insert_append(tab, g.tlog, g.tmask, ncnt, newdst, u, act, counts, err, lane);
+            }
+        } else if (k <= 32) {
+            // Floyd (readings c6, c7): lane s draws t_s in [0, d-k+s]; resolution in slot order
+            const int64_t i = d - k + lane;
+            int64_t tdraw = 0;
+            if (lane < k)
+                tdraw = (int64_t)__umul64hi(draw64(seed, (uint32_t)v, bid, (uint32_t)h, (uint32_t)lane),
+                                            (uint64_t)(i + 1));
+            int64_t S = -1;
+            for (int r = 0; r < k; ++r) {
+                const int64_t tr = __shfl_sync(kFull, tdraw, r);
+                const unsigned hit = __ballot_sync(kFull, lane < r && S == tr);
+                if (lane == r) S = hit ? i : tr;
+            }
+            int rank = 0;
+            for (int q = 0; q < k; ++q) {
+                const int64_t Sq = __shfl_sync(kFull, S, q);
+                rank += (Sq < S) ? 1 : 0;
+            }
+            const bool act = lane < k;
+            const int32_t u = act ? indices[start + S] : 0;
+            if (act) cand[base + rank] = u;
+            insert_append(tab, g.tlog, g.tmask, ncnt, newdst, u, act, counts, err, lane);
+        } else {
+            // k > 32: one lane runs Floyd sequentially using the candidate slots as scratch
+            if (lane == 0) {
+                if (d >= (int64_t)INT32_MAX) atomicOr(err, DEVERR_OVERFLOW);
+                for (int s2 = 0; s2 < k; ++s2) {
+                    const int64_t i = d - k + s2;
+                    const int64_t tt = (int64_t)__umul64hi(
+                        draw64(seed, (uint32_t)v, bid, (uint32_t)h, (uint32_t)s2), (uint64_t)(i + 1));
+                    bool present = false;
+                    for (int r = 0; r < s2; ++r)
+                        if ((int64_t)cand[base + r] == tt) {
+                            present = true;
+                            break;
+                        }
+                    cand[base + s2] = (int32_t)(present ? i : tt);
+                }
+                for (int a = 1; a < k; ++a) {
+                    const int32_t x = cand[base + a];
+                    int b = a - 1;
+                    while (b >= 0 && cand[base + b] > x) {
+                        cand[base + b + 1] = cand[base + b];
+                        --b;
+                    }
+                    cand[base + b + 1] = x;
+                }
+            }
+            __syncwarp();
+            for (int p0 = 0; p0 < k; p0 += 32) {
+                const int p = p0 + lane;
+                const bool act = p < k;
+                const int32_t u = act ? indices[start + cand[base + p]] : 0;
+                if (act) cand[base + p] = u;
+                insert_append(tab, g.tlog, g.tmask, ncnt, newdst, u, act, counts, err, lane);
+            }
+        }
+    }
+}
+
+// ---------------------------------- a3: order the new nodes of every batch
+__global__ void k_bucket_hist(Grp g, int64_t NB, int shift, int32_t* __restrict__ hist, int32_t* __restrict__ tmp_key,
+                              int32_t* __restrict__ tmp_pos) {
+    __shared__ int64_t s_off[kMaxGroup + 1];
+    for (int i = threadIdx.x; i <= g.G; i += blockDim.x) s_off[i] = g.new_off[i];
+    __syncthreads();
+    const int64_t TN = s_off[g.G];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < TN; i += (int64_t)gridDim.x * blockDim.x) {
+        const int s = segment_of(s_off, g.G + 1, i);
+        const int32_t u = g.nodes[(int64_t)s * g.cap_n + g.n[s] + (i - s_off[s])];
+        const int64_t b = (int64_t)s * NB + (u >> shift);
+        tmp_key[i] = u;
+        tmp_pos[i] = atomicAdd(&hist[b], 1);
+    }
+}
+
+__global__ void k_bucket_scatter(Grp g, int64_t NB, int shift, const int64_t* __restrict__ bstart,
+                                 const int32_t* __restrict__ tmp_key, const int32_t* __restrict__ tmp_pos,
+                                 int32_t* __restrict__ sorted) {
+    __shared__ int64_t s_off[kMaxGroup + 1];
+    for (int i = threadIdx.x; i <= g.G; i += blockDim.x) s_off[i] = g.new_off[i];
+    __syncthreads();
+    const int64_t TN = s_off[g.G];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < TN; i += (int64_t)gridDim.x * blockDim.x) {
+        const int s = segment_of(s_off, g.G + 1, i);
+        const int32_t u = tmp_key[i];
+        const int64_t b = (int64_t)s * NB + (u >> shift);
+        sorted[bstart[b] + tmp_pos[i]] = u;
+    }
+}
+
+// thread per bucket: insertion sort of its (few) keys, then local-ID assignment
+__global__ void k_bucket_sort_assign(Grp g, int64_t NB, const int64_t* __restrict__ bstart,
+                                     const int32_t* __restrict__ hist, int32_t* __restrict__ sorted, int* err) {
+    const int64_t nbk = (int64_t)g.G * NB;
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nbk; b += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t c = hist[b];
+        if (c == 0) continue;
+        const int64_t lo = bstart[b];
+        int32_t* a = sorted + lo;
+        for (int x = 1; x < c; ++x) {
+            const int32_t key = a[x];
+            int y = x - 1;
+            while (y >= 0 && a[y] > key) {
+                a[y + 1] = a[y];
+                --y;
+            }
+            a[y + 1] = key;
+        }
+        const int s = (int)(b / NB);
+        const int64_t off = g.new_off[s];
+        const int32_t n0 = g.n[s];
+        int2* tab = g.table + ((int64_t)s << g.tlog);
+        for (int x = 0; x < c; ++x) {
+            const int32_t u = a[x];
+            const int32_t local = n0 + (int32_t)(lo + x - off);
+            g.nodes[(int64_t)s * g.cap_n + local] = u;
+            int2* e = table_find(tab, g.tlog, g.tmask, u);
+            if (e) e->y = local;
+            else atomicOr(err, DEVERR_TABLE);
+        }
+    }
+}
+
+__global__ void k_remap(Grp g, int32_t* __restrict__ cand, int* err) {
+    __shared__ int64_t s_cb[kMaxGroup + 1];
+    for (int i = threadIdx.x; i <= g.G; i += blockDim.x) s_cb[i] = g.cand_base[i];
+    __syncthreads();
+    const int64_t C = s_cb[g.G];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < C; i += (int64_t)gridDim.x * blockDim.x) {
+        const int s = segment_of(s_cb, g.G + 1, i);
+        const int2* e = table_find(g.table + ((int64_t)s << g.tlog), g.tlog, g.tmask, cand[i]);
+        if (e) cand[i] = e->y;
+        else atomicOr(err, DEVERR_TABLE);
+    }
+}
+
+// ------------------------------------------------ batch-major compaction
+struct CompactPlan {
+    int G;
+    int H;
+    int64_t cap_n;
+    const int64_t* node_pre;     // [G+1] group-relative node prefix
+    const int64_t* edge_pre;     // [G+1]
+    const int64_t* eptr_pre;     // [G+1]
+    const int64_t* edges_before; // [H*G]
+    const int64_t* hop_fr_off;   // [H*(kMaxGroup+1)]
+    const int64_t* hop_cbase;    // [H*(kMaxGroup+1)]
+    const int32_t* hop_bound;    // [G*(H+2)]
+    int64_t* const* cptr;        // [H] device pointers
+};
+
+__global__ void k_compact_nodes(CompactPlan p, const int32_t* __restrict__ gnodes, int32_t* __restrict__ out) {
+    __shared__ int64_t s_pre[kMaxGroup + 1];
+    for (int i = threadIdx.x; i <= p.G; i += blockDim.x) s_pre[i] = p.node_pre[i];
+    __syncthreads();
+    const int64_t T = s_pre[p.G];
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < T; q += (int64_t)gridDim.x * blockDim.x) {
+        const int s = segment_of(s_pre, p.G + 1, q);
+        out[q] = gnodes[(int64_t)s * p.cap_n + (q - s_pre[s])];
+    }
+}
+
+__global__ void k_compact_edges(CompactPlan p, int h, const int32_t* __restrict__ cand, int32_t* __restrict__ out) {
+    __shared__ int64_t s_cb[kMaxGroup + 1];
+    const int64_t* cb = p.hop_cbase + h * (kMaxGroup + 1);
+    for (int i = threadIdx.x; i <= p.G; i += blockDim.x) s_cb[i] = cb[i];
+    __syncthreads();
+    const int64_t C = s_cb[p.G];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < C; i += (int64_t)gridDim.x * blockDim.x) {
+        const int s = segment_of(s_cb, p.G + 1, i);
+        out[p.edge_pre[s] + p.edges_before[h * p.G + s] + (i - s_cb[s])] = cand[i];
+    }
+}
+
+__global__ void k_compact_eptr(CompactPlan p, int32_t* __restrict__ out) {
+    __shared__ int64_t s_pre[kMaxGroup + 1];
+    for (int i = threadIdx.x; i <= p.G; i += blockDim.x) s_pre[i] = p.eptr_pre[i];
+    __syncthreads();
+    const int64_t T = s_pre[p.G];
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < T; q += (int64_t)gridDim.x * blockDim.x) {
+        const int s = segment_of(s_pre, p.G + 1, q);
+        const int64_t j = q - s_pre[s];
+        const int32_t* hb = p.hop_bound + s * (p.H + 2);
+        int64_t val;
+        if (j == hb[p.H]) {
+            val = p.edge_pre[s + 1] - p.edge_pre[s];
+        } else {
+            int h = 0;
+            while (!(j < hb[h + 1])) ++h;  // frontier of hop h: local [hb[h], hb[h+1])
+            const int64_t t = p.hop_fr_off[h * (kMaxGroup + 1) + s] + (j - hb[h]);
+            val = p.cptr[h][t] - p.hop_cbase[h * (kMaxGroup + 1) + s] + p.edges_before[h * p.G + s];
+        }
+        out[q] = (int32_t)val;
+    }
+}
+
+// ------------------------------------------------------------ host side
+int ceil_log2(int64_t x) {
+    int b = 0;
+    while (((int64_t)1 << b) < x) ++b;
+    return b;
+}
+
+int64_t sat_mul(int64_t a, int64_t b, int64_t cap) {
+    if (a == 0 || b == 0) return 0;
+    if (a > cap / b) return cap;
+    return std::min(a * b, cap);
+}
+
+struct Arena {
+    dgnn_ctx* c;
+    int32_t* p = nullptr;
+    int64_t cap = 0;
+    ~Arena() {
+        if (p) dev_free(c, p, (size_t)cap * 4);
+    }
+    int32_t* release() {
+        int32_t* q = p;
+        p = nullptr;
+        return q;
+    }
+    dgnn_status reserve(int64_t need, int64_t used) {
+        if (need <= cap) return DGNN_OK;
+        int64_t ncap = std::max<int64_t>(need, cap + cap / 2);
+        int32_t* q = (int32_t*)dev_alloc(c, (size_t)ncap * 4);
+        if (!q) {
+            set_error("sample arena allocation of %lld bytes failed", (long long)ncap * 4);
+            return DGNN_ENOMEM;
+        }
+        if (p) {
+            if (used) DGNN_CK(cudaMemcpyAsync(q, p, (size_t)used * 4, cudaMemcpyDeviceToDevice, c->stream));
+            dev_free(c, p, (size_t)cap * 4);
+        }
+        p = q;
+        cap = ncap;
+        return DGNN_OK;
+    }
+};
+
+}  // namespace
+}  // namespace dgnn
+
+using namespace dgnn;
+
+extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32_t* seeds, int64_t num_seeds,
+                                   int32_t batch_size, int64_t batch_id_base, const int32_t* fanout,
+                                   int32_t num_hops, uint64_t rng_seed, uint32_t* counts, dgnn_samples** out) {
+    DGNN_REQUIRE(c && csr && out, "dgnn_sample: NULL argument");
+    *out = nullptr;
+    DGNN_REQUIRE(csr->num_nodes > 0 && csr->num_nodes < ((int64_t)1 << DGNN_TIER_SHIFT),
+                 "dgnn_sample: num_nodes must be in [1, 2^30)");
+    DGNN_REQUIRE(csr->indptr && (csr->indices || csr->num_edges == 0), "dgnn_sample: CSR arrays are NULL");
+    DGNN_REQUIRE(batch_size > 0, "dgnn_sample: batch_size must be positive");
+    DGNN_REQUIRE(num_seeds >= 0 && (seeds || num_seeds == 0), "dgnn_sample: bad seeds");
+    DGNN_REQUIRE(batch_id_base >= 0, "dgnn_sample: batch_id_base must be >= 0");
+    DGNN_REQUIRE(num_hops >= 1 && num_hops <= 65535 && fanout, "dgnn_sample: num_hops must be in [1, 65535]");
+    for (int h = 0; h < num_hops; ++h)
+        DGNN_REQUIRE(fanout[h] >= 0 && fanout[h] <= 65535, "dgnn_sample: fanout[%d]=%d outside [0, 65535]", h,
+                     fanout[h]);
+    DGNN_CK(cudaSetDevice(c->device));
+    const int64_t N = csr->num_nodes;
+    const int H = num_hops;
+    const int64_t B = batch_size;
+    const int64_t nb = (num_seeds + B - 1) / B;
+
+    auto* S = new dgnn_samples();
+    S->ctx = c;
+    S->nb = nb;
+    S->H = H;
+    S->batch_id_base = batch_id_base;
+    struct Guard {
+        dgnn_samples* s;
+        ~Guard() { if (s) dgnn_samples_free(s); }
+    } guard{S};
+    S->node_off_h.assign(nb + 1, 0);
+    S->edge_off_h.assign(nb + 1, 0);
+    S->eptr_off_h.assign(nb + 1, 0);
+    S->hop_off_h.assign(nb * (H + 2), 0);
+
+    if (nb > 0) {
+        // all seeds in range before any counting
+        launch(c, DGNN_K_SAMPLE_SEED, 0.0, [&] {
+            k_seed_range<<<grid_for(c, num_seeds, 256), 256, 0, c->stream>>>(seeds, num_seeds, N, c->dev_err);
+        });
+        DGNN_CK_LAUNCH();
+        DGNN_TRY(check_dev_err(c));
+
+        // ---- capacities (exact upper bounds; reading c26 for k = 0) ----
+        const int64_t kCap = (int64_t)1 << 40;
+        std::vector<int64_t> fr_bound(H), cand_bound(H), new_bound(H);
+        int64_t prod = B, nodes_bound = B;
+        for (int h = 0; h < H; ++h) {
+            fr_bound[h] = prod;
+            prod = sat_mul(prod, fanout[h], kCap);
+            new_bound[h] = prod;
+            nodes_bound = std::min(kCap, nodes_bound + prod);
+        }
+        const int64_t cap_n = std::min(nodes_bound, N);  // a batch's nodes are distinct IDs
+        for (int h = 0; h < H; ++h) {
+            fr_bound[h] = std::min(fr_bound[h], cap_n);
+            new_bound[h] = std::min(new_bound[h], cap_n);
+            cand_bound[h] = sat_mul(fr_bound[h], fanout[h], kCap);
+        }
+        const int tlog = std::max(4, ceil_log2(2 * cap_n));
+        std::vector<int> bb(H), shift(H);
+        const int idbits = std::max(1, ceil_log2(N));
+        int64_t hist_per_slot = 1;
+        for (int h = 0; h < H; ++h) {
+            int b = ceil_log2(std::max<int64_t>(1, new_bound[h] / 4));
+            b = std::min(b, idbits);
+            bb[h] = b;
+            shift[h] = idbits - b;
+            hist_per_slot = std::max<int64_t>(hist_per_slot, (int64_t)1 << b);
+        }
+        int64_t per_slot = cap_n * 4 + ((int64_t)8 << tlog) + hist_per_slot * 12 + cap_n * 12;
+        for (int h = 0; h < H; ++h) per_slot += (fr_bound[h] + 1) * 8 + cand_bound[h] * 4;
+        int64_t G = c->sample_group;
+        if (G <= 0) {
+            const int64_t budget = (int64_t)6 << 30;
+            G = std::max<int64_t>(1, std::min<int64_t>(64, budget / std::max<int64_t>(per_slot, 1)));
+        }
+        G = std::min<int64_t>(std::min<int64_t>(G, kMaxGroup), nb);
+
+        // ---- group scratch ----
+        DevBuf<int32_t> d_nodes, d_small32, d_hist, d_tmpk, d_tmpp, d_sorted;
+        DevBuf<int2> d_table;
+        DevBuf<int64_t> d_small64, d_bstart, d_plan;
+        std::vector<DevBuf<int32_t>> d_cand(H);
+        std::vector<DevBuf<int64_t>> d_cptr(H);
+        DevBuf<int64_t*> d_cptr_list;
+        DGNN_TRY(d_nodes.alloc(c, (size_t)(G * cap_n)));
+        DGNN_TRY(d_table.alloc(c, (size_t)(G << tlog)));
+        DGNN_TRY(d_small32.alloc(c, (size_t)(4 * G + G * (H + 2))));
+        DGNN_TRY(d_small64.alloc(c, (size_t)(3 * (G + 1) + 1 + 2 * H * (kMaxGroup + 1))));
+        DGNN_TRY(d_hist.alloc(c, (size_t)(G * hist_per_slot)));
+        DGNN_TRY(d_bstart.alloc(c, (size_t)(G * hist_per_slot)));
+        DGNN_TRY(d_tmpk.alloc(c, (size_t)(G * cap_n)));
+        DGNN_TRY(d_tmpp.alloc(c, (size_t)(G * cap_n)));
+        DGNN_TRY(d_sorted.alloc(c, (size_t)(G * cap_n)));
+        for (int h = 0; h < H; ++h) {
+            DGNN_TRY(d_cand[h].alloc(c, (size_t)std::max<int64_t>(1, G * cand_bound[h])));
+            DGNN_TRY(d_cptr[h].alloc(c, (size_t)(G * fr_bound[h] + 1)));
+        }
+        DGNN_TRY(d_cptr_list.alloc(c, (size_t)H));
+        {
+            std::vector<int64_t*> ptrs(H);
+            for (int h = 0; h < H; ++h) ptrs[h] = d_cptr[h].p;
+            DGNN_CK(cudaMemcpyAsync(d_cptr_list.p, ptrs.data(), sizeof(int64_t*) * H, cudaMemcpyHostToDevice,
+                                    c->stream));
+            DGNN_CK(cudaStreamSynchronize(c->stream));  // ptrs is a stack vector
+        }
+        Grp g{};
+        g.tlog = tlog;
+        g.tmask = (uint32_t)((1ull << tlog) - 1);
+        g.H = H;
+        g.cap_n = cap_n;
+        g.nodes = d_nodes.p;
+        g.table = d_table.p;
+        g.n = d_small32.p;
+        g.fr_lo = g.n + G;
+        g.fr_hi = g.fr_lo + G;
+        g.new_cnt = g.fr_hi + G;
+        g.hop_bound = g.new_cnt + G;
+        g.fr_off = d_small64.p;
+        g.cand_base = g.fr_off + (G + 1);
+        g.new_off = g.cand_base + (G + 1);
+        g.cand_total = g.new_off + (G + 1);
+        g.hop_fr_off = g.cand_total + 1;
+        g.hop_cbase = g.hop_fr_off + H * (kMaxGroup + 1);
+
+        Arena a_nodes{c}, a_edges{c}, a_eptr{c};
+        int64_t used_nodes = 0, used_edges = 0, used_eptr = 0;
+        std::vector<int32_t> h_n(G), h_hb(G * (H + 2));
+        std::vector<int64_t> h_frs(H * (kMaxGroup + 1)), h_cbs(H * (kMaxGroup + 1));
+        std::vector<int64_t> h_plan;
+
+        for (int64_t t0 = 0; t0 < nb; t0 += G) {
+            const int Gc = (int)std::min<int64_t>(G, nb - t0);
+            g.G = Gc;
+            DGNN_TRY(memset_async(c, d_table.p, 0xFF, sizeof(int2) * ((size_t)Gc << tlog)));
+            launch(c, DGNN_K_SAMPLE_SEED, 0.0, [&] {
+                k_seed_init<<<Gc, 256, 0, c->stream>>>(g, seeds, num_seeds, batch_size, t0, N, counts, c->dev_err);
+            });
+            DGNN_CK_LAUNCH();
+            for (int h = 0; h < H; ++h) {
+                const int k = fanout[h];
+                launch(c, DGNN_K_SAMPLE_SETUP, 0.0, [&] { k_hop_begin<<<1, 32, 0, c->stream>>>(g, h); });
+                DGNN_CK_LAUNCH();
+                DGNN_TRY(scan::run(c, Gc * fr_bound[h], g.fr_off + Gc, DegIn{g, csr->indptr, k},
+                                   StoreExcl{d_cptr[h].p}, g.cand_total));
+                launch(c, DGNN_K_SAMPLE_SETUP, 0.0,
+                       [&] { k_hop_cands<<<1, 32, 0, c->stream>>>(g, h, d_cptr[h].p); });
+                DGNN_CK_LAUNCH();
+                launch(c, DGNN_K_SAMPLE_HOP, 0.0, [&] {
+                    k_sample_hop<<<grid_for(c, Gc * fr_bound[h] * 32, 256), 256, 0, c->stream>>>(
+                        g, csr->indptr, csr->indices, k, rng_seed, batch_id_base + t0, h, d_cptr[h].p, d_cand[h].p,
+                        counts, c->dev_err);
+                });
+                DGNN_CK_LAUNCH();
+                launch(c, DGNN_K_SAMPLE_SETUP, 0.0, [&] { k_new_setup<<<1, 32, 0, c->stream>>>(g); });
+                DGNN_CK_LAUNCH();
+                // order the new nodes: bucket sort by (slot, id >> shift)
+                const int64_t NB = (int64_t)1 << bb[h];
+                const int64_t nbk = Gc * NB;
+                const int64_t tn_bound = Gc * new_bound[h];
+                DGNN_TRY(memset_async(c, d_hist.p, 0, sizeof(int32_t) * (size_t)nbk));
+                launch(c, DGNN_K_SAMPLE_ORDER, 0.0, [&] {
+                    k_bucket_hist<<<grid_for(c, tn_bound, 256), 256, 0, c->stream>>>(g, NB, shift[h], d_hist.p,
+                                                                                       d_tmpk.p, d_tmpp.p);
+                });
+                DGNN_CK_LAUNCH();
+                {
+                    const int32_t* hist = d_hist.p;
+                    int64_t* bst = d_bstart.p;
+                    DGNN_TRY(scan::run(
+                        c, nbk, nullptr, [=] __device__(int64_t i) -> int64_t { return hist[i]; },
+                        [=] __device__(int64_t i, int64_t e, int64_t) { bst[i] = e; }, nullptr));
+                }
+                launch(c, DGNN_K_SAMPLE_ORDER, 0.0, [&] {
+                    k_bucket_scatter<<<grid_for(c, tn_bound, 256), 256, 0, c->stream>>>(
+                        g, NB, shift[h], d_bstart.p, d_tmpk.p, d_tmpp.p, d_sorted.p);
+                });
+                DGNN_CK_LAUNCH();
+                launch(c, DGNN_K_SAMPLE_ORDER, 0.0, [&] {
+                    k_bucket_sort_assign<<<grid_for(c, nbk, 256), 256, 0, c->stream>>>(g, NB, d_bstart.p, d_hist.p,
+                                                                                         d_sorted.p, c->dev_err);
+                });
+                DGNN_CK_LAUNCH();
+                launch(c, DGNN_K_SAMPLE_REMAP, 0.0, [&] {
+                    k_remap<<<grid_for(c, Gc * cand_bound[h], 256), 256, 0, c->stream>>>(g, d_cand[h].p,
+                                                                                         c->dev_err);
+                });
+                DGNN_CK_LAUNCH();
+                launch(c, DGNN_K_SAMPLE_SETUP, 0.0, [&] { k_hop_end<<<1, 256, 0, c->stream>>>(g, h); });
+                DGNN_CK_LAUNCH();
+            }
+            // ---- group end: read sizes, then compact into the batch-major arena ----
+            DGNN_CK(cudaMemcpyAsync(h_n.data(), g.n, sizeof(int32_t) * Gc, cudaMemcpyDeviceToHost, c->stream));
+            DGNN_CK(cudaMemcpyAsync(h_hb.data(), g.hop_bound, sizeof(int32_t) * Gc * (H + 2), cudaMemcpyDeviceToHost,
+                                    c->stream));
+            DGNN_CK(cudaMemcpyAsync(h_frs.data(), g.hop_fr_off, sizeof(int64_t) * H * (kMaxGroup + 1),
+                                    cudaMemcpyDeviceToHost, c->stream));
+            DGNN_CK(cudaMemcpyAsync(h_cbs.data(), g.hop_cbase, sizeof(int64_t) * H * (kMaxGroup + 1),
+                                    cudaMemcpyDeviceToHost, c->stream));
+            DGNN_TRY(check_dev_err(c));  // synchronizes
+            // plan: node_pre[G+1], edge_pre[G+1], eptr_pre[G+1], edges_before[H*G]
+            h_plan.assign(3 * (Gc + 1) + H * Gc, 0);
+            int64_t* node_pre = h_plan.data();
+            int64_t* edge_pre = node_pre + (Gc + 1);
+            int64_t* eptr_pre = edge_pre + (Gc + 1);
+            int64_t* ebef = eptr_pre + (Gc + 1);
+            for (int s = 0; s < Gc; ++s) {
+                int64_t e = 0;
+                for (int h = 0; h < H; ++h) {
+                    ebef[h * Gc + s] = e;
+                    e += h_cbs[h * (kMaxGroup + 1) + s + 1] - h_cbs[h * (kMaxGroup + 1) + s];
+                }
+                node_pre[s + 1] = node_pre[s] + h_n[s];
+                edge_pre[s + 1] = edge_pre[s] + e;
+                eptr_pre[s + 1] = eptr_pre[s] + h_hb[s * (H + 2) + H] + 1;
+                const int64_t b = t0 + s;
+                S->node_off_h[b + 1] = S->node_off_h[b] + h_n[s];
+                S->edge_off_h[b + 1] = S->edge_off_h[b] + e;
+                S->eptr_off_h[b + 1] = S->eptr_off_h[b] + h_hb[s * (H + 2) + H] + 1;
+                for (int x = 0; x < H + 2; ++x) S->hop_off_h[b * (H + 2) + x] = h_hb[s * (H + 2) + x];
+            }
+            // grow the arena (estimate the whole run from the groups seen so far)
+            const double frac = (double)nb / (double)(t0 + Gc);
+            auto est = [&](int64_t used, int64_t add) {
+                return (int64_t)((double)(used + add) * frac * 1.02) + 1024;
+            };
+            DGNN_TRY(a_nodes.reserve(used_nodes + node_pre[Gc] > a_nodes.cap ? est(used_nodes, node_pre[Gc]) : 0,
+                                     used_nodes));
+            DGNN_TRY(a_edges.reserve(used_edges + edge_pre[Gc] > a_edges.cap ? est(used_edges, edge_pre[Gc]) : 0,
+                                     used_edges));
+            DGNN_TRY(a_eptr.reserve(used_eptr + eptr_pre[Gc] > a_eptr.cap ? est(used_eptr, eptr_pre[Gc]) : 0,
+                                    used_eptr));
+            DGNN_TRY(d_plan.alloc(c, h_plan.size()));
+            DGNN_CK(cudaMemcpyAsync(d_plan.p, h_plan.data(), sizeof(int64_t) * h_plan.size(), cudaMemcpyHostToDevice,
+                                    c->stream));
+            CompactPlan p{};
+            p.G = Gc;
+            p.H = H;
+            p.cap_n = cap_n;
+            p.node_pre = d_plan.p;
+            p.edge_pre = p.node_pre + (Gc + 1);
+            p.eptr_pre = p.edge_pre + (Gc + 1);
+            p.edges_before = p.eptr_pre + (Gc + 1);
+            p.hop_fr_off = g.hop_fr_off;
+            p.hop_cbase = g.hop_cbase;
+            p.hop_bound = g.hop_bound;
+            p.cptr = d_cptr_list.p;
+            launch(c, DGNN_K_SAMPLE_COMPACT, 8.0 * node_pre[Gc], [&] {
+                k_compact_nodes<<<grid_for(c, node_pre[Gc], 256), 256, 0, c->stream>>>(p, g.nodes,
+                                                                                        a_nodes.p + used_nodes);
+            });
+            DGNN_CK_LAUNCH();
+            for (int h = 0; h < H; ++h) {
+                const int64_t Ch = h_cbs[h * (kMaxGroup + 1) + Gc];
+                if (Ch == 0) continue;
+                launch(c, DGNN_K_SAMPLE_COMPACT, 8.0 * Ch, [&] {
+                    k_compact_edges<<<grid_for(c, Ch, 256), 256, 0, c->stream>>>(p, h, d_cand[h].p,
+                                                                                 a_edges.p + used_edges);
+                });
+                DGNN_CK_LAUNCH();
+            }
+            launch(c, DGNN_K_SAMPLE_COMPACT, 0.0, [&] {
+                k_compact_eptr<<<grid_for(c, eptr_pre[Gc], 256), 256, 0, c->stream>>>(p, a_eptr.p + used_eptr);
+            });
+            DGNN_CK_LAUNCH();
+            used_nodes += node_pre[Gc];
+            used_edges += edge_pre[Gc];
+            used_eptr += eptr_pre[Gc];
+        }
+        S->cap_nodes = a_nodes.cap;
+        S->nodes = a_nodes.release();
+        S->cap_edges = a_edges.cap;
+        S->src_local = a_edges.release();
+        S->cap_eptr = a_eptr.cap;
+        S->eptr = a_eptr.release();
+        S->total_nodes = used_nodes;
+        S->total_edges = used_edges;
+        S->total_eptr = used_eptr;
+    }
+    // offset arrays (device copies of the host mirrors)
+    S->node_off = (int64_t*)dev_alloc(c, sizeof(int64_t) * (nb + 1));
+    S->edge_off = (int64_t*)dev_alloc(c, sizeof(int64_t) * (nb + 1));
+    S->eptr_off = (int64_t*)dev_alloc(c, sizeof(int64_t) * (nb + 1));
+    S->hop_off = (int32_t*)dev_alloc(c, sizeof(int32_t) * std::max<int64_t>(1, nb * (H + 2)));
+    if (!S->node_off || !S->edge_off || !S->eptr_off || !S->hop_off) {
+        set_error("dgnn_sample: offset allocation failed");
+        return DGNN_ENOMEM;
+    }
+    DGNN_CK(cudaMemcpyAsync(S->node_off, S->node_off_h.data(), sizeof(int64_t) * (nb + 1), cudaMemcpyHostToDevice,
+                            c->stream));
+    DGNN_CK(cudaMemcpyAsync(S->edge_off, S->edge_off_h.data(), sizeof(int64_t) * (nb + 1), cudaMemcpyHostToDevice,
+                            c->stream));
+    DGNN_CK(cudaMemcpyAsync(S->eptr_off, S->eptr_off_h.data(), sizeof(int64_t) * (nb + 1), cudaMemcpyHostToDevice,
+                            c->stream));
+    if (nb)
+        DGNN_CK(cudaMemcpyAsync(S->hop_off, S->hop_off_h.data(), sizeof(int32_t) * nb * (H + 2),
+                                cudaMemcpyHostToDevice, c->stream));
+    DGNN_CK(cudaStreamSynchronize(c->stream));  // host mirrors are the copy sources
+    *out = S;
+    guard.s = nullptr;
+    return DGNN_OK;
+}
+
+extern "C" dgnn_status dgnn_samples_get_info(const dgnn_samples* s, dgnn_samples_info* i) {
+    DGNN_REQUIRE(s && i, "dgnn_samples_get_info: NULL argument");
+    i->num_batches = s->nb;
+    i->num_hops = s->H;
+    i->batch_id_base = s->batch_id_base;
+    i->total_nodes = s->total_nodes;
+    i->total_edges = s->total_edges;
+    i->total_eptr = s->total_eptr;
+    i->node_off = s->node_off;
+    i->nodes = s->nodes;
+    i->hop_off = s->hop_off;
+    i->eptr_off = s->eptr_off;
+    i->eptr = s->eptr;
+    i->edge_off = s->edge_off;
+    i->src_local = s->src_local;
+    i->node_off_host = s->node_off_h.data();
+    i->edge_off_host = s->edge_off_h.data();
+    i->eptr_off_host = s->eptr_off_h.data();
+    i->hop_off_host = s->hop_off_h.data();
+    return DGNN_OK;
+}
+
+extern "C" void dgnn_samples_free(dgnn_samples* s) {
+    if (!s) return;
+    dgnn_ctx* c = s->ctx;
+    if (c) {
+        cudaSetDevice(c->device);
+        dev_free(c, s->nodes, (size_t)s->cap_nodes * 4);
+        dev_free(c, s->src_local, (size_t)s->cap_edges * 4);
+        dev_free(c, s->eptr, (size_t)s->cap_eptr * 4);
+        dev_free(c, s->node_off, sizeof(int64_t) * (s->nb + 1));
+        dev_free(c, s->edge_off, sizeof(int64_t) * (s->nb + 1));
+        dev_free(c, s->eptr_off, sizeof(int64_t) * (s->nb + 1));
+        dev_free(c, s->hop_off, sizeof(int32_t) * std::max<int64_t>(1, s->nb * (s->H + 2)));
+    }
+    delete s;
+}

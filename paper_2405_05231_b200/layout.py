@@ -1,0 +1,259 @@
+"""The offline-layout driver: DiskGNN's layout half (P:508-511 ``DiskGNN_train``)
+over the C ABI, plus the training-time assembler.
+
+    layout = offline_layout(ctx, indptr, indices, features, seeds, fanout, batch_size,
+                            gpu_rows, host_rows, rng_seed, group_size)
+    for b, feats in layout.assemble_epoch():   # feats: [n_b, dim] on the GPU
+        ...
+
+Every step runs in libdgnn.so kernels; this module only sequences the calls,
+owns buffers (torch device tensors, pinned host buffers) and, when
+torch.distributed is initialized with world size > 1, all-reduces the access
+counts (the one exchange step of the path).
+
+Data placement:
+  * CSR, features: HBM (inputs).
+  * GPU tier: HBM buffer [K_g, row_bytes]; host tier: pinned host [K_h, row_bytes]
+    read by the assemble kernel over PCIe through UVA.
+  * Disk tier: a pinned host arena holding every batch's 4 KiB-aligned chunk
+    (the "packed feature chunks" of P:283); chunks are staged to HBM on the side
+    stream, double-buffered, while the previous batch is being assembled.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _abi as A
+
+
+class HostBuffer:
+    """Pinned, device-mapped host memory (dgnn_host_alloc) viewed as a CPU uint8 tensor."""
+
+    def __init__(self, nbytes: int):
+        self.nbytes = int(nbytes)
+        p = ctypes.c_void_p()
+        A._check(A.load_library().dgnn_host_alloc(self.nbytes, ctypes.byref(p)), "dgnn_host_alloc")
+        self.ptr = int(p.value or 0)
+        import weakref
+        self._fin = weakref.finalize(self, A.load_library().dgnn_host_free, ctypes.c_void_p(self.ptr))
+        buf = (ctypes.c_uint8 * max(self.nbytes, 1)).from_address(self.ptr)
+        self.tensor = torch.frombuffer(buf, dtype=torch.uint8, count=self.nbytes) if self.nbytes else \
+            torch.empty(0, dtype=torch.uint8)
+
+    def free(self):
+        self._fin()
+
+
+class Workspace:
+    """Grow-only buffers reused across offline passes (pinning tens of GB per pass would
+    dominate the step otherwise)."""
+
+    def __init__(self):
+        self._host = {}
+        self._dev = {}
+
+    def host(self, name: str, nbytes: int) -> "HostBuffer":
+        b = self._host.get(name)
+        if b is None or b.nbytes < nbytes:
+            if b is not None:
+                b.free()
+            b = HostBuffer(int(nbytes * 1.05) + 4096 if b is not None else nbytes)
+            self._host[name] = b
+        return b
+
+    def dev(self, name: str, nbytes: int, device) -> torch.Tensor:
+        t = self._dev.get(name)
+        if t is None or t.numel() < nbytes:
+            t = torch.empty(max(int(nbytes), 16), dtype=torch.uint8, device=device)
+            self._dev[name] = t
+        return t
+
+
+def _dist():
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        return dist
+    return None
+
+
+def batch_range(num_batches: int, rank: int, world: int):
+    """Contiguous batch block of one rank (batches shard with no exchange)."""
+    lo = num_batches * rank // world
+    hi = num_batches * (rank + 1) // world
+    return lo, hi
+
+
+@dataclass
+class Group:
+    b_lo: int
+    b_hi: int
+    rows: np.ndarray          # packed rows per batch
+    chunk_off: np.ndarray     # group-relative chunk offsets (bytes), nb+1
+    arena_off: int            # where the group's chunks start in the disk arena
+    group_bytes: int
+
+
+@dataclass
+class Layout:
+    ctx: A.Ctx
+    samples: A.Samples
+    plan: A.CachePlan
+    counts: torch.Tensor
+    row_bytes: int
+    dim: int
+    dtype: torch.dtype
+    addr: torch.Tensor              # uint32 (as int32) address table of every node of every batch
+    gpu_tier: torch.Tensor          # [K_g, row_bytes] uint8, HBM
+    host_tier: HostBuffer           # [K_h * row_bytes] pinned
+    arena: HostBuffer | None        # disk tier (pinned), or None when kept in HBM
+    arena_dev: torch.Tensor | None  # disk tier kept in HBM (stage="hbm")
+    groups: list = field(default_factory=list)
+    batch_chunk: np.ndarray = None  # [nb, 2]: (arena byte offset, packed rows)
+    stats: dict = field(default_factory=dict)
+
+    @property
+    def num_batches(self) -> int:
+        return self.samples.num_batches
+
+    # ------------------------------------------------------------ a9
+    def assemble(self, b: int, out: torch.Tensor, chunk_dev: torch.Tensor | None = None) -> torch.Tensor:
+        """Assemble batch b into ``out`` ([n_b, dim]) reading the chunk from ``chunk_dev`` if given
+        (already staged to HBM), else directly from the arena (UVA over PCIe)."""
+        n0, n1 = int(self.samples.node_off_host[b]), int(self.samples.node_off_host[b + 1])
+        off, rows = int(self.batch_chunk[b, 0]), int(self.batch_chunk[b, 1])
+        if chunk_dev is not None:
+            chunk = chunk_dev
+        elif self.arena_dev is not None:
+            chunk = self.arena_dev.data_ptr() + off
+        else:
+            chunk = self.arena.ptr + off
+        A.dgnn_assemble(self.ctx, self.addr[n0:n1], self.gpu_tier, self.plan.k_gpu, self.host_tier.ptr,
+                        self.plan.k_host, chunk, rows, self.row_bytes, out)
+        return out
+
+    def assemble_epoch(self, batches=None, out_ring=None):
+        """Pipelined assembly: the chunk of batch b+1 is staged H2D on the side
+        stream while batch b is assembled on the ctx stream.  Yields (b, features)."""
+        ctx = self.ctx
+        bs = list(range(self.num_batches)) if batches is None else list(batches)
+        if not bs:
+            return
+        max_n = int(np.max(np.diff(self.samples.node_off_host))) if self.num_batches else 0
+        max_c = int(np.max(self.batch_chunk[:, 1])) * self.row_bytes if self.num_batches else 0
+        dev = ctx.device
+        if out_ring is None:
+            out_ring = [torch.empty((max_n, self.dim), dtype=self.dtype, device=dev) for _ in range(2)]
+        staged = self.arena is not None
+        chunk_ring = [torch.empty(max(max_c, 16), dtype=torch.uint8, device=dev) for _ in range(2)] if staged else None
+        tickets = {}
+
+        def stage(i):
+            b = bs[i]
+            off, rows = int(self.batch_chunk[b, 0]), int(self.batch_chunk[b, 1])
+            tickets[i] = A.dgnn_stage_copy(ctx, chunk_ring[i % 2], self.arena.ptr + off, rows * self.row_bytes, 1)
+
+        if staged:
+            stage(0)
+        for i, b in enumerate(bs):
+            if staged:
+                if i + 1 < len(bs):
+                    stage(i + 1)
+                A.dgnn_stage_wait(ctx, tickets.pop(i))
+            n = int(self.samples.node_off_host[b + 1] - self.samples.node_off_host[b])
+            out = out_ring[i % 2][:n]
+            self.assemble(b, out, chunk_ring[i % 2] if staged else None)
+            yield b, out
+
+
+def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, features: torch.Tensor,
+                   seeds: torch.Tensor, fanout, batch_size: int, gpu_rows: int, host_rows: int, rng_seed: int,
+                   group_size: int = 64, batch_id_base: int = 0, stage: str = "pinned",
+                   counts: torch.Tensor | None = None, ws: Workspace | None = None) -> Layout:
+    """Run a1-a8 on this rank's batches.
+
+    ``seeds`` are this rank's seeds (batch t of them gets bid = batch_id_base + t).
+    With torch.distributed initialized (world > 1) the counts are all-reduced so that
+    every rank derives the identical cache plan from all ranks' batches.
+    ``stage``: "pinned" (disk tier in a pinned host arena, the default) or "hbm".
+    """
+    dev = ctx.device
+    N = indptr.numel() - 1
+    row_bytes = features.element_size() * (features.numel() // max(features.shape[0], 1))
+    dim = features.numel() // max(features.shape[0], 1)
+    stats = {}
+    if counts is None:
+        counts = torch.zeros(N, dtype=torch.int32, device=dev)
+    # a1-a3 (+ the fused access counter)
+    samples = A.dgnn_sample(ctx, indptr, indices, seeds, batch_size, fanout, rng_seed, batch_id_base, counts)
+    # a4: global histogram across ranks
+    d = _dist()
+    if d is not None:
+        with torch.cuda.stream(ctx.stream):
+            d.all_reduce(counts, op=d.ReduceOp.SUM)
+    # a5
+    plan = A.dgnn_build_cache(ctx, counts, gpu_rows, host_rows)
+    # tier buffers as special mini-batches
+    gpu_tier = torch.empty((plan.k_gpu, row_bytes), dtype=torch.uint8, device=dev)
+    A.dgnn_gather_rows(ctx, features, plan.gpu_ids, gpu_tier)
+    host_tier = ws.host("host_tier", plan.k_host * row_bytes) if ws is not None else \
+        HostBuffer(plan.k_host * row_bytes)
+    A.dgnn_gather_rows(ctx, features, plan.host_ids, host_tier.ptr)
+    # a6 for every batch of this rank at once
+    nb = samples.num_batches
+    total_nodes = samples.total_nodes
+    addr = torch.empty(max(total_nodes, 1), dtype=torch.int32, device=dev)
+    packed_ids = torch.empty(max(total_nodes, 1), dtype=torch.int32, device=dev)
+    packed_off = torch.empty(nb + 1, dtype=torch.int64, device=dev)
+    po = A.dgnn_classify(ctx, plan, samples, 0, nb, addr, packed_ids, packed_off) if nb else np.zeros(1, np.int64)
+    rows = np.diff(po)
+    # a7 layout: groups of `group_size` batches, each a contiguous run of 4 KiB-aligned chunks
+    groups = []
+    batch_chunk = np.zeros((nb, 2), np.int64)
+    arena_off = 0
+    for g0 in range(0, nb, group_size):
+        g1 = min(nb, g0 + group_size)
+        rel = po[g0:g1 + 1] - po[g0]
+        co = A.dgnn_chunk_layout(rel, row_bytes)
+        groups.append(Group(g0, g1, rows[g0:g1], co, arena_off, int(co[-1])))
+        batch_chunk[g0:g1, 0] = arena_off + co[:-1]
+        batch_chunk[g0:g1, 1] = rows[g0:g1]
+        arena_off += int(co[-1])
+    arena = arena_dev = None
+    if stage == "pinned":
+        arena = ws.host("arena", arena_off) if ws is not None else HostBuffer(arena_off)
+    elif stage == "hbm":
+        arena_dev = torch.empty(max(arena_off, 16), dtype=torch.uint8, device=dev)
+    else:
+        raise ValueError(stage)
+    # a7 pack + a8 stage-out, double-buffered group buffers
+    max_gb = max([g.group_bytes for g in groups], default=0)
+    bufs = [torch.empty(max(max_gb, 16), dtype=torch.uint8, device=dev) for _ in range(2)] if arena is not None else []
+    tickets = [None, None]
+    for gi, g in enumerate(groups):
+        rel = torch.from_numpy(np.concatenate([po[g.b_lo:g.b_hi + 1] - po[g.b_lo], g.chunk_off])).to(dev,
+                                                                                                     non_blocking=False)
+        rel_po, rel_co = rel[:g.b_hi - g.b_lo + 1], rel[g.b_hi - g.b_lo + 1:]
+        ids = packed_ids[int(po[g.b_lo]):int(po[g.b_hi])]
+        total = int(po[g.b_hi] - po[g.b_lo])
+        if arena is not None:
+            slot = gi % 2
+            if tickets[slot] is not None:
+                A.dgnn_stage_wait(ctx, tickets[slot])
+            dst = bufs[slot]
+            A.dgnn_pack(ctx, features, ids, rel_po, rel_co, total, g.group_bytes, dst)
+            tickets[slot] = A.dgnn_stage_copy(ctx, arena.ptr + g.arena_off, dst, g.group_bytes, 0)
+        else:
+            dst = arena_dev[g.arena_off:g.arena_off + max(g.group_bytes, 0)]
+            A.dgnn_pack(ctx, features, ids, rel_po, rel_co, total, g.group_bytes, dst)
+    for t in tickets:
+        if t is not None:
+            A.dgnn_stage_wait(ctx, t)
+    stats.update(packed_rows=int(po[-1]), packed_bytes=int(po[-1]) * row_bytes, arena_bytes=arena_off,
+                 k_gpu=plan.k_gpu, k_host=plan.k_host, total_nodes=total_nodes, total_edges=samples.total_edges)
+    del packed_ids
+    return Layout(ctx, samples, plan, counts, row_bytes, dim, features.dtype, addr, gpu_tier, host_tier, arena,
+                  arena_dev, groups, batch_chunk, stats)

@@ -1,0 +1,253 @@
+"""GPU-vs-oracle parity through the C ABI (run on a B200 with -m gpu).
+
+Every output is compared byte for byte with the CPU oracle (oracle/) on the
+same seeded inputs: integer / index / byte-copy work, so the bar is bit-exact.
+Cases span several sampling groups, ragged last batches, fanout 0, fanout >
+32, degree <= fanout, empty packed chunks, 400-byte and 12-byte rows, and the
+degenerate inputs of the method.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from conftest import csr_from_adj, golden_lines, random_csr
+from workload import feature_rows_np, make_workload
+
+pytestmark = pytest.mark.gpu
+
+RNG_SEED = 0x5EEDD15C
+
+
+@pytest.fixture(scope="module")
+def dg():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_2405_05231_b200 as dg
+    return dg
+
+
+@pytest.fixture(scope="module")
+def ctx(dg):
+    return dg.Ctx(device=0)
+
+
+def _gpu_sample(dg, ctx, indptr, indices, seeds, B, fan, seed, base=0, group=0):
+    dev = torch.device("cuda", 0)
+    ip = torch.as_tensor(np.asarray(indptr, np.int64)).to(dev)
+    ix = torch.as_tensor(np.asarray(indices, np.int32)).to(dev)
+    sd = torch.as_tensor(np.asarray(seeds, np.int32)).to(dev)
+    counts = torch.zeros(len(indptr) - 1, dtype=torch.int32, device=dev)
+    ctx.set_sample_group(group)
+    S = dg.dgnn_sample(ctx, ip, ix, sd, B, fan, seed, base, counts)
+    ctx.set_sample_group(0)
+    return S, counts
+
+
+def _compare_samples(S, ref):
+    assert S.num_batches == len(ref)
+    nodes = S.nodes.cpu().numpy()
+    eptr = S.eptr.cpu().numpy()
+    src = S.src_local.cpu().numpy()
+    for b, r in enumerate(ref):
+        n0, n1 = S.node_off_host[b], S.node_off_host[b + 1]
+        assert np.array_equal(nodes[n0:n1], r.nodes), f"batch {b}: nodes differ"
+        assert np.array_equal(S.hop_off_host[b], r.hop_off), f"batch {b}: hop_off differ"
+        p0, p1 = S.eptr_off_host[b], S.eptr_off_host[b + 1]
+        assert np.array_equal(eptr[p0:p1], r.eptr), f"batch {b}: eptr differ"
+        e0, e1 = S.edge_off_host[b], S.edge_off_host[b + 1]
+        assert np.array_equal(src[e0:e1], r.src_local), f"batch {b}: src_local differ"
+
+
+@pytest.fixture(scope="module")
+def tiny():
+    return make_workload("tiny")
+
+
+def test_sample_parity_tiny(dg, ctx, tiny):
+    ip, ix, sd = tiny.indptr.numpy(), tiny.indices.numpy(), tiny.seeds.numpy()
+    ref = oracle.sample(ip, ix, sd, 256, [10, 5], RNG_SEED)
+    for group in (0, 3, 1):
+        S, counts = _gpu_sample(dg, ctx, ip, ix, sd, 256, [10, 5], RNG_SEED, group=group)
+        _compare_samples(S, ref)
+        assert np.array_equal(counts.cpu().numpy().view(np.uint32), oracle.count_frequencies(ref, 10_000))
+
+
+@pytest.mark.parametrize("trial", range(12))
+def test_sample_parity_random(dg, ctx, trial):
+    rng = np.random.default_rng(1000 + trial)
+    n = int(rng.integers(30, 4000))
+    indptr, indices = random_csr(rng, n, max_deg=int(rng.integers(1, 80)))
+    H = int(rng.integers(1, 4))
+    fan = [int(x) for x in rng.choice([0, 1, 2, 3, 5, 10, 15, 31, 32, 33, 40], size=H)]
+    ns = int(rng.integers(1, n))
+    seeds = rng.permutation(n)[:ns].astype(np.int32)
+    B = int(rng.integers(1, 300))
+    base = int(rng.integers(0, 1 << 40))
+    seed = int(rng.integers(0, 1 << 63))
+    ref = oracle.sample(indptr, indices, seeds, B, fan, seed, batch_id_base=base)
+    S, counts = _gpu_sample(dg, ctx, indptr, indices, seeds, B, fan, seed, base=base,
+                            group=int(rng.choice([0, 1, 2, 5])))
+    _compare_samples(S, ref)
+    assert np.array_equal(counts.cpu().numpy().view(np.uint32), oracle.count_frequencies(ref, n))
+
+
+def test_fig1_and_degenerate_cases(dg, ctx):
+    g = {}
+    for line in golden_lines("fig1_sampling.txt"):
+        k, *rest = line.split()
+        g[k] = rest
+    adj = {int(t.split(":")[0]): [int(x) for x in t.split(":")[1].split(",")] for t in g["edges"]}
+    ip, ix = csr_from_adj(12, adj)
+    S, _ = _gpu_sample(dg, ctx, ip, ix, [0], 1, [2, 2], 7)
+    assert S.nodes.cpu().tolist() == [int(x) for x in g["nodes"]]
+    # star graph and fanout [0]
+    ip, ix = csr_from_adj(6, {0: [1, 2, 3, 4, 5]})
+    S, _ = _gpu_sample(dg, ctx, ip, ix, [0], 1, [5], 3)
+    assert S.nodes.cpu().tolist() == [0, 1, 2, 3, 4, 5]
+    S, _ = _gpu_sample(dg, ctx, ip, ix, [0, 3], 2, [0], 3)
+    assert S.nodes.cpu().tolist() == [0, 3] and S.total_edges == 0
+    # empty seeds
+    S, _ = _gpu_sample(dg, ctx, ip, ix, np.zeros(0, np.int32), 4, [2], 3)
+    assert S.num_batches == 0
+
+
+def test_sample_errors(dg, ctx):
+    ip, ix = csr_from_adj(4, {0: [1], 1: [2]})
+    with pytest.raises(dg.DgnnError) as e:
+        _gpu_sample(dg, ctx, ip, ix, [1, 1], 2, [1], 0)
+    assert e.value.status == 1
+    with pytest.raises(dg.DgnnError) as e:
+        _gpu_sample(dg, ctx, ip, ix, [9], 1, [1], 0)
+    assert e.value.status == 1
+    with pytest.raises(dg.DgnnError):
+        _gpu_sample(dg, ctx, ip, ix, [1], 1, [70000], 0)
+    # across batches a repeated seed is fine (c12)
+    S, _ = _gpu_sample(dg, ctx, ip, ix, [1, 1], 1, [1], 0)
+    assert S.num_batches == 2
+
+
+def _plan_np(plan):
+    return (plan.tier_map.cpu().numpy().view(np.uint32), plan.gpu_ids.cpu().numpy(), plan.host_ids.cpu().numpy())
+
+
+@pytest.mark.parametrize("trial", range(10))
+def test_build_cache_parity(dg, ctx, trial):
+    rng = np.random.default_rng(trial)
+    n = int(rng.integers(1, 300_000))
+    hi = int(rng.choice([1, 2, 3, 9, 100, 70000]))
+    counts = rng.integers(0, hi + 1, n).astype(np.uint32)
+    if trial == 0:
+        counts[:] = 0
+    kg, kh = int(rng.integers(0, n + 5)), int(rng.integers(0, n + 5))
+    if trial == 1:
+        kg, kh = 0, 0
+    ref = oracle.select_tiers(counts, kg, kh)
+    plan = dg.dgnn_build_cache(ctx, torch.from_numpy(counts.view(np.int32)).cuda(), kg, kh)
+    got = _plan_np(plan)
+    for a, b in zip(got, ref):
+        assert np.array_equal(a, b)
+
+
+def test_fig3_address_table(dg, ctx):
+    g = {}
+    for line in golden_lines("fig3_assembly.txt"):
+        k, *rest = line.split()
+        g[k] = rest
+    counts = np.zeros(12, np.uint32)
+    for tok in g["counts"]:
+        v, c = tok.split(":")
+        counts[int(v)] = int(c)
+    plan = dg.dgnn_build_cache(ctx, torch.from_numpy(counts.view(np.int32)).cuda(), 2, 2)
+    assert plan.gpu_ids.cpu().tolist() == [4, 7] and plan.host_ids.cpu().tolist() == [1, 9]
+
+
+def _layout_parity(dg, ctx, w, fan, B, gpu_rows, host_rows, group, stage):
+    ip, ix, sd = w.indptr.numpy(), w.indices.numpy(), w.seeds.numpy()
+    feats = w.features.numpy()
+    ref = oracle.offline_layout(ip, ix, feats, sd, B, fan, RNG_SEED, gpu_rows, host_rows, group, threads=8)
+    dev = torch.device("cuda", 0)
+    L = dg.offline_layout(ctx, w.indptr.to(dev), w.indices.to(dev), w.features.to(dev), w.seeds.to(dev), fan, B,
+                          gpu_rows, host_rows, RNG_SEED, group_size=group, stage=stage)
+    ctx.sync()
+    rb = w.row_bytes
+    # a4-a5
+    assert np.array_equal(L.counts.cpu().numpy().view(np.uint32), ref["counts"])
+    tm, gi, hi = _plan_np(L.plan)
+    assert np.array_equal(tm, ref["tier_map"]) and np.array_equal(gi, ref["gpu_ids"]) and np.array_equal(hi, ref["host_ids"])
+    # tier buffers
+    assert np.array_equal(L.gpu_tier.cpu().numpy().reshape(-1), ref["gpu_buf"].reshape(-1))
+    assert np.array_equal(L.host_tier.tensor.numpy(), ref["host_buf"].reshape(-1))
+    # a6
+    addr = L.addr.cpu().numpy().view(np.uint32)
+    for b, s in enumerate(ref["samples"]):
+        n0, n1 = L.samples.node_off_host[b], L.samples.node_off_host[b + 1]
+        assert np.array_equal(addr[n0:n1], ref["addr"][b])
+        assert L.batch_chunk[b, 1] == len(ref["packed"][b])
+    # a7-a8: every packed group byte-identical (chunks + zero padding)
+    arena = L.arena.tensor.numpy() if L.arena is not None else L.arena_dev.cpu().numpy()
+    for g, (buf, off) in zip(L.groups, ref["groups"]):
+        assert np.array_equal(g.chunk_off, off)
+        assert np.array_equal(arena[g.arena_off:g.arena_off + g.group_bytes], buf)
+    # a9: assembled == direct gather
+    seen = 0
+    for b, out in L.assemble_epoch():
+        exp = oracle.assemble(feats, ref["samples"][b].nodes)
+        got = out.view(torch.uint8).reshape(out.shape[0], -1).cpu().numpy()
+        assert np.array_equal(got, exp), f"assemble batch {b}"
+        seen += 1
+    assert seen == len(ref["samples"])
+    ctx.sync()
+    return L
+
+
+def test_offline_layout_parity_tiny(dg, ctx, tiny):
+    _layout_parity(dg, ctx, tiny, [10, 5], 256, 500, 1000, 8, "pinned")
+
+
+def test_offline_layout_parity_hbm_stage_and_odd_rows(dg, ctx):
+    # 400-byte rows (dim 100: 4096 % 400 != 0) and 12-byte rows (scalar path)
+    w = make_workload("tiny", num_nodes=3000, num_edges=20000, dim=100, num_seeds=1500, batch_size=97)
+    _layout_parity(dg, ctx, w, [6, 4], 97, 120, 200, 5, "hbm")
+    w = make_workload("tiny", num_nodes=2000, num_edges=9000, dim=3, num_seeds=700, batch_size=64)
+    _layout_parity(dg, ctx, w, [3, 3, 2], 64, 0, 50, 4, "pinned")
+
+
+def test_spec_acceptance_fixture(dg, ctx):
+    """1000 nodes, dim 128, 100 batches, fanout [5,5], tiers 5% / 10%."""
+    w = make_workload("tiny", num_nodes=1000, num_edges=10_000, num_seeds=800, batch_size=8, fanout=(5, 5))
+    _layout_parity(dg, ctx, w, [5, 5], 8, 50, 100, 16, "pinned")
+
+
+def test_assemble_range_error(dg, ctx):
+    dev = torch.device("cuda", 0)
+    addr = torch.from_numpy(np.array([(2 << 30) | 5], np.uint32).view(np.int32)).to(dev)
+    out = torch.empty((1, 4), dtype=torch.float32, device=dev)
+    chunk = torch.zeros(64, dtype=torch.uint8, device=dev)
+    dg.dgnn_assemble(ctx, addr, None, 0, None, 0, chunk, 1, 16, out)
+    with pytest.raises(dg.DgnnError) as e:
+        ctx.sync()
+    assert e.value.status == 2
+
+
+def test_gather_rows_matches_closed_form(dg, ctx):
+    dev = torch.device("cuda", 0)
+    from workload import feature_rows
+    feats = feature_rows(torch.arange(5000, device=dev), 256, 4)
+    ids = torch.randint(0, 5000, (3333,), device=dev, dtype=torch.int32)
+    out = torch.empty((3333, 256), dtype=torch.float32, device=dev)
+    dg.dgnn_gather_rows(ctx, feats, ids, out)
+    exp = feature_rows_np(ids.cpu().numpy(), 256, 4)
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), exp.view(np.uint32))
+
+
+def test_launch_counter_and_timing(dg, ctx, tiny):
+    dev = torch.device("cuda", 0)
+    ctx.reset_stats()
+    ctx.set_timing(True)
+    l0 = ctx.launches()
+    dg.dgnn_sample(ctx, tiny.indptr.to(dev), tiny.indices.to(dev), tiny.seeds.to(dev), 256, [10, 5], 1)
+    st = ctx.kernel_stats()
+    ctx.set_timing(False)
+    assert ctx.launches() > l0
+    assert st["sample_hop"]["launches"] >= 2 and st["sample_hop"]["ms"] > 0
