@@ -1,0 +1,390 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 DiskGNN offline hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config papers] [--impl ours|reference]
+
+A step is one pass of the whole hot path over one
+epoch of synthetic input on every rank: sample all of the rank's mini-batches
+(with the fused access counter), all-reduce the counts (N > 1), build the
+cache plan, fill the GPU / host tiers, classify + pack every packing group and
+stage the chunks to the pinned-host disk tier, then assemble every batch
+(chunks staged back to HBM on the side stream).  Rank r processes epoch r of
+the seed list (batch ids r*nb .. (r+1)*nb-1, reading c9), so per-GPU work is
+fixed as N grows ("scaling": "weak") and the only collective is the count
+all-reduce.
+
+value  = mini-batches processed by all ranks / (max over ranks of the device
+         time of the K timed steps), inputs resident in HBM.
+e2e    = the same metric through the public API with the inputs (CSR, features,
+         seeds) in pinned host memory, copied H2D inside the timed region every
+         step, and the counts read back D2H.
+roofline: pack_gather (the HBM-bound gather the north star grades) -- bytes per
+         launch = packed rows x (2 x row_bytes + 4).
+cpu_baseline: the oracle (oracle/) on a bounded sample on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "packed feature GB/s and mini-batches/s at 1/2/4/8 B200 (frac. of HBM peak)"
+WORKLOAD_NAMES = {"tiny": "tiny synthetic CSR (configs[0])", "products": "ogbn-products-shaped (configs[1])",
+                  "papers": "ogbn-papers100M-shaped (configs[2])", "friendster": "Friendster-shaped (configs[3])",
+                  "igb": "IGB-large-shaped (configs[4])"}
+RNG_SEED = 0x5EEDD15C
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index: int):
+        self.f = tempfile.NamedTemporaryFile(prefix="clocks_", suffix=".csv", delete=False)
+        q = ("clocks.sm,clocks.max.sm,power.draw,utilization.gpu,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.close()
+        rows = []
+        for line in open(self.f.name):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 8:
+                rows.append(parts)
+        os.unlink(self.f.name)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        load = [r for r in rows if r[3] not in ("0", "[N/A]")] or rows
+        sm = [float(r[0]) for r in load if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        reasons = sorted({names[i] for r in load for i in range(4) if r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows), "samples_under_load": len(load)}
+
+
+def setup_dist(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(local)
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, ws: int) -> float:
+    if ws == 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x: float, ws: int) -> float:
+    if ws == 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def make_inputs(cfg_name: str, dev):
+    from workload import CONFIGS, make_graph, make_seeds, make_features, config_rows
+    cfg = dict(CONFIGS[cfg_name])
+    t = time.time()
+    indptr, indices = make_graph(cfg["num_nodes"], cfg["num_edges"], cfg["degree"], cfg["skew"], 0, dev)
+    seeds = make_seeds(cfg["num_nodes"], cfg["num_seeds"], 0, dev)
+    torch.cuda.synchronize()
+    log(f"[bench] graph {cfg_name}: N={indptr.numel() - 1} E={indices.numel()} in {time.time() - t:.1f}s")
+    t = time.time()
+    feats = make_features(cfg["num_nodes"], cfg["dim"], dev, fseed=1)
+    torch.cuda.synchronize()
+    log(f"[bench] features {tuple(feats.shape)} in {time.time() - t:.1f}s")
+    gpu_rows, host_rows = config_rows(cfg)
+    return cfg, indptr, indices, seeds, feats, gpu_rows, host_rows
+
+
+def run_step(dg, ctx, ws_buf, inp, rank, counts):
+    cfg, indptr, indices, seeds, feats, gpu_rows, host_rows = inp
+    nb = (seeds.numel() + cfg["batch_size"] - 1) // cfg["batch_size"]
+    counts.zero_()
+    L = dg.offline_layout(ctx, indptr, indices, feats, seeds, cfg["fanout"], cfg["batch_size"], gpu_rows, host_rows,
+                          RNG_SEED, group_size=cfg["group_size"], batch_id_base=rank * nb, counts=counts, ws=ws_buf)
+    for _b, _out in L.assemble_epoch(out_ring=ws_buf._rings):
+        pass
+    return L
+
+
+def cpu_baseline(cfg, inp_host, n_batches: int):
+    """The oracle as it stands, on a bounded sample: the first n_batches batches of rank 0's epoch."""
+    import oracle
+    indptr, indices, seeds, feats_u8 = inp_host
+    B = cfg["batch_size"]
+    threads = os.cpu_count() or 1
+    gpu_rows, host_rows = int(cfg["gpu_frac"] * cfg["num_nodes"]), int(cfg["host_frac"] * cfg["num_nodes"])
+    t0 = time.time()
+    S = oracle.sample(indptr, indices, seeds[: n_batches * B], B, list(cfg["fanout"]), RNG_SEED, threads=threads)
+    counts = oracle.count_frequencies(S, len(indptr) - 1)
+    tm, gpu_ids, host_ids = oracle.select_tiers(counts, gpu_rows, host_rows)
+    plists = []
+    for s in S:
+        plists.append(oracle.classify(s.nodes, tm)[1])
+    oracle.pack(feats_u8, plists)
+    oracle.gather_rows(feats_u8, gpu_ids)
+    oracle.gather_rows(feats_u8, host_ids)
+    for s in S:
+        oracle.assemble(feats_u8, s.nodes)
+    dt = time.time() - t0
+    return {"value": len(S) / dt, "unit": "mini-batches/s", "cores": threads, "kind": "oracle",
+            "sample": f"first {len(S)} batches of the {cfg['batch_size']}-seed epoch: sample (OpenMP over batches), "
+                      f"count, full-N tier select on their counts, classify, pack, tier gather, direct-gather "
+                      f"assembly; {dt:.1f}s"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=os.environ.get("DGNN_BENCH_CONFIG", "papers"))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--cpu-batches", type=int, default=32)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    ws, rank, local = setup_dist(args)
+    dev = torch.device("cuda", local)
+    if args.impl == "reference":
+        return reference_arm(args, ws, rank, dev)
+
+    import paper_2405_05231_b200 as dg
+    from paper_2405_05231_b200.layout import Workspace
+    inp = make_inputs(args.config, dev)
+    cfg, indptr, indices, seeds, feats, gpu_rows, host_rows = inp
+    N = indptr.numel() - 1
+    nb = (seeds.numel() + cfg["batch_size"] - 1) // cfg["batch_size"]
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    ctx = dg.Ctx(device=dev, stream=stream)
+    wsb = Workspace()
+    counts = torch.zeros(N, dtype=torch.int32, device=dev)
+    # output rings for assembly, sized once from a first pass
+    wsb._rings = None
+    t = time.time()
+    L = run_step(dg, ctx, wsb, inp, rank, counts)
+    max_n = int(np.max(np.diff(L.samples.node_off_host)))
+    wsb._rings = [torch.empty((int(max_n * 1.1) + 1024, cfg["dim"]), dtype=torch.float32, device=dev)
+                  for _ in range(2)]
+    stats0 = dict(L.stats)
+    del L
+    torch.cuda.synchronize()
+    log(f"[bench] first pass {time.time() - t:.1f}s stats={stats0}")
+    for _ in range(max(args.warmup - 1, 0)):
+        del_l = run_step(dg, ctx, wsb, inp, rank, counts)
+        del del_l
+    torch.cuda.synchronize()
+
+    # ---------------- timed region (device time, CUDA events on the ctx stream) ----------------
+    ctx.reset_stats()
+    ctx.set_timing(True)
+    clk = Clocks(local)
+    barrier(ws)
+    torch.cuda.synchronize()
+    l0 = ctx.launches()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        L = run_step(dg, ctx, wsb, inp, rank, counts)
+        del L
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(ws)
+    clocks = clk.stop()
+    launches = ctx.launches() - l0
+    ms = e0.elapsed_time(e1)
+    kst = ctx.kernel_stats()
+    ctx.set_timing(False)
+    ms_max = max_over_ranks(ms, ws)
+    total_batches = nb * ws * args.steps
+    value = total_batches / (ms_max / 1e3)
+
+    hbm_peak, peak_src = peaks()
+    pk = kst["pack_gather"]
+    pack_gbs = pk["bytes"] / (pk["ms"] / 1e3) / 1e9 if pk["ms"] > 0 else None
+    asm = kst["assemble"]
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "pack_gather_ncu.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    step_ms = ms / args.steps
+    kernels = {k: {"ms_per_step": round(v["ms"] / args.steps, 3), "launches_per_step": v["launches"] // args.steps,
+                   "share_of_step": round(v["ms"] / ms, 4) if ms else None,
+                   **({"gbs": round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 1)} if v["bytes"] and v["ms"] else {})}
+               for k, v in kst.items() if v["launches"]}
+    result = {
+        "metric": METRIC, "value": round(value, 2), "unit": "mini-batches/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 2), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic (seeded generator, workload/synth.py; closed-form fp32 features copied bytewise)",
+        "config": {"workload": WORKLOAD_NAMES[args.config], "num_nodes": N, "num_edges": int(indices.numel()),
+                   "dim": cfg["dim"], "fanout": list(cfg["fanout"]), "batch_size": cfg["batch_size"],
+                   "num_seeds": int(seeds.numel()), "batches_per_rank": nb, "gpu_rows": gpu_rows,
+                   "host_rows": host_rows, "group_size": cfg["group_size"], "disk_tier": "pinned host arena",
+                   "parallelism": f"dp{ws} (batch-sharded, count all-reduce)",
+                   "l2": "inputs larger than L2 (features %.1f GB, CSR %.1f GB); no flush needed" % (
+                       feats.numel() * 4 / 1e9, (indptr.numel() * 8 + indices.numel() * 4) / 1e9)},
+        "packed_gbs": round(stats0["packed_bytes"] * ws * args.steps / (ms_max / 1e3) / 1e9, 2),
+        "pack_kernel_gbs": round(pack_gbs, 1) if pack_gbs else None,
+        "roofline": {"bound": "hbm", "achieved": round(pack_gbs, 1) if pack_gbs else None, "peak": hbm_peak,
+                     "unit": "GB/s", "frac": round(pack_gbs / hbm_peak, 4) if pack_gbs else None, "traffic": traffic,
+                     "kernel": "pack_gather", "peak_source": peak_src,
+                     "bytes_per_launch": round(pk["bytes"] / max(pk["launches"], 1)),
+                     "launch_ms": round(pk["ms"] / max(pk["launches"], 1), 4)},
+        "kernels": kernels,
+        "layout_stats": stats0,
+        "clocks": clocks,
+        "gpu_launches": int(launches),
+    }
+    if asm["ms"] > 0:
+        result["assemble_gbs"] = round(asm["bytes"] / (asm["ms"] / 1e3) / 1e9, 1)
+
+    # ---------------- e2e through the public API with host buffers ----------------
+    inp_host = None
+    if not args.no_e2e or (not args.no_cpu and rank == 0 and ws == 1):
+        pinned = []
+
+        def pin_like(t):  # exact-size pinned buffer (torch's pinned allocator rounds to powers of two)
+            hb = dg.HostBuffer(t.numel() * t.element_size())
+            pinned.append(hb)
+            h = hb.tensor.view(t.dtype).view(t.shape)
+            h.copy_(t)
+            return h
+
+        inp_host = tuple(pin_like(t) for t in (indptr, indices, seeds, feats))
+    if not args.no_e2e:
+        h_counts = dg.HostBuffer(N * 4).tensor.view(torch.int32)
+        h2d = sum(t.numel() * t.element_size() for t in inp_host)
+        d2h = N * 4
+        barrier(ws)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            for h, d_ in zip(inp_host, (indptr, indices, seeds, feats)):
+                d_.copy_(h, non_blocking=True)
+            L = run_step(dg, ctx, wsb, inp, rank, counts)
+            h_counts.copy_(counts, non_blocking=True)
+            del L
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier(ws)
+        ms_e2e = max_over_ranks(e0.elapsed_time(e1), ws)
+        result["e2e"] = {"value": round(nb * ws * args.e2e_steps / (ms_e2e / 1e3), 2), "unit": "mini-batches/s",
+                         "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                         "steps": args.e2e_steps,
+                         "note": "inputs (CSR, features, seeds) copied from pinned host every step; counts read "
+                                 "back; the disk tier is host-resident by design (a8)"}
+    # ---------------- CPU baseline: the oracle on a bounded sample ----------------
+    if not args.no_cpu and rank == 0 and ws == 1:
+        h_indptr, h_indices, h_seeds, h_feats = inp_host
+        try:
+            result["cpu_baseline"] = cpu_baseline(cfg, (h_indptr.numpy(), h_indices.numpy(), h_seeds.numpy(),
+                                                        h_feats.numpy().view(np.uint8).reshape(N, -1)),
+                                                  min(args.cpu_batches, nb))
+        except Exception as ex:  # the baseline is reported, never required
+            result["cpu_baseline"] = {"value": None, "error": str(ex)[:200]}
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def reference_arm(args, ws, rank, dev):
+    """--impl reference: the oracle (the only reference this paper has), timed on the host cores."""
+    if rank != 0:
+        return
+    import oracle
+    from workload import CONFIGS
+    inp = make_inputs(args.config, dev)
+    cfg, indptr, indices, seeds, feats, gpu_rows, host_rows = inp
+    h = (indptr.cpu().numpy(), indices.cpu().numpy(), seeds.cpu().numpy(),
+         feats.cpu().numpy().view(np.uint8).reshape(feats.shape[0], -1))
+    del feats
+    torch.cuda.empty_cache()
+    per_step = max(1, min(8, (seeds.numel() + cfg["batch_size"] - 1) // cfg["batch_size"]))
+    for _ in range(args.warmup):
+        cpu_baseline(cfg, h, per_step)
+    t0 = time.time()
+    last = None
+    for _ in range(args.steps):
+        last = cpu_baseline(cfg, h, per_step)
+    dt = time.time() - t0
+    value = per_step * args.steps / dt
+    nb = (seeds.numel() + cfg["batch_size"] - 1) // cfg["batch_size"]
+    out = {"impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "mini-batches/s", "n_gpus": ws,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 1),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+           "data": "synthetic (seeded generator, workload/synth.py)",
+           "config": {"workload": WORKLOAD_NAMES[args.config], "num_nodes": int(indptr.numel() - 1),
+                      "dim": cfg["dim"], "fanout": list(cfg["fanout"]), "batch_size": cfg["batch_size"],
+                      "batches_per_rank": nb, "parallelism": "host cores (oracle)"},
+           "cpu_baseline": {"value": round(value, 3), "unit": "mini-batches/s", "cores": last["cores"],
+                            "kind": "oracle", "sample": f"{per_step} batches per step; " + last["sample"]},
+           "e2e": {"value": round(value, 3), "unit": "mini-batches/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -4,8 +4,8 @@ This module generates INPUTS only (graphs, feature tables, seed lists); it
 holds none of the method's arithmetic.  See ``synth.py`` and DESIGN.md
 ("Input recipe").
 """
-from .synth import (CONFIGS, Workload, make_workload, make_graph, make_seeds, feature_rows,
+from .synth import (CONFIGS, Workload, make_workload, make_graph, make_seeds, make_features, feature_rows,
                     feature_rows_np, config_rows)
 
-__all__ = ["CONFIGS", "Workload", "make_workload", "make_graph", "make_seeds", "feature_rows",
+__all__ = ["CONFIGS", "Workload", "make_workload", "make_graph", "make_seeds", "make_features", "feature_rows",
            "feature_rows_np", "config_rows"]
