@@ -134,6 +134,27 @@ def sum_over_ranks(x: float, ws: int) -> float:
     return float(t.item())
 
 
+def pcie_bandwidth(dev, nbytes: int = 1 << 30) -> dict:
+    """Pinned host <-> device copy bandwidth (best of 5), the PCIe roofline denominator."""
+    import paper_2405_05231_b200 as dg
+    hb = dg.HostBuffer(nbytes)
+    d = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    out = {}
+    for name, (dst, src) in {"h2d_gbs": (d, hb.tensor), "d2h_gbs": (hb.tensor, d)}.items():
+        best = 0.0
+        for _ in range(5):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            dst.copy_(src, non_blocking=True)
+            b.record()
+            b.synchronize()
+            best = max(best, nbytes / (a.elapsed_time(b) / 1e3) / 1e9)
+        out[name] = best
+    del d
+    hb.free()
+    return out
+
+
 def make_inputs(cfg_name: str, dev):
     from workload import CONFIGS, make_graph, make_seeds, make_features, config_rows
     cfg = dict(CONFIGS[cfg_name])
@@ -150,15 +171,71 @@ def make_inputs(cfg_name: str, dev):
     return cfg, indptr, indices, seeds, feats, gpu_rows, host_rows
 
 
-def run_step(dg, ctx, ws_buf, inp, rank, counts):
-    cfg, indptr, indices, seeds, feats, gpu_rows, host_rows = inp
-    nb = (seeds.numel() + cfg["batch_size"] - 1) // cfg["batch_size"]
-    counts.zero_()
-    L = dg.offline_layout(ctx, indptr, indices, feats, seeds, cfg["fanout"], cfg["batch_size"], gpu_rows, host_rows,
-                          RNG_SEED, group_size=cfg["group_size"], batch_id_base=rank * nb, counts=counts, ws=ws_buf)
-    for _b, _out in L.assemble_epoch(out_ring=ws_buf._rings):
-        pass
-    return L
+class Runner:
+    """K offline passes of the whole path on this rank.
+
+    Pipelined (default): the layout of pass e+1 (a1-a8, ctx A on stream A) overlaps the
+    assembly of pass e (a9, ctx B on stream B) -- the paper's pipelining
+    applied across the offline / training boundary.  Host tier, disk-tier arena and
+    counts are double-buffered; stream A waits for the assembly of pass e-1 before pass
+    e+1 overwrites that buffer slot.  Sequential: layout then assembly on one stream.
+    """
+
+    def __init__(self, dg, inp, rank, dev, pipelined=True):
+        from paper_2405_05231_b200.layout import Workspace
+        self.dg, self.inp, self.rank, self.dev, self.pipelined = dg, inp, rank, dev, pipelined
+        self.sA = torch.cuda.Stream(dev)
+        self.sB = torch.cuda.Stream(dev) if pipelined else self.sA
+        torch.cuda.set_stream(self.sA)
+        self.ctxA = dg.Ctx(device=dev, stream=self.sA)
+        self.ctxB = dg.Ctx(device=dev, stream=self.sB) if pipelined else self.ctxA
+        if pipelined:
+            self.ctxB.set_assemble_occupancy(2)  # PCIe-bound: leave SMs to the concurrent layout
+        N = inp[1].numel() - 1
+        self.ws = [Workspace(), Workspace()]
+        self.counts = [torch.zeros(N, dtype=torch.int32, device=dev) for _ in range(2)]
+        cfg = inp[0]
+        self.nb = (inp[3].numel() + cfg["batch_size"] - 1) // cfg["batch_size"]
+        self.before_layout = None  # hook: e.g. the e2e H2D copies of the inputs
+
+    def ctxs(self):
+        return [self.ctxA] if self.ctxB is self.ctxA else [self.ctxA, self.ctxB]
+
+    def layout(self, slot):
+        cfg, indptr, indices, seeds, feats, gpu_rows, host_rows = self.inp
+        if self.before_layout is not None:
+            self.before_layout()
+        c = self.counts[slot]
+        c.zero_()
+        return self.dg.offline_layout(self.ctxA, indptr, indices, feats, seeds, cfg["fanout"], cfg["batch_size"],
+                                      gpu_rows, host_rows, RNG_SEED, group_size=cfg["group_size"],
+                                      batch_id_base=self.rank * self.nb, counts=c, ws=self.ws[slot])
+
+    def run(self, K: int, keep_last=False):
+        """Enqueue K passes; returns the last Layout if keep_last."""
+        L = self.layout(0)
+        ev_l = torch.cuda.Event()
+        ev_l.record(self.sA)
+        prev_ev = None
+        last = None
+        for e in range(K):
+            self.sB.wait_event(ev_l)
+            for _ in L.assemble_epoch(ctx=self.ctxB):
+                pass
+            ev_a = torch.cuda.Event()
+            ev_a.record(self.sB)
+            Ln = None
+            if e + 1 < K:
+                if prev_ev is not None:
+                    self.sA.wait_event(prev_ev)  # slot (e+1)%2 was pass e-1's: its assembly must be done
+                Ln = self.layout((e + 1) % 2)
+                ev_l = torch.cuda.Event()
+                ev_l.record(self.sA)
+            prev_ev = ev_a
+            last = L
+            L = Ln
+        self.sA.wait_event(prev_ev)
+        return last if keep_last else None
 
 
 def cpu_baseline(cfg, inp_host, n_batches: int):
@@ -198,6 +275,7 @@ def main():
     ap.add_argument("--cpu-batches", type=int, default=32)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--sequential", action="store_true", help="no epoch pipelining (one stream)")
     args = ap.parse_args()
     ws, rank, local = setup_dist(args)
     dev = torch.device("cuda", local)
@@ -205,53 +283,47 @@ def main():
         return reference_arm(args, ws, rank, dev)
 
     import paper_2405_05231_b200 as dg
-    from paper_2405_05231_b200.layout import Workspace
     inp = make_inputs(args.config, dev)
     cfg, indptr, indices, seeds, feats, gpu_rows, host_rows = inp
     N = indptr.numel() - 1
     nb = (seeds.numel() + cfg["batch_size"] - 1) // cfg["batch_size"]
-    stream = torch.cuda.Stream(dev)
-    torch.cuda.set_stream(stream)
-    ctx = dg.Ctx(device=dev, stream=stream)
-    wsb = Workspace()
-    counts = torch.zeros(N, dtype=torch.int32, device=dev)
-    # output rings for assembly, sized once from a first pass
-    wsb._rings = None
+    R = Runner(dg, inp, rank, dev, pipelined=not args.sequential)
     t = time.time()
-    L = run_step(dg, ctx, wsb, inp, rank, counts)
-    max_n = int(np.max(np.diff(L.samples.node_off_host)))
-    wsb._rings = [torch.empty((int(max_n * 1.1) + 1024, cfg["dim"]), dtype=torch.float32, device=dev)
-                  for _ in range(2)]
-    stats0 = dict(L.stats)
-    del L
+    L = R.run(1, keep_last=True)
     torch.cuda.synchronize()
+    stats0 = dict(L.stats)
+    stats0.update(L.tier_mix())
+    del L
     log(f"[bench] first pass {time.time() - t:.1f}s stats={stats0}")
-    for _ in range(max(args.warmup - 1, 0)):
-        del_l = run_step(dg, ctx, wsb, inp, rank, counts)
-        del del_l
+    if args.warmup > 1:
+        R.run(args.warmup - 1)
     torch.cuda.synchronize()
 
-    # ---------------- timed region (device time, CUDA events on the ctx stream) ----------------
-    ctx.reset_stats()
-    ctx.set_timing(True)
+    # ---------------- timed region (device time, CUDA events; max over ranks) ----------------
+    for c in R.ctxs():
+        c.reset_stats()
+        c.set_timing(True)
     clk = Clocks(local)
     barrier(ws)
     torch.cuda.synchronize()
-    l0 = ctx.launches()
+    l0 = sum(c.launches() for c in R.ctxs())
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        L = run_step(dg, ctx, wsb, inp, rank, counts)
-        del L
-    e1.record(stream)
+    e0.record(R.sA)
+    R.run(args.steps)
+    e1.record(R.sA)
     torch.cuda.synchronize()
     barrier(ws)
     clocks = clk.stop()
-    launches = ctx.launches() - l0
+    launches = sum(c.launches() for c in R.ctxs()) - l0
     ms = e0.elapsed_time(e1)
-    kst = ctx.kernel_stats()
-    ctx.set_timing(False)
+    kst = {}
+    for c in R.ctxs():
+        for k, v in c.kernel_stats().items():
+            d = kst.setdefault(k, {"launches": 0, "ms": 0.0, "bytes": 0.0})
+            for f in d:
+                d[f] += v[f]
+        c.set_timing(False)
     ms_max = max_over_ranks(ms, ws)
     total_batches = nb * ws * args.steps
     value = total_batches / (ms_max / 1e3)
@@ -267,7 +339,6 @@ def main():
             traffic = json.load(open(prof)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    step_ms = ms / args.steps
     kernels = {k: {"ms_per_step": round(v["ms"] / args.steps, 3), "launches_per_step": v["launches"] // args.steps,
                    "share_of_step": round(v["ms"] / ms, 4) if ms else None,
                    **({"gbs": round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 1)} if v["bytes"] and v["ms"] else {})}
@@ -282,6 +353,8 @@ def main():
                    "num_seeds": int(seeds.numel()), "batches_per_rank": nb, "gpu_rows": gpu_rows,
                    "host_rows": host_rows, "group_size": cfg["group_size"], "disk_tier": "pinned host arena",
                    "parallelism": f"dp{ws} (batch-sharded, count all-reduce)",
+                   "schedule": "sequential" if args.sequential else
+                   "pipelined: layout of pass e+1 overlaps assembly of pass e (2 streams)",
                    "l2": "inputs larger than L2 (features %.1f GB, CSR %.1f GB); no flush needed" % (
                        feats.numel() * 4 / 1e9, (indptr.numel() * 8 + indices.numel() * 4) / 1e9)},
         "packed_gbs": round(stats0["packed_bytes"] * ws * args.steps / (ms_max / 1e3) / 1e9, 2),
@@ -298,12 +371,21 @@ def main():
     }
     if asm["ms"] > 0:
         result["assemble_gbs"] = round(asm["bytes"] / (asm["ms"] / 1e3) / 1e9, 1)
+        # a9's own roofline: host-tier rows cross PCIe inside the kernel (UVA); measured H2D copy BW
+        pcie = pcie_bandwidth(dev)
+        host_b = stats0["host_rows"] * stats0.get("row_bytes", cfg["dim"] * 4)
+        asm_pcie = host_b * args.steps / (asm["ms"] / 1e3) / 1e9
+        result["assemble_roofline"] = {"bound": "pcie", "achieved": round(asm_pcie, 1),
+                                       "peak": round(pcie["h2d_gbs"], 1), "unit": "GB/s",
+                                       "frac": round(asm_pcie / pcie["h2d_gbs"], 4),
+                                       "note": "host-tier bytes read over PCIe by the assemble kernels / their "
+                                               "device time; peak = pinned H2D cudaMemcpy measured in this run",
+                                       "pcie": pcie}
 
     # ---------------- e2e through the public API with host buffers ----------------
     inp_host = None
+    pinned = []
     if not args.no_e2e or (not args.no_cpu and rank == 0 and ws == 1):
-        pinned = []
-
         def pin_like(t):  # exact-size pinned buffer (torch's pinned allocator rounds to powers of two)
             hb = dg.HostBuffer(t.numel() * t.element_size())
             pinned.append(hb)
@@ -313,20 +395,26 @@ def main():
 
         inp_host = tuple(pin_like(t) for t in (indptr, indices, seeds, feats))
     if not args.no_e2e:
-        h_counts = dg.HostBuffer(N * 4).tensor.view(torch.int32)
+        h_counts_buf = dg.HostBuffer(N * 4)  # keep the owner alive while the view is used
+        h_counts = h_counts_buf.tensor.view(torch.int32)
         h2d = sum(t.numel() * t.element_size() for t in inp_host)
         d2h = N * 4
-        barrier(ws)
-        torch.cuda.synchronize()
-        e0.record(stream)
-        for _ in range(args.e2e_steps):
+
+        def copy_in():
+            # every pass: inputs H2D from pinned host (stream A, before the pass's layout) ...
             for h, d_ in zip(inp_host, (indptr, indices, seeds, feats)):
                 d_.copy_(h, non_blocking=True)
-            L = run_step(dg, ctx, wsb, inp, rank, counts)
-            h_counts.copy_(counts, non_blocking=True)
-            del L
-        e1.record(stream)
+
+        R.before_layout = copy_in
+        barrier(ws)
         torch.cuda.synchronize()
+        e0.record(R.sA)
+        R.run(args.e2e_steps)
+        # ... and the access counts read back
+        h_counts.copy_(R.counts[(args.e2e_steps - 1) % 2], non_blocking=True)
+        e1.record(R.sA)
+        torch.cuda.synchronize()
+        R.before_layout = None
         barrier(ws)
         ms_e2e = max_over_ranks(e0.elapsed_time(e1), ws)
         result["e2e"] = {"value": round(nb * ws * args.e2e_steps / (ms_e2e / 1e3), 2), "unit": "mini-batches/s",

@@ -114,6 +114,10 @@ dgnn_status dgnn_ctx_sync(dgnn_ctx* ctx);
 const char* dgnn_last_error(void);
 /* Tuning knob: batches sampled concurrently per sampling group (0 = automatic). */
 dgnn_status dgnn_ctx_set_sample_group(dgnn_ctx* ctx, int32_t batches);
+/* Tuning knob: resident CTAs per SM for the assemble kernels (default 8).  The assemble
+ * kernel is PCIe-bound on host-tier rows; a low value leaves SMs to a concurrent offline
+ * pass on another stream (epoch pipelining). */
+dgnn_status dgnn_ctx_set_assemble_occupancy(dgnn_ctx* ctx, int32_t blocks_per_sm);
 
 /* Statistics: number of kernels this ctx has launched; optional per-launch CUDA-event
  * timing on the ctx stream (enable before the region of interest). */
@@ -265,6 +269,19 @@ dgnn_status dgnn_host_free(void* p);
 dgnn_status dgnn_assemble(dgnn_ctx* ctx, const uint32_t* addr, int64_t n, const void* gpu_tier, int64_t k_gpu,
                           const void* host_tier, int64_t k_host, const void* chunk, int64_t chunk_rows,
                           int64_t row_bytes, void* out);
+
+/* A run of consecutive batches in one launch (same per-row semantics as dgnn_assemble).
+ *   addr        device uint32 [n]: the address tables of the batches, concatenated.
+ *   node_off    device int64 [nb+1]: row offsets of the batches inside addr / out (node_off[0] = 0,
+ *               node_off[nb] = n).
+ *   chunk_base  UVA base of the batches' staged chunks; chunk_off device int64 [nb+1] byte
+ *               offsets of each chunk from chunk_base; chunk_rows device int64 [nb+1] exclusive
+ *               prefix of the packed rows (a DISK slot of batch b must be < its packed rows).
+ *   out         device [n * row_bytes]. */
+dgnn_status dgnn_assemble_group(dgnn_ctx* ctx, const uint32_t* addr, const int64_t* node_off, int64_t nb, int64_t n,
+                                const void* gpu_tier, int64_t k_gpu, const void* host_tier, int64_t k_host,
+                                const void* chunk_base, const int64_t* chunk_off, const int64_t* chunk_rows,
+                                int64_t row_bytes, void* out);
 
 #ifdef __cplusplus
 }

@@ -37,7 +37,7 @@ EXPORTS = [
     "dgnn_ctx_kernel_stats", "dgnn_ctx_reset_stats", "dgnn_kernel_name", "dgnn_sample", "dgnn_samples_get_info",
     "dgnn_samples_free", "dgnn_build_cache", "dgnn_cache_plan_get_info", "dgnn_cache_plan_free", "dgnn_classify",
     "dgnn_chunk_layout", "dgnn_pack", "dgnn_gather_rows", "dgnn_stage_copy", "dgnn_stage_wait", "dgnn_stage_sync",
-    "dgnn_host_alloc", "dgnn_host_free", "dgnn_assemble",
+    "dgnn_host_alloc", "dgnn_host_free", "dgnn_assemble", "dgnn_assemble_group", "dgnn_ctx_set_assemble_occupancy",
 ]
 
 
@@ -87,7 +87,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         if _lib is not None:
             return _lib
         if not os.path.exists(path):
-            raise ImportError(f"{path} is missing: build it with `python -m paper_2405_05231_b200.build` "
+            raise ImportError(f"{path} is missing: build it with `python paper_2405_05231_b200/build.py` "
                               "(there is no CPU fallback)")
         L = ctypes.CDLL(path)
         sig = {
@@ -120,6 +120,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "dgnn_host_alloc": (i32, [i64, ctypes.POINTER(P)]),
             "dgnn_host_free": (i32, [P]),
             "dgnn_assemble": (i32, [P, P, i64, P, i64, P, i64, P, i64, i64, P]),
+            "dgnn_assemble_group": (i32, [P, P, P, i64, i64, P, i64, P, i64, P, P, P, i64, P]),
+            "dgnn_ctx_set_assemble_occupancy": (i32, [P, i32]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -241,6 +243,10 @@ class Ctx:
 
     def sync(self):
         _check(load_library().dgnn_ctx_sync(self.handle), "dgnn_ctx_sync")
+
+    def set_assemble_occupancy(self, blocks_per_sm: int):
+        _check(load_library().dgnn_ctx_set_assemble_occupancy(self.handle, int(blocks_per_sm)),
+               "dgnn_ctx_set_assemble_occupancy")
 
     def set_sample_group(self, batches: int):
         _check(load_library().dgnn_ctx_set_sample_group(self.handle, int(batches)), "dgnn_ctx_set_sample_group")
@@ -398,3 +404,12 @@ def dgnn_assemble(ctx: Ctx, addr: torch.Tensor, gpu_tier, k_gpu: int, host_tier,
     _check(load_library().dgnn_assemble(ctx.handle, _ptr(addr), addr.numel(), _ptr(gpu_tier), int(k_gpu),
                                         _ptr(host_tier), int(k_host), _ptr(chunk), int(chunk_rows), int(row_bytes),
                                         _ptr(out)), "dgnn_assemble")
+
+
+def dgnn_assemble_group(ctx: Ctx, addr: torch.Tensor, node_off: torch.Tensor, n: int, gpu_tier, k_gpu: int,
+                        host_tier, k_host: int, chunk_base, chunk_off: torch.Tensor, chunk_rows: torch.Tensor,
+                        row_bytes: int, out):
+    _check(load_library().dgnn_assemble_group(ctx.handle, _ptr(addr), _ptr(node_off), node_off.numel() - 1, int(n),
+                                              _ptr(gpu_tier), int(k_gpu), _ptr(host_tier), int(k_host),
+                                              _ptr(chunk_base), _ptr(chunk_off), _ptr(chunk_rows), int(row_bytes),
+                                              _ptr(out)), "dgnn_assemble_group")

@@ -1,6 +1,6 @@
 """Build libdgnn.so (the C-ABI library) in-tree with nvcc for sm_100a.
 
-    python -m paper_2405_05231_b200.build [--force]
+    python paper_2405_05231_b200/build.py [--force]
 
 The library has no torch dependency: it links only the CUDA runtime.
 """

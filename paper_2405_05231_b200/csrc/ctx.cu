@@ -182,6 +182,12 @@ dgnn_status dgnn_ctx_set_sample_group(dgnn_ctx* c, int32_t batches) {
     return DGNN_OK;
 }
 
+dgnn_status dgnn_ctx_set_assemble_occupancy(dgnn_ctx* c, int32_t blocks_per_sm) {
+    DGNN_REQUIRE(c && blocks_per_sm >= 1 && blocks_per_sm <= 32, "dgnn_ctx_set_assemble_occupancy: bad argument");
+    c->assemble_blocks_per_sm = blocks_per_sm;
+    return DGNN_OK;
+}
+
 int64_t dgnn_ctx_launches(const dgnn_ctx* c) { return c ? c->launches : 0; }
 
 dgnn_status dgnn_ctx_set_timing(dgnn_ctx* c, int enable) {

@@ -26,6 +26,7 @@ struct dgnn_ctx {
     int* dev_err = nullptr;  // device word: OR of DEVERR_* bits
     int64_t launches = 0;
     int32_t sample_group = 0;
+    int assemble_blocks_per_sm = 8;  // grid cap for a9 (lower it to leave SMs to a concurrent pass)
     // per-launch CUDA-event timing
     bool timing = false;
     struct Pending {
@@ -266,25 +267,36 @@ __global__ void __launch_bounds__(kThreads) scan_kernel(const int64_t* n_dev, in
             warp_excl += (w < warp) ? t : 0;
             block_total += t;
         }
-        if (threadIdx.x == 0) {
+        if (warp == 0) {
+            // warp-parallel look-back: lane l inspects predecessor tile-1-l of the window
             int64_t prefix = 0;
             if (tile == 0) {
-                st_relaxed(&status[0], kFlagP | (unsigned long long)block_total);
+                if (lane == 0) st_relaxed(&status[0], kFlagP | (unsigned long long)block_total);
             } else {
-                st_relaxed(&status[tile], kFlagA | (unsigned long long)block_total);
+                if (lane == 0) st_relaxed(&status[tile], kFlagA | (unsigned long long)block_total);
                 int64_t t = tile - 1;
                 for (;;) {
-                    const unsigned long long s = ld_relaxed(&status[t]);
+                    const int64_t idx = t - lane;
+                    const unsigned long long s = idx >= 0 ? ld_relaxed(&status[idx]) : kFlagP;
                     const unsigned long long flag = s & ~kMask;
-                    if (flag == 0) continue;  // predecessor not published yet
-                    prefix += (int64_t)(s & kMask);
-                    if (flag == kFlagP) break;
-                    --t;
+                    const unsigned pmask = __ballot_sync(0xffffffffu, flag == kFlagP);
+                    const unsigned xmask = __ballot_sync(0xffffffffu, flag == 0);
+                    const int first_p = pmask ? __ffs(pmask) - 1 : 31;
+                    const unsigned need = (first_p == 31) ? 0xffffffffu : ((2u << first_p) - 1u);
+                    if (xmask & need) continue;  // a needed predecessor has not published yet
+                    int64_t v = (lane <= first_p) ? (int64_t)(s & kMask) : 0;
+#pragma unroll
+                    for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+                    prefix += v;
+                    if (pmask) break;
+                    t -= 32;
                 }
-                st_relaxed(&status[tile], kFlagP | (unsigned long long)(prefix + block_total));
+                if (lane == 0) st_relaxed(&status[tile], kFlagP | (unsigned long long)(prefix + block_total));
             }
-            s_prefix = prefix;
-            if (tile == ntiles - 1 && total) *total = prefix + block_total;
+            if (lane == 0) {
+                s_prefix = prefix;
+                if (tile == ntiles - 1 && total) *total = prefix + block_total;
+            }
         }
         __syncthreads();
         const int64_t pre = s_prefix + warp_excl;

@@ -51,6 +51,9 @@ struct Grp {
     int32_t* hop_bound;  // [G*(H+2)]
     int64_t* hop_fr_off; // [H*(kMaxGroup+1)]
     int64_t* hop_cbase;  // [H*(kMaxGroup+1)]
+    int32_t* fv;         // [frontier] node id
+    int64_t* fst;        // [frontier] indptr[v]
+    int32_t* fdg;        // [frontier] degree
 };
 
 __device__ __forceinline__ uint32_t slot_hash(int32_t key, int tlog) {
@@ -145,37 +148,39 @@ __global__ void k_hop_cands(Grp g, int h, int64_t* cptr) {
     }
 }
 
-__global__ void k_new_setup(Grp g) {
-    if (threadIdx.x != 0) return;
-    int64_t acc = 0;
-    for (int s = 0; s < g.G; ++s) {
-        g.new_off[s] = acc;
-        acc += g.new_cnt[s];
-    }
-    g.new_off[g.G] = acc;
+// new_off[s] = start of slot s's new nodes in the flattened bucket order
+__global__ void k_new_setup(Grp g, const int64_t* __restrict__ bstart, int64_t NB, const int64_t* __restrict__ total) {
+    for (int s = threadIdx.x; s <= g.G; s += blockDim.x) g.new_off[s] = s < g.G ? bstart[(int64_t)s * NB] : *total;
 }
 
 __global__ void k_hop_end(Grp g, int h) {
     for (int s = threadIdx.x; s < g.G; s += blockDim.x) {
-        const int32_t n0 = g.n[s], c = g.new_cnt[s];
+        const int32_t n0 = g.n[s], c = (int32_t)(g.new_off[s + 1] - g.new_off[s]);
         g.hop_bound[s * (g.H + 2) + h + 2] = n0 + c;
         g.fr_lo[s] = n0;
         g.fr_hi[s] = n0 + c;
         g.n[s] = n0 + c;
-        g.new_cnt[s] = 0;
     }
 }
 
-// ------------------------------------------------ a2: the sampling kernel
+// ------------------------------------------------ a2: the sampling kernels
+// Scan input: frontier node t -> min(k, deg); records (v, indptr[v], deg) so the
+// sampling kernel reads them coalesced instead of chasing pointers.
 struct DegIn {
     Grp g;
     const int64_t* indptr;
     int k;
+    int* err;
     __device__ __forceinline__ int64_t operator()(int64_t t) const {
         const int s = segment_of(g.fr_off, g.G + 1, t);
         const int64_t j = g.fr_lo[s] + (t - g.fr_off[s]);
         const int32_t v = g.nodes[(int64_t)s * g.cap_n + j];
-        const int64_t d = indptr[v + 1] - indptr[v];
+        const int64_t start = indptr[v];
+        const int64_t d = indptr[v + 1] - start;
+        g.fv[t] = v;
+        g.fst[t] = start;
+        if (d >= (int64_t)INT32_MAX) atomicOr(err, DEVERR_OVERFLOW);
+        g.fdg[t] = (int32_t)d;
         return d < k ? d : k;
     }
 };
@@ -185,27 +190,69 @@ struct StoreExcl {
     __device__ __forceinline__ void operator()(int64_t i, int64_t excl, int64_t) const { out[i] = excl; }
 };
 
-__device__ __forceinline__ void insert_append(int2* tab, int tlog, uint32_t mask, int32_t* new_cnt_s,
-                                              int32_t* newdst, int32_t u, bool act, uint32_t* counts, int* err,
-                                              int lane) {
-    const int r = act ? table_insert(tab, tlog, mask, u, -1) : 0;
-    if (r < 0) atomicOr(err, DEVERR_TABLE);
-    const bool nw = r > 0;
-    if (nw && counts) atomicAdd(&counts[u], 1u);
-    const unsigned m = __ballot_sync(kFull, nw);
-    if (m) {
-        const int leader = __ffs(m) - 1;
-        int pos0 = 0;
-        if (lane == leader) pos0 = atomicAdd(new_cnt_s, __popc(m));
-        pos0 = __shfl_sync(kFull, pos0, leader);
-        if (nw) newdst[pos0 + __popc(m & lanemask_lt())] = u;
+// W lanes per frontier node (W = next power of two >= k, k <= 32): lane s of a
+// sub-warp draws slot s (Philox keyed (seed, v, bid, h, s)), Floyd's resolution
+// runs in slot order with sub-warp ballots, the k positions are ranked (they are
+// distinct) and the neighbour IDs gathered into cand[cptr[t] + rank].
+template <int W>
+__global__ void __launch_bounds__(256) k_sample_hop(Grp g, const int32_t* __restrict__ indices, int k, uint64_t seed,
+                                                    int64_t bid0, int h, const int64_t* __restrict__ cptr,
+                                                    int32_t* __restrict__ cand) {
+    __shared__ int64_t s_fr[kMaxGroup + 1];
+    for (int i = threadIdx.x; i <= g.G; i += blockDim.x) s_fr[i] = g.fr_off[i];
+    __syncthreads();
+    constexpr int NPW = 32 / W;  // frontier nodes per warp
+    const int64_t F = s_fr[g.G];
+    const int lane = threadIdx.x & 31, sub = lane / W, sl = lane % W;
+    const unsigned gmask = (W == 32) ? kFull : (((1u << W) - 1u) << (sub * W));
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t t0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * NPW; t0 < F;
+         t0 += nwarps * NPW) {
+        const int64_t t = t0 + sub;
+        const bool live = t < F;
+        int32_t v = 0, d = 0;
+        int64_t start = 0, base = 0;
+        int s = 0;
+        if (live) {
+            v = g.fv[t];
+            start = g.fst[t];
+            d = g.fdg[t];
+            base = cptr[t];
+            s = segment_of(s_fr, g.G + 1, t);
+        }
+        const bool floyd = live && d > k;
+        if (live && !floyd) {
+            // reading c3: take every position, in CSR order
+            for (int p = sl; p < d; p += W) cand[base + p] = indices[start + p];
+        }
+        if (__ballot_sync(kFull, floyd)) {
+            // Floyd (readings c6, c7): draw t_s in [0, d-k+s]; slot s takes i_s if t_s was taken
+            const int64_t i = (int64_t)d - k + sl;
+            int64_t tdraw = 0;
+            if (floyd && sl < k)
+                tdraw = (int64_t)__umul64hi(draw64(seed, (uint32_t)v, (uint64_t)(bid0 + s), (uint32_t)h, (uint32_t)sl),
+                                            (uint64_t)(i + 1));
+            int64_t S = -1;
+            for (int r = 0; r < k; ++r) {
+                const int64_t tr = __shfl_sync(kFull, tdraw, r, W);
+                const unsigned hit = __ballot_sync(kFull, sl < r && S == tr) & gmask;
+                if (sl == r) S = hit ? i : tr;
+            }
+            int rank = 0;
+            for (int q = 0; q < k; ++q) {
+                const int64_t Sq = __shfl_sync(kFull, S, q, W);
+                rank += (Sq < S) ? 1 : 0;
+            }
+            if (floyd && sl < k) cand[base + rank] = indices[start + S];
+        }
     }
 }
 
-__global__ void __launch_bounds__(256) k_sample_hop(Grp g, const int64_t* __restrict__ indptr,
-                                                    const int32_t* __restrict__ indices, int k, uint64_t seed,
-                                                    int64_t bid0, int h, const int64_t* __restrict__ cptr,
-                                                    int32_t* __restrict__ cand, uint32_t* counts, int* err) {
+// k > 32: one lane per frontier node runs Floyd sequentially, using the node's
+// candidate slots as scratch for the positions, then the warp gathers.
+__global__ void __launch_bounds__(256) k_sample_hop_wide(Grp g, const int32_t* __restrict__ indices, int k,
+                                                         uint64_t seed, int64_t bid0, int h,
+                                                         const int64_t* __restrict__ cptr, int32_t* __restrict__ cand) {
     __shared__ int64_t s_fr[kMaxGroup + 1];
     for (int i = threadIdx.x; i <= g.G; i += blockDim.x) s_fr[i] = g.fr_off[i];
     __syncthreads();
@@ -214,126 +261,109 @@ __global__ void __launch_bounds__(256) k_sample_hop(Grp g, const int64_t* __rest
     const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
     for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < F; t += nwarps) {
         const int s = segment_of(s_fr, g.G + 1, t);
-        const int64_t j = g.fr_lo[s] + (t - s_fr[s]);
-        const int32_t v = g.nodes[(int64_t)s * g.cap_n + j];
-        const int64_t start = indptr[v];
-        const int64_t d = indptr[v + 1] - start;
+        const int32_t v = g.fv[t];
+        const int64_t start = g.fst[t];
+        const int32_t d = g.fdg[t];
         const int64_t base = cptr[t];
-        const uint64_t bid = (uint64_t)(bid0 + s);
-        int2* tab = g.table + ((int64_t)s << g.tlog);
-        int32_t* newdst = g.nodes + (int64_t)s * g.cap_n + g.n[s];
-        int32_t* ncnt = g.new_cnt + s;
         if (d <= k) {
-            // reading c3: take every position, in CSR order
-            for (int64_t p0 = 0; p0 < d; p0 += 32) {
-                const int64_t p = p0 + lane;
-                const bool act = p < d;
-                const int32_t u = act ? indices[start + p] : 0;
-                if (act) cand[base + p] = u;
-                insert_append(tab, g.tlog, g.tmask, ncnt, newdst, u, act, counts, err, lane);
-            }
-        } else if (k <= 32) {
-            // Floyd (readings c6, c7): lane s draws t_s in [0, d-k+s]; resolution in slot order
-            const int64_t i = d - k + lane;
-            int64_t tdraw = 0;
-            if (lane < k)
-                tdraw = (int64_t)__umul64hi(draw64(seed, (uint32_t)v, bid, (uint32_t)h, (uint32_t)lane),
-                                            (uint64_t)(i + 1));
-            int64_t S = -1;
-            for (int r = 0; r < k; ++r) {
-                const int64_t tr = __shfl_sync(kFull, tdraw, r);
-                const unsigned hit = __ballot_sync(kFull, lane < r && S == tr);
-                if (lane == r) S = hit ? i : tr;
-            }
-            int rank = 0;
-            for (int q = 0; q < k; ++q) {
-                const int64_t Sq = __shfl_sync(kFull, S, q);
-                rank += (Sq < S) ? 1 : 0;
-            }
-            const bool act = lane < k;
-            const int32_t u = act ? indices[start + S] : 0;
-            if (act) cand[base + rank] = u;
-            insert_append(tab, g.tlog, g.tmask, ncnt, newdst, u, act, counts, err, lane);
-        } else {
-            // k > 32: one lane runs Floyd sequentially using the candidate slots as scratch
-            if (lane == 0) {
-                if (d >= (int64_t)INT32_MAX) atomicOr(err, DEVERR_OVERFLOW);
-                for (int s2 = 0; s2 < k; ++s2) {
-                    const int64_t i = d - k + s2;
-                    const int64_t tt = (int64_t)__umul64hi(
-                        draw64(seed, (uint32_t)v, bid, (uint32_t)h, (uint32_t)s2), (uint64_t)(i + 1));
-                    bool present = false;
-                    for (int r = 0; r < s2; ++r)
-                        if ((int64_t)cand[base + r] == tt) {
-                            present = true;
-                            break;
-                        }
-                    cand[base + s2] = (int32_t)(present ? i : tt);
-                }
-                for (int a = 1; a < k; ++a) {
-                    const int32_t x = cand[base + a];
-                    int b = a - 1;
-                    while (b >= 0 && cand[base + b] > x) {
-                        cand[base + b + 1] = cand[base + b];
-                        --b;
+            for (int p = lane; p < d; p += 32) cand[base + p] = indices[start + p];
+            continue;
+        }
+        if (lane == 0) {
+            for (int s2 = 0; s2 < k; ++s2) {
+                const int64_t i = (int64_t)d - k + s2;
+                const int64_t tt = (int64_t)__umul64hi(
+                    draw64(seed, (uint32_t)v, (uint64_t)(bid0 + s), (uint32_t)h, (uint32_t)s2), (uint64_t)(i + 1));
+                bool present = false;
+                for (int r = 0; r < s2; ++r)
+                    if ((int64_t)cand[base + r] == tt) {
+                        present = true;
+                        break;
                     }
-                    cand[base + b + 1] = x;
-                }
+                cand[base + s2] = (int32_t)(present ? i : tt);
             }
-            __syncwarp();
-            for (int p0 = 0; p0 < k; p0 += 32) {
-                const int p = p0 + lane;
-                const bool act = p < k;
-                const int32_t u = act ? indices[start + cand[base + p]] : 0;
-                if (act) cand[base + p] = u;
-                insert_append(tab, g.tlog, g.tmask, ncnt, newdst, u, act, counts, err, lane);
+            for (int a = 1; a < k; ++a) {
+                const int32_t x = cand[base + a];
+                int b = a - 1;
+                while (b >= 0 && cand[base + b] > x) {
+                    cand[base + b + 1] = cand[base + b];
+                    --b;
+                }
+                cand[base + b + 1] = x;
             }
         }
+        __syncwarp();
+        for (int p = lane; p < k; p += 32) cand[base + p] = indices[start + cand[base + p]];
+        __syncwarp();
     }
 }
 
-// ---------------------------------- a3: order the new nodes of every batch
-__global__ void k_bucket_hist(Grp g, int64_t NB, int shift, int32_t* __restrict__ hist, int32_t* __restrict__ tmp_key,
-                              int32_t* __restrict__ tmp_pos) {
-    __shared__ int64_t s_off[kMaxGroup + 1];
-    for (int i = threadIdx.x; i <= g.G; i += blockDim.x) s_off[i] = g.new_off[i];
+// ------------------------- a3: dedup insert + access counter + bucket histogram
+// Thread per candidate: insert into the batch's hash set; the first insert of u
+// in a batch is the node's discovery: counts[u] += 1 and a slot in the
+// (batch, u >> shift) bucket; the table index is kept so the local ID can be
+// written back without probing.
+__global__ void __launch_bounds__(256) k_insert(Grp g, const int32_t* __restrict__ cand, int64_t NB, int shift,
+                                                int32_t* __restrict__ hist, int32_t* __restrict__ npos,
+                                                int32_t* __restrict__ ntab, uint32_t* counts, int* err) {
+    __shared__ int64_t s_cb[kMaxGroup + 1];
+    for (int i = threadIdx.x; i <= g.G; i += blockDim.x) s_cb[i] = g.cand_base[i];
     __syncthreads();
-    const int64_t TN = s_off[g.G];
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < TN; i += (int64_t)gridDim.x * blockDim.x) {
-        const int s = segment_of(s_off, g.G + 1, i);
-        const int32_t u = g.nodes[(int64_t)s * g.cap_n + g.n[s] + (i - s_off[s])];
-        const int64_t b = (int64_t)s * NB + (u >> shift);
-        tmp_key[i] = u;
-        tmp_pos[i] = atomicAdd(&hist[b], 1);
+    const int64_t C = s_cb[g.G];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < C; i += (int64_t)gridDim.x * blockDim.x) {
+        const int s = segment_of(s_cb, g.G + 1, i);
+        const int32_t u = cand[i];
+        int2* tab = g.table + ((int64_t)s << g.tlog);
+        uint32_t p = slot_hash(u, g.tlog);
+        int pos = -1;
+        for (uint32_t probes = 0;; ++probes) {
+            if (probes > g.tmask) {
+                atomicOr(err, DEVERR_TABLE);
+                break;
+            }
+            const int prev = atomicCAS(&tab[p].x, kEmpty, u);
+            if (prev == kEmpty) {
+                if (counts) atomicAdd(&counts[u], 1u);
+                pos = atomicAdd(&hist[(int64_t)s * NB + (u >> shift)], 1);
+                break;
+            }
+            if (prev == u) break;
+            p = (p + 1) & g.tmask;
+        }
+        npos[i] = pos;
+        ntab[i] = (int32_t)p;
     }
 }
 
-__global__ void k_bucket_scatter(Grp g, int64_t NB, int shift, const int64_t* __restrict__ bstart,
-                                 const int32_t* __restrict__ tmp_key, const int32_t* __restrict__ tmp_pos,
-                                 int32_t* __restrict__ sorted) {
-    __shared__ int64_t s_off[kMaxGroup + 1];
-    for (int i = threadIdx.x; i <= g.G; i += blockDim.x) s_off[i] = g.new_off[i];
+__global__ void k_bucket_scatter(Grp g, const int32_t* __restrict__ cand, int64_t NB, int shift,
+                                 const int64_t* __restrict__ bstart, const int32_t* __restrict__ npos,
+                                 const int32_t* __restrict__ ntab, unsigned long long* __restrict__ sorted) {
+    __shared__ int64_t s_cb[kMaxGroup + 1];
+    for (int i = threadIdx.x; i <= g.G; i += blockDim.x) s_cb[i] = g.cand_base[i];
     __syncthreads();
-    const int64_t TN = s_off[g.G];
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < TN; i += (int64_t)gridDim.x * blockDim.x) {
-        const int s = segment_of(s_off, g.G + 1, i);
-        const int32_t u = tmp_key[i];
-        const int64_t b = (int64_t)s * NB + (u >> shift);
-        sorted[bstart[b] + tmp_pos[i]] = u;
+    const int64_t C = s_cb[g.G];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < C; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t pos = npos[i];
+        if (pos < 0) continue;
+        const int s = segment_of(s_cb, g.G + 1, i);
+        const int32_t u = cand[i];
+        sorted[bstart[(int64_t)s * NB + (u >> shift)] + pos] =
+            ((unsigned long long)(uint32_t)u << 32) | (uint32_t)ntab[i];
     }
 }
 
-// thread per bucket: insertion sort of its (few) keys, then local-ID assignment
+// thread per bucket: insertion sort of its (few) (id, table index) pairs by id,
+// then the ascending-ID local numbering (reading c10) into nodes[] and the hash set
 __global__ void k_bucket_sort_assign(Grp g, int64_t NB, const int64_t* __restrict__ bstart,
-                                     const int32_t* __restrict__ hist, int32_t* __restrict__ sorted, int* err) {
+                                     const int32_t* __restrict__ hist, unsigned long long* __restrict__ sorted) {
     const int64_t nbk = (int64_t)g.G * NB;
     for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nbk; b += (int64_t)gridDim.x * blockDim.x) {
         const int32_t c = hist[b];
         if (c == 0) continue;
         const int64_t lo = bstart[b];
-        int32_t* a = sorted + lo;
+        unsigned long long* a = sorted + lo;
         for (int x = 1; x < c; ++x) {
-            const int32_t key = a[x];
+            const unsigned long long key = a[x];
             int y = x - 1;
             while (y >= 0 && a[y] > key) {
                 a[y + 1] = a[y];
@@ -345,13 +375,12 @@ __global__ void k_bucket_sort_assign(Grp g, int64_t NB, const int64_t* __restric
         const int64_t off = g.new_off[s];
         const int32_t n0 = g.n[s];
         int2* tab = g.table + ((int64_t)s << g.tlog);
+        int32_t* nodes = g.nodes + (int64_t)s * g.cap_n;
         for (int x = 0; x < c; ++x) {
-            const int32_t u = a[x];
+            const unsigned long long e = a[x];
             const int32_t local = n0 + (int32_t)(lo + x - off);
-            g.nodes[(int64_t)s * g.cap_n + local] = u;
-            int2* e = table_find(tab, g.tlog, g.tmask, u);
-            if (e) e->y = local;
-            else atomicOr(err, DEVERR_TABLE);
+            nodes[local] = (int32_t)(e >> 32);
+            tab[(uint32_t)e].y = local;
         }
     }
 }
@@ -547,7 +576,12 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
             shift[h] = idbits - b;
             hist_per_slot = std::max<int64_t>(hist_per_slot, (int64_t)1 << b);
         }
-        int64_t per_slot = cap_n * 4 + ((int64_t)8 << tlog) + hist_per_slot * 12 + cap_n * 12;
+        int64_t max_fr = 1, max_cand = 1;
+        for (int h = 0; h < H; ++h) {
+            max_fr = std::max(max_fr, fr_bound[h]);
+            max_cand = std::max(max_cand, cand_bound[h]);
+        }
+        int64_t per_slot = cap_n * (4 + 8) + ((int64_t)8 << tlog) + hist_per_slot * 12 + max_fr * 16 + max_cand * 8;
         for (int h = 0; h < H; ++h) per_slot += (fr_bound[h] + 1) * 8 + cand_bound[h] * 4;
         int64_t G = c->sample_group;
         if (G <= 0) {
@@ -557,21 +591,25 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
         G = std::min<int64_t>(std::min<int64_t>(G, kMaxGroup), nb);
 
         // ---- group scratch ----
-        DevBuf<int32_t> d_nodes, d_small32, d_hist, d_tmpk, d_tmpp, d_sorted;
+        DevBuf<int32_t> d_nodes, d_small32, d_hist, d_npos, d_ntab, d_fv, d_fdg;
+        DevBuf<unsigned long long> d_sorted;
         DevBuf<int2> d_table;
-        DevBuf<int64_t> d_small64, d_bstart, d_plan;
+        DevBuf<int64_t> d_small64, d_bstart, d_plan, d_fst;
         std::vector<DevBuf<int32_t>> d_cand(H);
         std::vector<DevBuf<int64_t>> d_cptr(H);
         DevBuf<int64_t*> d_cptr_list;
         DGNN_TRY(d_nodes.alloc(c, (size_t)(G * cap_n)));
         DGNN_TRY(d_table.alloc(c, (size_t)(G << tlog)));
         DGNN_TRY(d_small32.alloc(c, (size_t)(4 * G + G * (H + 2))));
-        DGNN_TRY(d_small64.alloc(c, (size_t)(3 * (G + 1) + 1 + 2 * H * (kMaxGroup + 1))));
+        DGNN_TRY(d_small64.alloc(c, (size_t)(3 * (G + 1) + 2 + 2 * H * (kMaxGroup + 1))));
         DGNN_TRY(d_hist.alloc(c, (size_t)(G * hist_per_slot)));
         DGNN_TRY(d_bstart.alloc(c, (size_t)(G * hist_per_slot)));
-        DGNN_TRY(d_tmpk.alloc(c, (size_t)(G * cap_n)));
-        DGNN_TRY(d_tmpp.alloc(c, (size_t)(G * cap_n)));
         DGNN_TRY(d_sorted.alloc(c, (size_t)(G * cap_n)));
+        DGNN_TRY(d_npos.alloc(c, (size_t)(G * max_cand)));
+        DGNN_TRY(d_ntab.alloc(c, (size_t)(G * max_cand)));
+        DGNN_TRY(d_fv.alloc(c, (size_t)(G * max_fr)));
+        DGNN_TRY(d_fdg.alloc(c, (size_t)(G * max_fr)));
+        DGNN_TRY(d_fst.alloc(c, (size_t)(G * max_fr)));
         for (int h = 0; h < H; ++h) {
             DGNN_TRY(d_cand[h].alloc(c, (size_t)std::max<int64_t>(1, G * cand_bound[h])));
             DGNN_TRY(d_cptr[h].alloc(c, (size_t)(G * fr_bound[h] + 1)));
@@ -600,8 +638,12 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
         g.cand_base = g.fr_off + (G + 1);
         g.new_off = g.cand_base + (G + 1);
         g.cand_total = g.new_off + (G + 1);
-        g.hop_fr_off = g.cand_total + 1;
+        int64_t* new_total = g.cand_total + 1;
+        g.hop_fr_off = new_total + 1;
         g.hop_cbase = g.hop_fr_off + H * (kMaxGroup + 1);
+        g.fv = d_fv.p;
+        g.fst = d_fst.p;
+        g.fdg = d_fdg.p;
 
         Arena a_nodes{c}, a_edges{c}, a_eptr{c};
         int64_t used_nodes = 0, used_edges = 0, used_eptr = 0;
@@ -619,29 +661,46 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
             DGNN_CK_LAUNCH();
             for (int h = 0; h < H; ++h) {
                 const int k = fanout[h];
+                const int64_t fmax = Gc * fr_bound[h], cmax = Gc * cand_bound[h];
                 launch(c, DGNN_K_SAMPLE_SETUP, 0.0, [&] { k_hop_begin<<<1, 32, 0, c->stream>>>(g, h); });
                 DGNN_CK_LAUNCH();
-                DGNN_TRY(scan::run(c, Gc * fr_bound[h], g.fr_off + Gc, DegIn{g, csr->indptr, k},
+                // a2: candidate offsets (and the frontier's (v, start, deg) records)
+                DGNN_TRY(scan::run(c, fmax, g.fr_off + Gc, DegIn{g, csr->indptr, k, c->dev_err},
                                    StoreExcl{d_cptr[h].p}, g.cand_total));
                 launch(c, DGNN_K_SAMPLE_SETUP, 0.0,
                        [&] { k_hop_cands<<<1, 32, 0, c->stream>>>(g, h, d_cptr[h].p); });
                 DGNN_CK_LAUNCH();
-                launch(c, DGNN_K_SAMPLE_HOP, 0.0, [&] {
-                    k_sample_hop<<<grid_for(c, Gc * fr_bound[h] * 32, 256), 256, 0, c->stream>>>(
-                        g, csr->indptr, csr->indices, k, rng_seed, batch_id_base + t0, h, d_cptr[h].p, d_cand[h].p,
-                        counts, c->dev_err);
-                });
-                DGNN_CK_LAUNCH();
-                launch(c, DGNN_K_SAMPLE_SETUP, 0.0, [&] { k_new_setup<<<1, 32, 0, c->stream>>>(g); });
-                DGNN_CK_LAUNCH();
-                // order the new nodes: bucket sort by (slot, id >> shift)
+                // a2: draws + gather
+                if (k > 0) {
+                    const int64_t cb = batch_id_base + t0;
+                    const int64_t* cp = d_cptr[h].p;
+                    int32_t* cd = d_cand[h].p;
+                    launch(c, DGNN_K_SAMPLE_HOP, 0.0, [&] {
+                        if (k <= 4)
+                            k_sample_hop<4><<<grid_for(c, fmax * 4, 256), 256, 0, c->stream>>>(
+                                g, csr->indices, k, rng_seed, cb, h, cp, cd);
+                        else if (k <= 8)
+                            k_sample_hop<8><<<grid_for(c, fmax * 8, 256), 256, 0, c->stream>>>(
+                                g, csr->indices, k, rng_seed, cb, h, cp, cd);
+                        else if (k <= 16)
+                            k_sample_hop<16><<<grid_for(c, fmax * 16, 256), 256, 0, c->stream>>>(
+                                g, csr->indices, k, rng_seed, cb, h, cp, cd);
+                        else if (k <= 32)
+                            k_sample_hop<32><<<grid_for(c, fmax * 32, 256), 256, 0, c->stream>>>(
+                                g, csr->indices, k, rng_seed, cb, h, cp, cd);
+                        else
+                            k_sample_hop_wide<<<grid_for(c, fmax * 32, 256), 256, 0, c->stream>>>(
+                                g, csr->indices, k, rng_seed, cb, h, cp, cd);
+                    });
+                    DGNN_CK_LAUNCH();
+                }
+                // a3: dedup insert + count + bucket histogram of (slot, id >> shift)
                 const int64_t NB = (int64_t)1 << bb[h];
                 const int64_t nbk = Gc * NB;
-                const int64_t tn_bound = Gc * new_bound[h];
                 DGNN_TRY(memset_async(c, d_hist.p, 0, sizeof(int32_t) * (size_t)nbk));
                 launch(c, DGNN_K_SAMPLE_ORDER, 0.0, [&] {
-                    k_bucket_hist<<<grid_for(c, tn_bound, 256), 256, 0, c->stream>>>(g, NB, shift[h], d_hist.p,
-                                                                                       d_tmpk.p, d_tmpp.p);
+                    k_insert<<<grid_for(c, cmax, 256), 256, 0, c->stream>>>(g, d_cand[h].p, NB, shift[h], d_hist.p,
+                                                                            d_npos.p, d_ntab.p, counts, c->dev_err);
                 });
                 DGNN_CK_LAUNCH();
                 {
@@ -649,21 +708,23 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
                     int64_t* bst = d_bstart.p;
                     DGNN_TRY(scan::run(
                         c, nbk, nullptr, [=] __device__(int64_t i) -> int64_t { return hist[i]; },
-                        [=] __device__(int64_t i, int64_t e, int64_t) { bst[i] = e; }, nullptr));
+                        [=] __device__(int64_t i, int64_t e, int64_t) { bst[i] = e; }, new_total));
                 }
+                launch(c, DGNN_K_SAMPLE_SETUP, 0.0,
+                       [&] { k_new_setup<<<1, 256, 0, c->stream>>>(g, d_bstart.p, NB, new_total); });
+                DGNN_CK_LAUNCH();
                 launch(c, DGNN_K_SAMPLE_ORDER, 0.0, [&] {
-                    k_bucket_scatter<<<grid_for(c, tn_bound, 256), 256, 0, c->stream>>>(
-                        g, NB, shift[h], d_bstart.p, d_tmpk.p, d_tmpp.p, d_sorted.p);
+                    k_bucket_scatter<<<grid_for(c, cmax, 256), 256, 0, c->stream>>>(
+                        g, d_cand[h].p, NB, shift[h], d_bstart.p, d_npos.p, d_ntab.p, d_sorted.p);
                 });
                 DGNN_CK_LAUNCH();
                 launch(c, DGNN_K_SAMPLE_ORDER, 0.0, [&] {
                     k_bucket_sort_assign<<<grid_for(c, nbk, 256), 256, 0, c->stream>>>(g, NB, d_bstart.p, d_hist.p,
-                                                                                         d_sorted.p, c->dev_err);
+                                                                                         d_sorted.p);
                 });
                 DGNN_CK_LAUNCH();
                 launch(c, DGNN_K_SAMPLE_REMAP, 0.0, [&] {
-                    k_remap<<<grid_for(c, Gc * cand_bound[h], 256), 256, 0, c->stream>>>(g, d_cand[h].p,
-                                                                                         c->dev_err);
+                    k_remap<<<grid_for(c, cmax, 256), 256, 0, c->stream>>>(g, d_cand[h].p, c->dev_err);
                 });
                 DGNN_CK_LAUNCH();
                 launch(c, DGNN_K_SAMPLE_SETUP, 0.0, [&] { k_hop_end<<<1, 256, 0, c->stream>>>(g, h); });

@@ -120,6 +120,12 @@ class Layout:
         return self.samples.num_batches
 
     # ------------------------------------------------------------ a9
+    def tier_mix(self) -> dict:
+        """Rows of all batches by source tier (measurement only, torch ops outside the path)."""
+        t = (self.addr[:self.samples.total_nodes].view(torch.int32) >> 30) & 3
+        c = torch.bincount(t.to(torch.int64), minlength=3).cpu().tolist()
+        return {"gpu_rows": c[0], "host_rows": c[1], "disk_rows": c[2]}
+
     def assemble(self, b: int, out: torch.Tensor, chunk_dev: torch.Tensor | None = None) -> torch.Tensor:
         """Assemble batch b into ``out`` ([n_b, dim]) reading the chunk from ``chunk_dev`` if given
         (already staged to HBM), else directly from the arena (UVA over PCIe)."""
@@ -135,44 +141,84 @@ class Layout:
                         self.plan.k_host, chunk, rows, self.row_bytes, out)
         return out
 
-    def assemble_epoch(self, batches=None, out_ring=None):
-        """Pipelined assembly: the chunk of batch b+1 is staged H2D on the side
-        stream while batch b is assembled on the ctx stream.  Yields (b, features)."""
-        ctx = self.ctx
-        bs = list(range(self.num_batches)) if batches is None else list(batches)
-        if not bs:
+    def assembly_groups(self, out_budget: int = 1 << 30):
+        """Runs of consecutive batches assembled per launch: the output of a run fits
+        ``out_budget`` bytes and its chunks are one contiguous span of the disk tier."""
+        no = self.samples.node_off_host
+        groups = []
+        b0 = 0
+        nb = self.num_batches
+        while b0 < nb:
+            b1 = b0 + 1
+            while b1 < nb and (no[b1 + 1] - no[b0]) * self.row_bytes <= out_budget and b1 - b0 < 1024:
+                b1 += 1
+            groups.append((b0, b1))
+            b0 = b1
+        return groups
+
+    def assemble_epoch(self, ctx: A.Ctx | None = None, out_budget: int = 1 << 30):
+        """Pipelined assembly: the chunks of the next run of batches are staged H2D
+        on the side stream while the current run is assembled on the ctx stream (one
+        dgnn_assemble_group launch per run).  Yields (b, features[n_b, dim]) per batch; a
+        yielded view stays valid until two runs later."""
+        ctx = ctx or self.ctx
+        nb = self.num_batches
+        if nb == 0:
             return
-        max_n = int(np.max(np.diff(self.samples.node_off_host))) if self.num_batches else 0
-        max_c = int(np.max(self.batch_chunk[:, 1])) * self.row_bytes if self.num_batches else 0
+        groups = self.assembly_groups(out_budget)
+        no = self.samples.node_off_host
+        rows_pre = np.concatenate([[0], np.cumsum(self.batch_chunk[:, 1])])
+        # per-run device tables: node offsets, chunk byte offsets, packed-row prefix (relative to the run)
+        tabs, spans = [], []
+        for (b0, b1) in groups:
+            c_lo = int(self.batch_chunk[b0, 0])
+            # chunks of consecutive batches are contiguous (4 KiB-aligned) in the disk tier
+            c_hi = int(self.batch_chunk[b1, 0]) if b1 < nb else int(self.stats["arena_bytes"])
+            chunk_off = np.concatenate([self.batch_chunk[b0:b1, 0] - c_lo, [c_hi - c_lo]])
+            tabs.append(np.concatenate([no[b0:b1 + 1] - no[b0], chunk_off, rows_pre[b0:b1 + 1] - rows_pre[b0]]))
+            spans.append((int(no[b0]), int(no[b1]), c_lo, c_hi))
         dev = ctx.device
-        if out_ring is None:
-            out_ring = [torch.empty((max_n, self.dim), dtype=self.dtype, device=dev) for _ in range(2)]
-        staged = self.arena is not None
-        chunk_ring = [torch.empty(max(max_c, 16), dtype=torch.uint8, device=dev) for _ in range(2)] if staged else None
+        with torch.cuda.stream(ctx.stream):
+            flat = torch.from_numpy(np.concatenate(tabs).astype(np.int64)).to(dev, non_blocking=False)
+            max_rows = max(s[1] - s[0] for s in spans)
+            max_c = max(s[3] - s[2] for s in spans)
+            out_ring = [torch.empty((max_rows, self.dim), dtype=self.dtype, device=dev) for _ in range(2)]
+            staged = self.arena is not None
+            chunk_ring = [torch.empty(max(max_c, 16), dtype=torch.uint8, device=dev) for _ in range(2)] \
+                if staged else None
+        offs = np.concatenate([[0], np.cumsum([len(t) for t in tabs])])
         tickets = {}
 
         def stage(i):
-            b = bs[i]
-            off, rows = int(self.batch_chunk[b, 0]), int(self.batch_chunk[b, 1])
-            tickets[i] = A.dgnn_stage_copy(ctx, chunk_ring[i % 2], self.arena.ptr + off, rows * self.row_bytes, 1)
+            n0, n1, c_lo, c_hi = spans[i]
+            tickets[i] = A.dgnn_stage_copy(ctx, chunk_ring[i % 2], self.arena.ptr + c_lo, c_hi - c_lo, 1)
 
         if staged:
             stage(0)
-        for i, b in enumerate(bs):
+        for i, (b0, b1) in enumerate(groups):
+            n0, n1, c_lo, c_hi = spans[i]
             if staged:
-                if i + 1 < len(bs):
+                if i + 1 < len(groups):
                     stage(i + 1)
                 A.dgnn_stage_wait(ctx, tickets.pop(i))
-            n = int(self.samples.node_off_host[b + 1] - self.samples.node_off_host[b])
-            out = out_ring[i % 2][:n]
-            self.assemble(b, out, chunk_ring[i % 2] if staged else None)
-            yield b, out
+                chunk = chunk_ring[i % 2]
+            else:
+                chunk = self.arena_dev.data_ptr() + c_lo
+            k = b1 - b0
+            t = flat[int(offs[i]):int(offs[i + 1])]
+            out = out_ring[i % 2]
+            A.dgnn_assemble_group(ctx, self.addr[n0:n1], t[:k + 1], n1 - n0, self.gpu_tier, self.plan.k_gpu,
+                                  self.host_tier.ptr, self.plan.k_host, chunk, t[k + 1:2 * k + 2], t[2 * k + 2:],
+                                  self.row_bytes, out)
+            for b in range(b0, b1):
+                yield b, out[int(no[b] - n0):int(no[b + 1] - n0)]
 
 
 def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, features: torch.Tensor,
                    seeds: torch.Tensor, fanout, batch_size: int, gpu_rows: int, host_rows: int, rng_seed: int,
                    group_size: int = 64, batch_id_base: int = 0, stage: str = "pinned",
-                   counts: torch.Tensor | None = None, ws: Workspace | None = None) -> Layout:
+                   counts: torch.Tensor | None = None, ws: Workspace | None = None,
+                   group_budget: int = 4 << 30) -> Layout:
     """Run a1-a8 on this rank's batches.
 
     ``seeds`` are this rank's seeds (batch t of them gets bid = batch_id_base + t).
@@ -214,14 +260,21 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
     groups = []
     batch_chunk = np.zeros((nb, 2), np.int64)
     arena_off = 0
-    for g0 in range(0, nb, group_size):
-        g1 = min(nb, g0 + group_size)
+    g0 = 0
+    while g0 < nb:
+        # a packing group: at most `group_size` batches (0 = unbounded) whose chunks fit the
+        # group-buffer budget (the analogue of P:439's "C - 4N" partition sizing)
+        g1 = g0 + 1
+        while g1 < nb and (group_size <= 0 or g1 - g0 < group_size) and \
+                (po[g1 + 1] - po[g0]) * row_bytes + 4096 * (g1 + 1 - g0) <= group_budget:
+            g1 += 1
         rel = po[g0:g1 + 1] - po[g0]
         co = A.dgnn_chunk_layout(rel, row_bytes)
         groups.append(Group(g0, g1, rows[g0:g1], co, arena_off, int(co[-1])))
         batch_chunk[g0:g1, 0] = arena_off + co[:-1]
         batch_chunk[g0:g1, 1] = rows[g0:g1]
         arena_off += int(co[-1])
+        g0 = g1
     arena = arena_dev = None
     if stage == "pinned":
         arena = ws.host("arena", arena_off) if ws is not None else HostBuffer(arena_off)
@@ -252,7 +305,8 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
     for t in tickets:
         if t is not None:
             A.dgnn_stage_wait(ctx, t)
-    stats.update(packed_rows=int(po[-1]), packed_bytes=int(po[-1]) * row_bytes, arena_bytes=arena_off,
+    stats.update(row_bytes=row_bytes, groups=len(groups), packed_rows=int(po[-1]),
+                 packed_bytes=int(po[-1]) * row_bytes, arena_bytes=arena_off,
                  k_gpu=plan.k_gpu, k_host=plan.k_host, total_nodes=total_nodes, total_edges=samples.total_edges)
     del packed_ids
     return Layout(ctx, samples, plan, counts, row_bytes, dim, features.dtype, addr, gpu_tier, host_tier, arena,

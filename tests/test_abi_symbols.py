@@ -20,7 +20,8 @@ def _declared():
 
 @pytest.fixture(scope="module")
 def lib():
-    from paper_2405_05231_b200 import build
+    from __graft_entry__ import _build_module
+    build = _build_module()
     path = build.build()
     return ctypes.CDLL(path)
 
@@ -42,7 +43,8 @@ def test_binding_exports_match_header():
 
 
 def test_library_is_sm100a():
-    from paper_2405_05231_b200 import build
+    from __graft_entry__ import _build_module
+    build = _build_module()
     import subprocess
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", build.LIB], capture_output=True,
                          text=True).stdout

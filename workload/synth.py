@@ -42,19 +42,19 @@ CONFIGS = {
                  gpu_frac=0.05, host_frac=0.10),
     # configs[1]
     "products": dict(num_nodes=2_400_000, num_edges=62_000_000, degree="lognormal", skew="PS", dim=100,
-                     fanout=(15, 10, 5), batch_size=1024, num_seeds=196_615, group_size=64,
+                     fanout=(15, 10, 5), batch_size=1024, num_seeds=196_615, group_size=0,
                      gpu_frac=0.05, host_frac=0.10),
     # configs[2]: the north_star's scaling workload
     "papers": dict(num_nodes=111_000_000, num_edges=1_600_000_000, degree="lognormal", skew="PS", dim=128,
-                   fanout=(10, 10, 10), batch_size=1024, num_seeds=1_200_000, group_size=64,
+                   fanout=(10, 10, 10), batch_size=1024, num_seeds=1_200_000, group_size=0,
                    gpu_frac=0.05, host_frac=0.10),
     # configs[3]
     "friendster": dict(num_nodes=65_600_000, num_edges=1_800_000_000, degree="pareto", skew="FS", dim=256,
-                       fanout=(10, 10, 10), batch_size=1024, num_seeds=656_000, group_size=16,
+                       fanout=(10, 10, 10), batch_size=1024, num_seeds=656_000, group_size=0,
                        gpu_frac=0.05, host_frac=0.10),
     # configs[4] (features exceed one GPU: needs the sharded tier, not run at N=1)
     "igb": dict(num_nodes=100_000_000, num_edges=1_200_000_000, degree="lognormal", skew="IG", dim=1024,
-                fanout=(10, 10, 10), batch_size=1024, num_seeds=1_000_000, group_size=8,
+                fanout=(10, 10, 10), batch_size=1024, num_seeds=1_000_000, group_size=0,
                 gpu_frac=0.05, host_frac=0.10),
 }
 
