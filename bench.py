@@ -185,12 +185,14 @@ class Runner:
         from paper_2405_05231_b200.layout import Workspace
         self.dg, self.inp, self.rank, self.dev, self.pipelined = dg, inp, rank, dev, pipelined
         self.sA = torch.cuda.Stream(dev)
-        self.sB = torch.cuda.Stream(dev) if pipelined else self.sA
+        # the PCIe-bound assembly gets the higher stream priority: its CTAs are scheduled
+        # first and the layout of the next pass fills the remaining SM capacity
+        self.sB = torch.cuda.Stream(dev, priority=-1) if pipelined else self.sA
         torch.cuda.set_stream(self.sA)
         self.ctxA = dg.Ctx(device=dev, stream=self.sA)
         self.ctxB = dg.Ctx(device=dev, stream=self.sB) if pipelined else self.ctxA
         if pipelined:
-            self.ctxB.set_assemble_occupancy(2)  # PCIe-bound: leave SMs to the concurrent layout
+            self.ctxB.set_assemble_occupancy(int(os.environ.get("DGNN_ASM_OCC", "4")))  # PCIe-bound: leave SMs
         N = inp[1].numel() - 1
         self.ws = [Workspace(), Workspace()]
         self.counts = [torch.zeros(N, dtype=torch.int32, device=dev) for _ in range(2)]

@@ -1,0 +1,100 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py times.
+
+The papers100M-shaped workload (111 M nodes, 1.6 B edges, 128-d, fanout [10,10,10],
+1172 batches of 1024) runs through the same offline_layout + assemble_epoch calls as
+bench.py.  The oracle then recomputes, one by one, a sample of batches (first, middle,
+last, ragged tail) and the whole-epoch counts and tier plan; packed chunks and
+assembled rows are checked against the closed-form features (no 57 GB host copy).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from workload import CONFIGS, config_rows, feature_rows_np, make_features, make_graph, make_seeds
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+RNG_SEED = 0x5EEDD15C
+
+
+@pytest.fixture(scope="module")
+def papers():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_2405_05231_b200 as dg
+    dev = torch.device("cuda", 0)
+    cfg = dict(CONFIGS["papers"])
+    indptr, indices = make_graph(cfg["num_nodes"], cfg["num_edges"], cfg["degree"], cfg["skew"], 0, dev)
+    seeds = make_seeds(cfg["num_nodes"], cfg["num_seeds"], 0, dev)
+    feats = make_features(cfg["num_nodes"], cfg["dim"], dev, fseed=1)
+    gpu_rows, host_rows = config_rows(cfg)
+    ctx = dg.Ctx(device=dev)
+    L = dg.offline_layout(ctx, indptr, indices, feats, seeds, cfg["fanout"], cfg["batch_size"], gpu_rows, host_rows,
+                          RNG_SEED, group_size=cfg["group_size"])
+    ctx.sync()
+    del feats
+    host = dict(indptr=indptr.cpu().numpy(), indices=indices.cpu().numpy(), seeds=seeds.cpu().numpy())
+    return dict(dg=dg, ctx=ctx, L=L, cfg=cfg, gpu_rows=gpu_rows, host_rows=host_rows, **host)
+
+
+SAMPLED = [0, 1, 586, 1170, 1171]
+
+
+def test_sampled_batches_bit_exact(papers):
+    L, cfg = papers["L"], papers["cfg"]
+    ref = oracle.sample(papers["indptr"], papers["indices"], papers["seeds"], cfg["batch_size"], list(cfg["fanout"]),
+                        RNG_SEED, batches=SAMPLED, threads=8)
+    S = L.samples
+    assert S.num_batches == 1172
+    for r in ref:
+        b = r.bid
+        n0, n1 = S.node_off_host[b], S.node_off_host[b + 1]
+        assert np.array_equal(S.nodes[n0:n1].cpu().numpy(), r.nodes)
+        assert np.array_equal(S.hop_off_host[b], r.hop_off)
+        p0, p1 = S.eptr_off_host[b], S.eptr_off_host[b + 1]
+        assert np.array_equal(S.eptr[p0:p1].cpu().numpy(), r.eptr)
+        e0, e1 = S.edge_off_host[b], S.edge_off_host[b + 1]
+        assert np.array_equal(S.src_local[e0:e1].cpu().numpy(), r.src_local)
+    assert len(ref[-1].nodes[:ref[-1].hop_off[1]]) == 1_200_000 - 1171 * 1024  # ragged tail batch
+
+
+def test_epoch_counts_and_tier_plan_bit_exact(papers):
+    L, cfg = papers["L"], papers["cfg"]
+    counts = np.zeros(cfg["num_nodes"], np.uint32)
+    for t0 in range(0, 1172, 200):  # bounded host memory: stream the oracle's samples
+        part = oracle.sample(papers["indptr"], papers["indices"], papers["seeds"], cfg["batch_size"],
+                             list(cfg["fanout"]), RNG_SEED, batches=range(t0, min(1172, t0 + 200)), threads=16)
+        oracle.count_frequencies(part, cfg["num_nodes"], counts)
+        del part
+    got = L.counts.cpu().numpy().view(np.uint32)
+    assert np.array_equal(got, counts)
+    tm, gpu_ids, host_ids = oracle.select_tiers(counts, papers["gpu_rows"], papers["host_rows"])
+    assert np.array_equal(L.plan.gpu_ids.cpu().numpy(), gpu_ids)
+    assert np.array_equal(L.plan.host_ids.cpu().numpy(), host_ids)
+    assert np.array_equal(L.plan.tier_map.cpu().numpy().view(np.uint32), tm)
+
+
+def test_sampled_classify_pack_assemble(papers):
+    L, cfg = papers["L"], papers["cfg"]
+    dim, rb = cfg["dim"], cfg["dim"] * 4
+    tm = L.plan.tier_map.cpu().numpy().view(np.uint32)
+    arena = L.arena.tensor.numpy()
+    S = L.samples
+    for b in SAMPLED:
+        nodes = S.nodes[S.node_off_host[b]:S.node_off_host[b + 1]].cpu().numpy()
+        addr, P = oracle.classify(nodes, tm)
+        got_addr = L.addr[S.node_off_host[b]:S.node_off_host[b + 1]].cpu().numpy().view(np.uint32)
+        assert np.array_equal(got_addr, addr)
+        off, rows = L.batch_chunk[b]
+        assert rows == len(P)
+        chunk = arena[off:off + rows * rb].view(np.float32).reshape(rows, dim)
+        assert np.array_equal(chunk.view(np.uint32), feature_rows_np(P, dim, 1).view(np.uint32))
+        end = L.batch_chunk[b + 1, 0] if b + 1 < S.num_batches else L.stats["arena_bytes"]
+        assert not arena[off + rows * rb:end].any()  # zero tail (reading c20)
+    want = set(SAMPLED)
+    for b, out in L.assemble_epoch():
+        if b in want:
+            nodes = S.nodes[S.node_off_host[b]:S.node_off_host[b + 1]].cpu().numpy()
+            exp = feature_rows_np(nodes, dim, 1)
+            assert np.array_equal(out.cpu().numpy().view(np.uint32), exp.view(np.uint32)), f"batch {b}"
+    papers["ctx"].sync()
