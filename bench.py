@@ -192,13 +192,14 @@ class Runner:
         self.ctxA = dg.Ctx(device=dev, stream=self.sA)
         self.ctxB = dg.Ctx(device=dev, stream=self.sB) if pipelined else self.ctxA
         if pipelined:
-            self.ctxB.set_assemble_occupancy(int(os.environ.get("DGNN_ASM_OCC", "4")))  # PCIe-bound: leave SMs
+            self.ctxB.set_assemble_occupancy(int(os.environ.get("DGNN_ASM_OCC", "2")))  # PCIe-bound: leave SMs
         N = inp[1].numel() - 1
         self.ws = [Workspace(), Workspace()]
         self.counts = [torch.zeros(N, dtype=torch.int32, device=dev) for _ in range(2)]
         cfg = inp[0]
         self.nb = (inp[3].numel() + cfg["batch_size"] - 1) // cfg["batch_size"]
         self.before_layout = None  # hook: e.g. the e2e H2D copies of the inputs
+        self.host_window = 128
 
     def ctxs(self):
         return [self.ctxA] if self.ctxB is self.ctxA else [self.ctxA, self.ctxB]
@@ -222,7 +223,7 @@ class Runner:
         last = None
         for e in range(K):
             self.sB.wait_event(ev_l)
-            for _ in L.assemble_epoch(ctx=self.ctxB):
+            for _ in L.assemble_epoch(ctx=self.ctxB, host_window=self.host_window):
                 pass
             ev_a = torch.cuda.Event()
             ev_a.record(self.sB)
@@ -278,6 +279,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sequential", action="store_true", help="no epoch pipelining (one stream)")
+    ap.add_argument("--host-window", type=int, default=128,
+                    help="batches per host-row merging window in a9 (1 = per-batch UVA reads, the paper's)")
     args = ap.parse_args()
     ws, rank, local = setup_dist(args)
     dev = torch.device("cuda", local)
@@ -290,6 +293,7 @@ def main():
     N = indptr.numel() - 1
     nb = (seeds.numel() + cfg["batch_size"] - 1) // cfg["batch_size"]
     R = Runner(dg, inp, rank, dev, pipelined=not args.sequential)
+    R.host_window = args.host_window
     t = time.time()
     L = R.run(1, keep_last=True)
     torch.cuda.synchronize()
@@ -297,8 +301,8 @@ def main():
     stats0.update(L.tier_mix())
     del L
     log(f"[bench] first pass {time.time() - t:.1f}s stats={stats0}")
-    if args.warmup > 1:
-        R.run(args.warmup - 1)
+    # the remaining warm-up passes; at least 2 so that both double-buffer slots are allocated
+    R.run(max(args.warmup - 1, 2))
     torch.cuda.synchronize()
 
     # ---------------- timed region (device time, CUDA events; max over ranks) ----------------
@@ -355,6 +359,7 @@ def main():
                    "num_seeds": int(seeds.numel()), "batches_per_rank": nb, "gpu_rows": gpu_rows,
                    "host_rows": host_rows, "group_size": cfg["group_size"], "disk_tier": "pinned host arena",
                    "parallelism": f"dp{ws} (batch-sharded, count all-reduce)",
+                   "host_window_batches": args.host_window,
                    "schedule": "sequential" if args.sequential else
                    "pipelined: layout of pass e+1 overlaps assembly of pass e (2 streams)",
                    "l2": "inputs larger than L2 (features %.1f GB, CSR %.1f GB); no flush needed" % (

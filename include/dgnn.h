@@ -274,14 +274,33 @@ dgnn_status dgnn_assemble(dgnn_ctx* ctx, const uint32_t* addr, int64_t n, const 
  *   addr        device uint32 [n]: the address tables of the batches, concatenated.
  *   node_off    device int64 [nb+1]: row offsets of the batches inside addr / out (node_off[0] = 0,
  *               node_off[nb] = n).
+ *   host_tier   the host tier (pinned, UVA) when host_map is NULL; otherwise a device buffer of
+ *               staged host rows and host_map (device int32 [k_host]) gives the staged row of
+ *               each host slot (see dgnn_host_window).
  *   chunk_base  UVA base of the batches' staged chunks; chunk_off device int64 [nb+1] byte
  *               offsets of each chunk from chunk_base; chunk_rows device int64 [nb+1] exclusive
  *               prefix of the packed rows (a DISK slot of batch b must be < its packed rows).
  *   out         device [n * row_bytes]. */
 dgnn_status dgnn_assemble_group(dgnn_ctx* ctx, const uint32_t* addr, const int64_t* node_off, int64_t nb, int64_t n,
                                 const void* gpu_tier, int64_t k_gpu, const void* host_tier, int64_t k_host,
-                                const void* chunk_base, const int64_t* chunk_off, const int64_t* chunk_rows,
-                                int64_t row_bytes, void* out);
+                                const int32_t* host_map, const void* chunk_base, const int64_t* chunk_off,
+                                const int64_t* chunk_rows, int64_t row_bytes, void* out);
+
+/* Host-row merging for a window of consecutive batches (the paper's request merging, P:305,
+ * applied to CPU-cache rows): every host-tier slot referenced by addr[0..n) is listed once.
+ *   stamp      device int32 [k_host], caller-owned, set to -1 once before the first window;
+ *              window_id must differ between consecutive windows (use an increasing counter).
+ *   list       device int32 [capacity]: the distinct slots (arbitrary order).
+ *   smap       device int32 [k_host]: smap[slot] = position of slot in list (for listed slots).
+ *   count      device int64 [1]: number of listed slots (overwritten).
+ * Pair with dgnn_gather_rows_dev(host_tier, list, count -> staging) and dgnn_assemble_group
+ * (host_tier = staging, host_map = smap): each host row then crosses PCIe once per window
+ * instead of once per batch; outputs are unchanged. */
+dgnn_status dgnn_host_window(dgnn_ctx* ctx, const uint32_t* addr, int64_t n, int32_t window_id, int32_t* stamp,
+                             int64_t k_host, int32_t* list, int64_t capacity, int32_t* smap, int64_t* count);
+/* dgnn_gather_rows with the row count read from device memory (*n_dev <= n_max). */
+dgnn_status dgnn_gather_rows_dev(dgnn_ctx* ctx, const void* features, int64_t num_rows, int64_t row_bytes,
+                                 const int32_t* ids, const int64_t* n_dev, int64_t n_max, void* out);
 
 #ifdef __cplusplus
 }

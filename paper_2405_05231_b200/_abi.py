@@ -38,6 +38,7 @@ EXPORTS = [
     "dgnn_samples_free", "dgnn_build_cache", "dgnn_cache_plan_get_info", "dgnn_cache_plan_free", "dgnn_classify",
     "dgnn_chunk_layout", "dgnn_pack", "dgnn_gather_rows", "dgnn_stage_copy", "dgnn_stage_wait", "dgnn_stage_sync",
     "dgnn_host_alloc", "dgnn_host_free", "dgnn_assemble", "dgnn_assemble_group", "dgnn_ctx_set_assemble_occupancy",
+    "dgnn_host_window", "dgnn_gather_rows_dev",
 ]
 
 
@@ -120,7 +121,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "dgnn_host_alloc": (i32, [i64, ctypes.POINTER(P)]),
             "dgnn_host_free": (i32, [P]),
             "dgnn_assemble": (i32, [P, P, i64, P, i64, P, i64, P, i64, i64, P]),
-            "dgnn_assemble_group": (i32, [P, P, P, i64, i64, P, i64, P, i64, P, P, P, i64, P]),
+            "dgnn_assemble_group": (i32, [P, P, P, i64, i64, P, i64, P, i64, P, P, P, P, i64, P]),
+            "dgnn_host_window": (i32, [P, P, i64, i32, P, i64, P, i64, P, P]),
+            "dgnn_gather_rows_dev": (i32, [P, P, i64, i64, P, P, i64, P]),
             "dgnn_ctx_set_assemble_occupancy": (i32, [P, i32]),
         }
         for name, (res, args) in sig.items():
@@ -408,8 +411,21 @@ def dgnn_assemble(ctx: Ctx, addr: torch.Tensor, gpu_tier, k_gpu: int, host_tier,
 
 def dgnn_assemble_group(ctx: Ctx, addr: torch.Tensor, node_off: torch.Tensor, n: int, gpu_tier, k_gpu: int,
                         host_tier, k_host: int, chunk_base, chunk_off: torch.Tensor, chunk_rows: torch.Tensor,
-                        row_bytes: int, out):
+                        row_bytes: int, out, host_map=None):
     _check(load_library().dgnn_assemble_group(ctx.handle, _ptr(addr), _ptr(node_off), node_off.numel() - 1, int(n),
                                               _ptr(gpu_tier), int(k_gpu), _ptr(host_tier), int(k_host),
-                                              _ptr(chunk_base), _ptr(chunk_off), _ptr(chunk_rows), int(row_bytes),
-                                              _ptr(out)), "dgnn_assemble_group")
+                                              _ptr(host_map), _ptr(chunk_base), _ptr(chunk_off), _ptr(chunk_rows),
+                                              int(row_bytes), _ptr(out)), "dgnn_assemble_group")
+
+
+def dgnn_host_window(ctx: Ctx, addr: torch.Tensor, window_id: int, stamp: torch.Tensor, k_host: int,
+                     list_: torch.Tensor, smap: torch.Tensor, count: torch.Tensor):
+    _check(load_library().dgnn_host_window(ctx.handle, _ptr(addr), addr.numel(), int(window_id), _ptr(stamp),
+                                           int(k_host), _ptr(list_), list_.numel(), _ptr(smap), _ptr(count)),
+           "dgnn_host_window")
+
+
+def dgnn_gather_rows_dev(ctx: Ctx, features, num_rows: int, row_bytes: int, ids: torch.Tensor, n_dev: torch.Tensor,
+                         out):
+    _check(load_library().dgnn_gather_rows_dev(ctx.handle, _ptr(features), int(num_rows), int(row_bytes), _ptr(ids),
+                                               _ptr(n_dev), ids.numel(), _ptr(out)), "dgnn_gather_rows_dev")

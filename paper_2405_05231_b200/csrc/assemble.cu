@@ -45,7 +45,7 @@ struct AsmRow {
 };
 
 template <class V>
-__global__ void __launch_bounds__(256) k_assemble(AsmRow fn, int64_t n) {
+__global__ void __launch_bounds__(256, 6) k_assemble(AsmRow fn, int64_t n) {
     const int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
     copy_rows_warp<kAsmU, V>(n, fn.row_bytes, fn, warp, nwarps);
@@ -67,6 +67,7 @@ struct AsmGroupRow {
     int64_t kg;
     const uint8_t* host;
     int64_t kh;
+    const int32_t* host_map;   // NULL: host = the host tier; else host = staged rows, row host_map[slot]
     const uint8_t* chunk_base;
     int64_t row_bytes;
     uint8_t* out;
@@ -79,7 +80,7 @@ struct AsmGroupRow {
         if (tier == DGNN_TIER_GPU && slot < kg) {
             s = gpu + slot * row_bytes;
         } else if (tier == DGNN_TIER_HOST && slot < kh) {
-            s = host + slot * row_bytes;
+            s = host + (host_map ? (int64_t)host_map[slot] : slot) * row_bytes;
         } else if (tier == DGNN_TIER_DISK) {
             const int b = segment_of(node_off, nb + 1, j);
             if (slot >= chunk_rows[b + 1] - chunk_rows[b]) {
@@ -98,7 +99,7 @@ struct AsmGroupRow {
 };
 
 template <class V>
-__global__ void __launch_bounds__(256) k_assemble_group(AsmGroupRow fn, int64_t n) {
+__global__ void __launch_bounds__(256, 6) k_assemble_group(AsmGroupRow fn, int64_t n) {
     __shared__ int64_t s_no[kMaxSeg + 1], s_co[kMaxSeg + 1], s_cr[kMaxSeg + 1];
     if (fn.nb <= kMaxSeg) {
         for (int i = threadIdx.x; i <= fn.nb; i += blockDim.x) {
@@ -117,6 +118,65 @@ __global__ void __launch_bounds__(256) k_assemble_group(AsmGroupRow fn, int64_t 
 }
 
 bool al16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
+// Host-row merging over a window of batches: the first visit of a host-tier slot
+// in window `wid` (atomicExch on a per-slot stamp) appends it to the window's list
+// and records its position, so each host row crosses PCIe once per window.
+__global__ void __launch_bounds__(256) k_host_window(const uint32_t* __restrict__ addr, int64_t n, int32_t wid,
+                                                     int32_t* __restrict__ stamp, int64_t kh,
+                                                     int32_t* __restrict__ list, int64_t cap,
+                                                     int32_t* __restrict__ smap, unsigned long long* count,
+                                                     int* err) {
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x; i0 < n; i0 += stride) {
+        const int64_t i = i0 + threadIdx.x;
+        bool first = false;
+        int64_t slot = 0;
+        if (i < n) {
+            const uint32_t a = addr[i];
+            slot = a & DGNN_SLOT_MASK;
+            if ((a >> DGNN_TIER_SHIFT) == DGNN_TIER_HOST && slot < kh) first = atomicExch(&stamp[slot], wid) != wid;
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, first);
+        if (m) {
+            const int leader = __ffs(m) - 1;
+            unsigned long long base = 0;
+            if (lane == leader) base = atomicAdd(count, (unsigned long long)__popc(m));
+            base = __shfl_sync(0xffffffffu, base, leader);
+            if (first) {
+                const int64_t pos = (int64_t)base + __popc(m & lanemask_lt());
+                if (pos < cap) {
+                    list[pos] = (int32_t)slot;
+                    smap[slot] = (int32_t)pos;
+                } else {
+                    atomicOr(err, DEVERR_OVERFLOW);
+                }
+            }
+        }
+    }
+}
+
+struct Row {
+    const uint8_t* src;
+    int64_t rb;
+    const int32_t* ids;
+    uint8_t* dst;
+    __device__ __forceinline__ bool operator()(int64_t r, const uint8_t*& s, uint8_t*& d) const {
+        s = src + (int64_t)ids[r] * rb;
+        d = dst + r * rb;
+        return true;
+    }
+};
+
+template <class V>
+__global__ void __launch_bounds__(256, 6) k_gather_dev(const uint8_t* __restrict__ src, int64_t row_bytes,
+                                                    const int32_t* __restrict__ ids, const int64_t* __restrict__ n_dev,
+                                                    uint8_t* __restrict__ dst) {
+    const int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    copy_rows_warp<kAsmU, V>(*n_dev, row_bytes, Row{src, row_bytes, ids, dst}, warp, nwarps);
+}
 
 }  // namespace
 }  // namespace dgnn
@@ -145,10 +205,48 @@ extern "C" dgnn_status dgnn_assemble(dgnn_ctx* c, const uint32_t* addr, int64_t 
     return DGNN_OK;
 }
 
+extern "C" dgnn_status dgnn_host_window(dgnn_ctx* c, const uint32_t* addr, int64_t n, int32_t window_id,
+                                        int32_t* stamp, int64_t k_host, int32_t* list, int64_t capacity,
+                                        int32_t* smap, int64_t* count) {
+    DGNN_REQUIRE(c && stamp && list && smap && count && (n == 0 || addr), "dgnn_host_window: NULL argument");
+    DGNN_REQUIRE(n >= 0 && k_host >= 0 && capacity >= 0 && window_id >= 0, "dgnn_host_window: bad sizes");
+    DGNN_CK(cudaSetDevice(c->device));
+    DGNN_TRY(memset_async(c, count, 0, sizeof(int64_t)));
+    if (n == 0) return DGNN_OK;
+    launch(c, DGNN_K_ASSEMBLE, 0.0, [&] {
+        k_host_window<<<grid_for(c, n, 256, 8), 256, 0, c->stream>>>(addr, n, window_id, stamp, k_host, list,
+                                                                     capacity, smap, (unsigned long long*)count,
+                                                                     c->dev_err);
+    });
+    DGNN_CK_LAUNCH();
+    return DGNN_OK;
+}
+
+extern "C" dgnn_status dgnn_gather_rows_dev(dgnn_ctx* c, const void* features, int64_t num_rows, int64_t row_bytes,
+                                            const int32_t* ids, const int64_t* n_dev, int64_t n_max, void* out) {
+    DGNN_REQUIRE(c && n_dev && (n_max == 0 || (features && ids && out)), "dgnn_gather_rows_dev: NULL argument");
+    DGNN_REQUIRE(row_bytes > 0 && row_bytes % 4 == 0 && n_max >= 0, "dgnn_gather_rows_dev: bad sizes");
+    if (n_max == 0) return DGNN_OK;
+    DGNN_CK(cudaSetDevice(c->device));
+    const bool v16 = row_bytes % 16 == 0 && al16(features) && al16(out);
+    const int grid = grid_for(c, n_max * 32 / kAsmU, 256, c->assemble_blocks_per_sm);
+    launch(c, DGNN_K_ASSEMBLE, 0.0, [&] {
+        if (v16)
+            k_gather_dev<uint4><<<grid, 256, 0, c->stream>>>((const uint8_t*)features, row_bytes, ids, n_dev,
+                                                             (uint8_t*)out);
+        else
+            k_gather_dev<uint32_t><<<grid, 256, 0, c->stream>>>((const uint8_t*)features, row_bytes, ids, n_dev,
+                                                                (uint8_t*)out);
+    });
+    DGNN_CK_LAUNCH();
+    return DGNN_OK;
+}
+
 extern "C" dgnn_status dgnn_assemble_group(dgnn_ctx* c, const uint32_t* addr, const int64_t* node_off, int64_t nb,
                                            int64_t n, const void* gpu_tier, int64_t k_gpu, const void* host_tier,
-                                           int64_t k_host, const void* chunk_base, const int64_t* chunk_off,
-                                           const int64_t* chunk_rows, int64_t row_bytes, void* out) {
+                                           int64_t k_host, const int32_t* host_map, const void* chunk_base,
+                                           const int64_t* chunk_off, const int64_t* chunk_rows, int64_t row_bytes,
+                                           void* out) {
     DGNN_REQUIRE(c && (n == 0 || (addr && out && node_off && chunk_off && chunk_rows)),
                  "dgnn_assemble_group: NULL argument");
     DGNN_REQUIRE(row_bytes > 0 && row_bytes % 4 == 0 && n >= 0 && nb >= 0 && nb < (1 << 30) && k_gpu >= 0 &&
@@ -157,9 +255,9 @@ extern "C" dgnn_status dgnn_assemble_group(dgnn_ctx* c, const uint32_t* addr, co
     if (n == 0 || nb == 0) return DGNN_OK;
     DGNN_CK(cudaSetDevice(c->device));
     const bool v16 = row_bytes % 16 == 0 && al16(gpu_tier) && al16(host_tier) && al16(chunk_base) && al16(out);
-    AsmGroupRow fn{addr,    node_off, chunk_off, chunk_rows, (int)nb,  (const uint8_t*)gpu_tier, k_gpu,
-                   (const uint8_t*)host_tier, k_host, (const uint8_t*)chunk_base, row_bytes, (uint8_t*)out,
-                   c->dev_err};
+    AsmGroupRow fn{addr,     node_off, chunk_off, chunk_rows, (int)nb,   (const uint8_t*)gpu_tier, k_gpu,
+                   (const uint8_t*)host_tier, k_host, host_map, (const uint8_t*)chunk_base, row_bytes,
+                   (uint8_t*)out, c->dev_err};
     const int grid = grid_for(c, n * 32 / kAsmU, 256, c->assemble_blocks_per_sm);
     launch(c, DGNN_K_ASSEMBLE, (double)n * (2.0 * row_bytes + 4.0), [&] {
         if (v16) k_assemble_group<uint4><<<grid, 256, 0, c->stream>>>(fn, n);

@@ -128,7 +128,6 @@ dgnn_status dgnn_ctx_create(int device, void* stream, const dgnn_allocator* allo
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
         }
     }
-    for (int i = 0; i < dgnn_ctx::kStageRing; ++i) cudaEventCreateWithFlags(&c->stage_ev[i], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&c->order_ev, cudaEventDisableTiming);
     if (cudaMalloc(&c->dev_err, sizeof(int)) != cudaSuccess || cudaMemset(c->dev_err, 0, sizeof(int)) != cudaSuccess) {
         dgnn_ctx_destroy(c);
@@ -231,7 +230,9 @@ dgnn_status dgnn_stage_copy(dgnn_ctx* c, void* dst, const void* src, int64_t byt
                  "dgnn_stage_copy: bad argument");
     DGNN_CK(cudaSetDevice(c->device));
     const int64_t t = c->stage_next++;
-    cudaEvent_t ev = c->stage_ev[t % dgnn_ctx::kStageRing];
+    cudaEvent_t& slot = c->stage_ev[t % dgnn_ctx::kStageRing];
+    if (!slot) DGNN_CK(cudaEventCreateWithFlags(&slot, cudaEventDisableTiming));
+    cudaEvent_t ev = slot;
     if (t >= dgnn_ctx::kStageRing) DGNN_CK(cudaEventSynchronize(ev));  // slot reuse: the older copy must be done
     // order after everything already on the ctx stream
     DGNN_CK(cudaEventRecord(c->order_ev, c->stream));

@@ -40,7 +40,7 @@ struct dgnn_ctx {
     double stat_bytes[DGNN_K_NUM] = {};
     int64_t stat_n[DGNN_K_NUM] = {};
     // staging tickets (a8)
-    static constexpr int kStageRing = 256;
+    static constexpr int kStageRing = 8192;
     cudaEvent_t stage_ev[kStageRing] = {};
     int64_t stage_next = 0;
     cudaEvent_t order_ev = nullptr;
@@ -242,23 +242,26 @@ __global__ void __launch_bounds__(kThreads) scan_kernel(const int64_t* n_dev, in
         const int64_t tile = s_tile;
         if (tile >= ntiles) break;
         const int64_t base = tile * kTile + (int64_t)warp * (32 * kItems);
-        int64_t val[kItems], incl[kItems];
-        int64_t run = 0;
+        // V = the input's value type: int32 inputs keep the per-warp arrays in 32-bit
+        // registers (the warp covers 256 items, so int32 sums cannot overflow for them)
+        using V = decltype(in(int64_t(0)));
+        V val[kItems], incl[kItems];
+        V run = 0;
 #pragma unroll
         for (int i = 0; i < kItems; ++i) {
             const int64_t idx = base + i * 32 + lane;
-            const int64_t x = idx < n ? (int64_t)in(idx) : 0;
-            int64_t s = x;
+            const V x = idx < n ? in(idx) : V(0);
+            V s = x;
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
-                const int64_t y = __shfl_up_sync(0xffffffffu, s, d);
+                const V y = __shfl_up_sync(0xffffffffu, s, d);
                 if (lane >= d) s += y;
             }
             val[i] = x;
             incl[i] = run + s;
             run += __shfl_sync(0xffffffffu, s, 31);
         }
-        if (lane == 0) s_warp[warp] = run;
+        if (lane == 0) s_warp[warp] = (int64_t)run;
         __syncthreads();
         int64_t warp_excl = 0, block_total = 0;
 #pragma unroll
@@ -303,7 +306,7 @@ __global__ void __launch_bounds__(kThreads) scan_kernel(const int64_t* n_dev, in
 #pragma unroll
         for (int i = 0; i < kItems; ++i) {
             const int64_t idx = base + i * 32 + lane;
-            if (idx < n) out(idx, pre + incl[i] - val[i], val[i]);
+            if (idx < n) out(idx, pre + (int64_t)(incl[i] - val[i]), (int64_t)val[i]);
         }
         __syncthreads();
     }

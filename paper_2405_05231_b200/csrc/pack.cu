@@ -125,8 +125,8 @@ extern "C" dgnn_status dgnn_classify(dgnn_ctx* c, const dgnn_cache_plan* plan, c
         const int64_t* seg = S->node_off + b_lo;  // absolute offsets of batches b_lo..b_hi
         const uint32_t* tm = plan->tier_map;
         const int nseg = (int)nbg;
-        auto in = [=] __device__(int64_t i) -> int64_t {
-            return (int64_t)((tm[nodes[i]] >> DGNN_TIER_SHIFT) == DGNN_TIER_DISK);
+        auto in = [=] __device__(int64_t i) -> int32_t {
+            return (int32_t)((tm[nodes[i]] >> DGNN_TIER_SHIFT) == DGNN_TIER_DISK);
         };
         // pass 1: compaction of the DISK nodes (P_b concatenated), batch starts,
         // global packed index parked in addr

@@ -171,7 +171,7 @@ struct DegIn {
     const int64_t* indptr;
     int k;
     int* err;
-    __device__ __forceinline__ int64_t operator()(int64_t t) const {
+    __device__ __forceinline__ int32_t operator()(int64_t t) const {
         const int s = segment_of(g.fr_off, g.G + 1, t);
         const int64_t j = g.fr_lo[s] + (t - g.fr_off[s]);
         const int32_t v = g.nodes[(int64_t)s * g.cap_n + j];
@@ -181,7 +181,7 @@ struct DegIn {
         g.fst[t] = start;
         if (d >= (int64_t)INT32_MAX) atomicOr(err, DEVERR_OVERFLOW);
         g.fdg[t] = (int32_t)d;
-        return d < k ? d : k;
+        return (int32_t)(d < k ? d : k);
     }
 };
 
@@ -707,7 +707,7 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
                     const int32_t* hist = d_hist.p;
                     int64_t* bst = d_bstart.p;
                     DGNN_TRY(scan::run(
-                        c, nbk, nullptr, [=] __device__(int64_t i) -> int64_t { return hist[i]; },
+                        c, nbk, nullptr, [=] __device__(int64_t i) -> int32_t { return hist[i]; },
                         [=] __device__(int64_t i, int64_t e, int64_t) { bst[i] = e; }, new_total));
                 }
                 launch(c, DGNN_K_SAMPLE_SETUP, 0.0,

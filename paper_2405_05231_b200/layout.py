@@ -114,6 +114,7 @@ class Layout:
     groups: list = field(default_factory=list)
     batch_chunk: np.ndarray = None  # [nb, 2]: (arena byte offset, packed rows)
     stats: dict = field(default_factory=dict)
+    _asm_plans: dict = field(default_factory=dict)
 
     @property
     def num_batches(self) -> int:
@@ -156,19 +157,17 @@ class Layout:
             b0 = b1
         return groups
 
-    def assemble_epoch(self, ctx: A.Ctx | None = None, out_budget: int = 1 << 30):
-        """Pipelined assembly (P:465-470): the chunks of the next run of batches are staged H2D
-        on the side stream while the current run is assembled on the ctx stream (one
-        dgnn_assemble_group launch per run).  Yields (b, features[n_b, dim]) per batch; a
-        yielded view stays valid until two runs later."""
-        ctx = ctx or self.ctx
+    def assembly_plan(self, out_budget: int = 1 << 30):
+        """Per-run device tables (node offsets, chunk byte offsets, packed-row prefix, all
+        relative to the run), built once on the layout's stream and cached."""
+        key = int(out_budget)
+        plan = self._asm_plans.get(key)
+        if plan is not None:
+            return plan
         nb = self.num_batches
-        if nb == 0:
-            return
         groups = self.assembly_groups(out_budget)
         no = self.samples.node_off_host
         rows_pre = np.concatenate([[0], np.cumsum(self.batch_chunk[:, 1])])
-        # per-run device tables: node offsets, chunk byte offsets, packed-row prefix (relative to the run)
         tabs, spans = [], []
         for (b0, b1) in groups:
             c_lo = int(self.batch_chunk[b0, 0])
@@ -177,16 +176,57 @@ class Layout:
             chunk_off = np.concatenate([self.batch_chunk[b0:b1, 0] - c_lo, [c_hi - c_lo]])
             tabs.append(np.concatenate([no[b0:b1 + 1] - no[b0], chunk_off, rows_pre[b0:b1 + 1] - rows_pre[b0]]))
             spans.append((int(no[b0]), int(no[b1]), c_lo, c_hi))
+        with torch.cuda.stream(self.ctx.stream):
+            flat = torch.from_numpy(np.concatenate(tabs).astype(np.int64)).to(self.ctx.device, non_blocking=False)
+        offs = np.concatenate([[0], np.cumsum([len(t) for t in tabs])])
+        plan = (groups, spans, flat, offs)
+        self._asm_plans[key] = plan
+        return plan
+
+    def assemble_epoch(self, ctx: A.Ctx | None = None, out_budget: int = 1 << 30, host_window: int = 128):
+        """Pipelined assembly (P:465-470): the chunks of the next run of batches are staged H2D
+        on the side stream while the current run is assembled on the ctx stream (one
+        dgnn_assemble_group launch per run).  Yields (b, features[n_b, dim]) per batch; a
+        yielded view stays valid until two runs later.  Enqueueing never blocks the host.
+
+        ``host_window`` > 1 merges host-tier reads over windows of that many batches
+        (dgnn_host_window): each CPU-cache row crosses PCIe once per window into an HBM
+        staging buffer instead of once per batch.  ``host_window=1`` is the
+        paper's per-batch UVA read of the CPU cache.  The outputs are identical."""
+        ctx = ctx or self.ctx
+        nb = self.num_batches
+        if nb == 0:
+            return
+        groups, spans, flat, offs = self.assembly_plan(out_budget)
+        if ctx is not self.ctx:
+            ctx.stream.wait_stream(self.ctx.stream)  # tables were uploaded on the layout's stream
+        no = self.samples.node_off_host
         dev = ctx.device
+        kh = self.plan.k_host
+        windows = []  # (first run, last run + 1)
+        if host_window > 1 and kh > 0:
+            r0 = 0
+            while r0 < len(groups):
+                r1 = r0 + 1
+                while r1 < len(groups) and groups[r1 - 1][1] - groups[r0][0] < host_window:
+                    r1 += 1
+                windows.append((r0, r1))
+                r0 = r1
         with torch.cuda.stream(ctx.stream):
-            flat = torch.from_numpy(np.concatenate(tabs).astype(np.int64)).to(dev, non_blocking=False)
             max_rows = max(s[1] - s[0] for s in spans)
             max_c = max(s[3] - s[2] for s in spans)
             out_ring = [torch.empty((max_rows, self.dim), dtype=self.dtype, device=dev) for _ in range(2)]
             staged = self.arena is not None
             chunk_ring = [torch.empty(max(max_c, 16), dtype=torch.uint8, device=dev) for _ in range(2)] \
                 if staged else None
-        offs = np.concatenate([[0], np.cumsum([len(t) for t in tabs])])
+            if windows:
+                cap = min(kh, max(spans[r1 - 1][1] - spans[r0][0] for r0, r1 in windows))
+                stamp = torch.full((kh,), -1, dtype=torch.int32, device=dev)
+                smap = torch.empty(kh, dtype=torch.int32, device=dev)
+                wlist = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+                wcount = torch.zeros(1, dtype=torch.int64, device=dev)
+                staging = torch.empty(max(cap, 1) * self.row_bytes, dtype=torch.uint8, device=dev)
+        run_window = {r0: wi for wi, (r0, _) in enumerate(windows)}
         tickets = {}
 
         def stage(i):
@@ -204,12 +244,21 @@ class Layout:
                 chunk = chunk_ring[i % 2]
             else:
                 chunk = self.arena_dev.data_ptr() + c_lo
+            if i in run_window:  # first run of a host window: list its host rows once, stage them
+                w0, w1 = windows[run_window[i]]
+                A.dgnn_host_window(ctx, self.addr[spans[w0][0]:spans[w1 - 1][1]], run_window[i], stamp, kh, wlist,
+                                   smap, wcount)
+                A.dgnn_gather_rows_dev(ctx, self.host_tier.ptr, kh, self.row_bytes, wlist, wcount, staging)
             k = b1 - b0
             t = flat[int(offs[i]):int(offs[i + 1])]
             out = out_ring[i % 2]
+            if windows:
+                host_src, host_map = staging, smap
+            else:
+                host_src, host_map = self.host_tier.ptr, None
             A.dgnn_assemble_group(ctx, self.addr[n0:n1], t[:k + 1], n1 - n0, self.gpu_tier, self.plan.k_gpu,
-                                  self.host_tier.ptr, self.plan.k_host, chunk, t[k + 1:2 * k + 2], t[2 * k + 2:],
-                                  self.row_bytes, out)
+                                  host_src, kh, chunk, t[k + 1:2 * k + 2], t[2 * k + 2:], self.row_bytes, out,
+                                  host_map=host_map)
             for b in range(b0, b1):
                 yield b, out[int(no[b] - n0):int(no[b + 1] - n0)]
 
@@ -309,5 +358,8 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
                  packed_bytes=int(po[-1]) * row_bytes, arena_bytes=arena_off,
                  k_gpu=plan.k_gpu, k_host=plan.k_host, total_nodes=total_nodes, total_edges=samples.total_edges)
     del packed_ids
-    return Layout(ctx, samples, plan, counts, row_bytes, dim, features.dtype, addr, gpu_tier, host_tier, arena,
-                  arena_dev, groups, batch_chunk, stats)
+    L = Layout(ctx, samples, plan, counts, row_bytes, dim, features.dtype, addr, gpu_tier, host_tier, arena,
+               arena_dev, groups, batch_chunk, stats)
+    if nb:
+        L.assembly_plan()  # a9's per-run tables, uploaded here on the layout's stream
+    return L

@@ -162,7 +162,7 @@ def test_fig3_address_table(dg, ctx):
     assert plan.gpu_ids.cpu().tolist() == [4, 7] and plan.host_ids.cpu().tolist() == [1, 9]
 
 
-def _layout_parity(dg, ctx, w, fan, B, gpu_rows, host_rows, group, stage):
+def _layout_parity(dg, ctx, w, fan, B, gpu_rows, host_rows, group, stage, host_window=64, out_budget=1 << 30):
     ip, ix, sd = w.indptr.numpy(), w.indices.numpy(), w.seeds.numpy()
     feats = w.features.numpy()
     ref = oracle.offline_layout(ip, ix, feats, sd, B, fan, RNG_SEED, gpu_rows, host_rows, group, threads=8)
@@ -191,7 +191,7 @@ def _layout_parity(dg, ctx, w, fan, B, gpu_rows, host_rows, group, stage):
         assert np.array_equal(arena[g.arena_off:g.arena_off + g.group_bytes], buf)
     # a9: assembled == direct gather
     seen = 0
-    for b, out in L.assemble_epoch():
+    for b, out in L.assemble_epoch(host_window=host_window, out_budget=out_budget):
         exp = oracle.assemble(feats, ref["samples"][b].nodes)
         got = out.view(torch.uint8).reshape(out.shape[0], -1).cpu().numpy()
         assert np.array_equal(got, exp), f"assemble batch {b}"
@@ -203,6 +203,13 @@ def _layout_parity(dg, ctx, w, fan, B, gpu_rows, host_rows, group, stage):
 
 def test_offline_layout_parity_tiny(dg, ctx, tiny):
     _layout_parity(dg, ctx, tiny, [10, 5], 256, 500, 1000, 8, "pinned")
+
+
+@pytest.mark.parametrize("host_window,out_budget", [(1, 1 << 30), (2, 1 << 20), (3, 600_000), (1000, 1 << 20)])
+def test_assembly_windows_and_runs(dg, ctx, tiny, host_window, out_budget):
+    """a9 variants: per-batch UVA host reads (window 1), merged host windows of 2-3 runs,
+    one window for the epoch; runs of 1-2 batches (small out_budget)."""
+    _layout_parity(dg, ctx, tiny, [10, 5], 256, 500, 1000, 8, "pinned", host_window, out_budget)
 
 
 def test_offline_layout_parity_hbm_stage_and_odd_rows(dg, ctx):
