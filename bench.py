@@ -187,10 +187,12 @@ class Runner:
         self.sA = torch.cuda.Stream(dev)
         # the PCIe-bound assembly gets the higher stream priority: its CTAs are scheduled
         # first and the layout of the next pass fills the remaining SM capacity
-        self.sB = torch.cuda.Stream(dev, priority=-1) if pipelined else self.sA
+        # (sequential mode still assembles on its own stream: the stage-out of a pass overlaps
+        # the start of its assembly; only the next pass waits for the assembly to finish)
+        self.sB = torch.cuda.Stream(dev, priority=-1 if pipelined else 0)
         torch.cuda.set_stream(self.sA)
         self.ctxA = dg.Ctx(device=dev, stream=self.sA)
-        self.ctxB = dg.Ctx(device=dev, stream=self.sB) if pipelined else self.ctxA
+        self.ctxB = dg.Ctx(device=dev, stream=self.sB)
         if pipelined:
             self.ctxB.set_assemble_occupancy(int(os.environ.get("DGNN_ASM_OCC", "2")))  # PCIe-bound: leave SMs
         N = inp[1].numel() - 1
@@ -200,9 +202,14 @@ class Runner:
         self.nb = (inp[3].numel() + cfg["batch_size"] - 1) // cfg["batch_size"]
         self.before_layout = None  # hook: e.g. the e2e H2D copies of the inputs
         self.host_window = 128
+        # a9's host-row window gathers (PCIe) run on their own stream, overlapping the
+        # HBM-bound assembly runs of the previous window
+        self.sG = torch.cuda.Stream(dev)
+        self.ctxG = dg.Ctx(device=dev, stream=self.sG)
+        self.ctxG.set_assemble_occupancy(2)
 
     def ctxs(self):
-        return [self.ctxA] if self.ctxB is self.ctxA else [self.ctxA, self.ctxB]
+        return [self.ctxA, self.ctxB, self.ctxG]
 
     def layout(self, slot):
         cfg, indptr, indices, seeds, feats, gpu_rows, host_rows = self.inp
@@ -212,7 +219,8 @@ class Runner:
         c.zero_()
         return self.dg.offline_layout(self.ctxA, indptr, indices, feats, seeds, cfg["fanout"], cfg["batch_size"],
                                       gpu_rows, host_rows, RNG_SEED, group_size=cfg["group_size"],
-                                      batch_id_base=self.rank * self.nb, counts=c, ws=self.ws[slot])
+                                      batch_id_base=self.rank * self.nb, counts=c, ws=self.ws[slot],
+                                      stage_piece=int(os.environ.get("DGNN_STAGE_PIECE", str(256 << 20))))
 
     def run(self, K: int, keep_last=False):
         """Enqueue K passes; returns the last Layout if keep_last."""
@@ -223,13 +231,16 @@ class Runner:
         last = None
         for e in range(K):
             self.sB.wait_event(ev_l)
-            for _ in L.assemble_epoch(ctx=self.ctxB, host_window=self.host_window):
+            gctx = self.ctxG if os.environ.get("DGNN_GATHER_STREAM", "1") == "1" else None
+            for _ in L.assemble_epoch(ctx=self.ctxB, host_window=self.host_window, gather_ctx=gctx):
                 pass
             ev_a = torch.cuda.Event()
             ev_a.record(self.sB)
             Ln = None
             if e + 1 < K:
-                if prev_ev is not None:
+                if not self.pipelined:
+                    self.sA.wait_event(ev_a)  # sequential: the next pass starts after this assembly
+                elif prev_ev is not None:
                     self.sA.wait_event(prev_ev)  # slot (e+1)%2 was pass e-1's: its assembly must be done
                 Ln = self.layout((e + 1) % 2)
                 ev_l = torch.cuda.Event()
@@ -278,7 +289,9 @@ def main():
     ap.add_argument("--cpu-batches", type=int, default=32)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--sequential", action="store_true", help="no epoch pipelining (one stream)")
+    ap.add_argument("--pipelined", action="store_true",
+                    help="overlap the layout of pass e+1 with the assembly of pass e on two streams "
+                         "(measured slower on one B200: both halves contend for PCIe and HBM)")
     ap.add_argument("--host-window", type=int, default=128,
                     help="batches per host-row merging window in a9 (1 = per-batch UVA reads, the paper's)")
     args = ap.parse_args()
@@ -292,13 +305,14 @@ def main():
     cfg, indptr, indices, seeds, feats, gpu_rows, host_rows = inp
     N = indptr.numel() - 1
     nb = (seeds.numel() + cfg["batch_size"] - 1) // cfg["batch_size"]
-    R = Runner(dg, inp, rank, dev, pipelined=not args.sequential)
+    R = Runner(dg, inp, rank, dev, pipelined=args.pipelined)
     R.host_window = args.host_window
     t = time.time()
     L = R.run(1, keep_last=True)
     torch.cuda.synchronize()
-    stats0 = dict(L.stats)
+    stats0 = {k: v for k, v in L.stats.items() if not k.startswith("_")}
     stats0.update(L.tier_mix())
+    stats0["layout_phase_ms_first_pass"] = {k: round(v, 2) for k, v in L.phase_ms().items()}
     del L
     log(f"[bench] first pass {time.time() - t:.1f}s stats={stats0}")
     # the remaining warm-up passes; at least 2 so that both double-buffer slots are allocated
@@ -360,7 +374,7 @@ def main():
                    "host_rows": host_rows, "group_size": cfg["group_size"], "disk_tier": "pinned host arena",
                    "parallelism": f"dp{ws} (batch-sharded, count all-reduce)",
                    "host_window_batches": args.host_window,
-                   "schedule": "sequential" if args.sequential else
+                   "schedule": "sequential" if not args.pipelined else
                    "pipelined: layout of pass e+1 overlaps assembly of pass e (2 streams)",
                    "l2": "inputs larger than L2 (features %.1f GB, CSR %.1f GB); no flush needed" % (
                        feats.numel() * 4 / 1e9, (indptr.numel() * 8 + indices.numel() * 4) / 1e9)},

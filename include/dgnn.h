@@ -100,8 +100,8 @@ typedef struct {
 
 /* ------------------------------------------------------------------ context ---- */
 /* Create a context on CUDA device `device` enqueuing on `stream` (a cudaStream_t;
- * NULL = the context creates its own non-blocking stream).  A second, internal side
- * stream carries staging copies (a8).  One ctx per host thread. */
+ * NULL = the legacy default stream).  A second, internal side stream carries staging
+ * copies (a8).  One ctx per host thread. */
 dgnn_status dgnn_ctx_create(int device, void* stream, const dgnn_allocator* allocator, dgnn_ctx** out);
 void dgnn_ctx_destroy(dgnn_ctx* ctx);
 dgnn_status dgnn_ctx_set_stream(dgnn_ctx* ctx, void* stream);
@@ -255,6 +255,9 @@ dgnn_status dgnn_gather_rows(dgnn_ctx* ctx, const void* features, int64_t num_ro
 dgnn_status dgnn_stage_copy(dgnn_ctx* ctx, void* dst, const void* src, int64_t bytes, int32_t kind,
                             int64_t* ticket);
 dgnn_status dgnn_stage_wait(dgnn_ctx* ctx, int64_t ticket);
+/* Make another stream (a cudaStream_t; NULL = legacy default) wait for a staging copy, e.g.
+ * the assembler's stream waiting for a packing group's stage-out. */
+dgnn_status dgnn_stage_wait_stream(dgnn_ctx* ctx, int64_t ticket, void* stream);
 dgnn_status dgnn_stage_sync(dgnn_ctx* ctx, int64_t ticket);
 /* Pinned, device-mapped host memory for the host tier and the disk-tier arena. */
 dgnn_status dgnn_host_alloc(int64_t bytes, void** out);

@@ -38,7 +38,7 @@ EXPORTS = [
     "dgnn_samples_free", "dgnn_build_cache", "dgnn_cache_plan_get_info", "dgnn_cache_plan_free", "dgnn_classify",
     "dgnn_chunk_layout", "dgnn_pack", "dgnn_gather_rows", "dgnn_stage_copy", "dgnn_stage_wait", "dgnn_stage_sync",
     "dgnn_host_alloc", "dgnn_host_free", "dgnn_assemble", "dgnn_assemble_group", "dgnn_ctx_set_assemble_occupancy",
-    "dgnn_host_window", "dgnn_gather_rows_dev",
+    "dgnn_host_window", "dgnn_gather_rows_dev", "dgnn_stage_wait_stream",
 ]
 
 
@@ -117,6 +117,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "dgnn_gather_rows": (i32, [P, P, i64, i64, P, i64, P]),
             "dgnn_stage_copy": (i32, [P, P, P, i64, i32, ctypes.POINTER(i64)]),
             "dgnn_stage_wait": (i32, [P, i64]),
+            "dgnn_stage_wait_stream": (i32, [P, i64, P]),
             "dgnn_stage_sync": (i32, [P, i64]),
             "dgnn_host_alloc": (i32, [i64, ctypes.POINTER(P)]),
             "dgnn_host_free": (i32, [P]),
@@ -395,6 +396,11 @@ def dgnn_stage_copy(ctx: Ctx, dst, src, nbytes: int, kind: int) -> int:
 
 def dgnn_stage_wait(ctx: Ctx, ticket: int):
     _check(load_library().dgnn_stage_wait(ctx.handle, int(ticket)), "dgnn_stage_wait")
+
+
+def dgnn_stage_wait_stream(ctx: Ctx, ticket: int, stream: torch.cuda.Stream):
+    _check(load_library().dgnn_stage_wait_stream(ctx.handle, int(ticket), P(stream.cuda_stream)),
+           "dgnn_stage_wait_stream")
 
 
 def dgnn_stage_sync(ctx: Ctx, ticket: int):

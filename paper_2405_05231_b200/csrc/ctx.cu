@@ -103,16 +103,9 @@ dgnn_status dgnn_ctx_create(int device, void* stream, const dgnn_allocator* allo
     auto* c = new dgnn_ctx();
     c->device = device;
     cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
-    if (stream) {
-        c->stream = (cudaStream_t)stream;
-    } else {
-        if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
-            delete c;
-            set_error("cudaStreamCreate failed");
-            return DGNN_ECUDA;
-        }
-        c->own_stream = true;
-    }
+    // NULL = the legacy default stream (what frameworks call "the default stream"), so
+    // work enqueued by the caller on it is ordered with the library's kernels
+    c->stream = stream ? (cudaStream_t)stream : cudaStreamLegacy;
     if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess) {
         delete c;
         set_error("cudaStreamCreate (side) failed");
@@ -248,6 +241,14 @@ dgnn_status dgnn_stage_wait(dgnn_ctx* c, int64_t ticket) {
     DGNN_REQUIRE(c && ticket >= 0 && ticket < c->stage_next, "dgnn_stage_wait: bad ticket");
     if (c->stage_next - ticket > dgnn_ctx::kStageRing) return DGNN_OK;  // long since complete (slot was reused)
     DGNN_CK(cudaStreamWaitEvent(c->stream, c->stage_ev[ticket % dgnn_ctx::kStageRing], 0));
+    return DGNN_OK;
+}
+
+dgnn_status dgnn_stage_wait_stream(dgnn_ctx* c, int64_t ticket, void* stream) {
+    DGNN_REQUIRE(c && ticket >= 0 && ticket < c->stage_next, "dgnn_stage_wait_stream: bad ticket");
+    if (c->stage_next - ticket > dgnn_ctx::kStageRing) return DGNN_OK;
+    DGNN_CK(cudaStreamWaitEvent(stream ? (cudaStream_t)stream : cudaStreamLegacy,
+                                c->stage_ev[ticket % dgnn_ctx::kStageRing], 0));
     return DGNN_OK;
 }
 

@@ -115,6 +115,22 @@ class Layout:
     batch_chunk: np.ndarray = None  # [nb, 2]: (arena byte offset, packed rows)
     stats: dict = field(default_factory=dict)
     _asm_plans: dict = field(default_factory=dict)
+    stage_pieces: list = field(default_factory=list)  # (b_lo, b_hi, ticket) of each stage-out copy
+
+    def phase_ms(self) -> dict:
+        """Device time of the layout's phases (after the stream has passed them)."""
+        ev = self.stats.get("_events", [])
+        return {ev[i][0]: ev[i - 1][1].elapsed_time(ev[i][1]) for i in range(1, len(ev))}
+
+    def wait_chunks(self, stream, b_hi: int, _done=None):
+        """Make ``stream`` wait for the stage-out copies holding batches < b_hi."""
+        for pi, (b_lo, _, ticket) in enumerate(self.stage_pieces):
+            if b_lo >= b_hi:
+                break
+            if _done is None or pi not in _done:
+                A.dgnn_stage_wait_stream(self.ctx, ticket, stream)
+                if _done is not None:
+                    _done.add(pi)
 
     @property
     def num_batches(self) -> int:
@@ -183,7 +199,8 @@ class Layout:
         self._asm_plans[key] = plan
         return plan
 
-    def assemble_epoch(self, ctx: A.Ctx | None = None, out_budget: int = 1 << 30, host_window: int = 128):
+    def assemble_epoch(self, ctx: A.Ctx | None = None, out_budget: int = 1 << 30, host_window: int = 128,
+                       gather_ctx: A.Ctx | None = None):
         """Pipelined assembly: the chunks of the next run of batches are staged H2D
         on the side stream while the current run is assembled on the ctx stream (one
         dgnn_assemble_group launch per run).  Yields (b, features[n_b, dim]) per batch; a
@@ -192,8 +209,11 @@ class Layout:
         ``host_window`` > 1 merges host-tier reads over windows of that many batches
         (dgnn_host_window): each CPU-cache row crosses PCIe once per window into an HBM
         staging buffer instead of once per batch.  ``host_window=1`` is the
-        paper's per-batch UVA read of the CPU cache.  The outputs are identical."""
+        paper's per-batch UVA read of the CPU cache.  The outputs are identical.  With a
+        ``gather_ctx`` (a ctx on another stream) the next window's PCIe gather runs there,
+        double-buffered, overlapping the current window's HBM-bound runs."""
         ctx = ctx or self.ctx
+        gctx = gather_ctx or ctx
         nb = self.num_batches
         if nb == 0:
             return
@@ -222,15 +242,38 @@ class Layout:
             if windows:
                 cap = min(kh, max(spans[r1 - 1][1] - spans[r0][0] for r0, r1 in windows))
                 stamp = torch.full((kh,), -1, dtype=torch.int32, device=dev)
-                smap = torch.empty(kh, dtype=torch.int32, device=dev)
-                wlist = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
-                wcount = torch.zeros(1, dtype=torch.int64, device=dev)
-                staging = torch.empty(max(cap, 1) * self.row_bytes, dtype=torch.uint8, device=dev)
+                nbuf = 2 if gctx is not ctx else 1
+                smap = [torch.empty(kh, dtype=torch.int32, device=dev) for _ in range(nbuf)]
+                wlist = [torch.empty(max(cap, 1), dtype=torch.int32, device=dev) for _ in range(nbuf)]
+                wcount = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(nbuf)]
+                staging = [torch.empty(max(cap, 1) * self.row_bytes, dtype=torch.uint8, device=dev)
+                           for _ in range(nbuf)]
+        if gctx is not ctx:
+            gctx.stream.wait_stream(ctx.stream)  # stamp / buffers were created on the ctx stream
         run_window = {r0: wi for wi, (r0, _) in enumerate(windows)}
+        last_run = {r1 - 1: wi for wi, (_, r1) in enumerate(windows)}
+        ev_ready, ev_done = {}, {}
+
+        def prefetch(w):
+            # window w's distinct host rows -> staging[w % nbuf] (PCIe), on the gather stream
+            s = w % nbuf
+            if w >= nbuf and gctx is not ctx:
+                gctx.stream.wait_event(ev_done[w - nbuf])  # the runs that used this buffer are done
+            w0, w1 = windows[w]
+            A.dgnn_host_window(gctx, self.addr[spans[w0][0]:spans[w1 - 1][1]], w, stamp, kh, wlist[s], smap[s],
+                               wcount[s])
+            A.dgnn_gather_rows_dev(gctx, self.host_tier.ptr, kh, self.row_bytes, wlist[s], wcount[s], staging[s])
+            ev = torch.cuda.Event()
+            ev.record(gctx.stream)
+            ev_ready[w] = ev
+
         tickets = {}
+
+        waited = set()
 
         def stage(i):
             n0, n1, c_lo, c_hi = spans[i]
+            self.wait_chunks(ctx.stream, groups[i][1], waited)  # the run's chunks have been staged out
             tickets[i] = A.dgnn_stage_copy(ctx, chunk_ring[i % 2], self.arena.ptr + c_lo, c_hi - c_lo, 1)
 
         if staged:
@@ -244,21 +287,29 @@ class Layout:
                 chunk = chunk_ring[i % 2]
             else:
                 chunk = self.arena_dev.data_ptr() + c_lo
-            if i in run_window:  # first run of a host window: list its host rows once, stage them
-                w0, w1 = windows[run_window[i]]
-                A.dgnn_host_window(ctx, self.addr[spans[w0][0]:spans[w1 - 1][1]], run_window[i], stamp, kh, wlist,
-                                   smap, wcount)
-                A.dgnn_gather_rows_dev(ctx, self.host_tier.ptr, kh, self.row_bytes, wlist, wcount, staging)
+            if i in run_window:  # first run of a host window: its host rows must be staged
+                w = run_window[i]
+                if w not in ev_ready:
+                    prefetch(w)
+                if gctx is not ctx:
+                    ctx.stream.wait_event(ev_ready[w])
+                    if w + 1 < len(windows):
+                        prefetch(w + 1)  # overlaps this window's (HBM-bound) runs
+                cur = w % nbuf
             k = b1 - b0
             t = flat[int(offs[i]):int(offs[i + 1])]
             out = out_ring[i % 2]
             if windows:
-                host_src, host_map = staging, smap
+                host_src, host_map = staging[cur], smap[cur]
             else:
                 host_src, host_map = self.host_tier.ptr, None
             A.dgnn_assemble_group(ctx, self.addr[n0:n1], t[:k + 1], n1 - n0, self.gpu_tier, self.plan.k_gpu,
                                   host_src, kh, chunk, t[k + 1:2 * k + 2], t[2 * k + 2:], self.row_bytes, out,
                                   host_map=host_map)
+            if i in last_run:
+                ev = torch.cuda.Event()
+                ev.record(ctx.stream)
+                ev_done[last_run[i]] = ev
             for b in range(b0, b1):
                 yield b, out[int(no[b] - n0):int(no[b + 1] - n0)]
 
@@ -267,7 +318,7 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
                    seeds: torch.Tensor, fanout, batch_size: int, gpu_rows: int, host_rows: int, rng_seed: int,
                    group_size: int = 64, batch_id_base: int = 0, stage: str = "pinned",
                    counts: torch.Tensor | None = None, ws: Workspace | None = None,
-                   group_budget: int = 4 << 30) -> Layout:
+                   group_budget: int = 4 << 30, stage_piece: int = 256 << 20) -> Layout:
     """Run a1-a8 on this rank's batches.
 
     ``seeds`` are this rank's seeds (batch t of them gets bid = batch_id_base + t).
@@ -279,11 +330,19 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
     N = indptr.numel() - 1
     row_bytes = features.element_size() * (features.numel() // max(features.shape[0], 1))
     dim = features.numel() // max(features.shape[0], 1)
-    stats = {}
+    stats = {"_events": []}
+
+    def mark(name):  # phase boundaries on the layout's stream (measurement only)
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(ctx.stream)
+        stats["_events"].append((name, e))
+
+    mark("start")
     if counts is None:
         counts = torch.zeros(N, dtype=torch.int32, device=dev)
     # a1-a3 (+ the fused access counter)
     samples = A.dgnn_sample(ctx, indptr, indices, seeds, batch_size, fanout, rng_seed, batch_id_base, counts)
+    mark("sample")
     # a4: global histogram across ranks
     d = _dist()
     if d is not None:
@@ -291,12 +350,14 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
             d.all_reduce(counts, op=d.ReduceOp.SUM)
     # a5
     plan = A.dgnn_build_cache(ctx, counts, gpu_rows, host_rows)
+    mark("plan")
     # tier buffers as special mini-batches
     gpu_tier = torch.empty((plan.k_gpu, row_bytes), dtype=torch.uint8, device=dev)
     A.dgnn_gather_rows(ctx, features, plan.gpu_ids, gpu_tier)
     host_tier = ws.host("host_tier", plan.k_host * row_bytes) if ws is not None else \
         HostBuffer(plan.k_host * row_bytes)
     A.dgnn_gather_rows(ctx, features, plan.host_ids, host_tier.ptr)
+    mark("tiers")
     # a6 for every batch of this rank at once
     nb = samples.num_batches
     total_nodes = samples.total_nodes
@@ -331,35 +392,53 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
         arena_dev = torch.empty(max(arena_off, 16), dtype=torch.uint8, device=dev)
     else:
         raise ValueError(stage)
-    # a7 pack + a8 stage-out, double-buffered group buffers
-    max_gb = max([g.group_bytes for g in groups], default=0)
-    bufs = [torch.empty(max(max_gb, 16), dtype=torch.uint8, device=dev) for _ in range(2)] if arena is not None else []
-    tickets = [None, None]
-    for gi, g in enumerate(groups):
-        rel = torch.from_numpy(np.concatenate([po[g.b_lo:g.b_hi + 1] - po[g.b_lo], g.chunk_off])).to(dev,
-                                                                                                     non_blocking=False)
-        rel_po, rel_co = rel[:g.b_hi - g.b_lo + 1], rel[g.b_hi - g.b_lo + 1:]
-        ids = packed_ids[int(po[g.b_lo]):int(po[g.b_hi])]
-        total = int(po[g.b_hi] - po[g.b_lo])
-        if arena is not None:
-            slot = gi % 2
-            if tickets[slot] is not None:
-                A.dgnn_stage_wait(ctx, tickets[slot])
-            dst = bufs[slot]
-            A.dgnn_pack(ctx, features, ids, rel_po, rel_co, total, g.group_bytes, dst)
-            tickets[slot] = A.dgnn_stage_copy(ctx, arena.ptr + g.arena_off, dst, g.group_bytes, 0)
-        else:
-            dst = arena_dev[g.arena_off:g.arena_off + max(g.group_bytes, 0)]
-            A.dgnn_pack(ctx, features, ids, rel_po, rel_co, total, g.group_bytes, dst)
-    for t in tickets:
-        if t is not None:
-            A.dgnn_stage_wait(ctx, t)
+    L = Layout(ctx, samples, plan, counts, row_bytes, dim, features.dtype, addr, gpu_tier, host_tier, arena,
+               arena_dev, groups, batch_chunk, stats)
     stats.update(row_bytes=row_bytes, groups=len(groups), packed_rows=int(po[-1]),
                  packed_bytes=int(po[-1]) * row_bytes, arena_bytes=arena_off,
                  k_gpu=plan.k_gpu, k_host=plan.k_host, total_nodes=total_nodes, total_edges=samples.total_edges)
-    del packed_ids
-    L = Layout(ctx, samples, plan, counts, row_bytes, dim, features.dtype, addr, gpu_tier, host_tier, arena,
-               arena_dev, groups, batch_chunk, stats)
     if nb:
         L.assembly_plan()  # a9's per-run tables, uploaded here on the layout's stream
+    mark("classify")
+    # a7 pack + a8 stage-out, double-buffered group buffers; every group's stage-out
+    # ticket is kept so the assembler waits for exactly the chunks it reads
+    with torch.cuda.stream(ctx.stream):
+        rel_all = torch.from_numpy(np.concatenate(
+            [np.concatenate([po[g.b_lo:g.b_hi + 1] - po[g.b_lo], g.chunk_off]) for g in groups]
+            or [np.zeros(0, np.int64)]).astype(np.int64)).to(dev, non_blocking=False)
+        max_gb = max([g.group_bytes for g in groups], default=0)
+        L._group_bufs = [torch.empty(max(max_gb, 16), dtype=torch.uint8, device=dev)
+                         for _ in range(min(2, len(groups)))] if arena is not None else []
+    bufs = L._group_bufs
+    group_last_ticket = []
+    off = 0
+    for gi, g in enumerate(groups):
+        k = g.b_hi - g.b_lo
+        rel_po, rel_co = rel_all[off:off + k + 1], rel_all[off + k + 1:off + 2 * k + 2]
+        off += 2 * k + 2
+        ids = packed_ids[int(po[g.b_lo]):int(po[g.b_hi])]
+        total = int(po[g.b_hi] - po[g.b_lo])
+        if arena is not None:
+            if gi >= 2:
+                A.dgnn_stage_wait(ctx, group_last_ticket[gi - 2])  # its buffer is being reused
+            dst = bufs[gi % 2]
+            A.dgnn_pack(ctx, features, ids, rel_po, rel_co, total, g.group_bytes, dst)
+            # stage-out in pieces of <= stage_piece bytes on batch boundaries, so the assembler
+            # can start on the first batches while the rest is still crossing PCIe
+            b = g.b_lo
+            while b < g.b_hi:
+                e = b + 1
+                while e < g.b_hi and g.chunk_off[e + 1 - g.b_lo] - g.chunk_off[b - g.b_lo] <= stage_piece:
+                    e += 1
+                lo, hi = int(g.chunk_off[b - g.b_lo]), int(g.chunk_off[e - g.b_lo])
+                t = A.dgnn_stage_copy(ctx, arena.ptr + g.arena_off + lo, dst.data_ptr() + lo, hi - lo, 0)
+                L.stage_pieces.append((b, e, t))
+                b = e
+            group_last_ticket.append(L.stage_pieces[-1][2])
+        else:
+            dst = arena_dev[g.arena_off:g.arena_off + max(g.group_bytes, 0)]
+            A.dgnn_pack(ctx, features, ids, rel_po, rel_co, total, g.group_bytes, dst)
+    mark("pack")
+    L._rel_all = rel_all
+    L._packed_ids = packed_ids  # read by the pack kernels; released with the layout
     return L

@@ -162,7 +162,8 @@ def test_fig3_address_table(dg, ctx):
     assert plan.gpu_ids.cpu().tolist() == [4, 7] and plan.host_ids.cpu().tolist() == [1, 9]
 
 
-def _layout_parity(dg, ctx, w, fan, B, gpu_rows, host_rows, group, stage, host_window=64, out_budget=1 << 30):
+def _layout_parity(dg, ctx, w, fan, B, gpu_rows, host_rows, group, stage, host_window=64, out_budget=1 << 30,
+                   gather_ctx=None):
     ip, ix, sd = w.indptr.numpy(), w.indices.numpy(), w.seeds.numpy()
     feats = w.features.numpy()
     ref = oracle.offline_layout(ip, ix, feats, sd, B, fan, RNG_SEED, gpu_rows, host_rows, group, threads=8)
@@ -191,7 +192,7 @@ def _layout_parity(dg, ctx, w, fan, B, gpu_rows, host_rows, group, stage, host_w
         assert np.array_equal(arena[g.arena_off:g.arena_off + g.group_bytes], buf)
     # a9: assembled == direct gather
     seen = 0
-    for b, out in L.assemble_epoch(host_window=host_window, out_budget=out_budget):
+    for b, out in L.assemble_epoch(host_window=host_window, out_budget=out_budget, gather_ctx=gather_ctx):
         exp = oracle.assemble(feats, ref["samples"][b].nodes)
         got = out.view(torch.uint8).reshape(out.shape[0], -1).cpu().numpy()
         assert np.array_equal(got, exp), f"assemble batch {b}"
@@ -210,6 +211,13 @@ def test_assembly_windows_and_runs(dg, ctx, tiny, host_window, out_budget):
     """a9 variants: per-batch UVA host reads (window 1), merged host windows of 2-3 runs,
     one window for the epoch; runs of 1-2 batches (small out_budget)."""
     _layout_parity(dg, ctx, tiny, [10, 5], 256, 500, 1000, 8, "pinned", host_window, out_budget)
+
+
+@pytest.mark.parametrize("host_window", [2, 3])
+def test_assembly_gather_on_second_stream(dg, ctx, tiny, host_window):
+    """Window gathers on another ctx/stream, double-buffered, overlapping the runs."""
+    g = dg.Ctx(device=0, stream=torch.cuda.Stream())
+    _layout_parity(dg, ctx, tiny, [10, 5], 256, 500, 1000, 8, "pinned", host_window, 1 << 20, gather_ctx=g)
 
 
 def test_offline_layout_parity_hbm_stage_and_odd_rows(dg, ctx):
