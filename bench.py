@@ -220,7 +220,7 @@ class Runner:
         return self.dg.offline_layout(self.ctxA, indptr, indices, feats, seeds, cfg["fanout"], cfg["batch_size"],
                                       gpu_rows, host_rows, RNG_SEED, group_size=cfg["group_size"],
                                       batch_id_base=self.rank * self.nb, counts=c, ws=self.ws[slot],
-                                      stage_piece=int(os.environ.get("DGNN_STAGE_PIECE", str(256 << 20))))
+                                      stage_piece=int(os.environ.get("DGNN_STAGE_PIECE", str(1 << 40))))
 
     def run(self, K: int, keep_last=False):
         """Enqueue K passes; returns the last Layout if keep_last."""
@@ -338,8 +338,11 @@ def main():
     launches = sum(c.launches() for c in R.ctxs()) - l0
     ms = e0.elapsed_time(e1)
     kst = {}
-    for c in R.ctxs():
-        for k, v in c.kernel_stats().items():
+    per_stream = {}
+    for name, c in zip(("layout", "assemble", "host_gather"), R.ctxs()):
+        st = c.kernel_stats()
+        per_stream[name] = round(sum(v["ms"] for v in st.values()) / args.steps, 2)
+        for k, v in st.items():
             d = kst.setdefault(k, {"launches": 0, "ms": 0.0, "bytes": 0.0})
             for f in d:
                 d[f] += v[f]
@@ -389,6 +392,7 @@ def main():
         "layout_stats": stats0,
         "clocks": clocks,
         "gpu_launches": int(launches),
+        "kernel_ms_per_step_by_stream": per_stream,
     }
     if asm["ms"] > 0:
         result["assemble_gbs"] = round(asm["bytes"] / (asm["ms"] / 1e3) / 1e9, 1)

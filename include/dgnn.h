@@ -301,6 +301,30 @@ dgnn_status dgnn_assemble_group(dgnn_ctx* ctx, const uint32_t* addr, const int64
  * instead of once per batch; outputs are unchanged. */
 dgnn_status dgnn_host_window(dgnn_ctx* ctx, const uint32_t* addr, int64_t n, int32_t window_id, int32_t* stamp,
                              int64_t k_host, int32_t* list, int64_t capacity, int32_t* smap, int64_t* count);
+/* ---- sharded GPU tier (when the GPU tier does not fit replicated, slot s
+ * lives on rank s % world at local row s / world; remote rows travel over NVLink with
+ * all-to-all exchanges run by the caller's process group) ----
+ * dgnn_tier_shard_ids: ids[l] = gpu_ids[l*world + rank] for the rank's local rows
+ *   (*n_local = their count); fill the shard with dgnn_gather_rows(features, ids).
+ * dgnn_shard_requests: the GPU-tier rows of addr[0..n) owned by other ranks, grouped by
+ *   owner: req_off_host[world+1] (host, exclusive prefix; the call synchronizes),
+ *   req_slot (device int32 [n]): owner-local row, req_pos (device int32 [n]): row in out.
+ *   Order inside an owner's group is unspecified (each request carries its position).
+ * dgnn_scatter_rows: out[pos[i]] = rows[i] for i < n (the received remote rows).
+ * dgnn_assemble_group_sharded: dgnn_assemble_group with gpu_tier = this rank's shard;
+ *   GPU-tier rows owned by other ranks are left untouched (filled by dgnn_scatter_rows). */
+dgnn_status dgnn_tier_shard_ids(dgnn_ctx* ctx, const int32_t* gpu_ids, int64_t k_gpu, int32_t rank, int32_t world,
+                                int32_t* ids, int64_t* n_local);
+dgnn_status dgnn_shard_requests(dgnn_ctx* ctx, const uint32_t* addr, int64_t n, int64_t k_gpu, int32_t rank,
+                                int32_t world, int64_t* req_off_host, int32_t* req_slot, int32_t* req_pos);
+dgnn_status dgnn_scatter_rows(dgnn_ctx* ctx, const void* rows, int64_t n, int64_t row_bytes, const int32_t* pos,
+                              void* out);
+dgnn_status dgnn_assemble_group_sharded(dgnn_ctx* ctx, const uint32_t* addr, const int64_t* node_off, int64_t nb,
+                                        int64_t n, const void* gpu_tier, int64_t k_gpu, int32_t gpu_rank,
+                                        int32_t gpu_world, const void* host_tier, int64_t k_host,
+                                        const int32_t* host_map, const void* chunk_base, const int64_t* chunk_off,
+                                        const int64_t* chunk_rows, int64_t row_bytes, void* out);
+
 /* dgnn_gather_rows with the row count read from device memory (*n_dev <= n_max). */
 dgnn_status dgnn_gather_rows_dev(dgnn_ctx* ctx, const void* features, int64_t num_rows, int64_t row_bytes,
                                  const int32_t* ids, const int64_t* n_dev, int64_t n_max, void* out);

@@ -38,7 +38,8 @@ EXPORTS = [
     "dgnn_samples_free", "dgnn_build_cache", "dgnn_cache_plan_get_info", "dgnn_cache_plan_free", "dgnn_classify",
     "dgnn_chunk_layout", "dgnn_pack", "dgnn_gather_rows", "dgnn_stage_copy", "dgnn_stage_wait", "dgnn_stage_sync",
     "dgnn_host_alloc", "dgnn_host_free", "dgnn_assemble", "dgnn_assemble_group", "dgnn_ctx_set_assemble_occupancy",
-    "dgnn_host_window", "dgnn_gather_rows_dev", "dgnn_stage_wait_stream",
+    "dgnn_host_window", "dgnn_gather_rows_dev", "dgnn_stage_wait_stream", "dgnn_tier_shard_ids",
+    "dgnn_shard_requests", "dgnn_scatter_rows", "dgnn_assemble_group_sharded",
 ]
 
 
@@ -124,6 +125,10 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "dgnn_assemble": (i32, [P, P, i64, P, i64, P, i64, P, i64, i64, P]),
             "dgnn_assemble_group": (i32, [P, P, P, i64, i64, P, i64, P, i64, P, P, P, P, i64, P]),
             "dgnn_host_window": (i32, [P, P, i64, i32, P, i64, P, i64, P, P]),
+            "dgnn_tier_shard_ids": (i32, [P, P, i64, i32, i32, P, ctypes.POINTER(i64)]),
+            "dgnn_shard_requests": (i32, [P, P, i64, i64, i32, i32, P, P, P]),
+            "dgnn_scatter_rows": (i32, [P, P, i64, i64, P, P]),
+            "dgnn_assemble_group_sharded": (i32, [P, P, P, i64, i64, P, i64, i32, i32, P, i64, P, P, P, P, i64, P]),
             "dgnn_gather_rows_dev": (i32, [P, P, i64, i64, P, P, i64, P]),
             "dgnn_ctx_set_assemble_occupancy": (i32, [P, i32]),
         }
@@ -422,6 +427,44 @@ def dgnn_assemble_group(ctx: Ctx, addr: torch.Tensor, node_off: torch.Tensor, n:
                                               _ptr(gpu_tier), int(k_gpu), _ptr(host_tier), int(k_host),
                                               _ptr(host_map), _ptr(chunk_base), _ptr(chunk_off), _ptr(chunk_rows),
                                               int(row_bytes), _ptr(out)), "dgnn_assemble_group")
+
+
+def dgnn_assemble_group_sharded(ctx: Ctx, addr: torch.Tensor, node_off: torch.Tensor, n: int, gpu_shard, k_gpu: int,
+                                rank: int, world: int, host_tier, k_host: int, chunk_base, chunk_off: torch.Tensor,
+                                chunk_rows: torch.Tensor, row_bytes: int, out, host_map=None):
+    _check(load_library().dgnn_assemble_group_sharded(
+        ctx.handle, _ptr(addr), _ptr(node_off), node_off.numel() - 1, int(n), _ptr(gpu_shard), int(k_gpu), int(rank),
+        int(world), _ptr(host_tier), int(k_host), _ptr(host_map), _ptr(chunk_base), _ptr(chunk_off),
+        _ptr(chunk_rows), int(row_bytes), _ptr(out)), "dgnn_assemble_group_sharded")
+
+
+def dgnn_tier_shard_ids(ctx: Ctx, gpu_ids: torch.Tensor, k_gpu: int, rank: int, world: int) -> torch.Tensor:
+    n_local = max(0, (k_gpu - rank + world - 1) // world) if k_gpu > rank else 0
+    with torch.cuda.stream(ctx.stream):
+        ids = torch.empty(max(n_local, 1), dtype=torch.int32, device=ctx.device)
+    nl = i64()
+    _check(load_library().dgnn_tier_shard_ids(ctx.handle, _ptr(gpu_ids), int(k_gpu), int(rank), int(world),
+                                              _ptr(ids), ctypes.byref(nl)), "dgnn_tier_shard_ids")
+    return ids[:int(nl.value)]
+
+
+def dgnn_shard_requests(ctx: Ctx, addr: torch.Tensor, k_gpu: int, rank: int, world: int):
+    """-> (req_off_host int64 [world+1], req_slot, req_pos) grouped by owner rank."""
+    import numpy as np
+    n = addr.numel()
+    with torch.cuda.stream(ctx.stream):
+        req_slot = torch.empty(max(n, 1), dtype=torch.int32, device=ctx.device)
+        req_pos = torch.empty(max(n, 1), dtype=torch.int32, device=ctx.device)
+    off = np.zeros(world + 1, np.int64)
+    _check(load_library().dgnn_shard_requests(ctx.handle, _ptr(addr), n, int(k_gpu), int(rank), int(world),
+                                              P(off.ctypes.data), _ptr(req_slot), _ptr(req_pos)),
+           "dgnn_shard_requests")
+    return off, req_slot[:int(off[-1])], req_pos[:int(off[-1])]
+
+
+def dgnn_scatter_rows(ctx: Ctx, rows, n: int, row_bytes: int, pos: torch.Tensor, out):
+    _check(load_library().dgnn_scatter_rows(ctx.handle, _ptr(rows), int(n), int(row_bytes), _ptr(pos), _ptr(out)),
+           "dgnn_scatter_rows")
 
 
 def dgnn_host_window(ctx: Ctx, addr: torch.Tensor, window_id: int, stamp: torch.Tensor, k_host: int,

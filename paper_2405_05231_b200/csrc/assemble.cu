@@ -72,13 +72,24 @@ struct AsmGroupRow {
     int64_t row_bytes;
     uint8_t* out;
     int* err;
+    int gpu_world;             // > 1: the GPU tier is sharded, slot s lives on rank s % world at s / world
+    int gpu_rank;
     __device__ __forceinline__ bool operator()(int64_t j, const uint8_t*& s, uint8_t*& d) const {
         const uint32_t a = addr[j];
         const uint32_t tier = a >> DGNN_TIER_SHIFT;
         const int64_t slot = a & DGNN_SLOT_MASK;
         d = out + j * row_bytes;
         if (tier == DGNN_TIER_GPU && slot < kg) {
-            s = gpu + slot * row_bytes;
+            if (gpu_world > 1) {
+                if (slot % gpu_world != gpu_rank) {  // remote row: delivered by dgnn_scatter_rows
+                    d = nullptr;
+                    s = nullptr;
+                    return true;
+                }
+                s = gpu + (slot / gpu_world) * row_bytes;
+            } else {
+                s = gpu + slot * row_bytes;
+            }
         } else if (tier == DGNN_TIER_HOST && slot < kh) {
             s = host + (host_map ? (int64_t)host_map[slot] : slot) * row_bytes;
         } else if (tier == DGNN_TIER_DISK) {
@@ -247,6 +258,147 @@ extern "C" dgnn_status dgnn_assemble_group(dgnn_ctx* c, const uint32_t* addr, co
                                            int64_t k_host, const int32_t* host_map, const void* chunk_base,
                                            const int64_t* chunk_off, const int64_t* chunk_rows, int64_t row_bytes,
                                            void* out) {
+    return dgnn_assemble_group_sharded(c, addr, node_off, nb, n, gpu_tier, k_gpu, 0, 1, host_tier, k_host, host_map,
+                                       chunk_base, chunk_off, chunk_rows, row_bytes, out);
+}
+
+// ------------------------------------------------------- sharded GPU tier (C2)
+namespace dgnn {
+namespace {
+
+__global__ void k_shard_fill_ids(const int32_t* __restrict__ gpu_ids, int64_t k_gpu, int rank, int world,
+                                 int32_t* __restrict__ ids, int64_t n_local) {
+    for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < n_local; l += (int64_t)gridDim.x * blockDim.x)
+        ids[l] = gpu_ids[l * world + rank];
+}
+
+constexpr int kMaxWorld = 256;
+
+__global__ void k_owner_count(const uint32_t* __restrict__ addr, int64_t n, int64_t k_gpu, int rank, int world,
+                              unsigned long long* __restrict__ counts) {
+    __shared__ unsigned int sh[kMaxWorld];
+    for (int i = threadIdx.x; i < world; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t a = addr[j];
+        const int64_t slot = a & DGNN_SLOT_MASK;
+        if ((a >> DGNN_TIER_SHIFT) == DGNN_TIER_GPU && slot < k_gpu && slot % world != rank)
+            atomicAdd(&sh[slot % world], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < world; i += blockDim.x)
+        if (sh[i]) atomicAdd(&counts[i], (unsigned long long)sh[i]);
+}
+
+__global__ void k_owner_scatter(const uint32_t* __restrict__ addr, int64_t n, int64_t k_gpu, int rank, int world,
+                                unsigned long long* __restrict__ cursor, int32_t* __restrict__ req_slot,
+                                int32_t* __restrict__ req_pos) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t a = addr[j];
+        const int64_t slot = a & DGNN_SLOT_MASK;
+        if ((a >> DGNN_TIER_SHIFT) == DGNN_TIER_GPU && slot < k_gpu && slot % world != rank) {
+            const unsigned long long p = atomicAdd(&cursor[slot % world], 1ull);
+            req_slot[p] = (int32_t)(slot / world);  // the owner's local row
+            req_pos[p] = (int32_t)j;
+        }
+    }
+}
+
+struct ScatterRow {
+    const uint8_t* src;
+    const int32_t* pos;
+    int64_t rb;
+    uint8_t* out;
+    __device__ __forceinline__ bool operator()(int64_t r, const uint8_t*& s, uint8_t*& d) const {
+        s = src + r * rb;
+        d = out + (int64_t)pos[r] * rb;
+        return true;
+    }
+};
+
+template <class V>
+__global__ void __launch_bounds__(256, 6) k_scatter_rows(ScatterRow fn, int64_t n) {
+    const int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    copy_rows_warp<kAsmU, V>(n, fn.rb, fn, warp, nwarps);
+}
+
+}  // namespace
+}  // namespace dgnn
+
+extern "C" dgnn_status dgnn_tier_shard_ids(dgnn_ctx* c, const int32_t* gpu_ids, int64_t k_gpu, int32_t rank,
+                                           int32_t world, int32_t* ids, int64_t* n_local) {
+    DGNN_REQUIRE(c && n_local && world >= 1 && world <= kMaxWorld && rank >= 0 && rank < world && k_gpu >= 0,
+                 "dgnn_tier_shard_ids: bad argument");
+    const int64_t nl = k_gpu > rank ? (k_gpu - rank + world - 1) / world : 0;
+    *n_local = nl;
+    if (nl == 0) return DGNN_OK;
+    DGNN_REQUIRE(gpu_ids && ids, "dgnn_tier_shard_ids: NULL array");
+    DGNN_CK(cudaSetDevice(c->device));
+    launch(c, DGNN_K_GATHER, 0.0, [&] {
+        k_shard_fill_ids<<<grid_for(c, nl, 256), 256, 0, c->stream>>>(gpu_ids, k_gpu, rank, world, ids, nl);
+    });
+    DGNN_CK_LAUNCH();
+    return DGNN_OK;
+}
+
+extern "C" dgnn_status dgnn_shard_requests(dgnn_ctx* c, const uint32_t* addr, int64_t n, int64_t k_gpu, int32_t rank,
+                                           int32_t world, int64_t* req_off_host, int32_t* req_slot,
+                                           int32_t* req_pos) {
+    DGNN_REQUIRE(c && req_off_host && world >= 1 && world <= kMaxWorld && rank >= 0 && rank < world && n >= 0,
+                 "dgnn_shard_requests: bad argument");
+    DGNN_REQUIRE(n == 0 || (addr && req_slot && req_pos), "dgnn_shard_requests: NULL array");
+    DGNN_CK(cudaSetDevice(c->device));
+    DevBuf<unsigned long long> cnt;
+    DGNN_TRY(cnt.alloc(c, (size_t)world));
+    DGNN_TRY(memset_async(c, cnt.p, 0, sizeof(unsigned long long) * world));
+    if (n > 0) {
+        launch(c, DGNN_K_ASSEMBLE, 0.0, [&] {
+            k_owner_count<<<grid_for(c, n, 256, 4), 256, 0, c->stream>>>(addr, n, k_gpu, rank, world, cnt.p);
+        });
+        DGNN_CK_LAUNCH();
+    }
+    std::vector<unsigned long long> h(world);
+    DGNN_CK(cudaMemcpyAsync(h.data(), cnt.p, sizeof(unsigned long long) * world, cudaMemcpyDeviceToHost, c->stream));
+    DGNN_CK(cudaStreamSynchronize(c->stream));
+    req_off_host[0] = 0;
+    for (int o = 0; o < world; ++o) req_off_host[o + 1] = req_off_host[o] + (int64_t)h[o];
+    if (req_off_host[world] == 0) return DGNN_OK;
+    std::vector<unsigned long long> cur(world);
+    for (int o = 0; o < world; ++o) cur[o] = (unsigned long long)req_off_host[o];
+    DGNN_CK(cudaMemcpyAsync(cnt.p, cur.data(), sizeof(unsigned long long) * world, cudaMemcpyHostToDevice, c->stream));
+    launch(c, DGNN_K_ASSEMBLE, 0.0, [&] {
+        k_owner_scatter<<<grid_for(c, n, 256, 4), 256, 0, c->stream>>>(addr, n, k_gpu, rank, world, cnt.p, req_slot,
+                                                                        req_pos);
+    });
+    DGNN_CK_LAUNCH();
+    DGNN_CK(cudaStreamSynchronize(c->stream));  // `cur` (host) was a copy source
+    return DGNN_OK;
+}
+
+extern "C" dgnn_status dgnn_scatter_rows(dgnn_ctx* c, const void* rows, int64_t n, int64_t row_bytes,
+                                         const int32_t* pos, void* out) {
+    DGNN_REQUIRE(c && (n == 0 || (rows && pos && out)), "dgnn_scatter_rows: NULL argument");
+    DGNN_REQUIRE(row_bytes > 0 && row_bytes % 4 == 0 && n >= 0, "dgnn_scatter_rows: bad sizes");
+    if (n == 0) return DGNN_OK;
+    DGNN_CK(cudaSetDevice(c->device));
+    const bool v16 = row_bytes % 16 == 0 && al16(rows) && al16(out);
+    ScatterRow fn{(const uint8_t*)rows, pos, row_bytes, (uint8_t*)out};
+    launch(c, DGNN_K_ASSEMBLE, (double)n * (2.0 * row_bytes + 4.0), [&] {
+        if (v16) k_scatter_rows<uint4><<<grid_for(c, n * 32 / kAsmU, 256, 8), 256, 0, c->stream>>>(fn, n);
+        else k_scatter_rows<uint32_t><<<grid_for(c, n * 32 / kAsmU, 256, 8), 256, 0, c->stream>>>(fn, n);
+    });
+    DGNN_CK_LAUNCH();
+    return DGNN_OK;
+}
+
+extern "C" dgnn_status dgnn_assemble_group_sharded(dgnn_ctx* c, const uint32_t* addr, const int64_t* node_off,
+                                                   int64_t nb, int64_t n, const void* gpu_tier, int64_t k_gpu,
+                                                   int32_t gpu_rank, int32_t gpu_world, const void* host_tier,
+                                                   int64_t k_host, const int32_t* host_map, const void* chunk_base,
+                                                   const int64_t* chunk_off, const int64_t* chunk_rows,
+                                                   int64_t row_bytes, void* out) {
+    DGNN_REQUIRE(gpu_world >= 1 && gpu_rank >= 0 && gpu_rank < gpu_world, "dgnn_assemble_group: bad shard");
     DGNN_REQUIRE(c && (n == 0 || (addr && out && node_off && chunk_off && chunk_rows)),
                  "dgnn_assemble_group: NULL argument");
     DGNN_REQUIRE(row_bytes > 0 && row_bytes % 4 == 0 && n >= 0 && nb >= 0 && nb < (1 << 30) && k_gpu >= 0 &&
@@ -257,7 +409,7 @@ extern "C" dgnn_status dgnn_assemble_group(dgnn_ctx* c, const uint32_t* addr, co
     const bool v16 = row_bytes % 16 == 0 && al16(gpu_tier) && al16(host_tier) && al16(chunk_base) && al16(out);
     AsmGroupRow fn{addr,     node_off, chunk_off, chunk_rows, (int)nb,   (const uint8_t*)gpu_tier, k_gpu,
                    (const uint8_t*)host_tier, k_host, host_map, (const uint8_t*)chunk_base, row_bytes,
-                   (uint8_t*)out, c->dev_err};
+                   (uint8_t*)out, c->dev_err, gpu_world, gpu_rank};
     const int grid = grid_for(c, n * 32 / kAsmU, 256, c->assemble_blocks_per_sm);
     launch(c, DGNN_K_ASSEMBLE, (double)n * (2.0 * row_bytes + 4.0), [&] {
         if (v16) k_assemble_group<uint4><<<grid, 256, 0, c->stream>>>(fn, n);

@@ -26,7 +26,8 @@ __device__ __forceinline__ uint4 zero_of(uint4) { return make_uint4(0, 0, 0, 0);
 __device__ __forceinline__ uint32_t zero_of(uint32_t) { return 0u; }
 
 // RowFn: __device__ bool operator()(int64_t r, const uint8_t*& src, uint8_t*& dst) const
-// returns false to write a zero row (unresolvable address) -- dst must still be set.
+// returns false to write a zero row (unresolvable address) -- dst must still be set;
+// dst == nullptr skips the row (written by someone else, e.g. a remote GPU-tier row).
 template <int U, class V, class RowFn>
 __device__ __forceinline__ void copy_rows_warp(int64_t R, int64_t row_bytes, const RowFn& fn, int64_t warp_id,
                                                int64_t nwarps) {
@@ -45,7 +46,7 @@ __device__ __forceinline__ void copy_rows_warp(int64_t R, int64_t row_bytes, con
             src[u] = (const uint8_t*)__shfl_sync(0xffffffffu, (unsigned long long)my_src, u);
             dst[u] = (uint8_t*)__shfl_sync(0xffffffffu, (unsigned long long)my_dst, u);
             ok[u] = __shfl_sync(0xffffffffu, my_ok, u);
-            live[u] = r0 + u < R;
+            live[u] = r0 + u < R && dst[u] != nullptr;
         }
         for (int q0 = 0; q0 < nvec; q0 += 32) {
             const int q = q0 + lane;

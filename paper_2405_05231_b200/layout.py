@@ -200,7 +200,7 @@ class Layout:
         return plan
 
     def assemble_epoch(self, ctx: A.Ctx | None = None, out_budget: int = 1 << 30, host_window: int = 128,
-                       gather_ctx: A.Ctx | None = None):
+                       gather_ctx: A.Ctx | None = None, sharded_tier=None, remote=None):
         """Pipelined assembly: the chunks of the next run of batches are staged H2D
         on the side stream while the current run is assembled on the ctx stream (one
         dgnn_assemble_group launch per run).  Yields (b, features[n_b, dim]) per batch; a
@@ -211,7 +211,12 @@ class Layout:
         staging buffer instead of once per batch.  ``host_window=1`` is the
         paper's per-batch UVA read of the CPU cache.  The outputs are identical.  With a
         ``gather_ctx`` (a ctx on another stream) the next window's PCIe gather runs there,
-        double-buffered, overlapping the current window's HBM-bound runs."""
+        double-buffered, overlapping the current window's HBM-bound runs.
+
+        ``sharded_tier`` (a shard.ShardedTier) + ``remote(ctx, addr_run, out)`` assemble with
+        the GPU tier partitioned over ranks: local GPU-tier rows from this rank's shard,
+        remote ones delivered by ``remote`` (shard.fetch_remote_rows over NCCL, or the
+        single-process loopback)."""
         ctx = ctx or self.ctx
         gctx = gather_ctx or ctx
         nb = self.num_batches
@@ -303,9 +308,16 @@ class Layout:
                 host_src, host_map = staging[cur], smap[cur]
             else:
                 host_src, host_map = self.host_tier.ptr, None
-            A.dgnn_assemble_group(ctx, self.addr[n0:n1], t[:k + 1], n1 - n0, self.gpu_tier, self.plan.k_gpu,
-                                  host_src, kh, chunk, t[k + 1:2 * k + 2], t[2 * k + 2:], self.row_bytes, out,
-                                  host_map=host_map)
+            if sharded_tier is None:
+                A.dgnn_assemble_group(ctx, self.addr[n0:n1], t[:k + 1], n1 - n0, self.gpu_tier, self.plan.k_gpu,
+                                      host_src, kh, chunk, t[k + 1:2 * k + 2], t[2 * k + 2:], self.row_bytes, out,
+                                      host_map=host_map)
+            else:  # GPU tier sharded over ranks: local rows here, remote rows over the exchange
+                A.dgnn_assemble_group_sharded(ctx, self.addr[n0:n1], t[:k + 1], n1 - n0, sharded_tier.rows,
+                                              self.plan.k_gpu, sharded_tier.rank, sharded_tier.world, host_src, kh,
+                                              chunk, t[k + 1:2 * k + 2], t[2 * k + 2:], self.row_bytes, out,
+                                              host_map=host_map)
+                remote(ctx, self.addr[n0:n1], out)
             if i in last_run:
                 ev = torch.cuda.Event()
                 ev.record(ctx.stream)
@@ -318,7 +330,7 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
                    seeds: torch.Tensor, fanout, batch_size: int, gpu_rows: int, host_rows: int, rng_seed: int,
                    group_size: int = 64, batch_id_base: int = 0, stage: str = "pinned",
                    counts: torch.Tensor | None = None, ws: Workspace | None = None,
-                   group_budget: int = 4 << 30, stage_piece: int = 256 << 20) -> Layout:
+                   group_budget: int = 4 << 30, stage_piece: int = 1 << 40) -> Layout:
     """Run a1-a8 on this rank's batches.
 
     ``seeds`` are this rank's seeds (batch t of them gets bid = batch_id_base + t).

@@ -1,0 +1,100 @@
+"""Sharded GPU tier (north_star "the GPU feature cache is partitioned
+across the GPUs' HBM, and remote rows are fetched with NCCL all-to-all over NVLink").
+
+When the GPU tier does not fit replicated (IGB-shaped features, or forced), slot s of the
+tier lives on rank s % world at local row s // world.  Assembling a run of batches then
+needs, per rank, the GPU-tier rows other ranks own:
+
+    1. dgnn_shard_requests    -> requests grouped by owner (owner-local rows + out positions)
+    2. all_to_all  (counts)   -> how many rows every peer asks of me
+    3. all_to_all  (rows ids) -> the local rows every peer asks of me
+    4. dgnn_gather_rows       -> I gather them from my shard (HBM)
+    5. all_to_all  (rows)     -> the rows travel back over NVLink
+    6. dgnn_scatter_rows      -> they land at their positions in the output
+    and dgnn_assemble_group_sharded fills every other row locally.
+
+The collective choreography (steps 2-5) is ``exchange_remote_rows``; it is written against
+three small local callbacks so that the same code drives the CUDA kernels with NCCL in
+production and plain numpy with gloo in the CPU test of the protocol.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _abi as A
+
+
+def shard_of(slot: int, world: int):
+    """(owner rank, owner-local row) of a GPU-tier slot."""
+    return slot % world, slot // world
+
+
+class ShardedTier:
+    """This rank's shard of the GPU tier, gathered from the features (a7 "special mini-batch")."""
+
+    def __init__(self, ctx: A.Ctx, features: torch.Tensor, plan: A.CachePlan, rank: int, world: int):
+        self.ctx, self.rank, self.world = ctx, rank, world
+        self.k_gpu = plan.k_gpu
+        self.row_bytes = features.element_size() * (features.numel() // max(features.shape[0], 1))
+        ids = A.dgnn_tier_shard_ids(ctx, plan.gpu_ids, plan.k_gpu, rank, world)
+        with torch.cuda.stream(ctx.stream):
+            self.rows = torch.empty((ids.numel(), self.row_bytes), dtype=torch.uint8, device=ctx.device)
+        A.dgnn_gather_rows(ctx, features, ids, self.rows)
+
+
+def exchange_remote_rows(send_counts: np.ndarray, req_rows, serve, all_to_all, world: int, row_bytes: int):
+    """Steps 2-5.  ``send_counts[o]``: rows I request from owner o (grouped in ``req_rows``);
+    ``serve(ids)``: my shard's rows for the ids peers sent me; ``all_to_all(x, send_splits,
+    recv_splits)``: the process group's all-to-all on a flat tensor.  Returns the requested
+    rows grouped by owner, in request order."""
+    recv_counts = all_to_all(torch.as_tensor(send_counts, dtype=torch.int64), [1] * world, [1] * world)
+    recv_counts = [int(x) for x in recv_counts.cpu().tolist()]
+    send_counts = [int(x) for x in send_counts]
+    asked = all_to_all(req_rows, send_counts, recv_counts)           # ids peers want from my shard
+    served = serve(asked)                                            # [sum(recv_counts), row_bytes] uint8
+    back = all_to_all(served.reshape(-1), [c * row_bytes for c in recv_counts],
+                      [c * row_bytes for c in send_counts])
+    return back
+
+
+def nccl_all_to_all(group=None):
+    import torch.distributed as dist
+
+    def a2a(x: torch.Tensor, send_splits, recv_splits):
+        out = torch.empty(sum(recv_splits), dtype=x.dtype, device=x.device)
+        dist.all_to_all_single(out, x.contiguous(), output_split_sizes=list(recv_splits),
+                               input_split_sizes=list(send_splits), group=group)
+        return out
+    return a2a
+
+
+def fetch_remote_rows(ctx: A.Ctx, tier: ShardedTier, addr: torch.Tensor, out: torch.Tensor, all_to_all):
+    """Deliver the remote GPU-tier rows of one run into ``out`` (collective: every rank calls it
+    once per run, in the same order)."""
+    off, req_slot, req_pos = A.dgnn_shard_requests(ctx, addr, tier.k_gpu, tier.rank, tier.world)
+
+    def serve(ids: torch.Tensor) -> torch.Tensor:
+        with torch.cuda.stream(ctx.stream):
+            rows = torch.empty((ids.numel(), tier.row_bytes), dtype=torch.uint8, device=ctx.device)
+        A.dgnn_gather_rows(ctx, tier.rows, ids.to(torch.int32), rows)
+        return rows
+
+    with torch.cuda.stream(ctx.stream):
+        back = exchange_remote_rows(np.diff(off), req_slot, serve, all_to_all, tier.world, tier.row_bytes)
+    A.dgnn_scatter_rows(ctx, back, int(off[-1]), tier.row_bytes, req_pos, out)
+
+
+def fetch_remote_rows_loopback(ctx: A.Ctx, tiers: list, rank: int, addr: torch.Tensor, out: torch.Tensor):
+    """Single-process stand-in for the exchange (all shards local): owner o answers rank
+    ``rank``'s requests directly from its shard.  Used to test the kernels on one GPU."""
+    t = tiers[rank]
+    off, req_slot, req_pos = A.dgnn_shard_requests(ctx, addr, t.k_gpu, rank, t.world)
+    for o in range(t.world):
+        n = int(off[o + 1] - off[o])
+        if o == rank or n == 0:
+            continue
+        with torch.cuda.stream(ctx.stream):
+            rows = torch.empty((n, t.row_bytes), dtype=torch.uint8, device=ctx.device)
+        A.dgnn_gather_rows(ctx, tiers[o].rows, req_slot[int(off[o]):int(off[o + 1])], rows)
+        A.dgnn_scatter_rows(ctx, rows, n, t.row_bytes, req_pos[int(off[o]):int(off[o + 1])], out)

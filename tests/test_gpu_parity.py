@@ -228,6 +228,30 @@ def test_offline_layout_parity_hbm_stage_and_odd_rows(dg, ctx):
     _layout_parity(dg, ctx, w, [3, 3, 2], 64, 0, 50, 4, "pinned")
 
 
+@pytest.mark.parametrize("world,host_window", [(2, 1), (3, 128), (8, 2)])
+def test_sharded_gpu_tier_loopback(dg, ctx, tiny, world, host_window):
+    """GPU tier partitioned over `world` ranks (slot s on rank s % world), every rank
+    assembling every batch: local rows from its shard, remote rows through the request /
+    gather / scatter kernels (the all-to-all replaced by an in-process loopback)."""
+    from paper_2405_05231_b200 import shard
+    dev = torch.device("cuda", 0)
+    feats = tiny.features.to(dev)
+    L = dg.offline_layout(ctx, tiny.indptr.to(dev), tiny.indices.to(dev), feats, tiny.seeds.to(dev), [10, 5], 256,
+                          500, 1000, RNG_SEED, group_size=8)
+    tiers = [shard.ShardedTier(ctx, feats, L.plan, r, world) for r in range(world)]
+    assert sum(t.rows.shape[0] for t in tiers) == L.plan.k_gpu
+    host_feats = tiny.features.numpy()
+    for r in range(world):
+        def remote(c, addr, out, r=r):
+            shard.fetch_remote_rows_loopback(c, tiers, r, addr, out)
+        for b, out in L.assemble_epoch(host_window=host_window, sharded_tier=tiers[r], remote=remote,
+                                       out_budget=600_000):
+            nodes = L.samples.nodes[L.samples.node_off_host[b]:L.samples.node_off_host[b + 1]].cpu().numpy()
+            got = out.view(torch.uint8).reshape(out.shape[0], -1).cpu().numpy()
+            assert np.array_equal(got, oracle.assemble(host_feats, nodes)), f"rank {r} batch {b}"
+    ctx.sync()
+
+
 def test_spec_acceptance_fixture(dg, ctx):
     """1000 nodes, dim 128, 100 batches, fanout [5,5], tiers 5% / 10%."""
     w = make_workload("tiny", num_nodes=1000, num_edges=10_000, num_seeds=800, batch_size=8, fanout=(5, 5))

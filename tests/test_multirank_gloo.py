@@ -51,6 +51,55 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
+def _exchange_worker(rank, world, port, q):
+    """The sharded-tier all-to-all choreography (shard.exchange_remote_rows) with numpy
+    stand-ins for the CUDA request / gather kernels."""
+    from paper_2405_05231_b200.shard import exchange_remote_rows, shard_of
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rb, k_gpu = 16, 101
+        table = np.arange(k_gpu * rb, dtype=np.uint8).reshape(k_gpu, rb) ^ 0x5A  # GPU tier rows by slot
+        my_shard = table[rank::world]                                              # slot s on rank s % world
+        rng = np.random.default_rng(rank)
+        want = rng.integers(0, k_gpu, 300)
+        remote = [int(s) for s in want if shard_of(int(s), world)[0] != rank]
+        by_owner = [[s for s in remote if s % world == o] for o in range(world)]
+        send_counts = np.array([len(x) for x in by_owner], np.int64)
+        req = torch.tensor([shard_of(s, world)[1] for o in range(world) for s in by_owner[o]], dtype=torch.int32)
+
+        def serve(ids):
+            return torch.from_numpy(my_shard[ids.numpy()].copy())
+
+        def a2a(x, send_splits, recv_splits):
+            out = torch.empty(sum(recv_splits), dtype=x.dtype)
+            dist.all_to_all_single(out, x.contiguous(), output_split_sizes=list(recv_splits),
+                                   input_split_sizes=list(send_splits))
+            return out
+
+        back = exchange_remote_rows(send_counts, req, serve, a2a, world, rb).numpy().reshape(-1, rb)
+        expect = np.concatenate([table[by_owner[o]] for o in range(world)] or [np.zeros((0, rb), np.uint8)])
+        q.put((rank, bool(np.array_equal(back, expect)), len(remote)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_tier_all_to_all_protocol(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_exchange_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok, _ in res) and all(n > 0 for _, _, n in res)
+
+
 def test_count_allreduce_gives_the_single_process_plan():
     import oracle
     world = 2
