@@ -223,7 +223,9 @@ class Runner:
                                       stage_piece=int(os.environ.get("DGNN_STAGE_PIECE", str(1 << 40))))
 
     def run(self, K: int, keep_last=False):
-        """Enqueue K passes; returns the last Layout if keep_last."""
+        """Enqueue K passes; returns the last Layout if keep_last.  self.timeline collects
+        (layout events, assembly start/end events) per pass for the device timeline."""
+        self.timeline = []
         L = self.layout(0)
         ev_l = torch.cuda.Event()
         ev_l.record(self.sA)
@@ -231,11 +233,14 @@ class Runner:
         last = None
         for e in range(K):
             self.sB.wait_event(ev_l)
+            a0 = torch.cuda.Event(enable_timing=True)
+            a0.record(self.sB)
             gctx = self.ctxG if os.environ.get("DGNN_GATHER_STREAM", "1") == "1" else None
             for _ in L.assemble_epoch(ctx=self.ctxB, host_window=self.host_window, gather_ctx=gctx):
                 pass
-            ev_a = torch.cuda.Event()
+            ev_a = torch.cuda.Event(enable_timing=True)
             ev_a.record(self.sB)
+            self.timeline.append((L.stats.get("_events", []), a0, ev_a))
             Ln = None
             if e + 1 < K:
                 if not self.pipelined:
@@ -250,6 +255,19 @@ class Runner:
             L = Ln
         self.sA.wait_event(prev_ev)
         return last if keep_last else None
+
+    def timeline_ms(self):
+        """Per pass, relative to the first layout start: layout phase ends and assembly span."""
+        if not self.timeline:
+            return []
+        t0 = self.timeline[0][0][0][1] if self.timeline[0][0] else self.timeline[0][1]
+        out = []
+        for evs, a0, a1 in self.timeline:
+            d = {name: round(t0.elapsed_time(ev), 1) for name, ev in evs}
+            d["assemble_start"] = round(t0.elapsed_time(a0), 1)
+            d["assemble_end"] = round(t0.elapsed_time(a1), 1)
+            out.append(d)
+        return out
 
 
 def cpu_baseline(cfg, inp_host, n_batches: int):
@@ -393,6 +411,7 @@ def main():
         "clocks": clocks,
         "gpu_launches": int(launches),
         "kernel_ms_per_step_by_stream": per_stream,
+        "device_timeline_ms": R.timeline_ms(),
     }
     if asm["ms"] > 0:
         result["assemble_gbs"] = round(asm["bytes"] / (asm["ms"] / 1e3) / 1e9, 1)
