@@ -189,12 +189,12 @@ class Runner:
         # first and the layout of the next pass fills the remaining SM capacity
         # (sequential mode still assembles on its own stream: the stage-out of a pass overlaps
         # the start of its assembly; only the next pass waits for the assembly to finish)
-        self.sB = torch.cuda.Stream(dev, priority=-1 if pipelined else 0)
+        self.sB = torch.cuda.Stream(dev, priority=int(os.environ.get("DGNN_ASM_PRIORITY", "0")))
         torch.cuda.set_stream(self.sA)
         self.ctxA = dg.Ctx(device=dev, stream=self.sA)
         self.ctxB = dg.Ctx(device=dev, stream=self.sB)
         if pipelined:
-            self.ctxB.set_assemble_occupancy(int(os.environ.get("DGNN_ASM_OCC", "2")))  # PCIe-bound: leave SMs
+            self.ctxB.set_assemble_occupancy(int(os.environ.get("DGNN_ASM_OCC", "8")))
         N = inp[1].numel() - 1
         self.ws = [Workspace(), Workspace()]
         self.counts = [torch.zeros(N, dtype=torch.int32, device=dev) for _ in range(2)]
@@ -204,7 +204,8 @@ class Runner:
         self.host_window = 128
         # a9's host-row window gathers (PCIe) run on their own stream, overlapping the
         # HBM-bound assembly runs of the previous window
-        self.sG = torch.cuda.Stream(dev)
+        # the PCIe gathers need few SMs but should never wait for them: high priority
+        self.sG = torch.cuda.Stream(dev, priority=int(os.environ.get("DGNN_GATHER_PRIORITY", "-1")))
         self.ctxG = dg.Ctx(device=dev, stream=self.sG)
         self.ctxG.set_assemble_occupancy(2)
 
@@ -240,18 +241,25 @@ class Runner:
                 pass
             ev_a = torch.cuda.Event(enable_timing=True)
             ev_a.record(self.sB)
-            self.timeline.append((L.stats.get("_events", []), a0, ev_a))
+            self.timeline.append(((L.stats.get("_events", []), L.stats.get("_host", [])), a0, ev_a))
             Ln = None
             if e + 1 < K:
                 if not self.pipelined:
                     self.sA.wait_event(ev_a)  # sequential: the next pass starts after this assembly
                 elif prev_ev is not None:
                     self.sA.wait_event(prev_ev)  # slot (e+1)%2 was pass e-1's: its assembly must be done
+                # a pass whose assembly stream A has waited for is finished on the device:
+                # release it before allocating pass e+1, so at most two passes are resident
+                # (pipelined: pass e-1; sequential: pass e as well)
+                last = None
+                if not self.pipelined:
+                    L = None
                 Ln = self.layout((e + 1) % 2)
                 ev_l = torch.cuda.Event()
                 ev_l.record(self.sA)
             prev_ev = ev_a
-            last = L
+            if L is not None:
+                last = L
             L = Ln
         self.sA.wait_event(prev_ev)
         return last if keep_last else None
@@ -260,10 +268,11 @@ class Runner:
         """Per pass, relative to the first layout start: layout phase ends and assembly span."""
         if not self.timeline:
             return []
-        t0 = self.timeline[0][0][0][1] if self.timeline[0][0] else self.timeline[0][1]
+        t0 = self.timeline[0][0][0][0][1] if self.timeline[0][0][0] else self.timeline[0][1]
         out = []
-        for evs, a0, a1 in self.timeline:
+        for (evs, host), a0, a1 in self.timeline:
             d = {name: round(t0.elapsed_time(ev), 1) for name, ev in evs}
+            d["host_ms"] = {host[i][0]: round((host[i][1] - host[i - 1][1]) * 1e3, 1) for i in range(1, len(host))}
             d["assemble_start"] = round(t0.elapsed_time(a0), 1)
             d["assemble_end"] = round(t0.elapsed_time(a1), 1)
             out.append(d)

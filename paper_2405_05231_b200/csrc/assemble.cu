@@ -130,41 +130,15 @@ __global__ void __launch_bounds__(256, 6) k_assemble_group(AsmGroupRow fn, int64
 
 bool al16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
-// Host-row merging over a window of batches: the first visit of a host-tier slot
-// in window `wid` (atomicExch on a per-slot stamp) appends it to the window's list
-// and records its position, so each host row crosses PCIe once per window.
-__global__ void __launch_bounds__(256) k_host_window(const uint32_t* __restrict__ addr, int64_t n, int32_t wid,
-                                                     int32_t* __restrict__ stamp, int64_t kh,
-                                                     int32_t* __restrict__ list, int64_t cap,
-                                                     int32_t* __restrict__ smap, unsigned long long* count,
-                                                     int* err) {
-    const int lane = threadIdx.x & 31;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x; i0 < n; i0 += stride) {
-        const int64_t i = i0 + threadIdx.x;
-        bool first = false;
-        int64_t slot = 0;
-        if (i < n) {
-            const uint32_t a = addr[i];
-            slot = a & DGNN_SLOT_MASK;
-            if ((a >> DGNN_TIER_SHIFT) == DGNN_TIER_HOST && slot < kh) first = atomicExch(&stamp[slot], wid) != wid;
-        }
-        const unsigned m = __ballot_sync(0xffffffffu, first);
-        if (m) {
-            const int leader = __ffs(m) - 1;
-            unsigned long long base = 0;
-            if (lane == leader) base = atomicAdd(count, (unsigned long long)__popc(m));
-            base = __shfl_sync(0xffffffffu, base, leader);
-            if (first) {
-                const int64_t pos = (int64_t)base + __popc(m & lanemask_lt());
-                if (pos < cap) {
-                    list[pos] = (int32_t)slot;
-                    smap[slot] = (int32_t)pos;
-                } else {
-                    atomicOr(err, DEVERR_OVERFLOW);
-                }
-            }
-        }
+// Host-row merging over a window of batches: every host-tier slot the window reads
+// gets the window's stamp (plain stores: all writers store the same value); a scan
+// over the stamps then lists the slots once each, in ascending order.
+__global__ void __launch_bounds__(256) k_host_mark(const uint32_t* __restrict__ addr, int64_t n, int32_t wid,
+                                                   int32_t* __restrict__ stamp, int64_t kh) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t a = addr[i];
+        const int64_t slot = a & DGNN_SLOT_MASK;
+        if ((a >> DGNN_TIER_SHIFT) == DGNN_TIER_HOST && slot < kh) stamp[slot] = wid;
     }
 }
 
@@ -223,13 +197,23 @@ extern "C" dgnn_status dgnn_host_window(dgnn_ctx* c, const uint32_t* addr, int64
     DGNN_REQUIRE(n >= 0 && k_host >= 0 && capacity >= 0 && window_id >= 0, "dgnn_host_window: bad sizes");
     DGNN_CK(cudaSetDevice(c->device));
     DGNN_TRY(memset_async(c, count, 0, sizeof(int64_t)));
-    if (n == 0) return DGNN_OK;
+    if (n == 0 || k_host == 0) return DGNN_OK;
+    // mark the window's host slots, then list them in ascending slot order with one scan
+    // over the host tier: the staging gather then walks host memory in address order
     launch(c, DGNN_K_ASSEMBLE, 0.0, [&] {
-        k_host_window<<<grid_for(c, n, 256, 8), 256, 0, c->stream>>>(addr, n, window_id, stamp, k_host, list,
-                                                                     capacity, smap, (unsigned long long*)count,
-                                                                     c->dev_err);
+        k_host_mark<<<grid_for(c, n, 256, 8), 256, 0, c->stream>>>(addr, n, window_id, stamp, k_host);
     });
     DGNN_CK_LAUNCH();
+    const int32_t* st = stamp;
+    const int32_t wid = window_id;
+    auto in = [=] __device__(int64_t s) -> int32_t { return st[s] == wid ? 1 : 0; };
+    auto outf = [=] __device__(int64_t s, int64_t excl, int64_t val) {
+        if (val && excl < capacity) {
+            list[excl] = (int32_t)s;
+            smap[s] = (int32_t)excl;
+        }
+    };
+    DGNN_TRY(scan::run(c, k_host, nullptr, in, outf, count));
     return DGNN_OK;
 }
 

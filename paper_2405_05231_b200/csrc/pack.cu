@@ -82,6 +82,33 @@ __global__ void __launch_bounds__(256) k_gather(const uint8_t* __restrict__ src,
 
 bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
+__global__ void k_classify_min(const uint32_t* __restrict__ addr, int64_t n, const int64_t* __restrict__ seg,
+                               int nseg, int64_t n0, int64_t* __restrict__ packed_off) {
+    __shared__ int64_t s_seg[kMaxSmemSeg + 1];
+    const bool in_smem = nseg <= kMaxSmemSeg;
+    if (in_smem)
+        for (int i = threadIdx.x; i <= nseg; i += blockDim.x) s_seg[i] = seg[i];
+    __syncthreads();
+    const int64_t* sg = in_smem ? s_seg : seg;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t a = addr[i];
+        if ((a >> DGNN_TIER_SHIFT) == DGNN_TIER_DISK) {
+            const int b = segment_of(sg, nseg + 1, n0 + i);
+            // only the batch's first DISK node can hold the minimum: skip the atomic otherwise
+            if (i == 0 || n0 + i == sg[b] || (addr[i - 1] >> DGNN_TIER_SHIFT) != DGNN_TIER_DISK ||
+                ((addr[i - 1] & DGNN_SLOT_MASK) + 1 != (a & DGNN_SLOT_MASK)))
+                atomicMin((unsigned long long*)&packed_off[b], (unsigned long long)(a & DGNN_SLOT_MASK));
+        }
+    }
+}
+
+// batches without DISK nodes: packed_off[b] = packed_off[b+1] (packed_off[nseg] = total)
+__global__ void k_classify_fill(int64_t* packed_off, int nseg) {
+    if (threadIdx.x != 0) return;
+    for (int b = nseg - 1; b >= 0; --b)
+        if (packed_off[b] > packed_off[b + 1]) packed_off[b] = packed_off[b + 1];
+}
+
 __global__ void k_classify_fix(uint32_t* __restrict__ addr, int64_t n, const int64_t* __restrict__ seg, int nseg,
                                int64_t n0, const int64_t* __restrict__ packed_off) {
     __shared__ int64_t s_seg[kMaxSmemSeg + 1];
@@ -125,23 +152,28 @@ extern "C" dgnn_status dgnn_classify(dgnn_ctx* c, const dgnn_cache_plan* plan, c
         const int64_t* seg = S->node_off + b_lo;  // absolute offsets of batches b_lo..b_hi
         const uint32_t* tm = plan->tier_map;
         const int nseg = (int)nbg;
+        // pass 1: one gather of tier_map per node (parked in addr by the scan input), the
+        // compaction of the DISK nodes (P_b concatenated) and their global packed index
         auto in = [=] __device__(int64_t i) -> int32_t {
-            return (int32_t)((tm[nodes[i]] >> DGNN_TIER_SHIFT) == DGNN_TIER_DISK);
+            const uint32_t t = tm[nodes[i]];
+            addr[i] = t;
+            return (int32_t)((t >> DGNN_TIER_SHIFT) == DGNN_TIER_DISK);
         };
-        // pass 1: compaction of the DISK nodes (P_b concatenated), batch starts,
-        // global packed index parked in addr
         auto outf = [=] __device__(int64_t i, int64_t excl, int64_t val) {
-            const int b = segment_of(seg, nseg + 1, n0 + i);
-            if (n0 + i == seg[b]) packed_off[b] = excl;
             if (val) {
                 packed_ids[excl] = nodes[i];
                 addr[i] = (DGNN_TIER_DISK << DGNN_TIER_SHIFT) | (uint32_t)excl;
-            } else {
-                addr[i] = tm[nodes[i]];
             }
         };
         DGNN_TRY(scan::run(c, n, nullptr, in, outf, packed_off + nbg));
-        // pass 2: DISK slots relative to the batch (rank among the batch's DISK nodes)
+        // pass 2: packed_off[b] = the smallest global packed index of batch b (batches
+        // without DISK nodes take their successor's), then DISK slots relative to the batch
+        DGNN_TRY(memset_async(c, packed_off, 0x7F, sizeof(int64_t) * nbg));
+        launch(c, DGNN_K_CLASSIFY, 4.0 * n, [&] {
+            k_classify_min<<<grid_for(c, n, 256), 256, 0, c->stream>>>(addr, n, seg, nseg, n0, packed_off);
+            k_classify_fill<<<1, 32, 0, c->stream>>>(packed_off, nseg);
+        });
+        DGNN_CK_LAUNCH();
         launch(c, DGNN_K_CLASSIFY, 8.0 * n, [&] {
             k_classify_fix<<<grid_for(c, n, 256), 256, 0, c->stream>>>(addr, n, seg, nseg, n0, packed_off);
         });

@@ -165,10 +165,11 @@ class Layout:
         groups = []
         b0 = 0
         nb = self.num_batches
+        max_rows = max(1, out_budget // self.row_bytes)
         while b0 < nb:
-            b1 = b0 + 1
-            while b1 < nb and (no[b1 + 1] - no[b0]) * self.row_bytes <= out_budget and b1 - b0 < 1024:
-                b1 += 1
+            # the last b1 with no[b1] - no[b0] <= max_rows, at least one batch, at most 1024
+            b1 = int(np.searchsorted(no, no[b0] + max_rows, side="right")) - 1
+            b1 = min(max(b1, b0 + 1), b0 + 1024, nb)
             groups.append((b0, b1))
             b0 = b1
         return groups
@@ -344,10 +345,14 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
     dim = features.numel() // max(features.shape[0], 1)
     stats = {"_events": []}
 
-    def mark(name):  # phase boundaries on the layout's stream (measurement only)
+    import time as _time
+    stats["_host"] = []
+
+    def mark(name):  # phase boundaries on the layout's stream + host clock (measurement only)
         e = torch.cuda.Event(enable_timing=True)
         e.record(ctx.stream)
         stats["_events"].append((name, e))
+        stats["_host"].append((name, _time.perf_counter()))
 
     mark("start")
     if counts is None:

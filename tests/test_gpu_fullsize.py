@@ -40,6 +40,49 @@ def papers():
 SAMPLED = [0, 1, 586, 1170, 1171]
 
 
+def test_products_full_epoch_bit_exact():
+    """ogbn-products-shaped (configs[1]) at full size, every output of every batch: the oracle
+    recomputes the whole epoch (193 batches, 33.9 M sampled nodes, 400-byte rows)."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_2405_05231_b200 as dg
+    dev = torch.device("cuda", 0)
+    cfg = dict(CONFIGS["products"])
+    indptr, indices = make_graph(cfg["num_nodes"], cfg["num_edges"], cfg["degree"], cfg["skew"], 0, dev)
+    seeds = make_seeds(cfg["num_nodes"], cfg["num_seeds"], 0, dev)
+    feats = make_features(cfg["num_nodes"], cfg["dim"], dev, fseed=1)
+    gpu_rows, host_rows = config_rows(cfg)
+    ctx = dg.Ctx(device=dev)
+    L = dg.offline_layout(ctx, indptr, indices, feats, seeds, cfg["fanout"], cfg["batch_size"], gpu_rows, host_rows,
+                          RNG_SEED, group_size=cfg["group_size"])
+    ctx.sync()
+    hf = feats.cpu().numpy()
+    ref = oracle.offline_layout(indptr.cpu().numpy(), indices.cpu().numpy(), hf, seeds.cpu().numpy(),
+                                cfg["batch_size"], list(cfg["fanout"]), RNG_SEED, gpu_rows, host_rows,
+                                group_size=10_000, threads=16)
+    S = L.samples
+    assert S.num_batches == len(ref["samples"]) == 193
+    nodes, eptr, src = S.nodes.cpu().numpy(), S.eptr.cpu().numpy(), S.src_local.cpu().numpy()
+    addr = L.addr.cpu().numpy().view(np.uint32)
+    for b, r in enumerate(ref["samples"]):
+        n0, n1 = S.node_off_host[b], S.node_off_host[b + 1]
+        assert np.array_equal(nodes[n0:n1], r.nodes) and np.array_equal(S.hop_off_host[b], r.hop_off)
+        assert np.array_equal(eptr[S.eptr_off_host[b]:S.eptr_off_host[b + 1]], r.eptr)
+        assert np.array_equal(src[S.edge_off_host[b]:S.edge_off_host[b + 1]], r.src_local)
+        assert np.array_equal(addr[n0:n1], ref["addr"][b])
+    assert np.array_equal(L.counts.cpu().numpy().view(np.uint32), ref["counts"])
+    assert np.array_equal(L.plan.tier_map.cpu().numpy().view(np.uint32), ref["tier_map"])
+    buf, off = ref["groups"][0]  # one oracle group holding every chunk
+    assert L.stats["arena_bytes"] == off[-1]
+    assert np.array_equal(L.arena.tensor.numpy()[:off[-1]], buf)
+    check = {0, 1, 96, 191, 192}
+    for b, out in L.assemble_epoch():
+        if b in check:
+            got = out.view(torch.uint8).reshape(out.shape[0], -1).cpu().numpy()
+            assert np.array_equal(got, oracle.assemble(hf, ref["samples"][b].nodes)), f"batch {b}"
+    ctx.sync()
+
+
 def test_sampled_batches_bit_exact(papers):
     L, cfg = papers["L"], papers["cfg"]
     ref = oracle.sample(papers["indptr"], papers["indices"], papers["seeds"], cfg["batch_size"], list(cfg["fanout"]),
