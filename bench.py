@@ -134,6 +134,16 @@ def sum_over_ranks(x: float, ws: int) -> float:
     return float(t.item())
 
 
+def _mem_available_bytes():
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable:"):
+                return int(line.split()[1]) * 1024
+    except Exception:
+        return None
+    return None
+
+
 def pcie_bandwidth(dev, nbytes: int = 1 << 30) -> dict:
     """Pinned host <-> device copy bandwidth (best of 5), the PCIe roofline denominator."""
     import paper_2405_05231_b200 as dg
@@ -420,6 +430,9 @@ def main():
         "clocks": clocks,
         "gpu_launches": int(launches),
         "kernel_ms_per_step_by_stream": per_stream,
+        "memory": {"max_reserved_gb": round(torch.cuda.max_memory_reserved(dev) / 1e9, 1),
+                   "alloc_retries": int(torch.cuda.memory_stats(dev).get("num_alloc_retries", 0)),
+                   "cuda_malloc_retries": int(torch.cuda.memory_stats(dev).get("num_device_alloc", 0))},
         "device_timeline_ms": R.timeline_ms(),
     }
     if asm["ms"] > 0:
@@ -438,6 +451,15 @@ def main():
     # ---------------- e2e through the public API with host buffers ----------------
     inp_host = None
     pinned = []
+    in_bytes = sum(t.numel() * t.element_size() for t in (indptr, indices, seeds, feats))
+    # every rank pins a host copy of its inputs for the e2e leg: skip it (and say so) when
+    # the node's free memory cannot hold world_size copies plus a margin
+    avail = _mem_available_bytes()
+    if not args.no_e2e and avail is not None and avail < int(in_bytes * ws * 1.25) + (16 << 30):
+        args.no_e2e = True
+        result["e2e"] = {"value": None, "unit": "mini-batches/s",
+                         "skipped": f"host memory: {avail / 2**30:.0f} GiB available < {ws} x "
+                                    f"{in_bytes / 2**30:.0f} GiB pinned inputs"}
     if not args.no_e2e or (not args.no_cpu and rank == 0 and ws == 1):
         def pin_like(t):  # exact-size pinned buffer (torch's pinned allocator rounds to powers of two)
             hb = dg.HostBuffer(t.numel() * t.element_size())
