@@ -34,7 +34,11 @@ import tempfile
 import time
 
 import numpy as np
-import torch
+
+# two passes of the papers-shaped layout plus 64 GB of inputs come close to the 180 GB of HBM:
+# expandable segments keep the caching allocator from fragmenting (must precede CUDA init)
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
+import torch  # noqa: E402
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -214,8 +218,9 @@ class Runner:
         self.host_window = 128
         # a9's host-row window gathers (PCIe) run on their own stream, overlapping the
         # HBM-bound assembly runs of the previous window
-        # the PCIe gathers need few SMs but should never wait for them: high priority
-        self.sG = torch.cuda.Stream(dev, priority=int(os.environ.get("DGNN_GATHER_PRIORITY", "-1")))
+        # (stream priorities were measured: prioritising either assembly stream starves the
+        # concurrent layout and loses overall, so all streams run at the default priority)
+        self.sG = torch.cuda.Stream(dev, priority=int(os.environ.get("DGNN_GATHER_PRIORITY", "0")))
         self.ctxG = dg.Ctx(device=dev, stream=self.sG)
         self.ctxG.set_assemble_occupancy(2)
 
@@ -326,9 +331,8 @@ def main():
     ap.add_argument("--cpu-batches", type=int, default=32)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--pipelined", action="store_true",
-                    help="overlap the layout of pass e+1 with the assembly of pass e on two streams "
-                         "(measured slower on one B200: both halves contend for PCIe and HBM)")
+    ap.add_argument("--sequential", action="store_true",
+                    help="no epoch pipelining: the layout of pass e+1 starts after the assembly of pass e")
     ap.add_argument("--host-window", type=int, default=128,
                     help="batches per host-row merging window in a9 (1 = per-batch UVA reads, the paper's)")
     args = ap.parse_args()
@@ -342,7 +346,7 @@ def main():
     cfg, indptr, indices, seeds, feats, gpu_rows, host_rows = inp
     N = indptr.numel() - 1
     nb = (seeds.numel() + cfg["batch_size"] - 1) // cfg["batch_size"]
-    R = Runner(dg, inp, rank, dev, pipelined=args.pipelined)
+    R = Runner(dg, inp, rank, dev, pipelined=not args.sequential)
     R.host_window = args.host_window
     t = time.time()
     L = R.run(1, keep_last=True)
@@ -414,7 +418,7 @@ def main():
                    "host_rows": host_rows, "group_size": cfg["group_size"], "disk_tier": "pinned host arena",
                    "parallelism": f"dp{ws} (batch-sharded, count all-reduce)",
                    "host_window_batches": args.host_window,
-                   "schedule": "sequential" if not args.pipelined else
+                   "schedule": "sequential" if args.sequential else
                    "pipelined: layout of pass e+1 overlaps assembly of pass e (2 streams)",
                    "l2": "inputs larger than L2 (features %.1f GB, CSR %.1f GB); no flush needed" % (
                        feats.numel() * 4 / 1e9, (indptr.numel() * 8 + indices.numel() * 4) / 1e9)},

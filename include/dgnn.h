@@ -224,6 +224,12 @@ dgnn_status dgnn_classify(dgnn_ctx* ctx, const dgnn_cache_plan* plan, const dgnn
                           int64_t b_lo, int64_t b_hi, uint32_t* addr, int32_t* packed_ids, int64_t* packed_off,
                           int64_t* packed_off_host);
 
+/* Rows of each tier per batch, from the address tables of batches [b_lo, b_hi) (as written
+ * by dgnn_classify into addr): counts_host[3*(b-b_lo) + tier] (host int64; synchronizes).
+ * Sizing metadata for the assembler's staging buffers. */
+dgnn_status dgnn_batch_tier_counts(dgnn_ctx* ctx, const dgnn_samples* samples, int64_t b_lo, int64_t b_hi,
+                                   const uint32_t* addr, int64_t* counts_host);
+
 /* ------------------------------------------------------------- a7 pack ---- */
 /* Host arithmetic of the chunk layout (reading c20): chunk_off[0] = 0,
  * chunk_off[i+1] = roundup(chunk_off[i] + (packed_off[i+1]-packed_off[i]) * row_bytes, 4096). */

@@ -39,7 +39,7 @@ EXPORTS = [
     "dgnn_chunk_layout", "dgnn_pack", "dgnn_gather_rows", "dgnn_stage_copy", "dgnn_stage_wait", "dgnn_stage_sync",
     "dgnn_host_alloc", "dgnn_host_free", "dgnn_assemble", "dgnn_assemble_group", "dgnn_ctx_set_assemble_occupancy",
     "dgnn_host_window", "dgnn_gather_rows_dev", "dgnn_stage_wait_stream", "dgnn_tier_shard_ids",
-    "dgnn_shard_requests", "dgnn_scatter_rows", "dgnn_assemble_group_sharded",
+    "dgnn_shard_requests", "dgnn_scatter_rows", "dgnn_assemble_group_sharded", "dgnn_batch_tier_counts",
 ]
 
 
@@ -114,6 +114,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "dgnn_cache_plan_free": (None, [P]),
             "dgnn_classify": (i32, [P, P, P, i64, i64, P, P, P, P]),
             "dgnn_chunk_layout": (i32, [P, i64, i64, P]),
+            "dgnn_batch_tier_counts": (i32, [P, P, i64, i64, P, P]),
             "dgnn_pack": (i32, [P, P, i64, i64, P, P, P, i64, i64, i64, P]),
             "dgnn_gather_rows": (i32, [P, P, i64, i64, P, i64, P]),
             "dgnn_stage_copy": (i32, [P, P, P, i64, i32, ctypes.POINTER(i64)]),
@@ -365,6 +366,15 @@ def dgnn_classify(ctx: Ctx, plan: CachePlan, samples: Samples, b_lo: int, b_hi: 
                                         _ptr(packed_ids), _ptr(packed_off),
                                         P(host.ctypes.data) if host is not None else P(0)), "dgnn_classify")
     return host
+
+
+def dgnn_batch_tier_counts(ctx: Ctx, samples: Samples, b_lo: int, b_hi: int, addr: torch.Tensor):
+    """-> int64 [b_hi-b_lo, 3]: rows of each tier (GPU, HOST, DISK) per batch."""
+    import numpy as np
+    out = np.zeros((max(b_hi - b_lo, 0), 3), np.int64)
+    _check(load_library().dgnn_batch_tier_counts(ctx.handle, samples.handle, int(b_lo), int(b_hi), _ptr(addr),
+                                                 P(out.ctypes.data) if out.size else P(0)), "dgnn_batch_tier_counts")
+    return out
 
 
 def dgnn_chunk_layout(packed_off_host, row_bytes: int):

@@ -102,6 +102,29 @@ __global__ void k_classify_min(const uint32_t* __restrict__ addr, int64_t n, con
     }
 }
 
+// per-batch row counts of each tier (block per batch): sizing metadata for the assembler
+__global__ void k_tier_counts(const uint32_t* __restrict__ addr, const int64_t* __restrict__ node_off, int64_t n0,
+                              int nb, int64_t* __restrict__ out) {
+    __shared__ unsigned long long s[3];
+    for (int b = blockIdx.x; b < nb; b += gridDim.x) {
+        if (threadIdx.x < 3) s[threadIdx.x] = 0;
+        __syncthreads();
+        unsigned long long c[3] = {0, 0, 0};
+        for (int64_t i = node_off[b] - n0 + threadIdx.x; i < node_off[b + 1] - n0; i += blockDim.x) {
+            const uint32_t t = addr[i] >> DGNN_TIER_SHIFT;
+            if (t < 3) c[t] += 1;
+        }
+        for (int t = 0; t < 3; ++t) {
+            unsigned long long v = c[t];
+            for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+            if ((threadIdx.x & 31) == 0 && v) atomicAdd(&s[t], v);
+        }
+        __syncthreads();
+        if (threadIdx.x < 3) out[(int64_t)b * 3 + threadIdx.x] = (int64_t)s[threadIdx.x];
+        __syncthreads();
+    }
+}
+
 // batches without DISK nodes: packed_off[b] = packed_off[b+1] (packed_off[nseg] = total)
 __global__ void k_classify_fill(int64_t* packed_off, int nseg) {
     if (threadIdx.x != 0) return;
@@ -186,6 +209,25 @@ extern "C" dgnn_status dgnn_classify(dgnn_ctx* c, const dgnn_cache_plan* plan, c
                                 c->stream));
         DGNN_CK(cudaStreamSynchronize(c->stream));
     }
+    return DGNN_OK;
+}
+
+extern "C" dgnn_status dgnn_batch_tier_counts(dgnn_ctx* c, const dgnn_samples* S, int64_t b_lo, int64_t b_hi,
+                                              const uint32_t* addr, int64_t* counts_host) {
+    DGNN_REQUIRE(c && S && counts_host && (addr || b_hi == b_lo), "dgnn_batch_tier_counts: NULL argument");
+    DGNN_REQUIRE(0 <= b_lo && b_lo <= b_hi && b_hi <= S->nb, "dgnn_batch_tier_counts: bad batch range");
+    const int64_t nbg = b_hi - b_lo;
+    if (nbg == 0) return DGNN_OK;
+    DGNN_CK(cudaSetDevice(c->device));
+    DevBuf<int64_t> d;
+    DGNN_TRY(d.alloc(c, (size_t)(3 * nbg)));
+    launch(c, DGNN_K_CLASSIFY, 0.0, [&] {
+        k_tier_counts<<<(int)std::min<int64_t>(nbg, (int64_t)c->num_sms * 8), 256, 0, c->stream>>>(
+            addr, S->node_off + b_lo, S->node_off_h[b_lo], (int)nbg, d.p);
+    });
+    DGNN_CK_LAUNCH();
+    DGNN_CK(cudaMemcpyAsync(counts_host, d.p, sizeof(int64_t) * 3 * nbg, cudaMemcpyDeviceToHost, c->stream));
+    DGNN_CK(cudaStreamSynchronize(c->stream));
     return DGNN_OK;
 }
 

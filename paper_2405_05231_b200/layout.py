@@ -116,6 +116,7 @@ class Layout:
     stats: dict = field(default_factory=dict)
     _asm_plans: dict = field(default_factory=dict)
     stage_pieces: list = field(default_factory=list)  # (b_lo, b_hi, ticket) of each stage-out copy
+    batch_tiers: np.ndarray = None  # [nb, 3] rows per tier (GPU, HOST, DISK) of each batch
 
     def phase_ms(self) -> dict:
         """Device time of the layout's phases (after the stream has passed them)."""
@@ -246,7 +247,9 @@ class Layout:
             chunk_ring = [torch.empty(max(max_c, 16), dtype=torch.uint8, device=dev) for _ in range(2)] \
                 if staged else None
             if windows:
-                cap = min(kh, max(spans[r1 - 1][1] - spans[r0][0] for r0, r1 in windows))
+                # staging rows: the window's host-row accesses bound its distinct host rows
+                hpre = np.concatenate([[0], np.cumsum(self.batch_tiers[:, 1])])
+                cap = min(kh, max(int(hpre[groups[r1 - 1][1]] - hpre[groups[r0][0]]) for r0, r1 in windows))
                 stamp = torch.full((kh,), -1, dtype=torch.int32, device=dev)
                 nbuf = 2 if gctx is not ctx else 1
                 smap = [torch.empty(kh, dtype=torch.int32, device=dev) for _ in range(nbuf)]
@@ -383,6 +386,7 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
     packed_off = torch.empty(nb + 1, dtype=torch.int64, device=dev)
     po = A.dgnn_classify(ctx, plan, samples, 0, nb, addr, packed_ids, packed_off) if nb else np.zeros(1, np.int64)
     rows = np.diff(po)
+    batch_tiers = A.dgnn_batch_tier_counts(ctx, samples, 0, nb, addr) if nb else np.zeros((0, 3), np.int64)
     # a7 layout: groups of `group_size` batches, each a contiguous run of 4 KiB-aligned chunks
     groups = []
     batch_chunk = np.zeros((nb, 2), np.int64)
@@ -411,6 +415,7 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
         raise ValueError(stage)
     L = Layout(ctx, samples, plan, counts, row_bytes, dim, features.dtype, addr, gpu_tier, host_tier, arena,
                arena_dev, groups, batch_chunk, stats)
+    L.batch_tiers = batch_tiers
     stats.update(row_bytes=row_bytes, groups=len(groups), packed_rows=int(po[-1]),
                  packed_bytes=int(po[-1]) * row_bytes, arena_bytes=arena_off,
                  k_gpu=plan.k_gpu, k_host=plan.k_host, total_nodes=total_nodes, total_edges=samples.total_edges)
@@ -457,5 +462,6 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
             A.dgnn_pack(ctx, features, ids, rel_po, rel_co, total, g.group_bytes, dst)
     mark("pack")
     L._rel_all = rel_all
-    L._packed_ids = packed_ids  # read by the pack kernels; released with the layout
+    # packed_ids is only read by the pack kernels on this stream: releasing it now is
+    # stream-ordered, so later allocations on the stream reuse it after the packs
     return L
