@@ -206,6 +206,8 @@ class Runner:
         self.sB = torch.cuda.Stream(dev, priority=int(os.environ.get("DGNN_ASM_PRIORITY", "0")))
         torch.cuda.set_stream(self.sA)
         self.ctxA = dg.Ctx(device=dev, stream=self.sA)
+        if os.environ.get("DGNN_SAMPLE_GROUP"):
+            self.ctxA.set_sample_group(int(os.environ["DGNN_SAMPLE_GROUP"]))
         self.ctxB = dg.Ctx(device=dev, stream=self.sB)
         if pipelined:
             self.ctxB.set_assemble_occupancy(int(os.environ.get("DGNN_ASM_OCC", "8")))

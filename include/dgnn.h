@@ -265,6 +265,22 @@ dgnn_status dgnn_stage_wait(dgnn_ctx* ctx, int64_t ticket);
  * the assembler's stream waiting for a packing group's stage-out. */
 dgnn_status dgnn_stage_wait_stream(dgnn_ctx* ctx, int64_t ticket, void* stream);
 dgnn_status dgnn_stage_sync(dgnn_ctx* ctx, int64_t ticket);
+/* The disk tier as a file on local storage ("creates a disk chunk", "pread ...
+ * O_Direct").  dgnn_file_open opens (create=1: creates / truncates to `size`) a file, with
+ * O_DIRECT when direct=1 (offsets, sizes and the bounce buffer must then be 4096-aligned).
+ * dgnn_stage_file_write / _read move bytes between device memory and the file through a
+ * pinned bounce buffer (host, caller-owned, >= chunk_bytes): on the ctx side stream, each
+ * chunk_bytes piece is one cudaMemcpyAsync plus one pwrite/pread issued in stream order
+ * (cudaLaunchHostFunc), so the ticket completes when the data is on disk / in HBM.  I/O
+ * errors surface as DGNN_EIO at the next dgnn_ctx_sync. */
+typedef struct dgnn_file dgnn_file;
+dgnn_status dgnn_file_open(const char* path, int32_t direct, int32_t create, int64_t size, dgnn_file** out);
+dgnn_status dgnn_file_close(dgnn_file* f);
+dgnn_status dgnn_stage_file_write(dgnn_ctx* ctx, dgnn_file* f, int64_t file_off, const void* dev_src, int64_t bytes,
+                                  void* bounce, int64_t chunk_bytes, int64_t* ticket);
+dgnn_status dgnn_stage_file_read(dgnn_ctx* ctx, dgnn_file* f, int64_t file_off, void* dev_dst, int64_t bytes,
+                                 void* bounce, int64_t chunk_bytes, int64_t* ticket);
+
 /* Pinned, device-mapped host memory for the host tier and the disk-tier arena. */
 dgnn_status dgnn_host_alloc(int64_t bytes, void** out);
 dgnn_status dgnn_host_free(void* p);

@@ -40,6 +40,7 @@ EXPORTS = [
     "dgnn_host_alloc", "dgnn_host_free", "dgnn_assemble", "dgnn_assemble_group", "dgnn_ctx_set_assemble_occupancy",
     "dgnn_host_window", "dgnn_gather_rows_dev", "dgnn_stage_wait_stream", "dgnn_tier_shard_ids",
     "dgnn_shard_requests", "dgnn_scatter_rows", "dgnn_assemble_group_sharded", "dgnn_batch_tier_counts",
+    "dgnn_file_open", "dgnn_file_close", "dgnn_stage_file_write", "dgnn_stage_file_read",
 ]
 
 
@@ -115,6 +116,10 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "dgnn_classify": (i32, [P, P, P, i64, i64, P, P, P, P]),
             "dgnn_chunk_layout": (i32, [P, i64, i64, P]),
             "dgnn_batch_tier_counts": (i32, [P, P, i64, i64, P, P]),
+            "dgnn_file_open": (i32, [ctypes.c_char_p, i32, i32, i64, ctypes.POINTER(P)]),
+            "dgnn_file_close": (i32, [P]),
+            "dgnn_stage_file_write": (i32, [P, P, i64, P, i64, P, i64, ctypes.POINTER(i64)]),
+            "dgnn_stage_file_read": (i32, [P, P, i64, P, i64, P, i64, ctypes.POINTER(i64)]),
             "dgnn_pack": (i32, [P, P, i64, i64, P, P, P, i64, i64, i64, P]),
             "dgnn_gather_rows": (i32, [P, P, i64, i64, P, i64, P]),
             "dgnn_stage_copy": (i32, [P, P, P, i64, i32, ctypes.POINTER(i64)]),
@@ -406,6 +411,36 @@ def dgnn_stage_copy(ctx: Ctx, dst, src, nbytes: int, kind: int) -> int:
     t = i64()
     _check(load_library().dgnn_stage_copy(ctx.handle, _ptr(dst), _ptr(src), int(nbytes), int(kind), ctypes.byref(t)),
            "dgnn_stage_copy")
+    return int(t.value)
+
+
+class DiskFile:
+    """The disk tier as a file (dgnn_file_open); O_DIRECT by default."""
+
+    def __init__(self, path: str, size: int, direct: bool = True, create: bool = True):
+        h = P()
+        _check(load_library().dgnn_file_open(path.encode(), int(direct), int(create), int(size), ctypes.byref(h)),
+               "dgnn_file_open")
+        self.handle, self.path, self.direct, self.size = h, path, direct, size
+        self._finalizer = weakref.finalize(self, load_library().dgnn_file_close, h)
+
+    def close(self):
+        self._finalizer()
+
+
+def dgnn_stage_file_write(ctx: Ctx, f: DiskFile, file_off: int, dev_src, nbytes: int, bounce, chunk_bytes: int):
+    t = i64()
+    _check(load_library().dgnn_stage_file_write(ctx.handle, f.handle, int(file_off), _ptr(dev_src), int(nbytes),
+                                                _ptr(bounce), int(chunk_bytes), ctypes.byref(t)),
+           "dgnn_stage_file_write")
+    return int(t.value)
+
+
+def dgnn_stage_file_read(ctx: Ctx, f: DiskFile, file_off: int, dev_dst, nbytes: int, bounce, chunk_bytes: int):
+    t = i64()
+    _check(load_library().dgnn_stage_file_read(ctx.handle, f.handle, int(file_off), _ptr(dev_dst), int(nbytes),
+                                               _ptr(bounce), int(chunk_bytes), ctypes.byref(t)),
+           "dgnn_stage_file_read")
     return int(t.value)
 
 

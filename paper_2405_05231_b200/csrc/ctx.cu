@@ -1,4 +1,5 @@
 // ctx.cu -- context, errors, allocation, statistics and the a8 staging runtime.
+#include <atomic>
 #include <cstdarg>
 
 #include "internal.cuh"
@@ -69,10 +70,16 @@ dgnn_status memset_async(dgnn_ctx* c, void* p, int value, size_t bytes) {
     return DGNN_OK;
 }
 
+extern std::atomic<int> g_io_error;
+
 dgnn_status check_dev_err(dgnn_ctx* c) {
     int h = 0;
     DGNN_CK(cudaMemcpyAsync(&h, c->dev_err, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     DGNN_CK(cudaStreamSynchronize(c->stream));
+    if (g_io_error.exchange(0)) {
+        set_error("file staging: a pread/pwrite failed or hit end of file");
+        return DGNN_EIO;
+    }
     if (h) {
         DGNN_CK(cudaMemsetAsync(c->dev_err, 0, sizeof(int), c->stream));
         if (h & DEVERR_SEED_RANGE) { set_error("a seed is outside [0, num_nodes)"); return DGNN_EINVAL; }

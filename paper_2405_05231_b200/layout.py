@@ -30,6 +30,9 @@ import torch
 from . import _abi as A
 
 
+FILE_CHUNK = 64 << 20  # bounce-buffer piece for file staging (4096-aligned for O_DIRECT)
+
+
 class HostBuffer:
     """Pinned, device-mapped host memory (dgnn_host_alloc) viewed as a CPU uint8 tensor."""
 
@@ -116,6 +119,7 @@ class Layout:
     stats: dict = field(default_factory=dict)
     _asm_plans: dict = field(default_factory=dict)
     stage_pieces: list = field(default_factory=list)  # (b_lo, b_hi, ticket) of each stage-out copy
+    disk: A.DiskFile | None = None  # the disk tier as a file (stage="file")
     batch_tiers: np.ndarray = None  # [nb, 3] rows per tier (GPU, HOST, DISK) of each batch
 
     def phase_ms(self) -> dict:
@@ -243,7 +247,8 @@ class Layout:
             max_rows = max(s[1] - s[0] for s in spans)
             max_c = max(s[3] - s[2] for s in spans)
             out_ring = [torch.empty((max_rows, self.dim), dtype=self.dtype, device=dev) for _ in range(2)]
-            staged = self.arena is not None
+            staged = self.arena is not None or self.disk is not None
+            bounce_r = HostBuffer(FILE_CHUNK) if self.disk is not None else None
             chunk_ring = [torch.empty(max(max_c, 16), dtype=torch.uint8, device=dev) for _ in range(2)] \
                 if staged else None
             if windows:
@@ -283,7 +288,11 @@ class Layout:
         def stage(i):
             n0, n1, c_lo, c_hi = spans[i]
             self.wait_chunks(ctx.stream, groups[i][1], waited)  # the run's chunks have been staged out
-            tickets[i] = A.dgnn_stage_copy(ctx, chunk_ring[i % 2], self.arena.ptr + c_lo, c_hi - c_lo, 1)
+            if self.disk is not None:  # pread (O_DIRECT) of the run's chunk span, then H2D
+                tickets[i] = A.dgnn_stage_file_read(ctx, self.disk, c_lo, chunk_ring[i % 2], c_hi - c_lo,
+                                                    bounce_r.ptr, FILE_CHUNK)
+            else:
+                tickets[i] = A.dgnn_stage_copy(ctx, chunk_ring[i % 2], self.arena.ptr + c_lo, c_hi - c_lo, 1)
 
         if staged:
             stage(0)
@@ -334,7 +343,8 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
                    seeds: torch.Tensor, fanout, batch_size: int, gpu_rows: int, host_rows: int, rng_seed: int,
                    group_size: int = 64, batch_id_base: int = 0, stage: str = "pinned",
                    counts: torch.Tensor | None = None, ws: Workspace | None = None,
-                   group_budget: int = 4 << 30, stage_piece: int = 1 << 40) -> Layout:
+                   group_budget: int = 4 << 30, stage_piece: int = 1 << 40, file_path: str | None = None,
+                   direct_io: bool = True) -> Layout:
     """Run a1-a8 on this rank's batches.
 
     ``seeds`` are this rank's seeds (batch t of them gets bid = batch_id_base + t).
@@ -406,11 +416,15 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
         batch_chunk[g0:g1, 1] = rows[g0:g1]
         arena_off += int(co[-1])
         g0 = g1
-    arena = arena_dev = None
+    arena = arena_dev = disk = None
     if stage == "pinned":
         arena = ws.host("arena", arena_off) if ws is not None else HostBuffer(arena_off)
     elif stage == "hbm":
         arena_dev = torch.empty(max(arena_off, 16), dtype=torch.uint8, device=dev)
+    elif stage == "file":
+        if not file_path:
+            raise ValueError("stage='file' needs file_path")
+        disk = A.DiskFile(file_path, max(arena_off, 4096), direct=direct_io)
     else:
         raise ValueError(stage)
     L = Layout(ctx, samples, plan, counts, row_bytes, dim, features.dtype, addr, gpu_tier, host_tier, arena,
@@ -429,8 +443,12 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
             [np.concatenate([po[g.b_lo:g.b_hi + 1] - po[g.b_lo], g.chunk_off]) for g in groups]
             or [np.zeros(0, np.int64)]).astype(np.int64)).to(dev, non_blocking=False)
         max_gb = max([g.group_bytes for g in groups], default=0)
+        staged = arena is not None or disk is not None
         L._group_bufs = [torch.empty(max(max_gb, 16), dtype=torch.uint8, device=dev)
-                         for _ in range(min(2, len(groups)))] if arena is not None else []
+                         for _ in range(min(2, len(groups)))] if staged else []
+    if disk is not None:
+        L.disk = disk
+        L._bounce_w = ws.host("bounce_w", FILE_CHUNK) if ws is not None else HostBuffer(FILE_CHUNK)
     bufs = L._group_bufs
     group_last_ticket = []
     off = 0
@@ -440,7 +458,15 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
         off += 2 * k + 2
         ids = packed_ids[int(po[g.b_lo]):int(po[g.b_hi])]
         total = int(po[g.b_hi] - po[g.b_lo])
-        if arena is not None:
+        if disk is not None:  # a8 to a file: pwrite of the whole group through the bounce buffer
+            if gi >= 2:
+                A.dgnn_stage_wait(ctx, group_last_ticket[gi - 2])
+            dst = bufs[gi % 2]
+            A.dgnn_pack(ctx, features, ids, rel_po, rel_co, total, g.group_bytes, dst)
+            t = A.dgnn_stage_file_write(ctx, disk, g.arena_off, dst, g.group_bytes, L._bounce_w.ptr, FILE_CHUNK)
+            L.stage_pieces.append((g.b_lo, g.b_hi, t))
+            group_last_ticket.append(t)
+        elif arena is not None:
             if gi >= 2:
                 A.dgnn_stage_wait(ctx, group_last_ticket[gi - 2])  # its buffer is being reused
             dst = bufs[gi % 2]

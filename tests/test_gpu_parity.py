@@ -6,6 +6,9 @@ Cases span several sampling groups, ragged last batches, fanout 0, fanout >
 32, degree <= fanout, empty packed chunks, 400-byte and 12-byte rows, and the
 degenerate inputs of the method.
 """
+import os
+import tempfile
+
 import numpy as np
 import pytest
 import torch
@@ -169,7 +172,9 @@ def _layout_parity(dg, ctx, w, fan, B, gpu_rows, host_rows, group, stage, host_w
     ref = oracle.offline_layout(ip, ix, feats, sd, B, fan, RNG_SEED, gpu_rows, host_rows, group, threads=8)
     dev = torch.device("cuda", 0)
     L = dg.offline_layout(ctx, w.indptr.to(dev), w.indices.to(dev), w.features.to(dev), w.seeds.to(dev), fan, B,
-                          gpu_rows, host_rows, RNG_SEED, group_size=group, stage=stage)
+                          gpu_rows, host_rows, RNG_SEED, group_size=group, stage=stage,
+                          file_path=os.path.join(tempfile.mkdtemp(prefix="dgnn_disk_"), "chunks.bin")
+                          if stage == "file" else None)
     ctx.sync()
     rb = w.row_bytes
     # a4-a5
@@ -186,7 +191,12 @@ def _layout_parity(dg, ctx, w, fan, B, gpu_rows, host_rows, group, stage, host_w
         assert np.array_equal(addr[n0:n1], ref["addr"][b])
         assert L.batch_chunk[b, 1] == len(ref["packed"][b])
     # a7-a8: every packed group byte-identical (chunks + zero padding)
-    arena = L.arena.tensor.numpy() if L.arena is not None else L.arena_dev.cpu().numpy()
+    if L.arena is not None:
+        arena = L.arena.tensor.numpy()
+    elif L.disk is not None:
+        arena = np.fromfile(L.disk.path, dtype=np.uint8)
+    else:
+        arena = L.arena_dev.cpu().numpy()
     for g, (buf, off) in zip(L.groups, ref["groups"]):
         assert np.array_equal(g.chunk_off, off)
         assert np.array_equal(arena[g.arena_off:g.arena_off + g.group_bytes], buf)
@@ -204,6 +214,11 @@ def _layout_parity(dg, ctx, w, fan, B, gpu_rows, host_rows, group, stage, host_w
 
 def test_offline_layout_parity_tiny(dg, ctx, tiny):
     _layout_parity(dg, ctx, tiny, [10, 5], 256, 500, 1000, 8, "pinned")
+
+
+def test_offline_layout_parity_file_disk_tier(dg, ctx, tiny):
+    """a8 with the disk tier as a file: O_DIRECT pwrite of every packing group, pread back."""
+    _layout_parity(dg, ctx, tiny, [10, 5], 256, 500, 1000, 3, "file", host_window=2, out_budget=1 << 20)
 
 
 @pytest.mark.parametrize("host_window,out_budget", [(1, 1 << 30), (2, 1 << 20), (3, 600_000), (1000, 1 << 20)])
