@@ -67,3 +67,15 @@ def test_errors_without_gpu_are_reported_not_raised(lib):
     with pytest.raises(_abi.DgnnError):
         _abi.Ctx(device=0, stream=None, torch_allocator=False) if False else _abi._check(
             _abi.load_library().dgnn_ctx_create(0, None, None, ctypes.byref(ctypes.c_void_p())), "dgnn_ctx_create")
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    """No CPU fallback: a missing libdgnn.so is an ImportError, not a silent degradation."""
+    import subprocess
+    import sys
+    code = ("import paper_2405_05231_b200._abi as a\n"
+            "a._lib = None\n"
+            "try:\n    a.load_library('/nonexistent/libdgnn.so')\nexcept ImportError as e:\n"
+            "    print('IMPORT_ERROR', e)\n")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=ROOT).stdout
+    assert "IMPORT_ERROR" in out and "no CPU fallback" in out

@@ -85,8 +85,7 @@ def test_products_full_epoch_bit_exact():
 
 def test_sampled_batches_bit_exact(papers):
     L, cfg = papers["L"], papers["cfg"]
-    ref = oracle.sample(papers["indptr"], papers["indices"], papers["seeds"], cfg["batch_size"], list(cfg["fanout"]),
-                        RNG_SEED, batches=SAMPLED, threads=8)
+    ref = _oracle_ref(papers)["samples"]
     S = L.samples
     assert S.num_batches == 1172
     for r in ref:
@@ -101,30 +100,43 @@ def test_sampled_batches_bit_exact(papers):
     assert len(ref[-1].nodes[:ref[-1].hop_off[1]]) == 1_200_000 - 1171 * 1024  # ragged tail batch
 
 
+def _oracle_ref(papers):
+    """The oracle's own view (inputs from the generator only): the sampled batches, the
+    whole-epoch counts and the tier plan.  Computed once per module."""
+    if "ref" not in papers:
+        cfg = papers["cfg"]
+        samples = oracle.sample(papers["indptr"], papers["indices"], papers["seeds"], cfg["batch_size"],
+                                list(cfg["fanout"]), RNG_SEED, batches=SAMPLED, threads=8)
+        counts = np.zeros(cfg["num_nodes"], np.uint32)
+        for t0 in range(0, 1172, 200):  # bounded host memory: stream the oracle's samples
+            part = oracle.sample(papers["indptr"], papers["indices"], papers["seeds"], cfg["batch_size"],
+                                 list(cfg["fanout"]), RNG_SEED, batches=range(t0, min(1172, t0 + 200)), threads=16)
+            oracle.count_frequencies(part, cfg["num_nodes"], counts)
+            del part
+        tm, gpu_ids, host_ids = oracle.select_tiers(counts, papers["gpu_rows"], papers["host_rows"])
+        papers["ref"] = dict(samples=samples, counts=counts, tier_map=tm, gpu_ids=gpu_ids, host_ids=host_ids)
+    return papers["ref"]
+
+
 def test_epoch_counts_and_tier_plan_bit_exact(papers):
-    L, cfg = papers["L"], papers["cfg"]
-    counts = np.zeros(cfg["num_nodes"], np.uint32)
-    for t0 in range(0, 1172, 200):  # bounded host memory: stream the oracle's samples
-        part = oracle.sample(papers["indptr"], papers["indices"], papers["seeds"], cfg["batch_size"],
-                             list(cfg["fanout"]), RNG_SEED, batches=range(t0, min(1172, t0 + 200)), threads=16)
-        oracle.count_frequencies(part, cfg["num_nodes"], counts)
-        del part
-    got = L.counts.cpu().numpy().view(np.uint32)
-    assert np.array_equal(got, counts)
-    tm, gpu_ids, host_ids = oracle.select_tiers(counts, papers["gpu_rows"], papers["host_rows"])
-    assert np.array_equal(L.plan.gpu_ids.cpu().numpy(), gpu_ids)
-    assert np.array_equal(L.plan.host_ids.cpu().numpy(), host_ids)
-    assert np.array_equal(L.plan.tier_map.cpu().numpy().view(np.uint32), tm)
+    L = papers["L"]
+    ref = _oracle_ref(papers)
+    assert np.array_equal(L.counts.cpu().numpy().view(np.uint32), ref["counts"])
+    assert np.array_equal(L.plan.gpu_ids.cpu().numpy(), ref["gpu_ids"])
+    assert np.array_equal(L.plan.host_ids.cpu().numpy(), ref["host_ids"])
+    assert np.array_equal(L.plan.tier_map.cpu().numpy().view(np.uint32), ref["tier_map"])
 
 
 def test_sampled_classify_pack_assemble(papers):
     L, cfg = papers["L"], papers["cfg"]
     dim, rb = cfg["dim"], cfg["dim"] * 4
-    tm = L.plan.tier_map.cpu().numpy().view(np.uint32)
+    ref = _oracle_ref(papers)
+    tm = ref["tier_map"]
+    ref_nodes = {s.bid: s.nodes for s in ref["samples"]}
     arena = L.arena.tensor.numpy()
     S = L.samples
     for b in SAMPLED:
-        nodes = S.nodes[S.node_off_host[b]:S.node_off_host[b + 1]].cpu().numpy()
+        nodes = ref_nodes[b]
         addr, P = oracle.classify(nodes, tm)
         got_addr = L.addr[S.node_off_host[b]:S.node_off_host[b + 1]].cpu().numpy().view(np.uint32)
         assert np.array_equal(got_addr, addr)
@@ -137,7 +149,6 @@ def test_sampled_classify_pack_assemble(papers):
     want = set(SAMPLED)
     for b, out in L.assemble_epoch():
         if b in want:
-            nodes = S.nodes[S.node_off_host[b]:S.node_off_host[b + 1]].cpu().numpy()
-            exp = feature_rows_np(nodes, dim, 1)
+            exp = feature_rows_np(ref_nodes[b], dim, 1)
             assert np.array_equal(out.cpu().numpy().view(np.uint32), exp.view(np.uint32)), f"batch {b}"
     papers["ctx"].sync()

@@ -256,14 +256,14 @@ def test_sharded_gpu_tier_loopback(dg, ctx, tiny, world, host_window):
     tiers = [shard.ShardedTier(ctx, feats, L.plan, r, world) for r in range(world)]
     assert sum(t.rows.shape[0] for t in tiers) == L.plan.k_gpu
     host_feats = tiny.features.numpy()
+    ref = oracle.sample(tiny.indptr.numpy(), tiny.indices.numpy(), tiny.seeds.numpy(), 256, [10, 5], RNG_SEED)
     for r in range(world):
         def remote(c, addr, out, r=r):
             shard.fetch_remote_rows_loopback(c, tiers, r, addr, out)
         for b, out in L.assemble_epoch(host_window=host_window, sharded_tier=tiers[r], remote=remote,
                                        out_budget=600_000):
-            nodes = L.samples.nodes[L.samples.node_off_host[b]:L.samples.node_off_host[b + 1]].cpu().numpy()
             got = out.view(torch.uint8).reshape(out.shape[0], -1).cpu().numpy()
-            assert np.array_equal(got, oracle.assemble(host_feats, nodes)), f"rank {r} batch {b}"
+            assert np.array_equal(got, oracle.assemble(host_feats, ref[b].nodes)), f"rank {r} batch {b}"
     ctx.sync()
 
 
