@@ -382,7 +382,13 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
     plan = A.dgnn_build_cache(ctx, counts, gpu_rows, host_rows)
     mark("plan")
     # tier buffers as special mini-batches
-    gpu_tier = torch.empty((plan.k_gpu, row_bytes), dtype=torch.uint8, device=dev)
+    def buf(name, n, dtype, shape=None):  # per-pass buffers from the workspace (no allocator churn)
+        nbytes = max(int(n), 1) * torch.empty(0, dtype=dtype).element_size()
+        t = ws.dev(name, nbytes, dev)[:nbytes].view(dtype) if ws is not None else \
+            torch.empty(max(int(n), 1), dtype=dtype, device=dev)
+        return t.view(shape) if shape is not None else t
+
+    gpu_tier = buf("gpu_tier", plan.k_gpu * row_bytes, torch.uint8, (plan.k_gpu, row_bytes))
     A.dgnn_gather_rows(ctx, features, plan.gpu_ids, gpu_tier)
     host_tier = ws.host("host_tier", plan.k_host * row_bytes) if ws is not None else \
         HostBuffer(plan.k_host * row_bytes)
@@ -391,8 +397,8 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
     # a6 for every batch of this rank at once
     nb = samples.num_batches
     total_nodes = samples.total_nodes
-    addr = torch.empty(max(total_nodes, 1), dtype=torch.int32, device=dev)
-    packed_ids = torch.empty(max(total_nodes, 1), dtype=torch.int32, device=dev)
+    addr = buf("addr", total_nodes, torch.int32)
+    packed_ids = buf("packed_ids", total_nodes, torch.int32)
     packed_off = torch.empty(nb + 1, dtype=torch.int64, device=dev)
     po = A.dgnn_classify(ctx, plan, samples, 0, nb, addr, packed_ids, packed_off) if nb else np.zeros(1, np.int64)
     rows = np.diff(po)
@@ -444,8 +450,11 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
             or [np.zeros(0, np.int64)]).astype(np.int64)).to(dev, non_blocking=False)
         max_gb = max([g.group_bytes for g in groups], default=0)
         staged = arena is not None or disk is not None
-        L._group_bufs = [torch.empty(max(max_gb, 16), dtype=torch.uint8, device=dev)
-                         for _ in range(min(2, len(groups)))] if staged else []
+        # group buffers come from the workspace when there is one: re-allocating GBs every
+        # pass can force the caching allocator to map memory inside the timed region
+        L._group_bufs = [(ws.dev(f"group_buf{i}", max(max_gb, 16), dev)[:max(max_gb, 16)] if ws is not None
+                          else torch.empty(max(max_gb, 16), dtype=torch.uint8, device=dev))
+                         for i in range(min(2, len(groups)))] if staged else []
     if disk is not None:
         L.disk = disk
         L._bounce_w = ws.host("bounce_w", FILE_CHUNK) if ws is not None else HostBuffer(FILE_CHUNK)
