@@ -34,11 +34,7 @@ import tempfile
 import time
 
 import numpy as np
-
-# two passes of the papers-shaped layout plus 64 GB of inputs come close to the 180 GB of HBM:
-# expandable segments keep the caching allocator from fragmenting (must precede CUDA init)
-os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
-import torch  # noqa: E402
+import torch
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -212,7 +208,9 @@ class Runner:
         if pipelined:
             self.ctxB.set_assemble_occupancy(int(os.environ.get("DGNN_ASM_OCC", "8")))
         N = inp[1].numel() - 1
-        self.ws = [Workspace(), Workspace()]
+        # double-buffered slots only when two passes are in flight
+        w0 = Workspace()
+        self.ws = [w0, Workspace() if pipelined else w0]
         self.counts = [torch.zeros(N, dtype=torch.int32, device=dev) for _ in range(2)]
         cfg = inp[0]
         self.nb = (inp[3].numel() + cfg["batch_size"] - 1) // cfg["batch_size"]
@@ -437,6 +435,7 @@ def main():
         "gpu_launches": int(launches),
         "kernel_ms_per_step_by_stream": per_stream,
         "memory": {"max_reserved_gb": round(torch.cuda.max_memory_reserved(dev) / 1e9, 1),
+                   "max_allocated_gb": round(torch.cuda.max_memory_allocated(dev) / 1e9, 1),
                    "alloc_retries": int(torch.cuda.memory_stats(dev).get("num_alloc_retries", 0)),
                    "cuda_malloc_retries": int(torch.cuda.memory_stats(dev).get("num_device_alloc", 0))},
         "device_timeline_ms": R.timeline_ms(),

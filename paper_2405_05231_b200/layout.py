@@ -386,7 +386,7 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
         nbytes = max(int(n), 1) * torch.empty(0, dtype=dtype).element_size()
         t = ws.dev(name, nbytes, dev)[:nbytes].view(dtype) if ws is not None else \
             torch.empty(max(int(n), 1), dtype=dtype, device=dev)
-        return t.view(shape) if shape is not None else t
+        return t[:int(n)].view(shape) if shape is not None else t
 
     gpu_tier = buf("gpu_tier", plan.k_gpu * row_bytes, torch.uint8, (plan.k_gpu, row_bytes))
     A.dgnn_gather_rows(ctx, features, plan.gpu_ids, gpu_tier)
