@@ -21,6 +21,9 @@ Functions and the passage each follows:
 * ``chunk_offsets``, ``pack`` -- batched packing.
 * ``gather_rows``       -- tier buffers and direct-gather assembly.
 * ``assemble_tiers``    -- three-source reconstruction.
+* ``disk_space``, ``disk_search``, ``disk_perm``, ``disk_plan``,
+  ``disk_cache_fill``   -- segmented disk cache, Eq. 2 and Algorithm 1,
+  P:311-414 (readings d1-d8 in dgnn_oracle.c and DESIGN.md).
 """
 from __future__ import annotations
 
@@ -90,6 +93,12 @@ def _L():
             lib.oracle_gather_rows.argtypes = [P, i64, P, i64, P]
             lib.oracle_assemble_tiers.argtypes = [P, i64, P, i64, P, i64, P, i64, i64, P]
             lib.oracle_assemble_tiers.restype = ctypes.c_int
+            lib.oracle_disk_space.argtypes = [P, P, i64, i64, i64, i64, i64, P]
+            lib.oracle_disk_search.argtypes = [P, P, i64, i64, i64, i64, i64, P, P]
+            lib.oracle_disk_perm.argtypes = [u64, i64, i64, i64, P]
+            lib.oracle_disk_plan.argtypes = [P, P, i64, i64, i64, i64, i64, i32, u64, i32,
+                                             P, P, P, P, P, P, P, P, P]
+            lib.oracle_disk_cache_fill.argtypes = [P, i64, P, P, P, i64, P]
             _lib = lib
     return _lib
 
@@ -312,3 +321,121 @@ def offline_layout(indptr, indices, features, seeds, batch_size, fanout, rng_see
     return dict(samples=samples, counts=counts, tier_map=tier_map, gpu_ids=gpu_ids, host_ids=host_ids,
                 addr=addrs, packed=plists, groups=groups,
                 gpu_buf=gather_rows(features, gpu_ids), host_buf=gather_rows(features, host_ids))
+
+
+# ------------------------------------------------- segmented disk cache ----
+PAGE = 4096
+
+
+def _packed_concat(packed_lists):
+    rows = np.array([len(p) for p in packed_lists], np.int64)
+    off = np.zeros(len(rows) + 1, np.int64)
+    np.cumsum(rows, out=off[1:])
+    cat = (np.concatenate([np.asarray(p, np.int32) for p in packed_lists]) if len(packed_lists)
+           else np.zeros(0, np.int32))
+    return _c(cat, np.int32), off
+
+
+def disk_space(packed_lists, num_nodes: int, row_bytes: int, s: int, m: int) -> int:
+    """Eq. 2 space of (s, m) in 4096-byte pages (readings d1-d3)."""
+    cat, off = _packed_concat(packed_lists)
+    out = np.zeros(1, np.int64)
+    rc = _L().oracle_disk_space(_p(cat), _p(off), len(off) - 1, num_nodes, row_bytes, s, m, _p(out))
+    if rc != 0:
+        raise OracleError(rc, "disk_space")
+    return int(out[0])
+
+
+def disk_search(packed_lists, num_nodes: int, row_bytes: int, budget_pages: int, m: int = 1):
+    """Heuristic of P:410-413: (minimum s with space <= budget or 0, its space)."""
+    cat, off = _packed_concat(packed_lists)
+    s_out = np.zeros(1, np.int64)
+    pg = np.zeros(1, np.int64)
+    rc = _L().oracle_disk_search(_p(cat), _p(off), len(off) - 1, num_nodes, row_bytes, m, budget_pages,
+                                 _p(s_out), _p(pg))
+    if rc != 0:
+        raise OracleError(rc, "disk_search")
+    return int(s_out[0]), int(pg[0])
+
+
+def disk_perm(seed: int, g: int, t: int, n: int) -> np.ndarray:
+    """Permutation H_t of the n local batch indices of segment g (reading d5)."""
+    H = np.zeros(max(n, 1), np.int64)
+    rc = _L().oracle_disk_perm(seed, g, t, n, _p(H))
+    if rc != 0:
+        raise OracleError(rc, "disk_perm")
+    return H[:n].copy()
+
+
+@dataclass
+class DiskPlan:
+    s: int
+    m: int
+    seg_off: np.ndarray        # int64 [nseg+1]
+    cache_ids: np.ndarray      # int32 [seg_off[-1]] (V_r of every segment)
+    seg_page_off: np.ndarray   # int64 [nseg+1]
+    pk_ids: np.ndarray         # int32 (P_b' concatenated)
+    pk_off: np.ndarray         # int64 [nb+1]
+    req_pages: np.ndarray      # int64 (merged page requests)
+    req_off: np.ndarray        # int64 [nb+1]
+    dc_addr: np.ndarray        # uint32 [R] (reading d8)
+    space_pages: int
+    io_pages: int
+    cache_pages: int
+    chunk_pages: int
+
+
+def disk_plan(packed_lists, num_nodes: int, row_bytes: int, s: int, m: int, k: int = 4, seed: int = 0,
+              reorder: bool = True) -> DiskPlan:
+    """Segments, V_d, Algorithm 1 order, P_b', merged requests (d1-d8)."""
+    cat, off = _packed_concat(packed_lists)
+    nb = len(off) - 1
+    R = int(off[-1])
+    nseg = (nb + s - 1) // s if s >= 1 else 0
+    cap = max(R, 1)
+    seg_off = np.zeros(nseg + 1, np.int64)
+    seg_page_off = np.zeros(nseg + 1, np.int64)
+    cache_ids = np.zeros(cap, np.int32)
+    pk_ids = np.zeros(cap, np.int32)
+    pk_off = np.zeros(nb + 1, np.int64)
+    req_pages = np.zeros(cap, np.int64)
+    req_off = np.zeros(nb + 1, np.int64)
+    dc_addr = np.zeros(cap, np.uint32)
+    tot = np.zeros(4, np.int64)
+    rc = _L().oracle_disk_plan(_p(cat), _p(off), nb, num_nodes, row_bytes, s, m, k, seed, int(reorder),
+                               _p(seg_off), _p(cache_ids), _p(seg_page_off), _p(pk_ids), _p(pk_off),
+                               _p(req_pages), _p(req_off), _p(dc_addr), _p(tot))
+    if rc != 0:
+        raise OracleError(rc, "disk_plan")
+    return DiskPlan(s=s, m=m, seg_off=seg_off, cache_ids=cache_ids[: seg_off[-1]].copy(),
+                    seg_page_off=seg_page_off, pk_ids=pk_ids[: pk_off[-1]].copy(), pk_off=pk_off,
+                    req_pages=req_pages[: req_off[-1]].copy(), req_off=req_off, dc_addr=dc_addr[:R].copy(),
+                    space_pages=int(tot[0]), io_pages=int(tot[1]), cache_pages=int(tot[2]),
+                    chunk_pages=int(tot[3]))
+
+
+def disk_cache_fill(features, plan: DiskPlan) -> np.ndarray:
+    """The segment caches as bytes: V_r rows, fpp per 4096-byte page, zero tails."""
+    f = _rows_u8(features)
+    row_bytes = f.shape[1]
+    nseg = len(plan.seg_off) - 1
+    out = np.zeros(int(plan.seg_page_off[-1]) * PAGE, np.uint8)
+    ids = _c(plan.cache_ids, np.int32)
+    _L().oracle_disk_cache_fill(_p(f), row_bytes, _p(ids), _p(_c(plan.seg_off, np.int64)),
+                                _p(_c(plan.seg_page_off, np.int64)), nseg, _p(out))
+    return out
+
+
+def disk_partial_input(chunk: np.ndarray, pages: np.ndarray, dc_addr_b: np.ndarray, row_bytes: int) -> np.ndarray:
+    """Partial input of one batch: its DISK rows in local order, read from its
+    packed chunk (dc_addr < 2^31: chunk row) or its fetched cache pages (d8)."""
+    fpp = PAGE // row_bytes
+    out = np.zeros((len(dc_addr_b), row_bytes), np.uint8)
+    for r, a in enumerate(np.asarray(dc_addr_b, np.uint64)):
+        a = int(a)
+        if a >> 31:
+            q, slot = divmod(a & 0x7FFFFFFF, fpp)
+            out[r] = pages[q * PAGE + slot * row_bytes: q * PAGE + (slot + 1) * row_bytes]
+        else:
+            out[r] = chunk[a * row_bytes:(a + 1) * row_bytes]
+    return out

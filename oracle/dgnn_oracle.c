@@ -425,3 +425,282 @@ int oracle_assemble_tiers(const uint32_t* addr, int64_t n, const uint8_t* gpu_bu
     }
     return OR_OK;
 }
+
+/* ======================================================================== */
+/* Segmented disk cache (Sec. 5.1).          */
+/*                                                                          */
+/* Input: the packed lists P_b of an epoch (the DISK-tier nodes of each      */
+/* batch in local order, as oracle_classify returns them, concatenated with  */
+/* offsets packed_off[nb+1]).  Readings (DESIGN.md d1-d8):                   */
+/*  d1 segments = consecutive batches [g*s, min((g+1)*s, nb)).   */
+/*  d2 local frequency of v in segment g = number of the segment's batches   */
+/*     whose P_b holds v; > m -> disk cache V_d of g, <= m -> stays packed    */
+/*     in every P_b that holds it.  m = 0 is allowed (pure cache).    */
+/*  d3 space (Eq. 2) in 4096-byte pages: per segment              */
+/*     ceil(|V_d| / fpp) with fpp = floor(4096 / row_bytes) rows per page    */
+/*     (a cached row never straddles a page), per batch ceil(|P_b'| *        */
+/*     row_bytes / 4096) (the chunk of reading c20).  Constraint: <= budget.  */
+/*  d4 heuristic: m = 1 (caller's choice), s = the minimum s in   */
+/*     1..nb with space <= budget, by linear scan.                           */
+/*  d5 Permute (Alg. 1 line 3): H_t(i) for local batch index i of segment g   */
+/*     = rank of i when the segment's indices are ordered by (x_t(i), i),     */
+/*     x_t(i) = Philox4x32-10(ctr = {i, g, t, 0x4D48}, key = seed) as         */
+/*     out.y << 32 | out.x.                                                  */
+/*  d6 signature (Alg. 1 lines 4-8) read per hash function: S_t(v) =          */
+/*     min over the segment's batches i holding v of H_t(i) (the MinHash      */
+/*     signature of HashOrder); V_r = V_d sorted by (S_0..S_{k-1}, v)         */
+/*     lexicographically (line 9).  For k = 1 this is Algorithm 1 verbatim.  */
+/*     reorder = 0 gives the identity order (ascending v) for comparison.    */
+/*  d7 I/O (Eq. 2 objective): per batch ceil(|P_b'| * row_bytes / 4096)      */
+/*     chunk pages + the number of distinct cache pages holding D_b          */
+/*     (requests to one page merged).                                 */
+/*  d8 disk address of the r-th packed row of batch b (local DISK order):     */
+/*     cached -> 1 << 31 | (q * fpp + slot), q = index of its page in the     */
+/*     batch's ascending request list, slot = position inside the page;      */
+/*     packed -> rank of the row in P_b'.                                    */
+/* ======================================================================== */
+#define DC_PAGE 4096
+
+static int64_t dc_chunk_pages(int64_t rows, int64_t row_bytes)
+{
+    return (rows * row_bytes + DC_PAGE - 1) / DC_PAGE;
+}
+
+/* Eq. 2 space of configuration (s, m), in pages (d1-d3). */
+int oracle_disk_space(const int32_t* packed_ids, const int64_t* packed_off, int64_t nb, int64_t num_nodes,
+                      int64_t row_bytes, int64_t s, int64_t m, int64_t* pages_out)
+{
+    if (s < 1 || m < 0 || row_bytes < 1 || row_bytes > DC_PAGE) return OR_EINVAL;
+    int64_t fpp = DC_PAGE / row_bytes;
+    uint32_t* cnt = (uint32_t*)calloc((size_t)(num_nodes > 0 ? num_nodes : 1), sizeof(uint32_t));
+    if (!cnt) return OR_ENOMEM;
+    int64_t total = 0;
+    for (int64_t g0 = 0; g0 < nb; g0 += s) {
+        int64_t g1 = g0 + s < nb ? g0 + s : nb;
+        for (int64_t b = g0; b < g1; ++b)
+            for (int64_t r = packed_off[b]; r < packed_off[b + 1]; ++r) cnt[packed_ids[r]] += 1;
+        for (int64_t b = g0; b < g1; ++b) {
+            int64_t kept = 0;
+            for (int64_t r = packed_off[b]; r < packed_off[b + 1]; ++r)
+                if (cnt[packed_ids[r]] <= (uint64_t)m) kept += 1;
+            total += dc_chunk_pages(kept, row_bytes);
+        }
+        int64_t cached = 0;
+        for (int64_t b = g0; b < g1; ++b)
+            for (int64_t r = packed_off[b]; r < packed_off[b + 1]; ++r)
+                if (cnt[packed_ids[r]] > (uint64_t)m) { cached += 1; cnt[packed_ids[r]] = 0; }
+        total += (cached + fpp - 1) / fpp;
+        for (int64_t b = g0; b < g1; ++b)
+            for (int64_t r = packed_off[b]; r < packed_off[b + 1]; ++r) cnt[packed_ids[r]] = 0;
+    }
+    free(cnt);
+    *pages_out = total;
+    return OR_OK;
+}
+
+/* Heuristic search (d4): s_out = minimum feasible s, or 0 when even s = nb
+ * exceeds the budget; pages_out = the space of s_out (of s = nb if infeasible). */
+int oracle_disk_search(const int32_t* packed_ids, const int64_t* packed_off, int64_t nb, int64_t num_nodes,
+                       int64_t row_bytes, int64_t m, int64_t budget_pages, int64_t* s_out, int64_t* pages_out)
+{
+    int64_t sp = 0;
+    int64_t s_max = nb > 0 ? nb : 1;
+    for (int64_t s = 1; s <= s_max; ++s) {
+        int rc = oracle_disk_space(packed_ids, packed_off, nb, num_nodes, row_bytes, s, m, &sp);
+        if (rc) return rc;
+        if (sp <= budget_pages) { *s_out = s; *pages_out = sp; return OR_OK; }
+    }
+    *s_out = 0;
+    *pages_out = sp;
+    return OR_OK;
+}
+
+/* d5: one permutation H of the n local batch indices of segment g. */
+typedef struct { uint64_t x; int64_t i; } dc_key;
+
+static int cmp_dc_key(const void* a, const void* b)
+{
+    const dc_key* p = (const dc_key*)a;
+    const dc_key* q = (const dc_key*)b;
+    if (p->x != q->x) return p->x < q->x ? -1 : 1;
+    return (p->i > q->i) - (p->i < q->i);
+}
+
+int oracle_disk_perm(uint64_t seed, int64_t g, int64_t t, int64_t n, int64_t* H)
+{
+    dc_key* keys = (dc_key*)malloc((size_t)(n > 0 ? n : 1) * sizeof(dc_key));
+    if (!keys) return OR_ENOMEM;
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    for (int64_t i = 0; i < n; ++i) {
+        uint32_t ctr[4] = {(uint32_t)i, (uint32_t)g, (uint32_t)t, 0x4D48u};
+        uint32_t out[4];
+        oracle_philox4x32_10(ctr, key, out);
+        keys[i].x = ((uint64_t)out[1] << 32) | out[0];
+        keys[i].i = i;
+    }
+    qsort(keys, (size_t)n, sizeof(dc_key), cmp_dc_key);
+    for (int64_t p = 0; p < n; ++p) H[keys[p].i] = p;
+    free(keys);
+    return OR_OK;
+}
+
+/* cache entry of one segment for the Line-9 sort */
+typedef struct { int32_t v; int32_t k; const int64_t* sig; } dc_entry;
+
+static int cmp_dc_entry(const void* a, const void* b)
+{
+    const dc_entry* p = (const dc_entry*)a;
+    const dc_entry* q = (const dc_entry*)b;
+    for (int32_t t = 0; t < p->k; ++t)
+        if (p->sig[t] != q->sig[t]) return p->sig[t] < q->sig[t] ? -1 : 1;
+    return (p->v > q->v) - (p->v < q->v);
+}
+
+static int cmp_i64_asc(const void* a, const void* b)
+{
+    int64_t x = *(const int64_t*)a, y = *(const int64_t*)b;
+    return (x > y) - (x < y);
+}
+
+/* Full plan for (s, m) (d1-d8).  Output capacities: R = packed_off[nb] rows.
+ *   seg_off[nseg+1]       prefix of |V_d| per segment; cache_ids[R]: V_r of every
+ *                         segment, concatenated (segment g at seg_off[g]).
+ *   seg_page_off[nseg+1]  prefix of cache pages per segment.
+ *   pk_ids[R], pk_off[nb+1]       the reduced packed lists P_b'.
+ *   req_pages[R], req_off[nb+1]   per batch, the ascending distinct global cache
+ *                                 pages (seg_page_off[g] + page in segment).
+ *   dc_addr[R]                     d8, one per packed row of the input.
+ *   totals[4] = {space pages, io pages, cache pages, chunk pages}. */
+int oracle_disk_plan(const int32_t* packed_ids, const int64_t* packed_off, int64_t nb, int64_t num_nodes,
+                     int64_t row_bytes, int64_t s, int64_t m, int32_t k, uint64_t seed, int32_t reorder,
+                     int64_t* seg_off, int32_t* cache_ids, int64_t* seg_page_off, int32_t* pk_ids, int64_t* pk_off,
+                     int64_t* req_pages, int64_t* req_off, uint32_t* dc_addr, int64_t* totals)
+{
+    if (s < 1 || m < 0 || k < 1 || row_bytes < 1 || row_bytes > DC_PAGE) return OR_EINVAL;
+    int64_t fpp = DC_PAGE / row_bytes;
+    int64_t N = num_nodes > 0 ? num_nodes : 1;
+    uint32_t* cnt = (uint32_t*)calloc((size_t)N, sizeof(uint32_t));
+    int64_t* ent = (int64_t*)malloc((size_t)N * sizeof(int64_t));  /* v -> entry index, -1 if none */
+    int64_t R = packed_off[nb];
+    int64_t cap = R > 0 ? R : 1;
+    dc_entry* es = (dc_entry*)malloc((size_t)cap * sizeof(dc_entry));
+    int64_t* sig = (int64_t*)malloc((size_t)cap * (size_t)k * sizeof(int64_t));
+    int64_t* rank = (int64_t*)malloc((size_t)cap * sizeof(int64_t));  /* entry (by v) -> position in V_r */
+    int64_t* H = (int64_t*)malloc((size_t)(s > 0 ? s : 1) * (size_t)k * sizeof(int64_t));
+    int64_t* pages = (int64_t*)malloc((size_t)cap * sizeof(int64_t));
+    if (!cnt || !ent || !es || !sig || !rank || !H || !pages) {
+        free(cnt); free(ent); free(es); free(sig); free(rank); free(H); free(pages);
+        return OR_ENOMEM;
+    }
+    for (int64_t v = 0; v < N; ++v) ent[v] = -1;
+    int64_t nseg = (nb + s - 1) / s;
+    int64_t n_cache = 0, n_pk = 0, n_req = 0, cache_pages = 0, chunk_pages = 0, io = 0;
+    seg_off[0] = 0;
+    seg_page_off[0] = 0;
+    pk_off[0] = 0;
+    req_off[0] = 0;
+    for (int64_t g = 0; g < nseg; ++g) {
+        int64_t g0 = g * s, g1 = g0 + s < nb ? g0 + s : nb, sg = g1 - g0;
+        /* d2: local frequencies */
+        for (int64_t b = g0; b < g1; ++b)
+            for (int64_t r = packed_off[b]; r < packed_off[b + 1]; ++r) cnt[packed_ids[r]] += 1;
+        /* V_d of the segment, first-seen order (re-sorted below) */
+        int64_t e0 = n_cache, ne = 0;
+        for (int64_t b = g0; b < g1; ++b)
+            for (int64_t r = packed_off[b]; r < packed_off[b + 1]; ++r) {
+                int32_t v = packed_ids[r];
+                if (cnt[v] > (uint64_t)m && ent[v] < 0) {
+                    ent[v] = ne;
+                    es[ne].v = v;
+                    es[ne].k = k;
+                    es[ne].sig = sig + ne * k;
+                    for (int32_t t = 0; t < k; ++t) sig[ne * k + t] = INT64_MAX;  /* Alg. 1 line 1: inf */
+                    ne += 1;
+                }
+            }
+        /* Alg. 1 lines 2-3: k permutations of the local batch indices (d5) */
+        for (int32_t t = 0; t < k; ++t) {
+            int rc = oracle_disk_perm(seed, g, t, sg, H + (int64_t)t * sg);
+            if (rc) { free(cnt); free(ent); free(es); free(sig); free(rank); free(H); free(pages); return rc; }
+        }
+        /* Alg. 1 lines 4-8 (d6) */
+        for (int64_t i = 0; i < sg; ++i) {
+            int64_t b = g0 + i;
+            for (int64_t r = packed_off[b]; r < packed_off[b + 1]; ++r) {
+                int64_t e = ent[packed_ids[r]];
+                if (e < 0) continue;  /* line 5: V_i intersect V_d */
+                for (int32_t t = 0; t < k; ++t)
+                    if (H[(int64_t)t * sg + i] < sig[e * k + t]) sig[e * k + t] = H[(int64_t)t * sg + i];
+            }
+        }
+        /* line 9: V_r = V_d[Sort(S)] */
+        if (reorder) {
+            qsort(es, (size_t)ne, sizeof(dc_entry), cmp_dc_entry);
+        } else {
+            for (int64_t e = 0; e < ne; ++e) es[e].k = 0;  /* compare by v only */
+            qsort(es, (size_t)ne, sizeof(dc_entry), cmp_dc_entry);
+        }
+        for (int64_t p = 0; p < ne; ++p) {
+            cache_ids[e0 + p] = es[p].v;
+            rank[ent[es[p].v]] = p;
+        }
+        n_cache += ne;
+        seg_off[g + 1] = n_cache;
+        int64_t segp = (ne + fpp - 1) / fpp;
+        seg_page_off[g + 1] = seg_page_off[g] + segp;
+        cache_pages += segp;
+        /* per batch: P_b', merged page requests, disk addresses (d7, d8) */
+        for (int64_t b = g0; b < g1; ++b) {
+            int64_t kept = 0, np = 0;
+            for (int64_t r = packed_off[b]; r < packed_off[b + 1]; ++r) {
+                int32_t v = packed_ids[r];
+                if (ent[v] >= 0) pages[np++] = seg_page_off[g] + rank[ent[v]] / fpp;
+                else { pk_ids[n_pk + kept] = v; dc_addr[r] = (uint32_t)kept; kept += 1; }
+            }
+            qsort(pages, (size_t)np, sizeof(int64_t), cmp_i64_asc);
+            int64_t nu = 0;
+            for (int64_t q = 0; q < np; ++q)
+                if (nu == 0 || pages[q] != req_pages[n_req + nu - 1]) { req_pages[n_req + nu] = pages[q]; nu += 1; }
+            for (int64_t r = packed_off[b]; r < packed_off[b + 1]; ++r) {
+                int32_t v = packed_ids[r];
+                if (ent[v] < 0) continue;
+                int64_t pos = rank[ent[v]];
+                int64_t pg = seg_page_off[g] + pos / fpp;
+                int64_t q = 0;
+                while (req_pages[n_req + q] != pg) q += 1;
+                dc_addr[r] = 0x80000000u | (uint32_t)(q * fpp + pos % fpp);
+            }
+            n_pk += kept;
+            pk_off[b + 1] = n_pk;
+            n_req += nu;
+            req_off[b + 1] = n_req;
+            chunk_pages += dc_chunk_pages(kept, row_bytes);
+            io += dc_chunk_pages(kept, row_bytes) + nu;
+        }
+        for (int64_t b = g0; b < g1; ++b)
+            for (int64_t r = packed_off[b]; r < packed_off[b + 1]; ++r) {
+                cnt[packed_ids[r]] = 0;
+                ent[packed_ids[r]] = -1;
+            }
+    }
+    totals[0] = cache_pages + chunk_pages;
+    totals[1] = io;
+    totals[2] = cache_pages;
+    totals[3] = chunk_pages;
+    free(cnt); free(ent); free(es); free(sig); free(rank); free(H); free(pages);
+    return OR_OK;
+}
+
+/* Materialized segment caches ("laid out on disk by reordering"): the rows of
+ * V_r of segment g fill pages seg_page_off[g].. in order, fpp rows per page at
+ * slot * row_bytes; the rest of every page is zero. */
+void oracle_disk_cache_fill(const uint8_t* features, int64_t row_bytes, const int32_t* cache_ids,
+                            const int64_t* seg_off, const int64_t* seg_page_off, int64_t nseg, uint8_t* out)
+{
+    int64_t fpp = DC_PAGE / row_bytes;
+    memset(out, 0, (size_t)(seg_page_off[nseg] * DC_PAGE));
+    for (int64_t g = 0; g < nseg; ++g)
+        for (int64_t p = 0; p < seg_off[g + 1] - seg_off[g]; ++p)
+            memcpy(out + (seg_page_off[g] + p / fpp) * DC_PAGE + (p % fpp) * row_bytes,
+                   features + (int64_t)cache_ids[seg_off[g] + p] * row_bytes, (size_t)row_bytes);
+}

@@ -1,0 +1,251 @@
+"""Pins for the oracle's segmented disk cache (Sec. 5.1; readings d1-d8).
+
+* Fig. 4: {0,2,4,6} reads 4 pages in ID order and 2 after MinHash reordering,
+  for every k (golden fixture fig4_reorder.txt).
+* SPEC examples: segment grouping, m >= s empties the cache, a shared
+  node is cached and leaves the packed lists, the page ceiling.
+* Brute force: every output of oracle.disk_plan / disk_space / disk_search is recomputed
+  here from the definitions with Python sets, sorted() and the KAT-pinned Philox
+  (oracle.philox4x32_10) on random fixtures -- a dropped term, a wrong comparison or
+  an off-by-one segment boundary in the C code fails one of them.
+* Algorithm 1 verbatim (scalar S(v), line 8) coincides with reading d6 at k = 1; nodes with
+  identical batch sets are contiguous in V_r up to signature
+  collisions broken by ID, for every k.
+* Reconstruction: cache pages + reduced chunks + d8 addresses give back the batch's DISK
+  rows byte for byte (closed-form features, numpy transcription).
+"""
+import itertools
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import golden_lines
+from workload import feature_rows_np
+
+PAGE = 4096
+
+
+# ------------------------------------------------------------- brute force ----
+def bf_perm(seed, g, t, n):
+    xs = []
+    for i in range(n):
+        o = oracle.philox4x32_10([i, g, t, 0x4D48], [seed & 0xFFFFFFFF, seed >> 32])
+        xs.append(((o[1] << 32) | o[0], i))
+    H = [0] * n
+    for p, (_, i) in enumerate(sorted(xs)):
+        H[i] = p
+    return H
+
+
+def bf_plan(plists, row_bytes, s, m, k, seed, reorder=True):
+    fpp = PAGE // row_bytes
+    nb = len(plists)
+    out = dict(seg_off=[0], cache_ids=[], seg_page_off=[0], pk=[], req=[], addr=[], space=0, io=0)
+    for g, g0 in enumerate(range(0, nb, s)):
+        seg = [list(map(int, p)) for p in plists[g0:g0 + s]]
+        freq = {}
+        for p in seg:
+            for v in set(p):
+                freq[v] = freq.get(v, 0) + 1
+        Vd = sorted(v for v, c in freq.items() if c > m)
+        H = [bf_perm(seed, g, t, len(seg)) for t in range(k)]
+        sig = {v: tuple(min(H[t][i] for i, p in enumerate(seg) if v in p) for t in range(k)) for v in Vd}
+        Vr = sorted(Vd, key=lambda v: (sig[v], v)) if reorder else Vd
+        pos = {v: i for i, v in enumerate(Vr)}
+        out["cache_ids"] += Vr
+        out["seg_off"].append(out["seg_off"][-1] + len(Vr))
+        npg = -(-len(Vr) // fpp)
+        base = out["seg_page_off"][-1]
+        out["seg_page_off"].append(base + npg)
+        out["space"] += npg
+        for p in seg:
+            kept = [v for v in p if freq[v] <= m]
+            pages = sorted({base + pos[v] // fpp for v in p if v in pos})
+            addr = []
+            for v in p:
+                if v in pos:
+                    addr.append((1 << 31) | (pages.index(base + pos[v] // fpp) * fpp + pos[v] % fpp))
+                else:
+                    addr.append(kept.index(v))
+            out["pk"].append(kept)
+            out["req"].append(pages)
+            out["addr"].append(addr)
+            cp = -(-len(kept) * row_bytes // PAGE)
+            out["space"] += cp
+            out["io"] += cp + len(pages)
+    return out
+
+
+def bf_space(plists, row_bytes, s, m):
+    return bf_plan(plists, row_bytes, s, m, 1, 0)["space"]
+
+
+def random_plists(rng, nb, n_nodes, lo, hi, skew=1.0):
+    w = rng.random(n_nodes) ** skew
+    w /= w.sum()
+    out = []
+    for _ in range(nb):
+        sz = int(rng.integers(lo, hi + 1))
+        out.append(rng.choice(n_nodes, size=min(sz, n_nodes), replace=False, p=w).astype(np.int32))
+    return out
+
+
+def split(a, off):
+    return [a[off[i]:off[i + 1]].tolist() for i in range(len(off) - 1)]
+
+
+# ----------------------------------------------------------------- pins ----
+def _fig4():
+    g = {"batch": []}
+    for line in golden_lines("fig4_reorder.txt"):
+        key, *rest = line.split()
+        if key == "batch":
+            g["batch"].append([int(x) for x in rest])
+        else:
+            g[key] = [int(x) for x in rest]
+    return g
+
+
+@pytest.mark.parametrize("k", [1, 2, 4, 8])
+def test_fig4_reordering_halves_the_pages(k):
+    g = _fig4()
+    row_bytes = PAGE // g["fpp"][0]
+    ident = oracle.disk_plan(g["batch"], g["num_nodes"][0], row_bytes, s=2, m=0, k=k, reorder=False)
+    reord = oracle.disk_plan(g["batch"], g["num_nodes"][0], row_bytes, s=2, m=0, k=k, seed=11)
+    assert np.diff(ident.req_off).tolist() == g["identity_pages"]
+    assert np.diff(reord.req_off).tolist() == g["reordered_pages"]
+    # {0,2} and {4,6} share pages after reordering
+    pos = {int(v): i for i, v in enumerate(reord.cache_ids)}
+    assert pos[0] // 2 == pos[2] // 2 and pos[4] // 2 == pos[6] // 2
+
+
+def test_spec_examples():
+    # n=4, s=2 -> segments {0,1},{2,3}
+    pl = [[1, 2], [2, 3], [4, 5], [5, 6]]
+    d = oracle.disk_plan(pl, 8, 512, s=2, m=1)
+    assert len(d.seg_off) == 3
+    assert d.cache_ids.tolist() == [2, 5] and d.seg_off.tolist() == [0, 1, 2]
+    # shared node cached and in no packed list
+    assert 5 not in d.pk_ids.tolist() and 2 not in d.pk_ids.tolist()
+    # m >= s -> empty cache, everything packed
+    d = oracle.disk_plan(pl, 8, 512, s=2, m=2)
+    assert d.cache_ids.size == 0 and d.pk_ids.tolist() == [1, 2, 2, 3, 4, 5, 5, 6]
+    assert d.space_pages == 4 and d.io_pages == 4
+    # one segment, cache of 3 rows, fpp=2 -> 2 pages
+    d = oracle.disk_plan([[0, 1, 2], [0, 1, 2]], 3, 2048, s=2, m=1)
+    assert d.cache_pages == 2 and d.chunk_pages == 0 and d.space_pages == 2
+    # empty input -> zero space, s = 1 feasible
+    assert oracle.disk_space([], 4, 512, 1, 1) == 0
+    assert oracle.disk_search([], 4, 512, 0) == (1, 0)
+
+
+def test_single_batch_segment_is_ascending():
+    pl = [[9, 3, 7, 1]]
+    d = oracle.disk_plan(pl, 10, 1024, s=1, m=0, k=4, seed=5)
+    assert d.cache_ids.tolist() == [1, 3, 7, 9]
+    assert d.req_off.tolist() == [0, 1]
+
+
+def test_perm_is_the_philox_ranking():
+    for (seed, g, t, n) in [(0, 0, 0, 1), (1, 0, 0, 10), (7, 3, 2, 37), (2**40 + 5, 12, 7, 64)]:
+        H = oracle.disk_perm(seed, g, t, n)
+        assert sorted(H.tolist()) == list(range(n))
+        assert H.tolist() == bf_perm(seed, g, t, n)
+
+
+@pytest.mark.parametrize("trial", range(40))
+def test_plan_equals_brute_force(trial):
+    rng = np.random.default_rng(100 + trial)
+    nb = int(rng.integers(1, 9))
+    n_nodes = int(rng.integers(8, 64))
+    pl = random_plists(rng, nb, n_nodes, 0, 20, skew=3.0)
+    row_bytes = int(rng.choice([512, 1024, 400, 4096, 2048]))
+    s = int(rng.integers(1, nb + 2))
+    m = int(rng.integers(0, 3))
+    k = int(rng.integers(1, 5))
+    seed = int(rng.integers(0, 2**63))
+    reorder = bool(rng.integers(0, 2))
+    d = oracle.disk_plan(pl, n_nodes, row_bytes, s, m, k, seed, reorder)
+    e = bf_plan(pl, row_bytes, s, m, k, seed, reorder)
+    assert d.seg_off.tolist() == e["seg_off"]
+    assert d.cache_ids.tolist() == e["cache_ids"]
+    assert d.seg_page_off.tolist() == e["seg_page_off"]
+    assert split(d.pk_ids, d.pk_off) == e["pk"]
+    assert split(d.req_pages, d.req_off) == e["req"]
+    off = np.concatenate([[0], np.cumsum([len(p) for p in pl])])
+    assert split(d.dc_addr, off) == e["addr"]
+    assert d.space_pages == e["space"] == oracle.disk_space(pl, n_nodes, row_bytes, s, m)
+    assert d.io_pages == e["io"]
+    assert d.space_pages == d.cache_pages + d.chunk_pages
+
+
+def test_search_is_the_minimum_feasible_s():
+    rng = np.random.default_rng(7)
+    for trial in range(8):
+        pl = random_plists(rng, 10, 60, 5, 25, skew=4.0)
+        sp = [bf_space(pl, 512, s, 1) for s in range(1, 11)]
+        for budget in sorted(set(sp)) + [min(sp) - 1, max(sp) + 5]:
+            s, pages = oracle.disk_search(pl, 60, 512, budget, m=1)
+            feas = [i + 1 for i, x in enumerate(sp) if x <= budget]
+            if feas:
+                assert (s, pages) == (feas[0], sp[feas[0] - 1])
+            else:
+                assert (s, pages) == (0, sp[-1])
+
+
+def test_algorithm1_verbatim_at_k1_and_grouping():
+    """Algorithm 1 as printed (scalar S(v) = min over i, j of H_j(i)) equals reading d6 at k = 1;
+    for any k, nodes with identical batch sets sit contiguously in V_r."""
+    rng = np.random.default_rng(3)
+    for trial in range(10):
+        pl = random_plists(rng, 6, 30, 4, 12, skew=2.0)
+        seed = int(rng.integers(0, 2**31))
+        d = oracle.disk_plan(pl, 30, 512, s=6, m=0, k=1, seed=seed)
+        H = bf_perm(seed, 0, 0, 6)
+        S = {}
+        for i, p in enumerate(pl):          # lines 4-8, verbatim
+            for v in p:
+                S[v] = min(S.get(v, 10**9), H[i])
+        assert d.cache_ids.tolist() == sorted(S, key=lambda v: (S[v], v))
+        for k in (2, 5):
+            d = oracle.disk_plan(pl, 30, 512, s=6, m=0, k=k, seed=seed)
+            Hs = [bf_perm(seed, 0, t, 6) for t in range(k)]
+            order = d.cache_ids.tolist()
+            member = {v: frozenset(i for i, p in enumerate(pl) if v in p) for v in order}
+            sig = {v: tuple(min(Hs[t][i] for i in member[v]) for t in range(k)) for v in order}
+            for a, b in itertools.combinations(range(len(order)), 2):
+                if member[order[a]] == member[order[b]]:
+                    # everything between two same-set nodes shares their signature: the set is
+                    # contiguous up to signature collisions broken by ID
+                    assert all(sig[order[c]] == sig[order[a]] for c in range(a, b + 1))
+
+
+def test_reconstruction_from_pages_and_chunks():
+    rng = np.random.default_rng(5)
+    n_nodes, dim = 200, 100  # 400-byte rows: fpp = 10, pages with a 96-byte tail
+    feats = feature_rows_np(np.arange(n_nodes), dim, 1)
+    pl = random_plists(rng, 9, n_nodes, 10, 40, skew=3.0)
+    d = oracle.disk_plan(pl, n_nodes, 400, s=4, m=1, k=3, seed=2)
+    cache = oracle.disk_cache_fill(feats, d)
+    assert cache.size == d.cache_pages * PAGE
+    fb = feats.view(np.uint8).reshape(n_nodes, -1)
+    off = np.concatenate([[0], np.cumsum([len(p) for p in pl])])
+    for b, p in enumerate(pl):
+        kept = d.pk_ids[d.pk_off[b]:d.pk_off[b + 1]]
+        chunk = fb[kept].reshape(-1)
+        pages = np.concatenate([cache[q * PAGE:(q + 1) * PAGE] for q in d.req_pages[d.req_off[b]:d.req_off[b + 1]]]
+                               ) if d.req_off[b + 1] > d.req_off[b] else np.zeros(0, np.uint8)
+        pi = oracle.disk_partial_input(chunk, pages, d.dc_addr[off[b]:off[b + 1]], 400)
+        assert np.array_equal(pi, fb[np.asarray(p, np.int64)])
+
+
+def test_segmented_reordering_trend():
+    """Fig. 5a trend on a skewed fixture (measured regression values): segmented
+    MinHash order reads no more pages than the global one, which reads fewer than ID order."""
+    rng = np.random.default_rng(11)
+    pl = random_plists(rng, 40, 2000, 150, 250, skew=6.0)
+    ident = oracle.disk_plan(pl, 2000, 512, s=40, m=0, k=4, seed=1, reorder=False).io_pages
+    glob = oracle.disk_plan(pl, 2000, 512, s=40, m=0, k=4, seed=1).io_pages
+    seg = oracle.disk_plan(pl, 2000, 512, s=4, m=0, k=4, seed=1).io_pages
+    assert seg <= glob <= ident
