@@ -79,6 +79,9 @@ typedef enum {
     DGNN_K_GATHER,          /* a7: tier-buffer gather ("special mini-batches")          */
     DGNN_K_ASSEMBLE,        /* a9: three-source assembly                                */
     DGNN_K_MISC,            /* memsets and small helpers                                */
+    DGNN_K_SORT,            /* stable LSD radix sort (disk-cache index and order)       */
+    DGNN_K_DISK_PLAN,       /* segmented disk cache: groups, MinHash, pages, addresses  */
+    DGNN_K_DISK_GATHER,     /* segmented disk cache: page fill, partial input           */
     DGNN_K_NUM
 } dgnn_kernel_id;
 
@@ -350,6 +353,83 @@ dgnn_status dgnn_assemble_group_sharded(dgnn_ctx* ctx, const uint32_t* addr, con
 /* dgnn_gather_rows with the row count read from device memory (*n_dev <= n_max). */
 dgnn_status dgnn_gather_rows_dev(dgnn_ctx* ctx, const void* features, int64_t num_rows, int64_t row_bytes,
                                  const int32_t* ids, const int64_t* n_dev, int64_t n_max, void* out);
+
+/* ------------------------------------------- segmented disk cache (NEXT #1) ---- */
+/* Sec. 5.1: under a disk-space budget C the DISK rows of an epoch are split
+ * into per-segment disk caches (shared, de-duplicated, laid out by MinHash reordering,
+ * Algorithm 1) and reduced packed chunks.  Readings d1-d8 (oracle/dgnn_oracle.c):
+ *  d1 segment g = batches [g*s, min((g+1)*s, nb)).
+ *  d2 a node whose local frequency (batches of the segment whose packed list holds it)
+ *     exceeds m joins the segment's cache V_d; otherwise it stays in each packed list.
+ *  d3 space in 4096-byte pages: per segment ceil(|V_d| / fpp), fpp = floor(4096 / row_bytes),
+ *     per batch ceil(|P_b'| * row_bytes / 4096); feasible when space <= budget.
+ *  d4 heuristic: the minimum s in 1..nb with space <= budget (m = 1 advised).
+ *  d5 H_t = ranking of the segment's local batch indices i by (x, i), x = Philox4x32-10
+ *     (ctr = {i, g, t, 0x4D48}, key = seed) as out.y << 32 | out.x.
+ *  d6 S_t(v) = min over the segment's batches i holding v of H_t(i); V_r = V_d sorted by
+ *     (S_0, ..., S_{k-1}, v) (reorder = 1) or by v (reorder = 0).
+ *  d7 I/O = sum over batches of chunk pages + distinct cache pages (merged requests).
+ *  d8 dc_addr of the r-th packed row of the INPUT packed lists: cached -> 1 << 31 |
+ *     (q * fpp + slot), q = index of its page in the batch's request list; packed -> its
+ *     rank in P_b'.
+ * Input: the packed lists of all nb batches as dgnn_classify writes them (packed_ids,
+ * packed_off device int64 [nb+1], packed_off_host host int64 [nb+1]); the index copies
+ * what it needs, so the inputs may be freed after dgnn_disk_index_build returns.
+ * Node IDs must be < num_nodes <= 2^31; packed_off[nb] < 2^31.  All calls synchronize. */
+typedef struct dgnn_disk_index dgnn_disk_index;
+typedef struct dgnn_disk_plan dgnn_disk_plan;
+dgnn_status dgnn_disk_index_build(dgnn_ctx* ctx, const int32_t* packed_ids, const int64_t* packed_off,
+                                  const int64_t* packed_off_host, int64_t nb, int64_t num_nodes,
+                                  dgnn_disk_index** out);
+void dgnn_disk_index_free(dgnn_disk_index* idx);
+/* Eq. 2 space (d3) of (s_list[i], m) for i < n_s: pages_host[i] (host int64). */
+dgnn_status dgnn_disk_space(dgnn_ctx* ctx, const dgnn_disk_index* idx, int64_t row_bytes, const int64_t* s_list_host,
+                            int64_t n_s, int64_t m, int64_t* pages_host);
+/* d4: *s_out = minimum feasible s (0 if none), *pages_out = its space (of s = nb if none). */
+dgnn_status dgnn_disk_search(dgnn_ctx* ctx, const dgnn_disk_index* idx, int64_t row_bytes, int64_t m,
+                             int64_t budget_pages, int64_t* s_out, int64_t* pages_out);
+/* The plan of (s, m) with k hash functions (d1-d8).  k in [1, 16]. */
+dgnn_status dgnn_disk_plan_build(dgnn_ctx* ctx, const dgnn_disk_index* idx, int64_t row_bytes, int64_t s, int64_t m,
+                                 int32_t k, uint64_t seed, int32_t reorder, dgnn_disk_plan** out);
+typedef struct {
+    int64_t nb, nseg, s, m, fpp, row_bytes;
+    int64_t n_cache;             /* sum |V_d| over segments                              */
+    int64_t n_packed;            /* sum |P_b'|                                           */
+    int64_t n_req;               /* sum of merged page requests                          */
+    int64_t space_pages, io_pages, cache_pages, chunk_pages;
+    const int64_t* seg_off;      /* device [nseg+1]: V_r of segment g = cache_ids[seg_off[g]..) */
+    const int32_t* cache_ids;    /* device [n_cache]                                     */
+    const int64_t* seg_page_off; /* device [nseg+1]: first global cache page of segment g */
+    const int32_t* pk_ids;       /* device [n_packed]: P_b' concatenated                 */
+    const int64_t* pk_off;       /* device [nb+1]                                        */
+    const int32_t* req_pages;    /* device [n_req]: per batch ascending global pages     */
+    const int64_t* req_off;      /* device [nb+1]                                        */
+    const uint32_t* dc_addr;     /* device [packed_off[nb]]: d8                          */
+    const int64_t* pk_off_host;  /* host copies of pk_off, req_off, seg_off, seg_page_off */
+    const int64_t* req_off_host;
+    const int64_t* seg_off_host;
+    const int64_t* seg_page_off_host;
+} dgnn_disk_plan_info;
+dgnn_status dgnn_disk_plan_get_info(const dgnn_disk_plan* p, dgnn_disk_plan_info* info);
+void dgnn_disk_plan_free(dgnn_disk_plan* p);
+/* The segment caches ("laid out on disk by reordering"): out (device or pinned,
+ * [cache_pages * 4096] bytes) receives V_r of each segment, fpp rows per page at
+ * slot * row_bytes, every byte past the rows zeroed.  row_bytes % 16 == 0. */
+dgnn_status dgnn_disk_cache_fill(dgnn_ctx* ctx, const dgnn_disk_plan* p, const void* features, int64_t num_rows,
+                                 void* out);
+/* Partial input of batches [b_lo, b_hi) ("the CPU reads the features in the disk
+ * cache and packed feature chunks and prepares them as partial input"; here the GPU, from
+ * staged bytes): for input packed row r of batch b (local DISK rank j = r - packed_off[b]),
+ *   out + out_off[b-b_lo] + j*row_bytes  <-  cached: pages + (req_off[b] - req_off[b_lo] + q)*4096
+ *                                                   + slot*row_bytes
+ *                                           packed: chunks + chunk_off[b-b_lo] + rank*row_bytes
+ *   pages    device/pinned: the requested pages req_pages[req_off[b_lo] .. req_off[b_hi]), in order.
+ *   chunks   device/pinned: the reduced chunks of the batches; chunk_off device int64 [b_hi-b_lo+1].
+ *   out_off  device int64 [b_hi-b_lo+1] (e.g. the c20 layout of the input packed lists, so the
+ *            result is what dgnn_pack of the input lists would have produced, minus the padding). */
+dgnn_status dgnn_disk_partial(dgnn_ctx* ctx, const dgnn_disk_plan* p, int64_t b_lo, int64_t b_hi,
+                              const void* pages, const void* chunks, const int64_t* chunk_off, void* out,
+                              const int64_t* out_off);
 
 #ifdef __cplusplus
 }

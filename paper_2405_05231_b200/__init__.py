@@ -9,7 +9,8 @@ from . import _abi
 from ._abi import (Ctx, Samples, CachePlan, DgnnError, dgnn_sample, dgnn_build_cache, dgnn_classify,
                    dgnn_chunk_layout, dgnn_pack, dgnn_gather_rows, dgnn_stage_copy, dgnn_stage_wait,
                    dgnn_stage_sync, dgnn_assemble, load_library, TIER_GPU, TIER_HOST, TIER_DISK, TIER_SHIFT,
-                   SLOT_MASK)
+                   SLOT_MASK, DiskIndex, DiskPlan, dgnn_disk_space, dgnn_disk_search, dgnn_disk_plan_build,
+                   dgnn_disk_cache_fill, dgnn_disk_partial)
 from .layout import HostBuffer, Layout, Workspace, offline_layout, batch_range
 
 load_library()
@@ -17,4 +18,5 @@ load_library()
 __all__ = ["Ctx", "Samples", "CachePlan", "DgnnError", "dgnn_sample", "dgnn_build_cache", "dgnn_classify",
            "dgnn_chunk_layout", "dgnn_pack", "dgnn_gather_rows", "dgnn_stage_copy", "dgnn_stage_wait",
            "dgnn_stage_sync", "dgnn_assemble", "load_library", "HostBuffer", "Layout", "Workspace", "offline_layout",
-           "batch_range", "TIER_GPU", "TIER_HOST", "TIER_DISK", "TIER_SHIFT", "SLOT_MASK"]
+           "batch_range", "TIER_GPU", "TIER_HOST", "TIER_DISK", "TIER_SHIFT", "SLOT_MASK", "DiskIndex", "DiskPlan",
+           "dgnn_disk_space", "dgnn_disk_search", "dgnn_disk_plan_build", "dgnn_disk_cache_fill", "dgnn_disk_partial"]

@@ -27,7 +27,7 @@ TIER_GPU, TIER_HOST, TIER_DISK = 0, 1, 2
 TIER_SHIFT = 30
 SLOT_MASK = (1 << TIER_SHIFT) - 1
 KERNELS = ["scan", "sample_seed", "sample_hop", "sample_order", "sample_remap", "sample_compact", "sample_setup",
-           "cache_hist", "cache_select", "classify", "pack_gather", "tier_gather", "assemble", "misc"]
+           "cache_hist", "cache_select", "classify", "pack_gather", "tier_gather", "assemble", "misc", "sort", "disk_plan", "disk_gather"]
 K = {name: i for i, name in enumerate(KERNELS)}
 
 # every symbol include/dgnn.h declares (checked by tests/test_abi_symbols.py)
@@ -41,6 +41,8 @@ EXPORTS = [
     "dgnn_host_window", "dgnn_gather_rows_dev", "dgnn_stage_wait_stream", "dgnn_tier_shard_ids",
     "dgnn_shard_requests", "dgnn_scatter_rows", "dgnn_assemble_group_sharded", "dgnn_batch_tier_counts",
     "dgnn_file_open", "dgnn_file_close", "dgnn_stage_file_write", "dgnn_stage_file_read",
+    "dgnn_disk_index_build", "dgnn_disk_index_free", "dgnn_disk_space", "dgnn_disk_search", "dgnn_disk_plan_build",
+    "dgnn_disk_plan_get_info", "dgnn_disk_plan_free", "dgnn_disk_cache_fill", "dgnn_disk_partial",
 ]
 
 
@@ -65,6 +67,13 @@ class _SamplesInfo(ctypes.Structure):
 class _PlanInfo(ctypes.Structure):
     _fields_ = [("num_nodes", i64), ("k_gpu", i64), ("k_host", i64), ("tier_map", P), ("gpu_ids", P),
                 ("host_ids", P), ("gpu_min_count", u32), ("host_min_count", u32)]
+
+
+class _DiskPlanInfo(ctypes.Structure):
+    _fields_ = [(n, i64) for n in ("nb", "nseg", "s", "m", "fpp", "row_bytes", "n_cache", "n_packed", "n_req",
+                                   "space_pages", "io_pages", "cache_pages", "chunk_pages")] + \
+               [(n, P) for n in ("seg_off", "cache_ids", "seg_page_off", "pk_ids", "pk_off", "req_pages", "req_off",
+                                 "dc_addr", "pk_off_host", "req_off_host", "seg_off_host", "seg_page_off_host")]
 
 
 class _KStat(ctypes.Structure):
@@ -137,6 +146,15 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "dgnn_assemble_group_sharded": (i32, [P, P, P, i64, i64, P, i64, i32, i32, P, i64, P, P, P, P, i64, P]),
             "dgnn_gather_rows_dev": (i32, [P, P, i64, i64, P, P, i64, P]),
             "dgnn_ctx_set_assemble_occupancy": (i32, [P, i32]),
+            "dgnn_disk_index_build": (i32, [P, P, P, P, i64, i64, ctypes.POINTER(P)]),
+            "dgnn_disk_index_free": (None, [P]),
+            "dgnn_disk_space": (i32, [P, P, i64, P, i64, i64, P]),
+            "dgnn_disk_search": (i32, [P, P, i64, i64, i64, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
+            "dgnn_disk_plan_build": (i32, [P, P, i64, i64, i64, i32, u64, i32, ctypes.POINTER(P)]),
+            "dgnn_disk_plan_get_info": (i32, [P, ctypes.POINTER(_DiskPlanInfo)]),
+            "dgnn_disk_plan_free": (None, [P]),
+            "dgnn_disk_cache_fill": (i32, [P, P, P, i64, P]),
+            "dgnn_disk_partial": (i32, [P, P, i64, i64, P, P, P, P, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -523,3 +541,90 @@ def dgnn_gather_rows_dev(ctx: Ctx, features, num_rows: int, row_bytes: int, ids:
                          out):
     _check(load_library().dgnn_gather_rows_dev(ctx.handle, _ptr(features), int(num_rows), int(row_bytes), _ptr(ids),
                                                _ptr(n_dev), ids.numel(), _ptr(out)), "dgnn_gather_rows_dev")
+
+
+# ------------------------------------------------- segmented disk cache ----
+class DiskIndex:
+    """An epoch's packed lists sorted by (node, batch) on the device (dgnn_disk_index_build)."""
+
+    def __init__(self, ctx: Ctx, packed_ids: torch.Tensor, packed_off: torch.Tensor, packed_off_host, num_nodes: int):
+        import numpy as np
+        L = load_library()
+        _need_cuda(packed_ids, "packed_ids", torch.int32)
+        _need_cuda(packed_off, "packed_off", torch.int64)
+        po = np.ascontiguousarray(packed_off_host, dtype=np.int64)
+        self.ctx = ctx
+        self.nb = len(po) - 1
+        self.packed_off_host = po.copy()
+        h = P()
+        _check(L.dgnn_disk_index_build(ctx.handle, _ptr(packed_ids), _ptr(packed_off), P(po.ctypes.data), self.nb,
+                                       int(num_nodes), ctypes.byref(h)), "dgnn_disk_index_build")
+        self.handle = h
+        self._finalizer = weakref.finalize(self, L.dgnn_disk_index_free, h)
+
+
+def dgnn_disk_space(ctx: Ctx, idx: DiskIndex, row_bytes: int, s_list, m: int):
+    import numpy as np
+    sl = np.ascontiguousarray(s_list, dtype=np.int64)
+    out = np.zeros(len(sl), np.int64)
+    _check(load_library().dgnn_disk_space(ctx.handle, idx.handle, int(row_bytes), P(sl.ctypes.data) if sl.size else P(0),
+                                          len(sl), int(m), P(out.ctypes.data) if out.size else P(0)),
+           "dgnn_disk_space")
+    return out
+
+
+def dgnn_disk_search(ctx: Ctx, idx: DiskIndex, row_bytes: int, budget_pages: int, m: int = 1):
+    s = i64()
+    pg = i64()
+    _check(load_library().dgnn_disk_search(ctx.handle, idx.handle, int(row_bytes), int(m), int(budget_pages),
+                                           ctypes.byref(s), ctypes.byref(pg)), "dgnn_disk_search")
+    return int(s.value), int(pg.value)
+
+
+class DiskPlan:
+    """Segmented disk cache plan (readings d1-d8); zero-copy device views + host offsets."""
+
+    def __init__(self, ctx: Ctx, handle, R: int):
+        L = load_library()
+        self.ctx = ctx
+        self.handle = handle
+        self._finalizer = weakref.finalize(self, L.dgnn_disk_plan_free, handle)
+        info = _DiskPlanInfo()
+        _check(L.dgnn_disk_plan_get_info(handle, ctypes.byref(info)), "dgnn_disk_plan_get_info")
+        for n in ("nb", "nseg", "s", "m", "fpp", "row_bytes", "n_cache", "n_packed", "n_req", "space_pages",
+                  "io_pages", "cache_pages", "chunk_pages"):
+            setattr(self, n, int(getattr(info, n)))
+        dev = ctx.device
+        nb, nseg = self.nb, self.nseg
+        self.seg_off = _view(info.seg_off, nseg + 1, torch.int64, self, dev)
+        self.cache_ids = _view(info.cache_ids, self.n_cache, torch.int32, self, dev)
+        self.seg_page_off = _view(info.seg_page_off, nseg + 1, torch.int64, self, dev)
+        self.pk_ids = _view(info.pk_ids, self.n_packed, torch.int32, self, dev)
+        self.pk_off = _view(info.pk_off, nb + 1, torch.int64, self, dev)
+        self.req_pages = _view(info.req_pages, self.n_req, torch.int32, self, dev)
+        self.req_off = _view(info.req_off, nb + 1, torch.int64, self, dev)
+        self.dc_addr = _view(info.dc_addr, R, torch.uint32, self, dev)
+        self.pk_off_host = _host_array(info.pk_off_host, nb + 1, ctypes.c_int64)
+        self.req_off_host = _host_array(info.req_off_host, nb + 1, ctypes.c_int64)
+        self.seg_off_host = _host_array(info.seg_off_host, nseg + 1, ctypes.c_int64)
+        self.seg_page_off_host = _host_array(info.seg_page_off_host, nseg + 1, ctypes.c_int64)
+
+
+def dgnn_disk_plan_build(ctx: Ctx, idx: DiskIndex, row_bytes: int, s: int, m: int, k: int = 4, seed: int = 0,
+                         reorder: bool = True) -> DiskPlan:
+    h = P()
+    _check(load_library().dgnn_disk_plan_build(ctx.handle, idx.handle, int(row_bytes), int(s), int(m), int(k),
+                                               int(seed) & (2**64 - 1), int(bool(reorder)), ctypes.byref(h)),
+           "dgnn_disk_plan_build")
+    return DiskPlan(ctx, h, int(idx.packed_off_host[-1]))
+
+
+def dgnn_disk_cache_fill(ctx: Ctx, plan: DiskPlan, features: torch.Tensor, out):
+    _check(load_library().dgnn_disk_cache_fill(ctx.handle, plan.handle, _ptr(features), features.shape[0], _ptr(out)),
+           "dgnn_disk_cache_fill")
+
+
+def dgnn_disk_partial(ctx: Ctx, plan: DiskPlan, b_lo: int, b_hi: int, pages, chunks, chunk_off: torch.Tensor, out,
+                      out_off: torch.Tensor):
+    _check(load_library().dgnn_disk_partial(ctx.handle, plan.handle, int(b_lo), int(b_hi), _ptr(pages), _ptr(chunks),
+                                            _ptr(chunk_off), _ptr(out), _ptr(out_off)), "dgnn_disk_partial")

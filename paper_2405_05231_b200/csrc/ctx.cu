@@ -220,7 +220,8 @@ const char* dgnn_kernel_name(int32_t kid) {
     static const char* names[DGNN_K_NUM] = {"scan",           "sample_seed",   "sample_hop",    "sample_order",
                                             "sample_remap",   "sample_compact", "sample_setup", "cache_hist",
                                             "cache_select",   "classify",      "pack_gather",   "tier_gather",
-                                            "assemble",       "misc"};
+                                            "assemble",       "misc",          "sort",          "disk_plan",
+                                            "disk_gather"};
     return (kid >= 0 && kid < DGNN_K_NUM) ? names[kid] : "?";
 }
 

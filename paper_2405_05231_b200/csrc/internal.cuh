@@ -338,6 +338,16 @@ dgnn_status run(dgnn_ctx* c, int64_t max_n, const int64_t* n_dev, In in, Out out
 }
 }  // namespace scan
 
+// ------------------------------------------------------------ radix sort
+// Stable LSD radix sort of (uint32 key, uint32 value) pairs by key bits
+// [0, end_bit) (sort.cu).  On entry (*keys, *vals) hold the input and
+// (*keys_alt, *vals_alt) are scratch of the same size; the pointers are swapped
+// pass by pass, so on return (*keys, *vals) point at the sorted pairs.
+namespace radix {
+dgnn_status sort_pairs(dgnn_ctx* c, int64_t n, int end_bit, uint32_t** keys, uint32_t** vals, uint32_t** keys_alt,
+                       uint32_t** vals_alt);
+}  // namespace radix
+
 }  // namespace dgnn
 
 // Library-owned result objects.

@@ -234,3 +234,27 @@ def make_workload(name: str, device="cpu", seed: int = 0, fseed: int = 1, featur
     seeds = make_seeds(cfg["num_nodes"], cfg["num_seeds"], seed, device)
     feats = make_features(cfg["num_nodes"], cfg["dim"], device, fseed) if features else None
     return Workload(name, cfg, indptr, indices, seeds, feats, seed, fseed)
+
+
+def make_packed_lists(nb: int, num_nodes: int, rows_per_batch: int, alpha: float = 2.0, seed: int = 0,
+                      jitter: float = 0.25):
+    """Seeded stand-in for an epoch's packed lists (the DISK rows of each batch) -- an INPUT
+    for the segmented-disk-cache parity tests, not a product of the method.
+
+    Each batch draws about rows_per_batch node IDs as floor(N * u**alpha) through a seeded
+    permutation (alpha > 1: a few IDs are popular, as the cold tail of a sampled epoch),
+    drops duplicates and keeps them in a shuffled local order.  Returns (ids int32 [R],
+    off int64 [nb+1]).
+    """
+    rng = np.random.default_rng(seed)
+    perm = rng.permutation(num_nodes).astype(np.int32)
+    parts, off = [], np.zeros(nb + 1, np.int64)
+    for b in range(nb):
+        n = max(0, int(rows_per_batch * (1.0 + jitter * (2.0 * rng.random() - 1.0))))
+        raw = np.minimum((num_nodes * rng.random(n) ** alpha).astype(np.int64), num_nodes - 1)
+        ids = perm[np.unique(raw)]
+        rng.shuffle(ids)
+        parts.append(ids)
+        off[b + 1] = off[b] + len(ids)
+    ids = np.concatenate(parts) if parts else np.zeros(0, np.int32)
+    return ids.astype(np.int32), off
