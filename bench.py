@@ -216,6 +216,7 @@ class Runner:
         self.nb = (inp[3].numel() + cfg["batch_size"] - 1) // cfg["batch_size"]
         self.before_layout = None  # hook: e.g. the e2e H2D copies of the inputs
         self.host_window = 128
+        self.disk_budget_frac = None  # segmented disk cache off (unlimited disk budget, reading c18)
         # a9's host-row window gathers (PCIe) run on their own stream, overlapping the
         # HBM-bound assembly runs of the previous window
         # (stream priorities were measured: prioritising either assembly stream starves the
@@ -236,7 +237,8 @@ class Runner:
         return self.dg.offline_layout(self.ctxA, indptr, indices, feats, seeds, cfg["fanout"], cfg["batch_size"],
                                       gpu_rows, host_rows, RNG_SEED, group_size=cfg["group_size"],
                                       batch_id_base=self.rank * self.nb, counts=c, ws=self.ws[slot],
-                                      stage_piece=int(os.environ.get("DGNN_STAGE_PIECE", str(1 << 40))))
+                                      stage_piece=int(os.environ.get("DGNN_STAGE_PIECE", str(1 << 40))),
+                                      disk_budget_frac=self.disk_budget_frac)
 
     def run(self, K: int, keep_last=False):
         """Enqueue K passes; returns the last Layout if keep_last.  self.timeline collects
@@ -335,6 +337,8 @@ def main():
                     help="no epoch pipelining: the layout of pass e+1 starts after the assembly of pass e")
     ap.add_argument("--host-window", type=int, default=128,
                     help="batches per host-row merging window in a9 (1 = per-batch UVA reads, the paper's)")
+    ap.add_argument("--disk-budget", type=float, default=None,
+                    help="segmented disk cache (Sec. 5.1): disk budget as a fraction of the packed-only space")
     args = ap.parse_args()
     ws, rank, local = setup_dist(args)
     dev = torch.device("cuda", local)
@@ -348,6 +352,7 @@ def main():
     nb = (seeds.numel() + cfg["batch_size"] - 1) // cfg["batch_size"]
     R = Runner(dg, inp, rank, dev, pipelined=not args.sequential)
     R.host_window = args.host_window
+    R.disk_budget_frac = args.disk_budget
     t = time.time()
     L = R.run(1, keep_last=True)
     torch.cuda.synchronize()
@@ -415,7 +420,10 @@ def main():
         "config": {"workload": WORKLOAD_NAMES[args.config], "num_nodes": N, "num_edges": int(indices.numel()),
                    "dim": cfg["dim"], "fanout": list(cfg["fanout"]), "batch_size": cfg["batch_size"],
                    "num_seeds": int(seeds.numel()), "batches_per_rank": nb, "gpu_rows": gpu_rows,
-                   "host_rows": host_rows, "group_size": cfg["group_size"], "disk_tier": "pinned host arena",
+                   "host_rows": host_rows, "group_size": cfg["group_size"],
+                   "disk_tier": "pinned host arena" + ("" if args.disk_budget is None else
+                                                       f"; segmented disk cache at {args.disk_budget:g} x the "
+                                                       "packed-only space"),
                    "parallelism": f"dp{ws} (batch-sharded, count all-reduce)",
                    "host_window_batches": args.host_window,
                    "schedule": "sequential" if args.sequential else

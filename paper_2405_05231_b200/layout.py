@@ -121,6 +121,8 @@ class Layout:
     stage_pieces: list = field(default_factory=list)  # (b_lo, b_hi, ticket) of each stage-out copy
     disk: A.DiskFile | None = None  # the disk tier as a file (stage="file")
     batch_tiers: np.ndarray = None  # [nb, 3] rows per tier (GPU, HOST, DISK) of each batch
+    disk_plan: A.DiskPlan | None = None  # segmented disk cache (Sec. 5.1), when a disk budget is set
+    cache_off: int = 0              # byte offset of the segment caches in the disk tier
 
     def phase_ms(self) -> dict:
         """Device time of the layout's phases (after the stream has passed them)."""
@@ -150,7 +152,8 @@ class Layout:
 
     def assemble(self, b: int, out: torch.Tensor, chunk_dev: torch.Tensor | None = None) -> torch.Tensor:
         """Assemble batch b into ``out`` ([n_b, dim]) reading the chunk from ``chunk_dev`` if given
-        (already staged to HBM), else directly from the arena (UVA over PCIe)."""
+        (already staged to HBM), else directly from the arena (UVA over PCIe).  With a disk cache
+        the batch's partial input (chunk rows + its cache pages) is built first."""
         n0, n1 = int(self.samples.node_off_host[b]), int(self.samples.node_off_host[b + 1])
         off, rows = int(self.batch_chunk[b, 0]), int(self.batch_chunk[b, 1])
         if chunk_dev is not None:
@@ -159,8 +162,35 @@ class Layout:
             chunk = self.arena_dev.data_ptr() + off
         else:
             chunk = self.arena.ptr + off
+        if self.disk_plan is not None:
+            dev = self.ctx.device
+            dp = self.disk_plan
+            rows = int(self.batch_tiers[b, 2])
+            with torch.cuda.stream(self.ctx.stream):
+                q = int(dp.req_off_host[b + 1] - dp.req_off_host[b])
+                pages = torch.empty(max(q, 1) * 4096, dtype=torch.uint8, device=dev)
+                part = torch.empty(max(rows * self.row_bytes, 16), dtype=torch.uint8, device=dev)
+                zero = torch.zeros(2, dtype=torch.int64, device=dev)
+                chunk = self._partial(b, b + 1, chunk, zero, zero, pages, part)
         A.dgnn_assemble(self.ctx, self.addr[n0:n1], self.gpu_tier, self.plan.k_gpu, self.host_tier.ptr,
                         self.plan.k_host, chunk, rows, self.row_bytes, out)
+        return out
+
+    def _cache_rows(self) -> torch.Tensor:
+        """The segment caches as [pages, 4096] (pinned host through UVA, or HBM)."""
+        dp = self.disk_plan
+        src = self.arena.tensor if self.arena is not None else self.arena_dev
+        return src[self.cache_off:self.cache_off + max(dp.cache_pages, 1) * 4096].view(-1, 4096)
+
+    def _partial(self, b0: int, b1: int, chunk, chunk_off: torch.Tensor, out_off: torch.Tensor, pages, out):
+        """Partial input of batches [b0, b1): fetch their merged cache-page requests
+        into ``pages`` and interleave them with the (reduced) chunk rows into ``out``: dense DISK
+        rows in local order at ``out_off`` (device, run-relative byte offsets)."""
+        dp = self.disk_plan
+        q0, q1 = int(dp.req_off_host[b0]), int(dp.req_off_host[b1])
+        if q1 > q0:
+            A.dgnn_gather_rows(self.ctx, self._cache_rows(), dp.req_pages[q0:q1], pages)
+        A.dgnn_disk_partial(self.ctx, dp, b0, b1, pages, chunk, chunk_off, out, out_off)
         return out
 
     def assembly_groups(self, out_budget: int = 1 << 30):
@@ -194,9 +224,13 @@ class Layout:
         for (b0, b1) in groups:
             c_lo = int(self.batch_chunk[b0, 0])
             # chunks of consecutive batches are contiguous (4 KiB-aligned) in the disk tier
-            c_hi = int(self.batch_chunk[b1, 0]) if b1 < nb else int(self.stats["arena_bytes"])
+            c_hi = int(self.batch_chunk[b1, 0]) if b1 < nb else int(self.stats["chunk_bytes"])
             chunk_off = np.concatenate([self.batch_chunk[b0:b1, 0] - c_lo, [c_hi - c_lo]])
-            tabs.append(np.concatenate([no[b0:b1 + 1] - no[b0], chunk_off, rows_pre[b0:b1 + 1] - rows_pre[b0]]))
+            if self.disk_plan is None:
+                tabs.append(np.concatenate([no[b0:b1 + 1] - no[b0], chunk_off, rows_pre[b0:b1 + 1] - rows_pre[b0]]))
+            else:  # a9 reads the partial input: dense DISK rows of the run in local order
+                dpre = np.concatenate([[0], np.cumsum(self.batch_tiers[b0:b1, 2])])
+                tabs.append(np.concatenate([no[b0:b1 + 1] - no[b0], dpre * self.row_bytes, dpre, chunk_off]))
             spans.append((int(no[b0]), int(no[b1]), c_lo, c_hi))
         with torch.cuda.stream(self.ctx.stream):
             flat = torch.from_numpy(np.concatenate(tabs).astype(np.int64)).to(self.ctx.device, non_blocking=False)
@@ -251,6 +285,14 @@ class Layout:
             bounce_r = HostBuffer(FILE_CHUNK) if self.disk is not None else None
             chunk_ring = [torch.empty(max(max_c, 16), dtype=torch.uint8, device=dev) for _ in range(2)] \
                 if staged else None
+            dp = self.disk_plan
+            if dp is not None:  # per run: its cache pages and its partial input (dense DISK rows)
+                dpre = np.concatenate([[0], np.cumsum(self.batch_tiers[:, 2])])
+                max_pg = max(int(dp.req_off_host[b1] - dp.req_off_host[b0]) for b0, b1 in groups)
+                max_pi = max(int(dpre[b1] - dpre[b0]) for b0, b1 in groups)
+                page_ring = [torch.empty(max(max_pg, 1) * 4096, dtype=torch.uint8, device=dev) for _ in range(2)]
+                part_ring = [torch.empty(max(max_pi * self.row_bytes, 16), dtype=torch.uint8, device=dev)
+                             for _ in range(2)]
             if windows:
                 # staging rows: the window's host-row accesses bound its distinct host rows
                 hpre = np.concatenate([[0], np.cumsum(self.batch_tiers[:, 1])])
@@ -317,19 +359,22 @@ class Layout:
             k = b1 - b0
             t = flat[int(offs[i]):int(offs[i + 1])]
             out = out_ring[i % 2]
+            if dp is not None:
+                chunk = self._partial(b0, b1, chunk, t[3 * k + 3:4 * k + 4], t[k + 1:2 * k + 2], page_ring[i % 2],
+                                      part_ring[i % 2])
             if windows:
                 host_src, host_map = staging[cur], smap[cur]
             else:
                 host_src, host_map = self.host_tier.ptr, None
             if sharded_tier is None:
                 A.dgnn_assemble_group(ctx, self.addr[n0:n1], t[:k + 1], n1 - n0, self.gpu_tier, self.plan.k_gpu,
-                                      host_src, kh, chunk, t[k + 1:2 * k + 2], t[2 * k + 2:], self.row_bytes, out,
-                                      host_map=host_map)
+                                      host_src, kh, chunk, t[k + 1:2 * k + 2], t[2 * k + 2:3 * k + 3], self.row_bytes,
+                                      out, host_map=host_map)
             else:  # GPU tier sharded over ranks: local rows here, remote rows over the exchange
                 A.dgnn_assemble_group_sharded(ctx, self.addr[n0:n1], t[:k + 1], n1 - n0, sharded_tier.rows,
                                               self.plan.k_gpu, sharded_tier.rank, sharded_tier.world, host_src, kh,
-                                              chunk, t[k + 1:2 * k + 2], t[2 * k + 2:], self.row_bytes, out,
-                                              host_map=host_map)
+                                              chunk, t[k + 1:2 * k + 2], t[2 * k + 2:3 * k + 3], self.row_bytes,
+                                              out, host_map=host_map)
                 remote(ctx, self.addr[n0:n1], out)
             if i in last_run:
                 ev = torch.cuda.Event()
@@ -344,13 +389,18 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
                    group_size: int = 64, batch_id_base: int = 0, stage: str = "pinned",
                    counts: torch.Tensor | None = None, ws: Workspace | None = None,
                    group_budget: int = 4 << 30, stage_piece: int = 1 << 40, file_path: str | None = None,
-                   direct_io: bool = True) -> Layout:
+                   direct_io: bool = True, disk_budget: int | None = None, disk_m: int = 1,
+                   disk_k: int = 4, disk_budget_frac: float | None = None) -> Layout:
     """Run a1-a8 on this rank's batches.
 
     ``seeds`` are this rank's seeds (batch t of them gets bid = batch_id_base + t).
     With torch.distributed initialized (world > 1) the counts are all-reduced so that
     every rank derives the identical cache plan from all ranks' batches.
     ``stage``: "pinned" (disk tier in a pinned host arena, the default) or "hbm".
+    ``disk_budget`` (bytes): activate the segmented disk cache (Sec. 5.1) when
+    the packed chunks exceed it -- the heuristic of P:410-413 picks the smallest segment
+    size s whose Eq. 2 space fits (threshold ``disk_m``, MinHash with ``disk_k`` hashes).
+    ``disk_budget_frac`` states the budget as a fraction of the packed-only space instead.
     """
     dev = ctx.device
     N = indptr.numel() - 1
@@ -401,8 +451,22 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
     packed_ids = buf("packed_ids", total_nodes, torch.int32)
     packed_off = torch.empty(nb + 1, dtype=torch.int64, device=dev)
     po = A.dgnn_classify(ctx, plan, samples, 0, nb, addr, packed_ids, packed_off) if nb else np.zeros(1, np.int64)
-    rows = np.diff(po)
     batch_tiers = A.dgnn_batch_tier_counts(ctx, samples, 0, nb, addr) if nb else np.zeros((0, 3), np.int64)
+    dplan = None
+    if disk_budget_frac is not None and nb:
+        disk_budget = int(disk_budget_frac * int(((np.diff(po) * row_bytes + 4095) // 4096).sum())) * 4096
+    if disk_budget is not None and nb:
+        if stage == "file":
+            raise NotImplementedError("the segmented disk cache is staged in pinned host memory or HBM")
+        idx = A.DiskIndex(ctx, packed_ids[:int(po[-1])], packed_off, po, N)
+        s_seg, pages = A.dgnn_disk_search(ctx, idx, row_bytes, int(disk_budget) // 4096, disk_m)
+        if s_seg == 0:
+            raise ValueError(f"disk budget {disk_budget} B is below the smallest Eq. 2 space ({pages * 4096} B)")
+        dplan = A.dgnn_disk_plan_build(ctx, idx, row_bytes, s_seg, disk_m, disk_k, rng_seed)
+        del idx
+        po = dplan.pk_off_host  # the chunks now hold the reduced packed lists P_b'
+        packed_ids = dplan.pk_ids
+    rows = np.diff(po)
     # a7 layout: groups of `group_size` batches, each a contiguous run of 4 KiB-aligned chunks
     groups = []
     batch_chunk = np.zeros((nb, 2), np.int64)
@@ -422,6 +486,10 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
         batch_chunk[g0:g1, 1] = rows[g0:g1]
         arena_off += int(co[-1])
         g0 = g1
+    chunk_bytes = arena_off
+    cache_off = arena_off
+    if dplan is not None:
+        arena_off += dplan.cache_pages * 4096
     arena = arena_dev = disk = None
     if stage == "pinned":
         arena = ws.host("arena", arena_off) if ws is not None else HostBuffer(arena_off)
@@ -436,8 +504,15 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
     L = Layout(ctx, samples, plan, counts, row_bytes, dim, features.dtype, addr, gpu_tier, host_tier, arena,
                arena_dev, groups, batch_chunk, stats)
     L.batch_tiers = batch_tiers
+    L.disk_plan = dplan
+    L.cache_off = cache_off
+    if dplan is not None:
+        stats.update(disk_cache={"s": dplan.s, "m": dplan.m, "k": disk_k, "budget_pages": int(disk_budget) // 4096,
+                                 "space_pages": dplan.space_pages, "io_pages": dplan.io_pages,
+                                 "cache_pages": dplan.cache_pages, "chunk_pages": dplan.chunk_pages,
+                                 "cache_rows": dplan.n_cache, "requests": dplan.n_req})
     stats.update(row_bytes=row_bytes, groups=len(groups), packed_rows=int(po[-1]),
-                 packed_bytes=int(po[-1]) * row_bytes, arena_bytes=arena_off,
+                 packed_bytes=int(po[-1]) * row_bytes, arena_bytes=arena_off, chunk_bytes=chunk_bytes,
                  k_gpu=plan.k_gpu, k_host=plan.k_host, total_nodes=total_nodes, total_edges=samples.total_edges)
     if nb:
         L.assembly_plan()  # a9's per-run tables, uploaded here on the layout's stream
@@ -495,6 +570,9 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
         else:
             dst = arena_dev[g.arena_off:g.arena_off + max(g.group_bytes, 0)]
             A.dgnn_pack(ctx, features, ids, rel_po, rel_co, total, g.group_bytes, dst)
+    if dplan is not None and dplan.cache_pages:
+        # the segment caches, MinHash-ordered, after the chunks
+        A.dgnn_disk_cache_fill(ctx, dplan, features, L._cache_rows())
     mark("pack")
     L._rel_all = rel_all
     # packed_ids is only read by the pack kernels on this stream: releasing it now is

@@ -159,3 +159,75 @@ def test_papers_scale_plan(dg, ctx):
     for s in sorted({max(s_h, 1), 50}):
         ref = oracle.disk_plan(pl, N, row_bytes, s, 1, 4, 2024)
         _compare(dg.dgnn_disk_plan_build(ctx, idx, row_bytes, s, 1, 4, 2024), ref, len(ids))
+
+
+# ------------------------------------------ the four-level store end to end ----
+RNG_SEED = 0x5EEDD15C
+
+
+@pytest.mark.parametrize("stage,frac,window", [("pinned", 0.8, 64), ("hbm", 0.6, 1), ("pinned", 1.0, 128)])
+def test_layout_with_disk_cache_tiny(dg, ctx, stage, frac, window):
+    """offline_layout with a disk budget: the heuristic's s, the segment caches, the reduced
+    chunks and every assembled batch equal the oracle's (assembly == direct gather)."""
+    w = make_workload("tiny")
+    feats = w.features.numpy()
+    ref = oracle.offline_layout(w.indptr.numpy(), w.indices.numpy(), feats, w.seeds.numpy(), 256, [10, 5],
+                                RNG_SEED, 500, 1000, 8)
+    pl = ref["packed"]
+    rb = w.row_bytes
+    packed_only = sum((len(p) * rb + 4095) // 4096 for p in pl)
+    s_ref, _ = oracle.disk_search(pl, 10_000, rb, int(frac * packed_only), 1)
+    assert s_ref >= 1
+    dplan = oracle.disk_plan(pl, 10_000, rb, s_ref, 1, 4, RNG_SEED)
+    dev = torch.device("cuda", 0)
+    L = dg.offline_layout(ctx, w.indptr.to(dev), w.indices.to(dev), w.features.to(dev), w.seeds.to(dev), [10, 5],
+                          256, 500, 1000, RNG_SEED, group_size=8, stage=stage, disk_budget_frac=frac)
+    ctx.sync()
+    assert L.disk_plan.s == s_ref
+    assert L.stats["disk_cache"]["space_pages"] == dplan.space_pages
+    arena = L.arena.tensor.numpy() if L.arena is not None else L.arena_dev.cpu().numpy()
+    cache = arena[L.cache_off:L.cache_off + dplan.cache_pages * PAGE]
+    assert np.array_equal(cache, oracle.disk_cache_fill(feats, dplan))
+    # reduced chunks: the oracle's pack of P_b'
+    red = [dplan.pk_ids[dplan.pk_off[b]:dplan.pk_off[b + 1]] for b in range(len(pl))]
+    for g in L.groups:
+        buf, off = oracle.pack(feats, red[g.b_lo:g.b_hi])
+        assert np.array_equal(arena[g.arena_off:g.arena_off + g.group_bytes], buf)
+    seen = 0
+    for b, out in L.assemble_epoch(host_window=window):
+        got = out.view(torch.uint8).reshape(out.shape[0], -1).cpu().numpy()
+        assert np.array_equal(got, oracle.assemble(feats, ref["samples"][b].nodes)), f"batch {b}"
+        seen += 1
+    assert seen == len(pl)
+    for b in (0, len(pl) - 1):  # single-batch path
+        n = len(ref["samples"][b].nodes)
+        out = torch.empty((n, w.features.shape[1]), dtype=w.features.dtype, device=dev)
+        L.assemble(b, out)
+        ctx.sync()
+        got = out.view(torch.uint8).reshape(n, -1).cpu().numpy()
+        assert np.array_equal(got, oracle.assemble(feats, ref["samples"][b].nodes))
+
+
+def test_layout_with_disk_cache_products(dg, ctx):
+    """products-shaped epoch (193 batches, 400-byte rows: pages with a 96-byte tail) at 80 % of
+    the packed-only space: the plan's Eq. 2 space fits, the I/O beats identity order, and sampled
+    batches assemble to the direct gather."""
+    w = make_workload("products", device="cuda")
+    dev = torch.device("cuda", 0)
+    from workload import config_rows, CONFIGS
+    cfg = CONFIGS["products"]
+    gr, hr = config_rows(cfg)
+    L = dg.offline_layout(ctx, w.indptr, w.indices, w.features, w.seeds, cfg["fanout"], cfg["batch_size"], gr, hr,
+                          RNG_SEED, group_size=cfg["group_size"], disk_budget_frac=0.8)
+    ctx.sync()
+    dc = L.stats["disk_cache"]
+    assert dc["space_pages"] <= dc["budget_pages"] and L.disk_plan.s > 1
+    nodes = L.samples.nodes.cpu().numpy()
+    check = {0, 1, 96, L.num_batches - 1}
+    for b, out in L.assemble_epoch():
+        if b in check:
+            n0, n1 = L.samples.node_off_host[b], L.samples.node_off_host[b + 1]
+            ids = nodes[n0:n1]
+            exp = feature_rows_np(ids, cfg["dim"], 1).view(np.uint8).reshape(len(ids), -1)
+            got = out.view(torch.uint8).reshape(out.shape[0], -1).cpu().numpy()
+            assert np.array_equal(got, exp), f"batch {b}"
