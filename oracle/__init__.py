@@ -24,6 +24,7 @@ Functions and the passage each follows:
 * ``disk_space``, ``disk_search``, ``disk_perm``, ``disk_plan``,
   ``disk_cache_fill``   -- segmented disk cache, Eq. 2 and Algorithm 1,
   P:311-414 (readings d1-d8 in dgnn_oracle.c and DESIGN.md).
+* ``train_stub``        -- the trainer's surrogate of Eq. 1, reading t1.
 """
 from __future__ import annotations
 
@@ -99,6 +100,8 @@ def _L():
             lib.oracle_disk_plan.argtypes = [P, P, i64, i64, i64, i64, i64, i32, u64, i32,
                                              P, P, P, P, P, P, P, P, P]
             lib.oracle_disk_cache_fill.argtypes = [P, i64, P, P, P, i64, P]
+            lib.oracle_train_stub.argtypes = [P, i64, i64, P, i32, P, P]
+            lib.oracle_train_stub.restype = ctypes.c_int
             _lib = lib
     return _lib
 
@@ -439,3 +442,17 @@ def disk_partial_input(chunk: np.ndarray, pages: np.ndarray, dc_addr_b: np.ndarr
         else:
             out[r] = chunk[a * row_bytes:(a + 1) * row_bytes]
     return out
+
+
+# --------------------------------------------------------- trainer stub ----
+def train_stub(sample: Sample, feats) -> np.ndarray:
+    """Seed embeddings h^H of one batch (reading t1) from its assembled rows (fp32 [n, dim])."""
+    x = np.array(feats, dtype=np.float32, copy=True, order="C").reshape(len(sample.nodes), -1)
+    H = len(sample.hop_off) - 2
+    hop = _c(sample.hop_off, np.int32)
+    ep = _c(sample.eptr, np.int32)
+    src = _c(sample.src_local, np.int32)
+    rc = _L().oracle_train_stub(_p(x), x.shape[0], x.shape[1], _p(hop), H, _p(ep), _p(src))
+    if rc != 0:
+        raise OracleError(rc, "train_stub")
+    return x[: int(hop[1])].copy()

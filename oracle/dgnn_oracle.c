@@ -704,3 +704,36 @@ void oracle_disk_cache_fill(const uint8_t* features, int64_t row_bytes, const in
             memcpy(out + (seg_page_off[g] + p / fpp) * DC_PAGE + (p % fpp) * row_bytes,
                    features + (int64_t)cache_ids[seg_off[g] + p] * row_bytes, (size_t)row_bytes);
 }
+
+/* ======================================================================== */
+/* Trainer stub: the surrogate of Eq. 1  */
+/* that SPEC S:409-413 fixes -- h^k_v = h^{k-1}_v + mean{h^{k-1}_u : u in   */
+/* N(v)}, no W^k, no sigma.  Reading t1: layer k = 1..H runs    */
+/* over sampling hop h = H - k (deepest first); N(v) = v's sampled          */
+/* neighbours at the hop v expanded in; a node of hop h without edges, and  */
+/* every node outside hop h, keeps h^{k-1}.  fp32 throughout: the sum starts */
+/* at 0 and adds the neighbours in edge order, then one division by the     */
+/* edge count and one addition.  x: the batch's assembled rows [n][dim],    */
+/* updated in place; the seeds' embeddings are rows [0, hop_off[1]).         */
+/* ======================================================================== */
+int oracle_train_stub(float* x, int64_t n, int64_t dim, const int32_t* hop_off, int32_t H, const int32_t* eptr,
+                      const int32_t* src_local)
+{
+    float* prev = (float*)malloc((size_t)(n > 0 ? n : 1) * (size_t)dim * sizeof(float));
+    if (!prev) return OR_ENOMEM;
+    for (int32_t k = 1; k <= H; ++k) {
+        int32_t h = H - k;
+        memcpy(prev, x, (size_t)n * (size_t)dim * sizeof(float));  /* h^{k-1} */
+        for (int64_t j = hop_off[h]; j < hop_off[h + 1]; ++j) {
+            int32_t e0 = eptr[j], e1 = eptr[j + 1];
+            if (e1 == e0) continue;
+            for (int64_t d = 0; d < dim; ++d) {
+                float s = 0.0f;
+                for (int32_t e = e0; e < e1; ++e) s += prev[(int64_t)src_local[e] * dim + d];
+                x[j * dim + d] = prev[j * dim + d] + s / (float)(e1 - e0);
+            }
+        }
+    }
+    free(prev);
+    return OR_OK;
+}
