@@ -82,6 +82,7 @@ typedef enum {
     DGNN_K_SORT,            /* stable LSD radix sort (disk-cache index and order)       */
     DGNN_K_DISK_PLAN,       /* segmented disk cache: groups, MinHash, pages, addresses  */
     DGNN_K_DISK_GATHER,     /* segmented disk cache: page fill, partial input           */
+    DGNN_K_TRAIN,           /* trainer stub (mean aggregation per sampled hop)          */
     DGNN_K_NUM
 } dgnn_kernel_id;
 
@@ -430,6 +431,20 @@ dgnn_status dgnn_disk_cache_fill(dgnn_ctx* ctx, const dgnn_disk_plan* p, const v
 dgnn_status dgnn_disk_partial(dgnn_ctx* ctx, const dgnn_disk_plan* p, int64_t b_lo, int64_t b_hi,
                               const void* pages, const void* chunks, const int64_t* chunk_off, void* out,
                               const int64_t* out_off);
+
+/* ------------------------------------------------ trainer stub (NEXT #2) ---- */
+/* The model-training stage of the pipeline with the surrogate of Eq. 1
+ * that SPEC S:409-413 fixes: h^k_v = h^{k-1}_v + mean{h^{k-1}_u : u in N(v)}, no W, no sigma.
+ * Reading t1: layer k = 1..H handles sampling hop h = H-k (deepest first); N(v) = v's sampled
+ * neighbours at the hop v expanded in (src_local); a node outside hop h, or without edges,
+ * keeps its value.  fp32: the sum starts at 0 and adds neighbours in edge order, then one
+ * IEEE division by the edge count and one addition (bit-identical to the oracle).
+ *   x    device fp32 [node_off[b_hi] - node_off[b_lo], dim]: the assembled rows of batches
+ *        [b_lo, b_hi) in node order, updated IN PLACE; afterwards the rows of each batch's
+ *        seeds (local [0, hop_off[b][1])) hold the seed embeddings h^H.
+ * Enqueued on the ctx stream; scratch comes from the ctx allocator. */
+dgnn_status dgnn_train_stub(dgnn_ctx* ctx, const dgnn_samples* samples, int64_t b_lo, int64_t b_hi, float* x,
+                            int64_t dim);
 
 #ifdef __cplusplus
 }

@@ -27,7 +27,7 @@ TIER_GPU, TIER_HOST, TIER_DISK = 0, 1, 2
 TIER_SHIFT = 30
 SLOT_MASK = (1 << TIER_SHIFT) - 1
 KERNELS = ["scan", "sample_seed", "sample_hop", "sample_order", "sample_remap", "sample_compact", "sample_setup",
-           "cache_hist", "cache_select", "classify", "pack_gather", "tier_gather", "assemble", "misc", "sort", "disk_plan", "disk_gather"]
+           "cache_hist", "cache_select", "classify", "pack_gather", "tier_gather", "assemble", "misc", "sort", "disk_plan", "disk_gather", "train"]
 K = {name: i for i, name in enumerate(KERNELS)}
 
 # every symbol include/dgnn.h declares (checked by tests/test_abi_symbols.py)
@@ -43,6 +43,7 @@ EXPORTS = [
     "dgnn_file_open", "dgnn_file_close", "dgnn_stage_file_write", "dgnn_stage_file_read",
     "dgnn_disk_index_build", "dgnn_disk_index_free", "dgnn_disk_space", "dgnn_disk_search", "dgnn_disk_plan_build",
     "dgnn_disk_plan_get_info", "dgnn_disk_plan_free", "dgnn_disk_cache_fill", "dgnn_disk_partial",
+    "dgnn_train_stub",
 ]
 
 
@@ -155,6 +156,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "dgnn_disk_plan_free": (None, [P]),
             "dgnn_disk_cache_fill": (i32, [P, P, P, i64, P]),
             "dgnn_disk_partial": (i32, [P, P, i64, i64, P, P, P, P, P]),
+            "dgnn_train_stub": (i32, [P, P, i64, i64, P, i64]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -628,3 +630,13 @@ def dgnn_disk_partial(ctx: Ctx, plan: DiskPlan, b_lo: int, b_hi: int, pages, chu
                       out_off: torch.Tensor):
     _check(load_library().dgnn_disk_partial(ctx.handle, plan.handle, int(b_lo), int(b_hi), _ptr(pages), _ptr(chunks),
                                             _ptr(chunk_off), _ptr(out), _ptr(out_off)), "dgnn_disk_partial")
+
+
+# ------------------------------------------------------------ trainer stub ----
+def dgnn_train_stub(ctx: Ctx, samples: Samples, b_lo: int, b_hi: int, x: torch.Tensor):
+    """In place: x = the assembled fp32 rows of batches [b_lo, b_hi) ([n, dim]); afterwards each
+    batch's seed rows hold h^H (reading t1)."""
+    _need_cuda(x, "x", torch.float32)
+    dim = x.shape[-1] if x.dim() > 1 else 1
+    _check(load_library().dgnn_train_stub(ctx.handle, samples.handle, int(b_lo), int(b_hi), _ptr(x), int(dim)),
+           "dgnn_train_stub")

@@ -221,7 +221,7 @@ const char* dgnn_kernel_name(int32_t kid) {
                                             "sample_remap",   "sample_compact", "sample_setup", "cache_hist",
                                             "cache_select",   "classify",      "pack_gather",   "tier_gather",
                                             "assemble",       "misc",          "sort",          "disk_plan",
-                                            "disk_gather"};
+                                            "disk_gather",   "train"};
     return (kid >= 0 && kid < DGNN_K_NUM) ? names[kid] : "?";
 }
 

@@ -240,7 +240,8 @@ class Layout:
         return plan
 
     def assemble_epoch(self, ctx: A.Ctx | None = None, out_budget: int = 1 << 30, host_window: int = 128,
-                       gather_ctx: A.Ctx | None = None, sharded_tier=None, remote=None):
+                       gather_ctx: A.Ctx | None = None, sharded_tier=None, remote=None, runs: bool = False,
+                       ring_wait: dict | None = None):
         """Pipelined assembly: the chunks of the next run of batches are staged H2D
         on the side stream while the current run is assembled on the ctx stream (one
         dgnn_assemble_group launch per run).  Yields (b, features[n_b, dim]) per batch; a
@@ -256,7 +257,11 @@ class Layout:
         ``sharded_tier`` (a shard.ShardedTier) + ``remote(ctx, addr_run, out)`` assemble with
         the GPU tier partitioned over ranks: local GPU-tier rows from this rank's shard,
         remote ones delivered by ``remote`` (shard.fetch_remote_rows over NCCL, or the
-        single-process loopback)."""
+        single-process loopback).
+
+        ``runs=True`` yields (b0, b1, out_run) once per run instead; with ``ring_wait`` (run index
+        -> event) the run that reuses run i's output slot first waits for ring_wait[i] (a
+        consumer on another stream, e.g. the trainer: a queue of depth 2)."""
         ctx = ctx or self.ctx
         gctx = gather_ctx or ctx
         nb = self.num_batches
@@ -359,6 +364,8 @@ class Layout:
             k = b1 - b0
             t = flat[int(offs[i]):int(offs[i + 1])]
             out = out_ring[i % 2]
+            if ring_wait is not None and (i - 2) in ring_wait:
+                ctx.stream.wait_event(ring_wait.pop(i - 2))  # the consumer of run i-2 released the slot
             if dp is not None:
                 chunk = self._partial(b0, b1, chunk, t[3 * k + 3:4 * k + 4], t[k + 1:2 * k + 2], page_ring[i % 2],
                                       part_ring[i % 2])
@@ -380,8 +387,33 @@ class Layout:
                 ev = torch.cuda.Event()
                 ev.record(ctx.stream)
                 ev_done[last_run[i]] = ev
-            for b in range(b0, b1):
-                yield b, out[int(no[b] - n0):int(no[b + 1] - n0)]
+            if runs:
+                yield b0, b1, out[:n1 - n0]
+            else:
+                for b in range(b0, b1):
+                    yield b, out[int(no[b] - n0):int(no[b + 1] - n0)]
+
+    def train_epoch(self, ctx: A.Ctx | None = None, train_ctx: A.Ctx | None = None, **kw):
+        """The training pipeline over this layout: feature loading (chunk staging on
+        the side stream) -> feature assembling (ctx) -> model training (the trainer stub,
+        dgnn_train_stub, on ``train_ctx``'s stream), stages linked by queues of depth 2.
+        Graph loading is free here: the graph samples stay in HBM (reading c22).  Yields
+        (b0, b1, x_run) per run after its trainer launch; each batch's seed rows of x_run hold
+        its seed embeddings once ``train_ctx``'s stream has passed that point."""
+        ctx = ctx or self.ctx
+        tctx = train_ctx or ctx
+        ring_wait = {}
+        for i, (b0, b1, x) in enumerate(self.assemble_epoch(ctx, runs=True, ring_wait=ring_wait, **kw)):
+            if tctx is not ctx:
+                ev = torch.cuda.Event()
+                ev.record(ctx.stream)
+                tctx.stream.wait_event(ev)
+            A.dgnn_train_stub(tctx, self.samples, b0, b1, x)
+            yield b0, b1, x
+            if tctx is not ctx:
+                ev = torch.cuda.Event()
+                ev.record(tctx.stream)
+                ring_wait[i] = ev
 
 
 def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, features: torch.Tensor,
