@@ -217,6 +217,9 @@ class Runner:
         self.before_layout = None  # hook: e.g. the e2e H2D copies of the inputs
         self.host_window = 128
         self.disk_budget_frac = None  # segmented disk cache off (unlimited disk budget, reading c18)
+        self.train = False  # trainer stub after assembly (the training pipeline)
+        self.sT = torch.cuda.Stream(dev)
+        self.ctxT = dg.Ctx(device=dev, stream=self.sT)
         # a9's host-row window gathers (PCIe) run on their own stream, overlapping the
         # HBM-bound assembly runs of the previous window
         # (stream priorities were measured: prioritising either assembly stream starves the
@@ -226,7 +229,7 @@ class Runner:
         self.ctxG.set_assemble_occupancy(2)
 
     def ctxs(self):
-        return [self.ctxA, self.ctxB, self.ctxG]
+        return [self.ctxA, self.ctxB, self.ctxG, self.ctxT]
 
     def layout(self, slot):
         cfg, indptr, indices, seeds, feats, gpu_rows, host_rows = self.inp
@@ -254,8 +257,14 @@ class Runner:
             a0 = torch.cuda.Event(enable_timing=True)
             a0.record(self.sB)
             gctx = self.ctxG if os.environ.get("DGNN_GATHER_STREAM", "1") == "1" else None
-            for _ in L.assemble_epoch(ctx=self.ctxB, host_window=self.host_window, gather_ctx=gctx):
-                pass
+            if self.train:
+                for _ in L.train_epoch(ctx=self.ctxB, train_ctx=self.ctxT, host_window=self.host_window,
+                                       gather_ctx=gctx):
+                    pass
+                self.sB.wait_stream(self.sT)  # the pass ends when its last batch is trained
+            else:
+                for _ in L.assemble_epoch(ctx=self.ctxB, host_window=self.host_window, gather_ctx=gctx):
+                    pass
             ev_a = torch.cuda.Event(enable_timing=True)
             ev_a.record(self.sB)
             self.timeline.append(((L.stats.get("_events", []), L.stats.get("_host", [])), a0, ev_a))
@@ -337,6 +346,8 @@ def main():
                     help="no epoch pipelining: the layout of pass e+1 starts after the assembly of pass e")
     ap.add_argument("--host-window", type=int, default=128,
                     help="batches per host-row merging window in a9 (1 = per-batch UVA reads, the paper's)")
+    ap.add_argument("--train", action="store_true",
+                    help="include the trainer stub (dgnn_train_stub, its own stream, depth-2 queue) in every pass")
     ap.add_argument("--disk-budget", type=float, default=None,
                     help="segmented disk cache (Sec. 5.1): disk budget as a fraction of the packed-only space")
     args = ap.parse_args()
@@ -353,6 +364,7 @@ def main():
     R = Runner(dg, inp, rank, dev, pipelined=not args.sequential)
     R.host_window = args.host_window
     R.disk_budget_frac = args.disk_budget
+    R.train = args.train
     t = time.time()
     L = R.run(1, keep_last=True)
     torch.cuda.synchronize()
@@ -385,7 +397,7 @@ def main():
     ms = e0.elapsed_time(e1)
     kst = {}
     per_stream = {}
-    for name, c in zip(("layout", "assemble", "host_gather"), R.ctxs()):
+    for name, c in zip(("layout", "assemble", "host_gather", "train"), R.ctxs()):
         st = c.kernel_stats()
         per_stream[name] = round(sum(v["ms"] for v in st.values()) / args.steps, 2)
         for k, v in st.items():
@@ -426,8 +438,9 @@ def main():
                                                        "packed-only space"),
                    "parallelism": f"dp{ws} (batch-sharded, count all-reduce)",
                    "host_window_batches": args.host_window,
-                   "schedule": "sequential" if args.sequential else
-                   "pipelined: layout of pass e+1 overlaps assembly of pass e (2 streams)",
+                   "schedule": ("sequential" if args.sequential else
+                                "pipelined: layout of pass e+1 overlaps assembly of pass e (2 streams)")
+                               + ("; trainer stub per run on its own stream (depth-2 queue)" if args.train else ""),
                    "l2": "inputs larger than L2 (features %.1f GB, CSR %.1f GB); no flush needed" % (
                        feats.numel() * 4 / 1e9, (indptr.numel() * 8 + indices.numel() * 4) / 1e9)},
         "packed_gbs": round(stats0["packed_bytes"] * ws * args.steps / (ms_max / 1e3) / 1e9, 2),

@@ -112,14 +112,42 @@ __global__ void __launch_bounds__(256) k_layer(RunView v, int h, const int64_t* 
         V* dst = reinterpret_cast<V*>(scratch + f * dim);
         const int32_t* src = v.src_local + v.edge_off[b];
         const float cnt = (float)(e1 - e0);
-        for (int64_t q = lane; q < nvec; q += 32) {
+        for (int64_t q0 = 0; q0 < nvec; q0 += 32) {
+            const int64_t q = q0 + lane;
+            const bool in = q < nvec;
             if (e1 == e0) {
-                dst[q] = self[q];
+                if (in) dst[q] = self[q];
                 continue;
             }
             V s = vzero<V>();
-            for (int32_t e = e0; e < e1; ++e) acc<V>(s, reinterpret_cast<const V*>(x + (rb + src[e]) * dim)[q]);
-            dst[q] = upd(self[q], s, cnt);
+            // neighbour ids of 32 edges at a time, one per lane, broadcast with shuffles; four
+            // row loads in flight per lane, accumulated strictly in edge order
+            for (int32_t eb = e0; eb < e1; eb += 32) {
+                const int ne = min(32, e1 - eb);
+                const int32_t my = lane < ne ? src[eb + lane] : 0;
+                int t = 0;
+                for (; t + 4 <= ne; t += 4) {
+                    const int32_t u0 = __shfl_sync(0xffffffffu, my, t);
+                    const int32_t u1 = __shfl_sync(0xffffffffu, my, t + 1);
+                    const int32_t u2 = __shfl_sync(0xffffffffu, my, t + 2);
+                    const int32_t u3 = __shfl_sync(0xffffffffu, my, t + 3);
+                    if (in) {
+                        const V r0 = reinterpret_cast<const V*>(x + (rb + u0) * dim)[q];
+                        const V r1 = reinterpret_cast<const V*>(x + (rb + u1) * dim)[q];
+                        const V r2 = reinterpret_cast<const V*>(x + (rb + u2) * dim)[q];
+                        const V r3 = reinterpret_cast<const V*>(x + (rb + u3) * dim)[q];
+                        acc<V>(s, r0);
+                        acc<V>(s, r1);
+                        acc<V>(s, r2);
+                        acc<V>(s, r3);
+                    }
+                }
+                for (; t < ne; ++t) {
+                    const int32_t u = __shfl_sync(0xffffffffu, my, t);
+                    if (in) acc<V>(s, reinterpret_cast<const V*>(x + (rb + u) * dim)[q]);
+                }
+            }
+            if (in) dst[q] = upd(self[q], s, cnt);
         }
     }
 }
