@@ -211,6 +211,7 @@ class Runner:
         # double-buffered slots only when two passes are in flight
         w0 = Workspace()
         self.ws = [w0, Workspace() if pipelined else w0]
+        self.asm_ws = Workspace()  # assembly rings / staging: every pass assembles on stream B
         self.counts = [torch.zeros(N, dtype=torch.int32, device=dev) for _ in range(2)]
         cfg = inp[0]
         self.nb = (inp[3].numel() + cfg["batch_size"] - 1) // cfg["batch_size"]
@@ -259,11 +260,12 @@ class Runner:
             gctx = self.ctxG if os.environ.get("DGNN_GATHER_STREAM", "1") == "1" else None
             if self.train:
                 for _ in L.train_epoch(ctx=self.ctxB, train_ctx=self.ctxT, host_window=self.host_window,
-                                       gather_ctx=gctx):
+                                       gather_ctx=gctx, ws=self.asm_ws):
                     pass
                 self.sB.wait_stream(self.sT)  # the pass ends when its last batch is trained
             else:
-                for _ in L.assemble_epoch(ctx=self.ctxB, host_window=self.host_window, gather_ctx=gctx):
+                for _ in L.assemble_epoch(ctx=self.ctxB, host_window=self.host_window, gather_ctx=gctx,
+                                          ws=self.asm_ws):
                     pass
             ev_a = torch.cuda.Event(enable_timing=True)
             ev_a.record(self.sB)

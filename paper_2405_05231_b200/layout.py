@@ -241,7 +241,7 @@ class Layout:
 
     def assemble_epoch(self, ctx: A.Ctx | None = None, out_budget: int = 1 << 30, host_window: int = 128,
                        gather_ctx: A.Ctx | None = None, sharded_tier=None, remote=None, runs: bool = False,
-                       ring_wait: dict | None = None):
+                       ring_wait: dict | None = None, ws: Workspace | None = None):
         """Pipelined assembly: the chunks of the next run of batches are staged H2D
         on the side stream while the current run is assembled on the ctx stream (one
         dgnn_assemble_group launch per run).  Yields (b, features[n_b, dim]) per batch; a
@@ -261,7 +261,10 @@ class Layout:
 
         ``runs=True`` yields (b0, b1, out_run) once per run instead; with ``ring_wait`` (run index
         -> event) the run that reuses run i's output slot first waits for ring_wait[i] (a
-        consumer on another stream, e.g. the trainer: a queue of depth 2)."""
+        consumer on another stream, e.g. the trainer: a queue of depth 2).
+
+        ``ws``: a Workspace for the rings and staging buffers, reused by every epoch assembled
+        on the same stream (keeps tens of GB out of the caching allocator's churn)."""
         ctx = ctx or self.ctx
         gctx = gather_ctx or ctx
         nb = self.num_batches
@@ -282,33 +285,42 @@ class Layout:
                     r1 += 1
                 windows.append((r0, r1))
                 r0 = r1
+        def buf(name, nbytes, dtype=torch.uint8, shape=None):
+            nbytes = max(int(nbytes), 16)
+            if ws is None:
+                t = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+            else:
+                t = ws.dev(name, nbytes, dev)[:nbytes]
+            t = t[:nbytes // torch.empty(0, dtype=dtype).element_size() * torch.empty(0, dtype=dtype).element_size()]
+            t = t.view(dtype)
+            return t.view(shape) if shape is not None else t
+
         with torch.cuda.stream(ctx.stream):
             max_rows = max(s[1] - s[0] for s in spans)
             max_c = max(s[3] - s[2] for s in spans)
-            out_ring = [torch.empty((max_rows, self.dim), dtype=self.dtype, device=dev) for _ in range(2)]
+            esz = torch.empty(0, dtype=self.dtype).element_size()
+            out_ring = [buf(f"out{i}", max_rows * self.dim * esz, self.dtype, (max_rows, self.dim)) for i in range(2)]
             staged = self.arena is not None or self.disk is not None
             bounce_r = HostBuffer(FILE_CHUNK) if self.disk is not None else None
-            chunk_ring = [torch.empty(max(max_c, 16), dtype=torch.uint8, device=dev) for _ in range(2)] \
-                if staged else None
+            chunk_ring = [buf(f"chunk{i}", max_c) for i in range(2)] if staged else None
             dp = self.disk_plan
             if dp is not None:  # per run: its cache pages and its partial input (dense DISK rows)
                 dpre = np.concatenate([[0], np.cumsum(self.batch_tiers[:, 2])])
                 max_pg = max(int(dp.req_off_host[b1] - dp.req_off_host[b0]) for b0, b1 in groups)
                 max_pi = max(int(dpre[b1] - dpre[b0]) for b0, b1 in groups)
-                page_ring = [torch.empty(max(max_pg, 1) * 4096, dtype=torch.uint8, device=dev) for _ in range(2)]
-                part_ring = [torch.empty(max(max_pi * self.row_bytes, 16), dtype=torch.uint8, device=dev)
-                             for _ in range(2)]
+                page_ring = [buf(f"pages{i}", max(max_pg, 1) * 4096) for i in range(2)]
+                part_ring = [buf(f"partial{i}", max_pi * self.row_bytes) for i in range(2)]
             if windows:
                 # staging rows: the window's host-row accesses bound its distinct host rows
                 hpre = np.concatenate([[0], np.cumsum(self.batch_tiers[:, 1])])
                 cap = min(kh, max(int(hpre[groups[r1 - 1][1]] - hpre[groups[r0][0]]) for r0, r1 in windows))
-                stamp = torch.full((kh,), -1, dtype=torch.int32, device=dev)
+                stamp = buf("stamp", kh * 4, torch.int32)
+                stamp.fill_(-1)  # window ids restart at 0 every epoch
                 nbuf = 2 if gctx is not ctx else 1
-                smap = [torch.empty(kh, dtype=torch.int32, device=dev) for _ in range(nbuf)]
-                wlist = [torch.empty(max(cap, 1), dtype=torch.int32, device=dev) for _ in range(nbuf)]
-                wcount = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(nbuf)]
-                staging = [torch.empty(max(cap, 1) * self.row_bytes, dtype=torch.uint8, device=dev)
-                           for _ in range(nbuf)]
+                smap = [buf(f"smap{i}", kh * 4, torch.int32) for i in range(nbuf)]
+                wlist = [buf(f"wlist{i}", max(cap, 1) * 4, torch.int32) for i in range(nbuf)]
+                wcount = [buf(f"wcount{i}", 8, torch.int64)[:1] for i in range(nbuf)]
+                staging = [buf(f"staging{i}", max(cap, 1) * self.row_bytes) for i in range(nbuf)]
         if gctx is not ctx:
             gctx.stream.wait_stream(ctx.stream)  # stamp / buffers were created on the ctx stream
         run_window = {r0: wi for wi, (r0, _) in enumerate(windows)}

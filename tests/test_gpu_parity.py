@@ -305,3 +305,21 @@ def test_launch_counter_and_timing(dg, ctx, tiny):
     ctx.set_timing(False)
     assert ctx.launches() > l0
     assert st["sample_hop"]["launches"] >= 2 and st["sample_hop"]["ms"] > 0
+
+
+def test_assembly_workspace_reuse(dg, ctx, tiny):
+    """Rings and staging buffers from one Workspace reused across epochs (as bench.py's Runner
+    does): every epoch still equals the direct gather, including after a window-size change."""
+    from paper_2405_05231_b200.layout import Workspace
+    ip, ix, sd = tiny.indptr.numpy(), tiny.indices.numpy(), tiny.seeds.numpy()
+    feats = tiny.features.numpy()
+    ref = oracle.sample(ip, ix, sd, 256, [10, 5], RNG_SEED)
+    dev = torch.device("cuda", 0)
+    L = dg.offline_layout(ctx, tiny.indptr.to(dev), tiny.indices.to(dev), tiny.features.to(dev), tiny.seeds.to(dev),
+                          [10, 5], 256, 500, 1000, RNG_SEED, group_size=8)
+    ws = Workspace()
+    gctx = dg.Ctx(device=0, stream=torch.cuda.Stream(dev))
+    for window, budget in ((4, 1 << 30), (2, 256 * 7 * 512), (8, 1 << 30), (4, 1 << 30)):
+        for b, out in L.assemble_epoch(host_window=window, out_budget=budget, gather_ctx=gctx, ws=ws):
+            got = out.view(torch.uint8).reshape(out.shape[0], -1).cpu().numpy()
+            assert np.array_equal(got, oracle.assemble(feats, ref[b].nodes)), f"window {window} batch {b}"
