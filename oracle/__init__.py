@@ -25,6 +25,7 @@ Functions and the passage each follows:
   ``disk_cache_fill``   -- segmented disk cache, Eq. 2 and Algorithm 1,
   P:311-414 (readings d1-d8 in dgnn_oracle.c and DESIGN.md).
 * ``train_stub``        -- the trainer's surrogate of Eq. 1, reading t1.
+* ``pack_pages``        -- source pages read by individual vs batched packing (Fig. 6).
 """
 from __future__ import annotations
 
@@ -102,6 +103,8 @@ def _L():
             lib.oracle_disk_cache_fill.argtypes = [P, i64, P, P, P, i64, P]
             lib.oracle_train_stub.argtypes = [P, i64, i64, P, i32, P, P]
             lib.oracle_train_stub.restype = ctypes.c_int
+            lib.oracle_pack_pages.argtypes = [P, P, i64, i64, i64, i64, P, P]
+            lib.oracle_pack_pages.restype = ctypes.c_int
             _lib = lib
     return _lib
 
@@ -456,3 +459,15 @@ def train_stub(sample: Sample, feats) -> np.ndarray:
     if rc != 0:
         raise OracleError(rc, "train_stub")
     return x[: int(hop[1])].copy()
+
+
+# ------------------------------------------------- packing page accounting ----
+def pack_pages(packed_lists, num_nodes: int, row_bytes: int, part_rows: int):
+    """(individual, batched) 4096-byte source pages read to pack ``packed_lists`` (Fig. 6)."""
+    cat, off = _packed_concat(packed_lists)
+    ind = np.zeros(1, np.int64)
+    bat = np.zeros(1, np.int64)
+    rc = _L().oracle_pack_pages(_p(cat), _p(off), len(off) - 1, num_nodes, row_bytes, part_rows, _p(ind), _p(bat))
+    if rc != 0:
+        raise OracleError(rc, "pack_pages")
+    return int(ind[0]), int(bat[0])

@@ -737,3 +737,42 @@ int oracle_train_stub(float* x, int64_t n, int64_t dim, const int32_t* hop_off, 
     free(prev);
     return OR_OK;
 }
+
+/* ======================================================================== */
+/* Sec. 5.2 source-page accounting (Fig. 6). */
+/* The feature file holds row v at byte v * row_bytes, read in 4096-byte    */
+/* pages.  Individual packing fetches every needed row on its own, batch by */
+/* batch: the pages the row spans, re-read for every batch that needs it.   */
+/* Batched packing reads each partition of part_rows consecutive rows that  */
+/* holds at least one needed row exactly once, whole (part_rows * row_bytes */
+/* is a multiple of 4096: partitions never split a page).                  */
+/* ======================================================================== */
+int oracle_pack_pages(const int32_t* packed_ids, const int64_t* packed_off, int64_t nb, int64_t num_nodes,
+                      int64_t row_bytes, int64_t part_rows, int64_t* individual, int64_t* batched)
+{
+    if (row_bytes < 1 || part_rows < 1 || (part_rows * row_bytes) % DC_PAGE) return OR_EINVAL;
+    int64_t ind = 0;
+    int64_t nparts = (num_nodes + part_rows - 1) / part_rows;
+    uint8_t* touched = (uint8_t*)calloc((size_t)(nparts > 0 ? nparts : 1), 1);
+    if (!touched) return OR_ENOMEM;
+    for (int64_t b = 0; b < nb; ++b)
+        for (int64_t r = packed_off[b]; r < packed_off[b + 1]; ++r) {
+            int64_t v = packed_ids[r];
+            int64_t first = v * row_bytes / DC_PAGE, last = ((v + 1) * row_bytes - 1) / DC_PAGE;
+            ind += last - first + 1;
+            touched[v / part_rows] = 1;
+        }
+    int64_t bat = 0;
+    int64_t file_pages = (num_nodes * row_bytes + DC_PAGE - 1) / DC_PAGE;
+    for (int64_t p = 0; p < nparts; ++p) {
+        if (!touched[p]) continue;
+        int64_t p0 = p * part_rows * row_bytes / DC_PAGE;
+        int64_t p1 = (p + 1) * part_rows * row_bytes / DC_PAGE;
+        if (p1 > file_pages) p1 = file_pages;
+        bat += p1 - p0;
+    }
+    free(touched);
+    *individual = ind;
+    *batched = bat;
+    return OR_OK;
+}
