@@ -194,7 +194,7 @@ class Runner:
     def __init__(self, dg, inp, rank, dev, pipelined=True):
         from paper_2405_05231_b200.layout import Workspace
         self.dg, self.inp, self.rank, self.dev, self.pipelined = dg, inp, rank, dev, pipelined
-        self.sA = torch.cuda.Stream(dev)
+        self.sA = torch.cuda.Stream(dev, priority=int(os.environ.get("DGNN_LAYOUT_PRIORITY", "0")))
         # the PCIe-bound assembly gets the higher stream priority: its CTAs are scheduled
         # first and the layout of the next pass fills the remaining SM capacity
         # (sequential mode still assembles on its own stream: the stage-out of a pass overlaps

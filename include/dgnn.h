@@ -432,6 +432,28 @@ dgnn_status dgnn_disk_partial(dgnn_ctx* ctx, const dgnn_disk_plan* p, int64_t b_
                               const void* pages, const void* chunks, const int64_t* chunk_off, void* out,
                               const int64_t* out_off);
 
+/* ------------------------------- batched packing from partitions (NEXT #3) ---- */
+/* Sec. 5.2 (Fig. 6): when the feature table does not fit in HBM it is read in
+ * partitions of consecutive node IDs, each once and sequentially, and every packed row of every
+ * batch is routed from the partition that holds it.  The packed lists come as a
+ * dgnn_disk_index (its rows sorted by node, so the rows of a partition are one contiguous
+ * range).  Results equal dgnn_pack's ("append these node features to pack feature
+ * chunk of the mini-batch"); what differs is the source access pattern.
+ * dgnn_disk_index_partition_counts: counts_host[p] = packed rows whose node lies in
+ *   [p*part_rows, (p+1)*part_rows), p < nparts (host int64; synchronizes).
+ * dgnn_pack_partition: for the index's rows with node v in [p0, p1):
+ *   group_buf + chunk_off[b] + (r - packed_off[b]) * row_bytes  <-  part + (v - p0) * row_bytes
+ *   part       device (or pinned) [(p1-p0) * row_bytes]: rows p0 .. p1-1 of the feature table.
+ *   chunk_off  device int64 [nb+1]: the chunk layout (reading c20) of the index's packed lists.
+ * dgnn_pack_tails: zero every chunk's bytes past its rows (reading c20).
+ * Both are enqueued on the ctx stream without synchronizing; row_bytes % 16 == 0. */
+dgnn_status dgnn_disk_index_partition_counts(dgnn_ctx* ctx, const dgnn_disk_index* idx, int64_t part_rows,
+                                             int64_t nparts, int64_t* counts_host);
+dgnn_status dgnn_pack_partition(dgnn_ctx* ctx, const dgnn_disk_index* idx, const void* part, int64_t p0, int64_t p1,
+                                int64_t row_bytes, const int64_t* chunk_off, void* group_buf);
+dgnn_status dgnn_pack_tails(dgnn_ctx* ctx, const dgnn_disk_index* idx, int64_t row_bytes, const int64_t* chunk_off,
+                            void* group_buf);
+
 /* ------------------------------------------------ trainer stub (NEXT #2) ---- */
 /* The model-training stage of the pipeline with the surrogate of Eq. 1
  * that SPEC S:409-413 fixes: h^k_v = h^{k-1}_v + mean{h^{k-1}_u : u in N(v)}, no W, no sigma.

@@ -43,7 +43,7 @@ EXPORTS = [
     "dgnn_file_open", "dgnn_file_close", "dgnn_stage_file_write", "dgnn_stage_file_read",
     "dgnn_disk_index_build", "dgnn_disk_index_free", "dgnn_disk_space", "dgnn_disk_search", "dgnn_disk_plan_build",
     "dgnn_disk_plan_get_info", "dgnn_disk_plan_free", "dgnn_disk_cache_fill", "dgnn_disk_partial",
-    "dgnn_train_stub",
+    "dgnn_train_stub", "dgnn_disk_index_partition_counts", "dgnn_pack_partition", "dgnn_pack_tails",
 ]
 
 
@@ -157,6 +157,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "dgnn_disk_cache_fill": (i32, [P, P, P, i64, P]),
             "dgnn_disk_partial": (i32, [P, P, i64, i64, P, P, P, P, P]),
             "dgnn_train_stub": (i32, [P, P, i64, i64, P, i64]),
+            "dgnn_disk_index_partition_counts": (i32, [P, P, i64, i64, P]),
+            "dgnn_pack_partition": (i32, [P, P, P, i64, i64, i64, P, P]),
+            "dgnn_pack_tails": (i32, [P, P, i64, P, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -640,3 +643,23 @@ def dgnn_train_stub(ctx: Ctx, samples: Samples, b_lo: int, b_hi: int, x: torch.T
     dim = x.shape[-1] if x.dim() > 1 else 1
     _check(load_library().dgnn_train_stub(ctx.handle, samples.handle, int(b_lo), int(b_hi), _ptr(x), int(dim)),
            "dgnn_train_stub")
+
+
+# ------------------------------------------ batched packing from partitions ----
+def dgnn_disk_index_partition_counts(ctx: Ctx, idx: DiskIndex, part_rows: int, nparts: int):
+    import numpy as np
+    out = np.zeros(max(int(nparts), 1), np.int64)
+    _check(load_library().dgnn_disk_index_partition_counts(ctx.handle, idx.handle, int(part_rows), int(nparts),
+                                                           P(out.ctypes.data)), "dgnn_disk_index_partition_counts")
+    return out[:int(nparts)]
+
+
+def dgnn_pack_partition(ctx: Ctx, idx: DiskIndex, part, p0: int, p1: int, row_bytes: int, chunk_off: torch.Tensor,
+                        group_buf):
+    _check(load_library().dgnn_pack_partition(ctx.handle, idx.handle, _ptr(part), int(p0), int(p1), int(row_bytes),
+                                              _ptr(chunk_off), _ptr(group_buf)), "dgnn_pack_partition")
+
+
+def dgnn_pack_tails(ctx: Ctx, idx: DiskIndex, row_bytes: int, chunk_off: torch.Tensor, group_buf):
+    _check(load_library().dgnn_pack_tails(ctx.handle, idx.handle, int(row_bytes), _ptr(chunk_off), _ptr(group_buf)),
+           "dgnn_pack_tails")

@@ -870,3 +870,129 @@ extern "C" dgnn_status dgnn_disk_partial(dgnn_ctx* c, const dgnn_disk_plan* p, i
     DGNN_CK_LAUNCH();
     return DGNN_OK;
 }
+
+// ----------------------------------------- batched packing from partitions (NEXT #3)
+namespace dgnn {
+namespace {
+
+__global__ void k_part_counts(const uint32_t* __restrict__ rv, int64_t R, int64_t part_rows, int64_t nparts,
+                              unsigned long long* __restrict__ cnt) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < R; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = rv[j] / part_rows;
+        // rows are sorted by node: only the first row of each partition's run adds the run length
+        if (j > 0 && rv[j - 1] / part_rows == p) continue;
+        int64_t lo = j, hi = R;  // first row of the next partition
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if ((int64_t)(rv[mid] / part_rows) <= p) lo = mid + 1;
+            else hi = mid;
+        }
+        if (p < nparts) cnt[p] = (unsigned long long)(lo - j);
+    }
+}
+
+// [j0, j1) = rows of the sorted index with node in [p0, p1)
+__global__ void k_part_bounds(const uint32_t* __restrict__ rv, int64_t R, int64_t p0, int64_t p1,
+                              int64_t* __restrict__ bounds) {
+    const int64_t key = threadIdx.x == 0 ? p0 : p1;
+    if (threadIdx.x > 1) return;
+    int64_t lo = 0, hi = R;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((int64_t)rv[mid] < key) lo = mid + 1;
+        else hi = mid;
+    }
+    bounds[threadIdx.x] = lo;
+}
+
+struct PartRow {
+    const uint8_t* part;
+    int64_t p0, row_bytes, j0;
+    const uint32_t* rv;
+    const uint32_t* rr;
+    const int32_t* rb;
+    const int64_t* packed_off;
+    const int64_t* chunk_off;
+    uint8_t* dst;
+    __device__ __forceinline__ bool operator()(int64_t i, const uint8_t*& s, uint8_t*& d) const {
+        const int64_t j = j0 + i;
+        const int b = rb[j];
+        s = part + ((int64_t)rv[j] - p0) * row_bytes;
+        d = dst + chunk_off[b] + ((int64_t)rr[j] - packed_off[b]) * row_bytes;
+        return true;
+    }
+};
+
+__global__ void __launch_bounds__(256) k_pack_part(PartRow fn, const int64_t* __restrict__ bounds) {
+    const int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    PartRow f = fn;
+    f.j0 = bounds[0];
+    copy_rows_warp<4, uint4>(bounds[1] - bounds[0], f.row_bytes, f, warp, nwarps);
+}
+
+__global__ void k_pack_tails(const int64_t* __restrict__ packed_off, const int64_t* __restrict__ chunk_off, int nb,
+                             int64_t row_bytes, uint8_t* __restrict__ dst) {
+    const int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int lane = threadIdx.x & 31;
+    for (int64_t b = warp; b < nb; b += nwarps) {
+        const int64_t start = chunk_off[b] + (packed_off[b + 1] - packed_off[b]) * row_bytes;
+        const int64_t nz = (chunk_off[b + 1] - start) / 16;  // row_bytes % 16 == 0: 16-byte aligned
+        uint4* z = reinterpret_cast<uint4*>(dst + start);
+        for (int64_t i = lane; i < nz; i += 32) __stcs(z + i, make_uint4(0, 0, 0, 0));
+    }
+}
+
+}  // namespace
+}  // namespace dgnn
+
+extern "C" dgnn_status dgnn_disk_index_partition_counts(dgnn_ctx* c, const dgnn_disk_index* x, int64_t part_rows,
+                                                        int64_t nparts, int64_t* counts_host) {
+    DGNN_REQUIRE(c && x && part_rows > 0 && nparts >= 0 && (nparts == 0 || counts_host),
+                 "dgnn_disk_index_partition_counts: bad argument");
+    DGNN_CK(cudaSetDevice(c->device));
+    DevBuf<unsigned long long> cnt;
+    DGNN_TRY(cnt.alloc(c, (size_t)nparts));
+    DGNN_TRY(memset_async(c, cnt.p, 0, (size_t)(nparts > 0 ? nparts : 1) * 8));
+    if (x->R) {
+        launch(c, DGNN_K_PACK, 0.0, [&] {
+            k_part_counts<<<grid1(c, x->R), 256, 0, c->stream>>>(x->rv, x->R, part_rows, nparts, cnt.p);
+        });
+        DGNN_CK_LAUNCH();
+    }
+    return d2h(c, reinterpret_cast<unsigned long long*>(counts_host), cnt.p, (size_t)nparts);
+}
+
+extern "C" dgnn_status dgnn_pack_partition(dgnn_ctx* c, const dgnn_disk_index* x, const void* part, int64_t p0,
+                                           int64_t p1, int64_t row_bytes, const int64_t* chunk_off, void* group_buf) {
+    DGNN_REQUIRE(c && x && chunk_off && 0 <= p0 && p0 <= p1, "dgnn_pack_partition: bad argument");
+    DGNN_REQUIRE(row_bytes > 0 && row_bytes % 16 == 0 && al16(part) && al16(group_buf),
+                 "dgnn_pack_partition: rows and buffers must be 16-byte aligned");
+    if (x->R == 0 || p0 == p1) return DGNN_OK;
+    DGNN_REQUIRE(part && group_buf, "dgnn_pack_partition: NULL buffer");
+    DGNN_CK(cudaSetDevice(c->device));
+    DevBuf<int64_t> bounds;
+    DGNN_TRY(bounds.alloc(c, 2));
+    launch(c, DGNN_K_PACK, 0.0, [&] { k_part_bounds<<<1, 32, 0, c->stream>>>(x->rv, x->R, p0, p1, bounds.p); });
+    DGNN_CK_LAUNCH();
+    PartRow fn{(const uint8_t*)part, p0, row_bytes, 0, x->rv, x->rr, x->rb, x->packed_off, chunk_off, (uint8_t*)group_buf};
+    const int grid = grid_for(c, std::min<int64_t>(x->R, p1 - p0) * 32 / 4, 256, 5);
+    launch(c, DGNN_K_PACK, 0.0, [&] { k_pack_part<<<grid, 256, 0, c->stream>>>(fn, bounds.p); });
+    DGNN_CK_LAUNCH();
+    return DGNN_OK;
+}
+
+extern "C" dgnn_status dgnn_pack_tails(dgnn_ctx* c, const dgnn_disk_index* x, int64_t row_bytes,
+                                       const int64_t* chunk_off, void* group_buf) {
+    DGNN_REQUIRE(c && x && chunk_off && row_bytes > 0 && row_bytes % 16 == 0, "dgnn_pack_tails: bad argument");
+    if (x->nb == 0) return DGNN_OK;
+    DGNN_REQUIRE(group_buf && al16(group_buf), "dgnn_pack_tails: bad buffer");
+    DGNN_CK(cudaSetDevice(c->device));
+    launch(c, DGNN_K_PACK, 0.0, [&] {
+        k_pack_tails<<<grid_for(c, x->nb * 32, 256), 256, 0, c->stream>>>(x->packed_off, chunk_off, (int)x->nb,
+                                                                        row_bytes, (uint8_t*)group_buf);
+    });
+    DGNN_CK_LAUNCH();
+    return DGNN_OK;
+}
