@@ -232,7 +232,7 @@ class Runner:
     def ctxs(self):
         return [self.ctxA, self.ctxB, self.ctxG, self.ctxT]
 
-    def layout(self, slot):
+    def layout(self, slot, after_sample=None):
         cfg, indptr, indices, seeds, feats, gpu_rows, host_rows = self.inp
         if self.before_layout is not None:
             self.before_layout()
@@ -242,11 +242,36 @@ class Runner:
                                       gpu_rows, host_rows, RNG_SEED, group_size=cfg["group_size"],
                                       batch_id_base=self.rank * self.nb, counts=c, ws=self.ws[slot],
                                       stage_piece=int(os.environ.get("DGNN_STAGE_PIECE", str(1 << 40))),
-                                      disk_budget_frac=self.disk_budget_frac)
+                                      disk_budget_frac=self.disk_budget_frac, after_sample=after_sample)
+
+    def _assemble(self, L, ev_l):
+        """Enqueue the assembly (and trainer) of pass L on stream B after its layout; -> end event."""
+        self.sB.wait_event(ev_l)
+        a0 = torch.cuda.Event(enable_timing=True)
+        a0.record(self.sB)
+        gctx = self.ctxG if os.environ.get("DGNN_GATHER_STREAM", "1") == "1" else None
+        if self.train:
+            for _ in L.train_epoch(ctx=self.ctxB, train_ctx=self.ctxT, host_window=self.host_window,
+                                   gather_ctx=gctx, ws=self.asm_ws):
+                pass
+            self.sB.wait_stream(self.sT)  # the pass ends when its last batch is trained
+        else:
+            for _ in L.assemble_epoch(ctx=self.ctxB, host_window=self.host_window, gather_ctx=gctx,
+                                      ws=self.asm_ws):
+                pass
+        ev_a = torch.cuda.Event(enable_timing=True)
+        ev_a.record(self.sB)
+        self.timeline.append(((L.stats.get("_events", []), L.stats.get("_host", [])), a0, ev_a))
+        return ev_a
 
     def run(self, K: int, keep_last=False):
         """Enqueue K passes; returns the last Layout if keep_last.  self.timeline collects
-        (layout events, assembly start/end events) per pass for the device timeline."""
+        (layout events, assembly start/end events) per pass for the device timeline.
+
+        Pipelined: the assembly of pass e is enqueued first, then the layout of pass e+1 runs
+        next to it.  (Measured alternative: starting the assembly only after the next pass's
+        sampling -- which slows several-fold next to it -- gave 1250-1280 instead of ~1330
+        mini-batches/s: the assembly then overlaps the tier fill and stage-out instead.)"""
         self.timeline = []
         L = self.layout(0)
         ev_l = torch.cuda.Event()
@@ -254,22 +279,7 @@ class Runner:
         prev_ev = None
         last = None
         for e in range(K):
-            self.sB.wait_event(ev_l)
-            a0 = torch.cuda.Event(enable_timing=True)
-            a0.record(self.sB)
-            gctx = self.ctxG if os.environ.get("DGNN_GATHER_STREAM", "1") == "1" else None
-            if self.train:
-                for _ in L.train_epoch(ctx=self.ctxB, train_ctx=self.ctxT, host_window=self.host_window,
-                                       gather_ctx=gctx, ws=self.asm_ws):
-                    pass
-                self.sB.wait_stream(self.sT)  # the pass ends when its last batch is trained
-            else:
-                for _ in L.assemble_epoch(ctx=self.ctxB, host_window=self.host_window, gather_ctx=gctx,
-                                          ws=self.asm_ws):
-                    pass
-            ev_a = torch.cuda.Event(enable_timing=True)
-            ev_a.record(self.sB)
-            self.timeline.append(((L.stats.get("_events", []), L.stats.get("_host", [])), a0, ev_a))
+            ev_a = self._assemble(L, ev_l)
             Ln = None
             if e + 1 < K:
                 if not self.pipelined:

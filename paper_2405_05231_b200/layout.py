@@ -434,7 +434,7 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
                    counts: torch.Tensor | None = None, ws: Workspace | None = None,
                    group_budget: int = 4 << 30, stage_piece: int = 1 << 40, file_path: str | None = None,
                    direct_io: bool = True, disk_budget: int | None = None, disk_m: int = 1,
-                   disk_k: int = 4, disk_budget_frac: float | None = None) -> Layout:
+                   disk_k: int = 4, disk_budget_frac: float | None = None, after_sample=None) -> Layout:
     """Run a1-a8 on this rank's batches.
 
     ``seeds`` are this rank's seeds (batch t of them gets bid = batch_id_base + t).
@@ -445,6 +445,9 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
     the packed chunks exceed it -- the heuristic of P:410-413 picks the smallest segment
     size s whose Eq. 2 space fits (threshold ``disk_m``, MinHash with ``disk_k`` hashes).
     ``disk_budget_frac`` states the budget as a fraction of the packed-only space instead.
+    ``after_sample``: called once the samples are complete (dgnn_sample returns when they are),
+    before the rest of the pass is enqueued -- a scheduling hook (bench.py starts the previous
+    pass's assembly there, so that sampling never shares the GPU with it).
     """
     dev = ctx.device
     N = indptr.numel() - 1
@@ -467,6 +470,8 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
     # a1-a3 (+ the fused access counter)
     samples = A.dgnn_sample(ctx, indptr, indices, seeds, batch_size, fanout, rng_seed, batch_id_base, counts)
     mark("sample")
+    if after_sample is not None:
+        after_sample()
     # a4: global histogram across ranks
     d = _dist()
     if d is not None:
