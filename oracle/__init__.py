@@ -82,7 +82,7 @@ def _L():
             lib.oracle_draw64.restype = u64
             lib.oracle_floyd.argtypes = [i64, i32, u64, u32, u64, u32, P]
             lib.oracle_floyd_core.argtypes = [i64, i32, P, P]
-            lib.oracle_sample_range.argtypes = [P, P, i64, P, i64, i32, i64, P, i32, u64, i64, i64, i32, P]
+            lib.oracle_sample_range.argtypes = [P, P, i64, P, i64, i32, i64, P, i32, u64, i64, i64, i32, P, i32]
             lib.oracle_sample_range.restype = ctypes.c_int
             lib.oracle_batch_free.argtypes = [ctypes.POINTER(_Batch)]
             lib.oracle_count_add.argtypes = [P, i64, P]
@@ -101,7 +101,7 @@ def _L():
             lib.oracle_disk_plan.argtypes = [P, P, i64, i64, i64, i64, i64, i32, u64, i32,
                                              P, P, P, P, P, P, P, P, P]
             lib.oracle_disk_cache_fill.argtypes = [P, i64, P, P, P, i64, P]
-            lib.oracle_train_stub.argtypes = [P, i64, i64, P, i32, P, P]
+            lib.oracle_train_stub.argtypes = [P, i64, i64, P, i32, P, P, i32]
             lib.oracle_train_stub.restype = ctypes.c_int
             lib.oracle_pack_pages.argtypes = [P, P, i64, i64, i64, i64, P, P]
             lib.oracle_pack_pages.restype = ctypes.c_int
@@ -157,8 +157,9 @@ class Sample:
     bid: int
     nodes: np.ndarray      # int32 [n]
     hop_off: np.ndarray    # int32 [H+2]
-    eptr: np.ndarray       # int32 [hop_off[H]+1]
+    eptr: np.ndarray       # int32 [hop_off[H]+1]; blocks: per hop h, hop_off[h+1]+1 entries, concatenated
     src_local: np.ndarray  # int32 [num_edges]
+    blocks: bool = False   # the DGL-block variant (reading c27)
 
 
 def num_batches(num_seeds: int, batch_size: int) -> int:
@@ -166,8 +167,11 @@ def num_batches(num_seeds: int, batch_size: int) -> int:
 
 
 def sample(indptr, indices, seeds, batch_size: int, fanout, rng_seed: int,
-           batch_id_base: int = 0, batches=None, threads: int = 1) -> list:
+           batch_id_base: int = 0, batches=None, threads: int = 1, blocks: bool = False) -> list:
     """Sample batches t (default: all ceil(S/B)); returns a list of Sample.
+
+    ``blocks``: the DGL-block variant (reading c27): every node of the sample so far is
+    resampled at each hop, and each hop has its own eptr array.
 
     ``batches`` may be a range/list of batch ordinals t to sample (each keyed
     by bid = batch_id_base + t); they are processed as contiguous runs.
@@ -189,7 +193,7 @@ def sample(indptr, indices, seeds, batch_size: int, fanout, rng_seed: int,
         arr = (ctypes.POINTER(_Batch) * (t_hi - t_lo))()
         rc = L.oracle_sample_range(_p(indptr), _p(indices), len(indptr) - 1, _p(seeds), len(seeds),
                                    batch_size, batch_id_base, _p(fan), len(fan), rng_seed, t_lo, t_hi,
-                                   threads, ctypes.cast(arr, ctypes.c_void_p))
+                                   threads, ctypes.cast(arr, ctypes.c_void_p), int(bool(blocks)))
         try:
             if rc != 0:
                 raise OracleError(rc, "sample")
@@ -198,13 +202,15 @@ def sample(indptr, indices, seeds, batch_size: int, fanout, rng_seed: int,
                 H = b.num_hops
                 n = b.num_nodes
                 hop = np.ctypeslib.as_array(b.hop_off, (H + 2,)).copy()
+                n_eptr = int(sum(int(hop[h + 1]) + 1 for h in range(H))) if blocks else int(hop[H]) + 1
                 out.append(Sample(
                     bid=batch_id_base + t,
                     nodes=np.ctypeslib.as_array(b.nodes, (n,)).copy() if n else np.zeros(0, np.int32),
                     hop_off=hop,
-                    eptr=np.ctypeslib.as_array(b.eptr, (int(hop[H]) + 1,)).copy(),
+                    eptr=np.ctypeslib.as_array(b.eptr, (n_eptr,)).copy(),
                     src_local=(np.ctypeslib.as_array(b.src_local, (b.num_edges,)).copy()
                                if b.num_edges else np.zeros(0, np.int32)),
+                    blocks=bool(blocks),
                 ))
         finally:
             for t in range(t_lo, t_hi):
@@ -455,7 +461,8 @@ def train_stub(sample: Sample, feats) -> np.ndarray:
     hop = _c(sample.hop_off, np.int32)
     ep = _c(sample.eptr, np.int32)
     src = _c(sample.src_local, np.int32)
-    rc = _L().oracle_train_stub(_p(x), x.shape[0], x.shape[1], _p(hop), H, _p(ep), _p(src))
+    rc = _L().oracle_train_stub(_p(x), x.shape[0], x.shape[1], _p(hop), H, _p(ep), _p(src),
+                                int(bool(getattr(sample, "blocks", False))))
     if rc != 0:
         raise OracleError(rc, "train_stub")
     return x[: int(hop[1])].copy()

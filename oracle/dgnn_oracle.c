@@ -158,10 +158,15 @@ void oracle_batch_free(oracle_batch* b)
 
 /* Sample batch `bid` with seeds seeds[0..ns).  Oracle algorithm steps 2-3
  * of DESIGN.md: the frontier at hop h is the set of nodes first discovered
- * at hop h-1 (reading c4, following Fig. 1 P:205 where v0 does not resample). */
+ * at hop h-1 (reading c4, following Fig. 1 P:205 where v0 does not resample).
+ * blocks != 0: the DGL-block variant ("the
+ * multi-layer GNN computation ... the neighbors of each node", reading c27):
+ * the frontier at hop h is EVERY node of the sample so far (local [0,
+ * hop_off[h+1])), so every destination node of a layer resamples; eptr then
+ * holds one array of hop_off[h+1] + 1 entries per hop, concatenated. */
 oracle_batch* oracle_sample_batch(const int64_t* indptr, const int32_t* indices, int64_t num_nodes,
                                   const int32_t* seeds, int64_t ns, const int32_t* fanout,
-                                  int32_t num_hops, uint64_t rng_seed, uint64_t bid)
+                                  int32_t num_hops, uint64_t rng_seed, uint64_t bid, int32_t blocks)
 {
     oracle_batch* B = (oracle_batch*)calloc(1, sizeof(oracle_batch));
     if (!B) return NULL;
@@ -192,21 +197,26 @@ oracle_batch* oracle_sample_batch(const int64_t* indptr, const int32_t* indices,
     B->hop_off[0] = 0;
     B->hop_off[1] = (int32_t)ns;
 
-    /* eptr is indexed by frontier local index; every node with local index
-     * < hop_off[H] is a frontier node of exactly one hop. */
+    /* node-wise: eptr is indexed by frontier local index; every node with local
+     * index < hop_off[H] is a frontier node of exactly one hop.
+     * blocks: hop h's array starts at eptr_base = sum over i < h of (hop_off[i+1] + 1). */
     int64_t cap_eptr = ns + 1;
     B->eptr = (int32_t*)malloc((size_t)cap_eptr * sizeof(int32_t));
     B->eptr[0] = 0;
     int64_t ne = 0;
+    int64_t eptr_base = 0;
 
     int64_t lo = 0, hi = ns; /* frontier = local [lo, hi) */
     for (int32_t h = 0; h < num_hops; ++h) {
         int32_t k = fanout[h];
         /* eptr must cover frontier nodes lo..hi-1 */
-        if (hi + 1 > cap_eptr) {
-            cap_eptr = hi + 1;
+        int64_t need = blocks ? eptr_base + hi + 1 : hi + 1;
+        if (need > cap_eptr) {
+            cap_eptr = need;
             B->eptr = (int32_t*)realloc(B->eptr, (size_t)cap_eptr * sizeof(int32_t));
         }
+        int32_t* ep = blocks ? B->eptr + eptr_base : B->eptr;  /* ep[j] .. ep[j+1]: node j's edges */
+        if (blocks) ep[0] = (int32_t)ne;
         int64_t cand_begin = ne;
         /* step 3: per frontier node, ascending local j */
         for (int64_t j = lo; j < hi; ++j) {
@@ -226,8 +236,9 @@ oracle_batch* oracle_sample_batch(const int64_t* indptr, const int32_t* indices,
                 for (int32_t s = 0; s < k; ++s) B->src_local[ne++] = indices[start + P[s]];
                 free(P);
             }
-            B->eptr[j + 1] = (int32_t)ne;
+            ep[j + 1] = (int32_t)ne;
         }
+        if (blocks) eptr_base += hi + 1;
         /* new = sorted(set(candidates) - set(nodes)) ascending global ID (c10) */
         int64_t nc = ne - cand_begin;
         int32_t* cs = (int32_t*)malloc((size_t)(nc > 0 ? nc : 1) * sizeof(int32_t));
@@ -263,7 +274,7 @@ oracle_batch* oracle_sample_batch(const int64_t* indptr, const int32_t* indices,
             B->src_local[e] = hit->local;
         }
         free(all);
-        lo = n_before;
+        lo = blocks ? 0 : n_before;
         hi = n;
     }
     B->num_nodes = n;
@@ -277,7 +288,7 @@ int oracle_sample_range(const int64_t* indptr, const int32_t* indices, int64_t n
                         const int32_t* seeds, int64_t num_seeds, int32_t batch_size,
                         int64_t batch_id_base, const int32_t* fanout, int32_t num_hops,
                         uint64_t rng_seed, int64_t t_lo, int64_t t_hi, int32_t threads,
-                        oracle_batch** out)
+                        oracle_batch** out, int32_t blocks)
 {
     if (batch_size <= 0 || num_hops < 1) return OR_EINVAL;
     (void)threads;
@@ -286,7 +297,7 @@ int oracle_sample_range(const int64_t* indptr, const int32_t* indices, int64_t n
         int64_t a = t * batch_size;
         int64_t b = a + batch_size < num_seeds ? a + batch_size : num_seeds;
         out[t - t_lo] = oracle_sample_batch(indptr, indices, num_nodes, seeds + a, b - a, fanout,
-                                            num_hops, rng_seed, (uint64_t)(batch_id_base + t));
+                                            num_hops, rng_seed, (uint64_t)(batch_id_base + t), blocks);
     }
     for (int64_t t = t_lo; t < t_hi; ++t) {
         if (!out[t - t_lo]) return OR_ENOMEM;
@@ -717,15 +728,24 @@ void oracle_disk_cache_fill(const uint8_t* features, int64_t row_bytes, const in
 /* updated in place; the seeds' embeddings are rows [0, hop_off[1]).         */
 /* ======================================================================== */
 int oracle_train_stub(float* x, int64_t n, int64_t dim, const int32_t* hop_off, int32_t H, const int32_t* eptr,
-                      const int32_t* src_local)
+                      const int32_t* src_local, int32_t blocks)
 {
     float* prev = (float*)malloc((size_t)(n > 0 ? n : 1) * (size_t)dim * sizeof(float));
     if (!prev) return OR_ENOMEM;
     for (int32_t k = 1; k <= H; ++k) {
         int32_t h = H - k;
         memcpy(prev, x, (size_t)n * (size_t)dim * sizeof(float));  /* h^{k-1} */
-        for (int64_t j = hop_off[h]; j < hop_off[h + 1]; ++j) {
-            int32_t e0 = eptr[j], e1 = eptr[j + 1];
+        /* layer k's destination nodes: hop h's frontier (node-wise: the nodes discovered at
+         * hop h-1; blocks: every node of the sample so far) and where their edges start */
+        int64_t lo = blocks ? 0 : hop_off[h];
+        const int32_t* ep = eptr;
+        if (blocks) {
+            int64_t base = 0;
+            for (int32_t i = 0; i < h; ++i) base += hop_off[i + 1] + 1;
+            ep = eptr + base;
+        }
+        for (int64_t j = lo; j < hop_off[h + 1]; ++j) {
+            int32_t e0 = ep[j], e1 = ep[j + 1];
             if (e1 == e0) continue;
             for (int64_t d = 0; d < dim; ++d) {
                 float s = 0.0f;
