@@ -118,6 +118,14 @@ dgnn_status dgnn_ctx_sync(dgnn_ctx* ctx);
 const char* dgnn_last_error(void);
 /* Tuning knob: batches sampled concurrently per sampling group (0 = automatic). */
 dgnn_status dgnn_ctx_set_sample_group(dgnn_ctx* ctx, int32_t batches);
+/* Sampling variant for later dgnn_sample calls on this ctx: DGNN_SAMPLE_NODEWISE (default;
+ * reading c4: the frontier of hop h is the nodes first discovered at hop h-1) or
+ * DGNN_SAMPLE_BLOCKS (the DGL-block variant, reading c27: the frontier of hop h is every node
+ * of the sample so far, so each destination node of a layer resamples; eptr then holds one
+ * array of hop_off[b][h+1] + 1 entries per hop h, concatenated). */
+#define DGNN_SAMPLE_NODEWISE 0
+#define DGNN_SAMPLE_BLOCKS 1
+dgnn_status dgnn_ctx_set_sample_mode(dgnn_ctx* ctx, int32_t mode);
 /* Tuning knob: resident CTAs per SM for the assemble kernels (default 8).  The assemble
  * kernel is PCIe-bound on host-tier rows; a low value leaves SMs to a concurrent offline
  * pass on another stream (epoch pipelining). */
@@ -181,12 +189,14 @@ typedef struct {
     const int64_t* eptr_off;      /* [nb+1]: batch b's eptr starts at eptr[eptr_off[b]]               */
     const int32_t* eptr;          /* per batch hop_off[b][H]+1 entries: edges of frontier node j are  */
                                   /* src_local[edge_off[b] + eptr[j] .. edge_off[b] + eptr[j+1])      */
+                                  /* (DGNN_SAMPLE_BLOCKS: per hop h an array of hop_off[b][h+1]+1)   */
     const int64_t* edge_off;      /* [nb+1]                                                           */
     const int32_t* src_local;     /* [total_edges] local index (within the batch) of each neighbour   */
     const int64_t* node_off_host; /* host mirrors of the offset arrays                                */
     const int64_t* edge_off_host;
     const int64_t* eptr_off_host;
     const int32_t* hop_off_host;
+    int32_t mode;                 /* DGNN_SAMPLE_NODEWISE or DGNN_SAMPLE_BLOCKS (eptr layout)       */
 } dgnn_samples_info;
 dgnn_status dgnn_samples_get_info(const dgnn_samples* s, dgnn_samples_info* info);
 void dgnn_samples_free(dgnn_samples* s);
@@ -459,7 +469,8 @@ dgnn_status dgnn_pack_tails(dgnn_ctx* ctx, const dgnn_disk_index* idx, int64_t r
  * that SPEC S:409-413 fixes: h^k_v = h^{k-1}_v + mean{h^{k-1}_u : u in N(v)}, no W, no sigma.
  * Reading t1: layer k = 1..H handles sampling hop h = H-k (deepest first); N(v) = v's sampled
  * neighbours at the hop v expanded in (src_local); a node outside hop h, or without edges,
- * keeps its value.  fp32: the sum starts at 0 and adds neighbours in edge order, then one
+ * keeps its value.  For DGNN_SAMPLE_BLOCKS samples, hop h's destinations are every node of
+ * local index < hop_off[b][h+1] with their hop-h edges.  fp32: the sum starts at 0 and adds neighbours in edge order, then one
  * IEEE division by the edge count and one addition (bit-identical to the oracle).
  *   x    device fp32 [node_off[b_hi] - node_off[b_lo], dim]: the assembled rows of batches
  *        [b_lo, b_hi) in node order, updated IN PLACE; afterwards the rows of each batch's

@@ -43,7 +43,7 @@ EXPORTS = [
     "dgnn_file_open", "dgnn_file_close", "dgnn_stage_file_write", "dgnn_stage_file_read",
     "dgnn_disk_index_build", "dgnn_disk_index_free", "dgnn_disk_space", "dgnn_disk_search", "dgnn_disk_plan_build",
     "dgnn_disk_plan_get_info", "dgnn_disk_plan_free", "dgnn_disk_cache_fill", "dgnn_disk_partial",
-    "dgnn_train_stub", "dgnn_disk_index_partition_counts", "dgnn_pack_partition", "dgnn_pack_tails",
+    "dgnn_train_stub", "dgnn_ctx_set_sample_mode", "dgnn_disk_index_partition_counts", "dgnn_pack_partition", "dgnn_pack_tails",
 ]
 
 
@@ -62,7 +62,7 @@ class _SamplesInfo(ctypes.Structure):
     _fields_ = [("num_batches", i64), ("num_hops", i32), ("batch_id_base", i64), ("total_nodes", i64),
                 ("total_edges", i64), ("total_eptr", i64), ("node_off", P), ("nodes", P), ("hop_off", P),
                 ("eptr_off", P), ("eptr", P), ("edge_off", P), ("src_local", P), ("node_off_host", P),
-                ("edge_off_host", P), ("eptr_off_host", P), ("hop_off_host", P)]
+                ("edge_off_host", P), ("eptr_off_host", P), ("hop_off_host", P), ("mode", i32)]
 
 
 class _PlanInfo(ctypes.Structure):
@@ -157,6 +157,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "dgnn_disk_cache_fill": (i32, [P, P, P, i64, P]),
             "dgnn_disk_partial": (i32, [P, P, i64, i64, P, P, P, P, P]),
             "dgnn_train_stub": (i32, [P, P, i64, i64, P, i64]),
+            "dgnn_ctx_set_sample_mode": (i32, [P, i32]),
             "dgnn_disk_index_partition_counts": (i32, [P, P, i64, i64, P]),
             "dgnn_pack_partition": (i32, [P, P, P, i64, i64, i64, P, P]),
             "dgnn_pack_tails": (i32, [P, P, i64, P, P]),
@@ -289,6 +290,10 @@ class Ctx:
     def set_sample_group(self, batches: int):
         _check(load_library().dgnn_ctx_set_sample_group(self.handle, int(batches)), "dgnn_ctx_set_sample_group")
 
+    def set_sample_mode(self, blocks: bool):
+        """False: node-wise (reading c4, default); True: the DGL-block variant (reading c27)."""
+        _check(load_library().dgnn_ctx_set_sample_mode(self.handle, int(bool(blocks))), "dgnn_ctx_set_sample_mode")
+
     @property
     def side_stream_ptr(self) -> int:
         return int(load_library().dgnn_ctx_side_stream(self.handle) or 0)
@@ -323,6 +328,7 @@ class Samples:
         self.edge_off_host = _host_array(info.edge_off_host, nb + 1, ctypes.c_int64)
         self.eptr_off_host = _host_array(info.eptr_off_host, nb + 1, ctypes.c_int64)
         self.hop_off_host = _host_array(info.hop_off_host, nb * (H + 2), ctypes.c_int32).reshape(nb, H + 2)
+        self.blocks = bool(info.mode)
 
     def batch(self, b: int) -> dict:
         """Device views of batch b: nodes, hop_off (host), eptr, src_local."""

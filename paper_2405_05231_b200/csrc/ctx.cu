@@ -181,6 +181,13 @@ dgnn_status dgnn_ctx_set_sample_group(dgnn_ctx* c, int32_t batches) {
     return DGNN_OK;
 }
 
+dgnn_status dgnn_ctx_set_sample_mode(dgnn_ctx* c, int32_t mode) {
+    DGNN_REQUIRE(c && (mode == DGNN_SAMPLE_NODEWISE || mode == DGNN_SAMPLE_BLOCKS),
+                 "dgnn_ctx_set_sample_mode: bad argument");
+    c->sample_mode = mode;
+    return DGNN_OK;
+}
+
 dgnn_status dgnn_ctx_set_assemble_occupancy(dgnn_ctx* c, int32_t blocks_per_sm) {
     DGNN_REQUIRE(c && blocks_per_sm >= 1 && blocks_per_sm <= 32, "dgnn_ctx_set_assemble_occupancy: bad argument");
     c->assemble_blocks_per_sm = blocks_per_sm;

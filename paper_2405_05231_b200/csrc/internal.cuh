@@ -26,6 +26,7 @@ struct dgnn_ctx {
     int* dev_err = nullptr;  // device word: OR of DEVERR_* bits
     int64_t launches = 0;
     int32_t sample_group = 0;
+    int32_t sample_mode = DGNN_SAMPLE_NODEWISE;
     int assemble_blocks_per_sm = 8;  // grid cap for a9 (lower it to leave SMs to a concurrent pass)
     // per-launch CUDA-event timing
     bool timing = false;
@@ -355,6 +356,7 @@ struct dgnn_samples {
     dgnn_ctx* ctx = nullptr;
     int64_t nb = 0;
     int32_t H = 0;
+    int32_t mode = DGNN_SAMPLE_NODEWISE;
     int64_t batch_id_base = 0;
     int64_t total_nodes = 0, total_edges = 0, total_eptr = 0;
     int64_t cap_nodes = 0, cap_edges = 0, cap_eptr = 0;

@@ -34,6 +34,7 @@ constexpr unsigned kFull = 0xffffffffu;
 
 struct Grp {
     int G;
+    int blocks;  // DGNN_SAMPLE_BLOCKS: every node so far is in the next frontier (reading c27)
     int tlog;
     uint32_t tmask;
     int H;
@@ -157,7 +158,7 @@ __global__ void k_hop_end(Grp g, int h) {
     for (int s = threadIdx.x; s < g.G; s += blockDim.x) {
         const int32_t n0 = g.n[s], c = (int32_t)(g.new_off[s + 1] - g.new_off[s]);
         g.hop_bound[s * (g.H + 2) + h + 2] = n0 + c;
-        g.fr_lo[s] = n0;
+        g.fr_lo[s] = g.blocks ? 0 : n0;
         g.fr_hi[s] = n0 + c;
         g.n[s] = n0 + c;
     }
@@ -411,6 +412,7 @@ struct CompactPlan {
     const int64_t* hop_cbase;    // [H*(kMaxGroup+1)]
     const int32_t* hop_bound;    // [G*(H+2)]
     int64_t* const* cptr;        // [H] device pointers
+    int blocks;
 };
 
 __global__ void k_compact_nodes(CompactPlan p, const int32_t* __restrict__ gnodes, int32_t* __restrict__ out) {
@@ -443,16 +445,31 @@ __global__ void k_compact_eptr(CompactPlan p, int32_t* __restrict__ out) {
     const int64_t T = s_pre[p.G];
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < T; q += (int64_t)gridDim.x * blockDim.x) {
         const int s = segment_of(s_pre, p.G + 1, q);
-        const int64_t j = q - s_pre[s];
+        int64_t j = q - s_pre[s];
         const int32_t* hb = p.hop_bound + s * (p.H + 2);
         int64_t val;
-        if (j == hb[p.H]) {
-            val = p.edge_pre[s + 1] - p.edge_pre[s];
+        if (!p.blocks) {
+            if (j == hb[p.H]) {
+                val = p.edge_pre[s + 1] - p.edge_pre[s];
+            } else {
+                int h = 0;
+                while (!(j < hb[h + 1])) ++h;  // frontier of hop h: local [hb[h], hb[h+1])
+                const int64_t t = p.hop_fr_off[h * (kMaxGroup + 1) + s] + (j - hb[h]);
+                val = p.cptr[h][t] - p.hop_cbase[h * (kMaxGroup + 1) + s] + p.edges_before[h * p.G + s];
+            }
         } else {
+            // blocks: hop h's array has hb[h+1] + 1 entries (its frontier is local [0, hb[h+1]))
             int h = 0;
-            while (!(j < hb[h + 1])) ++h;  // frontier of hop h: local [hb[h], hb[h+1])
-            const int64_t t = p.hop_fr_off[h * (kMaxGroup + 1) + s] + (j - hb[h]);
-            val = p.cptr[h][t] - p.hop_cbase[h * (kMaxGroup + 1) + s] + p.edges_before[h * p.G + s];
+            while (j > hb[h + 1]) {
+                j -= hb[h + 1] + 1;
+                ++h;
+            }
+            if (j == hb[h + 1]) {
+                val = h + 1 < p.H ? p.edges_before[(h + 1) * p.G + s] : p.edge_pre[s + 1] - p.edge_pre[s];
+            } else {
+                const int64_t t = p.hop_fr_off[h * (kMaxGroup + 1) + s] + j;
+                val = p.cptr[h][t] - p.hop_cbase[h * (kMaxGroup + 1) + s] + p.edges_before[h * p.G + s];
+            }
         }
         out[q] = (int32_t)val;
     }
@@ -532,6 +549,7 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
     S->nb = nb;
     S->H = H;
     S->batch_id_base = batch_id_base;
+    S->mode = c->sample_mode;
     struct Guard {
         dgnn_samples* s;
         ~Guard() { if (s) dgnn_samples_free(s); }
@@ -552,10 +570,11 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
         // ---- capacities (exact upper bounds; reading c26 for k = 0) ----
         const int64_t kCap = (int64_t)1 << 40;
         std::vector<int64_t> fr_bound(H), cand_bound(H), new_bound(H);
+        const bool blocks = c->sample_mode == DGNN_SAMPLE_BLOCKS;
         int64_t prod = B, nodes_bound = B;
         for (int h = 0; h < H; ++h) {
-            fr_bound[h] = prod;
-            prod = sat_mul(prod, fanout[h], kCap);
+            fr_bound[h] = blocks ? nodes_bound : prod;  // blocks: every node so far expands
+            prod = sat_mul(fr_bound[h], fanout[h], kCap);
             new_bound[h] = prod;
             nodes_bound = std::min(kCap, nodes_bound + prod);
         }
@@ -623,6 +642,7 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
             DGNN_CK(cudaStreamSynchronize(c->stream));  // ptrs is a stack vector
         }
         Grp g{};
+        g.blocks = blocks ? 1 : 0;
         g.tlog = tlog;
         g.tmask = (uint32_t)((1ull << tlog) - 1);
         g.H = H;
@@ -753,11 +773,16 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
                 }
                 node_pre[s + 1] = node_pre[s] + h_n[s];
                 edge_pre[s + 1] = edge_pre[s] + e;
-                eptr_pre[s + 1] = eptr_pre[s] + h_hb[s * (H + 2) + H] + 1;
+                int64_t ne = h_hb[s * (H + 2) + H] + 1;
+                if (blocks) {
+                    ne = 0;
+                    for (int h = 0; h < H; ++h) ne += h_hb[s * (H + 2) + h + 1] + 1;
+                }
+                eptr_pre[s + 1] = eptr_pre[s] + ne;
                 const int64_t b = t0 + s;
                 S->node_off_h[b + 1] = S->node_off_h[b] + h_n[s];
                 S->edge_off_h[b + 1] = S->edge_off_h[b] + e;
-                S->eptr_off_h[b + 1] = S->eptr_off_h[b] + h_hb[s * (H + 2) + H] + 1;
+                S->eptr_off_h[b + 1] = S->eptr_off_h[b] + ne;
                 for (int x = 0; x < H + 2; ++x) S->hop_off_h[b * (H + 2) + x] = h_hb[s * (H + 2) + x];
             }
             // grow the arena (estimate the whole run from the groups seen so far)
@@ -786,6 +811,7 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
             p.hop_cbase = g.hop_cbase;
             p.hop_bound = g.hop_bound;
             p.cptr = d_cptr_list.p;
+            p.blocks = g.blocks;
             launch(c, DGNN_K_SAMPLE_COMPACT, 8.0 * node_pre[Gc], [&] {
                 k_compact_nodes<<<grid_for(c, node_pre[Gc], 256), 256, 0, c->stream>>>(p, g.nodes,
                                                                                         a_nodes.p + used_nodes);
@@ -861,6 +887,7 @@ extern "C" dgnn_status dgnn_samples_get_info(const dgnn_samples* s, dgnn_samples
     i->edge_off_host = s->edge_off_h.data();
     i->eptr_off_host = s->eptr_off_h.data();
     i->hop_off_host = s->hop_off_h.data();
+    i->mode = s->mode;
     return DGNN_OK;
 }
 

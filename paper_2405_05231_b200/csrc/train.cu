@@ -26,7 +26,21 @@ struct RunView {
     const int32_t* src_local;
     int H;
     int b_lo, nbr;
+    int blocks;  // DGNN_SAMPLE_BLOCKS: hop h's destinations are local [0, hop_off[h+1]), eptr per hop
 };
+
+// first destination of hop h and the start of hop h's eptr array (relative to the batch's eptr)
+__device__ __forceinline__ void hop_geometry(const RunView& v, const int32_t* ho, int h, int64_t& first,
+                                             int64_t& eptr_base) {
+    if (!v.blocks) {
+        first = ho[h];
+        eptr_base = 0;
+        return;
+    }
+    first = 0;
+    eptr_base = 0;
+    for (int i = 0; i < h; ++i) eptr_base += ho[i + 1] + 1;
+}
 
 // fr_off[bl] = exclusive prefix over the run's batches of |hop h| (single block)
 __global__ void k_frontier_off(RunView v, int h, int64_t* __restrict__ fr_off) {
@@ -40,7 +54,7 @@ __global__ void k_frontier_off(RunView v, int h, int64_t* __restrict__ fr_off) {
         int64_t x = 0;
         if (bl < v.nbr) {
             const int32_t* ho = v.hop_off + (int64_t)(v.b_lo + bl) * (v.H + 2);
-            x = ho[h + 1] - ho[h];
+            x = v.blocks ? ho[h + 1] : ho[h + 1] - ho[h];
         }
         int64_t s = x;
 #pragma unroll
@@ -104,8 +118,10 @@ __global__ void __launch_bounds__(256) k_layer(RunView v, int h, const int64_t* 
         const int bl = segment_of(fr_off, v.nbr + 1, f);
         const int b = v.b_lo + bl;
         const int32_t* ho = v.hop_off + (int64_t)b * (v.H + 2);
-        const int64_t j = ho[h] + (f - fr_off[bl]);
-        const int32_t* ep = v.eptr + v.eptr_off[b];
+        int64_t first, ebase;
+        hop_geometry(v, ho, h, first, ebase);
+        const int64_t j = first + (f - fr_off[bl]);
+        const int32_t* ep = v.eptr + v.eptr_off[b] + ebase;
         const int32_t e0 = ep[j], e1 = ep[j + 1];
         const int64_t rb = v.node_off[b] - x0;  // the batch's first row in x
         const V* self = reinterpret_cast<const V*>(x + (rb + j) * dim);
@@ -164,7 +180,7 @@ __global__ void __launch_bounds__(256) k_copyback(RunView v, int h, const int64_
     for (int64_t f = warp; f < F; f += nwarps) {
         const int bl = segment_of(fr_off, v.nbr + 1, f);
         const int b = v.b_lo + bl;
-        const int64_t j = v.hop_off[(int64_t)b * (v.H + 2) + h] + (f - fr_off[bl]);
+        const int64_t j = (v.blocks ? 0 : v.hop_off[(int64_t)b * (v.H + 2) + h]) + (f - fr_off[bl]);
         V* d = reinterpret_cast<V*>(x + (v.node_off[b] - x0 + j) * dim);
         const V* s = reinterpret_cast<const V*>(scratch + f * dim);
         for (int64_t q = lane; q < nvec; q += 32) d[q] = s[q];
@@ -189,7 +205,8 @@ extern "C" dgnn_status dgnn_train_stub(dgnn_ctx* c, const dgnn_samples* s, int64
     std::vector<int64_t> F(H, 0);
     for (int h = 0; h < H; ++h) {
         for (int64_t b = b_lo; b < b_hi; ++b)
-            F[h] += s->hop_off_h[b * (H + 2) + h + 1] - s->hop_off_h[b * (H + 2) + h];
+            F[h] += s->hop_off_h[b * (H + 2) + h + 1] -
+                    (s->mode == DGNN_SAMPLE_BLOCKS ? 0 : s->hop_off_h[b * (H + 2) + h]);
         F_max = std::max(F_max, F[h]);
     }
     if (F_max == 0) return DGNN_OK;
@@ -197,7 +214,8 @@ extern "C" dgnn_status dgnn_train_stub(dgnn_ctx* c, const dgnn_samples* s, int64
     DevBuf<int64_t> fr;
     DGNN_TRY(scratch.alloc(c, (size_t)(F_max * dim)));
     DGNN_TRY(fr.alloc(c, (size_t)nbr + 1));
-    RunView v{s->node_off, s->hop_off, s->eptr_off, s->eptr, s->edge_off, s->src_local, H, (int)b_lo, nbr};
+    RunView v{s->node_off, s->hop_off, s->eptr_off, s->eptr, s->edge_off, s->src_local, H, (int)b_lo, nbr,
+              s->mode == DGNN_SAMPLE_BLOCKS ? 1 : 0};
     const bool v4 = dim % 4 == 0 && ((uintptr_t)x & 15) == 0;
     for (int h = H - 1; h >= 0; --h) {
         if (F[h] == 0) continue;
