@@ -317,15 +317,17 @@ class Runner:
         return out
 
 
-def cpu_baseline(cfg, inp_host, n_batches: int):
-    """The oracle as it stands, on a bounded sample: the first n_batches batches of rank 0's epoch."""
+def cpu_baseline(cfg, inp_host, n_batches: int, blocks: bool = False, train: bool = False):
+    """The oracle as it stands, on a bounded sample: the first n_batches batches of rank 0's epoch
+    (with the same sampling variant and, if the GPU arm trains, the trainer stub)."""
     import oracle
     indptr, indices, seeds, feats_u8 = inp_host
     B = cfg["batch_size"]
     threads = os.cpu_count() or 1
     gpu_rows, host_rows = int(cfg["gpu_frac"] * cfg["num_nodes"]), int(cfg["host_frac"] * cfg["num_nodes"])
     t0 = time.time()
-    S = oracle.sample(indptr, indices, seeds[: n_batches * B], B, list(cfg["fanout"]), RNG_SEED, threads=threads)
+    S = oracle.sample(indptr, indices, seeds[: n_batches * B], B, list(cfg["fanout"]), RNG_SEED, threads=threads,
+                      blocks=blocks)
     counts = oracle.count_frequencies(S, len(indptr) - 1)
     tm, gpu_ids, host_ids = oracle.select_tiers(counts, gpu_rows, host_rows)
     plists = []
@@ -335,12 +337,14 @@ def cpu_baseline(cfg, inp_host, n_batches: int):
     oracle.gather_rows(feats_u8, gpu_ids)
     oracle.gather_rows(feats_u8, host_ids)
     for s in S:
-        oracle.assemble(feats_u8, s.nodes)
+        rows = oracle.assemble(feats_u8, s.nodes)
+        if train:
+            oracle.train_stub(s, rows.view(np.float32))
     dt = time.time() - t0
     return {"value": len(S) / dt, "unit": "mini-batches/s", "cores": threads, "kind": "oracle",
             "sample": f"first {len(S)} batches of the {cfg['batch_size']}-seed epoch: sample (OpenMP over batches), "
                       f"count, full-N tier select on their counts, classify, pack, tier gather, direct-gather "
-                      f"assembly; {dt:.1f}s"}
+                      f"assembly{' + trainer stub' if train else ''}{' (DGL blocks)' if blocks else ''}; {dt:.1f}s"}
 
 
 def main():
@@ -358,6 +362,8 @@ def main():
                     help="no epoch pipelining: the layout of pass e+1 starts after the assembly of pass e")
     ap.add_argument("--host-window", type=int, default=128,
                     help="batches per host-row merging window in a9 (1 = per-batch UVA reads, the paper's)")
+    ap.add_argument("--blocks", action="store_true",
+                    help="DGL-block sampling variant (reading c27): every node so far resamples at each hop")
     ap.add_argument("--train", action="store_true",
                     help="include the trainer stub (dgnn_train_stub, its own stream, depth-2 queue) in every pass")
     ap.add_argument("--disk-budget", type=float, default=None,
@@ -377,6 +383,8 @@ def main():
     R.host_window = args.host_window
     R.disk_budget_frac = args.disk_budget
     R.train = args.train
+    if args.blocks:
+        R.ctxA.set_sample_mode(True)
     t = time.time()
     L = R.run(1, keep_last=True)
     torch.cuda.synchronize()
@@ -452,7 +460,8 @@ def main():
                    "host_window_batches": args.host_window,
                    "schedule": ("sequential" if args.sequential else
                                 "pipelined: layout of pass e+1 overlaps assembly of pass e (2 streams)")
-                               + ("; trainer stub per run on its own stream (depth-2 queue)" if args.train else ""),
+                               + ("; trainer stub per run on its own stream (depth-2 queue)" if args.train else "")
+                               + ("; DGL-block sampling (every node so far resamples)" if args.blocks else ""),
                    "l2": "inputs larger than L2 (features %.1f GB, CSR %.1f GB); no flush needed" % (
                        feats.numel() * 4 / 1e9, (indptr.numel() * 8 + indices.numel() * 4) / 1e9)},
         "packed_gbs": round(stats0["packed_bytes"] * ws * args.steps / (ms_max / 1e3) / 1e9, 2),
@@ -541,7 +550,7 @@ def main():
         try:
             result["cpu_baseline"] = cpu_baseline(cfg, (h_indptr.numpy(), h_indices.numpy(), h_seeds.numpy(),
                                                         h_feats.numpy().view(np.uint8).reshape(N, -1)),
-                                                  min(args.cpu_batches, nb))
+                                                  min(args.cpu_batches, nb), blocks=args.blocks, train=args.train)
         except Exception as ex:  # the baseline is reported, never required
             result["cpu_baseline"] = {"value": None, "error": str(ex)[:200]}
     if rank == 0:
@@ -565,11 +574,11 @@ def reference_arm(args, ws, rank, dev):
     torch.cuda.empty_cache()
     per_step = max(1, min(8, (seeds.numel() + cfg["batch_size"] - 1) // cfg["batch_size"]))
     for _ in range(args.warmup):
-        cpu_baseline(cfg, h, per_step)
+        cpu_baseline(cfg, h, per_step, args.blocks, args.train)
     t0 = time.time()
     last = None
     for _ in range(args.steps):
-        last = cpu_baseline(cfg, h, per_step)
+        last = cpu_baseline(cfg, h, per_step, args.blocks, args.train)
     dt = time.time() - t0
     value = per_step * args.steps / dt
     nb = (seeds.numel() + cfg["batch_size"] - 1) // cfg["batch_size"]
