@@ -361,6 +361,31 @@ dgnn_status dgnn_assemble_group_sharded(dgnn_ctx* ctx, const uint32_t* addr, con
                                         const int32_t* host_map, const void* chunk_base, const int64_t* chunk_off,
                                         const int64_t* chunk_rows, int64_t row_bytes, void* out);
 
+/* ---- one-sided peer-memory GPU tier (the sharded tier without the
+ * all-to-all).  Every rank's shard is a dgnn_device_alloc allocation exported with
+ * dgnn_ipc_handle and mapped by the other ranks with dgnn_ipc_open (CUDA IPC; over NVLink /
+ * NVSwitch the mapped loads are peer loads), so the assembly kernel reads a remote GPU-tier row
+ * directly from its owner: the exchange of dgnn_shard_requests / all-to-all / dgnn_scatter_rows
+ * collapses into the gather itself.  Shards must be complete (filled + a barrier across ranks)
+ * before any rank assembles.
+ * dgnn_assemble_group_peer: dgnn_assemble_group with GPU-tier slot s read from
+ *   peers[s % world] + (s / world) * row_bytes; peers = device array [world] of shard bases
+ *   (this rank's own shard included); row_bytes % 16 == 0.
+ * dgnn_device_alloc / _free: plain cudaMalloc (an IPC handle names the allocation base).
+ * dgnn_ipc_handle: handle (DGNN_IPC_HANDLE_BYTES bytes, host) of a dgnn_device_alloc pointer.
+ * dgnn_ipc_open / _close: map / unmap another process's allocation on `device`. */
+#define DGNN_IPC_HANDLE_BYTES 64
+dgnn_status dgnn_assemble_group_peer(dgnn_ctx* ctx, const uint32_t* addr, const int64_t* node_off, int64_t nb,
+                                     int64_t n, const void* const* peers, int64_t k_gpu, int32_t world,
+                                     const void* host_tier, int64_t k_host, const int32_t* host_map,
+                                     const void* chunk_base, const int64_t* chunk_off, const int64_t* chunk_rows,
+                                     int64_t row_bytes, void* out);
+dgnn_status dgnn_device_alloc(int32_t device, int64_t bytes, void** out);
+dgnn_status dgnn_device_free(void* p);
+dgnn_status dgnn_ipc_handle(const void* dev_ptr, void* handle);
+dgnn_status dgnn_ipc_open(int32_t device, const void* handle, void** dev_ptr);
+dgnn_status dgnn_ipc_close(void* dev_ptr);
+
 /* dgnn_gather_rows with the row count read from device memory (*n_dev <= n_max). */
 dgnn_status dgnn_gather_rows_dev(dgnn_ctx* ctx, const void* features, int64_t num_rows, int64_t row_bytes,
                                  const int32_t* ids, const int64_t* n_dev, int64_t n_max, void* out);

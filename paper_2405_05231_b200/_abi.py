@@ -43,7 +43,8 @@ EXPORTS = [
     "dgnn_file_open", "dgnn_file_close", "dgnn_stage_file_write", "dgnn_stage_file_read",
     "dgnn_disk_index_build", "dgnn_disk_index_free", "dgnn_disk_space", "dgnn_disk_search", "dgnn_disk_plan_build",
     "dgnn_disk_plan_get_info", "dgnn_disk_plan_free", "dgnn_disk_cache_fill", "dgnn_disk_partial",
-    "dgnn_train_stub", "dgnn_ctx_set_sample_mode", "dgnn_disk_index_partition_counts", "dgnn_pack_partition", "dgnn_pack_tails",
+    "dgnn_train_stub", "dgnn_ctx_set_sample_mode", "dgnn_assemble_group_peer", "dgnn_device_alloc",
+    "dgnn_device_free", "dgnn_ipc_handle", "dgnn_ipc_open", "dgnn_ipc_close", "dgnn_disk_index_partition_counts", "dgnn_pack_partition", "dgnn_pack_tails",
 ]
 
 
@@ -158,6 +159,12 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "dgnn_disk_partial": (i32, [P, P, i64, i64, P, P, P, P, P]),
             "dgnn_train_stub": (i32, [P, P, i64, i64, P, i64]),
             "dgnn_ctx_set_sample_mode": (i32, [P, i32]),
+            "dgnn_assemble_group_peer": (i32, [P, P, P, i64, i64, P, i64, i32, P, i64, P, P, P, P, i64, P]),
+            "dgnn_device_alloc": (i32, [i32, i64, ctypes.POINTER(P)]),
+            "dgnn_device_free": (i32, [P]),
+            "dgnn_ipc_handle": (i32, [P, P]),
+            "dgnn_ipc_open": (i32, [i32, P, ctypes.POINTER(P)]),
+            "dgnn_ipc_close": (i32, [P]),
             "dgnn_disk_index_partition_counts": (i32, [P, P, i64, i64, P]),
             "dgnn_pack_partition": (i32, [P, P, P, i64, i64, i64, P, P]),
             "dgnn_pack_tails": (i32, [P, P, i64, P, P]),
@@ -669,3 +676,52 @@ def dgnn_pack_partition(ctx: Ctx, idx: DiskIndex, part, p0: int, p1: int, row_by
 def dgnn_pack_tails(ctx: Ctx, idx: DiskIndex, row_bytes: int, chunk_off: torch.Tensor, group_buf):
     _check(load_library().dgnn_pack_tails(ctx.handle, idx.handle, int(row_bytes), _ptr(chunk_off), _ptr(group_buf)),
            "dgnn_pack_tails")
+
+
+# ------------------------------------------------ one-sided peer-memory tier ----
+IPC_HANDLE_BYTES = 64
+
+
+def dgnn_assemble_group_peer(ctx: Ctx, addr: torch.Tensor, node_off: torch.Tensor, n: int, peers: torch.Tensor,
+                             k_gpu: int, world: int, host_tier, k_host: int, chunk_base, chunk_off: torch.Tensor,
+                             chunk_rows: torch.Tensor, row_bytes: int, out, host_map=None):
+    """peers: device int64 [world] of shard base addresses (dgnn_device_alloc / dgnn_ipc_open)."""
+    _check(load_library().dgnn_assemble_group_peer(
+        ctx.handle, _ptr(addr), _ptr(node_off), node_off.numel() - 1, int(n), _ptr(peers), int(k_gpu), int(world),
+        _ptr(host_tier), int(k_host), _ptr(host_map), _ptr(chunk_base), _ptr(chunk_off), _ptr(chunk_rows),
+        int(row_bytes), _ptr(out)), "dgnn_assemble_group_peer")
+
+
+class DeviceBuffer:
+    """A plain cudaMalloc allocation (dgnn_device_alloc) that CUDA IPC can export."""
+
+    def __init__(self, device: int, nbytes: int):
+        L = load_library()
+        p = P()
+        _check(L.dgnn_device_alloc(int(device), int(nbytes), ctypes.byref(p)), "dgnn_device_alloc")
+        self.ptr, self.nbytes, self.device = int(p.value or 0), int(nbytes), int(device)
+        self._fin = weakref.finalize(self, L.dgnn_device_free, P(self.ptr))
+
+    def ipc_handle(self) -> bytes:
+        buf = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
+        _check(load_library().dgnn_ipc_handle(P(self.ptr), buf), "dgnn_ipc_handle")
+        return buf.raw
+
+    def view(self, shape, dtype=torch.uint8) -> torch.Tensor:
+        n = 1
+        for d in shape:
+            n *= int(d)
+        return _view(self.ptr, n * torch.empty(0, dtype=dtype).element_size(), torch.uint8, self,
+                     torch.device("cuda", self.device)).view(dtype).view(*shape)
+
+
+class IpcMapping:
+    """Another process's DeviceBuffer mapped into this one (dgnn_ipc_open)."""
+
+    def __init__(self, device: int, handle: bytes):
+        L = load_library()
+        p = P()
+        _check(L.dgnn_ipc_open(int(device), ctypes.create_string_buffer(bytes(handle), IPC_HANDLE_BYTES),
+                               ctypes.byref(p)), "dgnn_ipc_open")
+        self.ptr = int(p.value or 0)
+        self._fin = weakref.finalize(self, L.dgnn_ipc_close, P(self.ptr))

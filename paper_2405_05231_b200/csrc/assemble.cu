@@ -74,13 +74,16 @@ struct AsmGroupRow {
     int* err;
     int gpu_world;             // > 1: the GPU tier is sharded, slot s lives on rank s % world at s / world
     int gpu_rank;
+    const uint8_t* const* peers;  // non-NULL: every shard's base (peer memory), read one-sided
     __device__ __forceinline__ bool operator()(int64_t j, const uint8_t*& s, uint8_t*& d) const {
         const uint32_t a = addr[j];
         const uint32_t tier = a >> DGNN_TIER_SHIFT;
         const int64_t slot = a & DGNN_SLOT_MASK;
         d = out + j * row_bytes;
         if (tier == DGNN_TIER_GPU && slot < kg) {
-            if (gpu_world > 1) {
+            if (peers) {  // one-sided: the owner's shard is mapped into this GPU's address space
+                s = peers[slot % gpu_world] + (slot / gpu_world) * row_bytes;
+            } else if (gpu_world > 1) {
                 if (slot % gpu_world != gpu_rank) {  // remote row: delivered by dgnn_scatter_rows
                     d = nullptr;
                     s = nullptr;
@@ -393,12 +396,75 @@ extern "C" dgnn_status dgnn_assemble_group_sharded(dgnn_ctx* c, const uint32_t* 
     const bool v16 = row_bytes % 16 == 0 && al16(gpu_tier) && al16(host_tier) && al16(chunk_base) && al16(out);
     AsmGroupRow fn{addr,     node_off, chunk_off, chunk_rows, (int)nb,   (const uint8_t*)gpu_tier, k_gpu,
                    (const uint8_t*)host_tier, k_host, host_map, (const uint8_t*)chunk_base, row_bytes,
-                   (uint8_t*)out, c->dev_err, gpu_world, gpu_rank};
+                   (uint8_t*)out, c->dev_err, gpu_world, gpu_rank, nullptr};
     const int grid = grid_for(c, n * 32 / kAsmU, 256, c->assemble_blocks_per_sm);
     launch(c, DGNN_K_ASSEMBLE, (double)n * (2.0 * row_bytes + 4.0), [&] {
         if (v16) k_assemble_group<uint4><<<grid, 256, 0, c->stream>>>(fn, n);
         else k_assemble_group<uint32_t><<<grid, 256, 0, c->stream>>>(fn, n);
     });
     DGNN_CK_LAUNCH();
+    return DGNN_OK;
+}
+
+// --------------------------------------------- one-sided peer-memory tier (NEXT #3)
+extern "C" dgnn_status dgnn_assemble_group_peer(dgnn_ctx* c, const uint32_t* addr, const int64_t* node_off, int64_t nb,
+                                                int64_t n, const void* const* peers, int64_t k_gpu, int32_t world,
+                                                const void* host_tier, int64_t k_host, const int32_t* host_map,
+                                                const void* chunk_base, const int64_t* chunk_off,
+                                                const int64_t* chunk_rows, int64_t row_bytes, void* out) {
+    DGNN_REQUIRE(world >= 1 && (k_gpu == 0 || peers), "dgnn_assemble_group_peer: bad shard table");
+    DGNN_REQUIRE(c && (n == 0 || (addr && out && node_off && chunk_off && chunk_rows)),
+                 "dgnn_assemble_group_peer: NULL argument");
+    DGNN_REQUIRE(row_bytes > 0 && row_bytes % 16 == 0 && n >= 0 && nb >= 0 && nb < (1 << 30) && k_gpu >= 0 &&
+                     k_host >= 0, "dgnn_assemble_group_peer: bad sizes (row_bytes must be a multiple of 16)");
+    DGNN_REQUIRE(k_host == 0 || host_tier, "dgnn_assemble_group_peer: NULL host tier");
+    if (n == 0 || nb == 0) return DGNN_OK;
+    DGNN_CK(cudaSetDevice(c->device));
+    const bool v16 = al16(host_tier) && al16(chunk_base) && al16(out);
+    AsmGroupRow fn{addr,     node_off, chunk_off, chunk_rows, (int)nb,   nullptr, k_gpu,
+                   (const uint8_t*)host_tier, k_host, host_map, (const uint8_t*)chunk_base, row_bytes,
+                   (uint8_t*)out, c->dev_err, world, 0, (const uint8_t* const*)peers};
+    const int grid = grid_for(c, n * 32 / kAsmU, 256, c->assemble_blocks_per_sm);
+    launch(c, DGNN_K_ASSEMBLE, (double)n * (2.0 * row_bytes + 4.0), [&] {
+        if (v16) k_assemble_group<uint4><<<grid, 256, 0, c->stream>>>(fn, n);
+        else k_assemble_group<uint32_t><<<grid, 256, 0, c->stream>>>(fn, n);
+    });
+    DGNN_CK_LAUNCH();
+    return DGNN_OK;
+}
+
+extern "C" dgnn_status dgnn_device_alloc(int32_t device, int64_t bytes, void** out) {
+    DGNN_REQUIRE(out && bytes >= 0, "dgnn_device_alloc: bad argument");
+    *out = nullptr;
+    DGNN_CK(cudaSetDevice(device));
+    DGNN_CK(cudaMalloc(out, (size_t)(bytes > 0 ? bytes : 16)));
+    return DGNN_OK;
+}
+
+extern "C" dgnn_status dgnn_device_free(void* p) {
+    if (p) DGNN_CK(cudaFree(p));
+    return DGNN_OK;
+}
+
+extern "C" dgnn_status dgnn_ipc_handle(const void* dev_ptr, void* handle) {
+    DGNN_REQUIRE(dev_ptr && handle, "dgnn_ipc_handle: NULL argument");
+    cudaIpcMemHandle_t h;
+    DGNN_CK(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
+    static_assert(sizeof(h) == DGNN_IPC_HANDLE_BYTES, "IPC handle size");
+    memcpy(handle, &h, sizeof(h));
+    return DGNN_OK;
+}
+
+extern "C" dgnn_status dgnn_ipc_open(int32_t device, const void* handle, void** dev_ptr) {
+    DGNN_REQUIRE(handle && dev_ptr, "dgnn_ipc_open: NULL argument");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    DGNN_CK(cudaSetDevice(device));
+    DGNN_CK(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return DGNN_OK;
+}
+
+extern "C" dgnn_status dgnn_ipc_close(void* dev_ptr) {
+    if (dev_ptr) DGNN_CK(cudaIpcCloseMemHandle(dev_ptr));
     return DGNN_OK;
 }

@@ -241,7 +241,7 @@ class Layout:
 
     def assemble_epoch(self, ctx: A.Ctx | None = None, out_budget: int = 1 << 30, host_window: int = 128,
                        gather_ctx: A.Ctx | None = None, sharded_tier=None, remote=None, runs: bool = False,
-                       ring_wait: dict | None = None, ws: Workspace | None = None):
+                       ring_wait: dict | None = None, ws: Workspace | None = None, peer_tier=None):
         """Pipelined assembly: the chunks of the next run of batches are staged H2D
         on the side stream while the current run is assembled on the ctx stream (one
         dgnn_assemble_group launch per run).  Yields (b, features[n_b, dim]) per batch; a
@@ -264,7 +264,10 @@ class Layout:
         consumer on another stream, e.g. the trainer: a queue of depth 2).
 
         ``ws``: a Workspace for the rings and staging buffers, reused by every epoch assembled
-        on the same stream (keeps tens of GB out of the caching allocator's churn)."""
+        on the same stream (keeps tens of GB out of the caching allocator's churn).
+
+        ``peer_tier`` (a shard.PeerTier): the GPU tier sharded over ranks and read one-sided
+        through peer memory (dgnn_assemble_group_peer), no exchange round."""
         ctx = ctx or self.ctx
         gctx = gather_ctx or ctx
         nb = self.num_batches
@@ -385,7 +388,11 @@ class Layout:
                 host_src, host_map = staging[cur], smap[cur]
             else:
                 host_src, host_map = self.host_tier.ptr, None
-            if sharded_tier is None:
+            if peer_tier is not None:
+                A.dgnn_assemble_group_peer(ctx, self.addr[n0:n1], t[:k + 1], n1 - n0, peer_tier.peers,
+                                           self.plan.k_gpu, peer_tier.world, host_src, kh, chunk, t[k + 1:2 * k + 2],
+                                           t[2 * k + 2:3 * k + 3], self.row_bytes, out, host_map=host_map)
+            elif sharded_tier is None:
                 A.dgnn_assemble_group(ctx, self.addr[n0:n1], t[:k + 1], n1 - n0, self.gpu_tier, self.plan.k_gpu,
                                       host_src, kh, chunk, t[k + 1:2 * k + 2], t[2 * k + 2:3 * k + 3], self.row_bytes,
                                       out, host_map=host_map)

@@ -98,3 +98,64 @@ def fetch_remote_rows_loopback(ctx: A.Ctx, tiers: list, rank: int, addr: torch.T
             rows = torch.empty((n, t.row_bytes), dtype=torch.uint8, device=ctx.device)
         A.dgnn_gather_rows(ctx, tiers[o].rows, req_slot[int(off[o]):int(off[o + 1])], rows)
         A.dgnn_scatter_rows(ctx, rows, n, t.row_bytes, req_pos[int(off[o]):int(off[o + 1])], out)
+
+
+class PeerTier:
+    """The sharded GPU tier read one-sided through peer memory.
+
+    Each rank fills its shard (slot s on rank s % world at row s // world) in a plain device
+    allocation, exports its CUDA IPC handle, and maps every other rank's shard; the assembly
+    kernel (dgnn_assemble_group_peer) then loads a remote GPU-tier row straight from its
+    owner's HBM over NVLink / NVSwitch.  The request / all-to-all / scatter round of
+    ``exchange_remote_rows`` disappears into the gather: one kernel, no collective on the
+    data path after the one-time handle exchange.
+
+    ``exchange(handle_bytes) -> [handle of rank 0, ..., rank world-1]`` is the process
+    group's all-gather of the 64-byte handles (``all_gather_handles``).
+    """
+
+    def __init__(self, ctx: A.Ctx, features: torch.Tensor, plan: A.CachePlan, rank: int, world: int, exchange):
+        self.ctx, self.rank, self.world, self.k_gpu = ctx, rank, world, plan.k_gpu
+        self.row_bytes = features.element_size() * (features.numel() // max(features.shape[0], 1))
+        dev = ctx.device.index if ctx.device.index is not None else 0
+        self.shard = _fill_shard(ctx, features, plan, rank, world, self.row_bytes)
+        ctx.sync()  # the shard is complete before anyone maps it
+        handles = exchange(self.shard.ipc_handle())
+        self.maps, ptrs = [], []
+        for r, h in enumerate(handles):
+            if r == rank:
+                ptrs.append(self.shard.ptr)
+            else:
+                m = A.IpcMapping(dev, h)
+                self.maps.append(m)
+                ptrs.append(m.ptr)
+        self.peers = torch.tensor(ptrs, dtype=torch.int64, device=ctx.device)
+
+    @classmethod
+    def loopback(cls, ctx: A.Ctx, features: torch.Tensor, plan: A.CachePlan, world: int):
+        """All world shards in this process (the single-GPU test of the kernel path)."""
+        self = cls.__new__(cls)
+        self.ctx, self.rank, self.world, self.k_gpu = ctx, 0, world, plan.k_gpu
+        self.row_bytes = features.element_size() * (features.numel() // max(features.shape[0], 1))
+        self.shards = [_fill_shard(ctx, features, plan, r, world, self.row_bytes) for r in range(world)]
+        self.maps = []
+        self.peers = torch.tensor([s.ptr for s in self.shards], dtype=torch.int64, device=ctx.device)
+        ctx.sync()
+        return self
+
+
+def _fill_shard(ctx, features, plan, rank, world, row_bytes):
+    ids = A.dgnn_tier_shard_ids(ctx, plan.gpu_ids, plan.k_gpu, rank, world)
+    dev = ctx.device.index if ctx.device.index is not None else 0
+    buf = A.DeviceBuffer(dev, max(ids.numel(), 1) * row_bytes)
+    if ids.numel():
+        A.dgnn_gather_rows(ctx, features, ids, buf.view((ids.numel(), row_bytes)))
+    return buf
+
+
+def all_gather_handles(handle: bytes, group=None) -> list:
+    """The process group's all-gather of this rank's 64-byte IPC handle (any backend)."""
+    import torch.distributed as dist
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, handle, group=group)
+    return out
