@@ -212,6 +212,7 @@ class Runner:
         w0 = Workspace()
         self.ws = [w0, Workspace() if pipelined else w0]
         self.asm_ws = Workspace()  # assembly rings / staging: every pass assembles on stream B
+        self.scratch_ws = Workspace()  # packed lists + pack group buffers: passes pack one after another on A
         self.counts = [torch.zeros(N, dtype=torch.int32, device=dev) for _ in range(2)]
         cfg = inp[0]
         self.nb = (inp[3].numel() + cfg["batch_size"] - 1) // cfg["batch_size"]
@@ -242,7 +243,8 @@ class Runner:
                                       gpu_rows, host_rows, RNG_SEED, group_size=cfg["group_size"],
                                       batch_id_base=self.rank * self.nb, counts=c, ws=self.ws[slot],
                                       stage_piece=int(os.environ.get("DGNN_STAGE_PIECE", str(1 << 40))),
-                                      disk_budget_frac=self.disk_budget_frac, after_sample=after_sample)
+                                      disk_budget_frac=self.disk_budget_frac, after_sample=after_sample,
+                                      scratch_ws=self.scratch_ws)
 
     def _assemble(self, L, ev_l):
         """Enqueue the assembly (and trainer) of pass L on stream B after its layout; -> end event."""

@@ -70,12 +70,29 @@ dgnn_status memset_async(dgnn_ctx* c, void* p, int value, size_t bytes) {
     return DGNN_OK;
 }
 
+void* pinned_scratch(dgnn_ctx* c, size_t bytes) {
+    if (bytes > c->pinned_bytes) {
+        if (c->pinned) cudaFreeHost(c->pinned);
+        c->pinned = nullptr;
+        c->pinned_bytes = 0;
+        const size_t n = bytes + bytes / 2 + 4096;
+        if (cudaHostAlloc(&c->pinned, n, cudaHostAllocDefault) != cudaSuccess) {
+            cudaGetLastError();
+            c->pinned = nullptr;
+            return nullptr;
+        }
+        c->pinned_bytes = n;
+    }
+    return c->pinned;
+}
+
 extern std::atomic<int> g_io_error;
 
 dgnn_status check_dev_err(dgnn_ctx* c) {
-    int h = 0;
-    DGNN_CK(cudaMemcpyAsync(&h, c->dev_err, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    if (!c->pinned_err) DGNN_CK(cudaHostAlloc((void**)&c->pinned_err, sizeof(int), cudaHostAllocDefault));
+    DGNN_CK(cudaMemcpyAsync(c->pinned_err, c->dev_err, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     DGNN_CK(cudaStreamSynchronize(c->stream));
+    const int h = *c->pinned_err;
     if (g_io_error.exchange(0)) {
         set_error("file staging: a pread/pwrite failed or hit end of file");
         return DGNN_EIO;
@@ -149,6 +166,8 @@ void dgnn_ctx_destroy(dgnn_ctx* c) {
         if (c->stage_ev[i]) cudaEventDestroy(c->stage_ev[i]);
     if (c->order_ev) cudaEventDestroy(c->order_ev);
     if (c->dev_err) cudaFree(c->dev_err);
+    if (c->pinned) cudaFreeHost(c->pinned);
+    if (c->pinned_err) cudaFreeHost(c->pinned_err);
     if (c->side) cudaStreamDestroy(c->side);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;

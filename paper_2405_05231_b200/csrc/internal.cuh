@@ -45,6 +45,11 @@ struct dgnn_ctx {
     cudaEvent_t stage_ev[kStageRing] = {};
     int64_t stage_next = 0;
     cudaEvent_t order_ev = nullptr;
+    // pinned host scratch for the small size read-backs / uploads (grow-only): pageable
+    // copies would stage through the driver and serialize with other streams' copies
+    void* pinned = nullptr;
+    size_t pinned_bytes = 0;
+    int* pinned_err = nullptr;  // check_dev_err's read-back word
 };
 
 namespace dgnn {
@@ -146,6 +151,7 @@ inline void launch(dgnn_ctx* c, int kid, double bytes, F&& f) {
 }
 
 dgnn_status memset_async(dgnn_ctx* c, void* p, int value, size_t bytes);
+void* pinned_scratch(dgnn_ctx* c, size_t bytes);  // NULL on failure; valid until the next call
 dgnn_status check_dev_err(dgnn_ctx* c);  // synchronizes
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

@@ -667,9 +667,20 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
 
         Arena a_nodes{c}, a_edges{c}, a_eptr{c};
         int64_t used_nodes = 0, used_edges = 0, used_eptr = 0;
-        std::vector<int32_t> h_n(G), h_hb(G * (H + 2));
-        std::vector<int64_t> h_frs(H * (kMaxGroup + 1)), h_cbs(H * (kMaxGroup + 1));
-        std::vector<int64_t> h_plan;
+        // host views of the per-group sizes and the compaction plan, in pinned memory
+        const size_t n_frs = (size_t)H * (kMaxGroup + 1);
+        const size_t plan_cap = 3 * (size_t)(G + 1) + (size_t)H * G;
+        const size_t pin_bytes = sizeof(int64_t) * (2 * n_frs + plan_cap) + sizeof(int32_t) * (G + G * (H + 2));
+        auto* pin = static_cast<uint8_t*>(pinned_scratch(c, pin_bytes));
+        if (!pin) {
+            set_error("pinned host allocation of %zu bytes failed", pin_bytes);
+            return DGNN_ENOMEM;
+        }
+        int64_t* h_frs = reinterpret_cast<int64_t*>(pin);
+        int64_t* h_cbs = h_frs + n_frs;
+        int64_t* h_plan = h_cbs + n_frs;
+        int32_t* h_n = reinterpret_cast<int32_t*>(h_plan + plan_cap);
+        int32_t* h_hb = h_n + G;
 
         for (int64_t t0 = 0; t0 < nb; t0 += G) {
             const int Gc = (int)std::min<int64_t>(G, nb - t0);
@@ -751,17 +762,18 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
                 DGNN_CK_LAUNCH();
             }
             // ---- group end: read sizes, then compact into the batch-major arena ----
-            DGNN_CK(cudaMemcpyAsync(h_n.data(), g.n, sizeof(int32_t) * Gc, cudaMemcpyDeviceToHost, c->stream));
-            DGNN_CK(cudaMemcpyAsync(h_hb.data(), g.hop_bound, sizeof(int32_t) * Gc * (H + 2), cudaMemcpyDeviceToHost,
+            DGNN_CK(cudaMemcpyAsync(h_n, g.n, sizeof(int32_t) * Gc, cudaMemcpyDeviceToHost, c->stream));
+            DGNN_CK(cudaMemcpyAsync(h_hb, g.hop_bound, sizeof(int32_t) * Gc * (H + 2), cudaMemcpyDeviceToHost,
                                     c->stream));
-            DGNN_CK(cudaMemcpyAsync(h_frs.data(), g.hop_fr_off, sizeof(int64_t) * H * (kMaxGroup + 1),
+            DGNN_CK(cudaMemcpyAsync(h_frs, g.hop_fr_off, sizeof(int64_t) * H * (kMaxGroup + 1),
                                     cudaMemcpyDeviceToHost, c->stream));
-            DGNN_CK(cudaMemcpyAsync(h_cbs.data(), g.hop_cbase, sizeof(int64_t) * H * (kMaxGroup + 1),
+            DGNN_CK(cudaMemcpyAsync(h_cbs, g.hop_cbase, sizeof(int64_t) * H * (kMaxGroup + 1),
                                     cudaMemcpyDeviceToHost, c->stream));
             DGNN_TRY(check_dev_err(c));  // synchronizes
             // plan: node_pre[G+1], edge_pre[G+1], eptr_pre[G+1], edges_before[H*G]
-            h_plan.assign(3 * (Gc + 1) + H * Gc, 0);
-            int64_t* node_pre = h_plan.data();
+            const size_t plan_n = 3 * (size_t)(Gc + 1) + (size_t)H * Gc;
+            std::fill(h_plan, h_plan + plan_n, int64_t(0));
+            int64_t* node_pre = h_plan;
             int64_t* edge_pre = node_pre + (Gc + 1);
             int64_t* eptr_pre = edge_pre + (Gc + 1);
             int64_t* ebef = eptr_pre + (Gc + 1);
@@ -796,8 +808,8 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
                                      used_edges));
             DGNN_TRY(a_eptr.reserve(used_eptr + eptr_pre[Gc] > a_eptr.cap ? est(used_eptr, eptr_pre[Gc]) : 0,
                                     used_eptr));
-            DGNN_TRY(d_plan.alloc(c, h_plan.size()));
-            DGNN_CK(cudaMemcpyAsync(d_plan.p, h_plan.data(), sizeof(int64_t) * h_plan.size(), cudaMemcpyHostToDevice,
+            DGNN_TRY(d_plan.alloc(c, plan_n));
+            DGNN_CK(cudaMemcpyAsync(d_plan.p, h_plan, sizeof(int64_t) * plan_n, cudaMemcpyHostToDevice,
                                     c->stream));
             CompactPlan p{};
             p.G = Gc;

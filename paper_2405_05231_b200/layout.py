@@ -441,7 +441,8 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
                    counts: torch.Tensor | None = None, ws: Workspace | None = None,
                    group_budget: int = 4 << 30, stage_piece: int = 1 << 40, file_path: str | None = None,
                    direct_io: bool = True, disk_budget: int | None = None, disk_m: int = 1,
-                   disk_k: int = 4, disk_budget_frac: float | None = None, after_sample=None) -> Layout:
+                   disk_k: int = 4, disk_budget_frac: float | None = None, after_sample=None,
+                   scratch_ws: Workspace | None = None) -> Layout:
     """Run a1-a8 on this rank's batches.
 
     ``seeds`` are this rank's seeds (batch t of them gets bid = batch_id_base + t).
@@ -452,6 +453,9 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
     the packed chunks exceed it -- the heuristic of P:410-413 picks the smallest segment
     size s whose Eq. 2 space fits (threshold ``disk_m``, MinHash with ``disk_k`` hashes).
     ``disk_budget_frac`` states the budget as a fraction of the packed-only space instead.
+    ``scratch_ws``: a Workspace for buffers that do not outlive this call (the packed lists and
+    the pack group buffers), shared by consecutive passes on the same ctx: before reusing them
+    the ctx stream waits for the previous pass's stage-out on the ctx side stream.
     ``after_sample``: called once the samples are complete (dgnn_sample returns when they are),
     before the rest of the pass is enqueued -- a scheduling hook (bench.py starts the previous
     pass's assembly there, so that sampling never shares the GPU with it).
@@ -504,7 +508,13 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
     nb = samples.num_batches
     total_nodes = samples.total_nodes
     addr = buf("addr", total_nodes, torch.int32)
-    packed_ids = buf("packed_ids", total_nodes, torch.int32)
+    if scratch_ws is not None:
+        # the previous pass on this ctx may still be copying its group buffer out
+        ctx.stream.wait_stream(torch.cuda.ExternalStream(ctx.side_stream_ptr, device=dev))
+        nbytes = max(int(total_nodes), 1) * 4
+        packed_ids = scratch_ws.dev("packed_ids", nbytes, dev)[:nbytes].view(torch.int32)
+    else:
+        packed_ids = buf("packed_ids", total_nodes, torch.int32)
     packed_off = torch.empty(nb + 1, dtype=torch.int64, device=dev)
     po = A.dgnn_classify(ctx, plan, samples, 0, nb, addr, packed_ids, packed_off) if nb else np.zeros(1, np.int64)
     batch_tiers = A.dgnn_batch_tier_counts(ctx, samples, 0, nb, addr) if nb else np.zeros((0, 3), np.int64)
@@ -583,7 +593,8 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
         staged = arena is not None or disk is not None
         # group buffers come from the workspace when there is one: re-allocating GBs every
         # pass can force the caching allocator to map memory inside the timed region
-        L._group_bufs = [(ws.dev(f"group_buf{i}", max(max_gb, 16), dev)[:max(max_gb, 16)] if ws is not None
+        gws = scratch_ws if scratch_ws is not None else ws
+        L._group_bufs = [(gws.dev(f"group_buf{i}", max(max_gb, 16), dev)[:max(max_gb, 16)] if gws is not None
                           else torch.empty(max(max_gb, 16), dtype=torch.uint8, device=dev))
                          for i in range(min(2, len(groups)))] if staged else []
     if disk is not None:
