@@ -133,6 +133,10 @@ dgnn_status dgnn_ctx_set_assemble_occupancy(dgnn_ctx* ctx, int32_t blocks_per_sm
 
 /* Statistics: number of kernels this ctx has launched; optional per-launch CUDA-event
  * timing on the ctx stream (enable before the region of interest). */
+/* Cap every grid this ctx launches at max_blocks CTAs (0 = no cap).  For a ctx running
+ * PCIe-bound UVA gathers next to latency-bound work on other streams: a few SMs' worth of
+ * outstanding host reads already saturate PCIe, more only queue up in the memory system. */
+dgnn_status dgnn_ctx_set_grid_cap(dgnn_ctx* ctx, int32_t max_blocks);
 int64_t dgnn_ctx_launches(const dgnn_ctx* ctx);
 dgnn_status dgnn_ctx_set_timing(dgnn_ctx* ctx, int enable);
 typedef struct {

@@ -43,7 +43,7 @@ EXPORTS = [
     "dgnn_file_open", "dgnn_file_close", "dgnn_stage_file_write", "dgnn_stage_file_read",
     "dgnn_disk_index_build", "dgnn_disk_index_free", "dgnn_disk_space", "dgnn_disk_search", "dgnn_disk_plan_build",
     "dgnn_disk_plan_get_info", "dgnn_disk_plan_free", "dgnn_disk_cache_fill", "dgnn_disk_partial",
-    "dgnn_train_stub", "dgnn_ctx_set_sample_mode", "dgnn_assemble_group_peer", "dgnn_device_alloc",
+    "dgnn_train_stub", "dgnn_ctx_set_sample_mode", "dgnn_ctx_set_grid_cap", "dgnn_assemble_group_peer", "dgnn_device_alloc",
     "dgnn_device_free", "dgnn_ipc_handle", "dgnn_ipc_open", "dgnn_ipc_close", "dgnn_disk_index_partition_counts", "dgnn_pack_partition", "dgnn_pack_tails",
 ]
 
@@ -159,6 +159,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "dgnn_disk_partial": (i32, [P, P, i64, i64, P, P, P, P, P]),
             "dgnn_train_stub": (i32, [P, P, i64, i64, P, i64]),
             "dgnn_ctx_set_sample_mode": (i32, [P, i32]),
+            "dgnn_ctx_set_grid_cap": (i32, [P, i32]),
             "dgnn_assemble_group_peer": (i32, [P, P, P, i64, i64, P, i64, i32, P, i64, P, P, P, P, i64, P]),
             "dgnn_device_alloc": (i32, [i32, i64, ctypes.POINTER(P)]),
             "dgnn_device_free": (i32, [P]),
@@ -296,6 +297,10 @@ class Ctx:
 
     def set_sample_group(self, batches: int):
         _check(load_library().dgnn_ctx_set_sample_group(self.handle, int(batches)), "dgnn_ctx_set_sample_group")
+
+    def set_grid_cap(self, max_blocks: int):
+        """Cap every grid this ctx launches (0 = none); see dgnn_ctx_set_grid_cap."""
+        _check(load_library().dgnn_ctx_set_grid_cap(self.handle, int(max_blocks)), "dgnn_ctx_set_grid_cap")
 
     def set_sample_mode(self, blocks: bool):
         """False: node-wise (reading c4, default); True: the DGL-block variant (reading c27)."""

@@ -200,6 +200,12 @@ dgnn_status dgnn_ctx_set_sample_group(dgnn_ctx* c, int32_t batches) {
     return DGNN_OK;
 }
 
+dgnn_status dgnn_ctx_set_grid_cap(dgnn_ctx* c, int32_t max_blocks) {
+    DGNN_REQUIRE(c && max_blocks >= 0, "dgnn_ctx_set_grid_cap: bad argument");
+    c->grid_cap = max_blocks;
+    return DGNN_OK;
+}
+
 dgnn_status dgnn_ctx_set_sample_mode(dgnn_ctx* c, int32_t mode) {
     DGNN_REQUIRE(c && (mode == DGNN_SAMPLE_NODEWISE || mode == DGNN_SAMPLE_BLOCKS),
                  "dgnn_ctx_set_sample_mode: bad argument");

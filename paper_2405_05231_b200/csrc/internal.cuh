@@ -28,6 +28,7 @@ struct dgnn_ctx {
     int32_t sample_group = 0;
     int32_t sample_mode = DGNN_SAMPLE_NODEWISE;
     int assemble_blocks_per_sm = 8;  // grid cap for a9 (lower it to leave SMs to a concurrent pass)
+    int grid_cap = 0;                // > 0: no launch of this ctx uses more CTAs (dgnn_ctx_set_grid_cap)
     // per-launch CUDA-event timing
     bool timing = false;
     struct Pending {
@@ -159,6 +160,7 @@ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline int grid_for(dgnn_ctx* c, int64_t work_items, int per_block, int blocks_per_sm = 8) {
     int64_t need = ceil_div(work_items > 0 ? work_items : 1, per_block);
     int64_t cap = (int64_t)c->num_sms * blocks_per_sm;
+    if (c->grid_cap > 0 && cap > c->grid_cap) cap = c->grid_cap;
     return (int)(need < cap ? need : cap);
 }
 

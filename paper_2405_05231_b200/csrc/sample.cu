@@ -22,6 +22,8 @@
 // then one host sync per group sizes the batch-major compaction into the
 // output arena.
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 
 #include "internal.cuh"
 
@@ -682,7 +684,13 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
         int32_t* h_n = reinterpret_cast<int32_t*>(h_plan + plan_cap);
         int32_t* h_hb = h_n + G;
 
+        // DGNN_TRACE_SAMPLE=1: host-side split of the call (enqueue vs waiting in the group syncs)
+        const bool trace = std::getenv("DGNN_TRACE_SAMPLE") != nullptr;
+        using clk = std::chrono::steady_clock;
+        double t_wait = 0.0, t_enq = 0.0, t_post = 0.0;
+        const auto t_start = clk::now();
         for (int64_t t0 = 0; t0 < nb; t0 += G) {
+            const auto tg0 = clk::now();
             const int Gc = (int)std::min<int64_t>(G, nb - t0);
             g.G = Gc;
             DGNN_TRY(memset_async(c, d_table.p, 0xFF, sizeof(int2) * ((size_t)Gc << tlog)));
@@ -769,7 +777,13 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
                                     cudaMemcpyDeviceToHost, c->stream));
             DGNN_CK(cudaMemcpyAsync(h_cbs, g.hop_cbase, sizeof(int64_t) * H * (kMaxGroup + 1),
                                     cudaMemcpyDeviceToHost, c->stream));
+            const auto tg1 = clk::now();
             DGNN_TRY(check_dev_err(c));  // synchronizes
+            const auto tg2 = clk::now();
+            if (trace) {
+                t_enq += std::chrono::duration<double, std::milli>(tg1 - tg0).count();
+                t_wait += std::chrono::duration<double, std::milli>(tg2 - tg1).count();
+            }
             // plan: node_pre[G+1], edge_pre[G+1], eptr_pre[G+1], edges_before[H*G]
             const size_t plan_n = 3 * (size_t)(Gc + 1) + (size_t)H * Gc;
             std::fill(h_plan, h_plan + plan_n, int64_t(0));
@@ -845,6 +859,13 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
             used_nodes += node_pre[Gc];
             used_edges += edge_pre[Gc];
             used_eptr += eptr_pre[Gc];
+        }
+        if (trace) {
+            const double tot = std::chrono::duration<double, std::milli>(clk::now() - t_start).count();
+            t_post = tot - t_enq - t_wait;
+            fprintf(stderr, "[dgnn_sample] groups=%lld G=%lld total %.1f ms: enqueue %.1f, sync-wait %.1f, "
+                    "post-sync host+compaction enqueue %.1f\n", (long long)((nb + G - 1) / G), (long long)G, tot,
+                    t_enq, t_wait, t_post);
         }
         S->cap_nodes = a_nodes.cap;
         S->nodes = a_nodes.release();
