@@ -218,6 +218,7 @@ class Runner:
         self.nb = (inp[3].numel() + cfg["batch_size"] - 1) // cfg["batch_size"]
         self.before_layout = None  # hook: e.g. the e2e H2D copies of the inputs
         self.host_window = 128
+        self.stage_piece = (512 << 20) if pipelined else (1 << 40)  # stage-out granularity (bytes)
         self.disk_budget_frac = None  # segmented disk cache off (unlimited disk budget, reading c18)
         self.train = False  # trainer stub after assembly (the training pipeline)
         self.sT = torch.cuda.Stream(dev)
@@ -239,7 +240,7 @@ class Runner:
     def ctxs(self):
         return [self.ctxA, self.ctxB, self.ctxG, self.ctxT]
 
-    def layout(self, slot, after_sample=None):
+    def layout(self, slot, after_sample=None, before_pack=None):
         cfg, indptr, indices, seeds, feats, gpu_rows, host_rows = self.inp
         if self.before_layout is not None:
             self.before_layout()
@@ -248,9 +249,9 @@ class Runner:
         return self.dg.offline_layout(self.ctxA, indptr, indices, feats, seeds, cfg["fanout"], cfg["batch_size"],
                                       gpu_rows, host_rows, RNG_SEED, group_size=cfg["group_size"],
                                       batch_id_base=self.rank * self.nb, counts=c, ws=self.ws[slot],
-                                      stage_piece=int(os.environ.get("DGNN_STAGE_PIECE", str(1 << 40))),
+                                      stage_piece=int(os.environ.get("DGNN_STAGE_PIECE", str(self.stage_piece))),
                                       disk_budget_frac=self.disk_budget_frac, after_sample=after_sample,
-                                      scratch_ws=self.scratch_ws)
+                                      scratch_ws=self.scratch_ws, before_pack=before_pack)
 
     def _assemble(self, L, ev_l):
         """Enqueue the assembly (and trainer) of pass L on stream B after its layout; -> end event."""
@@ -300,7 +301,13 @@ class Runner:
                 last = None
                 if not self.pipelined:
                     L = None
-                Ln = self.layout((e + 1) % 2)
+                pack_alone = None
+                if self.pipelined and os.environ.get("DGNN_PACK_ALONE", "1") == "1":
+                    # the HBM-bound pack of pass e+1 waits for the assembly of pass e (it would
+                    # share HBM with it otherwise); its chunks then go out in pieces so that the
+                    # next assembly starts on the first ones
+                    pack_alone = lambda ev=ev_a: self.sA.wait_event(ev)
+                Ln = self.layout((e + 1) % 2, before_pack=pack_alone)
                 ev_l = torch.cuda.Event()
                 ev_l.record(self.sA)
             prev_ev = ev_a
