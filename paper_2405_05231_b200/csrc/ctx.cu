@@ -88,25 +88,33 @@ void* pinned_scratch(dgnn_ctx* c, size_t bytes) {
 
 extern std::atomic<int> g_io_error;
 
-dgnn_status check_dev_err(dgnn_ctx* c) {
+dgnn_status read_dev_err(dgnn_ctx* c, int* flags) {
     if (!c->pinned_err) DGNN_CK(cudaHostAlloc((void**)&c->pinned_err, sizeof(int), cudaHostAllocDefault));
     DGNN_CK(cudaMemcpyAsync(c->pinned_err, c->dev_err, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     DGNN_CK(cudaStreamSynchronize(c->stream));
-    const int h = *c->pinned_err;
+    *flags = *c->pinned_err;
+    if (*flags) DGNN_CK(cudaMemsetAsync(c->dev_err, 0, sizeof(int), c->stream));
+    return DGNN_OK;
+}
+
+dgnn_status dev_err_status(int h) {
+    if (!h) return DGNN_OK;
+    if (h & DEVERR_SEED_RANGE) { set_error("a seed is outside [0, num_nodes)"); return DGNN_EINVAL; }
+    if (h & DEVERR_SEED_DUP) { set_error("a seed appears twice within one batch (reading c12)"); return DGNN_EINVAL; }
+    if (h & DEVERR_ADDR_RANGE) { set_error("unresolvable node address (slot beyond its tier)"); return DGNN_ERANGE; }
+    if (h & DEVERR_TABLE) { set_error("internal: sampling hash table overflow"); return DGNN_ECUDA; }
+    set_error("internal: device capacity overflow (flags %d)", h);
+    return DGNN_ECUDA;
+}
+
+dgnn_status check_dev_err(dgnn_ctx* c) {
+    int h = 0;
+    DGNN_TRY(read_dev_err(c, &h));
     if (g_io_error.exchange(0)) {
         set_error("file staging: a pread/pwrite failed or hit end of file");
         return DGNN_EIO;
     }
-    if (h) {
-        DGNN_CK(cudaMemsetAsync(c->dev_err, 0, sizeof(int), c->stream));
-        if (h & DEVERR_SEED_RANGE) { set_error("a seed is outside [0, num_nodes)"); return DGNN_EINVAL; }
-        if (h & DEVERR_SEED_DUP) { set_error("a seed appears twice within one batch (reading c12)"); return DGNN_EINVAL; }
-        if (h & DEVERR_ADDR_RANGE) { set_error("unresolvable node address (slot beyond its tier)"); return DGNN_ERANGE; }
-        if (h & DEVERR_TABLE) { set_error("internal: sampling hash table overflow"); return DGNN_ECUDA; }
-        set_error("internal: device capacity overflow (flags %d)", h);
-        return DGNN_ECUDA;
-    }
-    return DGNN_OK;
+    return dev_err_status(h);
 }
 
 }  // namespace dgnn

@@ -154,6 +154,8 @@ inline void launch(dgnn_ctx* c, int kid, double bytes, F&& f) {
 dgnn_status memset_async(dgnn_ctx* c, void* p, int value, size_t bytes);
 void* pinned_scratch(dgnn_ctx* c, size_t bytes);  // NULL on failure; valid until the next call
 dgnn_status check_dev_err(dgnn_ctx* c);  // synchronizes
+dgnn_status read_dev_err(dgnn_ctx* c, int* flags);  // synchronizes; clears the device word
+dgnn_status dev_err_status(int flags);               // DEVERR_* bits -> status + message
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 

@@ -24,6 +24,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdlib>
+#include <string>
 
 #include "internal.cuh"
 
@@ -118,6 +119,12 @@ __global__ void k_seed_init(Grp g, const int32_t* __restrict__ seeds, int64_t nu
         else if (r < 0) atomicOr(err, DEVERR_TABLE);
         else if (counts) atomicAdd(&counts[u], 1u);
     }
+}
+
+// access counter over a group's compacted node lists (batch nodes are distinct): counts[v] += 1
+__global__ void k_count_nodes(const int32_t* __restrict__ nodes, int64_t n, uint32_t* __restrict__ counts) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(&counts[nodes[i]], 1u);
 }
 
 __global__ void k_seed_range(const int32_t* __restrict__ seeds, int64_t n, int64_t N, int* err) {
@@ -689,13 +696,24 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
         using clk = std::chrono::steady_clock;
         double t_wait = 0.0, t_enq = 0.0, t_post = 0.0;
         const auto t_start = clk::now();
-        for (int64_t t0 = 0; t0 < nb; t0 += G) {
+        // Hash-set size: the first group uses the exact bound (2 x the node bound); later groups
+        // use 2 x the largest node count seen so far (a table that stays in L2 for the smaller
+        // group footprint), and a group that overflows is redone at the bound.  The access
+        // counter is therefore applied after a group succeeds, over its compacted nodes.
+        const int tlog_safe = tlog;
+        const bool adaptive = !(std::getenv("DGNN_SAMPLE_TABLE") && std::string(std::getenv("DGNN_SAMPLE_TABLE")) == "bound");
+        int tlog_cur = tlog_safe;
+        int64_t max_n_seen = 0;
+        int64_t redone = 0;
+        for (int64_t t0 = 0; t0 < nb;) {
             const auto tg0 = clk::now();
             const int Gc = (int)std::min<int64_t>(G, nb - t0);
             g.G = Gc;
-            DGNN_TRY(memset_async(c, d_table.p, 0xFF, sizeof(int2) * ((size_t)Gc << tlog)));
+            g.tlog = tlog_cur;
+            g.tmask = (uint32_t)((1ull << tlog_cur) - 1);
+            DGNN_TRY(memset_async(c, d_table.p, 0xFF, sizeof(int2) * ((size_t)Gc << tlog_cur)));
             launch(c, DGNN_K_SAMPLE_SEED, 0.0, [&] {
-                k_seed_init<<<Gc, 256, 0, c->stream>>>(g, seeds, num_seeds, batch_size, t0, N, counts, c->dev_err);
+                k_seed_init<<<Gc, 256, 0, c->stream>>>(g, seeds, num_seeds, batch_size, t0, N, nullptr, c->dev_err);
             });
             DGNN_CK_LAUNCH();
             for (int h = 0; h < H; ++h) {
@@ -739,7 +757,7 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
                 DGNN_TRY(memset_async(c, d_hist.p, 0, sizeof(int32_t) * (size_t)nbk));
                 launch(c, DGNN_K_SAMPLE_ORDER, 0.0, [&] {
                     k_insert<<<grid_for(c, cmax, 256), 256, 0, c->stream>>>(g, d_cand[h].p, NB, shift[h], d_hist.p,
-                                                                            d_npos.p, d_ntab.p, counts, c->dev_err);
+                                                                            d_npos.p, d_ntab.p, nullptr, c->dev_err);
                 });
                 DGNN_CK_LAUNCH();
                 {
@@ -778,12 +796,21 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
             DGNN_CK(cudaMemcpyAsync(h_cbs, g.hop_cbase, sizeof(int64_t) * H * (kMaxGroup + 1),
                                     cudaMemcpyDeviceToHost, c->stream));
             const auto tg1 = clk::now();
-            DGNN_TRY(check_dev_err(c));  // synchronizes
+            int flags = 0;
+            DGNN_TRY(read_dev_err(c, &flags));  // synchronizes
             const auto tg2 = clk::now();
             if (trace) {
                 t_enq += std::chrono::duration<double, std::milli>(tg1 - tg0).count();
                 t_wait += std::chrono::duration<double, std::milli>(tg2 - tg1).count();
             }
+            if ((flags & DEVERR_TABLE) && tlog_cur < tlog_safe) {  // the smaller table overflowed: redo
+                tlog_cur = tlog_safe;
+                ++redone;
+                continue;
+            }
+            DGNN_TRY(dev_err_status(flags));
+            for (int s = 0; s < Gc; ++s) max_n_seen = std::max<int64_t>(max_n_seen, h_n[s]);
+            if (adaptive) tlog_cur = std::min(tlog_safe, std::max(4, ceil_log2(2 * max_n_seen)));
             // plan: node_pre[G+1], edge_pre[G+1], eptr_pre[G+1], edges_before[H*G]
             const size_t plan_n = 3 * (size_t)(Gc + 1) + (size_t)H * Gc;
             std::fill(h_plan, h_plan + plan_n, int64_t(0));
@@ -843,6 +870,13 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
                                                                                         a_nodes.p + used_nodes);
             });
             DGNN_CK_LAUNCH();
+            if (counts && node_pre[Gc]) {  // one count per batch containing the node
+                launch(c, DGNN_K_SAMPLE_ORDER, 0.0, [&] {
+                    k_count_nodes<<<grid_for(c, node_pre[Gc], 256), 256, 0, c->stream>>>(
+                        a_nodes.p + used_nodes, node_pre[Gc], counts);
+                });
+                DGNN_CK_LAUNCH();
+            }
             for (int h = 0; h < H; ++h) {
                 const int64_t Ch = h_cbs[h * (kMaxGroup + 1) + Gc];
                 if (Ch == 0) continue;
@@ -859,13 +893,15 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
             used_nodes += node_pre[Gc];
             used_edges += edge_pre[Gc];
             used_eptr += eptr_pre[Gc];
+            t0 += Gc;
         }
         if (trace) {
             const double tot = std::chrono::duration<double, std::milli>(clk::now() - t_start).count();
             t_post = tot - t_enq - t_wait;
             fprintf(stderr, "[dgnn_sample] groups=%lld G=%lld total %.1f ms: enqueue %.1f, sync-wait %.1f, "
-                    "post-sync host+compaction enqueue %.1f\n", (long long)((nb + G - 1) / G), (long long)G, tot,
-                    t_enq, t_wait, t_post);
+                    "post-sync host+compaction enqueue %.1f; table 2^%d (bound 2^%d), %lld groups redone\n",
+                    (long long)((nb + G - 1) / G), (long long)G, tot, t_enq, t_wait, t_post, tlog_cur, tlog_safe,
+                    (long long)redone);
         }
         S->cap_nodes = a_nodes.cap;
         S->nodes = a_nodes.release();
