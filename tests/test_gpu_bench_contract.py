@@ -1,0 +1,66 @@
+"""bench.py keeps its JSON contract (one line on stdout; the keys the driver and the judge read),
+on small configurations so that the check takes seconds: the default path, every opt-in path
+(disk cache, trainer, DGL blocks, sequential) and the reference arm."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _run(*args, timeout=900):
+    p = subprocess.run([sys.executable, "bench.py", *args], cwd=ROOT, capture_output=True, text=True, timeout=timeout)
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = [l for l in p.stdout.splitlines() if l.strip()]
+    assert len(lines) == 1, p.stdout[-2000:]
+    return json.loads(lines[0])
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+
+
+def _check_common(d, steps, warmup):
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config"):
+        assert k in d, k
+    assert d["steps"] == steps and d["warmup"] == warmup and d["n_gpus"] == 1
+    assert d["value"] > 0 and d["higher_is_better"] is True and d["scaling"] == "weak"
+    assert "workload" in d["config"]
+
+
+def test_default_contract_products():
+    d = _run("--config", "products", "--steps", "2", "--warmup", "3", "--cpu-batches", "4", "--e2e-steps", "1")
+    _check_common(d, 2, 3)
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and 0 < r["frac"] <= 1.0 and r["peak"] > 0 and r["achieved"] > 0
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] > 0 and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    assert d["gpu_launches"] > 0 and "clocks" in d and d["clocks"]["sm_mhz"] is not None
+
+
+@pytest.mark.parametrize("flags", [["--disk-budget", "0.9", "--train"], ["--blocks", "--sequential"]])
+def test_opt_in_paths_tiny(flags):
+    d = _run("--config", "tiny", "--steps", "2", "--warmup", "3", "--no-e2e", "--cpu-batches", "8", *flags)
+    _check_common(d, 2, 3)
+    assert d["gpu_launches"] > 0
+    if "--disk-budget" in flags:
+        assert "disk_cache" in d["layout_stats"]
+        assert d["layout_stats"]["disk_cache"]["space_pages"] <= d["layout_stats"]["disk_cache"]["budget_pages"]
+        assert "trainer stub" in d["config"]["schedule"]
+    if "--blocks" in flags:
+        assert "DGL-block" in d["config"]["schedule"] and "DGL blocks" in d["cpu_baseline"]["sample"]
+
+
+def test_reference_arm_tiny():
+    d = _run("--impl", "reference", "--config", "tiny", "--steps", "1", "--warmup", "1")
+    assert d["impl"] == "reference" and d["value"] > 0
+    assert d["cpu_baseline"]["kind"] == "oracle"
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
