@@ -296,6 +296,14 @@ dgnn_status dgnn_file_open(const char* path, int32_t direct, int32_t create, int
 dgnn_status dgnn_file_close(dgnn_file* f);
 dgnn_status dgnn_stage_file_write(dgnn_ctx* ctx, dgnn_file* f, int64_t file_off, const void* dev_src, int64_t bytes,
                                   void* bounce, int64_t chunk_bytes, int64_t* ticket);
+/* Disk-cache page reads (P:307 merged requests; the paper's io_uring engine): the 4 KiB
+ * pages pages[0..n_pages) of the cache region at file offset base_off are read (runs of
+ * consecutive pages as one pread, runs spread over `threads` threads) into dev_dst back to back,
+ * through the pinned bounce buffer (bounce_bytes, page-aligned) in stream order on the side
+ * stream.  The page list is copied at the call; returns a staging ticket like dgnn_stage_copy. */
+dgnn_status dgnn_stage_file_read_pages(dgnn_ctx* ctx, dgnn_file* f, int64_t base_off, const int32_t* pages,
+                                       int64_t n_pages, void* dev_dst, void* bounce, int64_t bounce_bytes,
+                                       int32_t threads, int64_t* ticket);
 dgnn_status dgnn_stage_file_read(dgnn_ctx* ctx, dgnn_file* f, int64_t file_off, void* dev_dst, int64_t bytes,
                                  void* bounce, int64_t chunk_bytes, int64_t* ticket);
 

@@ -43,7 +43,7 @@ EXPORTS = [
     "dgnn_file_open", "dgnn_file_close", "dgnn_stage_file_write", "dgnn_stage_file_read",
     "dgnn_disk_index_build", "dgnn_disk_index_free", "dgnn_disk_space", "dgnn_disk_search", "dgnn_disk_plan_build",
     "dgnn_disk_plan_get_info", "dgnn_disk_plan_free", "dgnn_disk_cache_fill", "dgnn_disk_partial",
-    "dgnn_train_stub", "dgnn_ctx_set_sample_mode", "dgnn_ctx_set_grid_cap", "dgnn_assemble_group_peer", "dgnn_device_alloc",
+    "dgnn_train_stub", "dgnn_stage_file_read_pages", "dgnn_ctx_set_sample_mode", "dgnn_ctx_set_grid_cap", "dgnn_assemble_group_peer", "dgnn_device_alloc",
     "dgnn_device_free", "dgnn_ipc_handle", "dgnn_ipc_open", "dgnn_ipc_close", "dgnn_disk_index_partition_counts", "dgnn_pack_partition", "dgnn_pack_tails",
 ]
 
@@ -159,6 +159,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "dgnn_disk_partial": (i32, [P, P, i64, i64, P, P, P, P, P]),
             "dgnn_train_stub": (i32, [P, P, i64, i64, P, i64]),
             "dgnn_ctx_set_sample_mode": (i32, [P, i32]),
+            "dgnn_stage_file_read_pages": (i32, [P, P, i64, P, i64, P, P, i64, i32, ctypes.POINTER(i64)]),
             "dgnn_ctx_set_grid_cap": (i32, [P, i32]),
             "dgnn_assemble_group_peer": (i32, [P, P, P, i64, i64, P, i64, i32, P, i64, P, P, P, P, i64, P]),
             "dgnn_device_alloc": (i32, [i32, i64, ctypes.POINTER(P)]),
@@ -730,3 +731,16 @@ class IpcMapping:
                                ctypes.byref(p)), "dgnn_ipc_open")
         self.ptr = int(p.value or 0)
         self._fin = weakref.finalize(self, L.dgnn_ipc_close, P(self.ptr))
+
+
+def dgnn_stage_file_read_pages(ctx: Ctx, f: DiskFile, base_off: int, pages, dev_dst, bounce, bounce_bytes: int,
+                               threads: int = 4) -> int:
+    """Read 4 KiB pages (host int32 page indices) of the file's cache region into dev_dst."""
+    import numpy as np
+    pg = np.ascontiguousarray(pages, dtype=np.int32)
+    t = i64()
+    _check(load_library().dgnn_stage_file_read_pages(ctx.handle, f.handle, int(base_off),
+                                                     P(pg.ctypes.data) if pg.size else P(0), int(pg.size),
+                                                     _ptr(dev_dst), _ptr(bounce), int(bounce_bytes), int(threads),
+                                                     ctypes.byref(t)), "dgnn_stage_file_read_pages")
+    return int(t.value)

@@ -171,7 +171,7 @@ class Layout:
                 pages = torch.empty(max(q, 1) * 4096, dtype=torch.uint8, device=dev)
                 part = torch.empty(max(rows * self.row_bytes, 16), dtype=torch.uint8, device=dev)
                 zero = torch.zeros(2, dtype=torch.int64, device=dev)
-                chunk = self._partial(b, b + 1, chunk, zero, zero, pages, part)
+                chunk = self._partial(self.ctx, b, b + 1, chunk, zero, zero, pages, part)
         A.dgnn_assemble(self.ctx, self.addr[n0:n1], self.gpu_tier, self.plan.k_gpu, self.host_tier.ptr,
                         self.plan.k_host, chunk, rows, self.row_bytes, out)
         return out
@@ -182,15 +182,22 @@ class Layout:
         src = self.arena.tensor if self.arena is not None else self.arena_dev
         return src[self.cache_off:self.cache_off + max(dp.cache_pages, 1) * 4096].view(-1, 4096)
 
-    def _partial(self, b0: int, b1: int, chunk, chunk_off: torch.Tensor, out_off: torch.Tensor, pages, out):
-        """Partial input of batches [b0, b1): fetch their merged cache-page requests
-        into ``pages`` and interleave them with the (reduced) chunk rows into ``out``: dense DISK
-        rows in local order at ``out_off`` (device, run-relative byte offsets)."""
+    def _partial(self, ctx: A.Ctx, b0: int, b1: int, chunk, chunk_off: torch.Tensor, out_off: torch.Tensor, pages,
+                 out, bounce=None):
+        """Partial input of batches [b0, b1), enqueued on ``ctx``: fetch their merged
+        cache-page requests into ``pages`` (a UVA gather from the pinned / HBM cache region, or
+        page preads from the disk-tier file through ``bounce``) and interleave them with the
+        (reduced) chunk rows into ``out``: dense DISK rows in local order at ``out_off``."""
         dp = self.disk_plan
         q0, q1 = int(dp.req_off_host[b0]), int(dp.req_off_host[b1])
         if q1 > q0:
-            A.dgnn_gather_rows(self.ctx, self._cache_rows(), dp.req_pages[q0:q1], pages)
-        A.dgnn_disk_partial(self.ctx, dp, b0, b1, pages, chunk, chunk_off, out, out_off)
+            if self.disk is not None:
+                t = A.dgnn_stage_file_read_pages(ctx, self.disk, self.cache_off, self._req_pages_host[q0:q1], pages,
+                                                 bounce.ptr, FILE_CHUNK)
+                A.dgnn_stage_wait(ctx, t)
+            else:
+                A.dgnn_gather_rows(ctx, self._cache_rows(), dp.req_pages[q0:q1], pages)
+        A.dgnn_disk_partial(ctx, dp, b0, b1, pages, chunk, chunk_off, out, out_off)
         return out
 
     def assembly_groups(self, out_budget: int = 1 << 30):
@@ -379,8 +386,8 @@ class Layout:
             if ring_wait is not None and (i - 2) in ring_wait:
                 ctx.stream.wait_event(ring_wait.pop(i - 2))  # the consumer of run i-2 released the slot
             if dp is not None:
-                chunk = self._partial(b0, b1, chunk, t[3 * k + 3:4 * k + 4], t[k + 1:2 * k + 2], page_ring[i % 2],
-                                      part_ring[i % 2])
+                chunk = self._partial(ctx, b0, b1, chunk, t[3 * k + 3:4 * k + 4], t[k + 1:2 * k + 2],
+                                      page_ring[i % 2], part_ring[i % 2], bounce_r)
             if windows:
                 host_src, host_map = staging[cur], smap[cur]
             else:
@@ -521,8 +528,6 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
     if disk_budget_frac is not None and nb:
         disk_budget = int(disk_budget_frac * int(((np.diff(po) * row_bytes + 4095) // 4096).sum())) * 4096
     if disk_budget is not None and nb:
-        if stage == "file":
-            raise NotImplementedError("the segmented disk cache is staged in pinned host memory or HBM")
         idx = A.DiskIndex(ctx, packed_ids[:int(po[-1])], packed_off, po, N)
         s_seg, pages = A.dgnn_disk_search(ctx, idx, row_bytes, int(disk_budget) // 4096, disk_m)
         if s_seg == 0:
@@ -638,9 +643,19 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
         else:
             dst = arena_dev[g.arena_off:g.arena_off + max(g.group_bytes, 0)]
             A.dgnn_pack(ctx, features, ids, rel_po, rel_co, total, g.group_bytes, dst)
+    if dplan is not None:
+        L._req_pages_host = dplan.req_pages.cpu().numpy() if disk is not None else None
     if dplan is not None and dplan.cache_pages:
         # the segment caches, MinHash-ordered, after the chunks
-        A.dgnn_disk_cache_fill(ctx, dplan, features, L._cache_rows())
+        if disk is not None:  # through HBM into the disk-tier file
+            with torch.cuda.stream(ctx.stream):
+                cache_dev = torch.empty(dplan.cache_pages * 4096, dtype=torch.uint8, device=dev)
+            A.dgnn_disk_cache_fill(ctx, dplan, features, cache_dev)
+            t = A.dgnn_stage_file_write(ctx, disk, cache_off, cache_dev, cache_dev.numel(), L._bounce_w.ptr,
+                                        FILE_CHUNK)
+            A.dgnn_stage_sync(ctx, t)  # on disk before the layout returns (cache_dev is released)
+        else:
+            A.dgnn_disk_cache_fill(ctx, dplan, features, L._cache_rows())
     mark("pack")
     L._rel_all = rel_all
     # packed_ids is only read by the pack kernels on this stream: releasing it now is

@@ -165,7 +165,8 @@ def test_papers_scale_plan(dg, ctx):
 RNG_SEED = 0x5EEDD15C
 
 
-@pytest.mark.parametrize("stage,frac,window", [("pinned", 0.8, 64), ("hbm", 0.6, 1), ("pinned", 1.0, 128)])
+@pytest.mark.parametrize("stage,frac,window", [("pinned", 0.8, 64), ("hbm", 0.6, 1), ("pinned", 1.0, 128),
+                                               ("file", 0.7, 4)])
 def test_layout_with_disk_cache_tiny(dg, ctx, stage, frac, window):
     """offline_layout with a disk budget: the heuristic's s, the segment caches, the reduced
     chunks and every assembled batch equal the oracle's (assembly == direct gather)."""
@@ -180,12 +181,18 @@ def test_layout_with_disk_cache_tiny(dg, ctx, stage, frac, window):
     assert s_ref >= 1
     dplan = oracle.disk_plan(pl, 10_000, rb, s_ref, 1, 4, RNG_SEED)
     dev = torch.device("cuda", 0)
+    import os
+    import tempfile
+    path = os.path.join(tempfile.mkdtemp(prefix="dgnn_dc_"), "disk.bin") if stage == "file" else None
     L = dg.offline_layout(ctx, w.indptr.to(dev), w.indices.to(dev), w.features.to(dev), w.seeds.to(dev), [10, 5],
-                          256, 500, 1000, RNG_SEED, group_size=8, stage=stage, disk_budget_frac=frac)
+                          256, 500, 1000, RNG_SEED, group_size=8, stage=stage, disk_budget_frac=frac, file_path=path)
     ctx.sync()
     assert L.disk_plan.s == s_ref
     assert L.stats["disk_cache"]["space_pages"] == dplan.space_pages
-    arena = L.arena.tensor.numpy() if L.arena is not None else L.arena_dev.cpu().numpy()
+    if stage == "file":
+        arena = np.fromfile(path, dtype=np.uint8)
+    else:
+        arena = L.arena.tensor.numpy() if L.arena is not None else L.arena_dev.cpu().numpy()
     cache = arena[L.cache_off:L.cache_off + dplan.cache_pages * PAGE]
     assert np.array_equal(cache, oracle.disk_cache_fill(feats, dplan))
     # reduced chunks: the oracle's pack of P_b'
@@ -193,13 +200,17 @@ def test_layout_with_disk_cache_tiny(dg, ctx, stage, frac, window):
     for g in L.groups:
         buf, off = oracle.pack(feats, red[g.b_lo:g.b_hi])
         assert np.array_equal(arena[g.arena_off:g.arena_off + g.group_bytes], buf)
+    # the assembly on its own ctx / stream, as bench.py runs it (the partial input must be built
+    # on the assembling stream, ordered with its staged chunks)
+    actx = dg.Ctx(device=0, stream=torch.cuda.Stream(dev))
     seen = 0
-    for b, out in L.assemble_epoch(host_window=window):
-        got = out.view(torch.uint8).reshape(out.shape[0], -1).cpu().numpy()
+    for b, out in L.assemble_epoch(ctx=actx, host_window=window, out_budget=256 * 7 * 512):
+        with torch.cuda.stream(actx.stream):
+            got = out.view(torch.uint8).reshape(out.shape[0], -1).cpu().numpy()
         assert np.array_equal(got, oracle.assemble(feats, ref["samples"][b].nodes)), f"batch {b}"
         seen += 1
     assert seen == len(pl)
-    for b in (0, len(pl) - 1):  # single-batch path
+    for b in ((0, len(pl) - 1) if stage != "file" else ()):  # single-batch path (memory-resident tiers)
         n = len(ref["samples"][b].nodes)
         out = torch.empty((n, w.features.shape[1]), dtype=w.features.dtype, device=dev)
         L.assemble(b, out)
