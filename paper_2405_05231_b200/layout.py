@@ -248,7 +248,8 @@ class Layout:
 
     def assemble_epoch(self, ctx: A.Ctx | None = None, out_budget: int = 1 << 30, host_window: int = 128,
                        gather_ctx: A.Ctx | None = None, sharded_tier=None, remote=None, runs: bool = False,
-                       ring_wait: dict | None = None, ws: Workspace | None = None, peer_tier=None):
+                       ring_wait: dict | None = None, ws: Workspace | None = None, peer_tier=None,
+                       pcie_rows: torch.Tensor | None = None):
         """Pipelined assembly: the chunks of the next run of batches are staged H2D
         on the side stream while the current run is assembled on the ctx stream (one
         dgnn_assemble_group launch per run).  Yields (b, features[n_b, dim]) per batch; a
@@ -274,7 +275,10 @@ class Layout:
         on the same stream (keeps tens of GB out of the caching allocator's churn).
 
         ``peer_tier`` (a shard.PeerTier): the GPU tier sharded over ranks and read one-sided
-        through peer memory (dgnn_assemble_group_peer), no exchange round."""
+        through peer memory (dgnn_assemble_group_peer), no exchange round.
+
+        ``pcie_rows`` (device int64 [1], measurement only): accumulates the host-tier rows the
+        window gathers move over PCIe."""
         ctx = ctx or self.ctx
         gctx = gather_ctx or ctx
         nb = self.num_batches
@@ -343,6 +347,9 @@ class Layout:
             A.dgnn_host_window(gctx, self.addr[spans[w0][0]:spans[w1 - 1][1]], w, stamp, kh, wlist[s], smap[s],
                                wcount[s])
             A.dgnn_gather_rows_dev(gctx, self.host_tier.ptr, kh, self.row_bytes, wlist[s], wcount[s], staging[s])
+            if pcie_rows is not None:
+                with torch.cuda.stream(gctx.stream):
+                    pcie_rows.add_(wcount[s])
             ev = torch.cuda.Event()
             ev.record(gctx.stream)
             ev_ready[w] = ev
