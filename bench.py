@@ -230,13 +230,13 @@ class Runner:
         # concurrent layout and loses overall, so all streams run at the default priority)
         self.sG = torch.cuda.Stream(dev, priority=int(os.environ.get("DGNN_GATHER_PRIORITY", "0")))
         self.ctxG = dg.Ctx(device=dev, stream=self.sG)
-        # the window gathers are PCIe-bound UVA reads: half the SMs with one CTA each keep PCIe
-        # busy, and fewer outstanding host reads leave the memory system to the concurrent
-        # (latency-bound) sampling of the next pass -- measured 1450-1510 vs 1350-1370
-        # mini-batches/s with one-CTA-per-SM x 2 and no cap
+        # the window gathers are PCIe-bound UVA reads: three quarters of the SMs with one CTA
+        # each keep PCIe busy, and fewer outstanding host reads leave the memory system to the
+        # concurrent (latency-bound) sampling of the next pass -- measured 1450-1520 vs
+        # 1350-1370 mini-batches/s with two CTAs per SM and no cap
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
         self.ctxG.set_assemble_occupancy(int(os.environ.get("DGNN_GATHER_OCC", "1")))
-        self.ctxG.set_grid_cap(int(os.environ.get("DGNN_GATHER_GRID", str(sms // 2))))
+        self.ctxG.set_grid_cap(int(os.environ.get("DGNN_GATHER_GRID", str(3 * sms // 4))))
 
     def ctxs(self):
         return [self.ctxA, self.ctxB, self.ctxG, self.ctxT]

@@ -349,6 +349,16 @@ dgnn_status dgnn_assemble_group(dgnn_ctx* ctx, const uint32_t* addr, const int64
  * instead of once per batch; outputs are unchanged. */
 dgnn_status dgnn_host_window(dgnn_ctx* ctx, const uint32_t* addr, int64_t n, int32_t window_id, int32_t* stamp,
                              int64_t k_host, int32_t* list, int64_t capacity, int32_t* smap, int64_t* count);
+/* Runs of consecutive slots in the window's list (after dgnn_host_window with the same stamp,
+ * window_id and smap): runs[r] = list position where run r starts, *run_count = runs.  A run
+ * of k slots is k*row_bytes contiguous bytes, so dgnn_gather_runs_dev moves the window's rows
+ * with one contiguous copy per run (fewer, larger PCIe reads than one per row):
+ * out + p*row_bytes .. = src + list[p]*row_bytes .. for every list position p < *count. */
+dgnn_status dgnn_host_window_runs(dgnn_ctx* ctx, const int32_t* stamp, int64_t k_host, int32_t window_id,
+                                  const int32_t* smap, int32_t* runs, int64_t* run_count);
+dgnn_status dgnn_gather_runs_dev(dgnn_ctx* ctx, const void* src, int64_t row_bytes, const int32_t* list,
+                                 const int64_t* count, const int32_t* runs, const int64_t* run_count,
+                                 int64_t max_runs, void* out);
 /* ---- sharded GPU tier (when the GPU tier does not fit replicated, slot s
  * lives on rank s % world at local row s / world; remote rows travel over NVLink with
  * all-to-all exchanges run by the caller's process group) ----

@@ -43,7 +43,7 @@ EXPORTS = [
     "dgnn_file_open", "dgnn_file_close", "dgnn_stage_file_write", "dgnn_stage_file_read",
     "dgnn_disk_index_build", "dgnn_disk_index_free", "dgnn_disk_space", "dgnn_disk_search", "dgnn_disk_plan_build",
     "dgnn_disk_plan_get_info", "dgnn_disk_plan_free", "dgnn_disk_cache_fill", "dgnn_disk_partial",
-    "dgnn_train_stub", "dgnn_stage_file_read_pages", "dgnn_ctx_set_sample_mode", "dgnn_ctx_set_grid_cap", "dgnn_assemble_group_peer", "dgnn_device_alloc",
+    "dgnn_train_stub", "dgnn_stage_file_read_pages", "dgnn_host_window_runs", "dgnn_gather_runs_dev", "dgnn_ctx_set_sample_mode", "dgnn_ctx_set_grid_cap", "dgnn_assemble_group_peer", "dgnn_device_alloc",
     "dgnn_device_free", "dgnn_ipc_handle", "dgnn_ipc_open", "dgnn_ipc_close", "dgnn_disk_index_partition_counts", "dgnn_pack_partition", "dgnn_pack_tails",
 ]
 
@@ -159,6 +159,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "dgnn_disk_partial": (i32, [P, P, i64, i64, P, P, P, P, P]),
             "dgnn_train_stub": (i32, [P, P, i64, i64, P, i64]),
             "dgnn_ctx_set_sample_mode": (i32, [P, i32]),
+            "dgnn_host_window_runs": (i32, [P, P, i64, i32, P, P, P]),
+            "dgnn_gather_runs_dev": (i32, [P, P, i64, P, P, P, P, i64, P]),
             "dgnn_stage_file_read_pages": (i32, [P, P, i64, P, i64, P, P, i64, i32, ctypes.POINTER(i64)]),
             "dgnn_ctx_set_grid_cap": (i32, [P, i32]),
             "dgnn_assemble_group_peer": (i32, [P, P, P, i64, i64, P, i64, i32, P, i64, P, P, P, P, i64, P]),
@@ -744,3 +746,16 @@ def dgnn_stage_file_read_pages(ctx: Ctx, f: DiskFile, base_off: int, pages, dev_
                                                      _ptr(dev_dst), _ptr(bounce), int(bounce_bytes), int(threads),
                                                      ctypes.byref(t)), "dgnn_stage_file_read_pages")
     return int(t.value)
+
+
+def dgnn_host_window_runs(ctx: Ctx, stamp: torch.Tensor, k_host: int, window_id: int, smap: torch.Tensor,
+                          runs: torch.Tensor, run_count: torch.Tensor):
+    _check(load_library().dgnn_host_window_runs(ctx.handle, _ptr(stamp), int(k_host), int(window_id), _ptr(smap),
+                                                _ptr(runs), _ptr(run_count)), "dgnn_host_window_runs")
+
+
+def dgnn_gather_runs_dev(ctx: Ctx, src, row_bytes: int, lst: torch.Tensor, count: torch.Tensor, runs: torch.Tensor,
+                         run_count: torch.Tensor, max_runs: int, out):
+    _check(load_library().dgnn_gather_runs_dev(ctx.handle, _ptr(src), int(row_bytes), _ptr(lst), _ptr(count),
+                                               _ptr(runs), _ptr(run_count), int(max_runs), _ptr(out)),
+           "dgnn_gather_runs_dev")

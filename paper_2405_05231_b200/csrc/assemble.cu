@@ -220,6 +220,76 @@ extern "C" dgnn_status dgnn_host_window(dgnn_ctx* c, const uint32_t* addr, int64
     return DGNN_OK;
 }
 
+namespace dgnn {
+namespace {
+// Runs of consecutive host slots in a window's (ascending) list: one contiguous copy per run.
+// A run of k rows is k*row_bytes contiguous bytes in the host tier and in the staging buffer;
+// lanes move 16-byte vectors, four 512-byte strides in flight per warp.
+__global__ void __launch_bounds__(256) k_gather_runs(const uint8_t* __restrict__ src, int64_t row_bytes,
+                                                     const int32_t* __restrict__ list,
+                                                     const int64_t* __restrict__ count,
+                                                     const int32_t* __restrict__ runs,
+                                                     const int64_t* __restrict__ run_count,
+                                                     uint8_t* __restrict__ dst) {
+    const int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int lane = threadIdx.x & 31;
+    const int64_t nr = *run_count, n = *count;
+    for (int64_t r = warp; r < nr; r += nwarps) {
+        const int64_t p0 = runs[r], p1 = r + 1 < nr ? runs[r + 1] : n;
+        const uint4* s = reinterpret_cast<const uint4*>(src + (int64_t)list[p0] * row_bytes);
+        uint4* d = reinterpret_cast<uint4*>(dst + p0 * row_bytes);
+        const int64_t nv = (p1 - p0) * row_bytes / 16;
+        for (int64_t q = lane; q < nv; q += 4 * 32) {
+            uint4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (q + u * 32 < nv) v[u] = __ldg(s + q + u * 32);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (q + u * 32 < nv) __stcs(d + q + u * 32, v[u]);
+        }
+    }
+}
+}  // namespace
+}  // namespace dgnn
+
+extern "C" dgnn_status dgnn_host_window_runs(dgnn_ctx* c, const int32_t* stamp, int64_t k_host, int32_t window_id,
+                                             const int32_t* smap, int32_t* runs, int64_t* run_count) {
+    DGNN_REQUIRE(c && stamp && smap && runs && run_count && k_host >= 0 && window_id >= 0,
+                 "dgnn_host_window_runs: bad argument");
+    DGNN_CK(cudaSetDevice(c->device));
+    DGNN_TRY(memset_async(c, run_count, 0, sizeof(int64_t)));
+    if (k_host == 0) return DGNN_OK;
+    const int32_t wid = window_id;
+    auto in = [=] __device__(int64_t s) -> int32_t {
+        return (stamp[s] == wid && (s == 0 || stamp[s - 1] != wid)) ? 1 : 0;
+    };
+    auto outf = [=] __device__(int64_t s, int64_t excl, int64_t val) {
+        if (val) runs[excl] = smap[s];
+    };
+    DGNN_TRY(scan::run(c, k_host, nullptr, in, outf, run_count));
+    return DGNN_OK;
+}
+
+extern "C" dgnn_status dgnn_gather_runs_dev(dgnn_ctx* c, const void* src, int64_t row_bytes, const int32_t* list,
+                                            const int64_t* count, const int32_t* runs, const int64_t* run_count,
+                                            int64_t max_runs, void* out) {
+    DGNN_REQUIRE(c && count && run_count && (max_runs == 0 || (src && list && runs && out)),
+                 "dgnn_gather_runs_dev: NULL argument");
+    DGNN_REQUIRE(row_bytes > 0 && row_bytes % 16 == 0 && al16(src) && al16(out) && max_runs >= 0,
+                 "dgnn_gather_runs_dev: rows and buffers must be 16-byte aligned");
+    if (max_runs == 0) return DGNN_OK;
+    DGNN_CK(cudaSetDevice(c->device));
+    const int grid = grid_for(c, max_runs * 32, 256, c->assemble_blocks_per_sm);
+    launch(c, DGNN_K_ASSEMBLE, 0.0, [&] {
+        k_gather_runs<<<grid, 256, 0, c->stream>>>((const uint8_t*)src, row_bytes, list, count, runs, run_count,
+                                                   (uint8_t*)out);
+    });
+    DGNN_CK_LAUNCH();
+    return DGNN_OK;
+}
+
 extern "C" dgnn_status dgnn_gather_rows_dev(dgnn_ctx* c, const void* features, int64_t num_rows, int64_t row_bytes,
                                             const int32_t* ids, const int64_t* n_dev, int64_t n_max, void* out) {
     DGNN_REQUIRE(c && n_dev && (n_max == 0 || (features && ids && out)), "dgnn_gather_rows_dev: NULL argument");

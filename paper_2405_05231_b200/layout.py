@@ -22,6 +22,7 @@ Data placement:
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -331,6 +332,10 @@ class Layout:
                 smap = [buf(f"smap{i}", kh, torch.int32) for i in range(nbuf)]
                 wlist = [buf(f"wlist{i}", max(cap, 1), torch.int32) for i in range(nbuf)]
                 wcount = [buf(f"wcount{i}", 1, torch.int64) for i in range(nbuf)]
+                use_runs = self.row_bytes % 16 == 0 and os.environ.get("DGNN_GATHER_RUNS", "1") == "1"
+                if use_runs:  # runs of consecutive host slots: one contiguous copy each
+                    wruns = [buf(f"wruns{i}", max(cap, 1), torch.int32) for i in range(nbuf)]
+                    wnruns = [buf(f"wnruns{i}", 1, torch.int64) for i in range(nbuf)]
                 staging = [buf(f"staging{i}", max(cap, 1) * self.row_bytes) for i in range(nbuf)]
         if gctx is not ctx:
             gctx.stream.wait_stream(ctx.stream)  # stamp / buffers were created on the ctx stream
@@ -346,7 +351,13 @@ class Layout:
             w0, w1 = windows[w]
             A.dgnn_host_window(gctx, self.addr[spans[w0][0]:spans[w1 - 1][1]], w, stamp, kh, wlist[s], smap[s],
                                wcount[s])
-            A.dgnn_gather_rows_dev(gctx, self.host_tier.ptr, kh, self.row_bytes, wlist[s], wcount[s], staging[s])
+            if use_runs:
+                A.dgnn_host_window_runs(gctx, stamp, kh, w, smap[s], wruns[s], wnruns[s])
+                A.dgnn_gather_runs_dev(gctx, self.host_tier.ptr, self.row_bytes, wlist[s], wcount[s], wruns[s],
+                                       wnruns[s], cap, staging[s])
+            else:
+                A.dgnn_gather_rows_dev(gctx, self.host_tier.ptr, kh, self.row_bytes, wlist[s], wcount[s],
+                                       staging[s])
             if pcie_rows is not None:
                 with torch.cuda.stream(gctx.stream):
                     pcie_rows.add_(wcount[s])
