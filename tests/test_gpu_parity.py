@@ -323,3 +323,11 @@ def test_assembly_workspace_reuse(dg, ctx, tiny):
         for b, out in L.assemble_epoch(host_window=window, out_budget=budget, gather_ctx=gctx, ws=ws):
             got = out.view(torch.uint8).reshape(out.shape[0], -1).cpu().numpy()
             assert np.array_equal(got, oracle.assemble(feats, ref[b].nodes)), f"window {window} batch {b}"
+
+
+def test_window_gather_row_path(dg, ctx, tiny, monkeypatch):
+    """The per-row window gather (DGNN_GATHER_RUNS=0) still equals the direct gather; the
+    default run-copy path is covered by every other windowed test."""
+    monkeypatch.setenv("DGNN_GATHER_RUNS", "0")
+    gctx = dg.Ctx(device=0, stream=torch.cuda.Stream(torch.device("cuda", 0)))
+    _layout_parity(dg, ctx, tiny, [10, 5], 256, 500, 1000, 8, "pinned", host_window=3, gather_ctx=gctx)
