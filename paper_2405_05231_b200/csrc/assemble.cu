@@ -166,6 +166,46 @@ __global__ void __launch_bounds__(256, 6) k_gather_dev(const uint8_t* __restrict
     copy_rows_warp<kAsmU, V>(*n_dev, row_bytes, Row{src, row_bytes, ids, dst}, warp, nwarps);
 }
 
+// Staging gather of a window's host rows (PCIe-bound): each warp owns a chunk of
+// kGatherCH consecutive list positions, and every lane keeps kGatherV 16-byte loads
+// in flight across the chunk's rows (vector q of the chunk is row q / vpr, offset
+// q % vpr), i.e. up to 4 KiB per warp before the stores.  Rows of consecutive host
+// slots (runs) come out as contiguous requests without any run bookkeeping, and a
+// dense window (every slot, as on Friendster-shaped bounded epochs) is split evenly
+// over the warps.
+constexpr int kGatherCH = 8;
+constexpr int kGatherV = 8;
+__global__ void __launch_bounds__(256) k_gather_chunks(const uint8_t* __restrict__ src, int64_t row_bytes,
+                                                       const int32_t* __restrict__ ids,
+                                                       const int64_t* __restrict__ n_dev, uint8_t* __restrict__ dst) {
+    const int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int lane = threadIdx.x & 31;
+    const int64_t n = *n_dev;
+    const int vpr = (int)(row_bytes >> 4);
+    for (int64_t p0 = warp * kGatherCH; p0 < n; p0 += nwarps * kGatherCH) {
+        const int rows = (int)(n - p0 < kGatherCH ? n - p0 : kGatherCH);
+        const int64_t my_id = lane < rows ? (int64_t)ids[p0 + lane] : 0;
+        const int total = rows * vpr;
+        const uint4* d0 = reinterpret_cast<const uint4*>(dst + p0 * row_bytes);
+        for (int q0 = 0; q0 < total; q0 += 32 * kGatherV) {
+            uint4 v[kGatherV];
+            int qq[kGatherV];
+#pragma unroll
+            for (int i = 0; i < kGatherV; ++i) {
+                const int q = q0 + i * 32 + lane;
+                const int u = q / vpr;  // row of the chunk (warp-uniform per 32 consecutive q when vpr % 32 == 0)
+                const int64_t id = __shfl_sync(0xffffffffu, my_id, u < rows ? u : 0);
+                qq[i] = q;
+                if (q < total) v[i] = __ldg(reinterpret_cast<const uint4*>(src + id * row_bytes) + (q - u * vpr));
+            }
+#pragma unroll
+            for (int i = 0; i < kGatherV; ++i)
+                if (qq[i] < total) __stcs(const_cast<uint4*>(d0) + qq[i], v[i]);
+        }
+    }
+}
+
 }  // namespace
 }  // namespace dgnn
 
@@ -297,11 +337,12 @@ extern "C" dgnn_status dgnn_gather_rows_dev(dgnn_ctx* c, const void* features, i
     if (n_max == 0) return DGNN_OK;
     DGNN_CK(cudaSetDevice(c->device));
     const bool v16 = row_bytes % 16 == 0 && al16(features) && al16(out);
-    const int grid = grid_for(c, n_max * 32 / kAsmU, 256, c->assemble_blocks_per_sm);
+    const int grid = v16 ? grid_for(c, ceil_div(n_max, (int64_t)kGatherCH) * 32, 256, c->assemble_blocks_per_sm)
+                         : grid_for(c, n_max * 32 / kAsmU, 256, c->assemble_blocks_per_sm);
     launch(c, DGNN_K_ASSEMBLE, 0.0, [&] {
         if (v16)
-            k_gather_dev<uint4><<<grid, 256, 0, c->stream>>>((const uint8_t*)features, row_bytes, ids, n_dev,
-                                                             (uint8_t*)out);
+            k_gather_chunks<<<grid, 256, 0, c->stream>>>((const uint8_t*)features, row_bytes, ids, n_dev,
+                                                         (uint8_t*)out);
         else
             k_gather_dev<uint32_t><<<grid, 256, 0, c->stream>>>((const uint8_t*)features, row_bytes, ids, n_dev,
                                                                 (uint8_t*)out);

@@ -332,7 +332,7 @@ class Layout:
                 smap = [buf(f"smap{i}", kh, torch.int32) for i in range(nbuf)]
                 wlist = [buf(f"wlist{i}", max(cap, 1), torch.int32) for i in range(nbuf)]
                 wcount = [buf(f"wcount{i}", 1, torch.int64) for i in range(nbuf)]
-                use_runs = self.row_bytes % 16 == 0 and os.environ.get("DGNN_GATHER_RUNS", "1") == "1"
+                use_runs = self.row_bytes % 16 == 0 and os.environ.get("DGNN_GATHER_RUNS", "0") == "1"
                 if use_runs:  # runs of consecutive host slots: one contiguous copy each
                     wruns = [buf(f"wruns{i}", max(cap, 1), torch.int32) for i in range(nbuf)]
                     wnruns = [buf(f"wnruns{i}", 1, torch.int64) for i in range(nbuf)]

@@ -325,9 +325,35 @@ def test_assembly_workspace_reuse(dg, ctx, tiny):
             assert np.array_equal(got, oracle.assemble(feats, ref[b].nodes)), f"window {window} batch {b}"
 
 
-def test_window_gather_row_path(dg, ctx, tiny, monkeypatch):
-    """The per-row window gather (DGNN_GATHER_RUNS=0) still equals the direct gather; the
-    default run-copy path is covered by every other windowed test."""
-    monkeypatch.setenv("DGNN_GATHER_RUNS", "0")
+def test_window_gather_runs_path(dg, ctx, tiny, monkeypatch):
+    """The run-copy window gather (DGNN_GATHER_RUNS=1: one contiguous copy per run of
+    consecutive host slots) still equals the direct gather; the default chunked row gather is
+    covered by every other windowed test."""
+    monkeypatch.setenv("DGNN_GATHER_RUNS", "1")
     gctx = dg.Ctx(device=0, stream=torch.cuda.Stream(torch.device("cuda", 0)))
     _layout_parity(dg, ctx, tiny, [10, 5], 256, 500, 1000, 8, "pinned", host_window=3, gather_ctx=gctx)
+
+
+@pytest.mark.parametrize("row_bytes", [12, 16, 48, 400, 512, 1024, 4096])
+@pytest.mark.parametrize("n", [0, 1, 7, 8, 9, 1000, 4099])
+def test_gather_rows_dev_chunks(dg, ctx, row_bytes, n):
+    """dgnn_gather_rows_dev (the window staging gather: 8-row chunks per warp, 8 vectors in
+    flight per lane) equals the oracle's row gather for row sizes whose vector count is not a
+    multiple of 32 (48, 400 B), ragged last chunks, runs of consecutive ids and scattered ids;
+    the 12-byte rows take the 4-byte path."""
+    rng = np.random.default_rng(row_bytes * 7919 + n)
+    num_rows = 5000
+    table = rng.integers(0, 256, (num_rows, row_bytes), dtype=np.uint8)
+    # half runs of consecutive ids, half random ids, ascending like a window list
+    runs = np.concatenate([np.arange(s, s + 3) for s in rng.integers(0, num_rows - 3, max(n // 6, 1))])
+    ids = np.concatenate([runs, rng.integers(0, num_rows, n)])[:n].astype(np.int32)
+    dev = torch.device("cuda", 0)
+    src = torch.as_tensor(table).to(dev)
+    out = torch.full((max(n, 1) + 3, row_bytes), 0xAB, dtype=torch.uint8, device=dev)
+    ids_d = torch.as_tensor(ids).to(dev)
+    n_dev = torch.tensor([n], dtype=torch.int64, device=dev)
+    dg._abi.dgnn_gather_rows_dev(ctx, src, num_rows, row_bytes, ids_d, n_dev, out)
+    ctx.sync()
+    got = out.cpu().numpy()
+    assert np.array_equal(got[:n], oracle.assemble(table, ids)), "gathered rows differ"
+    assert (got[n:] == 0xAB).all(), "wrote past n"
