@@ -101,10 +101,18 @@ def setup_dist(args):
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("DGNN_BENCH_SHARE_GPU") == "1":
+        # test hook: several ranks on one GPU (the gpurun box has one), with gloo for the
+        # collectives since NCCL refuses two ranks on one device
+        local = local % torch.cuda.device_count()
     if ws > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("DGNN_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(local)
     return ws, rank, local

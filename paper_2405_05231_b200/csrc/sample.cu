@@ -79,18 +79,6 @@ __device__ __forceinline__ int table_insert(int2* tab, int tlog, uint32_t mask, 
     return -1;
 }
 
-__device__ __forceinline__ int2* table_find(int2* tab, int tlog, uint32_t mask, int32_t key) {
-    uint32_t p = slot_hash(key, tlog);
-    for (uint32_t probes = 0; probes <= mask; ++probes) {
-        int2* e = &tab[p];
-        const int k = e->x;
-        if (k == key) return e;
-        if (k == kEmpty) return nullptr;
-        p = (p + 1) & mask;
-    }
-    return nullptr;
-}
-
 // ----------------------------------------------------------------- seeds
 __global__ void k_seed_init(Grp g, const int32_t* __restrict__ seeds, int64_t num_seeds, int32_t B, int64_t t0,
                             int64_t N, uint32_t* counts, int* err) {
@@ -395,16 +383,16 @@ __global__ void k_bucket_sort_assign(Grp g, int64_t NB, const int64_t* __restric
     }
 }
 
-__global__ void k_remap(Grp g, int32_t* __restrict__ cand, int* err) {
+// Edge remap: the insert kept each candidate's table slot (ntab), so the local ID is one
+// load from the slot k_bucket_sort_assign filled -- no second probe sequence.
+__global__ void k_remap(Grp g, int32_t* __restrict__ cand, const int32_t* __restrict__ ntab) {
     __shared__ int64_t s_cb[kMaxGroup + 1];
     for (int i = threadIdx.x; i <= g.G; i += blockDim.x) s_cb[i] = g.cand_base[i];
     __syncthreads();
     const int64_t C = s_cb[g.G];
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < C; i += (int64_t)gridDim.x * blockDim.x) {
         const int s = segment_of(s_cb, g.G + 1, i);
-        const int2* e = table_find(g.table + ((int64_t)s << g.tlog), g.tlog, g.tmask, cand[i]);
-        if (e) cand[i] = e->y;
-        else atomicOr(err, DEVERR_TABLE);
+        cand[i] = g.table[((int64_t)s << g.tlog) + (uint32_t)ntab[i]].y;
     }
 }
 
@@ -781,7 +769,7 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
                 });
                 DGNN_CK_LAUNCH();
                 launch(c, DGNN_K_SAMPLE_REMAP, 0.0, [&] {
-                    k_remap<<<grid_for(c, cmax, 256), 256, 0, c->stream>>>(g, d_cand[h].p, c->dev_err);
+                    k_remap<<<grid_for(c, cmax, 256), 256, 0, c->stream>>>(g, d_cand[h].p, d_ntab.p);
                 });
                 DGNN_CK_LAUNCH();
                 launch(c, DGNN_K_SAMPLE_SETUP, 0.0, [&] { k_hop_end<<<1, 256, 0, c->stream>>>(g, h); });

@@ -64,3 +64,28 @@ def test_reference_arm_tiny():
     assert d["impl"] == "reference" and d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle"
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+
+
+def test_two_rank_launch_on_one_gpu():
+    """The N > 1 path of bench.py as the driver launches it (torch.distributed.run, one process
+    per rank, batch-sharded epochs, the count all-reduce, max-over-ranks timing, one JSON line
+    from rank 0), with both ranks on the box's one GPU and gloo standing in for NCCL."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, DGNN_BENCH_SHARE_GPU="1", DGNN_BENCH_BACKEND="gloo")
+    p = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                        "--master-addr=127.0.0.1", f"--master-port={port}", "bench.py", "--gpus", "2",
+                        "--config", "tiny", "--steps", "2", "--warmup", "3", "--no-cpu", "--e2e-steps", "1"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = [l for l in p.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1, p.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["scaling"] == "weak"
+    assert d["config"]["parallelism"].startswith("dp2")
+    # value counts the batches of both ranks
+    assert abs(d["value"] - 2 * d["config"]["batches_per_rank"] * d["steps"] / (d["ms_per_step"] * d["steps"] / 1e3)) \
+        <= 0.02 * d["value"]
+    assert d["e2e"]["value"] > 0
