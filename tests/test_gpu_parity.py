@@ -166,12 +166,18 @@ def test_fig3_address_table(dg, ctx):
 
 
 def _layout_parity(dg, ctx, w, fan, B, gpu_rows, host_rows, group, stage, host_window=64, out_budget=1 << 30,
-                   gather_ctx=None):
+                   gather_ctx=None, host_features=False):
     ip, ix, sd = w.indptr.numpy(), w.indices.numpy(), w.seeds.numpy()
     feats = w.features.numpy()
     ref = oracle.offline_layout(ip, ix, feats, sd, B, fan, RNG_SEED, gpu_rows, host_rows, group, threads=8)
     dev = torch.device("cuda", 0)
-    L = dg.offline_layout(ctx, w.indptr.to(dev), w.indices.to(dev), w.features.to(dev), w.seeds.to(dev), fan, B,
+    if host_features:  # the table stays in pinned host memory; the layout reads rows in place (UVA)
+        hb = dg.HostBuffer(w.features.numel() * w.features.element_size())
+        f_in = hb.tensor.view(w.features.dtype).view(w.features.shape)
+        f_in.copy_(w.features)
+    else:
+        f_in = w.features.to(dev)
+    L = dg.offline_layout(ctx, w.indptr.to(dev), w.indices.to(dev), f_in, w.seeds.to(dev), fan, B,
                           gpu_rows, host_rows, RNG_SEED, group_size=group, stage=stage,
                           file_path=os.path.join(tempfile.mkdtemp(prefix="dgnn_disk_"), "chunks.bin")
                           if stage == "file" else None)
@@ -357,3 +363,10 @@ def test_gather_rows_dev_chunks(dg, ctx, row_bytes, n):
     got = out.cpu().numpy()
     assert np.array_equal(got[:n], oracle.assemble(table, ids)), "gathered rows differ"
     assert (got[n:] == 0xAB).all(), "wrote past n"
+
+
+@pytest.mark.parametrize("stage", ["pinned", "hbm"])
+def test_layout_host_resident_features(dg, ctx, tiny, stage):
+    """Features in pinned host memory (bench.py's e2e mode, the paper's setting): tier fill and
+    pack read the rows in place over PCIe; every output equals the oracle."""
+    _layout_parity(dg, ctx, tiny, [10, 5], 256, 500, 1000, 8, stage, host_window=3, host_features=True)
