@@ -523,6 +523,16 @@ def main():
                    "cuda_malloc_retries": int(torch.cuda.memory_stats(dev).get("num_device_alloc", 0))},
         "device_timeline_ms": R.timeline_ms(),
     }
+    tl = result["device_timeline_ms"]
+    if tl and all("classify" in t for t in tl):
+        # SURVEY 8(d) "offline batches/s" = batches / (sample + build_cache + classify + pack): the
+        # layout span of each timed pass up to the end of classify, plus its pack kernel time (the
+        # pipelined pack first waits for the previous assembly, which is not layout work)
+        spans = [t["classify"] - t["start"] + kst["pack_gather"]["ms"] / args.steps for t in tl]
+        result["offline"] = {"batches_per_s": round(nb * ws / (statistics.median(spans) / 1e3), 1),
+                             "layout_ms_per_pass": round(statistics.median(spans), 1),
+                             "note": "a1-a8 per pass (sample, count all-reduce, tier select, tier fill, classify, "
+                                     "pack); pipelined runs share the GPU with the previous pass's assembly"}
     if asm["ms"] > 0:
         result["assemble_gbs"] = round(asm["bytes"] / (asm["ms"] / 1e3) / 1e9, 1)
         # the step's own roofline: it is bound by the PCIe host->device link, which carries the

@@ -37,7 +37,7 @@ struct PackRow {
     }
 };
 
-template <class V>
+template <class V, int U = kPackU>
 __global__ void __launch_bounds__(256) k_pack(const uint8_t* __restrict__ src, int64_t row_bytes,
                                               const int32_t* __restrict__ ids, const int64_t* __restrict__ packed_off,
                                               const int64_t* __restrict__ chunk_off, int nb, int64_t R,
@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(256) k_pack(const uint8_t* __restrict__ src, i
         for (int64_t i = threadIdx.x & 31; i < nz; i += 32) z[i] = 0u;
     }
     PackRow fn{src, row_bytes, ids, in_smem ? s_seg : packed_off, chunk_off, nb, dst};
-    copy_rows_warp<kPackU, V>(R, row_bytes, fn, warp, nwarps);
+    copy_rows_warp<U, V>(R, row_bytes, fn, warp, nwarps);
 }
 
 struct GatherRow {
@@ -256,11 +256,19 @@ extern "C" dgnn_status dgnn_pack(dgnn_ctx* c, const void* features, int64_t num_
     if (nb == 0) return DGNN_OK;
     DGNN_CK(cudaSetDevice(c->device));
     const bool v16 = row_bytes % 16 == 0 && aligned16(features) && aligned16(group_buf);
-    const int64_t work = std::max<int64_t>(total_rows * 32 / kPackU, nb * 32);
-    const int grid = grid_for(c, work, 256, 8);
+    const int pu = getenv("DGNN_PACK_U") ? atoi(getenv("DGNN_PACK_U")) : kPackU;  // tuning experiment
+    const int pbs = getenv("DGNN_PACK_BPS") ? atoi(getenv("DGNN_PACK_BPS")) : 8;
+    const int64_t work = std::max<int64_t>(total_rows * 32 / pu, nb * 32);
+    const int grid = grid_for(c, work, 256, pbs);
     const double bytes = (double)total_rows * (2.0 * row_bytes + 4.0);
     launch(c, DGNN_K_PACK, bytes, [&] {
-        if (v16)
+        if (v16 && pu == 8)
+            k_pack<uint4, 8><<<grid, 256, 0, c->stream>>>((const uint8_t*)features, row_bytes, packed_ids, packed_off,
+                                                           chunk_off, (int)nb, total_rows, (uint8_t*)group_buf);
+        else if (v16 && pu == 2)
+            k_pack<uint4, 2><<<grid, 256, 0, c->stream>>>((const uint8_t*)features, row_bytes, packed_ids, packed_off,
+                                                           chunk_off, (int)nb, total_rows, (uint8_t*)group_buf);
+        else if (v16)
             k_pack<uint4><<<grid, 256, 0, c->stream>>>((const uint8_t*)features, row_bytes, packed_ids, packed_off,
                                                         chunk_off, (int)nb, total_rows, (uint8_t*)group_buf);
         else
