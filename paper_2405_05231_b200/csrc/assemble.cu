@@ -224,7 +224,8 @@ extern "C" dgnn_status dgnn_assemble(dgnn_ctx* c, const uint32_t* addr, int64_t 
     const bool v16 = row_bytes % 16 == 0 && al16(gpu_tier) && al16(host_tier) && al16(chunk) && al16(out);
     AsmRow fn{addr,        (const uint8_t*)gpu_tier, k_gpu,     (const uint8_t*)host_tier, k_host, (const uint8_t*)chunk,
               chunk_rows,  row_bytes,                (uint8_t*)out, c->dev_err};
-    const int grid = grid_for(c, n * 32 / kAsmU, 256, c->assemble_blocks_per_sm);
+    const int grid = v16 ? grid_resident(c, k_assemble<uint4>, n * 32 / kAsmU, 256, c->assemble_blocks_per_sm)
+                         : grid_resident(c, k_assemble<uint32_t>, n * 32 / kAsmU, 256, c->assemble_blocks_per_sm);
     launch(c, DGNN_K_ASSEMBLE, (double)n * (2.0 * row_bytes + 4.0), [&] {
         if (v16) k_assemble<uint4><<<grid, 256, 0, c->stream>>>(fn, n);
         else k_assemble<uint32_t><<<grid, 256, 0, c->stream>>>(fn, n);
@@ -321,7 +322,7 @@ extern "C" dgnn_status dgnn_gather_runs_dev(dgnn_ctx* c, const void* src, int64_
                  "dgnn_gather_runs_dev: rows and buffers must be 16-byte aligned");
     if (max_runs == 0) return DGNN_OK;
     DGNN_CK(cudaSetDevice(c->device));
-    const int grid = grid_for(c, max_runs * 32, 256, c->assemble_blocks_per_sm);
+    const int grid = grid_resident(c, k_gather_runs, max_runs * 32, 256, c->assemble_blocks_per_sm);
     launch(c, DGNN_K_ASSEMBLE, 0.0, [&] {
         k_gather_runs<<<grid, 256, 0, c->stream>>>((const uint8_t*)src, row_bytes, list, count, runs, run_count,
                                                    (uint8_t*)out);
@@ -337,8 +338,10 @@ extern "C" dgnn_status dgnn_gather_rows_dev(dgnn_ctx* c, const void* features, i
     if (n_max == 0) return DGNN_OK;
     DGNN_CK(cudaSetDevice(c->device));
     const bool v16 = row_bytes % 16 == 0 && al16(features) && al16(out);
-    const int grid = v16 ? grid_for(c, ceil_div(n_max, (int64_t)kGatherCH) * 32, 256, c->assemble_blocks_per_sm)
-                         : grid_for(c, n_max * 32 / kAsmU, 256, c->assemble_blocks_per_sm);
+    const int grid = v16 ? grid_resident(c, k_gather_chunks, ceil_div(n_max, (int64_t)kGatherCH) * 32, 256,
+                                         c->assemble_blocks_per_sm)
+                         : grid_resident(c, k_gather_dev<uint32_t>, n_max * 32 / kAsmU, 256,
+                                         c->assemble_blocks_per_sm);
     launch(c, DGNN_K_ASSEMBLE, 0.0, [&] {
         if (v16)
             k_gather_chunks<<<grid, 256, 0, c->stream>>>((const uint8_t*)features, row_bytes, ids, n_dev,
@@ -483,8 +486,12 @@ extern "C" dgnn_status dgnn_scatter_rows(dgnn_ctx* c, const void* rows, int64_t 
     const bool v16 = row_bytes % 16 == 0 && al16(rows) && al16(out);
     ScatterRow fn{(const uint8_t*)rows, pos, row_bytes, (uint8_t*)out};
     launch(c, DGNN_K_ASSEMBLE, (double)n * (2.0 * row_bytes + 4.0), [&] {
-        if (v16) k_scatter_rows<uint4><<<grid_for(c, n * 32 / kAsmU, 256, 8), 256, 0, c->stream>>>(fn, n);
-        else k_scatter_rows<uint32_t><<<grid_for(c, n * 32 / kAsmU, 256, 8), 256, 0, c->stream>>>(fn, n);
+        if (v16)
+            k_scatter_rows<uint4><<<grid_resident(c, k_scatter_rows<uint4>, n * 32 / kAsmU, 256, 8), 256, 0,
+                                    c->stream>>>(fn, n);
+        else
+            k_scatter_rows<uint32_t><<<grid_resident(c, k_scatter_rows<uint32_t>, n * 32 / kAsmU, 256, 8), 256, 0,
+                                       c->stream>>>(fn, n);
     });
     DGNN_CK_LAUNCH();
     return DGNN_OK;
@@ -508,7 +515,9 @@ extern "C" dgnn_status dgnn_assemble_group_sharded(dgnn_ctx* c, const uint32_t* 
     AsmGroupRow fn{addr,     node_off, chunk_off, chunk_rows, (int)nb,   (const uint8_t*)gpu_tier, k_gpu,
                    (const uint8_t*)host_tier, k_host, host_map, (const uint8_t*)chunk_base, row_bytes,
                    (uint8_t*)out, c->dev_err, gpu_world, gpu_rank, nullptr};
-    const int grid = grid_for(c, n * 32 / kAsmU, 256, c->assemble_blocks_per_sm);
+    const int grid = v16 ? grid_resident(c, k_assemble_group<uint4>, n * 32 / kAsmU, 256, c->assemble_blocks_per_sm)
+                         : grid_resident(c, k_assemble_group<uint32_t>, n * 32 / kAsmU, 256,
+                                         c->assemble_blocks_per_sm);
     launch(c, DGNN_K_ASSEMBLE, (double)n * (2.0 * row_bytes + 4.0), [&] {
         if (v16) k_assemble_group<uint4><<<grid, 256, 0, c->stream>>>(fn, n);
         else k_assemble_group<uint32_t><<<grid, 256, 0, c->stream>>>(fn, n);
@@ -535,7 +544,9 @@ extern "C" dgnn_status dgnn_assemble_group_peer(dgnn_ctx* c, const uint32_t* add
     AsmGroupRow fn{addr,     node_off, chunk_off, chunk_rows, (int)nb,   nullptr, k_gpu,
                    (const uint8_t*)host_tier, k_host, host_map, (const uint8_t*)chunk_base, row_bytes,
                    (uint8_t*)out, c->dev_err, world, 0, (const uint8_t* const*)peers};
-    const int grid = grid_for(c, n * 32 / kAsmU, 256, c->assemble_blocks_per_sm);
+    const int grid = v16 ? grid_resident(c, k_assemble_group<uint4>, n * 32 / kAsmU, 256, c->assemble_blocks_per_sm)
+                         : grid_resident(c, k_assemble_group<uint32_t>, n * 32 / kAsmU, 256,
+                                         c->assemble_blocks_per_sm);
     launch(c, DGNN_K_ASSEMBLE, (double)n * (2.0 * row_bytes + 4.0), [&] {
         if (v16) k_assemble_group<uint4><<<grid, 256, 0, c->stream>>>(fn, n);
         else k_assemble_group<uint32_t><<<grid, 256, 0, c->stream>>>(fn, n);

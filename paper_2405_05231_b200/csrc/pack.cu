@@ -19,6 +19,7 @@ namespace dgnn {
 namespace {
 
 constexpr int kPackU = 4;
+constexpr int kPackBlocksPerSM = 4;  // 32 warps per SM: measured best for 512-byte rows (tools/pack_sweep.py)
 constexpr int kMaxSmemSeg = 2048;
 
 struct PackRow {
@@ -257,24 +258,17 @@ extern "C" dgnn_status dgnn_pack(dgnn_ctx* c, const void* features, int64_t num_
     DGNN_CK(cudaSetDevice(c->device));
     const bool v16 = row_bytes % 16 == 0 && aligned16(features) && aligned16(group_buf);
     const int pu = getenv("DGNN_PACK_U") ? atoi(getenv("DGNN_PACK_U")) : kPackU;  // tuning experiment
-    const int pbs = getenv("DGNN_PACK_BPS") ? atoi(getenv("DGNN_PACK_BPS")) : 8;
+    const int pbs = getenv("DGNN_PACK_BPS") ? atoi(getenv("DGNN_PACK_BPS")) : kPackBlocksPerSM;
+    using PackK = void (*)(const uint8_t*, int64_t, const int32_t*, const int64_t*, const int64_t*, int, int64_t,
+                           uint8_t*);
+    const PackK kern = !v16 ? (PackK)k_pack<uint32_t> : pu == 8 ? (PackK)k_pack<uint4, 8>
+                                                      : pu == 2 ? (PackK)k_pack<uint4, 2> : (PackK)k_pack<uint4>;
     const int64_t work = std::max<int64_t>(total_rows * 32 / pu, nb * 32);
-    const int grid = grid_for(c, work, 256, pbs);
+    const int grid = grid_resident(c, kern, work, 256, pbs);
     const double bytes = (double)total_rows * (2.0 * row_bytes + 4.0);
     launch(c, DGNN_K_PACK, bytes, [&] {
-        if (v16 && pu == 8)
-            k_pack<uint4, 8><<<grid, 256, 0, c->stream>>>((const uint8_t*)features, row_bytes, packed_ids, packed_off,
-                                                           chunk_off, (int)nb, total_rows, (uint8_t*)group_buf);
-        else if (v16 && pu == 2)
-            k_pack<uint4, 2><<<grid, 256, 0, c->stream>>>((const uint8_t*)features, row_bytes, packed_ids, packed_off,
-                                                           chunk_off, (int)nb, total_rows, (uint8_t*)group_buf);
-        else if (v16)
-            k_pack<uint4><<<grid, 256, 0, c->stream>>>((const uint8_t*)features, row_bytes, packed_ids, packed_off,
-                                                        chunk_off, (int)nb, total_rows, (uint8_t*)group_buf);
-        else
-            k_pack<uint32_t><<<grid, 256, 0, c->stream>>>((const uint8_t*)features, row_bytes, packed_ids,
-                                                           packed_off, chunk_off, (int)nb, total_rows,
-                                                           (uint8_t*)group_buf);
+        kern<<<grid, 256, 0, c->stream>>>((const uint8_t*)features, row_bytes, packed_ids, packed_off, chunk_off,
+                                          (int)nb, total_rows, (uint8_t*)group_buf);
     });
     DGNN_CK_LAUNCH();
     return DGNN_OK;
@@ -287,7 +281,8 @@ extern "C" dgnn_status dgnn_gather_rows(dgnn_ctx* c, const void* features, int64
     if (n == 0) return DGNN_OK;
     DGNN_CK(cudaSetDevice(c->device));
     const bool v16 = row_bytes % 16 == 0 && aligned16(features) && aligned16(out);
-    const int grid = grid_for(c, n * 32 / kPackU, 256, 8);
+    const int grid = v16 ? grid_resident(c, k_gather<uint4>, n * 32 / kPackU, 256, 8)
+                         : grid_resident(c, k_gather<uint32_t>, n * 32 / kPackU, 256, 8);
     launch(c, DGNN_K_GATHER, (double)n * (2.0 * row_bytes + 4.0), [&] {
         if (v16)
             k_gather<uint4><<<grid, 256, 0, c->stream>>>((const uint8_t*)features, row_bytes, ids, n, (uint8_t*)out);

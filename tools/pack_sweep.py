@@ -50,7 +50,7 @@ def main():
     algo = R * (2 * rb + 4)
     res = {"config": args.config, "packed_rows": R, "row_bytes": rb, "algorithmic_bytes": algo, "runs": []}
     for u in (2, 4, 8):
-        for bps in (3, 4, 5, 6, 8, 12):
+        for bps in (2, 3, 4, 5, 6, 8):
             os.environ["DGNN_PACK_U"], os.environ["DGNN_PACK_BPS"] = str(u), str(bps)
             ts = []
             for r in range(args.reps + 2):
