@@ -183,6 +183,12 @@ def make_inputs(cfg_name: str, dev, num_seeds=None):
         # a bounded epoch (the first num_seeds of the same seeded permutation): for configs whose
         # whole-epoch disk tier exceeds the box's host memory (Friendster: ~300 GB of chunks)
         cfg["num_seeds"] = num_seeds
+    feat_bytes = cfg["num_nodes"] * cfg["dim"] * 4
+    if feat_bytes > 0.8 * torch.cuda.get_device_properties(dev).total_memory:
+        # IGB-shaped (409.6 GB of features): the table needs the GPU tier sharded over 8 GPUs and
+        # a host larger than this box's; bench.py replicates features per rank
+        raise SystemExit(f"bench.py: config {cfg_name!r} has {feat_bytes / 1e9:.0f} GB of features, more than "
+                         f"one GPU holds; it is a parity case only (tests/test_gpu_bigconfigs.py)")
     t = time.time()
     indptr, indices = make_graph(cfg["num_nodes"], cfg["num_edges"], cfg["degree"], cfg["skew"], 0, dev)
     seeds = make_seeds(cfg["num_nodes"], cfg["num_seeds"], 0, dev)
