@@ -529,6 +529,14 @@ def main():
                    "cuda_malloc_retries": int(torch.cuda.memory_stats(dev).get("num_device_alloc", 0))},
         "device_timeline_ms": R.timeline_ms(),
     }
+    samp_ms = sum(v["ms"] for k, v in kst.items() if k.startswith("sample") or k == "scan") / args.steps
+    if samp_ms > 0:
+        # a2-a3 rates: sampled edges (= candidates) and batch nodes per second of
+        # sampler device time (scan + sample_* kernels; the scan also serves a6's compaction)
+        result["sampling"] = {"edges_per_pass": stats0["total_edges"], "nodes_per_pass": stats0["total_nodes"],
+                              "kernel_ms_per_pass": round(samp_ms, 1),
+                              "edges_per_s": round(stats0["total_edges"] / (samp_ms / 1e3), 0),
+                              "nodes_per_s": round(stats0["total_nodes"] / (samp_ms / 1e3), 0)}
     tl = result["device_timeline_ms"]
     if tl and all("classify" in t for t in tl):
         # SURVEY 8(d) "offline batches/s" = batches / (sample + build_cache + classify + pack): the
