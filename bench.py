@@ -100,6 +100,28 @@ class Clocks:
                 "reasons": reasons, "samples": len(rows), "samples_under_load": len(load)}
 
 
+def bind_numa(local: int):
+    """Pin this rank to the CPUs NVML reports as local to its GPU, before any pinned host buffer
+    is allocated: the host tier, the disk-tier arena and the e2e inputs are then placed (first
+    touch) on the GPU's own socket, so on a multi-socket node the ranks' PCIe traffic does not
+    cross the socket link.  Best effort: no NVML, no change."""
+    if os.environ.get("DGNN_BENCH_NO_BIND") == "1":
+        return
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        idx = int(vis.split(",")[local]) if vis and vis.split(",")[0].isdigit() else local
+        h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
+        cpus = {w * 64 + b for w, m in enumerate(words) for b in range(64) if (m >> b) & 1}
+        cpus &= set(range(os.cpu_count()))
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+    except Exception:
+        pass
+
+
 def setup_dist(args):
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -108,6 +130,7 @@ def setup_dist(args):
         # test hook: several ranks on one GPU (the gpurun box has one), with gloo for the
         # collectives since NCCL refuses two ranks on one device
         local = local % torch.cuda.device_count()
+    bind_numa(local)
     if ws > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
@@ -361,7 +384,7 @@ def cpu_baseline(cfg, inp_host, n_batches: int, blocks: bool = False, train: boo
     import oracle
     indptr, indices, seeds, feats_u8 = inp_host
     B = cfg["batch_size"]
-    threads = os.cpu_count() or 1
+    threads = len(os.sched_getaffinity(0)) or 1  # the cores this process may run on (bench binds ranks to their GPU's CPUs)
     gpu_rows, host_rows = int(cfg["gpu_frac"] * cfg["num_nodes"]), int(cfg["host_frac"] * cfg["num_nodes"])
     t0 = time.time()
     S = oracle.sample(indptr, indices, seeds[: n_batches * B], B, list(cfg["fanout"]), RNG_SEED, threads=threads,
