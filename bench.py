@@ -130,7 +130,8 @@ def setup_dist(args):
         # test hook: several ranks on one GPU (the gpurun box has one), with gloo for the
         # collectives since NCCL refuses two ranks on one device
         local = local % torch.cuda.device_count()
-    bind_numa(local)
+    if args.impl != "reference":  # the reference arm is CPU work: it keeps every host core
+        bind_numa(local)
     if ws > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
