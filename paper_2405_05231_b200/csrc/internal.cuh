@@ -27,6 +27,7 @@ struct dgnn_ctx {
     int64_t launches = 0;
     int32_t sample_group = 0;
     int32_t sample_mode = DGNN_SAMPLE_NODEWISE;
+    int64_t sample_n_hint = 0;  // largest batch (nodes) of the last dgnn_sample on this ctx
     int assemble_blocks_per_sm = 8;  // grid cap for a9 (lower it to leave SMs to a concurrent pass)
     int grid_cap = 0;                // > 0: no launch of this ctx uses more CTAs (dgnn_ctx_set_grid_cap)
     // per-launch CUDA-event timing

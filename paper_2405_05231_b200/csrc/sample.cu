@@ -690,7 +690,11 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
         // counter is therefore applied after a group succeeds, over its compacted nodes.
         const int tlog_safe = tlog;
         const bool adaptive = !(std::getenv("DGNN_SAMPLE_TABLE") && std::string(std::getenv("DGNN_SAMPLE_TABLE")) == "bound");
-        int tlog_cur = tlog_safe;
+        // the largest batch of the previous call on this ctx seeds the first group's size (an
+        // epoch resamples the same workload); a wrong hint costs one redo, never a wrong result
+        int tlog_cur = (adaptive && c->sample_n_hint > 0)
+                           ? std::min(tlog_safe, std::max(4, ceil_log2(2 * c->sample_n_hint)))
+                           : tlog_safe;
         int64_t max_n_seen = 0;
         int64_t redone = 0;
         for (int64_t t0 = 0; t0 < nb;) {
@@ -883,6 +887,7 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
             used_eptr += eptr_pre[Gc];
             t0 += Gc;
         }
+        if (max_n_seen > 0) c->sample_n_hint = max_n_seen;
         if (trace) {
             const double tot = std::chrono::duration<double, std::milli>(clk::now() - t_start).count();
             t_post = tot - t_enq - t_wait;

@@ -370,3 +370,18 @@ def test_layout_host_resident_features(dg, ctx, tiny, stage):
     """Features in pinned host memory (bench.py's e2e mode, the paper's setting): tier fill and
     pack read the rows in place over PCIe; every output equals the oracle."""
     _layout_parity(dg, ctx, tiny, [10, 5], 256, 500, 1000, 8, stage, host_window=3, host_features=True)
+
+
+def test_sample_table_hint_from_a_smaller_workload(dg, tiny):
+    """The hash-set size carried between dgnn_sample calls on one ctx (the previous call's largest
+    batch) is only a hint: after a call with tiny batches, a call with batches several times larger
+    overflows the small table, redoes the group at the bound and still equals the oracle."""
+    ctx = dg.Ctx(device=0)
+    ip, ix, sd = tiny.indptr.numpy(), tiny.indices.numpy(), tiny.seeds.numpy()
+    small = oracle.sample(ip, ix, sd[:64], 16, [1], RNG_SEED)
+    S, _ = _gpu_sample(dg, ctx, ip, ix, sd[:64], 16, [1], RNG_SEED)
+    _compare_samples(S, small)
+    big = oracle.sample(ip, ix, sd, 512, [10, 10], RNG_SEED)
+    S, counts = _gpu_sample(dg, ctx, ip, ix, sd, 512, [10, 10], RNG_SEED)
+    _compare_samples(S, big)
+    assert np.array_equal(counts.cpu().numpy().view(np.uint32), oracle.count_frequencies(big, len(ip) - 1))
