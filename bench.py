@@ -110,16 +110,16 @@ def bind_numa(local: int):
     try:
         import pynvml
         pynvml.nvmlInit()
-        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
-        idx = int(vis.split(",")[local]) if vis and vis.split(",")[0].isdigit() else local
-        h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+        p = torch.cuda.get_device_properties(local)  # match by PCI address: CUDA and NVML orders may differ
+        h = pynvml.nvmlDeviceGetHandleByPciBusId(f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0")
         words = pynvml.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
         cpus = {w * 64 + b for w, m in enumerate(words) for b in range(64) if (m >> b) & 1}
         cpus &= set(range(os.cpu_count()))
         if cpus:
             os.sched_setaffinity(0, cpus)
-    except Exception:
-        pass
+            log(f"[bench] rank on GPU {local}: bound to {len(cpus)} local CPUs")
+    except Exception as ex:
+        log(f"[bench] no CPU binding ({type(ex).__name__}: {ex})")
 
 
 def setup_dist(args):
