@@ -300,6 +300,20 @@ class Runner:
                                       disk_budget_frac=self.disk_budget_frac, after_sample=after_sample,
                                       scratch_ws=self.scratch_ws, before_pack=before_pack)
 
+    def _ready(self, L):
+        """The event the assembly of pass L waits for: the end of its classify step (a6) -- the
+        tiers, address tables and per-run tables exist by then, and every run's chunks are
+        waited for piece by piece (Layout.wait_chunks) -- so the assembly streams in while the
+        later packing groups are still being packed and staged out.  With a segmented disk
+        cache (its pages are written after the packs) or DGNN_ASM_EARLY=0: the end of the layout."""
+        if L.disk_plan is None and os.environ.get("DGNN_ASM_EARLY", "1") == "1":
+            for name, ev in L.stats.get("_events", []):
+                if name == "classify":
+                    return ev
+        ev = torch.cuda.Event()
+        ev.record(self.sA)
+        return ev
+
     def _assemble(self, L, ev_l):
         """Enqueue the assembly (and trainer) of pass L on stream B after its layout; -> end event."""
         self.sB.wait_event(ev_l)
@@ -330,8 +344,7 @@ class Runner:
         mini-batches/s: the assembly then overlaps the tier fill and stage-out instead.)"""
         self.timeline = []
         L = self.layout(0)
-        ev_l = torch.cuda.Event()
-        ev_l.record(self.sA)
+        ev_l = self._ready(L)
         prev_ev = None
         last = None
         for e in range(K):
@@ -355,8 +368,7 @@ class Runner:
                     # next assembly starts on the first ones
                     pack_alone = lambda ev=ev_a: self.sA.wait_event(ev)
                 Ln = self.layout((e + 1) % 2, before_pack=pack_alone)
-                ev_l = torch.cuda.Event()
-                ev_l.record(self.sA)
+                ev_l = self._ready(Ln)
             prev_ev = ev_a
             if L is not None:
                 last = L
