@@ -120,6 +120,7 @@ class Layout:
     stats: dict = field(default_factory=dict)
     _asm_plans: dict = field(default_factory=dict)
     stage_pieces: list = field(default_factory=list)  # (b_lo, b_hi, ticket) of each stage-out copy
+    _pinned_srcs: list = field(default_factory=list)  # pinned sources of async H2D table uploads
     disk: A.DiskFile | None = None  # the disk tier as a file (stage="file")
     batch_tiers: np.ndarray = None  # [nb, 3] rows per tier (GPU, HOST, DISK) of each batch
     disk_plan: A.DiskPlan | None = None  # segmented disk cache (Sec. 5.1), when a disk budget is set
@@ -241,9 +242,14 @@ class Layout:
                 tabs.append(np.concatenate([no[b0:b1 + 1] - no[b0], dpre * self.row_bytes, dpre, chunk_off]))
             spans.append((int(no[b0]), int(no[b1]), c_lo, c_hi))
         with torch.cuda.stream(self.ctx.stream):
-            flat = torch.from_numpy(np.concatenate(tabs).astype(np.int64)).to(self.ctx.device, non_blocking=False)
+            # pinned source + async copy: the host never waits for the layout's stream here
+            src = torch.from_numpy(np.concatenate(tabs).astype(np.int64)).pin_memory()
+            flat = src.to(self.ctx.device, non_blocking=True)
+            self._pinned_srcs.append(src)  # alive as long as the layout (the copy reads it later)
+            ready = torch.cuda.Event()
+            ready.record(self.ctx.stream)  # tiers, address tables and these tables are in place
         offs = np.concatenate([[0], np.cumsum([len(t) for t in tabs])])
-        plan = (groups, spans, flat, offs)
+        plan = (groups, spans, flat, offs, ready)
         self._asm_plans[key] = plan
         return plan
 
@@ -285,9 +291,15 @@ class Layout:
         nb = self.num_batches
         if nb == 0:
             return
-        groups, spans, flat, offs = self.assembly_plan(out_budget)
+        groups, spans, flat, offs, ready = self.assembly_plan(out_budget)
         if ctx is not self.ctx:
-            ctx.stream.wait_stream(self.ctx.stream)  # tables were uploaded on the layout's stream
+            if self.disk_plan is None and (self.arena is not None or self.disk is not None):
+                # the tables were uploaded on the layout's stream after the tiers and address
+                # tables; staged chunks are waited for run by run (wait_chunks, stage-out
+                # tickets), so the assembly need not wait for the packs of later groups
+                ctx.stream.wait_event(ready)
+            else:  # chunks packed straight into HBM, or segment caches written after the packs
+                ctx.stream.wait_stream(self.ctx.stream)
         no = self.samples.node_off_host
         dev = ctx.device
         kh = self.plan.k_host
@@ -612,7 +624,11 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
     with torch.cuda.stream(ctx.stream):
         rel_all = torch.from_numpy(np.concatenate(
             [np.concatenate([po[g.b_lo:g.b_hi + 1] - po[g.b_lo], g.chunk_off]) for g in groups]
-            or [np.zeros(0, np.int64)]).astype(np.int64)).to(dev, non_blocking=False)
+            or [np.zeros(0, np.int64)]).astype(np.int64)).pin_memory()
+        # async: a blocking copy would hold the host until this stream passes the wait for the
+        # previous pass's assembly (before_pack), delaying the enqueue of the next assembly
+        rel_src, rel_all = rel_all, rel_all.to(dev, non_blocking=True)
+        L._pinned_srcs.append(rel_src)
         max_gb = max([g.group_bytes for g in groups], default=0)
         staged = arena is not None or disk is not None
         # group buffers come from the workspace when there is one: re-allocating GBs every
