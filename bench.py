@@ -293,6 +293,15 @@ class Runner:
             self.before_layout()
         c = self.counts[slot]
         c.zero_()
+        cap = int(os.environ.get("DGNN_SAMPLE_GRID_CAP", "0"))
+        if cap > 0:  # experiment: the sampler's launches on fewer CTAs (less pressure on the memory
+            self.ctxA.set_grid_cap(cap)  # system next to the assembly); the rest of the layout uncapped
+            inner = after_sample
+
+            def after_sample():
+                self.ctxA.set_grid_cap(0)
+                if inner is not None:
+                    inner()
         return self.dg.offline_layout(self.ctxA, indptr, indices, feats, seeds, cfg["fanout"], cfg["batch_size"],
                                       gpu_rows, host_rows, RNG_SEED, group_size=cfg["group_size"],
                                       batch_id_base=self.rank * self.nb, counts=c, ws=self.ws[slot],
