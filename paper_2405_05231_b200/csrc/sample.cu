@@ -43,7 +43,8 @@ struct Grp {
     int H;
     int64_t cap_n;
     int32_t* nodes;      // [G*cap_n]
-    int2* table;         // [G << tlog] {key, local}
+    int32_t* table;      // [G << tlog] keys (kEmpty = free); the insert CASes only these
+    int32_t* local;      // [G << tlog] local ID of the key in the same slot (written after the insert)
     int32_t* n;          // [G] nodes so far
     int32_t* fr_lo;      // [G]
     int32_t* fr_hi;      // [G]
@@ -65,12 +66,13 @@ __device__ __forceinline__ uint32_t slot_hash(int32_t key, int tlog) {
 }
 
 // 1 = inserted, 0 = already present, -1 = table full
-__device__ __forceinline__ int table_insert(int2* tab, int tlog, uint32_t mask, int32_t key, int32_t value) {
+__device__ __forceinline__ int table_insert(int32_t* tab, int32_t* loc, int tlog, uint32_t mask, int32_t key,
+                                            int32_t value) {
     uint32_t p = slot_hash(key, tlog);
     for (uint32_t probes = 0; probes <= mask; ++probes) {
-        const int prev = atomicCAS(&tab[p].x, kEmpty, key);
+        const int prev = atomicCAS(&tab[p], kEmpty, key);
         if (prev == kEmpty) {
-            if (value >= 0) tab[p].y = value;
+            if (value >= 0) loc[p] = value;
             return 1;
         }
         if (prev == key) return 0;
@@ -93,7 +95,8 @@ __global__ void k_seed_init(Grp g, const int32_t* __restrict__ seeds, int64_t nu
         g.hop_bound[s * (g.H + 2) + 0] = 0;
         g.hop_bound[s * (g.H + 2) + 1] = (int32_t)ns;
     }
-    int2* tab = g.table + ((int64_t)s << g.tlog);
+    int32_t* tab = g.table + ((int64_t)s << g.tlog);
+    int32_t* loc = g.local + ((int64_t)s << g.tlog);
     for (int64_t i = threadIdx.x; i < ns; i += blockDim.x) {
         const int32_t u = seeds[a + i];
         if (u < 0 || (int64_t)u >= N) {
@@ -102,7 +105,7 @@ __global__ void k_seed_init(Grp g, const int32_t* __restrict__ seeds, int64_t nu
             continue;
         }
         g.nodes[(int64_t)s * g.cap_n + i] = u;
-        const int r = table_insert(tab, g.tlog, g.tmask, u, (int32_t)i);
+        const int r = table_insert(tab, loc, g.tlog, g.tmask, u, (int32_t)i);
         if (r == 0) atomicOr(err, DEVERR_SEED_DUP);
         else if (r < 0) atomicOr(err, DEVERR_TABLE);
         else if (counts) atomicAdd(&counts[u], 1u);
@@ -311,7 +314,7 @@ __global__ void __launch_bounds__(256) k_insert(Grp g, const int32_t* __restrict
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < C; i += (int64_t)gridDim.x * blockDim.x) {
         const int s = segment_of(s_cb, g.G + 1, i);
         const int32_t u = cand[i];
-        int2* tab = g.table + ((int64_t)s << g.tlog);
+        int32_t* tab = g.table + ((int64_t)s << g.tlog);
         uint32_t p = slot_hash(u, g.tlog);
         int pos = -1;
         for (uint32_t probes = 0;; ++probes) {
@@ -319,7 +322,7 @@ __global__ void __launch_bounds__(256) k_insert(Grp g, const int32_t* __restrict
                 atomicOr(err, DEVERR_TABLE);
                 break;
             }
-            const int prev = atomicCAS(&tab[p].x, kEmpty, u);
+            const int prev = atomicCAS(&tab[p], kEmpty, u);
             if (prev == kEmpty) {
                 if (counts) atomicAdd(&counts[u], 1u);
                 pos = atomicAdd(&hist[(int64_t)s * NB + (u >> shift)], 1);
@@ -372,13 +375,13 @@ __global__ void k_bucket_sort_assign(Grp g, int64_t NB, const int64_t* __restric
         const int s = (int)(b / NB);
         const int64_t off = g.new_off[s];
         const int32_t n0 = g.n[s];
-        int2* tab = g.table + ((int64_t)s << g.tlog);
+        int32_t* loc = g.local + ((int64_t)s << g.tlog);
         int32_t* nodes = g.nodes + (int64_t)s * g.cap_n;
         for (int x = 0; x < c; ++x) {
             const unsigned long long e = a[x];
             const int32_t local = n0 + (int32_t)(lo + x - off);
             nodes[local] = (int32_t)(e >> 32);
-            tab[(uint32_t)e].y = local;
+            loc[(uint32_t)e] = local;
         }
     }
 }
@@ -392,7 +395,7 @@ __global__ void k_remap(Grp g, int32_t* __restrict__ cand, const int32_t* __rest
     const int64_t C = s_cb[g.G];
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < C; i += (int64_t)gridDim.x * blockDim.x) {
         const int s = segment_of(s_cb, g.G + 1, i);
-        cand[i] = g.table[((int64_t)s << g.tlog) + (uint32_t)ntab[i]].y;
+        cand[i] = g.local[((int64_t)s << g.tlog) + (uint32_t)ntab[i]];
     }
 }
 
@@ -609,13 +612,14 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
         // ---- group scratch ----
         DevBuf<int32_t> d_nodes, d_small32, d_hist, d_npos, d_ntab, d_fv, d_fdg;
         DevBuf<unsigned long long> d_sorted;
-        DevBuf<int2> d_table;
+        DevBuf<int32_t> d_table, d_local;
         DevBuf<int64_t> d_small64, d_bstart, d_plan, d_fst;
         std::vector<DevBuf<int32_t>> d_cand(H);
         std::vector<DevBuf<int64_t>> d_cptr(H);
         DevBuf<int64_t*> d_cptr_list;
         DGNN_TRY(d_nodes.alloc(c, (size_t)(G * cap_n)));
         DGNN_TRY(d_table.alloc(c, (size_t)(G << tlog)));
+        DGNN_TRY(d_local.alloc(c, (size_t)(G << tlog)));
         DGNN_TRY(d_small32.alloc(c, (size_t)(4 * G + G * (H + 2))));
         DGNN_TRY(d_small64.alloc(c, (size_t)(3 * (G + 1) + 2 + 2 * H * (kMaxGroup + 1))));
         DGNN_TRY(d_hist.alloc(c, (size_t)(G * hist_per_slot)));
@@ -646,6 +650,7 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
         g.cap_n = cap_n;
         g.nodes = d_nodes.p;
         g.table = d_table.p;
+        g.local = d_local.p;
         g.n = d_small32.p;
         g.fr_lo = g.n + G;
         g.fr_hi = g.fr_lo + G;
@@ -703,7 +708,7 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
             g.G = Gc;
             g.tlog = tlog_cur;
             g.tmask = (uint32_t)((1ull << tlog_cur) - 1);
-            DGNN_TRY(memset_async(c, d_table.p, 0xFF, sizeof(int2) * ((size_t)Gc << tlog_cur)));
+            DGNN_TRY(memset_async(c, d_table.p, 0xFF, sizeof(int32_t) * ((size_t)Gc << tlog_cur)));
             launch(c, DGNN_K_SAMPLE_SEED, 0.0, [&] {
                 k_seed_init<<<Gc, 256, 0, c->stream>>>(g, seeds, num_seeds, batch_size, t0, N, nullptr, c->dev_err);
             });
