@@ -16,7 +16,7 @@ import weakref
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libdgnn.so")
+LIB_PATH = os.environ.get("DGNN_LIB") or os.path.join(_PKG, "libdgnn.so")  # DGNN_LIB: A/B builds
 
 P = ctypes.c_void_p
 i32, i64, u32, u64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint64
