@@ -6,9 +6,10 @@ OUT=${OUT:-gpurun_out}
 ARGS="bench.py --steps 1 --warmup 1 --no-e2e --no-cpu"
 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_final.csv \
     python $ARGS > $OUT/ncu_bench_final.json 2> $OUT/ncu_bench_final.err
-# (regexes anchored so that k_gather<uint4> -- the tier fill -- does not match k_gather_chunks)
-for K in "k_gather_chunks" "k_pack<" "k_gather<" "k_assemble_group<"; do
-  N=$(echo "$K" | tr -d '<')
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"^$K" -s 2 -c 1 -o $OUT/prof_${N}_final -f \
+# (ncu matches the base function name, without template arguments: anchor both ends so that
+# k_gather -- the tier fill -- does not also match k_gather_chunks)
+for K in k_gather_chunks k_pack k_gather k_assemble_group; do
+  N=$K
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"^$K\$" -s 2 -c 1 -o $OUT/prof_${N}_final -f \
       python $ARGS > /dev/null 2> $OUT/prof_${N}_final.err
 done
