@@ -44,6 +44,8 @@ def test_default_contract_products():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] > 0 and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] > 0 and "clocks" in d and d["clocks"]["sm_mhz"] is not None
+    assert d["e2e"]["mode"] == "host-features"
+    assert d["offline"]["batches_per_s"] > 0 and d["sampling"]["edges_per_s"] > 0
 
 
 @pytest.mark.parametrize("flags", [["--disk-budget", "0.9", "--train"], ["--blocks", "--sequential"]])
