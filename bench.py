@@ -37,7 +37,12 @@ import tempfile
 import time
 
 import numpy as np
-import torch
+
+# The caching allocator maps physical pages into growable segments instead of carving fixed
+# cudaMalloc blocks: the per-pass buffers of two in-flight passes (samples, window staging,
+# group buffers) then do not fragment HBM (read before torch's first CUDA allocation)
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
+import torch  # noqa: E402
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -198,6 +203,22 @@ def pcie_bandwidth(dev, nbytes: int = 1 << 30) -> dict:
     del d
     hb.free()
     return out
+
+
+HBM_BUDGET_GB = float(os.environ.get("DGNN_HBM_BUDGET_GB", "165"))  # the bench's own HBM ceiling (reserved)
+
+
+def memory_report(dev, R) -> dict:
+    """Caching-allocator peaks over the whole run (first pass included) against the HBM budget."""
+    st = torch.cuda.memory_stats(dev)
+    reserved = torch.cuda.max_memory_reserved(dev)
+    return {"max_reserved_gb": round(reserved / 1e9, 1),
+            "max_allocated_gb": round(torch.cuda.max_memory_allocated(dev) / 1e9, 1),
+            "budget_gb": HBM_BUDGET_GB, "within_budget": reserved <= HBM_BUDGET_GB * 1e9,
+            "device_total_gb": round(torch.cuda.get_device_properties(dev).total_memory / 1e9, 1),
+            "kept_by_ctx_gb": round(sum(c.kept_bytes() for c in R.ctxs()) / 1e9, 2),
+            "alloc_retries": int(st.get("num_alloc_retries", 0)), "ooms": int(st.get("num_ooms", 0)),
+            "allocator": os.environ.get("PYTORCH_CUDA_ALLOC_CONF", "")}
 
 
 def make_inputs(cfg_name: str, dev, num_seeds=None):
@@ -380,6 +401,10 @@ class Runner:
                     pack_alone = lambda ev=ev_a: self.sA.wait_event(ev)
                 Ln = self.layout((e + 1) % 2, before_pack=pack_alone)
                 ev_l = self._ready(Ln)
+                if os.environ.get("DGNN_MEM_TRACE") == "1":  # allocator counters (host side, no sync)
+                    log(f"[mem] pass {e + 1}: allocated {torch.cuda.memory_allocated(self.dev) / 1e9:.1f} GB, "
+                        f"reserved {torch.cuda.memory_reserved(self.dev) / 1e9:.1f} GB, kept "
+                        f"{sum(c.kept_bytes() for c in self.ctxs()) / 1e9:.1f} GB")
             prev_ev = ev_a
             if L is not None:
                 last = L
@@ -402,13 +427,24 @@ class Runner:
         return out
 
 
-def cpu_baseline(cfg, inp_host, n_batches: int, blocks: bool = False, train: bool = False):
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def cpu_baseline(cfg, inp_host, n_batches: int, blocks: bool = False, train: bool = False, threads: int = 0):
     """The oracle as it stands, on a bounded sample: the first n_batches batches of rank 0's epoch
-    (with the same sampling variant and, if the GPU arm trains, the trainer stub)."""
+    (with the same sampling variant and, if the GPU arm trains, the trainer stub).  threads = 0:
+    every core this process may run on (bench binds ranks to their GPU's CPUs)."""
     import oracle
     indptr, indices, seeds, feats_u8 = inp_host
     B = cfg["batch_size"]
-    threads = len(os.sched_getaffinity(0)) or 1  # the cores this process may run on (bench binds ranks to their GPU's CPUs)
+    threads = threads or len(os.sched_getaffinity(0)) or 1
     gpu_rows, host_rows = int(cfg["gpu_frac"] * cfg["num_nodes"]), int(cfg["host_frac"] * cfg["num_nodes"])
     t0 = time.time()
     S = oracle.sample(indptr, indices, seeds[: n_batches * B], B, list(cfg["fanout"]), RNG_SEED, threads=threads,
@@ -427,7 +463,9 @@ def cpu_baseline(cfg, inp_host, n_batches: int, blocks: bool = False, train: boo
             oracle.train_stub(s, rows.view(np.float32))
     dt = time.time() - t0
     return {"value": len(S) / dt, "unit": "mini-batches/s", "cores": threads, "kind": "oracle",
-            "sample": f"first {len(S)} batches of the {cfg['batch_size']}-seed epoch: sample (OpenMP over batches), "
+            "cpu_model": cpu_model(),
+            "sample": f"first {len(S)} batches of the {cfg['batch_size']}-seed epoch: sample "
+                      f"({'OpenMP over batches' if threads > 1 else 'one thread'}), "
                       f"count, full-N tier select on their counts, classify, pack, tier gather, direct-gather "
                       f"assembly{' + trainer stub' if train else ''}{' (DGL blocks)' if blocks else ''}; {dt:.1f}s"}
 
@@ -509,8 +547,10 @@ def main():
     ms = e0.elapsed_time(e1)
     kst = {}
     per_stream = {}
+    per_stream_stats = {}
     for name, c in zip(("layout", "assemble", "host_gather", "train"), R.ctxs()):
         st = c.kernel_stats()
+        per_stream_stats[name] = st
         per_stream[name] = round(sum(v["ms"] for v in st.values()) / args.steps, 2)
         for k, v in st.items():
             d = kst.setdefault(k, {"launches": 0, "ms": 0.0, "bytes": 0.0})
@@ -532,10 +572,35 @@ def main():
             traffic = json.load(open(prof)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    kernels = {k: {"ms_per_step": round(v["ms"] / args.steps, 3), "launches_per_step": v["launches"] // args.steps,
-                   "share_of_step": round(v["ms"] / ms, 4) if ms else None,
-                   **({"gbs": round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 1)} if v["bytes"] and v["ms"] else {})}
-               for k, v in kst.items() if v["launches"]}
+    pcie = pcie_bandwidth(dev)
+    rb = stats0.get("row_bytes", cfg["dim"] * 4)
+    gathered_rows = int(R.pcie_rows.item())
+    # per stream: every kernel family runs on one stream, so its share of the step is its
+    # summed launch time over the step time on that stream (<= 1; streams overlap each other)
+    kernels = {}
+    for sname, st in per_stream_stats.items():
+        fams = {}
+        for k, v in st.items():
+            if not v["launches"]:
+                continue
+            d = {"ms_per_step": round(v["ms"] / args.steps, 3), "launches_per_step": v["launches"] // args.steps,
+                 "share_of_step": round(v["ms"] / ms, 4) if ms else None}
+            if k == "tier_gather_pcie" and v["bytes"] and v["ms"]:
+                # the host-tier fill: SM stores into pinned host memory (D2H); with the table in
+                # pinned memory (e2e) also the UVA reads of the GPU-tier fill
+                g = v["bytes"] / (v["ms"] / 1e3) / 1e9
+                d.update(gbs=round(g, 1), bound="pcie", peak=round(pcie["d2h_gbs"], 1),
+                         frac=round(g / pcie["d2h_gbs"], 4))
+            elif k == "host_gather" and v["ms"] > 0:
+                # PCIe-bound UVA reads of the window's host-tier rows (bytes counted on the device)
+                g = gathered_rows * rb / (v["ms"] / 1e3) / 1e9
+                d.update(gbs=round(g, 1), bound="pcie", peak=round(pcie["h2d_gbs"], 1),
+                         frac=round(g / pcie["h2d_gbs"], 4))
+            elif v["bytes"] and v["ms"]:
+                g = v["bytes"] / (v["ms"] / 1e3) / 1e9
+                d.update(gbs=round(g, 1), bound="hbm", peak=hbm_peak, frac=round(g / hbm_peak, 4))
+            fams[k] = d
+        kernels[sname] = fams
     result = {
         "metric": METRIC, "value": round(value, 2), "unit": "mini-batches/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 2), "higher_is_better": True,
@@ -570,10 +635,7 @@ def main():
         "clocks": clocks,
         "gpu_launches": int(launches),
         "kernel_ms_per_step_by_stream": per_stream,
-        "memory": {"max_reserved_gb": round(torch.cuda.max_memory_reserved(dev) / 1e9, 1),
-                   "max_allocated_gb": round(torch.cuda.max_memory_allocated(dev) / 1e9, 1),
-                   "alloc_retries": int(torch.cuda.memory_stats(dev).get("num_alloc_retries", 0)),
-                   "cuda_malloc_retries": int(torch.cuda.memory_stats(dev).get("num_device_alloc", 0))},
+        "memory": memory_report(dev, R),
         "device_timeline_ms": R.timeline_ms(),
     }
     samp_ms = sum(v["ms"] for k, v in kst.items() if k.startswith("sample") or k == "scan") / args.steps
@@ -595,13 +657,10 @@ def main():
                              "note": "a1-a8 per pass (sample, count all-reduce, tier select, tier fill, classify, "
                                      "pack); pipelined runs share the GPU with the previous pass's assembly"}
     if asm["ms"] > 0:
-        result["assemble_gbs"] = round(asm["bytes"] / (asm["ms"] / 1e3) / 1e9, 1)
         # the step's own roofline: it is bound by the PCIe host->device link, which carries the
         # host-tier rows gathered per window plus the disk-tier chunks staged back in; measured
         # against the pinned H2D cudaMemcpy bandwidth of this box, over the whole step
-        pcie = pcie_bandwidth(dev)
-        rb = stats0.get("row_bytes", cfg["dim"] * 4)
-        gathered = int(R.pcie_rows.item()) * rb / args.steps
+        gathered = gathered_rows * rb / args.steps
         staged_in = stats0["chunk_bytes"] + 4096 * stats0.get("disk_cache", {}).get("requests", 0)
         h2d = gathered + staged_in
         h2d_gbs = h2d / (ms_max / args.steps / 1e3) / 1e9
@@ -689,9 +748,13 @@ def main():
     if not args.no_cpu and rank == 0 and ws == 1:
         h_indptr, h_indices, h_seeds, h_feats = inp_host
         try:
-            result["cpu_baseline"] = cpu_baseline(cfg, (h_indptr.numpy(), h_indices.numpy(), h_seeds.numpy(),
-                                                        h_feats.numpy().view(np.uint8).reshape(N, -1)),
-                                                  min(args.cpu_batches, nb), blocks=args.blocks, train=args.train)
+            hin = (h_indptr.numpy(), h_indices.numpy(), h_seeds.numpy(), h_feats.numpy().view(np.uint8).reshape(N, -1))
+            cb = cpu_baseline(cfg, hin, min(args.cpu_batches, nb), blocks=args.blocks, train=args.train)
+            # the 1-thread time beside the all-cores one (a smaller sample)
+            one = cpu_baseline(cfg, hin, min(max(args.cpu_batches // 8, 1), nb), blocks=args.blocks,
+                               train=args.train, threads=1)
+            cb["one_thread"] = {"value": one["value"], "unit": one["unit"], "cores": 1, "sample": one["sample"]}
+            result["cpu_baseline"] = cb
         except Exception as ex:  # the baseline is reported, never required
             result["cpu_baseline"] = {"value": None, "error": str(ex)[:200]}
     if rank == 0:
@@ -738,4 +801,11 @@ def reference_arm(args, ws, rank, dev):
 
 
 if __name__ == "__main__":
-    main()
+    _hist = os.environ.get("DGNN_MEM_HISTORY")  # diagnostics: dump the allocator history
+    if _hist:
+        torch.cuda.memory._record_memory_history(max_entries=100000, stacks="python")
+    try:
+        main()
+    finally:
+        if _hist:
+            torch.cuda.memory._dump_snapshot(_hist)

@@ -83,6 +83,9 @@ typedef enum {
     DGNN_K_DISK_PLAN,       /* segmented disk cache: groups, MinHash, pages, addresses  */
     DGNN_K_DISK_GATHER,     /* segmented disk cache: page fill, partial input           */
     DGNN_K_TRAIN,           /* trainer stub (mean aggregation per sampled hop)          */
+    DGNN_K_HOST_WINDOW,     /* a9: marking a host window's distinct host-tier rows      */
+    DGNN_K_HOST_GATHER,     /* a9: PCIe gather of a window's host rows into HBM staging */
+    DGNN_K_GATHER_PCIE,     /* a7: tier gather from / into pinned host memory (PCIe)   */
     DGNN_K_NUM
 } dgnn_kernel_id;
 
@@ -137,6 +140,19 @@ dgnn_status dgnn_ctx_set_assemble_occupancy(dgnn_ctx* ctx, int32_t blocks_per_sm
  * PCIe-bound UVA gathers next to latency-bound work on other streams: a few SMs' worth of
  * outstanding host reads already saturate PCIe, more only queue up in the memory system. */
 dgnn_status dgnn_ctx_set_grid_cap(dgnn_ctx* ctx, int32_t max_blocks);
+/* HBM footprint controls.  The ctx recycles the large buffers every dgnn_sample call needs
+ * (the output arenas of a dgnn_samples released with dgnn_samples_free, and the sampler's
+ * group scratch): they are kept by the ctx, up to `bytes` in total (default 24 GiB; 0 = keep
+ * nothing), and handed to the next call instead of being freed and re-allocated, so repeated
+ * offline passes settle on a fixed footprint.  Kept buffers are released by a lower limit, by
+ * an allocation that would otherwise fail, and by dgnn_ctx_destroy.  dgnn_ctx_kept_bytes
+ * reports the bytes currently kept. */
+dgnn_status dgnn_ctx_set_keep_limit(dgnn_ctx* ctx, int64_t bytes);
+int64_t dgnn_ctx_kept_bytes(const dgnn_ctx* ctx);
+/* Budget (bytes, >= 16 MiB; default 3 GiB) of the sampler's per-group scratch: the number of
+ * batches sampled concurrently (when dgnn_ctx_set_sample_group is 0) is the largest that fits
+ * it, at most 64.  Results do not depend on it. */
+dgnn_status dgnn_ctx_set_sample_budget(dgnn_ctx* ctx, int64_t bytes);
 int64_t dgnn_ctx_launches(const dgnn_ctx* ctx);
 dgnn_status dgnn_ctx_set_timing(dgnn_ctx* ctx, int enable);
 typedef struct {

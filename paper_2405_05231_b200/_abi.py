@@ -27,7 +27,8 @@ TIER_GPU, TIER_HOST, TIER_DISK = 0, 1, 2
 TIER_SHIFT = 30
 SLOT_MASK = (1 << TIER_SHIFT) - 1
 KERNELS = ["scan", "sample_seed", "sample_hop", "sample_order", "sample_remap", "sample_compact", "sample_setup",
-           "cache_hist", "cache_select", "classify", "pack_gather", "tier_gather", "assemble", "misc", "sort", "disk_plan", "disk_gather", "train"]
+           "cache_hist", "cache_select", "classify", "pack_gather", "tier_gather", "assemble", "misc", "sort", "disk_plan", "disk_gather", "train",
+           "host_window", "host_gather", "tier_gather_pcie"]
 K = {name: i for i, name in enumerate(KERNELS)}
 
 # every symbol include/dgnn.h declares (checked by tests/test_abi_symbols.py)
@@ -45,6 +46,7 @@ EXPORTS = [
     "dgnn_disk_plan_get_info", "dgnn_disk_plan_free", "dgnn_disk_cache_fill", "dgnn_disk_partial",
     "dgnn_train_stub", "dgnn_stage_file_read_pages", "dgnn_host_window_runs", "dgnn_gather_runs_dev", "dgnn_ctx_set_sample_mode", "dgnn_ctx_set_grid_cap", "dgnn_assemble_group_peer", "dgnn_device_alloc",
     "dgnn_device_free", "dgnn_ipc_handle", "dgnn_ipc_open", "dgnn_ipc_close", "dgnn_disk_index_partition_counts", "dgnn_pack_partition", "dgnn_pack_tails",
+    "dgnn_ctx_set_keep_limit", "dgnn_ctx_kept_bytes", "dgnn_ctx_set_sample_budget",
 ]
 
 
@@ -113,6 +115,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "dgnn_ctx_sync": (i32, [P]),
             "dgnn_last_error": (ctypes.c_char_p, []),
             "dgnn_ctx_set_sample_group": (i32, [P, i32]),
+            "dgnn_ctx_set_keep_limit": (i32, [P, i64]),
+            "dgnn_ctx_kept_bytes": (i64, [P]),
+            "dgnn_ctx_set_sample_budget": (i32, [P, i64]),
             "dgnn_ctx_launches": (i64, [P]),
             "dgnn_ctx_set_timing": (i32, [P, ctypes.c_int]),
             "dgnn_ctx_kernel_stats": (i32, [P, i32, ctypes.POINTER(_KStat)]),
@@ -219,6 +224,23 @@ class _DevView:
                                          "stream": None}
 
 
+class _Handle:
+    """Owns one library handle.  The zero-copy views of a result reference this object, not the
+    Python wrapper that stores them: wrapper -> views -> handle has no reference cycle, so the
+    library memory is released as soon as the wrapper and its views are dropped, not at the next
+    full cyclic garbage collection (which let whole epochs of samples pile up in HBM)."""
+
+    def __init__(self, free_fn, handle, ctx=None):
+        self.handle = handle
+        # the ctx is an argument of the finalizer: it outlives every result allocated through it
+        self.free = weakref.finalize(self, free_fn, handle) if ctx is None else \
+            weakref.finalize(self, _free_with_ctx, free_fn, handle, ctx)
+
+
+def _free_with_ctx(free_fn, handle, ctx):
+    free_fn(handle)
+
+
 def _view(ptr: int, n: int, dtype, owner, device) -> torch.Tensor:
     if n == 0:
         return torch.empty(0, dtype=dtype, device=device)
@@ -301,6 +323,17 @@ class Ctx:
     def set_sample_group(self, batches: int):
         _check(load_library().dgnn_ctx_set_sample_group(self.handle, int(batches)), "dgnn_ctx_set_sample_group")
 
+    def set_keep_limit(self, nbytes: int):
+        """Bytes of recycled sample arenas / sampler scratch the ctx may keep (dgnn_ctx_set_keep_limit)."""
+        _check(load_library().dgnn_ctx_set_keep_limit(self.handle, int(nbytes)), "dgnn_ctx_set_keep_limit")
+
+    def kept_bytes(self) -> int:
+        return int(load_library().dgnn_ctx_kept_bytes(self.handle))
+
+    def set_sample_budget(self, nbytes: int):
+        """Scratch budget of one sampling group (dgnn_ctx_set_sample_budget)."""
+        _check(load_library().dgnn_ctx_set_sample_budget(self.handle, int(nbytes)), "dgnn_ctx_set_sample_budget")
+
     def set_grid_cap(self, max_blocks: int):
         """Cap every grid this ctx launches (0 = none); see dgnn_ctx_set_grid_cap."""
         _check(load_library().dgnn_ctx_set_grid_cap(self.handle, int(max_blocks)), "dgnn_ctx_set_grid_cap")
@@ -322,7 +355,8 @@ class Samples:
         L = load_library()
         self.ctx = ctx
         self.handle = handle
-        self._finalizer = weakref.finalize(self, L.dgnn_samples_free, handle)
+        self._owner = _Handle(L.dgnn_samples_free, handle, ctx)
+        self._finalizer = self._owner.free
         info = _SamplesInfo()
         _check(L.dgnn_samples_get_info(handle, ctypes.byref(info)), "dgnn_samples_get_info")
         self.num_batches = int(info.num_batches)
@@ -332,13 +366,13 @@ class Samples:
         self.total_edges = int(info.total_edges)
         nb, H = self.num_batches, self.num_hops
         dev = ctx.device
-        self.node_off = _view(info.node_off, nb + 1, torch.int64, self, dev)
-        self.nodes = _view(info.nodes, self.total_nodes, torch.int32, self, dev)
-        self.hop_off = _view(info.hop_off, nb * (H + 2), torch.int32, self, dev)
-        self.eptr_off = _view(info.eptr_off, nb + 1, torch.int64, self, dev)
-        self.eptr = _view(info.eptr, int(info.total_eptr), torch.int32, self, dev)
-        self.edge_off = _view(info.edge_off, nb + 1, torch.int64, self, dev)
-        self.src_local = _view(info.src_local, self.total_edges, torch.int32, self, dev)
+        self.node_off = _view(info.node_off, nb + 1, torch.int64, self._owner, dev)
+        self.nodes = _view(info.nodes, self.total_nodes, torch.int32, self._owner, dev)
+        self.hop_off = _view(info.hop_off, nb * (H + 2), torch.int32, self._owner, dev)
+        self.eptr_off = _view(info.eptr_off, nb + 1, torch.int64, self._owner, dev)
+        self.eptr = _view(info.eptr, int(info.total_eptr), torch.int32, self._owner, dev)
+        self.edge_off = _view(info.edge_off, nb + 1, torch.int64, self._owner, dev)
+        self.src_local = _view(info.src_local, self.total_edges, torch.int32, self._owner, dev)
         self.node_off_host = _host_array(info.node_off_host, nb + 1, ctypes.c_int64)
         self.edge_off_host = _host_array(info.edge_off_host, nb + 1, ctypes.c_int64)
         self.eptr_off_host = _host_array(info.eptr_off_host, nb + 1, ctypes.c_int64)
@@ -378,7 +412,8 @@ class CachePlan:
         L = load_library()
         self.ctx = ctx
         self.handle = handle
-        self._finalizer = weakref.finalize(self, L.dgnn_cache_plan_free, handle)
+        self._owner = _Handle(L.dgnn_cache_plan_free, handle, ctx)
+        self._finalizer = self._owner.free
         info = _PlanInfo()
         _check(L.dgnn_cache_plan_get_info(handle, ctypes.byref(info)), "dgnn_cache_plan_get_info")
         self.num_nodes = int(info.num_nodes)
@@ -387,9 +422,9 @@ class CachePlan:
         self.gpu_min_count = int(info.gpu_min_count)
         self.host_min_count = int(info.host_min_count)
         dev = ctx.device
-        self.tier_map = _view(info.tier_map, self.num_nodes, torch.int32, self, dev)
-        self.gpu_ids = _view(info.gpu_ids, self.k_gpu, torch.int32, self, dev)
-        self.host_ids = _view(info.host_ids, self.k_host, torch.int32, self, dev)
+        self.tier_map = _view(info.tier_map, self.num_nodes, torch.int32, self._owner, dev)
+        self.gpu_ids = _view(info.gpu_ids, self.k_gpu, torch.int32, self._owner, dev)
+        self.host_ids = _view(info.host_ids, self.k_host, torch.int32, self._owner, dev)
 
 
 def dgnn_build_cache(ctx: Ctx, counts: torch.Tensor, gpu_rows: int, host_rows: int) -> CachePlan:
@@ -614,7 +649,8 @@ class DiskPlan:
         L = load_library()
         self.ctx = ctx
         self.handle = handle
-        self._finalizer = weakref.finalize(self, L.dgnn_disk_plan_free, handle)
+        self._owner = _Handle(L.dgnn_disk_plan_free, handle, ctx)
+        self._finalizer = self._owner.free
         info = _DiskPlanInfo()
         _check(L.dgnn_disk_plan_get_info(handle, ctypes.byref(info)), "dgnn_disk_plan_get_info")
         for n in ("nb", "nseg", "s", "m", "fpp", "row_bytes", "n_cache", "n_packed", "n_req", "space_pages",
@@ -622,14 +658,14 @@ class DiskPlan:
             setattr(self, n, int(getattr(info, n)))
         dev = ctx.device
         nb, nseg = self.nb, self.nseg
-        self.seg_off = _view(info.seg_off, nseg + 1, torch.int64, self, dev)
-        self.cache_ids = _view(info.cache_ids, self.n_cache, torch.int32, self, dev)
-        self.seg_page_off = _view(info.seg_page_off, nseg + 1, torch.int64, self, dev)
-        self.pk_ids = _view(info.pk_ids, self.n_packed, torch.int32, self, dev)
-        self.pk_off = _view(info.pk_off, nb + 1, torch.int64, self, dev)
-        self.req_pages = _view(info.req_pages, self.n_req, torch.int32, self, dev)
-        self.req_off = _view(info.req_off, nb + 1, torch.int64, self, dev)
-        self.dc_addr = _view(info.dc_addr, R, torch.uint32, self, dev)
+        self.seg_off = _view(info.seg_off, nseg + 1, torch.int64, self._owner, dev)
+        self.cache_ids = _view(info.cache_ids, self.n_cache, torch.int32, self._owner, dev)
+        self.seg_page_off = _view(info.seg_page_off, nseg + 1, torch.int64, self._owner, dev)
+        self.pk_ids = _view(info.pk_ids, self.n_packed, torch.int32, self._owner, dev)
+        self.pk_off = _view(info.pk_off, nb + 1, torch.int64, self._owner, dev)
+        self.req_pages = _view(info.req_pages, self.n_req, torch.int32, self._owner, dev)
+        self.req_off = _view(info.req_off, nb + 1, torch.int64, self._owner, dev)
+        self.dc_addr = _view(info.dc_addr, R, torch.uint32, self._owner, dev)
         self.pk_off_host = _host_array(info.pk_off_host, nb + 1, ctypes.c_int64)
         self.req_off_host = _host_array(info.req_off_host, nb + 1, ctypes.c_int64)
         self.seg_off_host = _host_array(info.seg_off_host, nseg + 1, ctypes.c_int64)

@@ -160,10 +160,10 @@ struct Row {
 template <class V>
 __global__ void __launch_bounds__(256, 6) k_gather_dev(const uint8_t* __restrict__ src, int64_t row_bytes,
                                                     const int32_t* __restrict__ ids, const int64_t* __restrict__ n_dev,
-                                                    uint8_t* __restrict__ dst) {
+                                                    int64_t n_max, uint8_t* __restrict__ dst) {
     const int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    copy_rows_warp<kAsmU, V>(*n_dev, row_bytes, Row{src, row_bytes, ids, dst}, warp, nwarps);
+    copy_rows_warp<kAsmU, V>(min(*n_dev, n_max), row_bytes, Row{src, row_bytes, ids, dst}, warp, nwarps);
 }
 
 // Staging gather of a window's host rows (PCIe-bound): each warp owns a chunk of
@@ -173,15 +173,20 @@ __global__ void __launch_bounds__(256, 6) k_gather_dev(const uint8_t* __restrict
 // slots (runs) come out as contiguous requests without any run bookkeeping, and a
 // dense window (every slot, as on Friendster-shaped bounded epochs) is split evenly
 // over the warps.
+__global__ void k_check_count(const int64_t* count, int64_t capacity, int* err) {
+    if (*count > capacity) atomicOr(err, DEVERR_OVERFLOW);
+}
+
 constexpr int kGatherCH = 8;
 constexpr int kGatherV = 8;
 __global__ void __launch_bounds__(256) k_gather_chunks(const uint8_t* __restrict__ src, int64_t row_bytes,
                                                        const int32_t* __restrict__ ids,
-                                                       const int64_t* __restrict__ n_dev, uint8_t* __restrict__ dst) {
+                                                       const int64_t* __restrict__ n_dev, int64_t n_max,
+                                                       uint8_t* __restrict__ dst) {
     const int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
     const int lane = threadIdx.x & 31;
-    const int64_t n = *n_dev;
+    const int64_t n = min(*n_dev, n_max);  // never past the caller's list / output capacity
     const int vpr = (int)(row_bytes >> 4);
     for (int64_t p0 = warp * kGatherCH; p0 < n; p0 += nwarps * kGatherCH) {
         const int rows = (int)(n - p0 < kGatherCH ? n - p0 : kGatherCH);
@@ -244,7 +249,7 @@ extern "C" dgnn_status dgnn_host_window(dgnn_ctx* c, const uint32_t* addr, int64
     if (n == 0 || k_host == 0) return DGNN_OK;
     // mark the window's host slots, then list them in ascending slot order with one scan
     // over the host tier: the staging gather then walks host memory in address order
-    launch(c, DGNN_K_ASSEMBLE, 0.0, [&] {
+    launch(c, DGNN_K_HOST_WINDOW, 0.0, [&] {
         k_host_mark<<<grid_for(c, n, 256, 8), 256, 0, c->stream>>>(addr, n, window_id, stamp, k_host);
     });
     DGNN_CK_LAUNCH();
@@ -258,6 +263,10 @@ extern "C" dgnn_status dgnn_host_window(dgnn_ctx* c, const uint32_t* addr, int64
         }
     };
     DGNN_TRY(scan::run(c, k_host, nullptr, in, outf, count));
+    // a window with more distinct host rows than the list holds: only `capacity` were listed
+    // (the gathers clamp to their n_max); reported as DGNN_ECUDA "capacity overflow" at the next sync
+    launch(c, DGNN_K_HOST_WINDOW, 0.0, [&] { k_check_count<<<1, 1, 0, c->stream>>>(count, capacity, c->dev_err); });
+    DGNN_CK_LAUNCH();
     return DGNN_OK;
 }
 
@@ -323,7 +332,7 @@ extern "C" dgnn_status dgnn_gather_runs_dev(dgnn_ctx* c, const void* src, int64_
     if (max_runs == 0) return DGNN_OK;
     DGNN_CK(cudaSetDevice(c->device));
     const int grid = grid_resident(c, k_gather_runs, max_runs * 32, 256, c->assemble_blocks_per_sm);
-    launch(c, DGNN_K_ASSEMBLE, 0.0, [&] {
+    launch(c, DGNN_K_HOST_GATHER, 0.0, [&] {
         k_gather_runs<<<grid, 256, 0, c->stream>>>((const uint8_t*)src, row_bytes, list, count, runs, run_count,
                                                    (uint8_t*)out);
     });
@@ -342,13 +351,13 @@ extern "C" dgnn_status dgnn_gather_rows_dev(dgnn_ctx* c, const void* features, i
                                          c->assemble_blocks_per_sm)
                          : grid_resident(c, k_gather_dev<uint32_t>, n_max * 32 / kAsmU, 256,
                                          c->assemble_blocks_per_sm);
-    launch(c, DGNN_K_ASSEMBLE, 0.0, [&] {
+    launch(c, DGNN_K_HOST_GATHER, 0.0, [&] {
         if (v16)
-            k_gather_chunks<<<grid, 256, 0, c->stream>>>((const uint8_t*)features, row_bytes, ids, n_dev,
+            k_gather_chunks<<<grid, 256, 0, c->stream>>>((const uint8_t*)features, row_bytes, ids, n_dev, n_max,
                                                          (uint8_t*)out);
         else
             k_gather_dev<uint32_t><<<grid, 256, 0, c->stream>>>((const uint8_t*)features, row_bytes, ids, n_dev,
-                                                                (uint8_t*)out);
+                                                                n_max, (uint8_t*)out);
     });
     DGNN_CK_LAUNCH();
     return DGNN_OK;

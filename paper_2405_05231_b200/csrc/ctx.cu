@@ -36,6 +36,49 @@ void dev_free(dgnn_ctx* c, void* p, size_t bytes) {
     else cudaFreeAsync(p, c->stream);
 }
 
+void* keep_take(dgnn_ctx* c, size_t need, size_t* got) {
+    if (need == 0) need = 1;
+    int best = -1;
+    for (int i = 0; i < (int)c->kept.size(); ++i) {
+        const size_t b = c->kept[i].bytes;
+        if (b >= need && b <= 2 * need + ((size_t)256 << 20) && (best < 0 || b < c->kept[best].bytes)) best = i;
+    }
+    if (best >= 0) {
+        void* p = c->kept[best].p;
+        *got = c->kept[best].bytes;
+        c->kept_bytes -= *got;
+        c->kept.erase(c->kept.begin() + best);
+        return p;
+    }
+    void* p = dev_alloc(c, need);
+    if (!p) {
+        // the kept buffers are the first thing to give back under memory pressure
+        keep_trim(c, 0);
+        p = dev_alloc(c, need);
+    }
+    *got = p ? need : 0;
+    return p;
+}
+
+void keep_trim(dgnn_ctx* c, size_t limit) {
+    while (!c->kept.empty() && c->kept_bytes > limit) {
+        dev_free(c, c->kept.front().p, c->kept.front().bytes);
+        c->kept_bytes -= c->kept.front().bytes;
+        c->kept.erase(c->kept.begin());
+    }
+}
+
+void keep_put(dgnn_ctx* c, void* p, size_t bytes) {
+    if (!p) return;
+    if (bytes > c->kept_limit) {
+        dev_free(c, p, bytes);
+        return;
+    }
+    c->kept.push_back({p, bytes});
+    c->kept_bytes += bytes;
+    keep_trim(c, c->kept_limit);
+}
+
 cudaEvent_t take_event(dgnn_ctx* c) {
     if (!c->event_pool.empty()) {
         cudaEvent_t e = c->event_pool.back();
@@ -169,6 +212,7 @@ void dgnn_ctx_destroy(dgnn_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->side) cudaStreamSynchronize(c->side);
     fold_pending(c, false);
+    keep_trim(c, 0);
     for (auto e : c->event_pool) cudaEventDestroy(e);
     for (int i = 0; i < dgnn_ctx::kStageRing; ++i)
         if (c->stage_ev[i]) cudaEventDestroy(c->stage_ev[i]);
@@ -205,6 +249,22 @@ dgnn_status dgnn_ctx_sync(dgnn_ctx* c) {
 dgnn_status dgnn_ctx_set_sample_group(dgnn_ctx* c, int32_t batches) {
     DGNN_REQUIRE(c && batches >= 0 && batches <= 1024, "dgnn_ctx_set_sample_group: bad argument");
     c->sample_group = batches;
+    return DGNN_OK;
+}
+
+dgnn_status dgnn_ctx_set_keep_limit(dgnn_ctx* c, int64_t bytes) {
+    DGNN_REQUIRE(c && bytes >= 0, "dgnn_ctx_set_keep_limit: bad argument");
+    DGNN_CK(cudaSetDevice(c->device));
+    c->kept_limit = (size_t)bytes;
+    keep_trim(c, c->kept_limit);
+    return DGNN_OK;
+}
+
+int64_t dgnn_ctx_kept_bytes(const dgnn_ctx* c) { return c ? (int64_t)c->kept_bytes : 0; }
+
+dgnn_status dgnn_ctx_set_sample_budget(dgnn_ctx* c, int64_t bytes) {
+    DGNN_REQUIRE(c && bytes >= ((int64_t)16 << 20), "dgnn_ctx_set_sample_budget: budget below 16 MiB");
+    c->sample_budget = (size_t)bytes;
     return DGNN_OK;
 }
 
@@ -261,7 +321,8 @@ const char* dgnn_kernel_name(int32_t kid) {
                                             "sample_remap",   "sample_compact", "sample_setup", "cache_hist",
                                             "cache_select",   "classify",      "pack_gather",   "tier_gather",
                                             "assemble",       "misc",          "sort",          "disk_plan",
-                                            "disk_gather",   "train"};
+                                            "disk_gather",   "train",
+                                            "host_window",    "host_gather",   "tier_gather_pcie"};
     return (kid >= 0 && kid < DGNN_K_NUM) ? names[kid] : "?";
 }
 

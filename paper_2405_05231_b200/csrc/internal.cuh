@@ -52,6 +52,17 @@ struct dgnn_ctx {
     void* pinned = nullptr;
     size_t pinned_bytes = 0;
     int* pinned_err = nullptr;  // check_dev_err's read-back word
+    // recycled device buffers (keep_take / keep_put): the sample arenas and the sampler's group
+    // scratch of one call are handed to the next call on the same ctx instead of going back to
+    // the allocator, so a steady stream of offline passes reaches a fixed HBM footprint
+    struct Kept {
+        void* p;
+        size_t bytes;
+    };
+    std::vector<Kept> kept;
+    size_t kept_bytes = 0;
+    size_t kept_limit = (size_t)24 << 30;      // dgnn_ctx_set_keep_limit
+    size_t sample_budget = (size_t)3 << 30;    // sampler group scratch budget (dgnn_ctx_set_sample_budget)
 };
 
 namespace dgnn {
@@ -92,6 +103,13 @@ dgnn_status cuda_fail(cudaError_t e, const char* what, const char* file, int lin
 // ------------------------------------------------------------- allocation
 void* dev_alloc(dgnn_ctx* c, size_t bytes);
 void dev_free(dgnn_ctx* c, void* p, size_t bytes);
+// The smallest kept buffer of >= need bytes (and not more than 2 x need + 256 MiB), else a fresh
+// allocation of exactly need bytes; *got = the buffer's size.  NULL on allocation failure.
+void* keep_take(dgnn_ctx* c, size_t need, size_t* got);
+// Hand a buffer back to the ctx for reuse (stream-ordered on the ctx stream like dev_free);
+// beyond the ctx's kept-bytes limit the oldest kept buffers are freed.
+void keep_put(dgnn_ctx* c, void* p, size_t bytes);
+void keep_trim(dgnn_ctx* c, size_t limit);
 
 // RAII device buffer, freed stream-ordered on the ctx stream.
 template <class T>
@@ -103,6 +121,7 @@ struct DevBuf {
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
     ~DevBuf() { reset(); }
+    size_t kept_bytes = 0;  // > 0: the buffer came from keep_take and goes back with keep_put
     dgnn_status alloc(dgnn_ctx* ctx, size_t count) {
         reset();
         c = ctx;
@@ -114,15 +133,30 @@ struct DevBuf {
         }
         return DGNN_OK;
     }
+    // same, recycled through the ctx's kept buffers (for scratch every call needs again)
+    dgnn_status alloc_kept(dgnn_ctx* ctx, size_t count) {
+        reset();
+        c = ctx;
+        n = count;
+        p = static_cast<T*>(keep_take(ctx, (count ? count : 1) * sizeof(T), &kept_bytes));
+        if (!p) {
+            set_error("device allocation of %zu bytes failed", count * sizeof(T));
+            return DGNN_ENOMEM;
+        }
+        return DGNN_OK;
+    }
     void reset() {
-        if (p) dev_free(c, p, (n ? n : 1) * sizeof(T));
+        if (p && kept_bytes) keep_put(c, p, kept_bytes);
+        else if (p) dev_free(c, p, (n ? n : 1) * sizeof(T));
         p = nullptr;
         n = 0;
+        kept_bytes = 0;
     }
     T* release() {
         T* q = p;
         p = nullptr;
         n = 0;
+        kept_bytes = 0;
         return q;
     }
 };

@@ -283,7 +283,18 @@ extern "C" dgnn_status dgnn_gather_rows(dgnn_ctx* c, const void* features, int64
     const bool v16 = row_bytes % 16 == 0 && aligned16(features) && aligned16(out);
     const int grid = v16 ? grid_resident(c, k_gather<uint4>, n * 32 / kPackU, 256, 8)
                          : grid_resident(c, k_gather<uint32_t>, n * 32 / kPackU, 256, 8);
-    launch(c, DGNN_K_GATHER, (double)n * (2.0 * row_bytes + 4.0), [&] {
+    // a gather that reads or writes pinned host memory crosses PCIe: its own kernel family
+    // (bytes = the rows that cross the link), so the HBM-bound GPU-tier fill is reported alone
+    auto on_host = [](const void* p) {
+        cudaPointerAttributes a{};
+        if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        return a.type == cudaMemoryTypeHost;
+    };
+    const bool pcie = on_host(features) || on_host(out);
+    launch(c, pcie ? DGNN_K_GATHER_PCIE : DGNN_K_GATHER, pcie ? (double)n * row_bytes : (double)n * (2.0 * row_bytes + 4.0), [&] {
         if (v16)
             k_gather<uint4><<<grid, 256, 0, c->stream>>>((const uint8_t*)features, row_bytes, ids, n, (uint8_t*)out);
         else

@@ -40,6 +40,7 @@ struct Grp {
     int blocks;  // DGNN_SAMPLE_BLOCKS: every node so far is in the next frontier (reading c27)
     int tlog;
     uint32_t tmask;
+    uint32_t max_probes;  // k_insert gives up (DEVERR_TABLE -> redo at the bound) after this many probes
     int H;
     int64_t cap_n;
     int32_t* nodes;      // [G*cap_n]
@@ -318,7 +319,7 @@ __global__ void __launch_bounds__(256) k_insert(Grp g, const int32_t* __restrict
         uint32_t p = slot_hash(u, g.tlog);
         int pos = -1;
         for (uint32_t probes = 0;; ++probes) {
-            if (probes > g.tmask) {
+            if (probes >= g.max_probes) {
                 atomicOr(err, DEVERR_TABLE);
                 break;
             }
@@ -488,12 +489,28 @@ int64_t sat_mul(int64_t a, int64_t b, int64_t cap) {
     return std::min(a * b, cap);
 }
 
+// sub-buffers carved from one allocation (sizing pass with base = NULL, then the real pass)
+struct Slab {
+    uint8_t* base = nullptr;
+    size_t off = 0;
+    template <class T>
+    T* take(size_t count) {
+        off = (off + 255) & ~(size_t)255;
+        T* q = base ? reinterpret_cast<T*>(base + off) : nullptr;
+        off += std::max<size_t>(count, 1) * sizeof(T);
+        return q;
+    }
+};
+
 struct Arena {
+    // an output array of dgnn_sample; its buffer comes from (and, on an error path, goes back
+    // to) the ctx's kept buffers, so an epoch resampled on the same ctx reuses the previous
+    // epoch's arena at its final size instead of growing a fresh one by copies
     dgnn_ctx* c;
     int32_t* p = nullptr;
     int64_t cap = 0;
     ~Arena() {
-        if (p) dev_free(c, p, (size_t)cap * 4);
+        if (p) keep_put(c, p, (size_t)cap * 4);
     }
     int32_t* release() {
         int32_t* q = p;
@@ -502,10 +519,13 @@ struct Arena {
     }
     dgnn_status reserve(int64_t need, int64_t used) {
         if (need <= cap) return DGNN_OK;
-        int64_t ncap = std::max<int64_t>(need, cap + cap / 2);
-        int32_t* q = (int32_t*)dev_alloc(c, (size_t)ncap * 4);
+        // a fresh arena gets 1/8 headroom: the next epoch's estimate (made after its first group)
+        // then still fits the kept buffer
+        const int64_t want = p ? std::max<int64_t>(need, cap + cap / 2) : need + need / 8;
+        size_t got = 0;
+        int32_t* q = (int32_t*)keep_take(c, (size_t)want * 4, &got);
         if (!q) {
-            set_error("sample arena allocation of %lld bytes failed", (long long)ncap * 4);
+            set_error("sample arena allocation of %lld bytes failed", (long long)want * 4);
             return DGNN_ENOMEM;
         }
         if (p) {
@@ -513,7 +533,7 @@ struct Arena {
             dev_free(c, p, (size_t)cap * 4);
         }
         p = q;
-        cap = ncap;
+        cap = (int64_t)(got / 4);
         return DGNN_OK;
     }
 };
@@ -600,45 +620,73 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
             max_fr = std::max(max_fr, fr_bound[h]);
             max_cand = std::max(max_cand, cand_bound[h]);
         }
-        int64_t per_slot = cap_n * (4 + 8) + ((int64_t)8 << tlog) + hist_per_slot * 12 + max_fr * 16 + max_cand * 8;
+        // Hash-set size: the first group uses the exact bound (2 x the node bound) unless the ctx
+        // carries the largest batch of its previous call (an epoch resamples the same workload);
+        // later groups use 2 x the largest node count seen so far (a table that stays closer to
+        // L2), and a group that overflows is redone at the bound.  The access counter is
+        // therefore applied after a group succeeds, over its compacted nodes.
+        const int tlog_safe = tlog;
+        const bool adaptive = !(std::getenv("DGNN_SAMPLE_TABLE") && std::string(std::getenv("DGNN_SAMPLE_TABLE")) == "bound");
+        int tlog_cur = (adaptive && c->sample_n_hint > 0)
+                           ? std::min(tlog_safe, std::max(4, ceil_log2(2 * c->sample_n_hint)))
+                           : tlog_safe;
+        // group size from the scratch budget (the table counted at its expected size)
+        int64_t per_slot = cap_n * (4 + 8) + ((int64_t)8 << tlog_cur) + hist_per_slot * 12 + max_fr * 16 + max_cand * 8;
         for (int h = 0; h < H; ++h) per_slot += (fr_bound[h] + 1) * 8 + cand_bound[h] * 4;
         int64_t G = c->sample_group;
         if (G <= 0) {
-            const int64_t budget = (int64_t)6 << 30;
+            const int64_t budget = (int64_t)c->sample_budget;
             G = std::max<int64_t>(1, std::min<int64_t>(64, budget / std::max<int64_t>(per_slot, 1)));
         }
         G = std::min<int64_t>(std::min<int64_t>(G, kMaxGroup), nb);
 
-        // ---- group scratch ----
-        DevBuf<int32_t> d_nodes, d_small32, d_hist, d_npos, d_ntab, d_fv, d_fdg;
-        DevBuf<unsigned long long> d_sorted;
-        DevBuf<int32_t> d_table, d_local;
-        DevBuf<int64_t> d_small64, d_bstart, d_plan, d_fst;
-        std::vector<DevBuf<int32_t>> d_cand(H);
-        std::vector<DevBuf<int64_t>> d_cptr(H);
-        DevBuf<int64_t*> d_cptr_list;
-        DGNN_TRY(d_nodes.alloc(c, (size_t)(G * cap_n)));
-        DGNN_TRY(d_table.alloc(c, (size_t)(G << tlog)));
-        DGNN_TRY(d_local.alloc(c, (size_t)(G << tlog)));
-        DGNN_TRY(d_small32.alloc(c, (size_t)(4 * G + G * (H + 2))));
-        DGNN_TRY(d_small64.alloc(c, (size_t)(3 * (G + 1) + 2 + 2 * H * (kMaxGroup + 1))));
-        DGNN_TRY(d_hist.alloc(c, (size_t)(G * hist_per_slot)));
-        DGNN_TRY(d_bstart.alloc(c, (size_t)(G * hist_per_slot)));
-        DGNN_TRY(d_sorted.alloc(c, (size_t)(G * cap_n)));
-        DGNN_TRY(d_npos.alloc(c, (size_t)(G * max_cand)));
-        DGNN_TRY(d_ntab.alloc(c, (size_t)(G * max_cand)));
-        DGNN_TRY(d_fv.alloc(c, (size_t)(G * max_fr)));
-        DGNN_TRY(d_fdg.alloc(c, (size_t)(G * max_fr)));
-        DGNN_TRY(d_fst.alloc(c, (size_t)(G * max_fr)));
-        for (int h = 0; h < H; ++h) {
-            DGNN_TRY(d_cand[h].alloc(c, (size_t)std::max<int64_t>(1, G * cand_bound[h])));
-            DGNN_TRY(d_cptr[h].alloc(c, (size_t)(G * fr_bound[h] + 1)));
+        // ---- group scratch: one slab recycled through the ctx (keep_take / keep_put) ----
+        int32_t *d_nodes = nullptr, *d_small32 = nullptr, *d_hist = nullptr, *d_npos = nullptr, *d_ntab = nullptr,
+                *d_fv = nullptr, *d_fdg = nullptr;
+        unsigned long long* d_sorted = nullptr;
+        int64_t *d_small64 = nullptr, *d_bstart = nullptr, *d_plan = nullptr, *d_fst = nullptr;
+        std::vector<int32_t*> d_cand(H);
+        std::vector<int64_t*> d_cptr(H);
+        int64_t** d_cptr_list = nullptr;
+        const size_t plan_max = 3 * (size_t)(G + 1) + (size_t)H * G;
+        auto carve = [&](Slab& sl) {
+            d_nodes = sl.take<int32_t>((size_t)(G * cap_n));
+            d_small32 = sl.take<int32_t>((size_t)(4 * G + G * (H + 2)));
+            d_small64 = sl.take<int64_t>((size_t)(3 * (G + 1) + 2 + 2 * H * (kMaxGroup + 1)));
+            d_hist = sl.take<int32_t>((size_t)(G * hist_per_slot));
+            d_bstart = sl.take<int64_t>((size_t)(G * hist_per_slot));
+            d_sorted = sl.take<unsigned long long>((size_t)(G * cap_n));
+            d_npos = sl.take<int32_t>((size_t)(G * max_cand));
+            d_ntab = sl.take<int32_t>((size_t)(G * max_cand));
+            d_fv = sl.take<int32_t>((size_t)(G * max_fr));
+            d_fdg = sl.take<int32_t>((size_t)(G * max_fr));
+            d_fst = sl.take<int64_t>((size_t)(G * max_fr));
+            for (int h = 0; h < H; ++h) {
+                d_cand[h] = sl.take<int32_t>((size_t)std::max<int64_t>(1, G * cand_bound[h]));
+                d_cptr[h] = sl.take<int64_t>((size_t)(G * fr_bound[h] + 1));
+            }
+            d_cptr_list = sl.take<int64_t*>((size_t)H);
+            d_plan = sl.take<int64_t>(plan_max);
+        };
+        Slab sizing;
+        carve(sizing);
+        DevBuf<uint8_t> d_slab;
+        DGNN_TRY(d_slab.alloc_kept(c, sizing.off));
+        {
+            Slab sl;
+            sl.base = d_slab.p;
+            carve(sl);
         }
-        DGNN_TRY(d_cptr_list.alloc(c, (size_t)H));
+        // the hash set (keys + local IDs), sized for tlog_cur and re-taken if a group needs more
+        DevBuf<int32_t> d_tabs;
+        int tlog_alloc = tlog_cur;
+        DGNN_TRY(d_tabs.alloc_kept(c, (size_t)(2 * G) << tlog_alloc));
+        int32_t* d_table = d_tabs.p;
+        int32_t* d_local = d_tabs.p + ((size_t)G << tlog_alloc);
         {
             std::vector<int64_t*> ptrs(H);
-            for (int h = 0; h < H; ++h) ptrs[h] = d_cptr[h].p;
-            DGNN_CK(cudaMemcpyAsync(d_cptr_list.p, ptrs.data(), sizeof(int64_t*) * H, cudaMemcpyHostToDevice,
+            for (int h = 0; h < H; ++h) ptrs[h] = d_cptr[h];
+            DGNN_CK(cudaMemcpyAsync(d_cptr_list, ptrs.data(), sizeof(int64_t*) * H, cudaMemcpyHostToDevice,
                                     c->stream));
             DGNN_CK(cudaStreamSynchronize(c->stream));  // ptrs is a stack vector
         }
@@ -646,26 +694,27 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
         g.blocks = blocks ? 1 : 0;
         g.tlog = tlog;
         g.tmask = (uint32_t)((1ull << tlog) - 1);
+        g.max_probes = g.tmask + 1;
         g.H = H;
         g.cap_n = cap_n;
-        g.nodes = d_nodes.p;
-        g.table = d_table.p;
-        g.local = d_local.p;
-        g.n = d_small32.p;
+        g.nodes = d_nodes;
+        g.table = d_table;
+        g.local = d_local;
+        g.n = d_small32;
         g.fr_lo = g.n + G;
         g.fr_hi = g.fr_lo + G;
         g.new_cnt = g.fr_hi + G;
         g.hop_bound = g.new_cnt + G;
-        g.fr_off = d_small64.p;
+        g.fr_off = d_small64;
         g.cand_base = g.fr_off + (G + 1);
         g.new_off = g.cand_base + (G + 1);
         g.cand_total = g.new_off + (G + 1);
         int64_t* new_total = g.cand_total + 1;
         g.hop_fr_off = new_total + 1;
         g.hop_cbase = g.hop_fr_off + H * (kMaxGroup + 1);
-        g.fv = d_fv.p;
-        g.fst = d_fst.p;
-        g.fdg = d_fdg.p;
+        g.fv = d_fv;
+        g.fst = d_fst;
+        g.fdg = d_fdg;
 
         Arena a_nodes{c}, a_edges{c}, a_eptr{c};
         int64_t used_nodes = 0, used_edges = 0, used_eptr = 0;
@@ -689,26 +738,24 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
         using clk = std::chrono::steady_clock;
         double t_wait = 0.0, t_enq = 0.0, t_post = 0.0;
         const auto t_start = clk::now();
-        // Hash-set size: the first group uses the exact bound (2 x the node bound); later groups
-        // use 2 x the largest node count seen so far (a table that stays in L2 for the smaller
-        // group footprint), and a group that overflows is redone at the bound.  The access
-        // counter is therefore applied after a group succeeds, over its compacted nodes.
-        const int tlog_safe = tlog;
-        const bool adaptive = !(std::getenv("DGNN_SAMPLE_TABLE") && std::string(std::getenv("DGNN_SAMPLE_TABLE")) == "bound");
-        // the largest batch of the previous call on this ctx seeds the first group's size (an
-        // epoch resamples the same workload); a wrong hint costs one redo, never a wrong result
-        int tlog_cur = (adaptive && c->sample_n_hint > 0)
-                           ? std::min(tlog_safe, std::max(4, ceil_log2(2 * c->sample_n_hint)))
-                           : tlog_safe;
         int64_t max_n_seen = 0;
         int64_t redone = 0;
         for (int64_t t0 = 0; t0 < nb;) {
             const auto tg0 = clk::now();
             const int Gc = (int)std::min<int64_t>(G, nb - t0);
             g.G = Gc;
+            if (tlog_cur > tlog_alloc) {  // a bigger table than the one taken (after a redo or growth)
+                tlog_alloc = tlog_cur;
+                DGNN_TRY(d_tabs.alloc_kept(c, (size_t)(2 * G) << tlog_alloc));
+                g.table = d_tabs.p;
+                g.local = d_tabs.p + ((size_t)G << tlog_alloc);
+            }
             g.tlog = tlog_cur;
             g.tmask = (uint32_t)((1ull << tlog_cur) - 1);
-            DGNN_TRY(memset_async(c, d_table.p, 0xFF, sizeof(int32_t) * ((size_t)Gc << tlog_cur)));
+            // inserts into a table below the bound give up after a bounded probe run (the group is
+            // then redone at the bound); at the bound the load is <= 1/2 and every insert succeeds
+            g.max_probes = tlog_cur < tlog_safe ? 128u : g.tmask + 1;
+            DGNN_TRY(memset_async(c, g.table, 0xFF, sizeof(int32_t) * ((size_t)Gc << tlog_cur)));
             launch(c, DGNN_K_SAMPLE_SEED, 0.0, [&] {
                 k_seed_init<<<Gc, 256, 0, c->stream>>>(g, seeds, num_seeds, batch_size, t0, N, nullptr, c->dev_err);
             });
@@ -720,15 +767,15 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
                 DGNN_CK_LAUNCH();
                 // a2: candidate offsets (and the frontier's (v, start, deg) records)
                 DGNN_TRY(scan::run(c, fmax, g.fr_off + Gc, DegIn{g, csr->indptr, k, c->dev_err},
-                                   StoreExcl{d_cptr[h].p}, g.cand_total));
+                                   StoreExcl{d_cptr[h]}, g.cand_total));
                 launch(c, DGNN_K_SAMPLE_SETUP, 0.0,
-                       [&] { k_hop_cands<<<1, 32, 0, c->stream>>>(g, h, d_cptr[h].p); });
+                       [&] { k_hop_cands<<<1, 32, 0, c->stream>>>(g, h, d_cptr[h]); });
                 DGNN_CK_LAUNCH();
                 // a2: draws + gather
                 if (k > 0) {
                     const int64_t cb = batch_id_base + t0;
-                    const int64_t* cp = d_cptr[h].p;
-                    int32_t* cd = d_cand[h].p;
+                    const int64_t* cp = d_cptr[h];
+                    int32_t* cd = d_cand[h];
                     launch(c, DGNN_K_SAMPLE_HOP, 0.0, [&] {
                         if (k <= 4)
                             k_sample_hop<4><<<grid_for(c, fmax * 4, 256), 256, 0, c->stream>>>(
@@ -751,34 +798,34 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
                 // a3: dedup insert + count + bucket histogram of (slot, id >> shift)
                 const int64_t NB = (int64_t)1 << bb[h];
                 const int64_t nbk = Gc * NB;
-                DGNN_TRY(memset_async(c, d_hist.p, 0, sizeof(int32_t) * (size_t)nbk));
+                DGNN_TRY(memset_async(c, d_hist, 0, sizeof(int32_t) * (size_t)nbk));
                 launch(c, DGNN_K_SAMPLE_ORDER, 0.0, [&] {
-                    k_insert<<<grid_for(c, cmax, 256), 256, 0, c->stream>>>(g, d_cand[h].p, NB, shift[h], d_hist.p,
-                                                                            d_npos.p, d_ntab.p, nullptr, c->dev_err);
+                    k_insert<<<grid_for(c, cmax, 256), 256, 0, c->stream>>>(g, d_cand[h], NB, shift[h], d_hist,
+                                                                            d_npos, d_ntab, nullptr, c->dev_err);
                 });
                 DGNN_CK_LAUNCH();
                 {
-                    const int32_t* hist = d_hist.p;
-                    int64_t* bst = d_bstart.p;
+                    const int32_t* hist = d_hist;
+                    int64_t* bst = d_bstart;
                     DGNN_TRY(scan::run(
                         c, nbk, nullptr, [=] __device__(int64_t i) -> int32_t { return hist[i]; },
                         [=] __device__(int64_t i, int64_t e, int64_t) { bst[i] = e; }, new_total));
                 }
                 launch(c, DGNN_K_SAMPLE_SETUP, 0.0,
-                       [&] { k_new_setup<<<1, 256, 0, c->stream>>>(g, d_bstart.p, NB, new_total); });
+                       [&] { k_new_setup<<<1, 256, 0, c->stream>>>(g, d_bstart, NB, new_total); });
                 DGNN_CK_LAUNCH();
                 launch(c, DGNN_K_SAMPLE_ORDER, 0.0, [&] {
                     k_bucket_scatter<<<grid_for(c, cmax, 256), 256, 0, c->stream>>>(
-                        g, d_cand[h].p, NB, shift[h], d_bstart.p, d_npos.p, d_ntab.p, d_sorted.p);
+                        g, d_cand[h], NB, shift[h], d_bstart, d_npos, d_ntab, d_sorted);
                 });
                 DGNN_CK_LAUNCH();
                 launch(c, DGNN_K_SAMPLE_ORDER, 0.0, [&] {
-                    k_bucket_sort_assign<<<grid_for(c, nbk, 256), 256, 0, c->stream>>>(g, NB, d_bstart.p, d_hist.p,
-                                                                                         d_sorted.p);
+                    k_bucket_sort_assign<<<grid_for(c, nbk, 256), 256, 0, c->stream>>>(g, NB, d_bstart, d_hist,
+                                                                                         d_sorted);
                 });
                 DGNN_CK_LAUNCH();
                 launch(c, DGNN_K_SAMPLE_REMAP, 0.0, [&] {
-                    k_remap<<<grid_for(c, cmax, 256), 256, 0, c->stream>>>(g, d_cand[h].p, d_ntab.p);
+                    k_remap<<<grid_for(c, cmax, 256), 256, 0, c->stream>>>(g, d_cand[h], d_ntab);
                 });
                 DGNN_CK_LAUNCH();
                 launch(c, DGNN_K_SAMPLE_SETUP, 0.0, [&] { k_hop_end<<<1, 256, 0, c->stream>>>(g, h); });
@@ -846,21 +893,20 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
                                      used_edges));
             DGNN_TRY(a_eptr.reserve(used_eptr + eptr_pre[Gc] > a_eptr.cap ? est(used_eptr, eptr_pre[Gc]) : 0,
                                     used_eptr));
-            DGNN_TRY(d_plan.alloc(c, plan_n));
-            DGNN_CK(cudaMemcpyAsync(d_plan.p, h_plan, sizeof(int64_t) * plan_n, cudaMemcpyHostToDevice,
+            DGNN_CK(cudaMemcpyAsync(d_plan, h_plan, sizeof(int64_t) * plan_n, cudaMemcpyHostToDevice,
                                     c->stream));
             CompactPlan p{};
             p.G = Gc;
             p.H = H;
             p.cap_n = cap_n;
-            p.node_pre = d_plan.p;
+            p.node_pre = d_plan;
             p.edge_pre = p.node_pre + (Gc + 1);
             p.eptr_pre = p.edge_pre + (Gc + 1);
             p.edges_before = p.eptr_pre + (Gc + 1);
             p.hop_fr_off = g.hop_fr_off;
             p.hop_cbase = g.hop_cbase;
             p.hop_bound = g.hop_bound;
-            p.cptr = d_cptr_list.p;
+            p.cptr = d_cptr_list;
             p.blocks = g.blocks;
             launch(c, DGNN_K_SAMPLE_COMPACT, 8.0 * node_pre[Gc], [&] {
                 k_compact_nodes<<<grid_for(c, node_pre[Gc], 256), 256, 0, c->stream>>>(p, g.nodes,
@@ -878,7 +924,7 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
                 const int64_t Ch = h_cbs[h * (kMaxGroup + 1) + Gc];
                 if (Ch == 0) continue;
                 launch(c, DGNN_K_SAMPLE_COMPACT, 8.0 * Ch, [&] {
-                    k_compact_edges<<<grid_for(c, Ch, 256), 256, 0, c->stream>>>(p, h, d_cand[h].p,
+                    k_compact_edges<<<grid_for(c, Ch, 256), 256, 0, c->stream>>>(p, h, d_cand[h],
                                                                                  a_edges.p + used_edges);
                 });
                 DGNN_CK_LAUNCH();
@@ -963,9 +1009,10 @@ extern "C" void dgnn_samples_free(dgnn_samples* s) {
     dgnn_ctx* c = s->ctx;
     if (c) {
         cudaSetDevice(c->device);
-        dev_free(c, s->nodes, (size_t)s->cap_nodes * 4);
-        dev_free(c, s->src_local, (size_t)s->cap_edges * 4);
-        dev_free(c, s->eptr, (size_t)s->cap_eptr * 4);
+        // the arenas go back to the ctx for the next dgnn_sample call (keep_put)
+        keep_put(c, s->nodes, (size_t)s->cap_nodes * 4);
+        keep_put(c, s->src_local, (size_t)s->cap_edges * 4);
+        keep_put(c, s->eptr, (size_t)s->cap_eptr * 4);
         dev_free(c, s->node_off, sizeof(int64_t) * (s->nb + 1));
         dev_free(c, s->edge_off, sizeof(int64_t) * (s->nb + 1));
         dev_free(c, s->eptr_off, sizeof(int64_t) * (s->nb + 1));

@@ -63,8 +63,8 @@ class Workspace:
     def host(self, name: str, nbytes: int) -> "HostBuffer":
         b = self._host.get(name)
         if b is None or b.nbytes < nbytes:
-            if b is not None:
-                b.free()
+            # the old buffer is only dropped here: a Layout built earlier may still hold it, and
+            # its finalizer frees it when the last holder lets go
             b = HostBuffer(int(nbytes * 1.05) + 4096 if b is not None else nbytes)
             self._host[name] = b
         return b
