@@ -284,6 +284,12 @@ class Runner:
         cfg = inp[0]
         self.nb = (inp[3].numel() + cfg["batch_size"] - 1) // cfg["batch_size"]
         self.before_layout = None  # hook: e.g. the e2e H2D copies of the inputs
+        self.bid_base = None  # first batch id of this rank's seeds (None: rank * nb, one epoch per rank)
+        # GPU tier: "replicated" (every rank holds all of it), or partitioned over the ranks and
+        # read through peer memory ("peer", one-sided NVLink loads) / the NCCL exchange ("nccl")
+        self.gpu_tier_mode = "replicated"
+        self.slots = None  # shard.PeerSlots in the partitioned modes
+        self.ws_n, self.slot_asm_ev = 1, [None, None]
         self.pack_alone = True  # pipelined: the HBM-bound pack waits for the previous assembly
         self.host_window = 128
         self.stage_piece = (512 << 20) if pipelined else (1 << 40)  # stage-out granularity (bytes)
@@ -308,10 +314,35 @@ class Runner:
     def ctxs(self):
         return [self.ctxA, self.ctxB, self.ctxG, self.ctxT]
 
+    def setup_gpu_tier(self, mode: str, ws: int):
+        """Partitioned GPU tier (HBM-budget mode, reading c16): shard buffers for both in-flight
+        passes, IPC handles all-gathered once."""
+        self.gpu_tier_mode, self.ws_n = mode, ws
+        if mode == "replicated":
+            return
+        from paper_2405_05231_b200 import shard
+        cfg, indptr, indices, seeds, feats, gpu_rows, host_rows = self.inp
+        row_bytes = feats.element_size() * (feats.numel() // max(feats.shape[0], 1))
+        exchange = shard.all_gather_handles if ws > 1 else (lambda h: [h])
+        self.slots = shard.PeerSlots(self.dev.index or 0, gpu_rows, row_bytes, self.rank, ws, exchange)
+
+    def _cross_rank(self, ev):
+        """Host-side rendezvous on a device event: ev is complete on every rank."""
+        if ev is not None:
+            ev.synchronize()
+        if self.ws_n > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
     def layout(self, slot, after_sample=None, before_pack=None):
         cfg, indptr, indices, seeds, feats, gpu_rows, host_rows = self.inp
         if self.before_layout is not None:
             self.before_layout()
+        gpu_shard = None
+        if self.slots is not None:
+            # every rank has finished reading this slot's shards (pass e-2) before it is refilled
+            self._cross_rank(self.slot_asm_ev[slot])
+            gpu_shard = (self.rank, self.ws_n, self.slots.shard(slot))
         c = self.counts[slot]
         c.zero_()
         cap = int(os.environ.get("DGNN_SAMPLE_GRID_CAP", "0"))
@@ -323,12 +354,15 @@ class Runner:
                 self.ctxA.set_grid_cap(0)
                 if inner is not None:
                     inner()
-        return self.dg.offline_layout(self.ctxA, indptr, indices, feats, seeds, cfg["fanout"], cfg["batch_size"],
+        L = self.dg.offline_layout(self.ctxA, indptr, indices, feats, seeds, cfg["fanout"], cfg["batch_size"],
                                       gpu_rows, host_rows, RNG_SEED, group_size=cfg["group_size"],
-                                      batch_id_base=self.rank * self.nb, counts=c, ws=self.ws[slot],
+                                      batch_id_base=self.rank * self.nb if self.bid_base is None else self.bid_base,
+                                      counts=c, ws=self.ws[slot],
                                       stage_piece=int(os.environ.get("DGNN_STAGE_PIECE", str(self.stage_piece))),
                                       disk_budget_frac=self.disk_budget_frac, after_sample=after_sample,
-                                      scratch_ws=self.scratch_ws, before_pack=before_pack)
+                                      scratch_ws=self.scratch_ws, before_pack=before_pack, gpu_shard=gpu_shard)
+        L._slot = slot
+        return L
 
     def _ready(self, L):
         """The event the assembly of pass L waits for: the end of its classify step (a6) -- the
@@ -352,17 +386,42 @@ class Runner:
         a0 = torch.cuda.Event(enable_timing=True)
         a0.record(self.sB)
         gctx = self.ctxG if os.environ.get("DGNN_GATHER_STREAM", "1") == "1" else None
+        kw = {}
+        if self.slots is not None:
+            # every rank's shard of this pass is filled before anyone reads it
+            self._cross_rank(dict(L.stats.get("_events", [])).get("tiers"))
+            if self.gpu_tier_mode == "peer":
+                kw["peer_tier"] = self.slots.view(L._slot)
+            else:
+                from paper_2405_05231_b200 import shard
+                tier = self.slots.sharded(L._slot, L.plan.k_gpu)
+                a2a = shard.nccl_all_to_all() if os.environ.get("DGNN_BENCH_BACKEND", "nccl") == "nccl" \
+                    else shard.gloo_all_to_all()
+                kw["sharded_tier"] = tier
+                kw["remote"] = lambda c, addr, out: shard.fetch_remote_rows(c, tier, addr, out, a2a)
         if self.train:
             for _ in L.train_epoch(ctx=self.ctxB, train_ctx=self.ctxT, host_window=self.host_window,
-                                   gather_ctx=gctx, ws=self.asm_ws, pcie_rows=self.pcie_rows):
+                                   gather_ctx=gctx, ws=self.asm_ws, pcie_rows=self.pcie_rows, **kw):
                 pass
             self.sB.wait_stream(self.sT)  # the pass ends when its last batch is trained
         else:
             for _ in L.assemble_epoch(ctx=self.ctxB, host_window=self.host_window, gather_ctx=gctx,
-                                      ws=self.asm_ws, pcie_rows=self.pcie_rows):
+                                      ws=self.asm_ws, pcie_rows=self.pcie_rows, **kw):
                 pass
+        if self.gpu_tier_mode == "nccl" and self.ws_n > 1:
+            # the exchange is collective per run: ranks with fewer runs join the others' extra
+            # exchanges with empty requests
+            import torch.distributed as dist
+            from paper_2405_05231_b200 import shard
+            n = torch.tensor([len(L.assembly_groups())], dtype=torch.int64, device=self.dev)
+            dist.all_reduce(n, op=dist.ReduceOp.MAX)
+            empty = torch.zeros(0, dtype=torch.int32, device=self.dev)
+            for _ in range(int(n.item()) - len(L.assembly_groups())):
+                kw["remote"](self.ctxB, empty, None)
         ev_a = torch.cuda.Event(enable_timing=True)
         ev_a.record(self.sB)
+        if self.slots is not None:
+            self.slot_asm_ev[L._slot] = ev_a
         self.timeline.append(((L.stats.get("_events", []), L.stats.get("_host", [])), a0, ev_a))
         return ev_a
 
@@ -495,6 +554,16 @@ def main():
                     help="include the trainer stub (dgnn_train_stub, its own stream, depth-2 queue) in every pass")
     ap.add_argument("--num-seeds", type=int, default=None,
                     help="bounded epoch: the first NUM_SEEDS training seeds of the config (not the headline)")
+    ap.add_argument("--split", default="weak", choices=["weak", "epoch"],
+                    help="weak: every rank processes a whole epoch (rank r: epoch r, batch ids r*nb..); "
+                         "epoch: the ranks split one epoch into contiguous batch blocks (strong scaling; the "
+                         "counts all-reduce makes every rank's tier plan the single-GPU plan, so every output "
+                         "is independent of N)")
+    ap.add_argument("--gpu-tier", default="replicated", choices=["replicated", "peer", "nccl"],
+                    help="replicated: every rank holds the whole GPU tier (config rows); peer / nccl: the GPU "
+                         "tier is partitioned over the ranks' HBM with N x the config's rows (HBM-budget mode, "
+                         "reading c16) and remote rows are read one-sided through peer memory (peer) or fetched "
+                         "with the NCCL all-to-all exchange (nccl)")
     ap.add_argument("--disk-budget", type=float, default=None,
                     help="segmented disk cache (Sec. 5.1): disk budget as a fraction of the packed-only space")
     args = ap.parse_args()
@@ -507,8 +576,24 @@ def main():
     inp = make_inputs(args.config, dev, args.num_seeds)
     cfg, indptr, indices, seeds, feats, gpu_rows, host_rows = inp
     N = indptr.numel() - 1
+    nb_epoch = (seeds.numel() + cfg["batch_size"] - 1) // cfg["batch_size"]
+    bid_base = None
+    if args.split == "epoch" and ws > 1:
+        # strong scaling: this rank's contiguous block of the epoch's batches (outputs
+        # are keyed by batch id, so placement never changes them)
+        from paper_2405_05231_b200.layout import batch_range
+        b_lo, b_hi = batch_range(nb_epoch, rank, ws)
+        B = cfg["batch_size"]
+        seeds = seeds[b_lo * B:min(b_hi * B, seeds.numel())]
+        inp = (cfg, indptr, indices, seeds, feats, gpu_rows, host_rows)
+        bid_base = b_lo
+    if args.gpu_tier != "replicated":
+        gpu_rows = min(N, gpu_rows * ws)  # HBM-budget mode: per-GPU rows x N, partitioned (reading c16)
+        inp = (cfg, indptr, indices, seeds, feats, gpu_rows, host_rows)
     nb = (seeds.numel() + cfg["batch_size"] - 1) // cfg["batch_size"]
     R = Runner(dg, inp, rank, dev, pipelined=not args.sequential)
+    R.bid_base = bid_base
+    R.setup_gpu_tier(args.gpu_tier, ws)
     R.host_window = args.host_window
     R.disk_budget_frac = args.disk_budget
     R.train = args.train
@@ -558,7 +643,8 @@ def main():
                 d[f] += v[f]
         c.set_timing(False)
     ms_max = max_over_ranks(ms, ws)
-    total_batches = nb * ws * args.steps
+    nb_all = int(sum_over_ranks(float(nb), ws))  # batches of one step over all ranks
+    total_batches = nb_all * args.steps
     value = total_batches / (ms_max / 1e3)
 
     hbm_peak, peak_src = peaks()
@@ -604,7 +690,7 @@ def main():
     result = {
         "metric": METRIC, "value": round(value, 2), "unit": "mini-batches/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 2), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "scaling": "strong" if args.split == "epoch" else "weak", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic (seeded generator, workload/synth.py; closed-form fp32 features copied bytewise)",
         "config": {"workload": WORKLOAD_NAMES[args.config] + ("" if args.num_seeds is None else
                                                              f", bounded epoch of {args.num_seeds} seeds"),
@@ -615,7 +701,12 @@ def main():
                    "disk_tier": "pinned host arena" + ("" if args.disk_budget is None else
                                                        f"; segmented disk cache at {args.disk_budget:g} x the "
                                                        "packed-only space"),
-                   "parallelism": f"dp{ws} (batch-sharded, count all-reduce)",
+                   "parallelism": f"dp{ws} (batch-sharded, count all-reduce)" + (
+                       "" if args.gpu_tier == "replicated" else
+                       f"; GPU tier partitioned over {ws} GPUs ({args.gpu_tier}: " +
+                       ("one-sided peer-memory loads)" if args.gpu_tier == "peer" else "NCCL all-to-all exchange)")),
+                   "split": ("one epoch split into contiguous batch blocks over the ranks (strong)"
+                             if args.split == "epoch" else "one epoch per rank (weak)"),
                    "host_window_batches": args.host_window,
                    "schedule": ("sequential" if args.sequential else
                                 "pipelined: layout of pass e+1 overlaps assembly of pass e (2 streams)")
@@ -623,7 +714,7 @@ def main():
                                + ("; DGL-block sampling (every node so far resamples)" if args.blocks else ""),
                    "l2": "inputs larger than L2 (features %.1f GB, CSR %.1f GB); no flush needed" % (
                        feats.numel() * 4 / 1e9, (indptr.numel() * 8 + indices.numel() * 4) / 1e9)},
-        "packed_gbs": round(stats0["packed_bytes"] * ws * args.steps / (ms_max / 1e3) / 1e9, 2),
+        "packed_gbs": round(sum_over_ranks(float(stats0["packed_bytes"]), ws) * args.steps / (ms_max / 1e3) / 1e9, 2),
         "pack_kernel_gbs": round(pack_gbs, 1) if pack_gbs else None,
         "roofline": {"bound": "hbm", "achieved": round(pack_gbs, 1) if pack_gbs else None, "peak": hbm_peak,
                      "unit": "GB/s", "frac": round(pack_gbs / hbm_peak, 4) if pack_gbs else None, "traffic": traffic,
@@ -652,7 +743,7 @@ def main():
         # layout span of each timed pass up to the end of classify, plus its pack kernel time (the
         # pipelined pack first waits for the previous assembly, which is not layout work)
         spans = [t["classify"] - t["start"] + kst["pack_gather"]["ms"] / args.steps for t in tl]
-        result["offline"] = {"batches_per_s": round(nb * ws / (statistics.median(spans) / 1e3), 1),
+        result["offline"] = {"batches_per_s": round(nb_all / (statistics.median(spans) / 1e3), 1),
                              "layout_ms_per_pass": round(statistics.median(spans), 1),
                              "note": "a1-a8 per pass (sample, count all-reduce, tier select, tier fill, classify, "
                                      "pack); pipelined runs share the GPU with the previous pass's assembly"}
@@ -734,7 +825,7 @@ def main():
             R.inp, R.pack_alone = saved_inp, True
         barrier(ws)
         ms_e2e = max_over_ranks(e0.elapsed_time(e1), ws)
-        result["e2e"] = {"value": round(nb * ws * args.e2e_steps / (ms_e2e / 1e3), 2), "unit": "mini-batches/s",
+        result["e2e"] = {"value": round(nb_all * args.e2e_steps / (ms_e2e / 1e3), 2), "unit": "mini-batches/s",
                          "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                          "steps": args.e2e_steps,
                          "mode": args.e2e_mode,

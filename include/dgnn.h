@@ -303,20 +303,31 @@ dgnn_status dgnn_stage_sync(dgnn_ctx* ctx, int64_t ticket);
  * O_Direct").  dgnn_file_open opens (create=1: creates / truncates to `size`) a file, with
  * O_DIRECT when direct=1 (offsets, sizes and the bounce buffer must then be 4096-aligned).
  * dgnn_stage_file_write / _read move bytes between device memory and the file through a
- * pinned bounce buffer (host, caller-owned, >= chunk_bytes): on the ctx side stream, each
- * chunk_bytes piece is one cudaMemcpyAsync plus one pwrite/pread issued in stream order
- * (cudaLaunchHostFunc), so the ticket completes when the data is on disk / in HBM.  I/O
- * errors surface as DGNN_EIO at the next dgnn_ctx_sync. */
+ * pinned bounce buffer (host, caller-owned, chunk_bytes): on the ctx side stream, pieces of
+ * chunk_bytes / 2 alternate between the buffer's halves, each one cudaMemcpyAsync plus the file
+ * engine's pwrite / pread parts, submitted and awaited in stream order (cudaLaunchHostFunc), so
+ * the ticket completes when the data is on disk / in HBM.  I/O errors surface as DGNN_EIO at
+ * the next dgnn_ctx_sync. */
 typedef struct dgnn_file dgnn_file;
 dgnn_status dgnn_file_open(const char* path, int32_t direct, int32_t create, int64_t size, dgnn_file** out);
 dgnn_status dgnn_file_close(dgnn_file* f);
 dgnn_status dgnn_stage_file_write(dgnn_ctx* ctx, dgnn_file* f, int64_t file_off, const void* dev_src, int64_t bytes,
                                   void* bounce, int64_t chunk_bytes, int64_t* ticket);
+/* Each file owns an I/O engine (the paper's multi-queue engine): `queues` worker threads
+ * with one request queue each (default 4), started at the file's first transfer; a transfer is
+ * split into 4 KiB-aligned parts (>= 1 MiB) spread over the queues.  dgnn_file_set_queues sets
+ * the count before the first transfer (EINVAL after it, or outside [1, 64]).  The staging calls
+ * are double-buffered: the bounce buffer's two halves alternate, so the disk side of one piece
+ * overlaps the PCIe copy of the next.  dgnn_file_close joins the engine: synchronize every
+ * staging ticket of the file first. */
+dgnn_status dgnn_file_set_queues(dgnn_file* f, int32_t queues);
 /* Disk-cache page reads (P:307 merged requests; the paper's io_uring engine): the 4 KiB
  * pages pages[0..n_pages) of the cache region at file offset base_off are read (runs of
- * consecutive pages as one pread, runs spread over `threads` threads) into dev_dst back to back,
- * through the pinned bounce buffer (bounce_bytes, page-aligned) in stream order on the side
- * stream.  The page list is copied at the call; returns a staging ticket like dgnn_stage_copy. */
+ * consecutive pages as one request each, spread over the file's I/O queues; `threads` raises the
+ * queue count of an engine that has not started yet) into dev_dst back to back, through the
+ * pinned bounce buffer (bounce_bytes, page-aligned; its halves alternate between fills) in stream
+ * order on the side stream.  The page list is copied at the call; returns a staging ticket like
+ * dgnn_stage_copy. */
 dgnn_status dgnn_stage_file_read_pages(dgnn_ctx* ctx, dgnn_file* f, int64_t base_off, const int32_t* pages,
                                        int64_t n_pages, void* dev_dst, void* bounce, int64_t bounce_bytes,
                                        int32_t threads, int64_t* ticket);

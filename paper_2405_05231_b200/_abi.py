@@ -46,7 +46,7 @@ EXPORTS = [
     "dgnn_disk_plan_get_info", "dgnn_disk_plan_free", "dgnn_disk_cache_fill", "dgnn_disk_partial",
     "dgnn_train_stub", "dgnn_stage_file_read_pages", "dgnn_host_window_runs", "dgnn_gather_runs_dev", "dgnn_ctx_set_sample_mode", "dgnn_ctx_set_grid_cap", "dgnn_assemble_group_peer", "dgnn_device_alloc",
     "dgnn_device_free", "dgnn_ipc_handle", "dgnn_ipc_open", "dgnn_ipc_close", "dgnn_disk_index_partition_counts", "dgnn_pack_partition", "dgnn_pack_tails",
-    "dgnn_ctx_set_keep_limit", "dgnn_ctx_kept_bytes", "dgnn_ctx_set_sample_budget",
+    "dgnn_ctx_set_keep_limit", "dgnn_ctx_kept_bytes", "dgnn_ctx_set_sample_budget", "dgnn_file_set_queues",
 ]
 
 
@@ -134,6 +134,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "dgnn_batch_tier_counts": (i32, [P, P, i64, i64, P, P]),
             "dgnn_file_open": (i32, [ctypes.c_char_p, i32, i32, i64, ctypes.POINTER(P)]),
             "dgnn_file_close": (i32, [P]),
+            "dgnn_file_set_queues": (i32, [P, i32]),
             "dgnn_stage_file_write": (i32, [P, P, i64, P, i64, P, i64, ctypes.POINTER(i64)]),
             "dgnn_stage_file_read": (i32, [P, P, i64, P, i64, P, i64, ctypes.POINTER(i64)]),
             "dgnn_pack": (i32, [P, P, i64, i64, P, P, P, i64, i64, i64, P]),
@@ -502,6 +503,10 @@ class DiskFile:
                "dgnn_file_open")
         self.handle, self.path, self.direct, self.size = h, path, direct, size
         self._finalizer = weakref.finalize(self, load_library().dgnn_file_close, h)
+
+    def set_queues(self, queues: int):
+        """I/O queues (worker threads) of the file's engine, before its first transfer."""
+        _check(load_library().dgnn_file_set_queues(self.handle, int(queues)), "dgnn_file_set_queues")
 
     def close(self):
         self._finalizer()

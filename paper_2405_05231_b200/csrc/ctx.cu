@@ -146,6 +146,7 @@ dgnn_status dev_err_status(int h) {
     if (h & DEVERR_SEED_DUP) { set_error("a seed appears twice within one batch (reading c12)"); return DGNN_EINVAL; }
     if (h & DEVERR_ADDR_RANGE) { set_error("unresolvable node address (slot beyond its tier)"); return DGNN_ERANGE; }
     if (h & DEVERR_TABLE) { set_error("internal: sampling hash table overflow"); return DGNN_ECUDA; }
+    if (h & DEVERR_PART) { set_error("internal: partitioned dedup bucket overflow"); return DGNN_ECUDA; }
     set_error("internal: device capacity overflow (flags %d)", h);
     return DGNN_ECUDA;
 }

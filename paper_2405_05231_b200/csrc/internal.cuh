@@ -73,6 +73,7 @@ enum DevErr : int {
     DEVERR_ADDR_RANGE = 4,
     DEVERR_OVERFLOW = 8,
     DEVERR_TABLE = 16,
+    DEVERR_PART = 32,  // a (batch, ID range) bucket of the partitioned dedup overflowed its table
 };
 
 void set_error(const char* fmt, ...);

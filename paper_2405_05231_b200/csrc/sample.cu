@@ -32,6 +32,7 @@ namespace dgnn {
 namespace {
 
 constexpr int kMaxGroup = 256;
+constexpr int kMaxHops = 30;  // hops of the partitioned dedup path (slices of nodes-so-far)
 constexpr int32_t kEmpty = -1;
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -84,7 +85,7 @@ __device__ __forceinline__ int table_insert(int32_t* tab, int32_t* loc, int tlog
 
 // ----------------------------------------------------------------- seeds
 __global__ void k_seed_init(Grp g, const int32_t* __restrict__ seeds, int64_t num_seeds, int32_t B, int64_t t0,
-                            int64_t N, uint32_t* counts, int* err) {
+                            int64_t N, uint32_t* counts, int* err, int use_table) {
     const int s = blockIdx.x;
     const int64_t a = (t0 + s) * (int64_t)B;
     const int64_t ns = min((int64_t)B, num_seeds - a);
@@ -106,6 +107,7 @@ __global__ void k_seed_init(Grp g, const int32_t* __restrict__ seeds, int64_t nu
             continue;
         }
         g.nodes[(int64_t)s * g.cap_n + i] = u;
+        if (!use_table) continue;  // partitioned path: k_seed_sort checks duplicates
         const int r = table_insert(tab, loc, g.tlog, g.tmask, u, (int32_t)i);
         if (r == 0) atomicOr(err, DEVERR_SEED_DUP);
         else if (r < 0) atomicOr(err, DEVERR_TABLE);
@@ -400,6 +402,372 @@ __global__ void k_remap(Grp g, int32_t* __restrict__ cand, const int32_t* __rest
     }
 }
 
+// ------------------------- a3, partitioned path: shared-memory dedup per (batch, ID range)
+// The per-batch global hash sets above cost one random CAS into a 4-8 MB table per candidate,
+// 64 batches at once (0.5 GB of tables against a 126 MB L2).  This path instead splits each
+// batch's candidates by ID range (partition p = u >> pshift, P = 2^pbits ranges) and dedups
+// each (batch, range) bucket inside one CTA's shared memory:
+//   k_seed_sort    per batch: the seeds sorted by ID with their local IDs (the one unsorted
+//                  slice of nodes-so-far; every hop's new nodes are already ID-ascending)
+//   k_part_bounds  per (batch, slice) and range: where the range starts in the sorted slice
+//   k_part_count   candidates per bucket (shared-memory histogram per tile)
+//   scan           bucket starts
+//   k_part_scatter (u, candidate index) pairs into their buckets
+//   k_part_dedup   one CTA per bucket, taken in (batch, range) order: the bucket's old nodes
+//                  and candidates go into a shared-memory hash set; the new IDs are sorted in
+//                  shared memory; the bucket's first local ID is the batch's node count plus
+//                  the new nodes of the lower ranges (decoupled look-back over the batch's
+//                  buckets); nodes[] is written and every candidate remapped to its local ID.
+// A bucket whose distinct IDs would load its table past 3/4 raises DEVERR_PART and the group
+// is redone on the hash-set path (adversarial ID distributions only).  Results are identical
+// by construction: the dedup is a set operation, new nodes are ordered by ID (reading c10), and
+// the remap is per candidate.
+constexpr int kPartThreads = 512;
+constexpr int kPartTableLog = 12;                       // 4096 slots: keys + locals + sort keys = 64 KB
+constexpr int kPartTable = 1 << kPartTableLog;
+constexpr size_t kPartSmem = (size_t)kPartTable * 16;  // dynamic shared memory of k_part_dedup
+
+constexpr int kSeedSortMax = 4096;                      // batch_size limit of the partitioned path
+constexpr int kPartTile = 8192;                         // candidates per tile in count / scatter
+constexpr int kPartTileThreads = 512;
+constexpr int kPartBins = 2048;                         // shared-memory bins per tile
+
+struct Part {
+    int pbits;   // P = 1 << pbits ranges per batch
+    int pshift;  // range of u = u >> pshift
+    int nslices; // slices of nodes-so-far: sorted seeds + one per finished hop
+    int32_t* sid;     // [G * B] seeds sorted by ID
+    int32_t* sloc;    // [G * B] their local IDs
+    int32_t* bnd;     // [G * (H+1) * (P+1)] start of range p in slice x, relative to the slice
+    int64_t* bstart;  // [G * P + 1] bucket starts (exclusive scan of the counts), total at the end
+    int64_t* bcur;    // [G * P] scatter cursors
+    int32_t* bcnt;    // [G * P] candidates per bucket
+    int32_t* pu;      // [C] bucketed candidate IDs
+    int32_t* pi;      // [C] their candidate indices
+    unsigned long long* status;  // [G * P] look-back words of k_part_dedup
+    unsigned int* ticket;        // bucket ticket counter
+    int32_t B;        // batch size (seed slice stride)
+};
+
+template <class T>
+__device__ __forceinline__ void bitonic_sort_smem(T* a, int n2) {
+    // ascending bitonic sort of a[0, n2) (n2 a power of two), all threads of the block, one
+    // compare-exchange pair per thread and stage.  Thread t's pairs q = t + m*blockDim touch
+    // elements [64*(q/32), 64*(q/32) + 64) while j <= 32, so those stages need only the warp's
+    // own barrier; a stage with j >= 64, and the stage after it, synchronize the block.
+    const int half = n2 >> 1;
+    int prev_j = 1 << 30;  // the caller synchronized before the call
+    for (int k = 2; k <= n2; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= 64 || prev_j >= 64) __syncthreads();
+            else __syncwarp();
+            prev_j = j;
+            for (int q = threadIdx.x; q < half; q += blockDim.x) {
+                const int i = 2 * q - (q & (j - 1));
+                const int l = i + j;
+                const T x = a[i], y = a[l];
+                if ((x > y) == ((i & k) == 0)) {
+                    a[i] = y;
+                    a[l] = x;
+                }
+            }
+        }
+    }
+    __syncthreads();
+}
+
+// one CTA per batch slot: seeds sorted by ID (local ID = input position); duplicates are the
+// EINVAL of reading c12
+__global__ void __launch_bounds__(kPartThreads) k_seed_sort(Grp g, Part pt, int* err) {
+    __shared__ unsigned long long s_k[kSeedSortMax];
+    const int s = blockIdx.x;
+    const int ns = g.hop_bound[s * (g.H + 2) + 1];
+    int n2 = 1;
+    while (n2 < ns) n2 <<= 1;
+    const int32_t* nodes = g.nodes + (int64_t)s * g.cap_n;
+    for (int i = threadIdx.x; i < n2; i += blockDim.x)
+        s_k[i] = i < ns ? ((unsigned long long)(uint32_t)nodes[i] << 32) | (uint32_t)i : ~0ull;
+    __syncthreads();
+    bitonic_sort_smem(s_k, n2);
+    for (int i = threadIdx.x; i < ns; i += blockDim.x) {
+        const unsigned long long e = s_k[i];
+        pt.sid[(int64_t)s * pt.B + i] = (int32_t)(e >> 32);
+        pt.sloc[(int64_t)s * pt.B + i] = (int32_t)(uint32_t)e;
+        if (i > 0 && (s_k[i - 1] >> 32) == (e >> 32)) atomicOr(err, DEVERR_SEED_DUP);
+    }
+}
+
+// Range starts inside each sorted slice of nodes-so-far: slice 0 = the sorted seeds, slice x >= 1
+// = the new nodes of hop x-1 (local [hb[x], hb[x+1]), ID-ascending).  The element that opens a
+// range writes its start for every (empty) range in between, so bnd[.][p] for p in [0, P] is
+// written exactly once per non-empty slice (empty slices keep the memset's zeros).
+__global__ void k_part_bounds(Grp g, Part pt) {
+    const int s = blockIdx.y;
+    const int32_t* hb = g.hop_bound + s * (g.H + 2);
+    const int P = 1 << pt.pbits;
+    const int32_t n = hb[pt.nslices];  // nodes so far
+    const int32_t* nodes = g.nodes + (int64_t)s * g.cap_n;
+    for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        int x = 0;
+        while (j >= hb[x + 1]) ++x;
+        const int32_t a = hb[x], e = hb[x + 1];
+        const int32_t id = x == 0 ? pt.sid[(int64_t)s * pt.B + j] : nodes[j];
+        const int q = id >> pt.pshift;
+        int qprev = -1;
+        if (j > a) qprev = (x == 0 ? pt.sid[(int64_t)s * pt.B + j - 1] : nodes[j - 1]) >> pt.pshift;
+        int32_t* bnd = pt.bnd + ((int64_t)s * (g.H + 1) + x) * (P + 1);
+        for (int r = qprev + 1; r <= q; ++r) bnd[r] = j - a;
+        if (j == e - 1)
+            for (int r = q + 1; r <= P; ++r) bnd[r] = e - a;
+    }
+}
+
+// Shared-memory histogram of a tile's candidates over (batch, range) bins; the tile's batches
+// span [s0, s1].  mode 0: add the counts to bcnt; mode 1: reserve the bins' runs at the cursors
+// and write the (u, index) pairs.
+template <int MODE>
+__global__ void __launch_bounds__(kPartTileThreads) k_part_tile(Grp g, Part pt, const int32_t* __restrict__ cand) {
+    constexpr int kIt = kPartTile / kPartTileThreads;
+    __shared__ int64_t s_cb[kMaxGroup + 1];
+    __shared__ int32_t s_h[kPartBins];
+    __shared__ int64_t s_base[MODE ? kPartBins : 1];
+    for (int i = threadIdx.x; i <= g.G; i += blockDim.x) s_cb[i] = g.cand_base[i];
+    __syncthreads();
+    const int64_t C = s_cb[g.G];
+    const int P = 1 << pt.pbits;
+    for (int64_t t0 = (int64_t)blockIdx.x * kPartTile; t0 < C; t0 += (int64_t)gridDim.x * kPartTile) {
+        const int64_t t1 = min(C, t0 + kPartTile);
+        const int s0 = segment_of(s_cb, g.G + 1, t0), s1 = segment_of(s_cb, g.G + 1, t1 - 1);
+        const bool local = (int64_t)(s1 - s0 + 1) * P <= kPartBins;
+        if (local) {
+            for (int i = threadIdx.x; i < (s1 - s0 + 1) * P; i += blockDim.x) s_h[i] = 0;
+            __syncthreads();
+        }
+        int32_t bin[kIt], rk[kIt], u[kIt];
+#pragma unroll
+        for (int it = 0; it < kIt; ++it) {
+            const int64_t i = t0 + it * kPartTileThreads + threadIdx.x;
+            bin[it] = -1;
+            if (i < t1) {
+                const int s = s0 == s1 ? s0 : segment_of(s_cb, g.G + 1, i);
+                u[it] = cand[i];
+                const int b = s * P + (u[it] >> pt.pshift);
+                if (local) {
+                    bin[it] = b - s0 * P;
+                    rk[it] = atomicAdd(&s_h[bin[it]], 1);
+                } else if (MODE == 0) {
+                    atomicAdd(&pt.bcnt[b], 1);
+                } else {
+                    const int64_t pos = atomicAdd((unsigned long long*)&pt.bcur[b], 1ull);
+                    pt.pu[pos] = u[it];
+                    pt.pi[pos] = (int32_t)i;
+                }
+            }
+        }
+        if (local) {
+            __syncthreads();
+            for (int i = threadIdx.x; i < (s1 - s0 + 1) * P; i += blockDim.x) {
+                const int c = s_h[i];
+                if (MODE == 0) {
+                    if (c) atomicAdd(&pt.bcnt[s0 * P + i], c);
+                } else if (c) {
+                    s_base[i] = (int64_t)atomicAdd((unsigned long long*)&pt.bcur[s0 * P + i], (unsigned long long)c);
+                }
+            }
+            __syncthreads();
+            if (MODE == 1) {
+#pragma unroll
+                for (int it = 0; it < kIt; ++it) {
+                    if (bin[it] < 0) continue;
+                    const int64_t pos = s_base[bin[it]] + rk[it];
+                    pt.pu[pos] = u[it];
+                    pt.pi[pos] = (int32_t)(t0 + it * kPartTileThreads + threadIdx.x);
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+__device__ __forceinline__ uint32_t part_hash(int32_t key, int tlog) {
+    return ((uint32_t)key * 2654435761u) >> (32 - tlog);
+}
+
+__global__ void __launch_bounds__(kPartThreads) k_part_dedup(Grp g, Part pt, int32_t* __restrict__ cand, int* err) {
+    extern __shared__ __align__(16) unsigned char s_dyn[];
+    unsigned long long* s_new = reinterpret_cast<unsigned long long*>(s_dyn);
+    int32_t* s_key = reinterpret_cast<int32_t*>(s_new + kPartTable);
+    int32_t* s_loc = s_key + kPartTable;
+    __shared__ int s_nnew;
+    __shared__ volatile int s_over;
+    __shared__ unsigned s_ticket;
+    __shared__ int64_t s_prefix;
+    __shared__ int32_t s_lo[kMaxHops + 1], s_hi[kMaxHops + 1], s_hb[kMaxHops + 2];
+    __shared__ int64_t s_c0, s_c1;
+    const int P = 1 << pt.pbits;
+    const unsigned nbk = (unsigned)g.G * P;
+    const int lane = threadIdx.x & 31;
+    const int X = pt.nslices;
+    for (;;) {
+        if (threadIdx.x == 0) {
+            s_ticket = atomicAdd(pt.ticket, 1u);
+            s_nnew = 0;
+            s_over = 0;
+        }
+        __syncthreads();
+        const unsigned b = s_ticket;
+        if (b >= nbk) break;
+        const int s = (int)(b >> pt.pbits), p = (int)(b & (P - 1));
+        // the bucket's extents, loaded in parallel: its old nodes (one run per slice of
+        // nodes-so-far) and its candidates
+        {
+            const int t = threadIdx.x;
+            if (t < X) {
+                s_lo[t] = pt.bnd[((int64_t)s * (g.H + 1) + t) * (P + 1) + p];
+            } else if (t >= 32 && t < 32 + X) {
+                s_hi[t - 32] = pt.bnd[((int64_t)s * (g.H + 1) + (t - 32)) * (P + 1) + p + 1];
+            } else if (t >= 64 && t < 64 + X + 1) {
+                s_hb[t - 64] = g.hop_bound[s * (g.H + 2) + (t - 64)];
+            } else if (t == 96) {
+                s_c0 = pt.bstart[b];
+            } else if (t == 97) {
+                s_c1 = pt.bstart[b + 1];
+            }
+        }
+        __syncthreads();
+        int nold = 0;
+        for (int x = 0; x < X; ++x) nold += s_hi[x] - s_lo[x];
+        const int64_t c0 = s_c0, c1 = s_c1;
+        // table size: twice the bucket's distinct-ID bound, at most kPartTable
+        const int64_t bound = (int64_t)nold + (c1 - c0);
+        int tlog = 6;
+        while (tlog < kPartTableLog && ((int64_t)1 << tlog) < 2 * bound) ++tlog;
+        const int tsize = 1 << tlog;
+        const uint32_t tmask = (uint32_t)tsize - 1;
+        const int limit = tsize - tsize / 4;  // distinct IDs before DEVERR_PART
+        for (int i = threadIdx.x; i < tsize; i += blockDim.x) s_key[i] = kEmpty;
+        if (nold > limit && threadIdx.x == 0) s_over = 1;
+        __syncthreads();
+        if (!s_over) {
+            // old nodes: (id, local) into the table; IDs are distinct
+            for (int r = threadIdx.x; r < nold; r += blockDim.x) {
+                int x = 0, rr = r;
+                while (rr >= s_hi[x] - s_lo[x]) {
+                    rr -= s_hi[x] - s_lo[x];
+                    ++x;
+                }
+                const int32_t j = s_lo[x] + rr;
+                int32_t id, loc;
+                if (x == 0) {
+                    id = pt.sid[(int64_t)s * pt.B + j];
+                    loc = pt.sloc[(int64_t)s * pt.B + j];
+                } else {
+                    loc = s_hb[x] + j;
+                    id = g.nodes[(int64_t)s * g.cap_n + loc];
+                }
+                uint32_t q = part_hash(id, tlog);
+                while (atomicCAS(&s_key[q], kEmpty, id) != kEmpty) q = (q + 1) & tmask;
+                s_loc[q] = loc;
+            }
+            __syncthreads();
+            // candidates: the first insert of an ID is a new node
+            for (int64_t j = c0 + threadIdx.x; j < c1; j += blockDim.x) {
+                const int32_t u = pt.pu[j];
+                uint32_t q = part_hash(u, tlog);
+                for (int probes = 0;; ++probes) {
+                    if (probes >= tsize) {  // unreachable below the limit; never spin
+                        s_over = 1;
+                        break;
+                    }
+                    const int32_t prev = atomicCAS(&s_key[q], kEmpty, u);
+                    if (prev == kEmpty) {
+                        const int r = atomicAdd(&s_nnew, 1);
+                        if (r + nold >= limit) s_over = 1;  // the bucket is abandoned
+                        else s_new[r] = ((unsigned long long)(uint32_t)u << 32) | q;
+                        break;
+                    }
+                    if (prev == u) break;
+                    q = (q + 1) & tmask;
+                }
+                if (s_over) break;
+            }
+        }
+        __syncthreads();
+        const bool over = s_over != 0;
+        const int nnew = over ? 0 : s_nnew;
+        if (over && threadIdx.x == 0) atomicOr(err, DEVERR_PART);
+        // publish this bucket's new-node count first (its successors in the batch look back at
+        // it), sort, and only then look back: the predecessors publish while this CTA sorts
+        if (threadIdx.x == 0)
+            st_relaxed(&pt.status[b], (p == 0 ? scan::kFlagP : scan::kFlagA) | (unsigned long long)nnew);
+        if (!over) {
+            int n2 = 1;
+            while (n2 < nnew) n2 <<= 1;
+            for (int i = nnew + threadIdx.x; i < n2; i += blockDim.x) s_new[i] = ~0ull;
+            __syncthreads();
+            if (nnew > 1) bitonic_sort_smem(s_new, n2);
+        }
+        // decoupled look-back over the batch's lower ranges (never past range 0 of batch s)
+        if (threadIdx.x < 32) {
+            int64_t prefix = 0;
+            if (p > 0) {
+                int t = p - 1;  // range index inside the batch
+                for (;;) {
+                    const int idx = t - lane;
+                    const unsigned long long w =
+                        idx >= 0 ? ld_relaxed(&pt.status[(unsigned)s * P + idx]) : scan::kFlagP;
+                    const unsigned long long flag = w & ~scan::kMask;
+                    const unsigned pmask = __ballot_sync(kFull, flag == scan::kFlagP);
+                    const unsigned xmask = __ballot_sync(kFull, flag == 0);
+                    const int first_p = pmask ? __ffs(pmask) - 1 : 31;
+                    const unsigned need = (first_p == 31) ? kFull : ((2u << first_p) - 1u);
+                    if (xmask & need) continue;
+                    int64_t v = (lane <= first_p && idx >= 0) ? (int64_t)(w & scan::kMask) : 0;
+#pragma unroll
+                    for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(kFull, v, d);
+                    prefix += v;
+                    if (pmask) break;
+                    t -= 32;
+                }
+                if (lane == 0) st_relaxed(&pt.status[b], scan::kFlagP | (unsigned long long)(prefix + nnew));
+            }
+            if (lane == 0) {
+                s_prefix = prefix;
+                if (p == P - 1) g.new_cnt[s] = (int32_t)(prefix + nnew);
+            }
+        }
+        __syncthreads();
+        if (!over) {
+            const int32_t base = s_hb[X] + (int32_t)s_prefix;  // nodes so far + lower ranges' new nodes
+            int32_t* onodes = g.nodes + (int64_t)s * g.cap_n;
+            for (int r = threadIdx.x; r < nnew; r += blockDim.x) {
+                const unsigned long long e = s_new[r];
+                onodes[base + r] = (int32_t)(e >> 32);
+                s_loc[(uint32_t)e] = base + r;
+            }
+            __syncthreads();
+            // remap: every candidate of the bucket to its local ID
+            for (int64_t j = c0 + threadIdx.x; j < c1; j += blockDim.x) {
+                const int32_t u = pt.pu[j];
+                uint32_t q = part_hash(u, tlog);
+                while (s_key[q] != u) q = (q + 1) & tmask;
+                cand[pt.pi[j]] = s_loc[q];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void k_hop_end_part(Grp g, int h) {
+    for (int s = threadIdx.x; s < g.G; s += blockDim.x) {
+        const int32_t n0 = g.n[s], c = g.new_cnt[s];
+        g.hop_bound[s * (g.H + 2) + h + 2] = n0 + c;
+        g.fr_lo[s] = g.blocks ? 0 : n0;
+        g.fr_hi[s] = n0 + c;
+        g.n[s] = n0 + c;
+    }
+}
+
 // ------------------------------------------------ batch-major compaction
 struct CompactPlan {
     int G;
@@ -640,6 +1008,28 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
         }
         G = std::min<int64_t>(std::min<int64_t>(G, kMaxGroup), nb);
 
+        // ---- dedup path: partitioned shared-memory buckets unless the batch is too large for the
+        // seed sort or DGNN_SAMPLE_DEDUP=table; per hop, P ranges so that a bucket expects ~1024
+        // distinct IDs (from the node bound after the hop, capped by the ctx's hint) ----
+        const char* dd = std::getenv("DGNN_SAMPLE_DEDUP");
+        bool part = batch_size <= kSeedSortMax && H <= kMaxHops && !(dd && std::string(dd) == "table");
+        const int pbits_max = std::min(idbits, 12);
+        std::vector<int64_t> after_bound(H), after_seen(H, 0);
+        {
+            int64_t acc = B;
+            for (int h = 0; h < H; ++h) {
+                acc = std::min<int64_t>(cap_n, acc + new_bound[h]);
+                after_bound[h] = acc;
+            }
+        }
+        auto pbits_for = [&](int h) {
+            int64_t est = after_bound[h];
+            if (after_seen[h] > 0) est = std::min(est, after_seen[h] + after_seen[h] / 4);
+            else if (c->sample_n_hint > 0) est = std::min(est, c->sample_n_hint + c->sample_n_hint / 4);
+            return std::min(pbits_max, std::max(0, ceil_log2((est + 1023) / 1024)));
+        };
+        const int64_t Pmax = (int64_t)1 << pbits_max;
+
         // ---- group scratch: one slab recycled through the ctx (keep_take / keep_put) ----
         int32_t *d_nodes = nullptr, *d_small32 = nullptr, *d_hist = nullptr, *d_npos = nullptr, *d_ntab = nullptr,
                 *d_fv = nullptr, *d_fdg = nullptr;
@@ -648,14 +1038,13 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
         std::vector<int32_t*> d_cand(H);
         std::vector<int64_t*> d_cptr(H);
         int64_t** d_cptr_list = nullptr;
+        Part pt{};
+        pt.B = batch_size;
         const size_t plan_max = 3 * (size_t)(G + 1) + (size_t)H * G;
         auto carve = [&](Slab& sl) {
             d_nodes = sl.take<int32_t>((size_t)(G * cap_n));
             d_small32 = sl.take<int32_t>((size_t)(4 * G + G * (H + 2)));
             d_small64 = sl.take<int64_t>((size_t)(3 * (G + 1) + 2 + 2 * H * (kMaxGroup + 1)));
-            d_hist = sl.take<int32_t>((size_t)(G * hist_per_slot));
-            d_bstart = sl.take<int64_t>((size_t)(G * hist_per_slot));
-            d_sorted = sl.take<unsigned long long>((size_t)(G * cap_n));
             d_npos = sl.take<int32_t>((size_t)(G * max_cand));
             d_ntab = sl.take<int32_t>((size_t)(G * max_cand));
             d_fv = sl.take<int32_t>((size_t)(G * max_fr));
@@ -667,6 +1056,16 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
             }
             d_cptr_list = sl.take<int64_t*>((size_t)H);
             d_plan = sl.take<int64_t>(plan_max);
+            if (part) {
+                pt.sid = sl.take<int32_t>((size_t)G * batch_size);
+                pt.sloc = sl.take<int32_t>((size_t)G * batch_size);
+                pt.bnd = sl.take<int32_t>((size_t)G * (H + 1) * (Pmax + 1));
+                pt.bstart = sl.take<int64_t>((size_t)(G * Pmax + 1));
+                pt.bcur = sl.take<int64_t>((size_t)(G * Pmax));
+                pt.bcnt = sl.take<int32_t>((size_t)(G * Pmax));
+                pt.status = sl.take<unsigned long long>((size_t)(G * Pmax));
+                pt.ticket = sl.take<unsigned int>(1);
+            }
         };
         Slab sizing;
         carve(sizing);
@@ -677,12 +1076,28 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
             sl.base = d_slab.p;
             carve(sl);
         }
-        // the hash set (keys + local IDs), sized for tlog_cur and re-taken if a group needs more
+        pt.pu = d_npos;
+        pt.pi = d_ntab;
+        // hash-set path scratch (bucket sort arrays + the hash sets), taken when that path runs
+        DevBuf<uint8_t> d_legacy;
         DevBuf<int32_t> d_tabs;
-        int tlog_alloc = tlog_cur;
-        DGNN_TRY(d_tabs.alloc_kept(c, (size_t)(2 * G) << tlog_alloc));
-        int32_t* d_table = d_tabs.p;
-        int32_t* d_local = d_tabs.p + ((size_t)G << tlog_alloc);
+        int tlog_alloc = 0;
+        auto take_legacy = [&]() -> dgnn_status {
+            if (!d_legacy.p) {
+                auto carve_l = [&](Slab& sl) {
+                    d_hist = sl.take<int32_t>((size_t)(G * hist_per_slot));
+                    d_bstart = sl.take<int64_t>((size_t)(G * hist_per_slot));
+                    d_sorted = sl.take<unsigned long long>((size_t)(G * cap_n));
+                };
+                Slab sz;
+                carve_l(sz);
+                DGNN_TRY(d_legacy.alloc_kept(c, sz.off));
+                Slab sl;
+                sl.base = d_legacy.p;
+                carve_l(sl);
+            }
+            return DGNN_OK;
+        };
         {
             std::vector<int64_t*> ptrs(H);
             for (int h = 0; h < H; ++h) ptrs[h] = d_cptr[h];
@@ -690,6 +1105,8 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
                                     c->stream));
             DGNN_CK(cudaStreamSynchronize(c->stream));  // ptrs is a stack vector
         }
+        if (part) DGNN_CK(cudaFuncSetAttribute(k_part_dedup, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPartSmem));
+        const int part_grid = part ? grid_resident(c, k_part_dedup, (int64_t)1 << 40, kPartThreads, 8, kPartSmem) : 0;
         Grp g{};
         g.blocks = blocks ? 1 : 0;
         g.tlog = tlog;
@@ -698,8 +1115,6 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
         g.H = H;
         g.cap_n = cap_n;
         g.nodes = d_nodes;
-        g.table = d_table;
-        g.local = d_local;
         g.n = d_small32;
         g.fr_lo = g.n + G;
         g.fr_hi = g.fr_lo + G;
@@ -744,22 +1159,32 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
             const auto tg0 = clk::now();
             const int Gc = (int)std::min<int64_t>(G, nb - t0);
             g.G = Gc;
-            if (tlog_cur > tlog_alloc) {  // a bigger table than the one taken (after a redo or growth)
-                tlog_alloc = tlog_cur;
-                DGNN_TRY(d_tabs.alloc_kept(c, (size_t)(2 * G) << tlog_alloc));
+            if (!part) {
+                DGNN_TRY(take_legacy());
+                if (!d_tabs.p || tlog_cur > tlog_alloc) {  // a bigger table than the one taken
+                    tlog_alloc = tlog_cur;
+                    DGNN_TRY(d_tabs.alloc_kept(c, (size_t)(2 * G) << tlog_alloc));
+                }
                 g.table = d_tabs.p;
                 g.local = d_tabs.p + ((size_t)G << tlog_alloc);
+                g.tlog = tlog_cur;
+                g.tmask = (uint32_t)((1ull << tlog_cur) - 1);
+                // inserts into a table below the bound give up after a bounded probe run (the group
+                // is then redone at the bound); at the bound the load is <= 1/2 and every insert
+                // succeeds
+                g.max_probes = tlog_cur < tlog_safe ? 128u : g.tmask + 1;
+                DGNN_TRY(memset_async(c, g.table, 0xFF, sizeof(int32_t) * ((size_t)Gc << tlog_cur)));
             }
-            g.tlog = tlog_cur;
-            g.tmask = (uint32_t)((1ull << tlog_cur) - 1);
-            // inserts into a table below the bound give up after a bounded probe run (the group is
-            // then redone at the bound); at the bound the load is <= 1/2 and every insert succeeds
-            g.max_probes = tlog_cur < tlog_safe ? 128u : g.tmask + 1;
-            DGNN_TRY(memset_async(c, g.table, 0xFF, sizeof(int32_t) * ((size_t)Gc << tlog_cur)));
             launch(c, DGNN_K_SAMPLE_SEED, 0.0, [&] {
-                k_seed_init<<<Gc, 256, 0, c->stream>>>(g, seeds, num_seeds, batch_size, t0, N, nullptr, c->dev_err);
+                k_seed_init<<<Gc, 256, 0, c->stream>>>(g, seeds, num_seeds, batch_size, t0, N, nullptr, c->dev_err,
+                                                       part ? 0 : 1);
             });
             DGNN_CK_LAUNCH();
+            if (part) {
+                launch(c, DGNN_K_SAMPLE_SEED, 0.0,
+                       [&] { k_seed_sort<<<Gc, kPartThreads, 0, c->stream>>>(g, pt, c->dev_err); });
+                DGNN_CK_LAUNCH();
+            }
             for (int h = 0; h < H; ++h) {
                 const int k = fanout[h];
                 const int64_t fmax = Gc * fr_bound[h], cmax = Gc * cand_bound[h];
@@ -794,6 +1219,51 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
                                 g, csr->indices, k, rng_seed, cb, h, cp, cd);
                     });
                     DGNN_CK_LAUNCH();
+                }
+                if (part) {
+                    // a3, partitioned: bucket the candidates by (batch, ID range), dedup + order +
+                    // remap each bucket in shared memory
+                    pt.pbits = pbits_for(h);
+                    pt.pshift = idbits - pt.pbits;
+                    pt.nslices = h + 1;
+                    const int64_t P = (int64_t)1 << pt.pbits, nbk = Gc * P;
+                    DGNN_TRY(memset_async(c, pt.bnd, 0, sizeof(int32_t) * (size_t)Gc * (H + 1) * (P + 1)));
+                    DGNN_TRY(memset_async(c, pt.bcnt, 0, sizeof(int32_t) * (size_t)nbk));
+                    launch(c, DGNN_K_SAMPLE_ORDER, 0.0, [&] {
+                        k_part_bounds<<<dim3(8, Gc), 256, 0, c->stream>>>(g, pt);
+                    });
+                    DGNN_CK_LAUNCH();
+                    const int tgrid = grid_for(c, cmax, kPartTile);
+                    launch(c, DGNN_K_SAMPLE_ORDER, 0.0, [&] {
+                        k_part_tile<0><<<tgrid, kPartTileThreads, 0, c->stream>>>(g, pt, d_cand[h]);
+                    });
+                    DGNN_CK_LAUNCH();
+                    {
+                        const int32_t* cnt = pt.bcnt;
+                        int64_t* bst = pt.bstart;
+                        int64_t* bcu = pt.bcur;
+                        DGNN_TRY(scan::run(
+                            c, nbk, nullptr, [=] __device__(int64_t i) -> int32_t { return cnt[i]; },
+                            [=] __device__(int64_t i, int64_t e, int64_t) {
+                                bst[i] = e;
+                                bcu[i] = e;
+                            },
+                            pt.bstart + nbk));
+                    }
+                    launch(c, DGNN_K_SAMPLE_ORDER, 0.0, [&] {
+                        k_part_tile<1><<<tgrid, kPartTileThreads, 0, c->stream>>>(g, pt, d_cand[h]);
+                    });
+                    DGNN_CK_LAUNCH();
+                    DGNN_TRY(memset_async(c, pt.status, 0, sizeof(unsigned long long) * (size_t)nbk));
+                    DGNN_TRY(memset_async(c, pt.ticket, 0, sizeof(unsigned int)));
+                    launch(c, DGNN_K_SAMPLE_ORDER, 0.0, [&] {
+                        k_part_dedup<<<(int)std::min<int64_t>(part_grid, nbk), kPartThreads, kPartSmem, c->stream>>>(
+                            g, pt, d_cand[h], c->dev_err);
+                    });
+                    DGNN_CK_LAUNCH();
+                    launch(c, DGNN_K_SAMPLE_SETUP, 0.0, [&] { k_hop_end_part<<<1, 256, 0, c->stream>>>(g, h); });
+                    DGNN_CK_LAUNCH();
+                    continue;
                 }
                 // a3: dedup insert + count + bucket histogram of (slot, id >> shift)
                 const int64_t NB = (int64_t)1 << bb[h];
@@ -847,13 +1317,23 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
                 t_enq += std::chrono::duration<double, std::milli>(tg1 - tg0).count();
                 t_wait += std::chrono::duration<double, std::milli>(tg2 - tg1).count();
             }
-            if ((flags & DEVERR_TABLE) && tlog_cur < tlog_safe) {  // the smaller table overflowed: redo
+            if ((flags & DEVERR_PART) && part && !(flags & (DEVERR_SEED_RANGE | DEVERR_SEED_DUP))) {
+                // a bucket of the partitioned dedup overflowed: this group and the rest of the call
+                // run on the hash-set path
+                part = false;
+                ++redone;
+                continue;
+            }
+            if ((flags & DEVERR_TABLE) && !part && tlog_cur < tlog_safe) {  // the smaller table overflowed: redo
                 tlog_cur = tlog_safe;
                 ++redone;
                 continue;
             }
             DGNN_TRY(dev_err_status(flags));
             for (int s = 0; s < Gc; ++s) max_n_seen = std::max<int64_t>(max_n_seen, h_n[s]);
+            for (int s = 0; s < Gc; ++s)
+                for (int h = 0; h < H; ++h)
+                    after_seen[h] = std::max<int64_t>(after_seen[h], h_hb[s * (H + 2) + h + 2]);
             if (adaptive) tlog_cur = std::min(tlog_safe, std::max(4, ceil_log2(2 * max_n_seen)));
             // plan: node_pre[G+1], edge_pre[G+1], eptr_pre[G+1], edges_before[H*G]
             const size_t plan_n = 3 * (size_t)(Gc + 1) + (size_t)H * Gc;

@@ -476,7 +476,7 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
                    group_budget: int = 4 << 30, stage_piece: int = 1 << 40, file_path: str | None = None,
                    direct_io: bool = True, disk_budget: int | None = None, disk_m: int = 1,
                    disk_k: int = 4, disk_budget_frac: float | None = None, after_sample=None,
-                   scratch_ws: Workspace | None = None, before_pack=None) -> Layout:
+                   scratch_ws: Workspace | None = None, before_pack=None, gpu_shard=None) -> Layout:
     """Run a1-a8 on this rank's batches.
 
     ``seeds`` are this rank's seeds (batch t of them gets bid = batch_id_base + t).
@@ -492,6 +492,10 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
     the ctx stream waits for the previous pass's stage-out on the ctx side stream.
     ``before_pack``: called right before a7 is enqueued (a scheduling hook: bench.py makes the
     layout stream wait there for the previous pass's assembly, so the HBM-bound pack runs alone).
+    ``gpu_shard`` = (rank, world, buffer [>= ceil(gpu_rows / world), row_bytes] uint8): the GPU tier is
+    partitioned over the ranks (SURVEY 8(e)(2); slot s on rank s % world at row s // world) and this
+    rank fills only its shard into ``buffer`` (Layout.gpu_tier is then the shard); the assembly
+    reads the other shards through peer memory (shard.PeerTier) or the NCCL exchange.
     ``after_sample``: called once the samples are complete (dgnn_sample returns when they are),
     before the rest of the pass is enqueued -- a scheduling hook (bench.py starts the previous
     pass's assembly there, so that sampling never shares the GPU with it).
@@ -534,8 +538,17 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
             torch.empty(max(int(n), 1), dtype=dtype, device=dev)
         return t[:int(n)].view(shape) if shape is not None else t
 
-    gpu_tier = buf("gpu_tier", plan.k_gpu * row_bytes, torch.uint8, (plan.k_gpu, row_bytes))
-    A.dgnn_gather_rows(ctx, features, plan.gpu_ids, gpu_tier)
+    if gpu_shard is None:
+        gpu_tier = buf("gpu_tier", plan.k_gpu * row_bytes, torch.uint8, (plan.k_gpu, row_bytes))
+        A.dgnn_gather_rows(ctx, features, plan.gpu_ids, gpu_tier)
+    else:  # this rank's shard of the partitioned GPU tier
+        rank, world, shard_buf = gpu_shard
+        ids = A.dgnn_tier_shard_ids(ctx, plan.gpu_ids, plan.k_gpu, rank, world)
+        if ids.numel() > shard_buf.shape[0]:
+            raise ValueError(f"GPU-tier shard of {ids.numel()} rows exceeds its buffer ({shard_buf.shape[0]})")
+        gpu_tier = shard_buf[:ids.numel()]
+        if ids.numel():
+            A.dgnn_gather_rows(ctx, features, ids, gpu_tier)
     host_tier = ws.host("host_tier", plan.k_host * row_bytes) if ws is not None else \
         HostBuffer(plan.k_host * row_bytes)
     A.dgnn_gather_rows(ctx, features, plan.host_ids, host_tier.ptr)

@@ -82,7 +82,8 @@ def fetch_remote_rows(ctx: A.Ctx, tier: ShardedTier, addr: torch.Tensor, out: to
 
     with torch.cuda.stream(ctx.stream):
         back = exchange_remote_rows(np.diff(off), req_slot, serve, all_to_all, tier.world, tier.row_bytes)
-    A.dgnn_scatter_rows(ctx, back, int(off[-1]), tier.row_bytes, req_pos, out)
+    if int(off[-1]):  # (an empty call only serves the peers' requests)
+        A.dgnn_scatter_rows(ctx, back, int(off[-1]), tier.row_bytes, req_pos, out)
 
 
 def fetch_remote_rows_loopback(ctx: A.Ctx, tiers: list, rank: int, addr: torch.Tensor, out: torch.Tensor):
@@ -159,3 +160,64 @@ def all_gather_handles(handle: bytes, group=None) -> list:
     out = [None] * dist.get_world_size(group)
     dist.all_gather_object(out, handle, group=group)
     return out
+
+
+class PeerSlots:
+    """The partitioned GPU tier of a pipelined multi-pass run (bench.py --gpu-tier peer|nccl).
+
+    Two passes are in flight, so every rank keeps two shard buffers (slot = pass % 2), each a
+    plain cudaMalloc allocation of ``ceil(gpu_rows / world)`` rows.  Their CUDA IPC handles are
+    all-gathered once; ``view(slot)`` then hands the assembly a peer table (this rank's shard plus
+    the mapped shards of every other rank) for dgnn_assemble_group_peer, and ``sharded(slot, k_gpu)``
+    the same shard for the NCCL exchange path.  Filling a slot and reading it are separated by
+    the Runner's two cross-rank barriers per pass (filled everywhere before any assembly reads it;
+    read everywhere before the pass after next refills it)."""
+
+    class _View:
+        def __init__(self, peers, world):
+            self.peers, self.world = peers, world
+
+    def __init__(self, device: int, gpu_rows: int, row_bytes: int, rank: int, world: int, exchange):
+        self.rank, self.world, self.row_bytes = rank, world, row_bytes
+        self.rows_cap = max(1, (gpu_rows + world - 1) // world)
+        self.bufs = [A.DeviceBuffer(device, self.rows_cap * row_bytes) for _ in range(2)]
+        self.maps, self.views = [], []
+        dev = torch.device("cuda", device)
+        for b in self.bufs:
+            handles = exchange(b.ipc_handle())
+            ptrs = []
+            for r, h in enumerate(handles):
+                if r == rank:
+                    ptrs.append(b.ptr)
+                else:
+                    m = A.IpcMapping(device, h)
+                    self.maps.append(m)
+                    ptrs.append(m.ptr)
+            self.views.append(self._View(torch.tensor(ptrs, dtype=torch.int64, device=dev), world))
+
+    def shard(self, slot: int) -> torch.Tensor:
+        return self.bufs[slot].view((self.rows_cap, self.row_bytes))
+
+    def view(self, slot: int):
+        return self.views[slot]
+
+    def sharded(self, slot: int, k_gpu: int):
+        t = ShardedTier.__new__(ShardedTier)
+        t.ctx, t.rank, t.world, t.k_gpu, t.row_bytes = None, self.rank, self.world, k_gpu, self.row_bytes
+        n_local = max(0, (k_gpu - self.rank + self.world - 1) // self.world)
+        t.rows = self.shard(slot)[:n_local]
+        return t
+
+
+def gloo_all_to_all(group=None):
+    """all_to_all through host memory (gloo has no CUDA all-to-all): the test stand-in for
+    nccl_all_to_all when several ranks share one GPU."""
+    import torch.distributed as dist
+
+    def a2a(x: torch.Tensor, send_splits, recv_splits):
+        xc = x.contiguous().cpu()
+        out = torch.empty(sum(recv_splits), dtype=x.dtype)
+        dist.all_to_all_single(out, xc, output_split_sizes=list(recv_splits), input_split_sizes=list(send_splits),
+                               group=group)
+        return out.to(x.device)
+    return a2a

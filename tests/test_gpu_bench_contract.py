@@ -68,10 +68,12 @@ def test_reference_arm_tiny():
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
 
 
-def test_two_rank_launch_on_one_gpu():
+@pytest.mark.parametrize("split", ["weak", "epoch"])
+def test_two_rank_launch_on_one_gpu(split):
     """The N > 1 path of bench.py as the driver launches it (torch.distributed.run, one process
     per rank, batch-sharded epochs, the count all-reduce, max-over-ranks timing, one JSON line
-    from rank 0), with both ranks on the box's one GPU and gloo standing in for NCCL."""
+    from rank 0), with both ranks on the box's one GPU and gloo standing in for NCCL.  weak: one
+    epoch per rank; epoch: one epoch split into contiguous batch blocks (strong scaling)."""
     import socket
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
@@ -79,15 +81,56 @@ def test_two_rank_launch_on_one_gpu():
     env = dict(os.environ, DGNN_BENCH_SHARE_GPU="1", DGNN_BENCH_BACKEND="gloo")
     p = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
                         "--master-addr=127.0.0.1", f"--master-port={port}", "bench.py", "--gpus", "2",
-                        "--config", "tiny", "--steps", "2", "--warmup", "3", "--no-cpu", "--e2e-steps", "1"],
+                        "--config", "tiny", "--steps", "2", "--warmup", "3", "--no-cpu", "--e2e-steps", "1",
+                        "--split", split],
                        cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
     assert p.returncode == 0, p.stderr[-3000:]
     lines = [l for l in p.stdout.splitlines() if l.strip().startswith("{")]
     assert len(lines) == 1, p.stdout[-2000:]
     d = json.loads(lines[0])
-    assert d["n_gpus"] == 2 and d["value"] > 0 and d["scaling"] == "weak"
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["scaling"] == ("weak" if split == "weak" else "strong")
     assert d["config"]["parallelism"].startswith("dp2")
-    # value counts the batches of both ranks
-    assert abs(d["value"] - 2 * d["config"]["batches_per_rank"] * d["steps"] / (d["ms_per_step"] * d["steps"] / 1e3)) \
-        <= 0.02 * d["value"]
+    # value counts the batches of both ranks: two epochs (weak) or one epoch of 8 batches (strong)
+    per_step = 2 * d["config"]["batches_per_rank"] if split == "weak" else 8
+    assert abs(d["value"] - per_step * d["steps"] / (d["ms_per_step"] * d["steps"] / 1e3)) <= 0.02 * d["value"]
     assert d["e2e"]["value"] > 0
+
+
+@pytest.mark.parametrize("split,mode", [("weak", "replicated"), ("epoch", "replicated"), ("epoch", "peer"),
+                                        ("weak", "peer"), ("epoch", "nccl")])
+def test_two_rank_runner_outputs_equal_the_oracle(split, mode):
+    """bench.py's Runner at world size 2 (both ranks on the one GPU, gloo for the collectives, the
+    all-to-all through host memory): every assembled batch of three pipelined passes equals the
+    oracle, for both splits and every GPU-tier mode (tests/multirank_runner_check.py)."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, DGNN_BENCH_SHARE_GPU="1", DGNN_BENCH_BACKEND="gloo")
+    p = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                        "--master-addr=127.0.0.1", f"--master-port={port}", "tests/multirank_runner_check.py",
+                        split, mode], cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
+    assert p.returncode == 0, p.stderr[-3000:]
+    oks = [l for l in p.stdout.splitlines() if l.startswith("rank ")]
+    assert sorted(oks) == ["rank 0: ok", "rank 1: ok"], p.stdout[-3000:]
+
+
+def test_two_rank_launch_partitioned_tier():
+    """bench.py at N = 2 with the GPU tier partitioned over the ranks (peer memory): one JSON line,
+    the HBM-budget capacities (2 x the config's GPU rows) and the mode in the config."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, DGNN_BENCH_SHARE_GPU="1", DGNN_BENCH_BACKEND="gloo")
+    p = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                        "--master-addr=127.0.0.1", f"--master-port={port}", "bench.py", "--gpus", "2",
+                        "--config", "tiny", "--steps", "2", "--warmup", "3", "--no-cpu", "--no-e2e",
+                        "--split", "epoch", "--gpu-tier", "peer"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = [l for l in p.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1, p.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["scaling"] == "strong"
+    assert d["config"]["gpu_rows"] == 1000 and "partitioned" in d["config"]["parallelism"]
