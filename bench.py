@@ -287,6 +287,9 @@ class Runner:
         self.bid_base = None  # first batch id of this rank's seeds (None: rank * nb, one epoch per rank)
         # GPU tier: "replicated" (every rank holds all of it), or partitioned over the ranks and
         # read through peer memory ("peer", one-sided NVLink loads) / the NCCL exchange ("nccl")
+        self.stage = "pinned"  # the disk tier: pinned host arena, or "file" (O_DIRECT on local storage)
+        self.disk_dir = os.environ.get("DGNN_DISK_DIR", tempfile.gettempdir())
+        self.embed_graph = False  # graph samples kept in the chunks, loaded back for training
         self.gpu_tier_mode = "replicated"
         self.slots = None  # shard.PeerSlots in the partitioned modes
         self.ws_n, self.slot_asm_ev = 1, [None, None]
@@ -339,6 +342,10 @@ class Runner:
         if self.before_layout is not None:
             self.before_layout()
         gpu_shard = None
+        if self.stage == "file" and self.slot_asm_ev[slot] is not None:
+            # the slot's file is re-created (truncated) on the host: the pass that read it last
+            # (its assembly's stage-in preads) must be finished
+            self.slot_asm_ev[slot].synchronize()
         if self.slots is not None:
             # every rank has finished reading this slot's shards (pass e-2) before it is refilled
             self._cross_rank(self.slot_asm_ev[slot])
@@ -360,7 +367,9 @@ class Runner:
                                       counts=c, ws=self.ws[slot],
                                       stage_piece=int(os.environ.get("DGNN_STAGE_PIECE", str(self.stage_piece))),
                                       disk_budget_frac=self.disk_budget_frac, after_sample=after_sample,
-                                      scratch_ws=self.scratch_ws, before_pack=before_pack, gpu_shard=gpu_shard)
+                                      scratch_ws=self.scratch_ws, before_pack=before_pack, gpu_shard=gpu_shard,
+                                      stage=self.stage, embed_graph=self.embed_graph,
+                                      file_path=os.path.join(self.disk_dir, f"dgnn_disk_r{self.rank}_s{slot}.bin"))
         L._slot = slot
         return L
 
@@ -420,8 +429,7 @@ class Runner:
                 kw["remote"](self.ctxB, empty, None)
         ev_a = torch.cuda.Event(enable_timing=True)
         ev_a.record(self.sB)
-        if self.slots is not None:
-            self.slot_asm_ev[L._slot] = ev_a
+        self.slot_asm_ev[L._slot] = ev_a
         self.timeline.append(((L.stats.get("_events", []), L.stats.get("_host", [])), a0, ev_a))
         return ev_a
 
@@ -559,6 +567,12 @@ def main():
                          "epoch: the ranks split one epoch into contiguous batch blocks (strong scaling; the "
                          "counts all-reduce makes every rank's tier plan the single-GPU plan, so every output "
                          "is independent of N)")
+    ap.add_argument("--stage", default="pinned", choices=["pinned", "file"],
+                    help="disk tier: a pinned host arena (default) or a file on local storage written and read "
+                         "with O_DIRECT through the 4-queue I/O engine ($DGNN_DISK_DIR, default the temp dir)")
+    ap.add_argument("--embed-graph", action="store_true",
+                    help="keep each batch's graph sample in its chunk (P:283) and read it back through the graph "
+                         "loader for the trainer (implies --train)")
     ap.add_argument("--gpu-tier", default="replicated", choices=["replicated", "peer", "nccl"],
                     help="replicated: every rank holds the whole GPU tier (config rows); peer / nccl: the GPU "
                          "tier is partitioned over the ranks' HBM with N x the config's rows (HBM-budget mode, "
@@ -596,7 +610,9 @@ def main():
     R.setup_gpu_tier(args.gpu_tier, ws)
     R.host_window = args.host_window
     R.disk_budget_frac = args.disk_budget
-    R.train = args.train
+    R.train = args.train or args.embed_graph
+    R.stage = args.stage
+    R.embed_graph = args.embed_graph
     if args.blocks:
         R.ctxA.set_sample_mode(True)
     t = time.time()
@@ -698,7 +714,10 @@ def main():
                    "dim": cfg["dim"], "fanout": list(cfg["fanout"]), "batch_size": cfg["batch_size"],
                    "num_seeds": int(seeds.numel()), "batches_per_rank": nb, "gpu_rows": gpu_rows,
                    "host_rows": host_rows, "group_size": cfg["group_size"],
-                   "disk_tier": "pinned host arena" + ("" if args.disk_budget is None else
+                   "disk_tier": ("pinned host arena" if args.stage == "pinned" else
+                                 "file on local storage (O_DIRECT, 4 I/O queues, double-buffered)") +
+                                ("; chunks keep their graph samples (P:283), read back by the graph loader"
+                                 if args.embed_graph else "") + ("" if args.disk_budget is None else
                                                        f"; segmented disk cache at {args.disk_budget:g} x the "
                                                        "packed-only space"),
                    "parallelism": f"dp{ws} (batch-sharded, count all-reduce)" + (
@@ -710,7 +729,7 @@ def main():
                    "host_window_batches": args.host_window,
                    "schedule": ("sequential" if args.sequential else
                                 "pipelined: layout of pass e+1 overlaps assembly of pass e (2 streams)")
-                               + ("; trainer stub per run on its own stream (depth-2 queue)" if args.train else "")
+                               + ("; trainer stub per run on its own stream (depth-2 queue)" if R.train else "")
                                + ("; DGL-block sampling (every node so far resamples)" if args.blocks else ""),
                    "l2": "inputs larger than L2 (features %.1f GB, CSR %.1f GB); no flush needed" % (
                        feats.numel() * 4 / 1e9, (indptr.numel() * 8 + indices.numel() * 4) / 1e9)},
@@ -765,6 +784,14 @@ def main():
                                                "peak = pinned H2D cudaMemcpy measured in this run",
                                        "pcie": pcie}
 
+    if args.stage == "file":
+        # the disk tier's traffic per step: every chunk written once (stage-out) and read once
+        # (stage-in) through the file; rates over the step time (the I/O overlaps the rest)
+        cb = stats0["chunk_bytes"]
+        result["disk_io"] = {"bytes_written_per_step": int(cb), "bytes_read_per_step": int(cb),
+                             "write_gbs_over_step": round(cb / (ms_max / args.steps / 1e3) / 1e9, 2),
+                             "read_gbs_over_step": round(cb / (ms_max / args.steps / 1e3) / 1e9, 2),
+                             "dir": R.disk_dir}
     # ---------------- e2e through the public API with host buffers ----------------
     inp_host = None
     pinned = []

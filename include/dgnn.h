@@ -86,6 +86,9 @@ typedef enum {
     DGNN_K_HOST_WINDOW,     /* a9: marking a host window's distinct host-tier rows      */
     DGNN_K_HOST_GATHER,     /* a9: PCIe gather of a window's host rows into HBM staging */
     DGNN_K_GATHER_PCIE,     /* a7: tier gather from / into pinned host memory (PCIe)   */
+    DGNN_K_PACK_GRAPH,      /* P:283 graph sample into / out of the chunk (pack, loader) */
+    DGNN_K_SAMPLE_DEDUP,    /* a3, partitioned path: per-(batch, ID range) dedup + order */
+    DGNN_K_SAMPLE_COUNT,    /* a4: access counter over a sampling group's nodes          */
     DGNN_K_NUM
 } dgnn_kernel_id;
 
@@ -269,6 +272,35 @@ dgnn_status dgnn_batch_tier_counts(dgnn_ctx* ctx, const dgnn_samples* samples, i
  * chunk_off[i+1] = roundup(chunk_off[i] + (packed_off[i+1]-packed_off[i]) * row_bytes, 4096). */
 dgnn_status dgnn_chunk_layout(const int64_t* packed_off_host, int64_t nb, int64_t row_bytes,
                               int64_t* chunk_off_host);
+
+/* The graph sample kept in the chunk ("the graph sample of the mini-batch is also kept in
+ * the chunk"; reading c22b, opt-in).  Chunk i then holds its |P_i| packed rows at offset 0, and
+ * at sec_off[i] = roundup(|P_i| * row_bytes, 16) a graph section of int32 words:
+ *     H, n_i, m_i, e_i, hop_off[H+2], nodes[n_i], eptr[m_i], src_local[e_i]
+ * (the batch's dgnn_samples arrays; m_i eptr entries, e_i edges), zero padding up to
+ * chunk_off[i+1] = roundup(sec_off[i] + 4 * words, 4096).
+ * dgnn_chunk_layout_graph: host arithmetic of chunk_off [nb+1] and sec_off [nb] for batches
+ *   [b_lo, b_lo + nb) of `samples` (sizes from its host mirrors), offsets relative to the group.
+ * dgnn_pack_graph: writes those sections into a group buffer already packed by dgnn_pack (which
+ *   zeroes the tails the sections overwrite); sec_off_dev = the device copy of sec_off.
+ *   EINVAL if the samples' device arrays were dropped.
+ * dgnn_samples_load: the graph loader: a library-owned samples object (free with
+ *   dgnn_samples_free) for batches [b_lo, b_hi) of `meta`, renumbered from 0, whose device arrays
+ *   are read from the staged chunks -- section i at base_dev + sec_off_dev[i] (device int64 [nb]);
+ *   its device offsets are a scan of the section headers.  Only the host mirrors (and the array
+ *   sizes) come from `meta`, the layout's metadata; headers that disagree with them raise
+ *   DGNN_ECUDA ("internal: device capacity overflow") at the next synchronizing call.  Enqueued
+ *   on the ctx stream, no host synchronization; the object's arrays come from the ctx allocator
+ *   (stream-ordered on the ctx stream: a consumer on another stream must finish before it is freed).
+ * dgnn_samples_drop_device: frees a samples object's nodes / eptr / src_local device arrays
+ *   (host mirrors and offsets stay), e.g. once they are in the chunks. */
+dgnn_status dgnn_chunk_layout_graph(const dgnn_samples* samples, int64_t b_lo, const int64_t* packed_off_host,
+                                    int64_t nb, int64_t row_bytes, int64_t* chunk_off_host, int64_t* sec_off_host);
+dgnn_status dgnn_pack_graph(dgnn_ctx* ctx, const dgnn_samples* samples, int64_t b_lo, int64_t nb,
+                            const int64_t* sec_off_dev, void* group_buf);
+dgnn_status dgnn_samples_load(dgnn_ctx* ctx, const dgnn_samples* meta, int64_t b_lo, int64_t b_hi,
+                              const void* base_dev, const int64_t* sec_off_dev, dgnn_samples** out);
+dgnn_status dgnn_samples_drop_device(dgnn_samples* samples);
 
 /* Batched pack of one packing group: for every batch i < nb and r <
  * |P_i|, group_buf[chunk_off[i] + r*row_bytes ..] = features[P_i[r]] (raw bytes), and

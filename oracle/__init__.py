@@ -283,6 +283,34 @@ def pack(features, packed_lists):
     return buf, off
 
 
+def pack_embedded(features, packed_lists, samples):
+    """Batched packing with the graph sample kept in each chunk (Sec. 4: "the graph sample
+    of the mini-batch is also kept in the chunk"; byte layout = reading c22b of DESIGN.md):
+    chunk i = its |P_i| rows (as ``pack``), then at roundup(|P_i| * row_bytes, 16) the int32 words
+    H, n_i, m_i, e_i, hop_off[H+2], nodes[n_i], eptr[m_i], src_local[e_i], then zeros up to a
+    4096-byte boundary.  Returns (group_buf uint8, chunk_off int64[nb+1], sec_off int64[nb])."""
+    f = _rows_u8(features)
+    row_bytes = f.shape[1]
+    chunks, off, sec = [], [0], []
+    for p, s in zip(packed_lists, samples):
+        rows = gather_rows(f, np.asarray(p, np.int32)).reshape(-1)
+        H = len(s.hop_off) - 2
+        words = np.concatenate([np.array([H, len(s.nodes), len(s.eptr), len(s.src_local)], np.int64),
+                                np.asarray(s.hop_off, np.int64), np.asarray(s.nodes, np.int64),
+                                np.asarray(s.eptr, np.int64), np.asarray(s.src_local, np.int64)])
+        sec_bytes = words.astype("<i4").view(np.uint8)
+        a = (len(rows) + 15) // 16 * 16
+        size = (a + len(sec_bytes) + 4095) // 4096 * 4096
+        chunk = np.zeros(size, np.uint8)
+        chunk[:len(rows)] = rows
+        chunk[a:a + len(sec_bytes)] = sec_bytes
+        chunks.append(chunk)
+        sec.append(off[-1] + a)
+        off.append(off[-1] + size)
+    buf = np.concatenate(chunks) if chunks else np.zeros(0, np.uint8)
+    return buf, np.array(off, np.int64), np.array(sec, np.int64)
+
+
 def gather_rows(features, ids) -> np.ndarray:
     """out[s] = features[ids[s]] as raw bytes (row_bytes per row)."""
     f = _rows_u8(features)

@@ -10,7 +10,8 @@ from ._abi import (Ctx, Samples, CachePlan, DgnnError, dgnn_sample, dgnn_build_c
                    dgnn_chunk_layout, dgnn_pack, dgnn_gather_rows, dgnn_stage_copy, dgnn_stage_wait,
                    dgnn_stage_sync, dgnn_assemble, load_library, TIER_GPU, TIER_HOST, TIER_DISK, TIER_SHIFT,
                    SLOT_MASK, DiskIndex, DiskPlan, dgnn_disk_space, dgnn_disk_search, dgnn_disk_plan_build,
-                   dgnn_disk_cache_fill, dgnn_disk_partial, dgnn_train_stub)
+                   dgnn_disk_cache_fill, dgnn_disk_partial, dgnn_train_stub, dgnn_chunk_layout_graph,
+                   dgnn_pack_graph, dgnn_samples_load)
 from .layout import HostBuffer, Layout, Workspace, offline_layout, batch_range
 
 load_library()
@@ -20,4 +21,4 @@ __all__ = ["Ctx", "Samples", "CachePlan", "DgnnError", "dgnn_sample", "dgnn_buil
            "dgnn_stage_sync", "dgnn_assemble", "load_library", "HostBuffer", "Layout", "Workspace", "offline_layout",
            "batch_range", "TIER_GPU", "TIER_HOST", "TIER_DISK", "TIER_SHIFT", "SLOT_MASK", "DiskIndex", "DiskPlan",
            "dgnn_disk_space", "dgnn_disk_search", "dgnn_disk_plan_build", "dgnn_disk_cache_fill", "dgnn_disk_partial",
-           "dgnn_train_stub"]
+           "dgnn_train_stub", "dgnn_chunk_layout_graph", "dgnn_pack_graph", "dgnn_samples_load"]

@@ -28,7 +28,7 @@ TIER_SHIFT = 30
 SLOT_MASK = (1 << TIER_SHIFT) - 1
 KERNELS = ["scan", "sample_seed", "sample_hop", "sample_order", "sample_remap", "sample_compact", "sample_setup",
            "cache_hist", "cache_select", "classify", "pack_gather", "tier_gather", "assemble", "misc", "sort", "disk_plan", "disk_gather", "train",
-           "host_window", "host_gather", "tier_gather_pcie"]
+           "host_window", "host_gather", "tier_gather_pcie", "graph_io", "sample_dedup", "sample_count"]
 K = {name: i for i, name in enumerate(KERNELS)}
 
 # every symbol include/dgnn.h declares (checked by tests/test_abi_symbols.py)
@@ -47,6 +47,7 @@ EXPORTS = [
     "dgnn_train_stub", "dgnn_stage_file_read_pages", "dgnn_host_window_runs", "dgnn_gather_runs_dev", "dgnn_ctx_set_sample_mode", "dgnn_ctx_set_grid_cap", "dgnn_assemble_group_peer", "dgnn_device_alloc",
     "dgnn_device_free", "dgnn_ipc_handle", "dgnn_ipc_open", "dgnn_ipc_close", "dgnn_disk_index_partition_counts", "dgnn_pack_partition", "dgnn_pack_tails",
     "dgnn_ctx_set_keep_limit", "dgnn_ctx_kept_bytes", "dgnn_ctx_set_sample_budget", "dgnn_file_set_queues",
+    "dgnn_chunk_layout_graph", "dgnn_pack_graph", "dgnn_samples_load", "dgnn_samples_drop_device",
 ]
 
 
@@ -135,6 +136,10 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "dgnn_file_open": (i32, [ctypes.c_char_p, i32, i32, i64, ctypes.POINTER(P)]),
             "dgnn_file_close": (i32, [P]),
             "dgnn_file_set_queues": (i32, [P, i32]),
+            "dgnn_chunk_layout_graph": (i32, [P, i64, P, i64, i64, P, P]),
+            "dgnn_pack_graph": (i32, [P, P, i64, i64, P, P]),
+            "dgnn_samples_load": (i32, [P, P, i64, i64, P, P, ctypes.POINTER(P)]),
+            "dgnn_samples_drop_device": (i32, [P]),
             "dgnn_stage_file_write": (i32, [P, P, i64, P, i64, P, i64, ctypes.POINTER(i64)]),
             "dgnn_stage_file_read": (i32, [P, P, i64, P, i64, P, i64, ctypes.POINTER(i64)]),
             "dgnn_pack": (i32, [P, P, i64, i64, P, P, P, i64, i64, i64, P]),
@@ -380,6 +385,12 @@ class Samples:
         self.hop_off_host = _host_array(info.hop_off_host, nb * (H + 2), ctypes.c_int32).reshape(nb, H + 2)
         self.blocks = bool(info.mode)
 
+    def drop_device(self):
+        """Free the nodes / eptr / src_local device arrays (dgnn_samples_drop_device); the host-side
+        offsets stay (the layout's metadata, e.g. for the graph loader)."""
+        _check(load_library().dgnn_samples_drop_device(self.handle), "dgnn_samples_drop_device")
+        self.nodes = self.eptr = self.src_local = None
+
     def batch(self, b: int) -> dict:
         """Device views of batch b: nodes, hop_off (host), eptr, src_local."""
         n0, n1 = int(self.node_off_host[b]), int(self.node_off_host[b + 1])
@@ -469,6 +480,31 @@ def dgnn_chunk_layout(packed_off_host, row_bytes: int):
     _check(load_library().dgnn_chunk_layout(P(po.ctypes.data), len(po) - 1, int(row_bytes), P(out.ctypes.data)),
            "dgnn_chunk_layout")
     return out
+
+
+def dgnn_chunk_layout_graph(samples: Samples, b_lo: int, packed_off_host, row_bytes: int):
+    """-> (chunk_off int64 [nb+1], sec_off int64 [nb]) with graph sections (reading c22b)."""
+    import numpy as np
+    po = np.ascontiguousarray(packed_off_host, dtype=np.int64)
+    nb = len(po) - 1
+    co = np.zeros(nb + 1, np.int64)
+    so = np.zeros(max(nb, 1), np.int64)
+    _check(load_library().dgnn_chunk_layout_graph(samples.handle, int(b_lo), P(po.ctypes.data), nb, int(row_bytes),
+                                                  P(co.ctypes.data), P(so.ctypes.data)), "dgnn_chunk_layout_graph")
+    return co, so[:nb]
+
+
+def dgnn_pack_graph(ctx: Ctx, samples: Samples, b_lo: int, nb: int, sec_off_dev: torch.Tensor, group_buf):
+    _check(load_library().dgnn_pack_graph(ctx.handle, samples.handle, int(b_lo), int(nb), _ptr(sec_off_dev),
+                                          _ptr(group_buf)), "dgnn_pack_graph")
+
+
+def dgnn_samples_load(ctx: Ctx, meta: Samples, b_lo: int, b_hi: int, base, sec_off_dev: torch.Tensor) -> Samples:
+    """The graph loader: batches [b_lo, b_hi) of ``meta`` read back from staged chunks."""
+    h = P()
+    _check(load_library().dgnn_samples_load(ctx.handle, meta.handle, int(b_lo), int(b_hi), _ptr(base),
+                                            _ptr(sec_off_dev), ctypes.byref(h)), "dgnn_samples_load")
+    return Samples(ctx, h)
 
 
 def dgnn_pack(ctx: Ctx, features: torch.Tensor, packed_ids: torch.Tensor, packed_off: torch.Tensor,

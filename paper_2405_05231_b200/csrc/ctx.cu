@@ -323,7 +323,8 @@ const char* dgnn_kernel_name(int32_t kid) {
                                             "cache_select",   "classify",      "pack_gather",   "tier_gather",
                                             "assemble",       "misc",          "sort",          "disk_plan",
                                             "disk_gather",   "train",
-                                            "host_window",    "host_gather",   "tier_gather_pcie"};
+                                            "host_window",    "host_gather",   "tier_gather_pcie",
+                                            "graph_io",       "sample_dedup",  "sample_count"};
     return (kid >= 0 && kid < DGNN_K_NUM) ? names[kid] : "?";
 }
 

@@ -252,6 +252,56 @@ __global__ void __launch_bounds__(256) k_sample_hop(Grp g, const int32_t* __rest
     }
 }
 
+// Thread per frontier node (k <= KMAX <= 32): the node's k Philox draws, Floyd's resolution and
+// the ranking of the k positions all stay in registers (unrolled to KMAX, predicated on k), so a
+// draw costs its Philox rounds plus a few compares -- no shuffles or ballots, no idle lanes.
+template <int KMAX>
+__global__ void __launch_bounds__(256) k_sample_hop_t(Grp g, const int32_t* __restrict__ indices, int k,
+                                                      uint64_t seed, int64_t bid0, int h,
+                                                      const int64_t* __restrict__ cptr, int32_t* __restrict__ cand) {
+    __shared__ int64_t s_fr[kMaxGroup + 1];
+    for (int i = threadIdx.x; i <= g.G; i += blockDim.x) s_fr[i] = g.fr_off[i];
+    __syncthreads();
+    const int64_t F = s_fr[g.G];
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < F; t += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = g.fv[t];
+        const int64_t start = g.fst[t];
+        const int32_t d = g.fdg[t];
+        const int64_t base = cptr[t];
+        if (d <= k) {  // reading c3: every position, in CSR order
+            for (int p = 0; p < d; ++p) cand[base + p] = indices[start + p];
+            continue;
+        }
+        const int s = segment_of(s_fr, g.G + 1, t);
+        const uint64_t bid = (uint64_t)(bid0 + s);
+        int32_t S[KMAX];
+        // Floyd (readings c6, c7): slot q draws t_q in [0, i_q], i_q = d - k + q; takes i_q if
+        // t_q was already taken
+#pragma unroll
+        for (int q = 0; q < KMAX; ++q) {
+            if (q < k) {
+                const int32_t i = d - k + q;
+                const int32_t tq =
+                    (int32_t)__umul64hi(draw64(seed, (uint32_t)v, bid, (uint32_t)h, (uint32_t)q), (uint64_t)i + 1);
+                bool hit = false;
+#pragma unroll
+                for (int r = 0; r < q; ++r) hit |= S[r] == tq;
+                S[q] = hit ? i : tq;
+            }
+        }
+        // positions ascending: slot q's rank among the k distinct positions
+#pragma unroll
+        for (int q = 0; q < KMAX; ++q) {
+            if (q < k) {
+                int rank = 0;
+#pragma unroll
+                for (int r = 0; r < KMAX; ++r) rank += (r < k && S[r] < S[q]) ? 1 : 0;
+                cand[base + rank] = indices[start + S[q]];
+            }
+        }
+    }
+}
+
 // k > 32: one lane per frontier node runs Floyd sequentially, using the node's
 // candidate slots as scratch for the positions, then the warp gathers.
 __global__ void __launch_bounds__(256) k_sample_hop_wide(Grp g, const int32_t* __restrict__ indices, int k,
@@ -768,6 +818,122 @@ __global__ void k_hop_end_part(Grp g, int h) {
     }
 }
 
+// ------------------------------- a4: the access counter, range-major over the epoch
+// counts[v] += the number of batches whose node list holds v.  One random RED per
+// (batch, node) spreads ~0.5 G read-modify-writes over the whole 444 MB array (papers); instead,
+// once every batch is sampled, each CTA owns one range of 2^kCntBits IDs, accumulates that range's
+// counts over every batch in shared memory and adds them to counts[] with plain coalesced
+// read-modify-writes (it is the range's only writer).  Every hop slice of a batch's node list is
+// ID-ascending (reading c10), so a range is one contiguous run per slice: k_cnt_bounds finds the
+// runs, k_cnt_ranges consumes them.  Seeds (input order) take one RED each.
+constexpr int kCntBits = 14;                   // 16384 IDs = 64 KB of shared counters per CTA
+constexpr int kCntThreads = 512;
+constexpr int kCntChunk = 2048;                // slices per block-scan chunk in k_cnt_ranges
+
+struct CntPlan {
+    const int64_t* node_off;  // [nb+1]
+    const int32_t* hop_off;   // [nb*(H+2)]
+    const int32_t* nodes;
+    int H;
+    int64_t nb;
+    int64_t P;                // ranges
+    int32_t* bnd;             // [(P+1) * nb*H]: row p = start of range p in every slice; row P = lengths
+};
+
+// blockIdx.y = batch: the run boundaries of its hop slices (x = 1..H), plus one RED per seed
+__global__ void k_cnt_bounds(CntPlan c, uint32_t* __restrict__ counts) {
+    const int64_t NS = c.nb * c.H;
+    for (int64_t b = blockIdx.y; b < c.nb; b += gridDim.y) {
+        const int32_t* hb = c.hop_off + b * (c.H + 2);
+        const int32_t* nodes = c.nodes + c.node_off[b];
+        const int32_t n = hb[c.H + 1];
+        for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+            const int32_t id = nodes[j];
+            if (j < hb[1]) {  // a seed
+                atomicAdd(&counts[id], 1u);
+                continue;
+            }
+            int x = 1;
+            while (j >= hb[x + 1]) ++x;
+            const int32_t a = hb[x], e = hb[x + 1];
+            const int64_t col = b * c.H + (x - 1);
+            const int64_t q = id >> kCntBits;
+            const int64_t qprev = j > a ? (int64_t)(nodes[j - 1] >> kCntBits) : -1;
+            for (int64_t r = qprev + 1; r <= q; ++r) c.bnd[r * NS + col] = j - a;
+            if (j == e - 1)
+                for (int64_t r = q + 1; r <= c.P; ++r) c.bnd[r * NS + col] = e - a;
+        }
+    }
+}
+
+// CTA per range p (grid-stride): shared counters over every slice's run of the range
+__global__ void __launch_bounds__(kCntThreads) k_cnt_ranges(CntPlan c, uint32_t* __restrict__ counts,
+                                                            int64_t N) {
+    extern __shared__ __align__(16) unsigned char s_dyn[];
+    uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_dyn);
+    __shared__ int64_t s_pre[kCntChunk + 1];
+    __shared__ int64_t s_wsum[kCntThreads / 32];
+    const int64_t NS = c.nb * c.H;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int64_t p = blockIdx.x; p < c.P; p += gridDim.x) {
+        for (int i = threadIdx.x; i < (1 << kCntBits); i += blockDim.x) s_cnt[i] = 0;
+        const int32_t* lo_row = c.bnd + p * NS;
+        const int32_t* hi_row = c.bnd + (p + 1) * NS;
+        for (int64_t s0 = 0; s0 < NS; s0 += kCntChunk) {
+            const int ns = (int)min((int64_t)kCntChunk, NS - s0);
+            // run lengths of this chunk of slices -> inclusive block scan into s_pre[1..ns]
+            __syncthreads();
+            constexpr int kPer = kCntChunk / kCntThreads;
+            int64_t len[kPer], run = 0;
+#pragma unroll
+            for (int k = 0; k < kPer; ++k) {
+                const int i = threadIdx.x * kPer + k;
+                len[k] = i < ns ? (int64_t)(hi_row[s0 + i] - lo_row[s0 + i]) : 0;
+                run += len[k];
+            }
+            int64_t incl = run;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (lane == 31) s_wsum[warp] = incl;
+            __syncthreads();
+            int64_t wpre = 0;
+            for (int w = 0; w < warp; ++w) wpre += s_wsum[w];
+            int64_t acc = wpre + incl - run;
+#pragma unroll
+            for (int k = 0; k < kPer; ++k) {
+                const int i = threadIdx.x * kPer + k;
+                if (i < ns) s_pre[i] = acc;
+                acc += len[k];
+            }
+            if (threadIdx.x == kCntThreads - 1) s_pre[ns] = acc;  // chunk total
+            __syncthreads();
+            const int64_t total = s_pre[ns];
+            // flattened over the chunk's runs: entry t is in slice i with s_pre[i] <= t < s_pre[i+1]
+            for (int64_t t = threadIdx.x; t < total; t += blockDim.x) {
+                int lo = 0, hi = ns;  // s_pre[lo] <= t < s_pre[hi]
+                while (hi - lo > 1) {
+                    const int mid = (lo + hi) >> 1;
+                    if (s_pre[mid] <= t) lo = mid;
+                    else hi = mid;
+                }
+                const int64_t sl = s0 + lo;
+                const int64_t b = sl / c.H;
+                const int x = (int)(sl - b * c.H) + 1;
+                const int64_t pos = c.node_off[b] + c.hop_off[b * (c.H + 2) + x] + lo_row[sl] + (t - s_pre[lo]);
+                atomicAdd(&s_cnt[c.nodes[pos] - (p << kCntBits)], 1u);
+            }
+        }
+        __syncthreads();
+        const int64_t v0 = p << kCntBits;
+        for (int i = threadIdx.x; i < (1 << kCntBits) && v0 + i < N; i += blockDim.x)
+            if (s_cnt[i]) counts[v0 + i] += s_cnt[i];
+        __syncthreads();
+    }
+}
+
 // ------------------------------------------------ batch-major compaction
 struct CompactPlan {
     int G;
@@ -946,6 +1112,9 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
     S->edge_off_h.assign(nb + 1, 0);
     S->eptr_off_h.assign(nb + 1, 0);
     S->hop_off_h.assign(nb * (H + 2), 0);
+    // a4 counter: range-major over the finished epoch (default) or per group (DGNN_SAMPLE_COUNT=group)
+    const char* cm = std::getenv("DGNN_SAMPLE_COUNT");
+    const bool range_count = !(cm && std::string(cm) == "group");
 
     if (nb > 0) {
         // all seeds in range before any counting
@@ -1201,8 +1370,19 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
                     const int64_t cb = batch_id_base + t0;
                     const int64_t* cp = d_cptr[h];
                     int32_t* cd = d_cand[h];
+                    const bool warp_hop = std::getenv("DGNN_SAMPLE_HOP") &&
+                                          std::string(std::getenv("DGNN_SAMPLE_HOP")) == "warp";
                     launch(c, DGNN_K_SAMPLE_HOP, 0.0, [&] {
-                        if (k <= 4)
+                        const int tg = grid_for(c, fmax, 256);
+                        if (!warp_hop && k <= 4)
+                            k_sample_hop_t<4><<<tg, 256, 0, c->stream>>>(g, csr->indices, k, rng_seed, cb, h, cp, cd);
+                        else if (!warp_hop && k <= 8)
+                            k_sample_hop_t<8><<<tg, 256, 0, c->stream>>>(g, csr->indices, k, rng_seed, cb, h, cp, cd);
+                        else if (!warp_hop && k <= 16)
+                            k_sample_hop_t<16><<<tg, 256, 0, c->stream>>>(g, csr->indices, k, rng_seed, cb, h, cp, cd);
+                        else if (!warp_hop && k <= 32)
+                            k_sample_hop_t<32><<<tg, 256, 0, c->stream>>>(g, csr->indices, k, rng_seed, cb, h, cp, cd);
+                        else if (k <= 4)
                             k_sample_hop<4><<<grid_for(c, fmax * 4, 256), 256, 0, c->stream>>>(
                                 g, csr->indices, k, rng_seed, cb, h, cp, cd);
                         else if (k <= 8)
@@ -1256,7 +1436,7 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
                     DGNN_CK_LAUNCH();
                     DGNN_TRY(memset_async(c, pt.status, 0, sizeof(unsigned long long) * (size_t)nbk));
                     DGNN_TRY(memset_async(c, pt.ticket, 0, sizeof(unsigned int)));
-                    launch(c, DGNN_K_SAMPLE_ORDER, 0.0, [&] {
+                    launch(c, DGNN_K_SAMPLE_DEDUP, 0.0, [&] {
                         k_part_dedup<<<(int)std::min<int64_t>(part_grid, nbk), kPartThreads, kPartSmem, c->stream>>>(
                             g, pt, d_cand[h], c->dev_err);
                     });
@@ -1393,8 +1573,8 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
                                                                                         a_nodes.p + used_nodes);
             });
             DGNN_CK_LAUNCH();
-            if (counts && node_pre[Gc]) {  // one count per batch containing the node
-                launch(c, DGNN_K_SAMPLE_ORDER, 0.0, [&] {
+            if (counts && node_pre[Gc] && !range_count) {  // one count per batch containing the node
+                launch(c, DGNN_K_SAMPLE_COUNT, 0.0, [&] {
                     k_count_nodes<<<grid_for(c, node_pre[Gc], 256), 256, 0, c->stream>>>(
                         a_nodes.p + used_nodes, node_pre[Gc], counts);
                 });
@@ -1455,6 +1635,26 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
     if (nb)
         DGNN_CK(cudaMemcpyAsync(S->hop_off, S->hop_off_h.data(), sizeof(int32_t) * nb * (H + 2),
                                 cudaMemcpyHostToDevice, c->stream));
+    if (counts && nb && S->total_nodes && range_count) {
+        // a4, range-major over the epoch (see k_cnt_ranges); DGNN_SAMPLE_COUNT=group counted per group
+        const int64_t P = (N + (1 << kCntBits) - 1) >> kCntBits;
+        const int64_t NS = nb * H;
+        DevBuf<int32_t> bnd;
+        DGNN_TRY(bnd.alloc_kept(c, (size_t)((P + 1) * NS)));
+        DGNN_TRY(memset_async(c, bnd.p, 0, sizeof(int32_t) * (size_t)((P + 1) * NS)));
+        CntPlan cp{S->node_off, S->hop_off, S->nodes, H, nb, P, bnd.p};
+        launch(c, DGNN_K_SAMPLE_COUNT, 0.0, [&] {
+            k_cnt_bounds<<<dim3(16, (unsigned)std::min<int64_t>(nb, 65535)), 256, 0, c->stream>>>(cp, counts);
+        });
+        DGNN_CK_LAUNCH();
+        const size_t smem = sizeof(uint32_t) << kCntBits;
+        DGNN_CK(cudaFuncSetAttribute(k_cnt_ranges, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        const int grid = grid_resident(c, k_cnt_ranges, P, 1, 8, smem);
+        launch(c, DGNN_K_SAMPLE_COUNT, 4.0 * S->total_nodes, [&] {
+            k_cnt_ranges<<<grid, kCntThreads, smem, c->stream>>>(cp, counts, N);
+        });
+        DGNN_CK_LAUNCH();
+    }
     DGNN_CK(cudaStreamSynchronize(c->stream));  // host mirrors are the copy sources
     *out = S;
     guard.s = nullptr;

@@ -99,6 +99,7 @@ class Group:
     chunk_off: np.ndarray     # group-relative chunk offsets (bytes), nb+1
     arena_off: int            # where the group's chunks start in the disk arena
     group_bytes: int
+    sec_off: np.ndarray = None  # group-relative byte offset of each batch's graph section (embed_graph)
 
 
 @dataclass
@@ -125,6 +126,7 @@ class Layout:
     batch_tiers: np.ndarray = None  # [nb, 3] rows per tier (GPU, HOST, DISK) of each batch
     disk_plan: A.DiskPlan | None = None  # segmented disk cache (Sec. 5.1), when a disk budget is set
     cache_off: int = 0              # byte offset of the segment caches in the disk tier
+    sec_abs: np.ndarray = None      # [nb] disk-tier byte offset of each batch's graph section
 
     def phase_ms(self) -> dict:
         """Device time of the layout's phases (after the stream has passed them)."""
@@ -236,7 +238,8 @@ class Layout:
             c_hi = int(self.batch_chunk[b1, 0]) if b1 < nb else int(self.stats["chunk_bytes"])
             chunk_off = np.concatenate([self.batch_chunk[b0:b1, 0] - c_lo, [c_hi - c_lo]])
             if self.disk_plan is None:
-                tabs.append(np.concatenate([no[b0:b1 + 1] - no[b0], chunk_off, rows_pre[b0:b1 + 1] - rows_pre[b0]]))
+                tabs.append(np.concatenate([no[b0:b1 + 1] - no[b0], chunk_off, rows_pre[b0:b1 + 1] - rows_pre[b0]] +
+                                           ([self.sec_abs[b0:b1] - c_lo] if self.sec_abs is not None else [])))
             else:  # a9 reads the partial input: dense DISK rows of the run in local order
                 dpre = np.concatenate([[0], np.cumsum(self.batch_tiers[b0:b1, 2])])
                 tabs.append(np.concatenate([no[b0:b1 + 1] - no[b0], dpre * self.row_bytes, dpre, chunk_off]))
@@ -256,7 +259,7 @@ class Layout:
     def assemble_epoch(self, ctx: A.Ctx | None = None, out_budget: int = 1 << 30, host_window: int = 128,
                        gather_ctx: A.Ctx | None = None, sharded_tier=None, remote=None, runs: bool = False,
                        ring_wait: dict | None = None, ws: Workspace | None = None, peer_tier=None,
-                       pcie_rows: torch.Tensor | None = None):
+                       pcie_rows: torch.Tensor | None = None, on_run=None):
         """Pipelined assembly: the chunks of the next run of batches are staged H2D
         on the side stream while the current run is assembled on the ctx stream (one
         dgnn_assemble_group launch per run).  Yields (b, features[n_b, dim]) per batch; a
@@ -285,7 +288,11 @@ class Layout:
         through peer memory (dgnn_assemble_group_peer), no exchange round.
 
         ``pcie_rows`` (device int64 [1], measurement only): accumulates the host-tier rows the
-        window gathers move over PCIe."""
+        window gathers move over PCIe.
+
+        ``on_run(i, b0, b1, chunk, sec_off)``: called on the ctx stream after run i is assembled,
+        with the run's staged chunks (device tensor or pointer) and, when the chunks keep their
+        graph samples (embed_graph), the device offsets of the batches' graph sections in it."""
         ctx = ctx or self.ctx
         gctx = gather_ctx or ctx
         nb = self.num_batches
@@ -436,6 +443,8 @@ class Layout:
                                               chunk, t[k + 1:2 * k + 2], t[2 * k + 2:3 * k + 3], self.row_bytes,
                                               out, host_map=host_map)
                 remote(ctx, self.addr[n0:n1], out)
+            if on_run is not None:
+                on_run(i, b0, b1, chunk, t[3 * k + 3:4 * k + 3] if self.sec_abs is not None else None)
             if i in last_run:
                 ev = torch.cuda.Event()
                 ev.record(ctx.stream)
@@ -456,12 +465,24 @@ class Layout:
         ctx = ctx or self.ctx
         tctx = train_ctx or ctx
         ring_wait = {}
+        loaded = {}
+        if self.sec_abs is not None:
+            # the graph loader: each run's graph samples come out of its staged chunks
+            def on_run(i, b0, b1, chunk, sec):
+                loaded[i] = A.dgnn_samples_load(ctx, self.samples, b0, b1, chunk, sec)
+            kw["on_run"] = on_run
         for i, (b0, b1, x) in enumerate(self.assemble_epoch(ctx, runs=True, ring_wait=ring_wait, **kw)):
             if tctx is not ctx:
                 ev = torch.cuda.Event()
                 ev.record(ctx.stream)
                 tctx.stream.wait_event(ev)
-            A.dgnn_train_stub(tctx, self.samples, b0, b1, x)
+            if self.sec_abs is not None:
+                # run i-2's samples: the ctx stream has waited for its trainer (the ring), so their
+                # stream-ordered release on the ctx stream is safe
+                loaded.pop(i - 2, None)
+                A.dgnn_train_stub(tctx, loaded[i], 0, b1 - b0, x)
+            else:
+                A.dgnn_train_stub(tctx, self.samples, b0, b1, x)
             yield b0, b1, x
             if tctx is not ctx:
                 ev = torch.cuda.Event()
@@ -476,7 +497,8 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
                    group_budget: int = 4 << 30, stage_piece: int = 1 << 40, file_path: str | None = None,
                    direct_io: bool = True, disk_budget: int | None = None, disk_m: int = 1,
                    disk_k: int = 4, disk_budget_frac: float | None = None, after_sample=None,
-                   scratch_ws: Workspace | None = None, before_pack=None, gpu_shard=None) -> Layout:
+                   scratch_ws: Workspace | None = None, before_pack=None, gpu_shard=None,
+                   embed_graph: bool = False) -> Layout:
     """Run a1-a8 on this rank's batches.
 
     ``seeds`` are this rank's seeds (batch t of them gets bid = batch_id_base + t).
@@ -496,6 +518,9 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
     partitioned over the ranks (SURVEY 8(e)(2); slot s on rank s % world at row s // world) and this
     rank fills only its shard into ``buffer`` (Layout.gpu_tier is then the shard); the assembly
     reads the other shards through peer memory (shard.PeerTier) or the NCCL exchange.
+    ``embed_graph``: keep each batch's graph sample in its chunk (reading c22b) and free the
+    samples' device arrays once packed: training then reads the graph through the loader stage
+    (Layout.train_epoch, dgnn_samples_load); the host-side offsets stay as the layout's metadata.
     ``after_sample``: called once the samples are complete (dgnn_sample returns when they are),
     before the rest of the pass is enqueued -- a scheduling hook (bench.py starts the previous
     pass's assembly there, so that sampling never shares the GPU with it).
@@ -585,6 +610,8 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
     batch_chunk = np.zeros((nb, 2), np.int64)
     arena_off = 0
     g0 = 0
+    if embed_graph and (disk_budget is not None or dplan is not None):
+        raise ValueError("embed_graph with the segmented disk cache is not supported")
     while g0 < nb:
         # a packing group: at most `group_size` batches (0 = unbounded) whose chunks fit the
         # group-buffer budget (the analogue of P:439's "C - 4N" partition sizing)
@@ -593,8 +620,12 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
                 (po[g1 + 1] - po[g0]) * row_bytes + 4096 * (g1 + 1 - g0) <= group_budget:
             g1 += 1
         rel = po[g0:g1 + 1] - po[g0]
-        co = A.dgnn_chunk_layout(rel, row_bytes)
-        groups.append(Group(g0, g1, rows[g0:g1], co, arena_off, int(co[-1])))
+        so = None
+        if embed_graph:
+            co, so = A.dgnn_chunk_layout_graph(samples, g0, rel, row_bytes)
+        else:
+            co = A.dgnn_chunk_layout(rel, row_bytes)
+        groups.append(Group(g0, g1, rows[g0:g1], co, arena_off, int(co[-1]), so))
         batch_chunk[g0:g1, 0] = arena_off + co[:-1]
         batch_chunk[g0:g1, 1] = rows[g0:g1]
         arena_off += int(co[-1])
@@ -619,6 +650,8 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
     L.batch_tiers = batch_tiers
     L.disk_plan = dplan
     L.cache_off = cache_off
+    if embed_graph and nb:
+        L.sec_abs = np.concatenate([g.arena_off + g.sec_off for g in groups]).astype(np.int64)
     if dplan is not None:
         stats.update(disk_cache={"s": dplan.s, "m": dplan.m, "k": disk_k, "budget_pages": int(disk_budget) // 4096,
                                  "space_pages": dplan.space_pages, "io_pages": dplan.io_pages,
@@ -642,6 +675,11 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
         # previous pass's assembly (before_pack), delaying the enqueue of the next assembly
         rel_src, rel_all = rel_all, rel_all.to(dev, non_blocking=True)
         L._pinned_srcs.append(rel_src)
+        sec_dev = None
+        if embed_graph and nb:  # group-relative graph-section offsets of every batch
+            sec_src = torch.from_numpy(np.concatenate([g.sec_off for g in groups]).astype(np.int64)).pin_memory()
+            sec_dev = sec_src.to(dev, non_blocking=True)
+            L._pinned_srcs.append(sec_src)
         max_gb = max([g.group_bytes for g in groups], default=0)
         staged = arena is not None or disk is not None
         # group buffers come from the workspace when there is one: re-allocating GBs every
@@ -667,6 +705,8 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
                 A.dgnn_stage_wait(ctx, group_last_ticket[gi - 2])
             dst = bufs[gi % 2]
             A.dgnn_pack(ctx, features, ids, rel_po, rel_co, total, g.group_bytes, dst)
+            if sec_dev is not None:
+                A.dgnn_pack_graph(ctx, samples, g.b_lo, k, sec_dev[g.b_lo:g.b_hi], dst)
             t = A.dgnn_stage_file_write(ctx, disk, g.arena_off, dst, g.group_bytes, L._bounce_w.ptr, FILE_CHUNK)
             L.stage_pieces.append((g.b_lo, g.b_hi, t))
             group_last_ticket.append(t)
@@ -675,6 +715,8 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
                 A.dgnn_stage_wait(ctx, group_last_ticket[gi - 2])  # its buffer is being reused
             dst = bufs[gi % 2]
             A.dgnn_pack(ctx, features, ids, rel_po, rel_co, total, g.group_bytes, dst)
+            if sec_dev is not None:
+                A.dgnn_pack_graph(ctx, samples, g.b_lo, k, sec_dev[g.b_lo:g.b_hi], dst)
             # stage-out in pieces of <= stage_piece bytes on batch boundaries, so the assembler
             # can start on the first batches while the rest is still crossing PCIe
             b = g.b_lo
@@ -690,6 +732,8 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
         else:
             dst = arena_dev[g.arena_off:g.arena_off + max(g.group_bytes, 0)]
             A.dgnn_pack(ctx, features, ids, rel_po, rel_co, total, g.group_bytes, dst)
+            if sec_dev is not None:
+                A.dgnn_pack_graph(ctx, samples, g.b_lo, k, sec_dev[g.b_lo:g.b_hi], dst)
     if dplan is not None:
         L._req_pages_host = dplan.req_pages.cpu().numpy() if disk is not None else None
     if dplan is not None and dplan.cache_pages:
@@ -703,6 +747,8 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
             A.dgnn_stage_sync(ctx, t)  # on disk before the layout returns (cache_dev is released)
         else:
             A.dgnn_disk_cache_fill(ctx, dplan, features, L._cache_rows())
+    if embed_graph and nb:
+        samples.drop_device()  # from here on the graph samples live in the chunks only
     mark("pack")
     L._rel_all = rel_all
     # packed_ids is only read by the pack kernels on this stream: releasing it now is

@@ -48,7 +48,8 @@ def test_default_contract_products():
     assert d["offline"]["batches_per_s"] > 0 and d["sampling"]["edges_per_s"] > 0
 
 
-@pytest.mark.parametrize("flags", [["--disk-budget", "0.9", "--train"], ["--blocks", "--sequential"]])
+@pytest.mark.parametrize("flags", [["--disk-budget", "0.9", "--train"], ["--blocks", "--sequential"],
+                                   ["--stage", "file", "--embed-graph"]])
 def test_opt_in_paths_tiny(flags):
     d = _run("--config", "tiny", "--steps", "2", "--warmup", "3", "--no-e2e", "--cpu-batches", "8", *flags)
     _check_common(d, 2, 3)
@@ -57,6 +58,9 @@ def test_opt_in_paths_tiny(flags):
         assert "disk_cache" in d["layout_stats"]
         assert d["layout_stats"]["disk_cache"]["space_pages"] <= d["layout_stats"]["disk_cache"]["budget_pages"]
         assert "trainer stub" in d["config"]["schedule"]
+    if "--stage" in flags:
+        assert "file on local storage" in d["config"]["disk_tier"] and "graph loader" in d["config"]["disk_tier"]
+        assert d["disk_io"]["bytes_read_per_step"] > 0 and "trainer stub" in d["config"]["schedule"]
     if "--blocks" in flags:
         assert "DGL-block" in d["config"]["schedule"] and "DGL blocks" in d["cpu_baseline"]["sample"]
 
@@ -111,8 +115,9 @@ def test_two_rank_runner_outputs_equal_the_oracle(split, mode):
                         "--master-addr=127.0.0.1", f"--master-port={port}", "tests/multirank_runner_check.py",
                         split, mode], cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
     assert p.returncode == 0, p.stderr[-3000:]
-    oks = [l for l in p.stdout.splitlines() if l.startswith("rank ")]
-    assert sorted(oks) == ["rank 0: ok", "rank 1: ok"], p.stdout[-3000:]
+    import re
+    oks = re.findall(r"rank (\d): (ok|FAIL[^\n]*?)(?=rank \d:|\n|$)", p.stdout)
+    assert sorted(oks) == [("0", "ok"), ("1", "ok")], p.stdout[-3000:]
 
 
 def test_two_rank_launch_partitioned_tier():

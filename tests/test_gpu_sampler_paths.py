@@ -126,3 +126,37 @@ def test_duplicate_seed_rejected_on_both_paths(dg, ctx, path):
     with pytest.raises(dg.DgnnError) as e:
         _run(dg, ctx, ip, ix, [3, 9, 3], 3, [1], 0)
     assert e.value.status == 1
+
+
+@pytest.mark.parametrize("mode", ["range", "group"])
+@pytest.mark.parametrize("trial", range(4))
+def test_access_counter_modes(dg, ctx, monkeypatch, mode, trial):
+    """a4: the range-major epoch counter (default: shared-memory counters per 2^14-ID
+    range over every batch's ID-ascending hop slices, one RED per seed) and the per-group
+    counter (DGNN_SAMPLE_COUNT=group) both equal the oracle's batch-membership counts; counts
+    accumulate across calls (+=), including N not a multiple of the range size."""
+    if mode == "group":
+        monkeypatch.setenv("DGNN_SAMPLE_COUNT", "group")
+    else:
+        monkeypatch.delenv("DGNN_SAMPLE_COUNT", raising=False)
+    rng = np.random.default_rng(9100 + trial)
+    n = int(rng.integers(100, 70000))
+    indptr, indices = random_csr(rng, n, max_deg=int(rng.integers(1, 30)))
+    fan = [int(x) for x in rng.choice([1, 2, 5, 10, 15], size=int(rng.integers(1, 4)))]
+    seeds = rng.permutation(n)[:int(rng.integers(1, min(n, 5000)))].astype(np.int32)
+    B = int(rng.integers(1, 700))
+    ref = oracle.sample(indptr, indices, seeds, B, fan, 5, blocks=bool(trial % 2))
+    want = oracle.count_frequencies(ref, n)
+    dev = torch.device("cuda", 0)
+    ip = torch.as_tensor(indptr).to(dev)
+    ix = torch.as_tensor(indices).to(dev)
+    sd = torch.as_tensor(seeds).to(dev)
+    counts = torch.zeros(n, dtype=torch.int32, device=dev)
+    ctx.set_sample_mode(bool(trial % 2))
+    try:
+        dg.dgnn_sample(ctx, ip, ix, sd, B, fan, 5, 0, counts)
+        assert np.array_equal(counts.cpu().numpy().view(np.uint32), want)
+        dg.dgnn_sample(ctx, ip, ix, sd, B, fan, 5, 0, counts)  # accumulates
+        assert np.array_equal(counts.cpu().numpy().view(np.uint32), 2 * want)
+    finally:
+        ctx.set_sample_mode(False)
