@@ -290,6 +290,8 @@ class Runner:
         self.stage = "pinned"  # the disk tier: pinned host arena, or "file" (O_DIRECT on local storage)
         self.disk_dir = os.environ.get("DGNN_DISK_DIR", tempfile.gettempdir())
         self.embed_graph = False  # graph samples kept in the chunks, loaded back for training
+        # window-ordered host tier: each host-row window is a few contiguous ranges for the copy engine
+        self.host_order = os.environ.get("DGNN_HOST_ORDER", "1") == "1"
         self.gpu_tier_mode = "replicated"
         self.slots = None  # shard.PeerSlots in the partitioned modes
         self.ws_n, self.slot_asm_ev = 1, [None, None]
@@ -369,6 +371,7 @@ class Runner:
                                       disk_budget_frac=self.disk_budget_frac, after_sample=after_sample,
                                       scratch_ws=self.scratch_ws, before_pack=before_pack, gpu_shard=gpu_shard,
                                       stage=self.stage, embed_graph=self.embed_graph,
+                                      host_order=self.host_window if self.host_order else None,
                                       file_path=os.path.join(self.disk_dir, f"dgnn_disk_r{self.rank}_s{slot}.bin"))
         L._slot = slot
         return L

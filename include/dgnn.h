@@ -366,6 +366,42 @@ dgnn_status dgnn_stage_file_read_pages(dgnn_ctx* ctx, dgnn_file* f, int64_t base
 dgnn_status dgnn_stage_file_read(dgnn_ctx* ctx, dgnn_file* f, int64_t file_off, void* dev_dst, int64_t bytes,
                                  void* bounce, int64_t chunk_bytes, int64_t* ticket);
 
+/* The window-ordered host tier (the ordering idea of the paper's disk cache,
+ * Sec. 5.1 / Algorithm 1, applied to the CPU-cache tier and the assembler's host-row
+ * windows).  Slots and addresses are unchanged (reading c17); the tier's PHYSICAL row order is
+ * (mask, slot), mask = the windows that address the slot, so that every window's host rows are a
+ * few contiguous ranges the copy engine moves at the link rate.
+ * dgnn_host_order: addr = the address tables of all batches (device uint32, batch-major), window w =
+ *   addr[win_node_off_host[w] .. win_node_off_host[w+1]), 1 <= nwin <= 32; host_ids = the plan's
+ *   host tier (device int32 [k_host]).  Outputs (device, caller-owned, k_host entries):
+ *   slot_mask[s] = OR of 1<<w over windows holding a HOST address of slot s; phys_of_slot[s] = its
+ *   physical row; phys_ids[p] = host_ids[the slot at row p] (fill the tier with dgnn_gather_rows
+ *   over phys_ids).  Host outputs: the n_groups runs of equal mask in physical order, their first
+ *   row (group_start_host) and mask (group_mask_host); DGNN_ERANGE if n_groups > max_groups (the
+ *   caller keeps the slot-ordered tier).  Synchronizes.
+ * dgnn_host_order_ranges: host arithmetic: window w's physical ranges (merged adjacent groups) as
+ *   triples (phys_lo, phys_hi, staging_lo) in ranges_host[3 * capacity]; *rows = the window's rows.
+ * dgnn_host_window_ranges: smap[s] = staging row of slot s for every slot of window w (ranges_dev =
+ *   the device copy of the triples, nr <= 4096); other entries untouched.
+ * dgnn_copy_ranges: one cudaMemcpyAsync (H2D, ctx stream) per triple: rows [phys_lo, phys_hi) of
+ *   src_host (the pinned tier) to dst_dev rows [staging_lo, ...).
+ * dgnn_remap_ids_dev: ids[i] = table[ids[i]] for i < min(*n_dev, n_max) (a window's slot list ->
+ *   physical rows, for the SM gather when the windows differ from the ordering's). */
+dgnn_status dgnn_host_order(dgnn_ctx* ctx, const uint32_t* addr, const int64_t* win_node_off_host, int32_t nwin,
+                            const int32_t* host_ids, int64_t k_host, int32_t* phys_ids, int32_t* phys_of_slot,
+                            uint32_t* slot_mask, int64_t max_groups, int64_t* group_start_host,
+                            uint32_t* group_mask_host, int64_t* n_groups);
+dgnn_status dgnn_host_order_ranges(const int64_t* group_start_host, const uint32_t* group_mask_host, int64_t n_groups,
+                                   int64_t k_host, int32_t window, int64_t* ranges_host, int64_t capacity,
+                                   int64_t* n_ranges, int64_t* rows);
+dgnn_status dgnn_host_window_ranges(dgnn_ctx* ctx, const uint32_t* slot_mask, const int32_t* phys_of_slot,
+                                    int64_t k_host, int32_t window, const int64_t* ranges_dev, int64_t nr,
+                                    int32_t* smap);
+dgnn_status dgnn_copy_ranges(dgnn_ctx* ctx, void* dst_dev, const void* src_host, const int64_t* ranges_host,
+                             int64_t nr, int64_t row_bytes);
+dgnn_status dgnn_remap_ids_dev(dgnn_ctx* ctx, int32_t* ids, const int64_t* n_dev, int64_t n_max,
+                               const int32_t* table);
+
 /* Pinned, device-mapped host memory for the host tier and the disk-tier arena. */
 dgnn_status dgnn_host_alloc(int64_t bytes, void** out);
 dgnn_status dgnn_host_free(void* p);
@@ -505,7 +541,9 @@ dgnn_status dgnn_disk_space(dgnn_ctx* ctx, const dgnn_disk_index* idx, int64_t r
 /* d4: *s_out = minimum feasible s (0 if none), *pages_out = its space (of s = nb if none). */
 dgnn_status dgnn_disk_search(dgnn_ctx* ctx, const dgnn_disk_index* idx, int64_t row_bytes, int64_t m,
                              int64_t budget_pages, int64_t* s_out, int64_t* pages_out);
-/* The plan of (s, m) with k hash functions (d1-d8).  k in [1, 16]. */
+/* The plan of (s, m) with k hash functions (d1-d8).  k in [1, 16].  reorder: 0 = identity order
+ * (ascending node ID), 1 = reading d6 (sort by the per-function signatures S_0..S_{k-1}),
+ * 2 = Algorithm 1 line 8 as printed (one scalar MinHash value min_t S_t(v)). */
 dgnn_status dgnn_disk_plan_build(dgnn_ctx* ctx, const dgnn_disk_index* idx, int64_t row_bytes, int64_t s, int64_t m,
                                  int32_t k, uint64_t seed, int32_t reorder, dgnn_disk_plan** out);
 typedef struct {

@@ -426,8 +426,11 @@ class DiskPlan:
 
 
 def disk_plan(packed_lists, num_nodes: int, row_bytes: int, s: int, m: int, k: int = 4, seed: int = 0,
-              reorder: bool = True) -> DiskPlan:
-    """Segments, V_d, Algorithm 1 order, P_b', merged requests (d1-d8)."""
+              reorder: bool = True, literal: bool = False) -> DiskPlan:
+    """Segments, V_d, Algorithm 1 order, P_b', merged requests (d1-d8).
+
+    ``literal``: Algorithm 1 line 8 as printed: one scalar MinHash value per node,
+    the minimum over the k hash functions, instead of reading d6's per-function signature."""
     cat, off = _packed_concat(packed_lists)
     nb = len(off) - 1
     R = int(off[-1])
@@ -442,7 +445,8 @@ def disk_plan(packed_lists, num_nodes: int, row_bytes: int, s: int, m: int, k: i
     req_off = np.zeros(nb + 1, np.int64)
     dc_addr = np.zeros(cap, np.uint32)
     tot = np.zeros(4, np.int64)
-    rc = _L().oracle_disk_plan(_p(cat), _p(off), nb, num_nodes, row_bytes, s, m, k, seed, int(reorder),
+    rc = _L().oracle_disk_plan(_p(cat), _p(off), nb, num_nodes, row_bytes, s, m, k, seed,
+                               (2 if literal else 1) if reorder else 0,
                                _p(seg_off), _p(cache_ids), _p(seg_page_off), _p(pk_ids), _p(pk_off),
                                _p(req_pages), _p(req_off), _p(dc_addr), _p(tot))
     if rc != 0:

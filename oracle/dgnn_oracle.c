@@ -461,7 +461,9 @@ int oracle_assemble_tiers(const uint32_t* addr, int64_t n, const uint8_t* gpu_bu
 /*     min over the segment's batches i holding v of H_t(i) (the MinHash      */
 /*     signature of HashOrder); V_r = V_d sorted by (S_0..S_{k-1}, v)         */
 /*     lexicographically (line 9).  For k = 1 this is Algorithm 1 verbatim.  */
-/*     reorder = 0 gives the identity order (ascending v) for comparison.    */
+/*     reorder = 0 gives the identity order (ascending v) for comparison;    */
+/*     reorder = 2 is line 8 verbatim for any k: the scalar S(v) = min over   */
+/*     t of S_t(v), V_r sorted by (S(v), v).                          */
 /*  d7 I/O (Eq. 2 objective): per batch ceil(|P_b'| * row_bytes / 4096)      */
 /*     chunk pages + the number of distinct cache pages holding D_b          */
 /*     (requests to one page merged).                                 */
@@ -644,6 +646,15 @@ int oracle_disk_plan(const int32_t* packed_ids, const int64_t* packed_off, int64
                     if (H[(int64_t)t * sg + i] < sig[e * k + t]) sig[e * k + t] = H[(int64_t)t * sg + i];
             }
         }
+        /* line 8 read literally (reorder = 2, P:368 / P:377: "the MinHash value is the minimum
+           over the outputs of the k hash functions"): one scalar S(v) = min_t S_t(v) */
+        if (reorder == 2)
+            for (int64_t e = 0; e < ne; ++e) {
+                int64_t mn = INT64_MAX;
+                for (int32_t t = 0; t < k; ++t) mn = es[e].sig[t] < mn ? es[e].sig[t] : mn;
+                sig[e * k] = mn;  /* es[e].sig == sig + e * k before the sort */
+                es[e].k = 1;
+            }
         /* line 9: V_r = V_d[Sort(S)] */
         if (reorder) {
             qsort(es, (size_t)ne, sizeof(dc_entry), cmp_dc_entry);

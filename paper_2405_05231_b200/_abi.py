@@ -48,6 +48,7 @@ EXPORTS = [
     "dgnn_device_free", "dgnn_ipc_handle", "dgnn_ipc_open", "dgnn_ipc_close", "dgnn_disk_index_partition_counts", "dgnn_pack_partition", "dgnn_pack_tails",
     "dgnn_ctx_set_keep_limit", "dgnn_ctx_kept_bytes", "dgnn_ctx_set_sample_budget", "dgnn_file_set_queues",
     "dgnn_chunk_layout_graph", "dgnn_pack_graph", "dgnn_samples_load", "dgnn_samples_drop_device",
+    "dgnn_host_order", "dgnn_host_order_ranges", "dgnn_host_window_ranges", "dgnn_copy_ranges", "dgnn_remap_ids_dev",
 ]
 
 
@@ -140,6 +141,11 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "dgnn_pack_graph": (i32, [P, P, i64, i64, P, P]),
             "dgnn_samples_load": (i32, [P, P, i64, i64, P, P, ctypes.POINTER(P)]),
             "dgnn_samples_drop_device": (i32, [P]),
+            "dgnn_host_order": (i32, [P, P, P, i32, P, i64, P, P, P, i64, P, P, ctypes.POINTER(i64)]),
+            "dgnn_host_order_ranges": (i32, [P, P, i64, i64, i32, P, i64, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
+            "dgnn_host_window_ranges": (i32, [P, P, P, i64, i32, P, i64, P]),
+            "dgnn_copy_ranges": (i32, [P, P, P, P, i64, i64]),
+            "dgnn_remap_ids_dev": (i32, [P, P, P, i64, P]),
             "dgnn_stage_file_write": (i32, [P, P, i64, P, i64, P, i64, ctypes.POINTER(i64)]),
             "dgnn_stage_file_read": (i32, [P, P, i64, P, i64, P, i64, ctypes.POINTER(i64)]),
             "dgnn_pack": (i32, [P, P, i64, i64, P, P, P, i64, i64, i64, P]),
@@ -507,6 +513,65 @@ def dgnn_samples_load(ctx: Ctx, meta: Samples, b_lo: int, b_hi: int, base, sec_o
     return Samples(ctx, h)
 
 
+class HostOrder:
+    """The window-ordered host tier of one layout (dgnn_host_order): device slot_mask / phys_of_slot
+    / phys_ids, and per window its physical ranges (host triples + device copy)."""
+
+    def __init__(self, ctx: Ctx, addr: torch.Tensor, win_node_off, host_ids: torch.Tensor, k_host: int,
+                 max_groups: int = 4096):
+        import numpy as np
+        wo = np.ascontiguousarray(win_node_off, dtype=np.int64)
+        self.nwin, self.k_host = len(wo) - 1, int(k_host)
+        dev = ctx.device
+        with torch.cuda.stream(ctx.stream):
+            self.slot_mask = torch.empty(max(self.k_host, 1), dtype=torch.int32, device=dev)
+            self.phys_of_slot = torch.empty(max(self.k_host, 1), dtype=torch.int32, device=dev)
+            self.phys_ids = torch.empty(max(self.k_host, 1), dtype=torch.int32, device=dev)
+        gs = np.zeros(max_groups, np.int64)
+        gm = np.zeros(max_groups, np.uint32)
+        ng = i64()
+        _check(load_library().dgnn_host_order(ctx.handle, _ptr(addr), P(wo.ctypes.data), self.nwin, _ptr(host_ids),
+                                              self.k_host, _ptr(self.phys_ids), _ptr(self.phys_of_slot),
+                                              _ptr(self.slot_mask), int(max_groups), P(gs.ctypes.data),
+                                              P(gm.ctypes.data), ctypes.byref(ng)), "dgnn_host_order")
+        self.n_groups = int(ng.value)
+        self.ranges, self.rows = [], []
+        cap = max(self.n_groups, 1)
+        for w in range(self.nwin):
+            rg = np.zeros(3 * cap, np.int64)
+            nr, rows = i64(), i64()
+            _check(load_library().dgnn_host_order_ranges(P(gs.ctypes.data), P(gm.ctypes.data), self.n_groups,
+                                                         self.k_host, w, P(rg.ctypes.data), cap, ctypes.byref(nr),
+                                                         ctypes.byref(rows)), "dgnn_host_order_ranges")
+            self.ranges.append(rg[:3 * int(nr.value)].copy())
+            self.rows.append(int(rows.value))
+        with torch.cuda.stream(ctx.stream):
+            cat = np.concatenate(self.ranges + [np.zeros(1, np.int64)])
+            src = torch.from_numpy(cat).pin_memory()
+            flat = src.to(dev, non_blocking=True)
+        self._src = src
+        offs = np.concatenate([[0], np.cumsum([len(r) for r in self.ranges])])
+        self.ranges_dev = [flat[int(offs[w]):int(offs[w + 1])] for w in range(self.nwin)]
+
+
+def dgnn_host_window_ranges(ctx: Ctx, ho: HostOrder, window: int, smap: torch.Tensor):
+    _check(load_library().dgnn_host_window_ranges(ctx.handle, _ptr(ho.slot_mask), _ptr(ho.phys_of_slot), ho.k_host,
+                                                  int(window), _ptr(ho.ranges_dev[window]),
+                                                  len(ho.ranges[window]) // 3, _ptr(smap)), "dgnn_host_window_ranges")
+
+
+def dgnn_copy_ranges(ctx: Ctx, dst, src_host_ptr: int, ranges, row_bytes: int):
+    import numpy as np
+    rg = np.ascontiguousarray(ranges, dtype=np.int64)
+    _check(load_library().dgnn_copy_ranges(ctx.handle, _ptr(dst), P(src_host_ptr), P(rg.ctypes.data) if rg.size
+                                           else P(0), len(rg) // 3, int(row_bytes)), "dgnn_copy_ranges")
+
+
+def dgnn_remap_ids_dev(ctx: Ctx, ids: torch.Tensor, n_dev: torch.Tensor, table: torch.Tensor):
+    _check(load_library().dgnn_remap_ids_dev(ctx.handle, _ptr(ids), _ptr(n_dev), ids.numel(), _ptr(table)),
+           "dgnn_remap_ids_dev")
+
+
 def dgnn_pack(ctx: Ctx, features: torch.Tensor, packed_ids: torch.Tensor, packed_off: torch.Tensor,
               chunk_off: torch.Tensor, total_rows: int, group_bytes: int, group_buf: torch.Tensor):
     row_bytes = features.element_size() * (features.numel() // max(features.shape[0], 1))
@@ -714,10 +779,12 @@ class DiskPlan:
 
 
 def dgnn_disk_plan_build(ctx: Ctx, idx: DiskIndex, row_bytes: int, s: int, m: int, k: int = 4, seed: int = 0,
-                         reorder: bool = True) -> DiskPlan:
+                         reorder: bool = True, literal: bool = False) -> DiskPlan:
+    """``literal``: Algorithm 1 line 8 as printed (scalar MinHash over the k functions)."""
     h = P()
     _check(load_library().dgnn_disk_plan_build(ctx.handle, idx.handle, int(row_bytes), int(s), int(m), int(k),
-                                               int(seed) & (2**64 - 1), int(bool(reorder)), ctypes.byref(h)),
+                                               int(seed) & (2**64 - 1), (2 if literal else 1) if reorder else 0,
+                                               ctypes.byref(h)),
            "dgnn_disk_plan_build")
     return DiskPlan(ctx, h, int(idx.packed_off_host[-1]))
 

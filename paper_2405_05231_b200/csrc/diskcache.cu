@@ -194,6 +194,15 @@ __global__ void k_signatures(const uint32_t* __restrict__ ent_j, int64_t ne, con
     }
 }
 
+// reading d6 vs Algorithm 1 line 8 as printed (reorder = 2): S(v) = min over t of S_t(v)
+__global__ void k_sig_min(uint32_t* __restrict__ sig, int64_t ne, int k) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ne; e += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t mn = sig[e];
+        for (int t = 1; t < k; ++t) mn = min(mn, sig[(int64_t)t * ne + e]);
+        sig[e] = mn;
+    }
+}
+
 __global__ void k_iota(uint32_t* __restrict__ a, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         a[i] = (uint32_t)i;
@@ -648,8 +657,14 @@ extern "C" dgnn_status dgnn_disk_plan_build(dgnn_ctx* c, const dgnn_disk_index* 
                 DGNN_CK_LAUNCH();
                 return radix::sort_pairs(c, ne, bits, &ky, &o, &ka, &oa);
             };
-            if (reorder)
+            if (reorder == 2) {  // Algorithm 1 line 8 verbatim: one scalar min over the k functions
+                launch(c, DGNN_K_DISK_PLAN, 0.0,
+                       [&] { k_sig_min<<<grid1(c, ne), 256, 0, c->stream>>>(sig.p, ne, kk); });
+                DGNN_CK_LAUNCH();
+                DGNN_TRY(pass(sig.p, bits_for(si - 1)));
+            } else if (reorder) {
                 for (int t = k - 1; t >= 0; --t) DGNN_TRY(pass(sig.p + (int64_t)t * ne, bits_for(si - 1)));
+            }
             DGNN_TRY(pass(ent_seg.p, bits_for(nseg - 1)));
             if (o != ord.p) std::swap(ord.p, ord_alt.p);  // the sorted order lives in ord.p
         }

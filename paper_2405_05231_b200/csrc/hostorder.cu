@@ -1,0 +1,221 @@
+// hostorder.cu -- the window-ordered host tier ("window-ordered host tier").
+//
+// a9 reads the host (CPU-cache) tier over PCIe once per window of W consecutive batches: each
+// window needs the distinct host rows its batches address (≈ half of the tier at papers scale,
+// W = 128), scattered over the tier in slot order, so an SM-driven UVA gather moves them at
+// ~0.7-0.8 of the link rate.  The paper reorders its disk cache so that the rows one segment of
+// batches needs share pages (Sec. 5.1, Algorithm 1); here the windows are known when the
+// layout is built, so the host tier can be ordered exactly: slot s gets the window-membership mask
+// m(s) (bit w = some batch of window w addresses s), and the tier is laid out physically in
+// (m(s), s) order.  Rows with equal masks form one contiguous group; window w needs exactly the
+// groups whose mask has bit w, i.e. a few hundred contiguous ranges, which the copy engine moves
+// at the full link rate.  Slots, tier_map and every address stay as the oracle defines them
+// (reading c17); only the physical row of a slot changes, and every reader goes through a map.
+//
+//   dgnn_host_order         masks, physical order (radix sort), phys_ids for the tier fill, groups
+//   dgnn_host_order_ranges  host: window w's physical ranges and their staging offsets
+//   dgnn_host_window_ranges smap[slot] = staging row of the slot in window w
+//   dgnn_copy_ranges        the copy-engine copies of a window's ranges (H2D)
+//   dgnn_remap_ids_dev      ids[i] = table[ids[i]] (slot -> physical row for the generic gather)
+#include <algorithm>
+
+#include "internal.cuh"
+
+namespace dgnn {
+namespace {
+
+__global__ void k_host_masks(const uint32_t* __restrict__ addr, int64_t n, uint32_t bit, int64_t kh,
+                             uint32_t* __restrict__ mask) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t a = addr[i];
+        const int64_t slot = a & DGNN_SLOT_MASK;
+        if ((a >> DGNN_TIER_SHIFT) == DGNN_TIER_HOST && slot < kh && !(mask[slot] & bit)) atomicOr(&mask[slot], bit);
+    }
+}
+
+__global__ void k_iota(uint32_t* __restrict__ v, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        v[i] = (uint32_t)i;
+}
+
+__global__ void k_phys(const uint32_t* __restrict__ skey, const uint32_t* __restrict__ sslot, int64_t kh,
+                       const int32_t* __restrict__ host_ids, int32_t* __restrict__ phys_ids,
+                       int32_t* __restrict__ phys_of_slot) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < kh; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t s = sslot[i];
+        phys_of_slot[s] = (int32_t)i;
+        phys_ids[i] = host_ids[s];
+    }
+}
+
+__global__ void k_window_smap(const uint32_t* __restrict__ mask, const int32_t* __restrict__ phys_of_slot, int64_t kh,
+                              uint32_t bit, const int64_t* __restrict__ ranges, int nr, int32_t* __restrict__ smap) {
+    extern __shared__ int64_t s_rg[];  // [3 * nr]: phys_lo, phys_hi, stage_lo
+    for (int i = threadIdx.x; i < 3 * nr; i += blockDim.x) s_rg[i] = ranges[i];
+    __syncthreads();
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < kh; s += (int64_t)gridDim.x * blockDim.x) {
+        if (!(mask[s] & bit)) continue;
+        const int64_t p = phys_of_slot[s];
+        int lo = 0, hi = nr;  // the range with phys_lo <= p
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (s_rg[3 * mid] <= p) lo = mid;
+            else hi = mid;
+        }
+        smap[s] = (int32_t)(s_rg[3 * lo + 2] + (p - s_rg[3 * lo]));
+    }
+}
+
+__global__ void k_remap_ids(int32_t* __restrict__ ids, const int64_t* __restrict__ n_dev, int64_t n_max,
+                            const int32_t* __restrict__ table) {
+    const int64_t n = min(*n_dev, n_max);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        ids[i] = table[ids[i]];
+}
+
+}  // namespace
+}  // namespace dgnn
+
+using namespace dgnn;
+
+extern "C" dgnn_status dgnn_host_order(dgnn_ctx* c, const uint32_t* addr, const int64_t* win_node_off_host,
+                                       int32_t nwin, const int32_t* host_ids, int64_t k_host, int32_t* phys_ids,
+                                       int32_t* phys_of_slot, uint32_t* slot_mask, int64_t max_groups,
+                                       int64_t* group_start_host, uint32_t* group_mask_host, int64_t* n_groups) {
+    DGNN_REQUIRE(c && win_node_off_host && n_groups && nwin >= 1 && nwin <= 32 && k_host >= 0 && max_groups >= 1,
+                 "dgnn_host_order: bad argument (1 <= nwin <= 32)");
+    DGNN_REQUIRE(k_host == 0 || (host_ids && phys_ids && phys_of_slot && slot_mask && group_start_host && group_mask_host),
+                 "dgnn_host_order: NULL array");
+    DGNN_REQUIRE(win_node_off_host[nwin] == 0 || addr, "dgnn_host_order: NULL addr");
+    *n_groups = 0;
+    if (k_host == 0) return DGNN_OK;
+    DGNN_CK(cudaSetDevice(c->device));
+    DGNN_TRY(memset_async(c, slot_mask, 0, sizeof(uint32_t) * (size_t)k_host));
+    for (int w = 0; w < nwin; ++w) {
+        const int64_t a = win_node_off_host[w], n = win_node_off_host[w + 1] - a;
+        DGNN_REQUIRE(n >= 0, "dgnn_host_order: window node offsets must be non-decreasing");
+        if (n == 0) continue;
+        launch(c, DGNN_K_HOST_WINDOW, 0.0, [&] {
+            k_host_masks<<<grid_for(c, n, 256), 256, 0, c->stream>>>(addr + a, n, 1u << w, k_host, slot_mask);
+        });
+        DGNN_CK_LAUNCH();
+    }
+    // physical order: slots sorted by (mask, slot) -- a stable radix sort on the nwin mask bits
+    DevBuf<uint32_t> keys, vals, keys_alt, vals_alt;
+    DGNN_TRY(keys.alloc_kept(c, (size_t)k_host));
+    DGNN_TRY(vals.alloc_kept(c, (size_t)k_host));
+    DGNN_TRY(keys_alt.alloc_kept(c, (size_t)k_host));
+    DGNN_TRY(vals_alt.alloc_kept(c, (size_t)k_host));
+    DGNN_CK(cudaMemcpyAsync(keys.p, slot_mask, sizeof(uint32_t) * (size_t)k_host, cudaMemcpyDeviceToDevice, c->stream));
+    launch(c, DGNN_K_MISC, 0.0, [&] { k_iota<<<grid_for(c, k_host, 256), 256, 0, c->stream>>>(vals.p, k_host); });
+    DGNN_CK_LAUNCH();
+    uint32_t *k0 = keys.p, *v0 = vals.p, *k1 = keys_alt.p, *v1 = vals_alt.p;
+    DGNN_TRY(radix::sort_pairs(c, k_host, nwin, &k0, &v0, &k1, &v1));
+    launch(c, DGNN_K_HOST_WINDOW, 0.0, [&] {
+        k_phys<<<grid_for(c, k_host, 256), 256, 0, c->stream>>>(k0, v0, k_host, host_ids, phys_ids, phys_of_slot);
+    });
+    DGNN_CK_LAUNCH();
+    // groups: maximal runs of equal mask in physical order (compacted with one scan)
+    DevBuf<int64_t> gstart, total;
+    DevBuf<uint32_t> gmask;
+    DGNN_TRY(gstart.alloc(c, (size_t)max_groups));
+    DGNN_TRY(gmask.alloc(c, (size_t)max_groups));
+    DGNN_TRY(total.alloc(c, 1));
+    {
+        const uint32_t* sk = k0;
+        int64_t* gs = gstart.p;
+        uint32_t* gm = gmask.p;
+        const int64_t cap = max_groups;
+        auto in = [=] __device__(int64_t i) -> int32_t { return (i == 0 || sk[i] != sk[i - 1]) ? 1 : 0; };
+        auto out = [=] __device__(int64_t i, int64_t excl, int64_t v) {
+            if (v && excl < cap) {
+                gs[excl] = i;
+                gm[excl] = sk[i];
+            }
+        };
+        DGNN_TRY(scan::run(c, k_host, nullptr, in, out, total.p));
+    }
+    int64_t ng = 0;
+    DGNN_CK(cudaMemcpyAsync(&ng, total.p, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    DGNN_CK(cudaStreamSynchronize(c->stream));
+    *n_groups = ng;
+    if (ng > max_groups) {
+        set_error("dgnn_host_order: %lld mask groups exceed max_groups %lld", (long long)ng, (long long)max_groups);
+        return DGNN_ERANGE;
+    }
+    DGNN_CK(cudaMemcpy(group_start_host, gstart.p, sizeof(int64_t) * (size_t)ng, cudaMemcpyDeviceToHost));
+    DGNN_CK(cudaMemcpy(group_mask_host, gmask.p, sizeof(uint32_t) * (size_t)ng, cudaMemcpyDeviceToHost));
+    return DGNN_OK;
+}
+
+extern "C" dgnn_status dgnn_host_order_ranges(const int64_t* group_start_host, const uint32_t* group_mask_host,
+                                              int64_t n_groups, int64_t k_host, int32_t window, int64_t* ranges_host,
+                                              int64_t capacity, int64_t* n_ranges, int64_t* rows) {
+    DGNN_REQUIRE(n_ranges && rows && n_groups >= 0 && window >= 0 && window < 32 && capacity >= 0 &&
+                     (n_groups == 0 || (group_start_host && group_mask_host)) && (capacity == 0 || ranges_host),
+                 "dgnn_host_order_ranges: bad argument");
+    int64_t nr = 0, stage = 0;
+    for (int64_t g = 0; g < n_groups; ++g) {
+        if (!((group_mask_host[g] >> window) & 1u)) continue;
+        const int64_t lo = group_start_host[g], hi = g + 1 < n_groups ? group_start_host[g + 1] : k_host;
+        if (nr > 0 && ranges_host[3 * (nr - 1) + 1] == lo) {
+            ranges_host[3 * (nr - 1) + 1] = hi;  // adjacent group: one longer range
+        } else {
+            DGNN_REQUIRE(nr < capacity, "dgnn_host_order_ranges: more than %lld ranges", (long long)capacity);
+            ranges_host[3 * nr] = lo;
+            ranges_host[3 * nr + 1] = hi;
+            ranges_host[3 * nr + 2] = stage;
+            ++nr;
+        }
+        stage += hi - lo;
+    }
+    *n_ranges = nr;
+    *rows = stage;
+    return DGNN_OK;
+}
+
+extern "C" dgnn_status dgnn_host_window_ranges(dgnn_ctx* c, const uint32_t* slot_mask, const int32_t* phys_of_slot,
+                                               int64_t k_host, int32_t window, const int64_t* ranges_dev, int64_t nr,
+                                               int32_t* smap) {
+    DGNN_REQUIRE(c && window >= 0 && window < 32 && nr >= 0 && k_host >= 0 &&
+                     (k_host == 0 || (slot_mask && phys_of_slot && smap)) && (nr == 0 || ranges_dev),
+                 "dgnn_host_window_ranges: bad argument");
+    DGNN_REQUIRE(nr <= 4096, "dgnn_host_window_ranges: at most 4096 ranges per window");
+    if (k_host == 0 || nr == 0) return DGNN_OK;
+    DGNN_CK(cudaSetDevice(c->device));
+    const size_t smem = sizeof(int64_t) * 3 * (size_t)nr;
+    if (smem > 48 * 1024)
+        DGNN_CK(cudaFuncSetAttribute(k_window_smap, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    launch(c, DGNN_K_HOST_WINDOW, 0.0, [&] {
+        k_window_smap<<<grid_for(c, k_host, 256), 256, smem, c->stream>>>(slot_mask, phys_of_slot, k_host, 1u << window,
+                                                                          ranges_dev, (int)nr, smap);
+    });
+    DGNN_CK_LAUNCH();
+    return DGNN_OK;
+}
+
+extern "C" dgnn_status dgnn_copy_ranges(dgnn_ctx* c, void* dst_dev, const void* src_host, const int64_t* ranges_host,
+                                        int64_t nr, int64_t row_bytes) {
+    DGNN_REQUIRE(c && row_bytes > 0 && nr >= 0 && (nr == 0 || (dst_dev && src_host && ranges_host)),
+                 "dgnn_copy_ranges: bad argument");
+    DGNN_CK(cudaSetDevice(c->device));
+    for (int64_t r = 0; r < nr; ++r) {
+        const int64_t lo = ranges_host[3 * r], hi = ranges_host[3 * r + 1], st = ranges_host[3 * r + 2];
+        DGNN_REQUIRE(hi >= lo && st >= 0, "dgnn_copy_ranges: bad range");
+        DGNN_CK(cudaMemcpyAsync((uint8_t*)dst_dev + st * row_bytes, (const uint8_t*)src_host + lo * row_bytes,
+                                (size_t)((hi - lo) * row_bytes), cudaMemcpyHostToDevice, c->stream));
+    }
+    return DGNN_OK;
+}
+
+extern "C" dgnn_status dgnn_remap_ids_dev(dgnn_ctx* c, int32_t* ids, const int64_t* n_dev, int64_t n_max,
+                                          const int32_t* table) {
+    DGNN_REQUIRE(c && n_dev && n_max >= 0 && (n_max == 0 || (ids && table)), "dgnn_remap_ids_dev: bad argument");
+    if (n_max == 0) return DGNN_OK;
+    DGNN_CK(cudaSetDevice(c->device));
+    launch(c, DGNN_K_HOST_WINDOW, 0.0, [&] {
+        k_remap_ids<<<grid_for(c, n_max, 256), 256, 0, c->stream>>>(ids, n_dev, n_max, table);
+    });
+    DGNN_CK_LAUNCH();
+    return DGNN_OK;
+}

@@ -127,6 +127,8 @@ class Layout:
     disk_plan: A.DiskPlan | None = None  # segmented disk cache (Sec. 5.1), when a disk budget is set
     cache_off: int = 0              # byte offset of the segment caches in the disk tier
     sec_abs: np.ndarray = None      # [nb] disk-tier byte offset of each batch's graph section
+    host_order: A.HostOrder | None = None  # window-ordered host tier (physical rows permuted)
+    host_order_key: tuple = None    # (host_window, out_budget) the ordering was built for
 
     def phase_ms(self) -> dict:
         """Device time of the layout's phases (after the stream has passed them)."""
@@ -176,9 +178,32 @@ class Layout:
                 part = torch.empty(max(rows * self.row_bytes, 16), dtype=torch.uint8, device=dev)
                 zero = torch.zeros(2, dtype=torch.int64, device=dev)
                 chunk = self._partial(self.ctx, b, b + 1, chunk, zero, zero, pages, part)
-        A.dgnn_assemble(self.ctx, self.addr[n0:n1], self.gpu_tier, self.plan.k_gpu, self.host_tier.ptr,
-                        self.plan.k_host, chunk, rows, self.row_bytes, out)
+        if self.host_order is None:
+            A.dgnn_assemble(self.ctx, self.addr[n0:n1], self.gpu_tier, self.plan.k_gpu, self.host_tier.ptr,
+                            self.plan.k_host, chunk, rows, self.row_bytes, out)
+        else:  # window-ordered host tier: slot s is physical row phys_of_slot[s]
+            with torch.cuda.stream(self.ctx.stream):
+                t = torch.tensor([0, n1 - n0, 0, 1 << 62, 0, rows], dtype=torch.int64).to(self.ctx.device,
+                                                                                          non_blocking=False)
+            A.dgnn_assemble_group(self.ctx, self.addr[n0:n1], t[0:2], n1 - n0, self.gpu_tier, self.plan.k_gpu,
+                                  self.host_tier.ptr, self.plan.k_host, chunk, t[2:4], t[4:6], self.row_bytes, out,
+                                  host_map=self.host_order.phys_of_slot)
         return out
+
+    def host_windows(self, host_window: int, out_budget: int = 1 << 30):
+        """The assembler's host-row windows: (first run, last run + 1) over assembly_groups(out_budget),
+        each spanning fewer than ``host_window`` batches past its first run's start."""
+        groups = self.assembly_groups(out_budget)
+        windows = []
+        if host_window > 1 and self.plan.k_host > 0:
+            r0 = 0
+            while r0 < len(groups):
+                r1 = r0 + 1
+                while r1 < len(groups) and groups[r1 - 1][1] - groups[r0][0] < host_window:
+                    r1 += 1
+                windows.append((r0, r1))
+                r0 = r1
+        return groups, windows
 
     def _cache_rows(self) -> torch.Tensor:
         """The segment caches as [pages, 4096] (pinned host through UVA, or HBM)."""
@@ -310,15 +335,9 @@ class Layout:
         no = self.samples.node_off_host
         dev = ctx.device
         kh = self.plan.k_host
-        windows = []  # (first run, last run + 1)
-        if host_window > 1 and kh > 0:
-            r0 = 0
-            while r0 < len(groups):
-                r1 = r0 + 1
-                while r1 < len(groups) and groups[r1 - 1][1] - groups[r0][0] < host_window:
-                    r1 += 1
-                windows.append((r0, r1))
-                r0 = r1
+        windows = self.host_windows(host_window, out_budget)[1]  # (first run, last run + 1)
+        ho = self.host_order
+        ordered = ho is not None and bool(windows) and self.host_order_key == (host_window, int(out_budget))
         def buf(name, n, dtype=torch.uint8, shape=None):
             """n elements of dtype, from the workspace when there is one (grow-only, >= 16 bytes)."""
             esz = torch.empty(0, dtype=dtype).element_size()
@@ -345,13 +364,15 @@ class Layout:
                 # staging rows: the window's host-row accesses bound its distinct host rows
                 hpre = np.concatenate([[0], np.cumsum(self.batch_tiers[:, 1])])
                 cap = min(kh, max(int(hpre[groups[r1 - 1][1]] - hpre[groups[r0][0]]) for r0, r1 in windows))
+                if ordered:
+                    cap = max(ho.rows)  # exact: the rows of each window's physical ranges
                 stamp = buf("stamp", kh, torch.int32)
                 stamp.fill_(-1)  # window ids restart at 0 every epoch
                 nbuf = 2 if gctx is not ctx else 1
                 smap = [buf(f"smap{i}", kh, torch.int32) for i in range(nbuf)]
                 wlist = [buf(f"wlist{i}", max(cap, 1), torch.int32) for i in range(nbuf)]
                 wcount = [buf(f"wcount{i}", 1, torch.int64) for i in range(nbuf)]
-                use_runs = self.row_bytes % 16 == 0 and os.environ.get("DGNN_GATHER_RUNS", "0") == "1"
+                use_runs = self.row_bytes % 16 == 0 and os.environ.get("DGNN_GATHER_RUNS", "0") == "1" and ho is None
                 if use_runs:  # runs of consecutive host slots: one contiguous copy each
                     wruns = [buf(f"wruns{i}", max(cap, 1), torch.int32) for i in range(nbuf)]
                     wnruns = [buf(f"wnruns{i}", 1, torch.int64) for i in range(nbuf)]
@@ -368,8 +389,21 @@ class Layout:
             if w >= nbuf and gctx is not ctx:
                 gctx.stream.wait_event(ev_done[w - nbuf])  # the runs that used this buffer are done
             w0, w1 = windows[w]
+            if ordered:
+                # window-ordered host tier: the window's rows are a few physical ranges -> copy engine
+                A.dgnn_host_window_ranges(gctx, ho, w, smap[s])
+                A.dgnn_copy_ranges(gctx, staging[s], self.host_tier.ptr, ho.ranges[w], self.row_bytes)
+                if pcie_rows is not None:
+                    with torch.cuda.stream(gctx.stream):
+                        pcie_rows.add_(ho.rows[w])
+                ev = torch.cuda.Event()
+                ev.record(gctx.stream)
+                ev_ready[w] = ev
+                return
             A.dgnn_host_window(gctx, self.addr[spans[w0][0]:spans[w1 - 1][1]], w, stamp, kh, wlist[s], smap[s],
                                wcount[s])
+            if ho is not None:  # (windows other than the ordering's) slot list -> physical rows
+                A.dgnn_remap_ids_dev(gctx, wlist[s], wcount[s], ho.phys_of_slot)
             if use_runs:
                 A.dgnn_host_window_runs(gctx, stamp, kh, w, smap[s], wruns[s], wnruns[s])
                 A.dgnn_gather_runs_dev(gctx, self.host_tier.ptr, self.row_bytes, wlist[s], wcount[s], wruns[s],
@@ -428,7 +462,7 @@ class Layout:
             if windows:
                 host_src, host_map = staging[cur], smap[cur]
             else:
-                host_src, host_map = self.host_tier.ptr, None
+                host_src, host_map = self.host_tier.ptr, (ho.phys_of_slot if ho is not None else None)
             if peer_tier is not None:
                 A.dgnn_assemble_group_peer(ctx, self.addr[n0:n1], t[:k + 1], n1 - n0, peer_tier.peers,
                                            self.plan.k_gpu, peer_tier.world, host_src, kh, chunk, t[k + 1:2 * k + 2],
@@ -498,7 +532,7 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
                    direct_io: bool = True, disk_budget: int | None = None, disk_m: int = 1,
                    disk_k: int = 4, disk_budget_frac: float | None = None, after_sample=None,
                    scratch_ws: Workspace | None = None, before_pack=None, gpu_shard=None,
-                   embed_graph: bool = False) -> Layout:
+                   embed_graph: bool = False, host_order: int | None = None) -> Layout:
     """Run a1-a8 on this rank's batches.
 
     ``seeds`` are this rank's seeds (batch t of them gets bid = batch_id_base + t).
@@ -521,6 +555,9 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
     ``embed_graph``: keep each batch's graph sample in its chunk (reading c22b) and free the
     samples' device arrays once packed: training then reads the graph through the loader stage
     (Layout.train_epoch, dgnn_samples_load); the host-side offsets stay as the layout's metadata.
+    ``host_order`` = W: lay the host tier out in window order (dgnn_host_order) for an assembly with
+    host_window=W (default out_budget): each window's host rows become a few contiguous ranges that
+    the copy engine moves; outputs are unchanged (every reader maps slot -> physical row).
     ``after_sample``: called once the samples are complete (dgnn_sample returns when they are),
     before the rest of the pass is enqueued -- a scheduling hook (bench.py starts the previous
     pass's assembly there, so that sampling never shares the GPU with it).
@@ -576,7 +613,8 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
             A.dgnn_gather_rows(ctx, features, ids, gpu_tier)
     host_tier = ws.host("host_tier", plan.k_host * row_bytes) if ws is not None else \
         HostBuffer(plan.k_host * row_bytes)
-    A.dgnn_gather_rows(ctx, features, plan.host_ids, host_tier.ptr)
+    if not host_order:
+        A.dgnn_gather_rows(ctx, features, plan.host_ids, host_tier.ptr)
     mark("tiers")
     # a6 for every batch of this rank at once
     nb = samples.num_batches
@@ -660,6 +698,25 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
     stats.update(row_bytes=row_bytes, groups=len(groups), packed_rows=int(po[-1]),
                  packed_bytes=int(po[-1]) * row_bytes, arena_bytes=arena_off, chunk_bytes=chunk_bytes,
                  k_gpu=plan.k_gpu, k_host=plan.k_host, total_nodes=total_nodes, total_edges=samples.total_edges)
+    if host_order and plan.k_host > 0:
+        # window-ordered host tier (needs the address tables): fill it in physical order
+        ho = None
+        if nb:
+            groups_a, wins = L.host_windows(int(host_order))
+            if 0 < len(wins) <= 32:
+                no = samples.node_off_host
+                wo = [int(no[groups_a[r0][0]]) for r0, _ in wins] + [int(no[groups_a[wins[-1][1] - 1][1]])]
+                try:
+                    ho = A.HostOrder(ctx, addr, wo, plan.host_ids, plan.k_host)
+                except A.DgnnError:  # too many distinct window masks: keep the slot order
+                    ho = None
+        if ho is not None:
+            L.host_order, L.host_order_key = ho, (int(host_order), 1 << 30)
+            A.dgnn_gather_rows(ctx, features, ho.phys_ids[:plan.k_host], host_tier.ptr)
+            stats["host_order"] = {"windows": ho.nwin, "groups": ho.n_groups,
+                                   "ranges_per_window": [len(r) // 3 for r in ho.ranges], "rows": ho.rows}
+        else:
+            A.dgnn_gather_rows(ctx, features, plan.host_ids, host_tier.ptr)
     if nb:
         L.assembly_plan()  # a9's per-run tables, uploaded here on the layout's stream
     mark("classify")

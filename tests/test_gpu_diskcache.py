@@ -79,6 +79,19 @@ def test_plan_parity(dg, ctx, case):
     _compare(P, ref, int(off[-1]))
 
 
+@pytest.mark.parametrize("case", [c for c in CASES if c[8]][:6])
+def test_plan_parity_literal_algorithm1(dg, ctx, case):
+    """Algorithm 1 line 8 as printed (one scalar MinHash value, the minimum over the k functions,
+    P:368): the kernels' plan equals the oracle's literal plan."""
+    nb, N, rows, alpha, rb, s, m, k, _ = case
+    ids, off = make_packed_lists(nb, N, rows, alpha, seed=nb * 31 + s)
+    seed = 0xD15C0000 + nb
+    ref = oracle.disk_plan(_lists(ids, off), N, rb, s, m, k, seed, True, literal=True)
+    idx = _index(dg, ctx, ids, off, N)
+    P = dg.dgnn_disk_plan_build(ctx, idx, rb, s, m, k, seed, True, literal=True)
+    _compare(P, ref, int(off[-1]))
+
+
 @pytest.mark.parametrize("m", [0, 1, 3])
 def test_space_and_search(dg, ctx, m):
     ids, off = make_packed_lists(70, 4000, 400, 5.0, seed=5 + m)

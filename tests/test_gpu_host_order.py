@@ -1,0 +1,93 @@
+"""The window-ordered host tier against the oracle (run on a B200 with -m gpu).
+
+offline_layout(host_order=W) lays the host tier out physically in (window mask, slot) order so that
+the assembler's host-row windows of W batches are a few contiguous ranges (copy-engine copies).
+Slots, tier map and addresses stay the oracle's; checked here: the masks equal a numpy
+recomputation from the oracle's address tables, the physical order is the (mask, slot) sort, the
+physical tier rows are the oracle's host-tier rows permuted, every window's ranges cover exactly
+its slots, and every batch assembled through every reader -- the ordered windows, other window
+sizes (slot list remapped), per-batch UVA reads and Layout.assemble -- equals the direct gather.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from workload import make_workload
+
+pytestmark = pytest.mark.gpu
+RNG_SEED = 0x5EEDD15C
+FAN, B, GPU_ROWS, HOST_ROWS = [10, 5], 256, 500, 1000
+
+
+@pytest.fixture(scope="module")
+def dg():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_2405_05231_b200 as dg
+    return dg
+
+
+@pytest.fixture(scope="module")
+def tiny():
+    return make_workload("tiny")
+
+
+@pytest.fixture(scope="module")
+def ref(tiny):
+    return oracle.offline_layout(tiny.indptr.numpy(), tiny.indices.numpy(), tiny.features.numpy(),
+                                 tiny.seeds.numpy(), B, FAN, RNG_SEED, GPU_ROWS, HOST_ROWS, 8)
+
+
+@pytest.mark.parametrize("W,budget,group", [(2, 1 << 30, 8), (3, 1 << 30, 3), (1, 1 << 30, 8), (4, 600_000, 2)])
+def test_window_ordered_host_tier(dg, tiny, ref, W, budget, group):
+    ctx = dg.Ctx(device=0)
+    dev = torch.device("cuda", 0)
+    gctx = dg.Ctx(device=0, stream=torch.cuda.Stream())
+    L = dg.offline_layout(ctx, tiny.indptr.to(dev), tiny.indices.to(dev), tiny.features.to(dev), tiny.seeds.to(dev),
+                          FAN, B, GPU_ROWS, HOST_ROWS, RNG_SEED, group_size=group, host_order=W)
+    ctx.sync()
+    feats = tiny.features.numpy()
+    kh = L.plan.k_host
+    if W == 1:
+        assert L.host_order is None  # one batch per window: nothing to order
+        return
+    ho = L.host_order
+    assert ho is not None and L.host_order_key == (W, 1 << 30)
+    # masks from the oracle's address tables and the windows of the default assembly plan
+    groups, wins = L.host_windows(W)
+    want = np.zeros(kh, np.uint32)
+    for w, (r0, r1) in enumerate(wins):
+        for b in range(groups[r0][0], groups[r1 - 1][1]):
+            a = ref["addr"][b]
+            host = a[(a >> 30) == 1] & ((1 << 30) - 1)
+            want[host] |= np.uint32(1 << w)
+    mask = ho.slot_mask[:kh].cpu().numpy().view(np.uint32)
+    assert np.array_equal(mask, want)
+    order = np.lexsort((np.arange(kh), want))  # by mask, then slot
+    phys_of_slot = ho.phys_of_slot[:kh].cpu().numpy()
+    assert np.array_equal(phys_of_slot[order], np.arange(kh))
+    host_rows = L.host_tier.tensor.numpy().reshape(kh, -1)
+    assert np.array_equal(host_rows[phys_of_slot], ref["host_buf"])
+    for w in range(ho.nwin):
+        rg = ho.ranges[w].reshape(-1, 3)
+        covered = np.concatenate([np.arange(lo, hi) for lo, hi, _ in rg]) if len(rg) else np.zeros(0, np.int64)
+        assert np.array_equal(np.sort(covered), np.sort(phys_of_slot[(want >> w) & 1 == 1]))
+        assert ho.rows[w] == len(covered)
+    nodes = ref["samples"]
+    for hw in (W, W + 3, 1):
+        n = 0
+        for b, out in L.assemble_epoch(host_window=hw, gather_ctx=gctx, out_budget=budget):
+            got = out.view(torch.uint8).reshape(out.shape[0], -1).cpu().numpy()
+            assert np.array_equal(got, oracle.assemble(feats, nodes[b].nodes)), f"window {hw} batch {b}"
+            n += 1
+        assert n == len(nodes)
+    for b in (0, len(nodes) - 1):
+        n_b = len(nodes[b].nodes)
+        with torch.cuda.stream(ctx.stream):
+            out = torch.empty((n_b, 128), dtype=torch.float32, device=dev)
+        L.assemble(b, out)
+        ctx.sync()
+        assert np.array_equal(out.view(torch.uint8).reshape(n_b, -1).cpu().numpy(), oracle.assemble(feats, nodes[b].nodes))
+    ctx.sync()
+    gctx.sync()

@@ -75,9 +75,13 @@ def main():
         if s > 0:
             P, ms_plan, host_plan = timed(lambda: dg.dgnn_disk_plan_build(ctx, idx, row_bytes, s, 1, args.k, 7), s_)
             Pi = dg.dgnn_disk_plan_build(ctx, idx, row_bytes, s, 1, args.k, 7, reorder=False)
+            # Algorithm 1 line 8 as printed (scalar MinHash over the k functions) at k and at 1
+            lit = {kk: dg.dgnn_disk_plan_build(ctx, idx, row_bytes, s, 1, kk, 7, literal=True).io_pages
+                   for kk in sorted({1, args.k})}
             cache = torch.empty(max(P.cache_pages, 1) * 4096, dtype=torch.uint8, device=dev)
             _, ms_fill, _ = timed(lambda: dg.dgnn_disk_cache_fill(ctx, P, feats, cache), s_)
             run.update(space_pages=P.space_pages, io_pages=P.io_pages, io_pages_identity=Pi.io_pages,
+                       io_pages_literal={str(kk): v for kk, v in lit.items()},
                        cache_pages=P.cache_pages, chunk_pages=P.chunk_pages, cache_rows=P.n_cache,
                        packed_rows=P.n_packed, requests=P.n_req, plan_ms=round(ms_plan, 2),
                        plan_host_ms=round(host_plan, 2), fill_ms=round(ms_fill, 3),
