@@ -221,7 +221,28 @@ def memory_report(dev, R) -> dict:
             "allocator": os.environ.get("PYTORCH_CUDA_ALLOC_CONF", "")}
 
 
-def make_inputs(cfg_name: str, dev, num_seeds=None):
+def make_sharded_features(cfg, dev, rank: int, ws: int):
+    """The closed-form table partitioned by node range over the ranks: this rank
+    materializes rows [rank * shard_rows, ...) in its own HBM; the others' shards are mapped through
+    CUDA IPC (one-sided reads over NVLink by the tier fill and the pack)."""
+    import paper_2405_05231_b200 as dg
+    from paper_2405_05231_b200 import shard as shard_mod
+    from workload import feature_rows
+    N, dim = cfg["num_nodes"], cfg["dim"]
+    shard_rows = (N + ws - 1) // ws
+    lo, hi = min(N, rank * shard_rows), min(N, (rank + 1) * shard_rows)
+    buf = dg._abi.DeviceBuffer(dev.index or 0, max(hi - lo, 1) * dim * 4)
+    view = buf.view((max(hi - lo, 1), dim), torch.float32)
+    step = 1 << 22
+    for r0 in range(lo, hi, step):
+        r1 = min(hi, r0 + step)
+        view[r0 - lo:r1 - lo] = feature_rows(torch.arange(r0, r1, device=dev, dtype=torch.int64), dim)
+    torch.cuda.synchronize()
+    exchange = shard_mod.all_gather_handles if ws > 1 else (lambda h: [h])
+    return dg._abi.ShardedFeatures(buf, N, shard_rows, dim, torch.float32, rank, ws, exchange)
+
+
+def make_inputs(cfg_name: str, dev, num_seeds=None, shard_features=False, rank=0, ws=1):
     from workload import CONFIGS, make_graph, make_seeds, make_features, config_rows
     cfg = dict(CONFIGS[cfg_name])
     if num_seeds is not None:
@@ -229,20 +250,24 @@ def make_inputs(cfg_name: str, dev, num_seeds=None):
         # whole-epoch disk tier exceeds the box's host memory (Friendster: ~300 GB of chunks)
         cfg["num_seeds"] = num_seeds
     feat_bytes = cfg["num_nodes"] * cfg["dim"] * 4
-    if feat_bytes > 0.8 * torch.cuda.get_device_properties(dev).total_memory:
-        # IGB-shaped (409.6 GB of features): the table needs the GPU tier sharded over 8 GPUs and
-        # a host larger than this box's; bench.py replicates features per rank
+    if feat_bytes / (ws if shard_features else 1) > 0.6 * torch.cuda.get_device_properties(dev).total_memory:
+        # IGB-shaped (409.6 GB of features): only partitioned over >= 4 GPUs' HBM (--shard-features)
         raise SystemExit(f"bench.py: config {cfg_name!r} has {feat_bytes / 1e9:.0f} GB of features, more than "
-                         f"one GPU holds; it is a parity case only (tests/test_gpu_bigconfigs.py)")
+                         f"one GPU holds: run it on >= 4 GPUs with --shard-features --split epoch (parity cases: "
+                         f"tests/test_gpu_bigconfigs.py, tests/test_gpu_sharded_features.py)")
     t = time.time()
     indptr, indices = make_graph(cfg["num_nodes"], cfg["num_edges"], cfg["degree"], cfg["skew"], 0, dev)
     seeds = make_seeds(cfg["num_nodes"], cfg["num_seeds"], 0, dev)
     torch.cuda.synchronize()
     log(f"[bench] graph {cfg_name}: N={indptr.numel() - 1} E={indices.numel()} in {time.time() - t:.1f}s")
     t = time.time()
-    feats = make_features(cfg["num_nodes"], cfg["dim"], dev, fseed=1)
+    if shard_features:
+        feats = make_sharded_features(cfg, dev, rank, ws)
+    else:
+        feats = make_features(cfg["num_nodes"], cfg["dim"], dev, fseed=1)
     torch.cuda.synchronize()
-    log(f"[bench] features {tuple(feats.shape)} in {time.time() - t:.1f}s")
+    log(f"[bench] features {tuple(feats.shape)}{' partitioned over %d ranks' % ws if shard_features else ''} "
+        f"in {time.time() - t:.1f}s")
     gpu_rows, host_rows = config_rows(cfg)
     return cfg, indptr, indices, seeds, feats, gpu_rows, host_rows
 
@@ -327,7 +352,8 @@ class Runner:
             return
         from paper_2405_05231_b200 import shard
         cfg, indptr, indices, seeds, feats, gpu_rows, host_rows = self.inp
-        row_bytes = feats.element_size() * (feats.numel() // max(feats.shape[0], 1))
+        row_bytes = feats.row_bytes if hasattr(feats, "row_bytes") else \
+            feats.element_size() * (feats.numel() // max(feats.shape[0], 1))
         exchange = shard.all_gather_handles if ws > 1 else (lambda h: [h])
         self.slots = shard.PeerSlots(self.dev.index or 0, gpu_rows, row_bytes, self.rank, ws, exchange)
 
@@ -576,6 +602,9 @@ def main():
     ap.add_argument("--embed-graph", action="store_true",
                     help="keep each batch's graph sample in its chunk (P:283) and read it back through the graph "
                          "loader for the trainer (implies --train)")
+    ap.add_argument("--shard-features", action="store_true",
+                    help="partition the feature table by node range over the ranks' HBM (SURVEY 8(e)(4)); the tier "
+                         "fill and the pack read remote rows through CUDA IPC peer mappings (needed for IGB: >= 4 GPUs)")
     ap.add_argument("--gpu-tier", default="replicated", choices=["replicated", "peer", "nccl"],
                     help="replicated: every rank holds the whole GPU tier (config rows); peer / nccl: the GPU "
                          "tier is partitioned over the ranks' HBM with N x the config's rows (HBM-budget mode, "
@@ -590,8 +619,11 @@ def main():
         return reference_arm(args, ws, rank, dev)
 
     import paper_2405_05231_b200 as dg
-    inp = make_inputs(args.config, dev, args.num_seeds)
+    inp = make_inputs(args.config, dev, args.num_seeds, shard_features=args.shard_features, rank=rank, ws=ws)
     cfg, indptr, indices, seeds, feats, gpu_rows, host_rows = inp
+    sharded_feats = args.shard_features
+    if sharded_feats:
+        args.no_e2e = True  # the e2e leg pins a host copy of the whole table per rank
     N = indptr.numel() - 1
     nb_epoch = (seeds.numel() + cfg["batch_size"] - 1) // cfg["batch_size"]
     bid_base = None
@@ -734,8 +766,10 @@ def main():
                                 "pipelined: layout of pass e+1 overlaps assembly of pass e (2 streams)")
                                + ("; trainer stub per run on its own stream (depth-2 queue)" if R.train else "")
                                + ("; DGL-block sampling (every node so far resamples)" if args.blocks else ""),
+                   "features": ("partitioned by node range over %d ranks (peer-mapped)" % ws if sharded_feats
+                                else "replicated in every rank's HBM"),
                    "l2": "inputs larger than L2 (features %.1f GB, CSR %.1f GB); no flush needed" % (
-                       feats.numel() * 4 / 1e9, (indptr.numel() * 8 + indices.numel() * 4) / 1e9)},
+                       N * cfg["dim"] * 4 / 1e9, (indptr.numel() * 8 + indices.numel() * 4) / 1e9)},
         "packed_gbs": round(sum_over_ranks(float(stats0["packed_bytes"]), ws) * args.steps / (ms_max / 1e3) / 1e9, 2),
         "pack_kernel_gbs": round(pack_gbs, 1) if pack_gbs else None,
         "roofline": {"bound": "hbm", "achieved": round(pack_gbs, 1) if pack_gbs else None, "peak": hbm_peak,
@@ -798,7 +832,7 @@ def main():
     # ---------------- e2e through the public API with host buffers ----------------
     inp_host = None
     pinned = []
-    in_bytes = sum(t.numel() * t.element_size() for t in (indptr, indices, seeds, feats))
+    in_bytes = sum(t.numel() * t.element_size() for t in (indptr, indices, seeds)) + N * cfg["dim"] * 4
     # every rank pins a host copy of its inputs for the e2e leg: skip it (and say so) when
     # the node's free memory cannot hold world_size copies plus a margin
     avail = _mem_available_bytes()
@@ -807,7 +841,12 @@ def main():
         result["e2e"] = {"value": None, "unit": "mini-batches/s",
                          "skipped": f"host memory: {avail / 2**30:.0f} GiB available < {ws} x "
                                     f"{in_bytes / 2**30:.0f} GiB pinned inputs"}
-    if not args.no_e2e or (not args.no_cpu and rank == 0 and ws == 1):
+    if sharded_feats and not args.no_e2e:
+        args.no_e2e = True
+    if sharded_feats:
+        result["e2e"] = {"value": None, "unit": "mini-batches/s",
+                         "skipped": "features partitioned over ranks: the e2e leg pins a host copy of the whole table"}
+    if not sharded_feats and (not args.no_e2e or (not args.no_cpu and rank == 0 and ws == 1)):
         def pin_like(t):  # exact-size pinned buffer (torch's pinned allocator rounds to powers of two)
             hb = dg.HostBuffer(t.numel() * t.element_size())
             pinned.append(hb)
@@ -866,7 +905,7 @@ def main():
                                   "inputs (CSR, features, seeds) copied from pinned host every step") +
                                  "; counts read back; the disk tier is host-resident by design (a8)"}
     # ---------------- CPU baseline: the oracle on a bounded sample ----------------
-    if not args.no_cpu and rank == 0 and ws == 1:
+    if not args.no_cpu and rank == 0 and ws == 1 and not sharded_feats:
         h_indptr, h_indices, h_seeds, h_feats = inp_host
         try:
             hin = (h_indptr.numpy(), h_indices.numpy(), h_seeds.numpy(), h_feats.numpy().view(np.uint8).reshape(N, -1))
@@ -891,6 +930,11 @@ def reference_arm(args, ws, rank, dev):
         return
     import oracle
     from workload import CONFIGS
+    cfg0 = CONFIGS[args.config]
+    if cfg0["num_nodes"] * cfg0["dim"] * 4 > 0.6 * torch.cuda.get_device_properties(dev).total_memory:
+        print(json.dumps({"impl": "reference", "unavailable": f"the oracle arm materializes the whole "
+                          f"{args.config} feature table on one host; it exceeds this box"}), flush=True)
+        return
     inp = make_inputs(args.config, dev, args.num_seeds)
     cfg, indptr, indices, seeds, feats, gpu_rows, host_rows = inp
     h = (indptr.cpu().numpy(), indices.cpu().numpy(), seeds.cpu().numpy(),

@@ -302,6 +302,19 @@ dgnn_status dgnn_samples_load(dgnn_ctx* ctx, const dgnn_samples* meta, int64_t b
                               const void* base_dev, const int64_t* sec_off_dev, dgnn_samples** out);
 dgnn_status dgnn_samples_drop_device(dgnn_samples* samples);
 
+/* a7 from a feature table partitioned by node range over several devices (the
+ * IGB-shaped table, 409.6 GB, exceeds one GPU): row v lives in shard r = v / shard_rows at row
+ * v - r * shard_rows of peers_dev[r] (a device array of nshards pointers: this rank's own shard and
+ * the CUDA IPC mappings of the others', read over NVLink).  dgnn_pack_sharded / dgnn_gather_rows_sharded
+ * are dgnn_pack / dgnn_gather_rows with that source; row_bytes a multiple of 16, outputs 16-byte
+ * aligned. */
+dgnn_status dgnn_pack_sharded(dgnn_ctx* ctx, const void* const* peers_dev, int64_t shard_rows, int32_t nshards,
+                              int64_t row_bytes, const int32_t* packed_ids, const int64_t* packed_off,
+                              const int64_t* chunk_off, int64_t nb, int64_t total_rows, int64_t group_bytes,
+                              void* group_buf);
+dgnn_status dgnn_gather_rows_sharded(dgnn_ctx* ctx, const void* const* peers_dev, int64_t shard_rows, int32_t nshards,
+                                     int64_t row_bytes, const int32_t* ids, int64_t n, void* out);
+
 /* Batched pack of one packing group: for every batch i < nb and r <
  * |P_i|, group_buf[chunk_off[i] + r*row_bytes ..] = features[P_i[r]] (raw bytes), and
  * the tail of each chunk up to chunk_off[i+1] is zeroed.

@@ -49,6 +49,7 @@ EXPORTS = [
     "dgnn_ctx_set_keep_limit", "dgnn_ctx_kept_bytes", "dgnn_ctx_set_sample_budget", "dgnn_file_set_queues",
     "dgnn_chunk_layout_graph", "dgnn_pack_graph", "dgnn_samples_load", "dgnn_samples_drop_device",
     "dgnn_host_order", "dgnn_host_order_ranges", "dgnn_host_window_ranges", "dgnn_copy_ranges", "dgnn_remap_ids_dev",
+    "dgnn_pack_sharded", "dgnn_gather_rows_sharded",
 ]
 
 
@@ -146,6 +147,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "dgnn_host_window_ranges": (i32, [P, P, P, i64, i32, P, i64, P]),
             "dgnn_copy_ranges": (i32, [P, P, P, P, i64, i64]),
             "dgnn_remap_ids_dev": (i32, [P, P, P, i64, P]),
+            "dgnn_pack_sharded": (i32, [P, P, i64, i32, i64, P, P, P, i64, i64, i64, P]),
+            "dgnn_gather_rows_sharded": (i32, [P, P, i64, i32, i64, P, i64, P]),
             "dgnn_stage_file_write": (i32, [P, P, i64, P, i64, P, i64, ctypes.POINTER(i64)]),
             "dgnn_stage_file_read": (i32, [P, P, i64, P, i64, P, i64, ctypes.POINTER(i64)]),
             "dgnn_pack": (i32, [P, P, i64, i64, P, P, P, i64, i64, i64, P]),
@@ -572,8 +575,53 @@ def dgnn_remap_ids_dev(ctx: Ctx, ids: torch.Tensor, n_dev: torch.Tensor, table: 
            "dgnn_remap_ids_dev")
 
 
-def dgnn_pack(ctx: Ctx, features: torch.Tensor, packed_ids: torch.Tensor, packed_off: torch.Tensor,
+class ShardedFeatures:
+    """A feature table partitioned by node range over ranks: rank r holds rows
+    [r * shard_rows, min((r + 1) * shard_rows, num_rows)) in a DeviceBuffer; ``peers`` (device
+    int64 [world]) points at every shard (this rank's own, the others' CUDA IPC mappings).  Passed as
+    ``features`` to offline_layout / dgnn_pack / dgnn_gather_rows, which then read rows through it."""
+
+    def __init__(self, shard: "DeviceBuffer", num_rows: int, shard_rows: int, dim: int, dtype, rank: int,
+                 world: int, exchange):
+        self.shard, self.num_rows, self.shard_rows, self.dim, self.dtype = shard, int(num_rows), int(shard_rows), \
+            int(dim), dtype
+        self.rank, self.world = rank, world
+        self.row_bytes = torch.empty(0, dtype=dtype).element_size() * self.dim
+        dev = torch.device("cuda", shard.device)
+        handles = exchange(shard.ipc_handle())
+        self.maps, ptrs = [], []
+        for r, h in enumerate(handles):
+            if r == rank:
+                ptrs.append(shard.ptr)
+            else:
+                m = IpcMapping(shard.device, h)
+                self.maps.append(m)
+                ptrs.append(m.ptr)
+        self.peers = torch.tensor(ptrs, dtype=torch.int64, device=dev)
+        self.shape = (self.num_rows, self.dim)
+
+    @classmethod
+    def loopback(cls, shards: list, num_rows: int, shard_rows: int, dim: int, dtype):
+        """Every shard in this process (the single-GPU test of the sharded source)."""
+        self = cls.__new__(cls)
+        self.shard, self.shards, self.num_rows, self.shard_rows, self.dim, self.dtype = shards[0], shards, \
+            int(num_rows), int(shard_rows), int(dim), dtype
+        self.rank, self.world, self.maps = 0, len(shards), []
+        self.row_bytes = torch.empty(0, dtype=dtype).element_size() * self.dim
+        self.peers = torch.tensor([s.ptr for s in shards], dtype=torch.int64, device=torch.device("cuda", shards[0].device))
+        self.shape = (self.num_rows, self.dim)
+        return self
+
+
+def dgnn_pack(ctx: Ctx, features, packed_ids: torch.Tensor, packed_off: torch.Tensor,
               chunk_off: torch.Tensor, total_rows: int, group_bytes: int, group_buf: torch.Tensor):
+    if isinstance(features, ShardedFeatures):
+        f = features
+        _check(load_library().dgnn_pack_sharded(ctx.handle, _ptr(f.peers), f.shard_rows, f.world, f.row_bytes,
+                                                _ptr(packed_ids), _ptr(packed_off), _ptr(chunk_off),
+                                                chunk_off.numel() - 1, int(total_rows), int(group_bytes),
+                                                _ptr(group_buf)), "dgnn_pack_sharded")
+        return
     row_bytes = features.element_size() * (features.numel() // max(features.shape[0], 1))
     nb = chunk_off.numel() - 1
     _check(load_library().dgnn_pack(ctx.handle, _ptr(features), features.shape[0], row_bytes, _ptr(packed_ids),
@@ -581,7 +629,12 @@ def dgnn_pack(ctx: Ctx, features: torch.Tensor, packed_ids: torch.Tensor, packed
                                     _ptr(group_buf)), "dgnn_pack")
 
 
-def dgnn_gather_rows(ctx: Ctx, features: torch.Tensor, ids: torch.Tensor, out: torch.Tensor):
+def dgnn_gather_rows(ctx: Ctx, features, ids: torch.Tensor, out):
+    if isinstance(features, ShardedFeatures):
+        f = features
+        _check(load_library().dgnn_gather_rows_sharded(ctx.handle, _ptr(f.peers), f.shard_rows, f.world, f.row_bytes,
+                                                       _ptr(ids), ids.numel(), _ptr(out)), "dgnn_gather_rows_sharded")
+        return
     row_bytes = features.element_size() * (features.numel() // max(features.shape[0], 1))
     _check(load_library().dgnn_gather_rows(ctx.handle, _ptr(features), features.shape[0], row_bytes, _ptr(ids),
                                            ids.numel(), _ptr(out)), "dgnn_gather_rows")

@@ -22,8 +22,27 @@ constexpr int kPackU = 4;
 constexpr int kPackBlocksPerSM = 4;  // 32 warps per SM: measured best for 512-byte rows (tools/pack_sweep.py)
 constexpr int kMaxSmemSeg = 2048;
 
+// Row sources: one table (HBM, or pinned host through UVA), or a table partitioned by node range
+// over several devices' memory (shard r holds rows [r * shard_rows, (r + 1) * shard_rows), read
+// through peer mappings: SURVEY 8(e)(4), the IGB-shaped table that no single GPU holds)
+struct FlatSrc {
+    const uint8_t* base;
+    int64_t row_bytes;
+    __device__ __forceinline__ const uint8_t* operator()(int32_t id) const { return base + (int64_t)id * row_bytes; }
+};
+struct ShardSrc {
+    const uint8_t* const* peers;
+    int64_t shard_rows;
+    int64_t row_bytes;
+    __device__ __forceinline__ const uint8_t* operator()(int32_t id) const {
+        const int64_t r = id / shard_rows;
+        return peers[r] + (id - r * shard_rows) * row_bytes;
+    }
+};
+
+template <class Src>
 struct PackRow {
-    const uint8_t* src;
+    Src src;
     int64_t row_bytes;
     const int32_t* ids;
     const int64_t* seg;  // packed_off (smem or global), nb+1
@@ -32,14 +51,14 @@ struct PackRow {
     uint8_t* dst;
     __device__ __forceinline__ bool operator()(int64_t r, const uint8_t*& s, uint8_t*& d) const {
         const int b = segment_of(seg, nb + 1, r);
-        s = src + (int64_t)ids[r] * row_bytes;
+        s = src(ids[r]);
         d = dst + chunk_off[b] + (r - seg[b]) * row_bytes;
         return true;
     }
 };
 
-template <class V, int U = kPackU>
-__global__ void __launch_bounds__(256) k_pack(const uint8_t* __restrict__ src, int64_t row_bytes,
+template <class V, int U = kPackU, class Src = FlatSrc>
+__global__ void __launch_bounds__(256) k_pack(Src src, int64_t row_bytes,
                                               const int32_t* __restrict__ ids, const int64_t* __restrict__ packed_off,
                                               const int64_t* __restrict__ chunk_off, int nb, int64_t R,
                                               uint8_t* __restrict__ dst) {
@@ -57,28 +76,29 @@ __global__ void __launch_bounds__(256) k_pack(const uint8_t* __restrict__ src, i
         const int64_t nz = (chunk_off[b + 1] - chunk_off[b] - rows * row_bytes) >> 2;
         for (int64_t i = threadIdx.x & 31; i < nz; i += 32) z[i] = 0u;
     }
-    PackRow fn{src, row_bytes, ids, in_smem ? s_seg : packed_off, chunk_off, nb, dst};
+    PackRow<Src> fn{src, row_bytes, ids, in_smem ? s_seg : packed_off, chunk_off, nb, dst};
     copy_rows_warp<U, V>(R, row_bytes, fn, warp, nwarps);
 }
 
+template <class Src>
 struct GatherRow {
-    const uint8_t* src;
+    Src src;
     int64_t row_bytes;
     const int32_t* ids;
     uint8_t* dst;
     __device__ __forceinline__ bool operator()(int64_t r, const uint8_t*& s, uint8_t*& d) const {
-        s = src + (int64_t)ids[r] * row_bytes;
+        s = src(ids[r]);
         d = dst + r * row_bytes;
         return true;
     }
 };
 
-template <class V>
-__global__ void __launch_bounds__(256) k_gather(const uint8_t* __restrict__ src, int64_t row_bytes,
-                                                const int32_t* __restrict__ ids, int64_t R, uint8_t* __restrict__ dst) {
+template <class V, class Src = FlatSrc>
+__global__ void __launch_bounds__(256) k_gather(Src src, int64_t row_bytes, const int32_t* __restrict__ ids, int64_t R,
+                                                uint8_t* __restrict__ dst) {
     const int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    copy_rows_warp<kPackU, V>(R, row_bytes, GatherRow{src, row_bytes, ids, dst}, warp, nwarps);
+    copy_rows_warp<kPackU, V>(R, row_bytes, GatherRow<Src>{src, row_bytes, ids, dst}, warp, nwarps);
 }
 
 bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
@@ -259,16 +279,15 @@ extern "C" dgnn_status dgnn_pack(dgnn_ctx* c, const void* features, int64_t num_
     const bool v16 = row_bytes % 16 == 0 && aligned16(features) && aligned16(group_buf);
     const int pu = getenv("DGNN_PACK_U") ? atoi(getenv("DGNN_PACK_U")) : kPackU;  // tuning experiment
     const int pbs = getenv("DGNN_PACK_BPS") ? atoi(getenv("DGNN_PACK_BPS")) : kPackBlocksPerSM;
-    using PackK = void (*)(const uint8_t*, int64_t, const int32_t*, const int64_t*, const int64_t*, int, int64_t,
-                           uint8_t*);
+    using PackK = void (*)(FlatSrc, int64_t, const int32_t*, const int64_t*, const int64_t*, int, int64_t, uint8_t*);
     const PackK kern = !v16 ? (PackK)k_pack<uint32_t> : pu == 8 ? (PackK)k_pack<uint4, 8>
                                                       : pu == 2 ? (PackK)k_pack<uint4, 2> : (PackK)k_pack<uint4>;
     const int64_t work = std::max<int64_t>(total_rows * 32 / pu, nb * 32);
     const int grid = grid_resident(c, kern, work, 256, pbs);
     const double bytes = (double)total_rows * (2.0 * row_bytes + 4.0);
     launch(c, DGNN_K_PACK, bytes, [&] {
-        kern<<<grid, 256, 0, c->stream>>>((const uint8_t*)features, row_bytes, packed_ids, packed_off, chunk_off,
-                                          (int)nb, total_rows, (uint8_t*)group_buf);
+        kern<<<grid, 256, 0, c->stream>>>(FlatSrc{(const uint8_t*)features, row_bytes}, row_bytes, packed_ids,
+                                          packed_off, chunk_off, (int)nb, total_rows, (uint8_t*)group_buf);
     });
     DGNN_CK_LAUNCH();
     return DGNN_OK;
@@ -295,11 +314,56 @@ extern "C" dgnn_status dgnn_gather_rows(dgnn_ctx* c, const void* features, int64
     };
     const bool pcie = on_host(features) || on_host(out);
     launch(c, pcie ? DGNN_K_GATHER_PCIE : DGNN_K_GATHER, pcie ? (double)n * row_bytes : (double)n * (2.0 * row_bytes + 4.0), [&] {
+        const FlatSrc src{(const uint8_t*)features, row_bytes};
         if (v16)
-            k_gather<uint4><<<grid, 256, 0, c->stream>>>((const uint8_t*)features, row_bytes, ids, n, (uint8_t*)out);
+            k_gather<uint4><<<grid, 256, 0, c->stream>>>(src, row_bytes, ids, n, (uint8_t*)out);
         else
-            k_gather<uint32_t><<<grid, 256, 0, c->stream>>>((const uint8_t*)features, row_bytes, ids, n,
-                                                             (uint8_t*)out);
+            k_gather<uint32_t><<<grid, 256, 0, c->stream>>>(src, row_bytes, ids, n, (uint8_t*)out);
+    });
+    DGNN_CK_LAUNCH();
+    return DGNN_OK;
+}
+
+// ------------------------------------------- a7 from a table partitioned by node range
+extern "C" dgnn_status dgnn_pack_sharded(dgnn_ctx* c, const void* const* peers_dev, int64_t shard_rows,
+                                         int32_t nshards, int64_t row_bytes, const int32_t* packed_ids,
+                                         const int64_t* packed_off, const int64_t* chunk_off, int64_t nb,
+                                         int64_t total_rows, int64_t group_bytes, void* group_buf) {
+    DGNN_REQUIRE(c && peers_dev && packed_off && chunk_off && (group_buf || group_bytes == 0),
+                 "dgnn_pack_sharded: NULL argument");
+    DGNN_REQUIRE(shard_rows > 0 && nshards >= 1 && row_bytes > 0 && row_bytes % 16 == 0,
+                 "dgnn_pack_sharded: shard_rows > 0, nshards >= 1, row_bytes a positive multiple of 16");
+    DGNN_REQUIRE(nb >= 0 && nb < (1 << 30) && total_rows >= 0 && (packed_ids || total_rows == 0) &&
+                     total_rows * row_bytes <= group_bytes,
+                 "dgnn_pack_sharded: bad sizes");
+    if (nb == 0) return DGNN_OK;
+    DGNN_CK(cudaSetDevice(c->device));
+    DGNN_REQUIRE(aligned16(group_buf), "dgnn_pack_sharded: group_buf must be 16-byte aligned");
+    auto kern = k_pack<uint4, kPackU, ShardSrc>;
+    const int grid = grid_resident(c, kern, std::max<int64_t>(total_rows * 32 / kPackU, nb * 32), 256,
+                                   kPackBlocksPerSM);
+    launch(c, DGNN_K_PACK, (double)total_rows * (2.0 * row_bytes + 4.0), [&] {
+        kern<<<grid, 256, 0, c->stream>>>(ShardSrc{(const uint8_t* const*)peers_dev, shard_rows, row_bytes}, row_bytes,
+                                          packed_ids, packed_off, chunk_off, (int)nb, total_rows, (uint8_t*)group_buf);
+    });
+    DGNN_CK_LAUNCH();
+    return DGNN_OK;
+}
+
+extern "C" dgnn_status dgnn_gather_rows_sharded(dgnn_ctx* c, const void* const* peers_dev, int64_t shard_rows,
+                                                int32_t nshards, int64_t row_bytes, const int32_t* ids, int64_t n,
+                                                void* out) {
+    DGNN_REQUIRE(c && peers_dev && (n == 0 || (ids && out)), "dgnn_gather_rows_sharded: NULL argument");
+    DGNN_REQUIRE(shard_rows > 0 && nshards >= 1 && row_bytes > 0 && row_bytes % 16 == 0 && n >= 0,
+                 "dgnn_gather_rows_sharded: bad sizes");
+    if (n == 0) return DGNN_OK;
+    DGNN_CK(cudaSetDevice(c->device));
+    DGNN_REQUIRE(aligned16(out), "dgnn_gather_rows_sharded: out must be 16-byte aligned");
+    auto kern = k_gather<uint4, ShardSrc>;
+    const int grid = grid_resident(c, kern, n * 32 / kPackU, 256, 8);
+    launch(c, DGNN_K_GATHER, (double)n * (2.0 * row_bytes + 4.0), [&] {
+        kern<<<grid, 256, 0, c->stream>>>(ShardSrc{(const uint8_t* const*)peers_dev, shard_rows, row_bytes}, row_bytes,
+                                          ids, n, (uint8_t*)out);
     });
     DGNN_CK_LAUNCH();
     return DGNN_OK;

@@ -564,8 +564,13 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
     """
     dev = ctx.device
     N = indptr.numel() - 1
-    row_bytes = features.element_size() * (features.numel() // max(features.shape[0], 1))
-    dim = features.numel() // max(features.shape[0], 1)
+    if isinstance(features, A.ShardedFeatures):  # the table partitioned by node range over ranks
+        row_bytes, dim = features.row_bytes, features.dim
+        if disk_budget is not None or disk_budget_frac is not None:
+            raise ValueError("the segmented disk cache reads an unpartitioned feature table")
+    else:
+        row_bytes = features.element_size() * (features.numel() // max(features.shape[0], 1))
+        dim = features.numel() // max(features.shape[0], 1)
     stats = {"_events": []}
 
     import time as _time

@@ -44,6 +44,20 @@ def random_csr(rng, n, max_deg, allow_empty=True):
     return csr_from_adj(n, adj)
 
 
+def random_csr_fast(rng, n, max_deg):
+    """Vectorized random CSR for larger n: out-degree ~ U[0, max_deg], neighbours uniform over the
+    other nodes, duplicates dropped, rows sorted (same contract as random_csr)."""
+    deg = rng.integers(0, max_deg + 1, n)
+    rows = np.repeat(np.arange(n, dtype=np.int64), deg)
+    cols = rng.integers(0, max(n - 1, 1), rows.size)
+    cols = cols + (cols >= rows)  # skip the self-loop
+    code = np.unique(rows * n + cols)
+    r, c = code // n, code % n
+    indptr = np.zeros(n + 1, np.int64)
+    np.add.at(indptr, r + 1, 1)
+    return np.cumsum(indptr), c.astype(np.int32)
+
+
 @pytest.fixture(scope="session")
 def gpu_available():
     try:

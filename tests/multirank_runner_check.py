@@ -23,6 +23,7 @@ sys.path.insert(0, ROOT)
 
 def main():
     split, mode = sys.argv[1], sys.argv[2]
+    shard = len(sys.argv) > 3 and sys.argv[3] == "shard"  # feature table partitioned by node range
     import torch.distributed as dist
 
     import bench
@@ -33,7 +34,8 @@ def main():
     torch.cuda.set_device(0)
     dev = torch.device("cuda", 0)
     dist.init_process_group(os.environ.get("DGNN_BENCH_BACKEND", "gloo"), rank=rank, world_size=ws)
-    cfg, indptr, indices, seeds, feats, gpu_rows, host_rows = bench.make_inputs("tiny", dev)
+    cfg, indptr, indices, seeds, feats, gpu_rows, host_rows = bench.make_inputs("tiny", dev, shard_features=shard,
+                                                                                rank=rank, ws=ws)
     cfg["group_size"] = 3
     B = cfg["batch_size"]
     nb_epoch = (seeds.numel() + B - 1) // B
@@ -70,7 +72,11 @@ def main():
     R.run(3)
     torch.cuda.synchronize()
     ip, ix, sd = indptr.cpu().numpy(), indices.cpu().numpy(), all_seeds.cpu().numpy()
-    f = feats.cpu().numpy()
+    if shard:
+        from workload import feature_rows_np
+        f = feature_rows_np(np.arange(cfg["num_nodes"]), cfg["dim"])
+    else:
+        f = feats.cpu().numpy()
     if split == "epoch":
         ref_all = oracle.sample(ip, ix, sd, B, list(cfg["fanout"]), bench.RNG_SEED)
         mine = ref_all[base:base + (seeds.numel() + B - 1) // B]

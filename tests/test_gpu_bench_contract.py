@@ -100,12 +100,14 @@ def test_two_rank_launch_on_one_gpu(split):
     assert d["e2e"]["value"] > 0
 
 
-@pytest.mark.parametrize("split,mode", [("weak", "replicated"), ("epoch", "replicated"), ("epoch", "peer"),
-                                        ("weak", "peer"), ("epoch", "nccl")])
-def test_two_rank_runner_outputs_equal_the_oracle(split, mode):
+@pytest.mark.parametrize("split,mode,shard", [("weak", "replicated", ""), ("epoch", "replicated", ""),
+                                              ("epoch", "peer", ""), ("weak", "peer", ""), ("epoch", "nccl", ""),
+                                              ("epoch", "peer", "shard"), ("weak", "replicated", "shard")])
+def test_two_rank_runner_outputs_equal_the_oracle(split, mode, shard):
     """bench.py's Runner at world size 2 (both ranks on the one GPU, gloo for the collectives, the
     all-to-all through host memory): every assembled batch of three pipelined passes equals the
-    oracle, for both splits and every GPU-tier mode (tests/multirank_runner_check.py)."""
+    oracle, for both splits, every GPU-tier mode, and the feature table partitioned by node range
+    over the ranks (CUDA IPC mappings) (tests/multirank_runner_check.py)."""
     import socket
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
@@ -113,7 +115,7 @@ def test_two_rank_runner_outputs_equal_the_oracle(split, mode):
     env = dict(os.environ, DGNN_BENCH_SHARE_GPU="1", DGNN_BENCH_BACKEND="gloo")
     p = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
                         "--master-addr=127.0.0.1", f"--master-port={port}", "tests/multirank_runner_check.py",
-                        split, mode], cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
+                        split, mode, shard], cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
     assert p.returncode == 0, p.stderr[-3000:]
     import re
     oks = re.findall(r"rank (\d): (ok|FAIL[^\n]*?)(?=rank \d:|\n|$)", p.stdout)

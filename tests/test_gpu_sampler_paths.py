@@ -12,7 +12,7 @@ import pytest
 import torch
 
 import oracle
-from conftest import csr_from_adj, random_csr
+from conftest import csr_from_adj, random_csr, random_csr_fast
 from workload import make_workload
 
 pytestmark = pytest.mark.gpu
@@ -73,7 +73,7 @@ def _check(S, counts, ref, n):
 def test_random_graphs_both_paths(dg, ctx, path, trial):
     rng = np.random.default_rng(7000 + trial)
     n = int(rng.integers(30, 20000))
-    indptr, indices = random_csr(rng, n, max_deg=int(rng.integers(1, 60)))
+    indptr, indices = random_csr_fast(rng, n, max_deg=int(rng.integers(1, 60)))
     H = int(rng.integers(1, 4))
     fan = [int(x) for x in rng.choice([0, 1, 2, 3, 5, 10, 15, 31, 32, 33, 40], size=H)]
     seeds = rng.permutation(n)[:int(rng.integers(1, n))].astype(np.int32)
@@ -114,7 +114,7 @@ def test_large_batch_uses_table_path(dg, ctx, path):
     """batch_size above the partitioned path's seed-sort limit (4096) still samples bit-exactly."""
     rng = np.random.default_rng(99)
     n = 30000
-    indptr, indices = random_csr(rng, n, max_deg=12)
+    indptr, indices = random_csr_fast(rng, n, max_deg=12)
     seeds = rng.permutation(n)[:12000].astype(np.int32)
     ref = oracle.sample(indptr, indices, seeds, 5000, [4, 3], RNG_SEED)
     S, counts = _run(dg, ctx, indptr, indices, seeds, 5000, [4, 3], RNG_SEED)
@@ -141,7 +141,7 @@ def test_access_counter_modes(dg, ctx, monkeypatch, mode, trial):
         monkeypatch.delenv("DGNN_SAMPLE_COUNT", raising=False)
     rng = np.random.default_rng(9100 + trial)
     n = int(rng.integers(100, 70000))
-    indptr, indices = random_csr(rng, n, max_deg=int(rng.integers(1, 30)))
+    indptr, indices = random_csr_fast(rng, n, max_deg=int(rng.integers(1, 30)))
     fan = [int(x) for x in rng.choice([1, 2, 5, 10, 15], size=int(rng.integers(1, 4)))]
     seeds = rng.permutation(n)[:int(rng.integers(1, min(n, 5000)))].astype(np.int32)
     B = int(rng.integers(1, 700))
