@@ -394,6 +394,15 @@ dgnn_status dgnn_stage_file_read(dgnn_ctx* ctx, dgnn_file* f, int64_t file_off, 
  *   caller keeps the slot-ordered tier).  Synchronizes.
  * dgnn_host_order_ranges: host arithmetic: window w's physical ranges (merged adjacent groups) as
  *   triples (phys_lo, phys_hi, staging_lo) in ranges_host[3 * capacity]; *rows = the window's rows.
+ * dgnn_host_order_schedule: host arithmetic: the staging schedule of all nwin windows in one arena
+ *   of capacity_rows rows.  A group is needed by the maximal runs of consecutive windows in its
+ *   mask; each (group, run) is copied once, at the prefetch of its first window, and stays in the
+ *   arena until its last window is done (window w is prefetched once window w-2 is done), so rows
+ *   shared by consecutive windows cross PCIe once.  Outputs per window w (CSR, copy_off / map_off
+ *   [nwin+1]): the copies to issue (copy_out triples) and the map of every row w reads (map_out
+ *   triples sorted by phys_lo: the input of dgnn_host_window_ranges); *rows_copied = total rows
+ *   moved.  EINVAL if the capacity (>= max over w of |S_{w-1}| + |S_w| always fits) or an output
+ *   capacity is exceeded.
  * dgnn_host_window_ranges: smap[s] = staging row of slot s for every slot of window w (ranges_dev =
  *   the device copy of the triples, nr <= 4096); other entries untouched.
  * dgnn_copy_ranges: one cudaMemcpyAsync (H2D, ctx stream) per triple: rows [phys_lo, phys_hi) of
@@ -407,6 +416,10 @@ dgnn_status dgnn_host_order(dgnn_ctx* ctx, const uint32_t* addr, const int64_t* 
 dgnn_status dgnn_host_order_ranges(const int64_t* group_start_host, const uint32_t* group_mask_host, int64_t n_groups,
                                    int64_t k_host, int32_t window, int64_t* ranges_host, int64_t capacity,
                                    int64_t* n_ranges, int64_t* rows);
+dgnn_status dgnn_host_order_schedule(const int64_t* group_start_host, const uint32_t* group_mask_host,
+                                     int64_t n_groups, int64_t k_host, int32_t nwin, int64_t capacity_rows,
+                                     int64_t* copy_out, int64_t copy_cap, int64_t* copy_off, int64_t* map_out,
+                                     int64_t map_cap, int64_t* map_off, int64_t* rows_copied);
 dgnn_status dgnn_host_window_ranges(dgnn_ctx* ctx, const uint32_t* slot_mask, const int32_t* phys_of_slot,
                                     int64_t k_host, int32_t window, const int64_t* ranges_dev, int64_t nr,
                                     int32_t* smap);

@@ -49,7 +49,7 @@ EXPORTS = [
     "dgnn_ctx_set_keep_limit", "dgnn_ctx_kept_bytes", "dgnn_ctx_set_sample_budget", "dgnn_file_set_queues",
     "dgnn_chunk_layout_graph", "dgnn_pack_graph", "dgnn_samples_load", "dgnn_samples_drop_device",
     "dgnn_host_order", "dgnn_host_order_ranges", "dgnn_host_window_ranges", "dgnn_copy_ranges", "dgnn_remap_ids_dev",
-    "dgnn_pack_sharded", "dgnn_gather_rows_sharded",
+    "dgnn_pack_sharded", "dgnn_gather_rows_sharded", "dgnn_host_order_schedule",
 ]
 
 
@@ -147,6 +147,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "dgnn_host_window_ranges": (i32, [P, P, P, i64, i32, P, i64, P]),
             "dgnn_copy_ranges": (i32, [P, P, P, P, i64, i64]),
             "dgnn_remap_ids_dev": (i32, [P, P, P, i64, P]),
+            "dgnn_host_order_schedule": (i32, [P, P, i64, i64, i32, i64, P, i64, P, P, i64, P,
+                                                ctypes.POINTER(i64)]),
             "dgnn_pack_sharded": (i32, [P, P, i64, i32, i64, P, P, P, i64, i64, i64, P]),
             "dgnn_gather_rows_sharded": (i32, [P, P, i64, i32, i64, P, i64, P]),
             "dgnn_stage_file_write": (i32, [P, P, i64, P, i64, P, i64, ctypes.POINTER(i64)]),
@@ -548,19 +550,39 @@ class HostOrder:
                                                          ctypes.byref(rows)), "dgnn_host_order_ranges")
             self.ranges.append(rg[:3 * int(nr.value)].copy())
             self.rows.append(int(rows.value))
+        # the staging schedule: one arena of two windows' rows; rows shared by consecutive windows
+        # are copied once (dgnn_host_order_schedule)
+        self.capacity = 2 * max(self.rows) if self.rows else 0
+        cap_t = 4 * cap * (self.nwin + 1) + 16
+        co, mo = np.zeros(3 * cap_t, np.int64), np.zeros(3 * cap_t, np.int64)
+        coff, moff = np.zeros(self.nwin + 1, np.int64), np.zeros(self.nwin + 1, np.int64)
+        copied = i64()
+        _check(load_library().dgnn_host_order_schedule(P(gs.ctypes.data), P(gm.ctypes.data), self.n_groups,
+                                                       self.k_host, self.nwin, self.capacity, P(co.ctypes.data),
+                                                       cap_t, P(coff.ctypes.data), P(mo.ctypes.data), cap_t,
+                                                       P(moff.ctypes.data), ctypes.byref(copied)),
+               "dgnn_host_order_schedule")
+        self.rows_copied = int(copied.value)
+        self.copies = [co[3 * coff[w]:3 * coff[w + 1]].copy() for w in range(self.nwin)]
+        self.copy_rows = [int((c[1::3] - c[0::3]).sum()) for c in self.copies]
+        maps = [mo[3 * moff[w]:3 * moff[w + 1]].copy() for w in range(self.nwin)]
+        self.map_len = [len(m) // 3 for m in maps]
         with torch.cuda.stream(ctx.stream):
-            cat = np.concatenate(self.ranges + [np.zeros(1, np.int64)])
+            cat = np.concatenate(self.ranges + maps + [np.zeros(1, np.int64)])
             src = torch.from_numpy(cat).pin_memory()
             flat = src.to(dev, non_blocking=True)
         self._src = src
-        offs = np.concatenate([[0], np.cumsum([len(r) for r in self.ranges])])
+        offs = np.concatenate([[0], np.cumsum([len(r) for r in self.ranges + maps])])
         self.ranges_dev = [flat[int(offs[w]):int(offs[w + 1])] for w in range(self.nwin)]
+        self.map_dev = [flat[int(offs[self.nwin + w]):int(offs[self.nwin + w + 1])] for w in range(self.nwin)]
 
 
-def dgnn_host_window_ranges(ctx: Ctx, ho: HostOrder, window: int, smap: torch.Tensor):
+def dgnn_host_window_ranges(ctx: Ctx, ho: HostOrder, window: int, smap: torch.Tensor, scheduled: bool = True):
+    """smap of window ``window``: into the scheduled arena (default) or the per-window ranges."""
+    rg, n = (ho.map_dev[window], ho.map_len[window]) if scheduled else \
+        (ho.ranges_dev[window], len(ho.ranges[window]) // 3)
     _check(load_library().dgnn_host_window_ranges(ctx.handle, _ptr(ho.slot_mask), _ptr(ho.phys_of_slot), ho.k_host,
-                                                  int(window), _ptr(ho.ranges_dev[window]),
-                                                  len(ho.ranges[window]) // 3, _ptr(smap)), "dgnn_host_window_ranges")
+                                                  int(window), _ptr(rg), n, _ptr(smap)), "dgnn_host_window_ranges")
 
 
 def dgnn_copy_ranges(ctx: Ctx, dst, src_host_ptr: int, ranges, row_bytes: int):

@@ -18,6 +18,9 @@
 //   dgnn_copy_ranges        the copy-engine copies of a window's ranges (H2D)
 //   dgnn_remap_ids_dev      ids[i] = table[ids[i]] (slot -> physical row for the generic gather)
 #include <algorithm>
+#include <array>
+#include <utility>
+#include <vector>
 
 #include "internal.cuh"
 
@@ -217,5 +220,107 @@ extern "C" dgnn_status dgnn_remap_ids_dev(dgnn_ctx* c, int32_t* ids, const int64
         k_remap_ids<<<grid_for(c, n_max, 256), 256, 0, c->stream>>>(ids, n_dev, n_max, table);
     });
     DGNN_CK_LAUNCH();
+    return DGNN_OK;
+}
+
+// The staging schedule of the ordered windows: a row needed by consecutive windows stays in the
+// HBM staging arena between them instead of crossing PCIe once per window.  A group (equal mask)
+// is needed by the maximal runs [a, b] of consecutive set bits of its mask; each (group, run) is
+// one "item", copied when window a is prefetched and resident until window b is done.  The
+// assembler prefetches window w once window w-2's runs are done (while w-1's execute), so at that
+// point the items ending at or before w-2 are freed and the items starting at w are placed in
+// free staging rows (split over free fragments as needed: a copy is a range of physical rows).
+// capacity_rows >= max_w |S_{w-1}| + |S_w| always suffices (both windows' rows resident).
+// Outputs per window (CSR over windows): the copies to issue at its prefetch, and the map of all
+// its rows (every resident item it needs), both as (phys_lo, phys_hi, stage_lo) triples, the map
+// sorted by phys_lo.
+extern "C" dgnn_status dgnn_host_order_schedule(const int64_t* group_start_host, const uint32_t* group_mask_host,
+                                                int64_t n_groups, int64_t k_host, int32_t nwin, int64_t capacity_rows,
+                                                int64_t* copy_out, int64_t copy_cap, int64_t* copy_off,
+                                                int64_t* map_out, int64_t map_cap, int64_t* map_off,
+                                                int64_t* rows_copied) {
+    DGNN_REQUIRE(n_groups >= 0 && k_host >= 0 && nwin >= 1 && nwin <= 32 && capacity_rows >= 0 && copy_off &&
+                     map_off && rows_copied && (n_groups == 0 || (group_start_host && group_mask_host)),
+                 "dgnn_host_order_schedule: bad argument");
+    struct Item {
+        int64_t lo, hi;  // physical rows of the group
+        int a, b;        // first and last window of the run
+        std::vector<std::pair<int64_t, int64_t>> frag;  // (stage_lo, rows) pieces, in phys order
+    };
+    std::vector<Item> items;
+    for (int64_t g = 0; g < n_groups; ++g) {
+        const uint32_t m = group_mask_host[g];
+        const int64_t lo = group_start_host[g], hi = g + 1 < n_groups ? group_start_host[g + 1] : k_host;
+        for (int w = 0; w < nwin;) {
+            if (!((m >> w) & 1u)) {
+                ++w;
+                continue;
+            }
+            int e = w;
+            while (e + 1 < nwin && ((m >> (e + 1)) & 1u)) ++e;
+            items.push_back(Item{lo, hi, w, e, {}});
+            w = e + 1;
+        }
+    }
+    std::vector<std::pair<int64_t, int64_t>> freel{{0, capacity_rows}};  // [start, end) free staging rows
+    int64_t nc = 0, nm = 0, copied = 0;
+    auto release = [&](const Item& it) {
+        for (auto& f : it.frag) freel.push_back({f.first, f.first + f.second});
+        std::sort(freel.begin(), freel.end());
+        std::vector<std::pair<int64_t, int64_t>> merged;
+        for (auto& f : freel) {
+            if (!merged.empty() && merged.back().second == f.first) merged.back().second = f.second;
+            else merged.push_back(f);
+        }
+        freel.swap(merged);
+    };
+    for (int w = 0; w < nwin; ++w) {
+        copy_off[w] = nc;
+        for (auto& it : items)
+            if (it.b == w - 2) release(it);
+        for (auto& it : items) {
+            if (it.a != w) continue;
+            int64_t need = it.hi - it.lo, p = it.lo;
+            while (need > 0) {
+                DGNN_REQUIRE(!freel.empty(), "dgnn_host_order_schedule: staging capacity of %lld rows exceeded",
+                             (long long)capacity_rows);
+                auto& f = freel.front();
+                const int64_t take = std::min(need, f.second - f.first);
+                it.frag.push_back({f.first, take});
+                DGNN_REQUIRE(nc < copy_cap, "dgnn_host_order_schedule: copy_cap too small");
+                copy_out[3 * nc] = p;
+                copy_out[3 * nc + 1] = p + take;
+                copy_out[3 * nc + 2] = f.first;
+                ++nc;
+                f.first += take;
+                if (f.first == f.second) freel.erase(freel.begin());
+                p += take;
+                need -= take;
+                copied += take;
+            }
+        }
+        // the map of window w: every piece of every item covering w, by physical row
+        map_off[w] = nm;
+        std::vector<std::array<int64_t, 3>> mp;
+        for (auto& it : items) {
+            if (it.a > w || it.b < w) continue;
+            int64_t p = it.lo;
+            for (auto& f : it.frag) {
+                mp.push_back({p, p + f.second, f.first});
+                p += f.second;
+            }
+        }
+        std::sort(mp.begin(), mp.end());
+        for (auto& t : mp) {
+            DGNN_REQUIRE(nm < map_cap, "dgnn_host_order_schedule: map_cap too small");
+            map_out[3 * nm] = t[0];
+            map_out[3 * nm + 1] = t[1];
+            map_out[3 * nm + 2] = t[2];
+            ++nm;
+        }
+    }
+    copy_off[nwin] = nc;
+    map_off[nwin] = nm;
+    *rows_copied = copied;
     return DGNN_OK;
 }

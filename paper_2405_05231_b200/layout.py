@@ -366,6 +366,7 @@ class Layout:
                 cap = min(kh, max(int(hpre[groups[r1 - 1][1]] - hpre[groups[r0][0]]) for r0, r1 in windows))
                 if ordered:
                     cap = max(ho.rows)  # exact: the rows of each window's physical ranges
+                    arena_rows = ho.capacity  # the scheduled staging arena (two windows' rows)
                 stamp = buf("stamp", kh, torch.int32)
                 stamp.fill_(-1)  # window ids restart at 0 every epoch
                 nbuf = 2 if gctx is not ctx else 1
@@ -376,7 +377,11 @@ class Layout:
                 if use_runs:  # runs of consecutive host slots: one contiguous copy each
                     wruns = [buf(f"wruns{i}", max(cap, 1), torch.int32) for i in range(nbuf)]
                     wnruns = [buf(f"wnruns{i}", 1, torch.int64) for i in range(nbuf)]
-                staging = [buf(f"staging{i}", max(cap, 1) * self.row_bytes) for i in range(nbuf)]
+                if ordered:  # one arena; each window's rows sit where the schedule put them
+                    arena = buf("staging0", max(arena_rows, 1) * self.row_bytes)
+                    staging = [arena, arena]
+                else:
+                    staging = [buf(f"staging{i}", max(cap, 1) * self.row_bytes) for i in range(nbuf)]
         if gctx is not ctx:
             gctx.stream.wait_stream(ctx.stream)  # stamp / buffers were created on the ctx stream
         run_window = {r0: wi for wi, (r0, _) in enumerate(windows)}
@@ -392,10 +397,10 @@ class Layout:
             if ordered:
                 # window-ordered host tier: the window's rows are a few physical ranges -> copy engine
                 A.dgnn_host_window_ranges(gctx, ho, w, smap[s])
-                A.dgnn_copy_ranges(gctx, staging[s], self.host_tier.ptr, ho.ranges[w], self.row_bytes)
+                A.dgnn_copy_ranges(gctx, staging[s], self.host_tier.ptr, ho.copies[w], self.row_bytes)
                 if pcie_rows is not None:
                     with torch.cuda.stream(gctx.stream):
-                        pcie_rows.add_(ho.rows[w])
+                        pcie_rows.add_(ho.copy_rows[w])
                 ev = torch.cuda.Event()
                 ev.record(gctx.stream)
                 ev_ready[w] = ev
@@ -719,7 +724,8 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
             L.host_order, L.host_order_key = ho, (int(host_order), 1 << 30)
             A.dgnn_gather_rows(ctx, features, ho.phys_ids[:plan.k_host], host_tier.ptr)
             stats["host_order"] = {"windows": ho.nwin, "groups": ho.n_groups,
-                                   "ranges_per_window": [len(r) // 3 for r in ho.ranges], "rows": ho.rows}
+                                   "ranges_per_window": [len(r) // 3 for r in ho.ranges], "rows": ho.rows,
+                                   "rows_copied": ho.copy_rows, "arena_rows": ho.capacity}
         else:
             A.dgnn_gather_rows(ctx, features, plan.host_ids, host_tier.ptr)
     if nb:
