@@ -310,6 +310,9 @@ class Runner:
         self.nb = (inp[3].numel() + cfg["batch_size"] - 1) // cfg["batch_size"]
         self.before_layout = None  # hook: e.g. the e2e H2D copies of the inputs
         self.bid_base = None  # first batch id of this rank's seeds (None: rank * nb, one epoch per rank)
+        # enqueue each assembly from a worker thread (see _submit_assembly)
+        self.async_asm = os.environ.get("DGNN_ASYNC_ASM", "1") == "1"
+        self._pool = None
         # GPU tier: "replicated" (every rank holds all of it), or partitioned over the ranks and
         # read through peer memory ("peer", one-sided NVLink loads) / the NCCL exchange ("nccl")
         self.stage = "pinned"  # the disk tier: pinned host arena, or "file" (O_DIRECT on local storage)
@@ -426,8 +429,6 @@ class Runner:
         gctx = self.ctxG if os.environ.get("DGNN_GATHER_STREAM", "1") == "1" else None
         kw = {}
         if self.slots is not None:
-            # every rank's shard of this pass is filled before anyone reads it
-            self._cross_rank(dict(L.stats.get("_events", [])).get("tiers"))
             if self.gpu_tier_mode == "peer":
                 kw["peer_tier"] = self.slots.view(L._slot)
             else:
@@ -476,13 +477,13 @@ class Runner:
         prev_ev = None
         last = None
         for e in range(K):
-            ev_a = self._assemble(L, ev_l)
+            ev_a = self._submit_assembly(L, ev_l)
             Ln = None
             if e + 1 < K:
                 if not self.pipelined:
-                    self.sA.wait_event(ev_a)  # sequential: the next pass starts after this assembly
+                    self.sA.wait_event(ev_a.result())  # sequential: the next pass starts after this assembly
                 elif prev_ev is not None:
-                    self.sA.wait_event(prev_ev)  # slot (e+1)%2 was pass e-1's: its assembly must be done
+                    self.sA.wait_event(prev_ev.result())  # slot (e+1)%2 was pass e-1's: its assembly must be done
                 # a pass whose assembly stream A has waited for is finished on the device:
                 # release it before allocating pass e+1, so at most two passes are resident
                 # (pipelined: pass e-1; sequential: pass e as well)
@@ -494,7 +495,7 @@ class Runner:
                     # the HBM-bound pack of pass e+1 waits for the assembly of pass e (it would
                     # share HBM with it otherwise); its chunks then go out in pieces so that the
                     # next assembly starts on the first ones
-                    pack_alone = lambda ev=ev_a: self.sA.wait_event(ev)
+                    pack_alone = lambda ev=ev_a: self.sA.wait_event(ev.result())
                 Ln = self.layout((e + 1) % 2, before_pack=pack_alone)
                 ev_l = self._ready(Ln)
                 if os.environ.get("DGNN_MEM_TRACE") == "1":  # allocator counters (host side, no sync)
@@ -505,8 +506,27 @@ class Runner:
             if L is not None:
                 last = L
             L = Ln
-        self.sA.wait_event(prev_ev)
+        self.sA.wait_event(prev_ev.result())
         return last if keep_last else None
+
+    def _submit_assembly(self, L, ev_l):
+        """Enqueue the assembly of pass L -> a future of its end event.  The assembly's host-side
+        enqueue (hundreds of runs) runs on a worker thread when it is free of collectives and of
+        waits on the layout stream's tail, so the main thread starts enqueueing the next pass's
+        layout at once; both threads only enqueue device work on their own streams."""
+        import concurrent.futures as cf
+        if self.slots is not None:
+            # every rank's shard of this pass is filled before anyone reads it (a collective: here,
+            # on the main thread, in pass order)
+            self._cross_rank(dict(L.stats.get("_events", [])).get("tiers"))
+        staged = L.disk_plan is None and (L.arena is not None or L.disk is not None)
+        if self.async_asm and staged and self.gpu_tier_mode != "nccl":
+            if self._pool is None:
+                self._pool = cf.ThreadPoolExecutor(max_workers=1, thread_name_prefix="dgnn-asm")
+            return self._pool.submit(self._assemble, L, ev_l)
+        f = cf.Future()
+        f.set_result(self._assemble(L, ev_l))
+        return f
 
     def timeline_ms(self):
         """Per pass, relative to the first layout start: layout phase ends and assembly span."""
