@@ -200,8 +200,28 @@ def pcie_bandwidth(dev, nbytes: int = 1 << 30) -> dict:
             b.synchronize()
             best = max(best, nbytes / (a.elapsed_time(b) / 1e3) / 1e9)
         out[name] = best
-    del d
+    # both directions at once on two streams (the copy engines share the link / host memory)
+    hb2 = dg.HostBuffer(nbytes)
+    d2 = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    best = 0.0
+    for _ in range(5):
+        torch.cuda.synchronize(dev)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev[0].record(s1)
+        ev[2].record(s2)
+        with torch.cuda.stream(s1):
+            d.copy_(hb.tensor, non_blocking=True)
+        with torch.cuda.stream(s2):
+            hb2.tensor.copy_(d2, non_blocking=True)
+        ev[1].record(s1)
+        ev[3].record(s2)
+        torch.cuda.synchronize(dev)
+        best = max(best, 2 * nbytes / (max(ev[0].elapsed_time(ev[1]), ev[2].elapsed_time(ev[3])) / 1e3) / 1e9)
+    out["bidir_total_gbs"] = best
+    del d, d2
     hb.free()
+    hb2.free()
     return out
 
 
@@ -840,6 +860,19 @@ def main():
                                                "gathers + staged-in chunks and cache pages) / ms_per_step; "
                                                "peak = pinned H2D cudaMemcpy measured in this run",
                                        "pcie": pcie}
+        # the whole step against the link in both directions: H2D above; D2H = the host-tier fill
+        # (SM stores into pinned memory) + the chunks staged out; the floor is the slowest of the
+        # two directions alone and of both together against the measured bidirectional copy rate
+        d2h = stats0["k_host"] * rb + stats0["chunk_bytes"]
+        fl = {"h2d": h2d / pcie["h2d_gbs"] / 1e6, "d2h": d2h / pcie["d2h_gbs"] / 1e6,
+              "both": (h2d + d2h) / pcie["bidir_total_gbs"] / 1e6}
+        floor_ms = max(fl.values())
+        result["step_roofline"] = {"bound": "pcie", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                                   "floor_ms": round(floor_ms, 1), "floor_by": max(fl, key=fl.get),
+                                   "ms_per_step": round(ms_max / args.steps, 1),
+                                   "frac": round(floor_ms / (ms_max / args.steps), 4),
+                                   "note": "PCIe floor of one pass (bytes / measured copy rates: H2D, D2H, both "
+                                           "directions at once) over the measured step time"}
 
     if args.stage == "file":
         # the disk tier's traffic per step: every chunk written once (stage-out) and read once

@@ -37,8 +37,9 @@ def _check_common(d, steps, warmup):
 
 
 def test_default_contract_products():
-    d = _run("--config", "products", "--steps", "2", "--warmup", "3", "--cpu-batches", "4", "--e2e-steps", "1")
-    _check_common(d, 2, 3)
+    # (a products pass takes ~50 ms: enough steps that the clock sampler sees the GPU under load)
+    d = _run("--config", "products", "--steps", "12", "--warmup", "3", "--cpu-batches", "4", "--e2e-steps", "1")
+    _check_common(d, 12, 3)
     r = d["roofline"]
     assert r["bound"] == "hbm" and 0 < r["frac"] <= 1.0 and r["peak"] > 0 and r["achieved"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] > 0 and d["cpu_baseline"]["cores"] >= 1
