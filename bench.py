@@ -332,6 +332,7 @@ class Runner:
         self.bid_base = None  # first batch id of this rank's seeds (None: rank * nb, one epoch per rank)
         # enqueue each assembly from a worker thread (see _submit_assembly)
         self.async_asm = os.environ.get("DGNN_ASYNC_ASM", "1") == "1"
+        self.asm_traces = []  # DGNN_ASM_TRACE=1: (assembly start event, per-window events)
         self._pool = None
         # GPU tier: "replicated" (every rank holds all of it), or partitioned over the ranks and
         # read through peer memory ("peer", one-sided NVLink loads) / the NCCL exchange ("nccl")
@@ -480,6 +481,8 @@ class Runner:
         ev_a = torch.cuda.Event(enable_timing=True)
         ev_a.record(self.sB)
         self.slot_asm_ev[L._slot] = ev_a
+        if getattr(L, "_asm_trace", None):
+            self.asm_traces.append((a0, L._asm_trace))
         self.timeline.append(((L.stats.get("_events", []), L.stats.get("_host", [])), a0, ev_a))
         return ev_a
 
@@ -970,6 +973,13 @@ def main():
             result["cpu_baseline"] = cb
         except Exception as ex:  # the baseline is reported, never required
             result["cpu_baseline"] = {"value": None, "error": str(ex)[:200]}
+    if R.asm_traces:  # DGNN_ASM_TRACE=1: per-window copy / runs spans of the last traced assembly
+        a0, tr = R.asm_traces[-1]
+        log("[asm-trace] w: copy start-end | runs start-end (ms from the assembly start)")
+        for w in sorted(tr):
+            t = tr[w]
+            f = lambda k: round(a0.elapsed_time(t[k]), 1) if k in t else None
+            log(f"[asm-trace] {w}: {f('copy0')}-{f('copy1')} | {f('runs0')}-{f('runs1')}")
     if rank == 0:
         print(json.dumps(result), flush=True)
     if ws > 1:

@@ -55,7 +55,7 @@ __global__ void k_pack_graph(SampleSrc s, int64_t b_lo, int64_t nb, const int64_
 }
 
 struct LoadDst {
-    int64_t* node_off;  // [nb+1] (uploaded)
+    int64_t* node_off;  // [nb+2]: offsets, then node_off[nb+1] = 1 if the headers are inconsistent
     int32_t* nodes;
     int32_t* hop_off;
     int64_t* eptr_off;
@@ -68,6 +68,7 @@ struct LoadDst {
 // the loader: section i -> batch i of the run's samples object (offsets from k_load_offsets)
 __global__ void k_load_graph(LoadDst d, int64_t nb, const uint8_t* __restrict__ base,
                              const int64_t* __restrict__ sec_off, int*) {
+    if (d.node_off[nb + 1]) return;  // inconsistent headers (k_load_offsets): write nothing
     for (int64_t i = blockIdx.y; i < nb; i += gridDim.y) {
         const int32_t* in = reinterpret_cast<const int32_t*>(base + sec_off[i]);
         const int64_t n = d.node_off[i + 1] - d.node_off[i], m = d.eptr_off[i + 1] - d.eptr_off[i],
@@ -92,7 +93,9 @@ __global__ void __launch_bounds__(1024) k_load_offsets(LoadDst d, int64_t nb, co
                                                       int64_t m_tot, int64_t e_tot, int* err) {
     __shared__ int64_t s_w[3][32];
     __shared__ int64_t s_run[3];
+    __shared__ int s_bad;
     if (threadIdx.x < 3) s_run[threadIdx.x] = 0;
+    if (threadIdx.x == 0) s_bad = 0;
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int64_t i0 = 0; i0 < nb; i0 += blockDim.x) {
@@ -100,7 +103,7 @@ __global__ void __launch_bounds__(1024) k_load_offsets(LoadDst d, int64_t nb, co
         int64_t v[3] = {0, 0, 0};
         if (i < nb) {
             const int32_t* in = reinterpret_cast<const int32_t*>(base + sec_off[i]);
-            if (in[0] != d.H || in[1] < 0 || in[2] < 0 || in[3] < 0) atomicOr(err, DEVERR_OVERFLOW);
+            if (in[0] != d.H || in[1] < 0 || in[2] < 0 || in[3] < 0) s_bad = 1;
             v[0] = in[1];
             v[1] = in[2];
             v[2] = in[3];
@@ -143,11 +146,14 @@ __global__ void __launch_bounds__(1024) k_load_offsets(LoadDst d, int64_t nb, co
             for (int k = 0; k < 3; ++k) s_run[k] += s_w[k][(int)(blockDim.x >> 5) - 1];
         __syncthreads();
     }
+    __syncthreads();
     if (threadIdx.x == 0) {
         d.node_off[nb] = s_run[0];
         d.eptr_off[nb] = s_run[1];
         d.edge_off[nb] = s_run[2];
-        if (s_run[0] != n_tot || s_run[1] != m_tot || s_run[2] != e_tot) atomicOr(err, DEVERR_OVERFLOW);
+        const int bad = s_bad || s_run[0] != n_tot || s_run[1] != m_tot || s_run[2] != e_tot;
+        d.node_off[nb + 1] = bad;
+        if (bad) atomicOr(err, DEVERR_OVERFLOW);
     }
 }
 
@@ -238,7 +244,7 @@ extern "C" dgnn_status dgnn_samples_load(dgnn_ctx* c, const dgnn_samples* meta, 
     S->nodes = (int32_t*)dev_alloc(c, 4 * (size_t)S->cap_nodes);
     S->src_local = (int32_t*)dev_alloc(c, 4 * (size_t)S->cap_edges);
     S->eptr = (int32_t*)dev_alloc(c, 4 * (size_t)S->cap_eptr);
-    S->node_off = (int64_t*)dev_alloc(c, sizeof(int64_t) * (nb + 1));
+    S->node_off = (int64_t*)dev_alloc(c, sizeof(int64_t) * (nb + 2));  // + the loader's consistency flag
     S->edge_off = (int64_t*)dev_alloc(c, sizeof(int64_t) * (nb + 1));
     S->eptr_off = (int64_t*)dev_alloc(c, sizeof(int64_t) * (nb + 1));
     S->hop_off = (int32_t*)dev_alloc(c, sizeof(int32_t) * std::max<int64_t>(1, nb * (H + 2)));

@@ -387,6 +387,14 @@ class Layout:
         run_window = {r0: wi for wi, (r0, _) in enumerate(windows)}
         last_run = {r1 - 1: wi for wi, (_, r1) in enumerate(windows)}
         ev_ready, ev_done = {}, {}
+        # DGNN_ASM_TRACE=1 (measurement only): per window, timing events of its copy and its runs
+        trace = {} if os.environ.get("DGNN_ASM_TRACE") == "1" else None
+        self._asm_trace = trace
+
+        def _tev(stream):
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            return e
 
         def prefetch(w):
             # window w's distinct host rows -> staging[w % nbuf] (PCIe), on the gather stream
@@ -394,6 +402,8 @@ class Layout:
             if w >= nbuf and gctx is not ctx:
                 gctx.stream.wait_event(ev_done[w - nbuf])  # the runs that used this buffer are done
             w0, w1 = windows[w]
+            if trace is not None:
+                trace.setdefault(w, {})["copy0"] = _tev(gctx.stream)
             if ordered:
                 # window-ordered host tier: the window's rows are a few physical ranges -> copy engine
                 A.dgnn_host_window_ranges(gctx, ho, w, smap[s])
@@ -401,9 +411,11 @@ class Layout:
                 if pcie_rows is not None:
                     with torch.cuda.stream(gctx.stream):
                         pcie_rows.add_(ho.copy_rows[w])
-                ev = torch.cuda.Event()
+                ev = torch.cuda.Event(enable_timing=trace is not None)
                 ev.record(gctx.stream)
                 ev_ready[w] = ev
+                if trace is not None:
+                    trace[w]["copy1"] = ev
                 return
             A.dgnn_host_window(gctx, self.addr[spans[w0][0]:spans[w1 - 1][1]], w, stamp, kh, wlist[s], smap[s],
                                wcount[s])
@@ -455,6 +467,8 @@ class Layout:
                     ctx.stream.wait_event(ev_ready[w])
                     if w + 1 < len(windows):
                         prefetch(w + 1)  # overlaps this window's (HBM-bound) runs
+                if trace is not None:
+                    trace.setdefault(w, {})["runs0"] = _tev(ctx.stream)
                 cur = w % nbuf
             k = b1 - b0
             t = flat[int(offs[i]):int(offs[i + 1])]
@@ -485,9 +499,11 @@ class Layout:
             if on_run is not None:
                 on_run(i, b0, b1, chunk, t[3 * k + 3:4 * k + 3] if self.sec_abs is not None else None)
             if i in last_run:
-                ev = torch.cuda.Event()
+                ev = torch.cuda.Event(enable_timing=trace is not None)
                 ev.record(ctx.stream)
                 ev_done[last_run[i]] = ev
+                if trace is not None:
+                    trace[last_run[i]]["runs1"] = ev
             if runs:
                 yield b0, b1, out[:n1 - n0]
             else:
