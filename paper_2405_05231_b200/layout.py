@@ -382,6 +382,16 @@ class Layout:
                     staging = [arena, arena]
                 else:
                     staging = [buf(f"staging{i}", max(cap, 1) * self.row_bytes) for i in range(nbuf)]
+            # ordered windows over a pinned disk tier: each window's chunk span (contiguous) is staged
+            # with its host rows in one copy on the gather stream, so a run never waits for a copy of
+            # its own (the runs then chain at HBM speed); spans above the budget keep per-run staging
+            wspan = []
+            if ordered and self.arena is not None and self.disk_plan is None and gctx is not ctx:
+                wspan = [(spans[r0][2], spans[r1 - 1][3]) for r0, r1 in windows]
+                if max(hi - lo for lo, hi in wspan) > int(os.environ.get("DGNN_WIN_CHUNK_BUDGET", str(4 << 30))):
+                    wspan = []
+            if wspan:
+                wchunk = [buf(f"wchunk{i}", max(hi - lo for lo, hi in wspan)) for i in range(2)]
         if gctx is not ctx:
             gctx.stream.wait_stream(ctx.stream)  # stamp / buffers were created on the ctx stream
         run_window = {r0: wi for wi, (r0, _) in enumerate(windows)}
@@ -408,6 +418,10 @@ class Layout:
                 # window-ordered host tier: the window's rows are a few physical ranges -> copy engine
                 A.dgnn_host_window_ranges(gctx, ho, w, smap[s])
                 A.dgnn_copy_ranges(gctx, staging[s], self.host_tier.ptr, ho.copies[w], self.row_bytes)
+                if wspan:  # and the window's chunks, once their stage-out pieces are in the arena
+                    self.wait_chunks(gctx.stream, groups[w1 - 1][1], waited_g)
+                    lo, hi = wspan[w]
+                    A.dgnn_copy_ranges(gctx, wchunk[w % 2], self.arena.ptr, [lo, hi, 0], 1)
                 if pcie_rows is not None:
                     with torch.cuda.stream(gctx.stream):
                         pcie_rows.add_(ho.copy_rows[w])
@@ -438,6 +452,7 @@ class Layout:
         tickets = {}
 
         waited = set()
+        waited_g = set()
 
         def stage(i):
             n0, n1, c_lo, c_hi = spans[i]
@@ -448,11 +463,18 @@ class Layout:
             else:
                 tickets[i] = A.dgnn_stage_copy(ctx, chunk_ring[i % 2], self.arena.ptr + c_lo, c_hi - c_lo, 1)
 
-        if staged:
+        run_win = {}
+        for wi, (r0, r1) in enumerate(windows):
+            for r in range(r0, r1):
+                run_win[r] = wi
+        if staged and not wspan:
             stage(0)
         for i, (b0, b1) in enumerate(groups):
             n0, n1, c_lo, c_hi = spans[i]
-            if staged:
+            if wspan:  # the window's chunks were staged with its host rows
+                w_i = run_win[i]
+                chunk = wchunk[w_i % 2].data_ptr() + (c_lo - wspan[w_i][0])
+            elif staged:
                 if i + 1 < len(groups):
                     stage(i + 1)
                 A.dgnn_stage_wait(ctx, tickets.pop(i))

@@ -58,6 +58,21 @@ def random_csr_fast(rng, n, max_deg):
     return np.cumsum(indptr), c.astype(np.int32)
 
 
+@pytest.fixture(scope="module", autouse=True)
+def _release_gpu_memory_after_module():
+    """Module fixtures hold tens of GB at papers scale: after each module, collect them and hand
+    the caching allocator's blocks back, so later modules (and their subprocesses) get the GPU."""
+    yield
+    import gc
+    gc.collect()
+    try:
+        import torch
+        if torch.cuda.is_available():
+            torch.cuda.empty_cache()
+    except Exception:
+        pass
+
+
 @pytest.fixture(scope="session")
 def gpu_available():
     try:

@@ -34,7 +34,14 @@ def papers():
     ctx.sync()
     del feats
     host = dict(indptr=indptr.cpu().numpy(), indices=indices.cpu().numpy(), seeds=seeds.cpu().numpy())
-    return dict(dg=dg, ctx=ctx, L=L, cfg=cfg, gpu_rows=gpu_rows, host_rows=host_rows, **host)
+    d = dict(dg=dg, ctx=ctx, L=L, cfg=cfg, gpu_rows=gpu_rows, host_rows=host_rows, **host)
+    yield d
+    # release the ~100 GB this module holds before later modules (and their subprocesses) run
+    d.clear()
+    del L, ctx, indptr, indices, seeds
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()
 
 
 SAMPLED = [0, 1, 586, 1170, 1171]

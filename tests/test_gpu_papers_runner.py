@@ -23,6 +23,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def test_driver_command_passes_within_budget_and_exact():
     if not torch.cuda.is_available():
         pytest.skip("needs a GPU")
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()  # this process's cached blocks: the subprocess needs the whole GPU
     p = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "papers_runner_check.py"), "5", "20"],
                        capture_output=True, text=True, timeout=1200, cwd=ROOT)
     assert p.returncode == 0, p.stderr[-3000:]
