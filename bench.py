@@ -332,6 +332,11 @@ class Runner:
         self.bid_base = None  # first batch id of this rank's seeds (None: rank * nb, one epoch per rank)
         # enqueue each assembly from a worker thread (see _submit_assembly)
         self.async_asm = os.environ.get("DGNN_ASYNC_ASM", "1") == "1"
+        if self.async_asm:
+            # two host threads enqueue (layout, assembly); the library calls back into Python for
+            # device memory (torch's caching allocator), so a callback waits for the GIL: switch
+            # it every 0.5 ms instead of the default 5 ms
+            sys.setswitchinterval(float(os.environ.get("DGNN_SWITCH_INTERVAL", "0.0005")))
         self.asm_traces = []  # DGNN_ASM_TRACE=1: (assembly start event, per-window events)
         self._pool = None
         # GPU tier: "replicated" (every rank holds all of it), or partitioned over the ranks and
@@ -713,6 +718,7 @@ def main():
     barrier(ws)
     torch.cuda.synchronize()
     l0 = sum(c.launches() for c in R.ctxs())
+    cb0 = dg._abi.CALLBACKS[0]
     R.pcie_rows.zero_()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -825,7 +831,8 @@ def main():
         "clocks": clocks,
         "gpu_launches": int(launches),
         "kernel_ms_per_step_by_stream": per_stream,
-        "memory": memory_report(dev, R),
+        "memory": dict(memory_report(dev, R),
+                       allocator_callbacks_per_step=round((dg._abi.CALLBACKS[0] - cb0) / args.steps, 1)),
         "device_timeline_ms": R.timeline_ms(),
     }
     samp_ms = sum(v["ms"] for k, v in kst.items() if k.startswith("sample") or k == "scan") / args.steps

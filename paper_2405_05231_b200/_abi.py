@@ -30,6 +30,7 @@ KERNELS = ["scan", "sample_seed", "sample_hop", "sample_order", "sample_remap", 
            "cache_hist", "cache_select", "classify", "pack_gather", "tier_gather", "assemble", "misc", "sort", "disk_plan", "disk_gather", "train",
            "host_window", "host_gather", "tier_gather_pcie", "graph_io", "sample_dedup", "sample_count"]
 K = {name: i for i, name in enumerate(KERNELS)}
+CALLBACKS = [0]  # allocator callbacks from the library into Python (each needs the GIL)
 
 # every symbol include/dgnn.h declares (checked by tests/test_abi_symbols.py)
 EXPORTS = [
@@ -290,12 +291,14 @@ class Ctx:
             dev = self.device.index
 
             def _a(nbytes, stream, user):
+                CALLBACKS[0] += 1
                 try:
                     return torch.cuda.caching_allocator_alloc(int(nbytes), dev, int(stream or 0))
                 except Exception:
                     return None
 
             def _f(ptr, nbytes, stream, user):
+                CALLBACKS[0] += 1
                 try:
                     torch.cuda.caching_allocator_delete(int(ptr))
                 except Exception:

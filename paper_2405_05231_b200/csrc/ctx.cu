@@ -1,3 +1,4 @@
+#include <algorithm>
 // ctx.cu -- context, errors, allocation, statistics and the a8 staging runtime.
 #include <atomic>
 #include <cstdarg>
@@ -140,6 +141,28 @@ dgnn_status read_dev_err(dgnn_ctx* c, int* flags) {
     return DGNN_OK;
 }
 
+namespace scan {
+dgnn_status scratch(dgnn_ctx* c, size_t bytes, unsigned long long** status) {
+    if (c->scan_bytes < bytes) {
+        if (c->scan_buf) {
+            DGNN_CK(cudaStreamSynchronize(c->stream));  // (growth is rare: the old buffer may be in use)
+            DGNN_CK(cudaFree(c->scan_buf));
+            c->scan_buf = nullptr;
+        }
+        const size_t want = std::max<size_t>(bytes + bytes / 2, (size_t)1 << 20);
+        if (cudaMalloc(&c->scan_buf, want) != cudaSuccess) {
+            cudaGetLastError();
+            c->scan_bytes = 0;
+            set_error("scan scratch allocation of %zu bytes failed", want);
+            return DGNN_ENOMEM;
+        }
+        c->scan_bytes = want;
+    }
+    *status = static_cast<unsigned long long*>(c->scan_buf);
+    return DGNN_OK;
+}
+}  // namespace scan
+
 dgnn_status dev_err_status(int h) {
     if (!h) return DGNN_OK;
     if (h & DEVERR_SEED_RANGE) { set_error("a seed is outside [0, num_nodes)"); return DGNN_EINVAL; }
@@ -219,6 +242,7 @@ void dgnn_ctx_destroy(dgnn_ctx* c) {
         if (c->stage_ev[i]) cudaEventDestroy(c->stage_ev[i]);
     if (c->order_ev) cudaEventDestroy(c->order_ev);
     if (c->dev_err) cudaFree(c->dev_err);
+    if (c->scan_buf) cudaFree(c->scan_buf);
     if (c->pinned) cudaFreeHost(c->pinned);
     if (c->pinned_err) cudaFreeHost(c->pinned_err);
     if (c->side) cudaStreamDestroy(c->side);

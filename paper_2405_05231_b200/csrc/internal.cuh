@@ -62,6 +62,11 @@ struct dgnn_ctx {
     std::vector<Kept> kept;
     size_t kept_bytes = 0;
     size_t kept_limit = (size_t)24 << 30;      // dgnn_ctx_set_keep_limit
+    // grow-only scan scratch (status words + tile counter), plain cudaMalloc: the scans of a ctx run
+    // in its stream order, so one buffer serves them all, and no allocator callback (Python, the
+    // GIL) sits on the sampler's hot path
+    void* scan_buf = nullptr;
+    size_t scan_bytes = 0;
     size_t sample_budget = (size_t)3 << 30;    // sampler group scratch budget (dgnn_ctx_set_sample_budget)
 };
 
@@ -371,26 +376,21 @@ __global__ void __launch_bounds__(kThreads) scan_kernel(const int64_t* n_dev, in
     }
 }
 
-// Scratch for one scan launch: status words for up to max_n items.
-struct Scratch {
-    DevBuf<unsigned long long> status;
-    DevBuf<unsigned int> counter;
-};
+dgnn_status scratch(dgnn_ctx* c, size_t bytes, unsigned long long** status);  // ctx.cu
 
 template <class In, class Out>
 dgnn_status run(dgnn_ctx* c, int64_t max_n, const int64_t* n_dev, In in, Out out, int64_t* total_dev) {
     if (max_n < 0) max_n = 0;
     const int64_t tiles = (max_n + kTile - 1) / kTile;
-    Scratch s;
-    DGNN_TRY(s.status.alloc(c, (size_t)(tiles > 0 ? tiles : 1)));
-    DGNN_TRY(s.counter.alloc(c, 1));
-    DGNN_TRY(memset_async(c, s.status.p, 0, sizeof(unsigned long long) * (size_t)(tiles > 0 ? tiles : 1)));
-    DGNN_TRY(memset_async(c, s.counter.p, 0, sizeof(unsigned int)));
+    const size_t nst = (size_t)(tiles > 0 ? tiles : 1);
+    unsigned long long* status = nullptr;
+    DGNN_TRY(scratch(c, sizeof(unsigned long long) * (nst + 1), &status));
+    unsigned int* counter = reinterpret_cast<unsigned int*>(status + nst);
+    DGNN_TRY(memset_async(c, status, 0, sizeof(unsigned long long) * (nst + 1)));
     int blocks = (int)(tiles < (int64_t)c->num_sms * 4 ? tiles : (int64_t)c->num_sms * 4);
     if (blocks < 1) blocks = 1;
     launch(c, DGNN_K_SCAN, 0.0, [&] {
-        scan_kernel<In, Out><<<blocks, kThreads, 0, c->stream>>>(n_dev, max_n, in, out, s.status.p, s.counter.p,
-                                                                  total_dev);
+        scan_kernel<In, Out><<<blocks, kThreads, 0, c->stream>>>(n_dev, max_n, in, out, status, counter, total_dev);
     });
     DGNN_CK_LAUNCH();
     return DGNN_OK;
