@@ -346,6 +346,8 @@ class Runner:
         self.embed_graph = False  # graph samples kept in the chunks, loaded back for training
         # window-ordered host tier: each host-row window is a few contiguous ranges for the copy engine
         self.host_order = os.environ.get("DGNN_HOST_ORDER", "1") == "1"
+        # output bytes per assembly run (one launch): fewer, larger runs are fewer host-side calls
+        self.out_budget = int(os.environ.get("DGNN_ASM_OUT_BUDGET", str(1 << 30)))
         self.gpu_tier_mode = "replicated"
         self.slots = None  # shard.PeerSlots in the partitioned modes
         self.ws_n, self.slot_asm_ev = 1, [None, None]
@@ -427,6 +429,7 @@ class Runner:
                                       scratch_ws=self.scratch_ws, before_pack=before_pack, gpu_shard=gpu_shard,
                                       stage=self.stage, embed_graph=self.embed_graph,
                                       host_order=self.host_window if self.host_order else None,
+                                      asm_out_budget=self.out_budget,
                                       file_path=os.path.join(self.disk_dir, f"dgnn_disk_r{self.rank}_s{slot}.bin"))
         L._slot = slot
         return L
@@ -466,22 +469,23 @@ class Runner:
                 kw["remote"] = lambda c, addr, out: shard.fetch_remote_rows(c, tier, addr, out, a2a)
         if self.train:
             for _ in L.train_epoch(ctx=self.ctxB, train_ctx=self.ctxT, host_window=self.host_window,
-                                   gather_ctx=gctx, ws=self.asm_ws, pcie_rows=self.pcie_rows, **kw):
+                                   gather_ctx=gctx, ws=self.asm_ws, pcie_rows=self.pcie_rows,
+                                   out_budget=self.out_budget, **kw):
                 pass
             self.sB.wait_stream(self.sT)  # the pass ends when its last batch is trained
         else:
             for _ in L.assemble_epoch(ctx=self.ctxB, host_window=self.host_window, gather_ctx=gctx,
-                                      ws=self.asm_ws, pcie_rows=self.pcie_rows, **kw):
+                                      ws=self.asm_ws, pcie_rows=self.pcie_rows, out_budget=self.out_budget, **kw):
                 pass
         if self.gpu_tier_mode == "nccl" and self.ws_n > 1:
             # the exchange is collective per run: ranks with fewer runs join the others' extra
             # exchanges with empty requests
             import torch.distributed as dist
             from paper_2405_05231_b200 import shard
-            n = torch.tensor([len(L.assembly_groups())], dtype=torch.int64, device=self.dev)
+            n = torch.tensor([len(L.assembly_groups(self.out_budget))], dtype=torch.int64, device=self.dev)
             dist.all_reduce(n, op=dist.ReduceOp.MAX)
             empty = torch.zeros(0, dtype=torch.int32, device=self.dev)
-            for _ in range(int(n.item()) - len(L.assembly_groups())):
+            for _ in range(int(n.item()) - len(L.assembly_groups(self.out_budget))):
                 kw["remote"](self.ctxB, empty, None)
         ev_a = torch.cuda.Event(enable_timing=True)
         ev_a.record(self.sB)

@@ -202,9 +202,11 @@ extern "C" dgnn_status dgnn_copy_ranges(dgnn_ctx* c, void* dst_dev, const void* 
     DGNN_REQUIRE(c && row_bytes > 0 && nr >= 0 && (nr == 0 || (dst_dev && src_host && ranges_host)),
                  "dgnn_copy_ranges: bad argument");
     DGNN_CK(cudaSetDevice(c->device));
+    if (nr == 0) return DGNN_OK;
     for (int64_t r = 0; r < nr; ++r) {
         const int64_t lo = ranges_host[3 * r], hi = ranges_host[3 * r + 1], st = ranges_host[3 * r + 2];
         DGNN_REQUIRE(hi >= lo && st >= 0, "dgnn_copy_ranges: bad range");
+        if (hi == lo) continue;
         DGNN_CK(cudaMemcpyAsync((uint8_t*)dst_dev + st * row_bytes, (const uint8_t*)src_host + lo * row_bytes,
                                 (size_t)((hi - lo) * row_bytes), cudaMemcpyHostToDevice, c->stream));
     }

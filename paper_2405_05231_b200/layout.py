@@ -575,7 +575,8 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
                    direct_io: bool = True, disk_budget: int | None = None, disk_m: int = 1,
                    disk_k: int = 4, disk_budget_frac: float | None = None, after_sample=None,
                    scratch_ws: Workspace | None = None, before_pack=None, gpu_shard=None,
-                   embed_graph: bool = False, host_order: int | None = None) -> Layout:
+                   embed_graph: bool = False, host_order: int | None = None,
+                   asm_out_budget: int = 1 << 30) -> Layout:
     """Run a1-a8 on this rank's batches.
 
     ``seeds`` are this rank's seeds (batch t of them gets bid = batch_id_base + t).
@@ -599,8 +600,8 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
     samples' device arrays once packed: training then reads the graph through the loader stage
     (Layout.train_epoch, dgnn_samples_load); the host-side offsets stay as the layout's metadata.
     ``host_order`` = W: lay the host tier out in window order (dgnn_host_order) for an assembly with
-    host_window=W (default out_budget): each window's host rows become a few contiguous ranges that
-    the copy engine moves; outputs are unchanged (every reader maps slot -> physical row).
+    host_window=W and out_budget=``asm_out_budget``: each window's host rows become a few contiguous
+    ranges that the copy engine moves; outputs are unchanged (every reader maps slot -> physical row).
     ``after_sample``: called once the samples are complete (dgnn_sample returns when they are),
     before the rest of the pass is enqueued -- a scheduling hook (bench.py starts the previous
     pass's assembly there, so that sampling never shares the GPU with it).
@@ -750,7 +751,7 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
         # window-ordered host tier (needs the address tables): fill it in physical order
         ho = None
         if nb:
-            groups_a, wins = L.host_windows(int(host_order))
+            groups_a, wins = L.host_windows(int(host_order), int(asm_out_budget))
             if 0 < len(wins) <= 32:
                 no = samples.node_off_host
                 wo = [int(no[groups_a[r0][0]]) for r0, _ in wins] + [int(no[groups_a[wins[-1][1] - 1][1]])]
@@ -759,7 +760,7 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
                 except A.DgnnError:  # too many distinct window masks: keep the slot order
                     ho = None
         if ho is not None:
-            L.host_order, L.host_order_key = ho, (int(host_order), 1 << 30)
+            L.host_order, L.host_order_key = ho, (int(host_order), int(asm_out_budget))
             A.dgnn_gather_rows(ctx, features, ho.phys_ids[:plan.k_host], host_tier.ptr)
             stats["host_order"] = {"windows": ho.nwin, "groups": ho.n_groups,
                                    "ranges_per_window": [len(r) // 3 for r in ho.ranges], "rows": ho.rows,
@@ -767,7 +768,7 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
         else:
             A.dgnn_gather_rows(ctx, features, plan.host_ids, host_tier.ptr)
     if nb:
-        L.assembly_plan()  # a9's per-run tables, uploaded here on the layout's stream
+        L.assembly_plan(int(asm_out_budget))  # a9's per-run tables, uploaded here on the layout's stream
     mark("classify")
     if before_pack is not None:
         before_pack()
