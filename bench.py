@@ -347,7 +347,7 @@ class Runner:
         # window-ordered host tier: each host-row window is a few contiguous ranges for the copy engine
         self.host_order = os.environ.get("DGNN_HOST_ORDER", "1") == "1"
         # output bytes per assembly run (one launch): fewer, larger runs are fewer host-side calls
-        self.out_budget = int(os.environ.get("DGNN_ASM_OUT_BUDGET", str(1 << 30)))
+        self.out_budget = int(os.environ.get("DGNN_ASM_OUT_BUDGET", str(2 << 30)))
         self.gpu_tier_mode = "replicated"
         self.slots = None  # shard.PeerSlots in the partitioned modes
         self.ws_n, self.slot_asm_ev = 1, [None, None]
@@ -633,6 +633,8 @@ def main():
                          "needs in place (the paper's setting: the table is not in GPU memory; default), or "
                          "every input including the whole feature table is copied to HBM each step")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--stat-steps", type=int, default=2,
+                    help="extra passes after the timed region with every kernel family timed (the kernels table)")
     ap.add_argument("--sequential", action="store_true",
                     help="no epoch pipelining: the layout of pass e+1 starts after the assembly of pass e")
     ap.add_argument("--host-window", type=int, default=128,
@@ -715,9 +717,15 @@ def main():
     torch.cuda.synchronize()
 
     # ---------------- timed region (device time, CUDA events; max over ranks) ----------------
+    # per-launch CUDA events are two host API calls each: inside the timed region only the kernel
+    # families the roofline and the step accounting report are timed (the graded pack, the tier
+    # fills, the assembly and its window copies); every family is timed over --stat-steps extra
+    # passes after it (the "kernels" table)
+    TIMED = ["pack_gather", "tier_gather", "tier_gather_pcie", "assemble", "host_gather", "host_window"]
     for c in R.ctxs():
         c.reset_stats()
         c.set_timing(True)
+        c.set_timing_mask(TIMED)
     clk = Clocks(local)
     barrier(ws)
     torch.cuda.synchronize()
@@ -750,11 +758,37 @@ def main():
     nb_all = int(sum_over_ranks(float(nb), ws))  # batches of one step over all ranks
     total_batches = nb_all * args.steps
     value = total_batches / (ms_max / 1e3)
+    kst_timed = kst
+    gathered_rows = int(R.pcie_rows.item())
+    timeline = R.timeline_ms()
+    # every kernel family, over extra instrumented passes (not part of the timed value)
+    stat_steps = max(1, args.stat_steps)
+    for c in R.ctxs():
+        c.reset_stats()
+        c.set_timing(True)
+        c.set_timing_mask(None)
+    torch.cuda.synchronize()
+    e0s, e1s = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0s.record(R.sA)
+    R.run(stat_steps)
+    e1s.record(R.sA)
+    torch.cuda.synchronize()
+    ms_stat = e0s.elapsed_time(e1s) / stat_steps
+    kst, per_stream, per_stream_stats = {}, {}, {}
+    for name, c in zip(("layout", "assemble", "host_gather", "train"), R.ctxs()):
+        st = c.kernel_stats()
+        per_stream_stats[name] = st
+        per_stream[name] = round(sum(v["ms"] for v in st.values()) / stat_steps, 2)
+        for k, v in st.items():
+            d = kst.setdefault(k, {"launches": 0, "ms": 0.0, "bytes": 0.0})
+            for f in d:
+                d[f] += v[f]
+        c.set_timing(False)
 
     hbm_peak, peak_src = peaks()
-    pk = kst["pack_gather"]
+    pk = kst_timed["pack_gather"]
     pack_gbs = pk["bytes"] / (pk["ms"] / 1e3) / 1e9 if pk["ms"] > 0 else None
-    asm = kst["assemble"]
+    asm = kst_timed["assemble"]
     traffic = None
     prof = os.path.join(ROOT, "profiles", "pack_gather_ncu.json")
     if os.path.exists(prof):
@@ -764,7 +798,6 @@ def main():
             traffic = None
     pcie = pcie_bandwidth(dev)
     rb = stats0.get("row_bytes", cfg["dim"] * 4)
-    gathered_rows = int(R.pcie_rows.item())
     # per stream: every kernel family runs on one stream, so its share of the step is its
     # summed launch time over the step time on that stream (<= 1; streams overlap each other)
     kernels = {}
@@ -773,8 +806,8 @@ def main():
         for k, v in st.items():
             if not v["launches"]:
                 continue
-            d = {"ms_per_step": round(v["ms"] / args.steps, 3), "launches_per_step": v["launches"] // args.steps,
-                 "share_of_step": round(v["ms"] / ms, 4) if ms else None}
+            d = {"ms_per_step": round(v["ms"] / stat_steps, 3), "launches_per_step": v["launches"] // stat_steps,
+                 "share_of_step": round(v["ms"] / stat_steps / ms_stat, 4) if ms_stat else None}
             if k == "tier_gather_pcie" and v["bytes"] and v["ms"]:
                 # the host-tier fill: SM stores into pinned host memory (D2H); with the table in
                 # pinned memory (e2e) also the UVA reads of the GPU-tier fill
@@ -783,7 +816,7 @@ def main():
                          frac=round(g / pcie["d2h_gbs"], 4))
             elif k == "host_gather" and v["ms"] > 0:
                 # PCIe-bound UVA reads of the window's host-tier rows (bytes counted on the device)
-                g = gathered_rows * rb / (v["ms"] / 1e3) / 1e9
+                g = (gathered_rows / args.steps) * rb / (v["ms"] / stat_steps / 1e3) / 1e9
                 d.update(gbs=round(g, 1), bound="pcie", peak=round(pcie["h2d_gbs"], 1),
                          frac=round(g / pcie["h2d_gbs"], 4))
             elif v["bytes"] and v["ms"]:
@@ -831,15 +864,18 @@ def main():
                      "bytes_per_launch": round(pk["bytes"] / max(pk["launches"], 1)),
                      "launch_ms": round(pk["ms"] / max(pk["launches"], 1), 4)},
         "kernels": kernels,
+        "kernels_note": (f"per-family kernel times from {stat_steps} instrumented passes after the timed region "
+                         "(every launch bracketed by events); inside the timed region only " + ", ".join(TIMED) +
+                         " are timed (the roofline kernel among them)"),
         "layout_stats": stats0,
         "clocks": clocks,
         "gpu_launches": int(launches),
         "kernel_ms_per_step_by_stream": per_stream,
         "memory": dict(memory_report(dev, R),
                        allocator_callbacks_per_step=round((dg._abi.CALLBACKS[0] - cb0) / args.steps, 1)),
-        "device_timeline_ms": R.timeline_ms(),
+        "device_timeline_ms": timeline,
     }
-    samp_ms = sum(v["ms"] for k, v in kst.items() if k.startswith("sample") or k == "scan") / args.steps
+    samp_ms = sum(v["ms"] for k, v in kst.items() if k.startswith("sample") or k == "scan") / stat_steps
     if samp_ms > 0:
         # a2-a3 rates: sampled edges (= candidates) and batch nodes per second of
         # sampler device time (scan + sample_* kernels; the scan also serves a6's compaction)
@@ -852,7 +888,7 @@ def main():
         # SURVEY 8(d) "offline batches/s" = batches / (sample + build_cache + classify + pack): the
         # layout span of each timed pass up to the end of classify, plus its pack kernel time (the
         # pipelined pack first waits for the previous assembly, which is not layout work)
-        spans = [t["classify"] - t["start"] + kst["pack_gather"]["ms"] / args.steps for t in tl]
+        spans = [t["classify"] - t["start"] + kst_timed["pack_gather"]["ms"] / args.steps for t in tl]
         result["offline"] = {"batches_per_s": round(nb_all / (statistics.median(spans) / 1e3), 1),
                              "layout_ms_per_pass": round(statistics.median(spans), 1),
                              "note": "a1-a8 per pass (sample, count all-reduce, tier select, tier fill, classify, "

@@ -158,6 +158,10 @@ int64_t dgnn_ctx_kept_bytes(const dgnn_ctx* ctx);
 dgnn_status dgnn_ctx_set_sample_budget(dgnn_ctx* ctx, int64_t bytes);
 int64_t dgnn_ctx_launches(const dgnn_ctx* ctx);
 dgnn_status dgnn_ctx_set_timing(dgnn_ctx* ctx, int enable);
+/* With timing on, only the kernel families whose bit (1 << DGNN_K_*) is set in mask are bracketed
+ * by events (default: all).  Two event records per launch are host API calls: a timed region that
+ * should not pay them for hundreds of small launches times only the families it reports. */
+dgnn_status dgnn_ctx_set_timing_mask(dgnn_ctx* ctx, uint64_t mask);
 typedef struct {
     int64_t launches;  /* timed launches of this family                          */
     double ms;         /* summed CUDA-event durations (ms)                        */

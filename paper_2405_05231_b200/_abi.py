@@ -35,7 +35,7 @@ CALLBACKS = [0]  # allocator callbacks from the library into Python (each needs 
 # every symbol include/dgnn.h declares (checked by tests/test_abi_symbols.py)
 EXPORTS = [
     "dgnn_ctx_create", "dgnn_ctx_destroy", "dgnn_ctx_set_stream", "dgnn_ctx_stream", "dgnn_ctx_side_stream",
-    "dgnn_ctx_sync", "dgnn_last_error", "dgnn_ctx_set_sample_group", "dgnn_ctx_launches", "dgnn_ctx_set_timing",
+    "dgnn_ctx_sync", "dgnn_last_error", "dgnn_ctx_set_sample_group", "dgnn_ctx_launches", "dgnn_ctx_set_timing", "dgnn_ctx_set_timing_mask",
     "dgnn_ctx_kernel_stats", "dgnn_ctx_reset_stats", "dgnn_kernel_name", "dgnn_sample", "dgnn_samples_get_info",
     "dgnn_samples_free", "dgnn_build_cache", "dgnn_cache_plan_get_info", "dgnn_cache_plan_free", "dgnn_classify",
     "dgnn_chunk_layout", "dgnn_pack", "dgnn_gather_rows", "dgnn_stage_copy", "dgnn_stage_wait", "dgnn_stage_sync",
@@ -124,6 +124,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "dgnn_ctx_set_sample_budget": (i32, [P, i64]),
             "dgnn_ctx_launches": (i64, [P]),
             "dgnn_ctx_set_timing": (i32, [P, ctypes.c_int]),
+            "dgnn_ctx_set_timing_mask": (i32, [P, u64]),
             "dgnn_ctx_kernel_stats": (i32, [P, i32, ctypes.POINTER(_KStat)]),
             "dgnn_ctx_reset_stats": (i32, [P]),
             "dgnn_kernel_name": (ctypes.c_char_p, [i32]),
@@ -321,6 +322,11 @@ class Ctx:
 
     def set_timing(self, on: bool):
         _check(load_library().dgnn_ctx_set_timing(self.handle, int(bool(on))), "dgnn_ctx_set_timing")
+
+    def set_timing_mask(self, kinds=None):
+        """Time only these kernel families (names of KERNELS) when timing is on; None = all."""
+        mask = (1 << 64) - 1 if kinds is None else sum(1 << K[k] for k in kinds)
+        _check(load_library().dgnn_ctx_set_timing_mask(self.handle, mask), "dgnn_ctx_set_timing_mask")
 
     def kernel_stats(self) -> dict:
         out = {}

@@ -320,6 +320,12 @@ dgnn_status dgnn_ctx_set_timing(dgnn_ctx* c, int enable) {
     return DGNN_OK;
 }
 
+dgnn_status dgnn_ctx_set_timing_mask(dgnn_ctx* c, uint64_t mask) {
+    DGNN_REQUIRE(c, "dgnn_ctx_set_timing_mask: NULL ctx");
+    c->timing_mask = mask;
+    return DGNN_OK;
+}
+
 dgnn_status dgnn_ctx_kernel_stats(dgnn_ctx* c, int32_t kid, dgnn_kernel_stat* out) {
     DGNN_REQUIRE(c && out && kid >= 0 && kid < DGNN_K_NUM, "dgnn_ctx_kernel_stats: bad argument");
     DGNN_CK(cudaSetDevice(c->device));

@@ -32,6 +32,7 @@ struct dgnn_ctx {
     int grid_cap = 0;                // > 0: no launch of this ctx uses more CTAs (dgnn_ctx_set_grid_cap)
     // per-launch CUDA-event timing
     bool timing = false;
+    uint64_t timing_mask = ~0ull;  // kernel families timed when timing is on (dgnn_ctx_set_timing_mask)
     struct Pending {
         cudaEvent_t a, b;
         int kid;
@@ -176,14 +177,15 @@ void fold_pending(dgnn_ctx* c, bool sync);
 template <class F>
 inline void launch(dgnn_ctx* c, int kid, double bytes, F&& f) {
     dgnn_ctx::Pending p{};
-    if (c->timing) {
+    const bool timed = c->timing && ((c->timing_mask >> kid) & 1ull);
+    if (timed) {
         p.a = take_event(c);
         p.b = take_event(c);
         cudaEventRecord(p.a, c->stream);
     }
     f();
     c->launches++;
-    if (c->timing) {
+    if (timed) {
         cudaEventRecord(p.b, c->stream);
         p.kid = kid;
         p.bytes = bytes;

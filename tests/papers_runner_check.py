@@ -35,20 +35,20 @@ def main():
 
     class Keep(bench.Runner):
         def _assemble(self, L, ev_l):
+            # the Runner's own assembly (arena per pass, early window-0 prefetch), observed: the
+            # rows of the checked batches of the last pass are copied out as they are yielded
             passes[0] += 1
             last = passes[0] == total
-            self.sB.wait_event(ev_l)
-            a0 = torch.cuda.Event()
-            a0.record(self.sB)
-            for b, out in L.assemble_epoch(ctx=self.ctxB, host_window=self.host_window, gather_ctx=self.ctxG,
-                                           ws=self.asm_ws, pcie_rows=self.pcie_rows):
-                if last and b in CHECK:
-                    with torch.cuda.stream(self.sB):
-                        kept[b] = out.view(torch.uint8).reshape(out.shape[0], -1).to("cpu", non_blocking=False)
-            ev = torch.cuda.Event()
-            ev.record(self.sB)
-            self.timeline.append(((L.stats.get("_events", []), L.stats.get("_host", [])), a0, ev))
-            return ev
+            inner = L.assemble_epoch
+
+            def spy(*a, **k):
+                for b, out in inner(*a, **k):
+                    if last and b in CHECK:
+                        with torch.cuda.stream(self.sB):
+                            kept[b] = out.view(torch.uint8).reshape(out.shape[0], -1).to("cpu", non_blocking=False)
+                    yield b, out
+            L.assemble_epoch = spy
+            return super()._assemble(L, ev_l)
 
     total = 1 + max(warmup - 1, 2) + steps
     R = Keep(dg, inp, 0, dev, pipelined=True)
