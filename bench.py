@@ -338,6 +338,8 @@ class Runner:
             # it every 0.5 ms instead of the default 5 ms
             sys.setswitchinterval(float(os.environ.get("DGNN_SWITCH_INTERVAL", "0.0005")))
         self.asm_traces = []  # DGNN_ASM_TRACE=1: (assembly start event, per-window events)
+        self.observe = None  # test hook: observe(pass, batch, rows) for every assembled batch
+        self.pass_index = 0
         self._pool = None
         # GPU tier: "replicated" (every rank holds all of it), or partitioned over the ranks and
         # read through peer memory ("peer", one-sided NVLink loads) / the NCCL exchange ("nccl")
@@ -474,9 +476,12 @@ class Runner:
                 pass
             self.sB.wait_stream(self.sT)  # the pass ends when its last batch is trained
         else:
-            for _ in L.assemble_epoch(ctx=self.ctxB, host_window=self.host_window, gather_ctx=gctx,
-                                      ws=self.asm_ws, pcie_rows=self.pcie_rows, out_budget=self.out_budget, **kw):
-                pass
+            for b, out in L.assemble_epoch(ctx=self.ctxB, host_window=self.host_window, gather_ctx=gctx,
+                                           ws=self.asm_ws, pcie_rows=self.pcie_rows, out_budget=self.out_budget,
+                                           **kw):
+                if self.observe is not None:  # (tests: each assembled batch, on the assembly stream)
+                    self.observe(self.pass_index, b, out)
+        self.pass_index += 1
         if self.gpu_tier_mode == "nccl" and self.ws_n > 1:
             # the exchange is collective per run: ranks with fewer runs join the others' extra
             # exchanges with empty requests
