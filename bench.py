@@ -350,6 +350,9 @@ class Runner:
         self.host_order = os.environ.get("DGNN_HOST_ORDER", "1") == "1"
         # output bytes per assembly run (one launch): fewer, larger runs are fewer host-side calls
         self.out_budget = int(os.environ.get("DGNN_ASM_OUT_BUDGET", str(2 << 30)))
+        # window 0's host rows of the next pass staged during this pass's last windows (one staging
+        # arena per pass in flight)
+        self.early_prefetch = os.environ.get("DGNN_EARLY_PREFETCH", "1") == "1"
         self.gpu_tier_mode = "replicated"
         self.slots = None  # shard.PeerSlots in the partitioned modes
         self.ws_n, self.slot_asm_ev = 1, [None, None]
@@ -472,13 +475,14 @@ class Runner:
         if self.train:
             for _ in L.train_epoch(ctx=self.ctxB, train_ctx=self.ctxT, host_window=self.host_window,
                                    gather_ctx=gctx, ws=self.asm_ws, pcie_rows=self.pcie_rows,
-                                   out_budget=self.out_budget, **kw):
+                                   out_budget=self.out_budget, arena_tag=f"_{L._slot}",
+                                   early=getattr(L, "_early", None), **kw):
                 pass
             self.sB.wait_stream(self.sT)  # the pass ends when its last batch is trained
         else:
             for b, out in L.assemble_epoch(ctx=self.ctxB, host_window=self.host_window, gather_ctx=gctx,
                                            ws=self.asm_ws, pcie_rows=self.pcie_rows, out_budget=self.out_budget,
-                                           **kw):
+                                           arena_tag=f"_{L._slot}", early=getattr(L, "_early", None), **kw):
                 if self.observe is not None:  # (tests: each assembled batch, on the assembly stream)
                     self.observe(self.pass_index, b, out)
         self.pass_index += 1
@@ -535,6 +539,14 @@ class Runner:
                     pack_alone = lambda ev=ev_a: self.sA.wait_event(ev.result())
                 Ln = self.layout((e + 1) % 2, before_pack=pack_alone)
                 ev_l = self._ready(Ln)
+                if self.pipelined and self.early_prefetch and self.gpu_tier_mode != "nccl":
+                    # window 0's host rows of pass e+1 cross PCIe while pass e's last windows run:
+                    # after pass e's copies on the gather stream (its enqueue is complete), once that
+                    # part of the tier is filled and the arena's previous user (pass e-1) is done
+                    after = [prev_ev.result()] if prev_ev is not None else []
+                    ev_a.result()
+                    Ln._early = Ln.early_host_prefetch(self.ctxG, self.asm_ws, self.host_window, self.out_budget,
+                                                       f"_{(e + 1) % 2}", after)
                 if os.environ.get("DGNN_MEM_TRACE") == "1":  # allocator counters (host side, no sync)
                     log(f"[mem] pass {e + 1}: allocated {torch.cuda.memory_allocated(self.dev) / 1e9:.1f} GB, "
                         f"reserved {torch.cuda.memory_reserved(self.dev) / 1e9:.1f} GB, kept "

@@ -386,13 +386,14 @@ dgnn_status dgnn_stage_file_read(dgnn_ctx* ctx, dgnn_file* f, int64_t file_off, 
 /* The window-ordered host tier (the ordering idea of the paper's disk cache,
  * Sec. 5.1 / Algorithm 1, applied to the CPU-cache tier and the assembler's host-row
  * windows).  Slots and addresses are unchanged (reading c17); the tier's PHYSICAL row order is
- * (mask, slot), mask = the windows that address the slot, so that every window's host rows are a
+ * (reversed mask, slot), mask = the windows that address the slot (bits reversed: window 0 most
+ * significant, so window 0's rows are one contiguous range), so that every window's host rows are a
  * few contiguous ranges the copy engine moves at the link rate.
  * dgnn_host_order: addr = the address tables of all batches (device uint32, batch-major), window w =
  *   addr[win_node_off_host[w] .. win_node_off_host[w+1]), 1 <= nwin <= 32; host_ids = the plan's
  *   host tier (device int32 [k_host]).  Outputs (device, caller-owned, k_host entries):
  *   slot_mask[s] = OR of 1<<w over windows holding a HOST address of slot s; phys_of_slot[s] = its
- *   physical row; phys_ids[p] = host_ids[the slot at row p] (fill the tier with dgnn_gather_rows
+ *   physical row (slots sorted by (bit-reversed mask, slot)); phys_ids[p] = host_ids[the slot at row p] (fill the tier with dgnn_gather_rows
  *   over phys_ids).  Host outputs: the n_groups runs of equal mask in physical order, their first
  *   row (group_start_host) and mask (group_mask_host); DGNN_ERANGE if n_groups > max_groups (the
  *   caller keeps the slot-ordered tier).  Synchronizes.

@@ -7,7 +7,7 @@
 // batches needs share pages (Sec. 5.1, Algorithm 1); here the windows are known when the
 // layout is built, so the host tier can be ordered exactly: slot s gets the window-membership mask
 // m(s) (bit w = some batch of window w addresses s), and the tier is laid out physically in
-// (m(s), s) order.  Rows with equal masks form one contiguous group; window w needs exactly the
+// (brev(m(s)), s) order -- masks with their window bits reversed, window 0 most significant.  Rows with equal masks form one contiguous group; window w needs exactly the
 // groups whose mask has bit w, i.e. a few hundred contiguous ranges, which the copy engine moves
 // at the full link rate.  Slots, tier_map and every address stay as the oracle defines them
 // (reading c17); only the physical row of a slot changes, and every reader goes through a map.
@@ -34,6 +34,16 @@ __global__ void k_host_masks(const uint32_t* __restrict__ addr, int64_t n, uint3
         const int64_t slot = a & DGNN_SLOT_MASK;
         if ((a >> DGNN_TIER_SHIFT) == DGNN_TIER_HOST && slot < kh && !(mask[slot] & bit)) atomicOr(&mask[slot], bit);
     }
+}
+
+// sort key of a mask: its nwin bits reversed, so window 0 is the most significant -- the rows of
+// window 0 (the first one the assembler stages, and the one staged ahead of it) are one
+// contiguous range at the end of the physical order
+__device__ __forceinline__ uint32_t mask_key(uint32_t m, int nwin) { return __brev(m) >> (32 - nwin); }
+
+__global__ void k_mask_keys(const uint32_t* __restrict__ mask, int64_t n, int nwin, uint32_t* __restrict__ key) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        key[i] = mask_key(mask[i], nwin);
 }
 
 __global__ void k_iota(uint32_t* __restrict__ v, int64_t n) {
@@ -103,13 +113,16 @@ extern "C" dgnn_status dgnn_host_order(dgnn_ctx* c, const uint32_t* addr, const 
         });
         DGNN_CK_LAUNCH();
     }
-    // physical order: slots sorted by (mask, slot) -- a stable radix sort on the nwin mask bits
+    // physical order: slots sorted by (reversed mask, slot) -- a stable radix sort on nwin bits
     DevBuf<uint32_t> keys, vals, keys_alt, vals_alt;
     DGNN_TRY(keys.alloc_kept(c, (size_t)k_host));
     DGNN_TRY(vals.alloc_kept(c, (size_t)k_host));
     DGNN_TRY(keys_alt.alloc_kept(c, (size_t)k_host));
     DGNN_TRY(vals_alt.alloc_kept(c, (size_t)k_host));
-    DGNN_CK(cudaMemcpyAsync(keys.p, slot_mask, sizeof(uint32_t) * (size_t)k_host, cudaMemcpyDeviceToDevice, c->stream));
+    launch(c, DGNN_K_MISC, 0.0, [&] {
+        k_mask_keys<<<grid_for(c, k_host, 256), 256, 0, c->stream>>>(slot_mask, k_host, nwin, keys.p);
+    });
+    DGNN_CK_LAUNCH();
     launch(c, DGNN_K_MISC, 0.0, [&] { k_iota<<<grid_for(c, k_host, 256), 256, 0, c->stream>>>(vals.p, k_host); });
     DGNN_CK_LAUNCH();
     uint32_t *k0 = keys.p, *v0 = vals.p, *k1 = keys_alt.p, *v1 = vals_alt.p;
@@ -129,11 +142,12 @@ extern "C" dgnn_status dgnn_host_order(dgnn_ctx* c, const uint32_t* addr, const 
         int64_t* gs = gstart.p;
         uint32_t* gm = gmask.p;
         const int64_t cap = max_groups;
+        const int nw = nwin;
         auto in = [=] __device__(int64_t i) -> int32_t { return (i == 0 || sk[i] != sk[i - 1]) ? 1 : 0; };
         auto out = [=] __device__(int64_t i, int64_t excl, int64_t v) {
             if (v && excl < cap) {
                 gs[excl] = i;
-                gm[excl] = sk[i];
+                gm[excl] = mask_key(sk[i], nw);  // (bit reversal is its own inverse)
             }
         };
         DGNN_TRY(scan::run(c, k_host, nullptr, in, out, total.p));

@@ -129,6 +129,7 @@ class Layout:
     sec_abs: np.ndarray = None      # [nb] disk-tier byte offset of each batch's graph section
     host_order: A.HostOrder | None = None  # window-ordered host tier (physical rows permuted)
     host_order_key: tuple = None    # (host_window, out_budget) the ordering was built for
+    host_w0_event: object = None    # the layout stream's event once window 0's host rows are filled
 
     def phase_ms(self) -> dict:
         """Device time of the layout's phases (after the stream has passed them)."""
@@ -189,6 +190,26 @@ class Layout:
                                   self.host_tier.ptr, self.plan.k_host, chunk, t[2:4], t[4:6], self.row_bytes, out,
                                   host_map=self.host_order.phys_of_slot)
         return out
+
+    def early_host_prefetch(self, gctx: A.Ctx, ws: "Workspace", host_window: int, out_budget: int,
+                            arena_tag: str, after=()):
+        """Stage window 0's host rows (one contiguous physical range) into this epoch's staging arena
+        ahead of its assembly, on ``gctx``'s stream once that part of the tier is filled and the
+        ``after`` events (the arena's previous user done) have passed -> the event to hand to
+        assemble_epoch(early=...), or None when the assembly would not use the ordering."""
+        ho = self.host_order
+        if ho is None or self.host_w0_event is None or self.host_order_key != (host_window, int(out_budget)):
+            return None
+        with torch.cuda.stream(gctx.stream):
+            nbytes = max(ho.capacity, 1) * self.row_bytes
+            arena = ws.dev("staging0" + arena_tag, nbytes, gctx.device)[:nbytes]
+        gctx.stream.wait_event(self.host_w0_event)
+        for ev in after:
+            gctx.stream.wait_event(ev)
+        A.dgnn_copy_ranges(gctx, arena, self.host_tier.ptr, ho.copies[0], self.row_bytes)
+        ev = torch.cuda.Event()
+        ev.record(gctx.stream)
+        return ev
 
     def host_windows(self, host_window: int, out_budget: int = 1 << 30):
         """The assembler's host-row windows: (first run, last run + 1) over assembly_groups(out_budget),
@@ -284,7 +305,7 @@ class Layout:
     def assemble_epoch(self, ctx: A.Ctx | None = None, out_budget: int = 1 << 30, host_window: int = 128,
                        gather_ctx: A.Ctx | None = None, sharded_tier=None, remote=None, runs: bool = False,
                        ring_wait: dict | None = None, ws: Workspace | None = None, peer_tier=None,
-                       pcie_rows: torch.Tensor | None = None, on_run=None):
+                       pcie_rows: torch.Tensor | None = None, on_run=None, arena_tag: str = "", early=None):
         """Pipelined assembly: the chunks of the next run of batches are staged H2D
         on the side stream while the current run is assembled on the ctx stream (one
         dgnn_assemble_group launch per run).  Yields (b, features[n_b, dim]) per batch; a
@@ -314,6 +335,10 @@ class Layout:
 
         ``pcie_rows`` (device int64 [1], measurement only): accumulates the host-tier rows the
         window gathers move over PCIe.
+
+        ``arena_tag`` names this epoch's staging arena in ``ws`` (epochs in flight at once use
+        different tags); ``early`` = the event of early_host_prefetch: window 0's host rows are
+        already in that arena.
 
         ``on_run(i, b0, b1, chunk, sec_off)``: called on the ctx stream after run i is assembled,
         with the run's staged chunks (device tensor or pointer) and, when the chunks keep their
@@ -378,7 +403,7 @@ class Layout:
                     wruns = [buf(f"wruns{i}", max(cap, 1), torch.int32) for i in range(nbuf)]
                     wnruns = [buf(f"wnruns{i}", 1, torch.int64) for i in range(nbuf)]
                 if ordered:  # one arena; each window's rows sit where the schedule put them
-                    arena = buf("staging0", max(arena_rows, 1) * self.row_bytes)
+                    arena = buf("staging0" + arena_tag, max(arena_rows, 1) * self.row_bytes)
                     staging = [arena, arena]
                 else:
                     staging = [buf(f"staging{i}", max(cap, 1) * self.row_bytes) for i in range(nbuf)]
@@ -417,7 +442,10 @@ class Layout:
             if ordered:
                 # window-ordered host tier: the window's rows are a few physical ranges -> copy engine
                 A.dgnn_host_window_ranges(gctx, ho, w, smap[s])
-                A.dgnn_copy_ranges(gctx, staging[s], self.host_tier.ptr, ho.copies[w], self.row_bytes)
+                if w == 0 and early is not None:  # (staged ahead: early_host_prefetch)
+                    gctx.stream.wait_event(early)
+                else:
+                    A.dgnn_copy_ranges(gctx, staging[s], self.host_tier.ptr, ho.copies[w], self.row_bytes)
                 if wspan:  # and the window's chunks, once their stage-out pieces are in the arena
                     self.wait_chunks(gctx.stream, groups[w1 - 1][1], waited_g)
                     lo, hi = wspan[w]
@@ -761,7 +789,20 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
                     ho = None
         if ho is not None:
             L.host_order, L.host_order_key = ho, (int(host_order), int(asm_out_budget))
-            A.dgnn_gather_rows(ctx, features, ho.phys_ids[:plan.k_host], host_tier.ptr)
+            # window 0's rows first (one contiguous range of the physical order), then the rest: the
+            # assembler may stage window 0 as soon as its part is filled (Layout.early_host_prefetch)
+            kh, rb = plan.k_host, row_bytes
+            first = ho.ranges[0].reshape(-1, 3)[:, :2] if len(ho.ranges[0]) else np.zeros((0, 2), np.int64)
+            done = np.zeros(kh + 1, np.int8)
+            for lo, hi in first:
+                A.dgnn_gather_rows(ctx, features, ho.phys_ids[int(lo):int(hi)], host_tier.ptr + int(lo) * rb)
+                done[int(lo):int(hi)] = 1
+            ev = torch.cuda.Event()
+            ev.record(ctx.stream)
+            L.host_w0_event = ev
+            edges = np.flatnonzero(np.diff(np.concatenate([[1], done[:kh], [1]])))  # runs of unfilled rows
+            for lo, hi in zip(edges[0::2], edges[1::2]):
+                A.dgnn_gather_rows(ctx, features, ho.phys_ids[int(lo):int(hi)], host_tier.ptr + int(lo) * rb)
             stats["host_order"] = {"windows": ho.nwin, "groups": ho.n_groups,
                                    "ranges_per_window": [len(r) // 3 for r in ho.ranges], "rows": ho.rows,
                                    "rows_copied": ho.copy_rows, "arena_rows": ho.capacity}

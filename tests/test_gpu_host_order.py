@@ -3,7 +3,7 @@
 offline_layout(host_order=W) lays the host tier out physically in (window mask, slot) order so that
 the assembler's host-row windows of W batches are a few contiguous ranges (copy-engine copies).
 Slots, tier map and addresses stay the oracle's; checked here: the masks equal a numpy
-recomputation from the oracle's address tables, the physical order is the (mask, slot) sort, the
+recomputation from the oracle's address tables, the physical order is the (reversed mask, slot) sort, the
 physical tier rows are the oracle's host-tier rows permuted, every window's ranges cover exactly
 its slots, and every batch assembled through every reader -- the ordered windows, other window
 sizes (slot list remapped), per-batch UVA reads and Layout.assemble -- equals the direct gather.
@@ -64,11 +64,15 @@ def test_window_ordered_host_tier(dg, tiny, ref, W, budget, group):
             want[host] |= np.uint32(1 << w)
     mask = ho.slot_mask[:kh].cpu().numpy().view(np.uint32)
     assert np.array_equal(mask, want)
-    order = np.lexsort((np.arange(kh), want))  # by mask, then slot
+    rev = np.zeros(kh, np.uint32)  # the sort key: the mask's window bits reversed (window 0 most significant)
+    for w in range(ho.nwin):
+        rev |= ((want >> w) & 1) << (ho.nwin - 1 - w)
+    order = np.lexsort((np.arange(kh), rev))  # by reversed mask, then slot
     phys_of_slot = ho.phys_of_slot[:kh].cpu().numpy()
     assert np.array_equal(phys_of_slot[order], np.arange(kh))
     host_rows = L.host_tier.tensor.numpy().reshape(kh, -1)
     assert np.array_equal(host_rows[phys_of_slot], ref["host_buf"])
+    assert len(ho.ranges[0]) == 3  # window 0's rows: one contiguous range (the most significant key bit)
     for w in range(ho.nwin):
         rg = ho.ranges[w].reshape(-1, 3)
         covered = np.concatenate([np.arange(lo, hi) for lo, hi, _ in rg]) if len(rg) else np.zeros(0, np.int64)
