@@ -339,6 +339,9 @@ class Runner:
             sys.setswitchinterval(float(os.environ.get("DGNN_SWITCH_INTERVAL", "0.0005")))
         self.asm_traces = []  # DGNN_ASM_TRACE=1: (assembly start event, per-window events)
         self.observe = None  # test hook: observe(pass, batch, rows) for every assembled batch
+        self.asm_host_ms = []  # host time of each assembly's enqueue (measurement only)
+        self.asm_trace_on = os.environ.get("DGNN_ASM_TRACE") == "1"
+        self.early_trace = []  # (enqueue point, end) events of the early window-0 copies (trace only)
         self.pass_index = 0
         self._pool = None
         # GPU tier: "replicated" (every rank holds all of it), or partitioned over the ranks and
@@ -457,6 +460,7 @@ class Runner:
 
     def _assemble(self, L, ev_l):
         """Enqueue the assembly (and trainer) of pass L on stream B after its layout; -> end event."""
+        t_host0 = time.perf_counter()
         self.sB.wait_event(ev_l)
         a0 = torch.cuda.Event(enable_timing=True)
         a0.record(self.sB)
@@ -499,6 +503,7 @@ class Runner:
         ev_a = torch.cuda.Event(enable_timing=True)
         ev_a.record(self.sB)
         self.slot_asm_ev[L._slot] = ev_a
+        self.asm_host_ms.append((time.perf_counter() - t_host0) * 1e3)  # host time to enqueue the assembly
         if getattr(L, "_asm_trace", None):
             self.asm_traces.append((a0, L._asm_trace))
         self.timeline.append(((L.stats.get("_events", []), L.stats.get("_host", [])), a0, ev_a))
@@ -545,8 +550,16 @@ class Runner:
                     # part of the tier is filled and the arena's previous user (pass e-1) is done
                     after = [prev_ev.result()] if prev_ev is not None else []
                     ev_a.result()
+                    t0e = None
+                    if self.asm_trace_on:
+                        t0e = torch.cuda.Event(enable_timing=True)
+                        t0e.record(self.ctxG.stream)
                     Ln._early = Ln.early_host_prefetch(self.ctxG, self.asm_ws, self.host_window, self.out_budget,
                                                        f"_{(e + 1) % 2}", after)
+                    if self.asm_trace_on and Ln._early is not None:
+                        t1e = torch.cuda.Event(enable_timing=True)
+                        t1e.record(self.ctxG.stream)
+                        self.early_trace.append((t0e, t1e))
                 if os.environ.get("DGNN_MEM_TRACE") == "1":  # allocator counters (host side, no sync)
                     log(f"[mem] pass {e + 1}: allocated {torch.cuda.memory_allocated(self.dev) / 1e9:.1f} GB, "
                         f"reserved {torch.cuda.memory_reserved(self.dev) / 1e9:.1f} GB, kept "
@@ -1039,6 +1052,13 @@ def main():
             result["cpu_baseline"] = {"value": None, "error": str(ex)[:200]}
     if R.asm_traces:  # DGNN_ASM_TRACE=1: per-window copy / runs spans of the last traced assembly
         a0, tr = R.asm_traces[-1]
+        log(f"[asm-trace] host enqueue ms per assembly: {[round(x, 1) for x in R.asm_host_ms[-6:]]}")
+        t0 = R.timeline[0][1]
+        for (evs, _), a0_, a1_ in R.timeline[-4:]:
+            d = {name: round(t0.elapsed_time(ev), 1) for name, ev in evs}
+            log(f"[asm-trace] layout {d} assembly {round(t0.elapsed_time(a0_), 1)}-{round(t0.elapsed_time(a1_), 1)}")
+        for x, y in R.early_trace[-4:]:
+            log(f"[asm-trace] early copy issued {round(t0.elapsed_time(x), 1)} done {round(t0.elapsed_time(y), 1)}")
         log("[asm-trace] w: copy start-end | runs start-end (ms from the assembly start)")
         for w in sorted(tr):
             t = tr[w]

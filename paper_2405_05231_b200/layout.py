@@ -130,6 +130,8 @@ class Layout:
     host_order: A.HostOrder | None = None  # window-ordered host tier (physical rows permuted)
     host_order_key: tuple = None    # (host_window, out_budget) the ordering was built for
     host_w0_event: object = None    # the layout stream's event once window 0's host rows are filled
+    host_w0_ticket: int = None      # (fill through HBM) the side-stream ticket of window 0's rows
+    host_fill_ticket: int = None    # (fill through HBM) the ticket after which the whole tier is filled
 
     def phase_ms(self) -> dict:
         """Device time of the layout's phases (after the stream has passed them)."""
@@ -179,6 +181,8 @@ class Layout:
                 part = torch.empty(max(rows * self.row_bytes, 16), dtype=torch.uint8, device=dev)
                 zero = torch.zeros(2, dtype=torch.int64, device=dev)
                 chunk = self._partial(self.ctx, b, b + 1, chunk, zero, zero, pages, part)
+        if self.host_fill_ticket is not None:
+            A.dgnn_stage_wait(self.ctx, self.host_fill_ticket)
         if self.host_order is None:
             A.dgnn_assemble(self.ctx, self.addr[n0:n1], self.gpu_tier, self.plan.k_gpu, self.host_tier.ptr,
                             self.plan.k_host, chunk, rows, self.row_bytes, out)
@@ -198,12 +202,16 @@ class Layout:
         ``after`` events (the arena's previous user done) have passed -> the event to hand to
         assemble_epoch(early=...), or None when the assembly would not use the ordering."""
         ho = self.host_order
-        if ho is None or self.host_w0_event is None or self.host_order_key != (host_window, int(out_budget)):
+        if ho is None or self.host_order_key != (host_window, int(out_budget)) or \
+                (self.host_w0_event is None and self.host_w0_ticket is None):
             return None
         with torch.cuda.stream(gctx.stream):
             nbytes = max(ho.capacity, 1) * self.row_bytes
             arena = ws.dev("staging0" + arena_tag, nbytes, gctx.device)[:nbytes]
-        gctx.stream.wait_event(self.host_w0_event)
+        if self.host_w0_ticket is not None:
+            A.dgnn_stage_wait_stream(self.ctx, self.host_w0_ticket, gctx.stream)
+        else:
+            gctx.stream.wait_event(self.host_w0_event)
         for ev in after:
             gctx.stream.wait_event(ev)
         A.dgnn_copy_ranges(gctx, arena, self.host_tier.ptr, ho.copies[0], self.row_bytes)
@@ -417,6 +425,8 @@ class Layout:
                     wspan = []
             if wspan:
                 wchunk = [buf(f"wchunk{i}", max(hi - lo for lo, hi in wspan)) for i in range(2)]
+        if self.host_fill_ticket is not None:  # the host tier is filled on the layout's side stream
+            A.dgnn_stage_wait_stream(self.ctx, self.host_fill_ticket, ctx.stream)
         if gctx is not ctx:
             gctx.stream.wait_stream(ctx.stream)  # stamp / buffers were created on the ctx stream
         run_window = {r0: wi for wi, (r0, _) in enumerate(windows)}
@@ -795,14 +805,36 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
             first = ho.ranges[0].reshape(-1, 3)[:, :2] if len(ho.ranges[0]) else np.zeros((0, 2), np.int64)
             done = np.zeros(kh + 1, np.int8)
             for lo, hi in first:
-                A.dgnn_gather_rows(ctx, features, ho.phys_ids[int(lo):int(hi)], host_tier.ptr + int(lo) * rb)
                 done[int(lo):int(hi)] = 1
-            ev = torch.cuda.Event()
-            ev.record(ctx.stream)
-            L.host_w0_event = ev
             edges = np.flatnonzero(np.diff(np.concatenate([[1], done[:kh], [1]])))  # runs of unfilled rows
-            for lo, hi in zip(edges[0::2], edges[1::2]):
-                A.dgnn_gather_rows(ctx, features, ho.phys_ids[int(lo):int(hi)], host_tier.ptr + int(lo) * rb)
+            rest = list(zip(edges[0::2], edges[1::2]))
+            fws = scratch_ws if scratch_ws is not None else ws
+            if fws is not None and not isinstance(features, A.ShardedFeatures):
+                # through HBM: the rows gathered in physical order on the layout's stream (HBM-bound,
+                # milliseconds), then copied to the pinned tier by the copy engine on the side stream
+                # (window 0's range first), so the layout's stream does not spend the D2H time.  The
+                # buffer is scratch: the next pass on this ctx reuses it after waiting for the side
+                # stream (the wait before classify)
+                with torch.cuda.stream(ctx.stream):
+                    hbuf = fws.dev("host_fill", kh * rb, dev)[:kh * rb]
+                A.dgnn_gather_rows(ctx, features, ho.phys_ids[:kh], hbuf)
+                t = None
+                for lo, hi in first:
+                    t = A.dgnn_stage_copy(ctx, host_tier.ptr + int(lo) * rb, hbuf.data_ptr() + int(lo) * rb,
+                                          (int(hi) - int(lo)) * rb, 0)
+                L.host_w0_ticket = t
+                for lo, hi in rest:
+                    t = A.dgnn_stage_copy(ctx, host_tier.ptr + int(lo) * rb, hbuf.data_ptr() + int(lo) * rb,
+                                          (int(hi) - int(lo)) * rb, 0)
+                L.host_fill_ticket = t
+            else:  # SM stores into the pinned tier, window 0's range first
+                for lo, hi in first:
+                    A.dgnn_gather_rows(ctx, features, ho.phys_ids[int(lo):int(hi)], host_tier.ptr + int(lo) * rb)
+                ev = torch.cuda.Event()
+                ev.record(ctx.stream)
+                L.host_w0_event = ev
+                for lo, hi in rest:
+                    A.dgnn_gather_rows(ctx, features, ho.phys_ids[int(lo):int(hi)], host_tier.ptr + int(lo) * rb)
             stats["host_order"] = {"windows": ho.nwin, "groups": ho.n_groups,
                                    "ranges_per_window": [len(r) // 3 for r in ho.ranges], "rows": ho.rows,
                                    "rows_copied": ho.copy_rows, "arena_rows": ho.capacity}
@@ -810,11 +842,8 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
             A.dgnn_gather_rows(ctx, features, plan.host_ids, host_tier.ptr)
     if nb:
         L.assembly_plan(int(asm_out_budget))  # a9's per-run tables, uploaded here on the layout's stream
-    mark("classify")
-    if before_pack is not None:
-        before_pack()
-    # a7 pack + a8 stage-out, double-buffered group buffers; every group's stage-out
-    # ticket is kept so the assembler waits for exactly the chunks it reads
+    # a7's tables go up before the pack's wait (before_pack): an H2D copy queued between that wait
+    # and the pack would sit behind whatever the copy engines are moving for the assembly then
     with torch.cuda.stream(ctx.stream):
         rel_all = torch.from_numpy(np.concatenate(
             [np.concatenate([po[g.b_lo:g.b_hi + 1] - po[g.b_lo], g.chunk_off]) for g in groups]
@@ -828,6 +857,13 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
             sec_src = torch.from_numpy(np.concatenate([g.sec_off for g in groups]).astype(np.int64)).pin_memory()
             sec_dev = sec_src.to(dev, non_blocking=True)
             L._pinned_srcs.append(sec_src)
+    mark("classify")
+    if before_pack is not None:
+        before_pack()
+        mark("pack_wait")  # (measurement: where the pack's wait for the previous assembly ended)
+    # a7 pack + a8 stage-out, double-buffered group buffers; every group's stage-out
+    # ticket is kept so the assembler waits for exactly the chunks it reads
+    with torch.cuda.stream(ctx.stream):
         max_gb = max([g.group_bytes for g in groups], default=0)
         staged = arena is not None or disk is not None
         # group buffers come from the workspace when there is one: re-allocating GBs every

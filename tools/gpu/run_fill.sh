@@ -1,0 +1,5 @@
+timeout 900 python -m pytest tests/test_gpu_host_order.py tests/test_gpu_bench_runner.py -m gpu -x -q 2>&1 | tail -2
+DGNN_ASM_TRACE=1 timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu --no-e2e > gpurun_out/r2_bench_fill.json 2> gpurun_out/r2_bench_fill.err
+python -c "
+import json;d=json.loads(open('gpurun_out/r2_bench_fill.json').read().strip().splitlines()[-1]); print(d['value'], d['ms_per_step'], d['memory']['max_reserved_gb'], d['step_roofline']['frac'])"
+grep "asm-trace" gpurun_out/r2_bench_fill.err | grep -v "^\[asm-trace\] [0-9]:"
