@@ -476,6 +476,9 @@ constexpr int kPartThreads = 512;
 constexpr int kPartTableLog = 12;                       // 4096 slots: keys + locals + sort keys = 64 KB
 constexpr int kPartTable = 1 << kPartTableLog;
 constexpr size_t kPartSmem = (size_t)kPartTable * 16;  // dynamic shared memory of k_part_dedup
+constexpr int kRankBits = 10;  // sub-ranges of a bucket's ID range in the counting order
+constexpr int kRankMax = 2048; // new IDs a bucket ranks by counting (above: bitonic sort)
+static_assert((kPartTable - kRankMax) * 2 >= (1 << kRankBits) + 1 + kRankMax, "rank scratch in s_new");
 
 constexpr int kSeedSortMax = 4096;                      // batch_size limit of the partitioned path
 constexpr int kPartTile = 8192;                         // candidates per tile in count / scatter
@@ -486,6 +489,7 @@ struct Part {
     int pbits;   // P = 1 << pbits ranges per batch
     int pshift;  // range of u = u >> pshift
     int nslices; // slices of nodes-so-far: sorted seeds + one per finished hop
+    int rank_max;  // buckets with at most this many new IDs order them by counting, others sort
     int32_t* sid;     // [G * B] seeds sorted by ID
     int32_t* sloc;    // [G * B] their local IDs
     int32_t* bnd;     // [G * (H+1) * (P+1)] start of range p in slice x, relative to the slice
@@ -522,6 +526,32 @@ __device__ __forceinline__ void bitonic_sort_smem(T* a, int n2) {
                 }
             }
         }
+    }
+    __syncthreads();
+}
+
+// in-place exclusive prefix sum of a[0, n) in shared memory, all threads of the block (each
+// thread sums a contiguous piece, warp scan of the piece totals, block combine)
+__device__ __forceinline__ void block_excl_scan_smem(int32_t* a, int n, int32_t* warp_tmp) {
+    const int per = (n + blockDim.x - 1) / blockDim.x;
+    const int lo = min(n, (int)threadIdx.x * per), hi = min(n, lo + per);
+    int32_t sum = 0;
+    for (int i = lo; i < hi; ++i) sum += a[i];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int32_t x = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tmp[warp] = x;
+    __syncthreads();
+    int32_t pre = x - sum;
+    for (int w = 0; w < warp; ++w) pre += warp_tmp[w];
+    for (int i = lo; i < hi; ++i) {
+        const int32_t v = a[i];
+        a[i] = pre;
+        pre += v;
     }
     __syncthreads();
 }
@@ -648,6 +678,7 @@ __global__ void __launch_bounds__(kPartThreads) k_part_dedup(Grp g, Part pt, int
     unsigned long long* s_new = reinterpret_cast<unsigned long long*>(s_dyn);
     int32_t* s_key = reinterpret_cast<int32_t*>(s_new + kPartTable);
     int32_t* s_loc = s_key + kPartTable;
+    __shared__ int32_t s_scan_tmp[kPartThreads / 32];
     __shared__ int s_nnew;
     __shared__ volatile int s_over;
     __shared__ unsigned s_ticket;
@@ -750,7 +781,46 @@ __global__ void __launch_bounds__(kPartThreads) k_part_dedup(Grp g, Part pt, int
         // it), sort, and only then look back: the predecessors publish while this CTA sorts
         if (threadIdx.x == 0)
             st_relaxed(&pt.status[b], (p == 0 ? scan::kFlagP : scan::kFlagA) | (unsigned long long)nnew);
-        if (!over) {
+        // ranked: s_new[r] = (rank << 32 | slot) instead of sorted (u << 32 | slot)
+        const bool ranked = !over && nnew > 1 && nnew <= pt.rank_max;
+        if (ranked) {
+            // order (reading c10) by counting: the bucket's ID range in 2^kRankBits sub-ranges
+            // (counts and the grouped list live in s_new past its kRankMax used entries); an ID's
+            // rank = the new IDs of lower sub-ranges + those of its own sub-range below it
+            int32_t* s_cnt = reinterpret_cast<int32_t*>(s_new + kRankMax);  // [nsub + 1]
+            int32_t* s_grp = s_cnt + (1 << kRankBits) + 1;                  // [nnew]
+            const int rs = pt.pshift > kRankBits ? pt.pshift - kRankBits : 0;
+            const int nsub = 1 << (pt.pshift < kRankBits ? pt.pshift : kRankBits);
+            const int32_t base_id = p << pt.pshift;
+            for (int i = threadIdx.x; i <= nsub; i += blockDim.x) s_cnt[i] = 0;
+            __syncthreads();
+            for (int r = threadIdx.x; r < nnew; r += blockDim.x)
+                atomicAdd(&s_cnt[((int32_t)(s_new[r] >> 32) - base_id) >> rs], 1);
+            __syncthreads();
+            block_excl_scan_smem(s_cnt, nsub, s_scan_tmp);  // s_cnt[sub] = start of sub
+            for (int r = threadIdx.x; r < nnew; r += blockDim.x)
+                s_grp[atomicAdd(&s_cnt[((int32_t)(s_new[r] >> 32) - base_id) >> rs], 1)] = r;
+            __syncthreads();  // now s_cnt[sub] = end of sub = start of sub + 1
+            int rk[kRankMax / kPartThreads];
+#pragma unroll
+            for (int k = 0; k < kRankMax / kPartThreads; ++k) {
+                const int r = threadIdx.x + k * kPartThreads;
+                if (r >= nnew) break;
+                const int32_t u = (int32_t)(s_new[r] >> 32);
+                const int sub = (u - base_id) >> rs;
+                const int lo = sub ? s_cnt[sub - 1] : 0, hi = s_cnt[sub];
+                int rank = lo;
+                for (int q = lo; q < hi; ++q) rank += ((int32_t)(s_new[s_grp[q]] >> 32) < u) ? 1 : 0;
+                rk[k] = rank;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int k = 0; k < kRankMax / kPartThreads; ++k) {
+                const int r = threadIdx.x + k * kPartThreads;
+                if (r >= nnew) break;
+                s_new[r] = ((unsigned long long)(uint32_t)rk[k] << 32) | (uint32_t)s_new[r];
+            }
+        } else if (!over) {
             int n2 = 1;
             while (n2 < nnew) n2 <<= 1;
             for (int i = nnew + threadIdx.x; i < n2; i += blockDim.x) s_new[i] = ~0ull;
@@ -792,8 +862,9 @@ __global__ void __launch_bounds__(kPartThreads) k_part_dedup(Grp g, Part pt, int
             int32_t* onodes = g.nodes + (int64_t)s * g.cap_n;
             for (int r = threadIdx.x; r < nnew; r += blockDim.x) {
                 const unsigned long long e = s_new[r];
-                onodes[base + r] = (int32_t)(e >> 32);
-                s_loc[(uint32_t)e] = base + r;
+                const int32_t local = ranked ? base + (int32_t)(e >> 32) : base + r;  // (rank | slot) or sorted
+                onodes[local] = ranked ? s_key[(uint32_t)e] : (int32_t)(e >> 32);
+                s_loc[(uint32_t)e] = local;
             }
             __syncthreads();
             // remap: every candidate of the bucket to its local ID
@@ -1182,6 +1253,8 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
         // distinct IDs (from the node bound after the hop, capped by the ctx's hint) ----
         const char* dd = std::getenv("DGNN_SAMPLE_DEDUP");
         bool part = batch_size <= kSeedSortMax && H <= kMaxHops && !(dd && std::string(dd) == "table");
+        const char* so = std::getenv("DGNN_SAMPLE_ORDER");  // "sort": bitonic order for every bucket
+        const int rank_max = (so && std::string(so) == "sort") ? 0 : kRankMax;
         const int pbits_max = std::min(idbits, 12);
         std::vector<int64_t> after_bound(H), after_seen(H, 0);
         {
@@ -1406,6 +1479,7 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
                     pt.pbits = pbits_for(h);
                     pt.pshift = idbits - pt.pbits;
                     pt.nslices = h + 1;
+                    pt.rank_max = rank_max;
                     const int64_t P = (int64_t)1 << pt.pbits, nbk = Gc * P;
                     DGNN_TRY(memset_async(c, pt.bnd, 0, sizeof(int32_t) * (size_t)Gc * (H + 1) * (P + 1)));
                     DGNN_TRY(memset_async(c, pt.bcnt, 0, sizeof(int32_t) * (size_t)nbk));

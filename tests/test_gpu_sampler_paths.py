@@ -4,6 +4,9 @@ The sampler has two implementations of "new = distinct(cand) minus nodes-so-far,
 edges remapped" (readings c10/c11): the default partitioned path (candidates bucketed by
 (batch, ID range), deduplicated in shared memory) and the per-batch global hash-set path, which
 also serves as its fallback when a bucket overflows.  DGNN_SAMPLE_DEDUP=table selects the second.
+The partitioned path orders a bucket's new IDs by counting (sub-range counts, rank within the
+sub-range) up to 2048 of them and by a bitonic sort above; DGNN_SAMPLE_ORDER=sort sorts every
+bucket, so both orderings are compared.
 Every case is compared byte for byte with the oracle, including inputs built so that one ID range
 holds more distinct IDs than a shared-memory bucket (the fallback must give the same bytes).
 """
@@ -33,12 +36,15 @@ def ctx(dg):
     return dg.Ctx(device=0)
 
 
-@pytest.fixture(params=["part", "table"])
+@pytest.fixture(params=["part", "part-sort", "table"])
 def path(request, monkeypatch):
+    monkeypatch.delenv("DGNN_SAMPLE_ORDER", raising=False)
     if request.param == "table":
         monkeypatch.setenv("DGNN_SAMPLE_DEDUP", "table")
     else:
         monkeypatch.delenv("DGNN_SAMPLE_DEDUP", raising=False)
+    if request.param == "part-sort":  # every bucket's new IDs ordered by the bitonic sort
+        monkeypatch.setenv("DGNN_SAMPLE_ORDER", "sort")
     return request.param
 
 

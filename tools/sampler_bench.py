@@ -43,6 +43,10 @@ def main():
             os.environ["DGNN_SAMPLE_DEDUP"] = "table"
         else:
             os.environ.pop("DGNN_SAMPLE_DEDUP", None)
+        if path == "part-sort":  # bitonic order in every bucket instead of the counting order
+            os.environ["DGNN_SAMPLE_ORDER"] = "sort"
+        else:
+            os.environ.pop("DGNN_SAMPLE_ORDER", None)
         ctx = dg.Ctx(device=dev)
         counts = torch.zeros(N, dtype=torch.int32, device=dev)
         times, stats = [], None
@@ -71,9 +75,9 @@ def main():
         print(path, json.dumps(res[path]), file=sys.stderr)
         del S
         ctx.close()
-    if len(keep) == 2:
-        a, b = keep["part"], keep["table"]
-        res["paths_identical"] = all(torch.equal(x, y) for x, y in zip(a, b))
+    if len(keep) >= 2:
+        a = next(iter(keep.values()))
+        res["paths_identical"] = all(all(torch.equal(x, y) for x, y in zip(a, b)) for b in keep.values())
     print(json.dumps(res))
     if args.out:
         with open(args.out, "w") as f:
