@@ -559,7 +559,7 @@ class Runner:
                     if self.asm_trace_on and Ln._early is not None:
                         t1e = torch.cuda.Event(enable_timing=True)
                         t1e.record(self.ctxG.stream)
-                        self.early_trace.append((t0e, t1e))
+                        self.early_trace.append((t0e, t1e, getattr(Ln, "_early_start", None)))
                 if os.environ.get("DGNN_MEM_TRACE") == "1":  # allocator counters (host side, no sync)
                     log(f"[mem] pass {e + 1}: allocated {torch.cuda.memory_allocated(self.dev) / 1e9:.1f} GB, "
                         f"reserved {torch.cuda.memory_reserved(self.dev) / 1e9:.1f} GB, kept "
@@ -791,6 +791,7 @@ def main():
     kst_timed = kst
     gathered_rows = int(R.pcie_rows.item())
     timeline = R.timeline_ms()
+    timed_trace = (list(R.asm_traces), list(R.timeline), list(R.early_trace))  # DGNN_ASM_TRACE: timed passes
     # every kernel family, over extra instrumented passes (not part of the timed value)
     stat_steps = max(1, args.stat_steps)
     for c in R.ctxs():
@@ -1050,20 +1051,23 @@ def main():
             result["cpu_baseline"] = cb
         except Exception as ex:  # the baseline is reported, never required
             result["cpu_baseline"] = {"value": None, "error": str(ex)[:200]}
-    if R.asm_traces:  # DGNN_ASM_TRACE=1: per-window copy / runs spans of the last traced assembly
-        a0, tr = R.asm_traces[-1]
+    if timed_trace[0]:  # DGNN_ASM_TRACE=1: per-window copy / runs spans of the timed region's last assemblies
+        traces, tl, early = timed_trace
         log(f"[asm-trace] host enqueue ms per assembly: {[round(x, 1) for x in R.asm_host_ms[-6:]]}")
-        t0 = R.timeline[0][1]
-        for (evs, _), a0_, a1_ in R.timeline[-4:]:
+        t0 = tl[-4][1] if len(tl) >= 4 else tl[0][1]
+        for (evs, _), a0_, a1_ in tl[-4:]:
             d = {name: round(t0.elapsed_time(ev), 1) for name, ev in evs}
             log(f"[asm-trace] layout {d} assembly {round(t0.elapsed_time(a0_), 1)}-{round(t0.elapsed_time(a1_), 1)}")
-        for x, y in R.early_trace[-4:]:
-            log(f"[asm-trace] early copy issued {round(t0.elapsed_time(x), 1)} done {round(t0.elapsed_time(y), 1)}")
-        log("[asm-trace] w: copy start-end | runs start-end (ms from the assembly start)")
-        for w in sorted(tr):
-            t = tr[w]
-            f = lambda k: round(a0.elapsed_time(t[k]), 1) if k in t else None
-            log(f"[asm-trace] {w}: {f('copy0')}-{f('copy1')} | {f('runs0')}-{f('runs1')}")
+        for x, y, z in early[-4:]:
+            log(f"[asm-trace] early copy issued {round(t0.elapsed_time(x), 1)} started "
+                f"{round(t0.elapsed_time(z), 1) if z is not None else None} done {round(t0.elapsed_time(y), 1)}")
+        for a0, tr in traces[-3:-1]:  # (the last one ends the run: no next pass beside it)
+            log(f"[asm-trace] assembly at {round(t0.elapsed_time(a0), 1)}; "
+                "w: copy start-end | runs start-end (ms from the assembly start)")
+            for w in sorted(tr):
+                t = tr[w]
+                f = lambda k: round(a0.elapsed_time(t[k]), 1) if k in t else None
+                log(f"[asm-trace] {w}: {f('copy0')}-{f('copy1')} | {f('runs0')}-{f('runs1')}")
     if rank == 0:
         print(json.dumps(result), flush=True)
     if ws > 1:

@@ -403,7 +403,9 @@ dgnn_status dgnn_stage_file_read(dgnn_ctx* ctx, dgnn_file* f, int64_t file_off, 
  *   of capacity_rows rows.  A group is needed by the maximal runs of consecutive windows in its
  *   mask; each (group, run) is copied once, at the prefetch of its first window, and stays in the
  *   arena until its last window is done (window w is prefetched once window w-2 is done), so rows
- *   shared by consecutive windows cross PCIe once.  Outputs per window w (CSR, copy_off / map_off
+ *   shared by consecutive windows cross PCIe once.  Spare capacity bridges the gaps between runs of a
+ *   group (shortest first, when the arena has room in every window of the gap): with capacity_rows
+ *   >= the rows the windows touch, every row crosses once per pass.  Outputs per window w (CSR, copy_off / map_off
  *   [nwin+1]): the copies to issue (copy_out triples) and the map of every row w reads (map_out
  *   triples sorted by phys_lo: the input of dgnn_host_window_ranges); *rows_copied = total rows
  *   moved.  EINVAL if the capacity (>= max over w of |S_{w-1}| + |S_w| always fits) or an output
@@ -428,6 +430,13 @@ dgnn_status dgnn_host_order_schedule(const int64_t* group_start_host, const uint
 dgnn_status dgnn_host_window_ranges(dgnn_ctx* ctx, const uint32_t* slot_mask, const int32_t* phys_of_slot,
                                     int64_t k_host, int32_t window, const int64_t* ranges_dev, int64_t nr,
                                     int32_t* smap);
+/* Small host -> device table upload (the per-run assembly tables, the pack's offset tables; a
+ * scheduling primitive, no arithmetic of the method): `bytes` of src_host (any host memory, read
+ * before the call returns) to dst_dev (device, caller-owned), enqueued on the ctx stream as kernels
+ * that carry the bytes in their parameters -- not the copy engines, where a small copy queues behind
+ * the gigabytes of window and stage copies in flight (and the stream's next operations with it).
+ * Above 256 KiB: one cudaMemcpyAsync.  Errors: DGNN_EINVAL (NULL with bytes > 0, bytes < 0). */
+dgnn_status dgnn_upload(dgnn_ctx* ctx, void* dst_dev, const void* src_host, int64_t bytes);
 dgnn_status dgnn_copy_ranges(dgnn_ctx* ctx, void* dst_dev, const void* src_host, const int64_t* ranges_host,
                              int64_t nr, int64_t row_bytes);
 dgnn_status dgnn_remap_ids_dev(dgnn_ctx* ctx, int32_t* ids, const int64_t* n_dev, int64_t n_max,

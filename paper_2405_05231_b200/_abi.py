@@ -50,7 +50,7 @@ EXPORTS = [
     "dgnn_ctx_set_keep_limit", "dgnn_ctx_kept_bytes", "dgnn_ctx_set_sample_budget", "dgnn_file_set_queues",
     "dgnn_chunk_layout_graph", "dgnn_pack_graph", "dgnn_samples_load", "dgnn_samples_drop_device",
     "dgnn_host_order", "dgnn_host_order_ranges", "dgnn_host_window_ranges", "dgnn_copy_ranges", "dgnn_remap_ids_dev",
-    "dgnn_pack_sharded", "dgnn_gather_rows_sharded", "dgnn_host_order_schedule",
+    "dgnn_pack_sharded", "dgnn_gather_rows_sharded", "dgnn_host_order_schedule", "dgnn_upload",
 ]
 
 
@@ -148,6 +148,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "dgnn_host_order_ranges": (i32, [P, P, i64, i64, i32, P, i64, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
             "dgnn_host_window_ranges": (i32, [P, P, P, i64, i32, P, i64, P]),
             "dgnn_copy_ranges": (i32, [P, P, P, P, i64, i64]),
+            "dgnn_upload": (i32, [P, P, P, i64]),
             "dgnn_remap_ids_dev": (i32, [P, P, P, i64, P]),
             "dgnn_host_order_schedule": (i32, [P, P, i64, i64, i32, i64, P, i64, P, P, i64, P,
                                                 ctypes.POINTER(i64)]),
@@ -197,12 +198,29 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "dgnn_pack_partition": (i32, [P, P, P, i64, i64, i64, P, P]),
             "dgnn_pack_tails": (i32, [P, P, i64, P, P]),
         }
+        # Enqueue-only entry points (kernel launches, async copies, stream waits: they never wait
+        # for the device or another thread) are called through a PyDLL handle, which keeps the
+        # GIL across the call.  Releasing it for a few microseconds would make the calling thread
+        # queue for it again behind the other host thread (the layout and the assembly are
+        # enqueued by two threads): up to a switch interval per call, hundreds of calls per pass.
+        # Calls that synchronize (sizes read back, dgnn_sample, ...) keep releasing the GIL.
+        LP = ctypes.PyDLL(path) if os.environ.get("DGNN_PYDLL", "1") == "1" else None
         for name, (res, args) in sig.items():
-            f = getattr(L, name)
+            f = getattr(LP if (LP is not None and name in _ENQUEUE_ONLY) else L, name)
             f.restype = res
             f.argtypes = args
+            setattr(L, name, f)
         _lib = L
         return L
+
+
+# entry points that only enqueue work on streams (no synchronization, no host waits); see load_library
+_ENQUEUE_ONLY = frozenset([
+    "dgnn_assemble_group", "dgnn_assemble_group_peer", "dgnn_assemble_group_sharded", "dgnn_copy_ranges", "dgnn_upload",
+    "dgnn_host_window_ranges", "dgnn_host_window", "dgnn_remap_ids_dev", "dgnn_stage_wait",
+    "dgnn_stage_wait_stream", "dgnn_stage_copy", "dgnn_gather_rows", "dgnn_gather_rows_dev", "dgnn_pack",
+    "dgnn_ctx_launches", "dgnn_ctx_stream", "dgnn_ctx_side_stream", "dgnn_last_error", "dgnn_kernel_name",
+])
 
 
 def _check(status: int, fn: str):
@@ -527,6 +545,19 @@ def dgnn_samples_load(ctx: Ctx, meta: Samples, b_lo: int, b_hi: int, base, sec_o
     return Samples(ctx, h)
 
 
+def dgnn_upload(ctx: Ctx, src, dtype=torch.int64) -> torch.Tensor:
+    """A small host array (numpy) -> a new device tensor on ctx's stream, through kernel
+    parameters (dgnn_upload), not the copy engines."""
+    import numpy as np
+    a = np.ascontiguousarray(src)
+    with torch.cuda.stream(ctx.stream):
+        out = torch.empty(a.size, dtype=dtype, device=ctx.device)
+    if out.element_size() != a.itemsize:
+        raise ValueError("dgnn_upload: dtype size mismatch")
+    _check(load_library().dgnn_upload(ctx.handle, _ptr(out), P(a.ctypes.data), a.nbytes), "dgnn_upload")
+    return out
+
+
 class HostOrder:
     """The window-ordered host tier of one layout (dgnn_host_order): device slot_mask / phys_of_slot
     / phys_ids, and per window its physical ranges (host triples + device copy)."""
@@ -576,11 +607,8 @@ class HostOrder:
         self.copy_rows = [int((c[1::3] - c[0::3]).sum()) for c in self.copies]
         maps = [mo[3 * moff[w]:3 * moff[w + 1]].copy() for w in range(self.nwin)]
         self.map_len = [len(m) // 3 for m in maps]
-        with torch.cuda.stream(ctx.stream):
-            cat = np.concatenate(self.ranges + maps + [np.zeros(1, np.int64)])
-            src = torch.from_numpy(cat).pin_memory()
-            flat = src.to(dev, non_blocking=True)
-        self._src = src
+        cat = np.concatenate(self.ranges + maps + [np.zeros(1, np.int64)]).astype(np.int64)
+        flat = dgnn_upload(ctx, cat)
         offs = np.concatenate([[0], np.cumsum([len(r) for r in self.ranges + maps])])
         self.ranges_dev = [flat[int(offs[w]):int(offs[w + 1])] for w in range(self.nwin)]
         self.map_dev = [flat[int(offs[self.nwin + w]):int(offs[self.nwin + w + 1])] for w in range(self.nwin)]

@@ -69,8 +69,7 @@ extern "C" dgnn_status dgnn_build_cache(dgnn_ctx* c, const uint32_t* counts, int
     });
     DGNN_CK_LAUNCH();
     unsigned int mx = 0;
-    DGNN_CK(cudaMemcpyAsync(&mx, d_max.p, sizeof(mx), cudaMemcpyDeviceToHost, c->stream));
-    DGNN_CK(cudaStreamSynchronize(c->stream));
+    DGNN_TRY(read_small(c, &mx, d_max.p, sizeof(mx)));
     if (mx >= kMaxCount) {
         set_error("dgnn_build_cache: max count %u >= 2^24 is outside the supported envelope", mx);
         return DGNN_EUNSUPPORTED;
@@ -84,8 +83,7 @@ extern "C" dgnn_status dgnn_build_cache(dgnn_ctx* c, const uint32_t* counts, int
     });
     DGNN_CK_LAUNCH();
     std::vector<unsigned int> hist(nbins);
-    DGNN_CK(cudaMemcpyAsync(hist.data(), d_hist.p, sizeof(unsigned int) * nbins, cudaMemcpyDeviceToHost, c->stream));
-    DGNN_CK(cudaStreamSynchronize(c->stream));
+    DGNN_TRY(read_small(c, hist.data(), d_hist.p, sizeof(unsigned int) * nbins));
 
     // ---- host: ranks above each count value, capacities and boundary values ----
     const int64_t nnz = N - (int64_t)hist[0];
@@ -108,7 +106,7 @@ extern "C" dgnn_status dgnn_build_cache(dgnn_ctx* c, const uint32_t* counts, int
     const uint32_t ch = kh > 0 ? value_at_rank(kg + kh - 1) : 0;   // boundary group of the host tier
     DevBuf<int64_t> d_above;
     DGNN_TRY(d_above.alloc(c, nbins));
-    DGNN_CK(cudaMemcpyAsync(d_above.p, above.data(), sizeof(int64_t) * nbins, cudaMemcpyHostToDevice, c->stream));
+    DGNN_TRY(upload_small(c, d_above.p, above.data(), sizeof(int64_t) * nbins));
 
     auto* P = new dgnn_cache_plan();
     P->ctx = c;

@@ -2,6 +2,9 @@
 // ctx.cu -- context, errors, allocation, statistics and the a8 staging runtime.
 #include <atomic>
 #include <cstdarg>
+#include <cstdlib>
+#include <cstring>
+#include <string>
 
 #include "internal.cuh"
 
@@ -132,11 +135,96 @@ void* pinned_scratch(dgnn_ctx* c, size_t bytes) {
 
 extern std::atomic<int> g_io_error;
 
-dgnn_status read_dev_err(dgnn_ctx* c, int* flags) {
-    if (!c->pinned_err) DGNN_CK(cudaHostAlloc((void**)&c->pinned_err, sizeof(int), cudaHostAllocDefault));
-    DGNN_CK(cudaMemcpyAsync(c->pinned_err, c->dev_err, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+namespace {
+// word-wise copy into mapped pinned host memory; SM stores go out as posted PCIe writes
+__global__ void k_readback(uint32_t* __restrict__ dst, const uint32_t* __restrict__ src, size_t nw) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nw; i += (size_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+    __threadfence_system();
+}
+bool readback_by_copy() {
+    static const bool v = [] {
+        const char* e = std::getenv("DGNN_SMALL_D2H");
+        return e && std::string(e) == "copy";
+    }();
+    return v;
+}
+}  // namespace
+
+dgnn_status readback_reserve(dgnn_ctx* c, size_t bytes) {
+    if (bytes <= c->rb_bytes) return DGNN_OK;
+    if (c->rb) DGNN_CK(cudaFreeHost(c->rb));
+    c->rb = nullptr;
+    c->rb_bytes = 0;
+    const size_t n = std::max<size_t>(bytes + bytes / 2, 64 << 10);
+    DGNN_CK(cudaHostAlloc(&c->rb, n, cudaHostAllocMapped | cudaHostAllocPortable));
+    c->rb_bytes = n;
+    return DGNN_OK;
+}
+
+dgnn_status readback_enqueue(dgnn_ctx* c, size_t off, const void* src_dev, size_t n) {
+    if (!n) return DGNN_OK;
+    if (off + n > c->rb_bytes || (off | n | (size_t)src_dev) % 4) {
+        set_error("readback_enqueue: %zu bytes at %zu outside the reserved %zu (or misaligned)", n, off, c->rb_bytes);
+        return DGNN_EINVAL;
+    }
+    uint8_t* dst = static_cast<uint8_t*>(c->rb) + off;
+    if (readback_by_copy()) {
+        DGNN_CK(cudaMemcpyAsync(dst, src_dev, n, cudaMemcpyDeviceToHost, c->stream));
+        return DGNN_OK;
+    }
+    uint32_t* ddst = nullptr;
+    DGNN_CK(cudaHostGetDevicePointer((void**)&ddst, dst, 0));
+    const size_t nw = n / 4;
+    const int grid = (int)std::min<size_t>((nw + 1023) / 1024, (size_t)c->num_sms);
+    k_readback<<<std::max(grid, 1), 256, 0, c->stream>>>(ddst, static_cast<const uint32_t*>(src_dev), nw);
+    DGNN_CK(cudaGetLastError());
+    return DGNN_OK;
+}
+
+constexpr int kUploadChunk = 4000;  // bytes per launch (kernel parameter space)
+struct UploadChunk {
+    uint8_t b[kUploadChunk];
+};
+__global__ void k_upload(uint8_t* __restrict__ dst, const UploadChunk chunk, int n) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = chunk.b[i];
+}
+
+dgnn_status upload_small(dgnn_ctx* c, void* dst_dev, const void* src_host, size_t n) {
+    if (!n) return DGNN_OK;
+    if (n > kUploadMax || readback_by_copy()) {
+        DGNN_CK(cudaMemcpyAsync(dst_dev, src_host, n, cudaMemcpyHostToDevice, c->stream));
+        return DGNN_OK;
+    }
+    UploadChunk ch;
+    for (size_t off = 0; off < n; off += kUploadChunk) {
+        const int len = (int)std::min<size_t>(kUploadChunk, n - off);
+        std::memcpy(ch.b, static_cast<const uint8_t*>(src_host) + off, (size_t)len);
+        k_upload<<<1, 256, 0, c->stream>>>(static_cast<uint8_t*>(dst_dev) + off, ch, len);
+        DGNN_CK(cudaGetLastError());
+    }
+    return DGNN_OK;
+}
+
+dgnn_status read_small(dgnn_ctx* c, void* dst_host, const void* src_dev, size_t n) {
+    if (!n) return DGNN_OK;
+    const size_t n4 = (n + 3) & ~(size_t)3;
+    DGNN_TRY(readback_reserve(c, n4));
+    if (n % 4 || (size_t)src_dev % 4) {  // (odd sizes: the copy engine)
+        DGNN_CK(cudaMemcpyAsync(c->rb, src_dev, n, cudaMemcpyDeviceToHost, c->stream));
+    } else {
+        DGNN_TRY(readback_enqueue(c, 0, src_dev, n));
+    }
     DGNN_CK(cudaStreamSynchronize(c->stream));
-    *flags = *c->pinned_err;
+    std::memcpy(dst_host, c->rb, n);
+    return DGNN_OK;
+}
+
+dgnn_status read_dev_err(dgnn_ctx* c, int* flags) {
+    DGNN_TRY(readback_reserve(c, 64));
+    DGNN_TRY(readback_enqueue(c, 0, c->dev_err, sizeof(int)));
+    DGNN_CK(cudaStreamSynchronize(c->stream));
+    *flags = *reinterpret_cast<volatile int*>(c->rb);
     if (*flags) DGNN_CK(cudaMemsetAsync(c->dev_err, 0, sizeof(int), c->stream));
     return DGNN_OK;
 }
@@ -245,6 +333,7 @@ void dgnn_ctx_destroy(dgnn_ctx* c) {
     if (c->scan_buf) cudaFree(c->scan_buf);
     if (c->pinned) cudaFreeHost(c->pinned);
     if (c->pinned_err) cudaFreeHost(c->pinned_err);
+    if (c->rb) cudaFreeHost(c->rb);
     if (c->side) cudaStreamDestroy(c->side);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
@@ -269,6 +358,12 @@ dgnn_status dgnn_ctx_sync(dgnn_ctx* c) {
     DGNN_CK(cudaSetDevice(c->device));
     DGNN_CK(cudaStreamSynchronize(c->side));
     return check_dev_err(c);
+}
+
+dgnn_status dgnn_upload(dgnn_ctx* c, void* dst_dev, const void* src_host, int64_t bytes) {
+    DGNN_REQUIRE(c && bytes >= 0 && (bytes == 0 || (dst_dev && src_host)), "dgnn_upload: bad argument");
+    DGNN_CK(cudaSetDevice(c->device));
+    return upload_small(c, dst_dev, src_host, (size_t)bytes);
 }
 
 dgnn_status dgnn_ctx_set_sample_group(dgnn_ctx* c, int32_t batches) {

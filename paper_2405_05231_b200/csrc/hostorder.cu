@@ -153,15 +153,14 @@ extern "C" dgnn_status dgnn_host_order(dgnn_ctx* c, const uint32_t* addr, const 
         DGNN_TRY(scan::run(c, k_host, nullptr, in, out, total.p));
     }
     int64_t ng = 0;
-    DGNN_CK(cudaMemcpyAsync(&ng, total.p, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
-    DGNN_CK(cudaStreamSynchronize(c->stream));
+    DGNN_TRY(read_small(c, &ng, total.p, sizeof(int64_t)));
     *n_groups = ng;
     if (ng > max_groups) {
         set_error("dgnn_host_order: %lld mask groups exceed max_groups %lld", (long long)ng, (long long)max_groups);
         return DGNN_ERANGE;
     }
-    DGNN_CK(cudaMemcpy(group_start_host, gstart.p, sizeof(int64_t) * (size_t)ng, cudaMemcpyDeviceToHost));
-    DGNN_CK(cudaMemcpy(group_mask_host, gmask.p, sizeof(uint32_t) * (size_t)ng, cudaMemcpyDeviceToHost));
+    DGNN_TRY(read_small(c, group_start_host, gstart.p, sizeof(int64_t) * (size_t)ng));
+    DGNN_TRY(read_small(c, group_mask_host, gmask.p, sizeof(uint32_t) * (size_t)ng));
     return DGNN_OK;
 }
 
@@ -247,9 +246,13 @@ extern "C" dgnn_status dgnn_remap_ids_dev(dgnn_ctx* c, int32_t* ids, const int64
 // point the items ending at or before w-2 are freed and the items starting at w are placed in
 // free staging rows (split over free fragments as needed: a copy is a range of physical rows).
 // capacity_rows >= max_w |S_{w-1}| + |S_w| always suffices (both windows' rows resident).
+// Spare capacity is then spent on bridging: two runs of a group separated by a gap of windows are
+// merged into one item (copied once, resident through the gap) when the arena has room for it in
+// every window of the gap -- shortest gaps first (a gap of one window costs no extra room at all);
+// with capacity_rows >= the rows the windows touch, every row crosses PCIe exactly once per pass.
 // Outputs per window (CSR over windows): the copies to issue at its prefetch, and the map of all
-// its rows (every resident item it needs), both as (phys_lo, phys_hi, stage_lo) triples, the map
-// sorted by phys_lo.
+// its rows (every resident item whose group it needs), both as (phys_lo, phys_hi, stage_lo) triples,
+// the map sorted by phys_lo.
 extern "C" dgnn_status dgnn_host_order_schedule(const int64_t* group_start_host, const uint32_t* group_mask_host,
                                                 int64_t n_groups, int64_t k_host, int32_t nwin, int64_t capacity_rows,
                                                 int64_t* copy_out, int64_t copy_cap, int64_t* copy_off,
@@ -260,13 +263,21 @@ extern "C" dgnn_status dgnn_host_order_schedule(const int64_t* group_start_host,
                  "dgnn_host_order_schedule: bad argument");
     struct Item {
         int64_t lo, hi;  // physical rows of the group
-        int a, b;        // first and last window of the run
+        int a, b;        // first and last window it stays resident for
+        uint32_t m;      // the group's mask (the windows that read it)
         std::vector<std::pair<int64_t, int64_t>> frag;  // (stage_lo, rows) pieces, in phys order
     };
-    std::vector<Item> items;
+    // runs of consecutive set bits per group; an item occupies the arena for windows [a, b + 1]
+    // (it is released when window b + 2 is prefetched)
+    struct Run {
+        int64_t g;
+        int a, b;
+    };
+    std::vector<Run> runs;
+    std::vector<int64_t> occ(nwin + 1, 0);
     for (int64_t g = 0; g < n_groups; ++g) {
         const uint32_t m = group_mask_host[g];
-        const int64_t lo = group_start_host[g], hi = g + 1 < n_groups ? group_start_host[g + 1] : k_host;
+        const int64_t rows = (g + 1 < n_groups ? group_start_host[g + 1] : k_host) - group_start_host[g];
         for (int w = 0; w < nwin;) {
             if (!((m >> w) & 1u)) {
                 ++w;
@@ -274,9 +285,39 @@ extern "C" dgnn_status dgnn_host_order_schedule(const int64_t* group_start_host,
             }
             int e = w;
             while (e + 1 < nwin && ((m >> (e + 1)) & 1u)) ++e;
-            items.push_back(Item{lo, hi, w, e, {}});
+            runs.push_back(Run{g, w, e});
+            for (int x = w; x <= std::min(e + 1, nwin - 1); ++x) occ[x] += rows;
             w = e + 1;
         }
+    }
+    // bridging: gap k lies between runs k and k + 1 of the same group; bridged[k] merges them
+    std::vector<char> bridged(runs.size(), 0);
+    {
+        std::vector<size_t> gaps;
+        for (size_t k = 0; k + 1 < runs.size(); ++k)
+            if (runs[k].g == runs[k + 1].g) gaps.push_back(k);
+        std::stable_sort(gaps.begin(), gaps.end(), [&](size_t x, size_t y) {
+            return runs[x + 1].a - runs[x].b < runs[y + 1].a - runs[y].b;
+        });
+        for (size_t k : gaps) {
+            const int64_t g = runs[k].g;
+            const int64_t rows = (g + 1 < n_groups ? group_start_host[g + 1] : k_host) - group_start_host[g];
+            const int w0 = runs[k].b + 2, w1 = runs[k + 1].a - 1;  // windows neither run occupies
+            bool fits = true;
+            for (int x = w0; x <= w1 && fits; ++x) fits = occ[x] + rows <= capacity_rows;
+            if (!fits) continue;
+            for (int x = w0; x <= w1; ++x) occ[x] += rows;
+            bridged[k] = 1;
+        }
+    }
+    std::vector<Item> items;
+    for (size_t k = 0; k < runs.size();) {
+        size_t e = k;
+        while (bridged[e]) ++e;  // (a bridged gap always has a next run of the same group)
+        const int64_t g = runs[k].g;
+        const int64_t lo = group_start_host[g], hi = g + 1 < n_groups ? group_start_host[g + 1] : k_host;
+        items.push_back(Item{lo, hi, runs[k].a, runs[e].b, group_mask_host[g], {}});
+        k = e + 1;
     }
     std::vector<std::pair<int64_t, int64_t>> freel{{0, capacity_rows}};  // [start, end) free staging rows
     int64_t nc = 0, nm = 0, copied = 0;
@@ -319,7 +360,7 @@ extern "C" dgnn_status dgnn_host_order_schedule(const int64_t* group_start_host,
         map_off[w] = nm;
         std::vector<std::array<int64_t, 3>> mp;
         for (auto& it : items) {
-            if (it.a > w || it.b < w) continue;
+            if (it.a > w || it.b < w || !((it.m >> w) & 1u)) continue;
             int64_t p = it.lo;
             for (auto& f : it.frag) {
                 mp.push_back({p, p + f.second, f.first});

@@ -53,6 +53,11 @@ struct dgnn_ctx {
     void* pinned = nullptr;
     size_t pinned_bytes = 0;
     int* pinned_err = nullptr;  // check_dev_err's read-back word
+    // small device -> host read-backs (sizes, flags) land here from SM stores over PCIe
+    // (readback_enqueue): a cudaMemcpy D2H would queue on a copy engine behind the gigabytes of
+    // stage-out / tier-fill copies another stream has in flight
+    void* rb = nullptr;
+    size_t rb_bytes = 0;
     // recycled device buffers (keep_take / keep_put): the sample arenas and the sampler's group
     // scratch of one call are handed to the next call on the same ctx instead of going back to
     // the allocator, so a steady stream of offline passes reaches a fixed HBM footprint
@@ -198,6 +203,21 @@ dgnn_status memset_async(dgnn_ctx* c, void* p, int value, size_t bytes);
 void* pinned_scratch(dgnn_ctx* c, size_t bytes);  // NULL on failure; valid until the next call
 dgnn_status check_dev_err(dgnn_ctx* c);  // synchronizes
 dgnn_status read_dev_err(dgnn_ctx* c, int* flags);  // synchronizes; clears the device word
+// Small device -> host read-backs by SM stores into the ctx's pinned read-back buffer (no copy
+// engine): readback_reserve(c, bytes) first (grow-only; nothing may be in flight), then any number
+// of readback_enqueue(c, off, src, n) on the ctx stream (off, n multiples of 4, src 4-byte
+// aligned), then cudaStreamSynchronize; the bytes are at readback_host(c) + off.
+// DGNN_SMALL_D2H=copy uses cudaMemcpyAsync into the same buffer instead (A/B measurement).
+dgnn_status readback_reserve(dgnn_ctx* c, size_t bytes);
+dgnn_status readback_enqueue(dgnn_ctx* c, size_t off, const void* src_dev, size_t n);
+inline uint8_t* readback_host(dgnn_ctx* c) { return static_cast<uint8_t*>(c->rb); }
+// the three together: n bytes of device memory into any host memory (synchronizes)
+dgnn_status read_small(dgnn_ctx* c, void* dst_host, const void* src_dev, size_t n);
+// Small host -> device uploads carried in kernel parameters (copied at launch: no copy engine, and
+// the host source may be reused as soon as the call returns); above kUploadMax bytes, or with
+// DGNN_SMALL_D2H=copy, an ordinary cudaMemcpyAsync on the ctx stream.
+constexpr size_t kUploadMax = (size_t)256 << 10;
+dgnn_status upload_small(dgnn_ctx* c, void* dst_dev, const void* src_host, size_t n);
 dgnn_status dev_err_status(int flags);               // DEVERR_* bits -> status + message
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

@@ -226,9 +226,7 @@ extern "C" dgnn_status dgnn_classify(dgnn_ctx* c, const dgnn_cache_plan* plan, c
         DGNN_TRY(memset_async(c, packed_off, 0, sizeof(int64_t) * (nbg + 1)));
     }
     if (packed_off_host) {
-        DGNN_CK(cudaMemcpyAsync(packed_off_host, packed_off, sizeof(int64_t) * (nbg + 1), cudaMemcpyDeviceToHost,
-                                c->stream));
-        DGNN_CK(cudaStreamSynchronize(c->stream));
+        DGNN_TRY(read_small(c, packed_off_host, packed_off, sizeof(int64_t) * (nbg + 1)));
     }
     return DGNN_OK;
 }
@@ -247,8 +245,7 @@ extern "C" dgnn_status dgnn_batch_tier_counts(dgnn_ctx* c, const dgnn_samples* S
             addr, S->node_off + b_lo, S->node_off_h[b_lo], (int)nbg, d.p);
     });
     DGNN_CK_LAUNCH();
-    DGNN_CK(cudaMemcpyAsync(counts_host, d.p, sizeof(int64_t) * 3 * nbg, cudaMemcpyDeviceToHost, c->stream));
-    DGNN_CK(cudaStreamSynchronize(c->stream));
+    DGNN_TRY(read_small(c, counts_host, d.p, sizeof(int64_t) * 3 * nbg));
     return DGNN_OK;
 }
 

@@ -1164,6 +1164,8 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
         DGNN_REQUIRE(fanout[h] >= 0 && fanout[h] <= 65535, "dgnn_sample: fanout[%d]=%d outside [0, 65535]", h,
                      fanout[h]);
     DGNN_CK(cudaSetDevice(c->device));
+    const auto t_entry = std::chrono::steady_clock::now();  // (DGNN_TRACE_SAMPLE only)
+    auto t_synced = t_entry;
     const int64_t N = csr->num_nodes;
     const int H = num_hops;
     const int64_t B = batch_size;
@@ -1194,6 +1196,7 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
         });
         DGNN_CK_LAUNCH();
         DGNN_TRY(check_dev_err(c));
+        t_synced = std::chrono::steady_clock::now();
 
         // ---- capacities (exact upper bounds; reading c26 for k = 0) ----
         const int64_t kCap = (int64_t)1 << 40;
@@ -1343,9 +1346,7 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
         {
             std::vector<int64_t*> ptrs(H);
             for (int h = 0; h < H; ++h) ptrs[h] = d_cptr[h];
-            DGNN_CK(cudaMemcpyAsync(d_cptr_list, ptrs.data(), sizeof(int64_t*) * H, cudaMemcpyHostToDevice,
-                                    c->stream));
-            DGNN_CK(cudaStreamSynchronize(c->stream));  // ptrs is a stack vector
+            DGNN_TRY(upload_small(c, d_cptr_list, ptrs.data(), sizeof(int64_t*) * H));
         }
         if (part) DGNN_CK(cudaFuncSetAttribute(k_part_dedup, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPartSmem));
         const int part_grid = part ? grid_resident(c, k_part_dedup, (int64_t)1 << 40, kPartThreads, 8, kPartSmem) : 0;
@@ -1378,17 +1379,22 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
         // host views of the per-group sizes and the compaction plan, in pinned memory
         const size_t n_frs = (size_t)H * (kMaxGroup + 1);
         const size_t plan_cap = 3 * (size_t)(G + 1) + (size_t)H * G;
-        const size_t pin_bytes = sizeof(int64_t) * (2 * n_frs + plan_cap) + sizeof(int32_t) * (G + G * (H + 2));
+        const size_t pin_bytes = sizeof(int64_t) * plan_cap;
         auto* pin = static_cast<uint8_t*>(pinned_scratch(c, pin_bytes));
         if (!pin) {
             set_error("pinned host allocation of %zu bytes failed", pin_bytes);
             return DGNN_ENOMEM;
         }
-        int64_t* h_frs = reinterpret_cast<int64_t*>(pin);
-        int64_t* h_cbs = h_frs + n_frs;
-        int64_t* h_plan = h_cbs + n_frs;
-        int32_t* h_n = reinterpret_cast<int32_t*>(h_plan + plan_cap);
-        int32_t* h_hb = h_n + G;
+        int64_t* h_plan = reinterpret_cast<int64_t*>(pin);  // (upload source)
+        // the group-end sizes come back through the read-back buffer (SM stores, no copy engine);
+        // its first 64 bytes are read_dev_err's
+        const size_t rb_frs = 64, rb_cbs = rb_frs + sizeof(int64_t) * n_frs, rb_n = rb_cbs + sizeof(int64_t) * n_frs,
+                     rb_hb = rb_n + sizeof(int32_t) * G, rb_end = rb_hb + sizeof(int32_t) * G * (H + 2);
+        DGNN_TRY(readback_reserve(c, rb_end));
+        int64_t* h_frs = reinterpret_cast<int64_t*>(readback_host(c) + rb_frs);
+        int64_t* h_cbs = reinterpret_cast<int64_t*>(readback_host(c) + rb_cbs);
+        int32_t* h_n = reinterpret_cast<int32_t*>(readback_host(c) + rb_n);
+        int32_t* h_hb = reinterpret_cast<int32_t*>(readback_host(c) + rb_hb);
 
         // DGNN_TRACE_SAMPLE=1: host-side split of the call (enqueue vs waiting in the group syncs)
         const bool trace = std::getenv("DGNN_TRACE_SAMPLE") != nullptr;
@@ -1556,13 +1562,10 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
                 DGNN_CK_LAUNCH();
             }
             // ---- group end: read sizes, then compact into the batch-major arena ----
-            DGNN_CK(cudaMemcpyAsync(h_n, g.n, sizeof(int32_t) * Gc, cudaMemcpyDeviceToHost, c->stream));
-            DGNN_CK(cudaMemcpyAsync(h_hb, g.hop_bound, sizeof(int32_t) * Gc * (H + 2), cudaMemcpyDeviceToHost,
-                                    c->stream));
-            DGNN_CK(cudaMemcpyAsync(h_frs, g.hop_fr_off, sizeof(int64_t) * H * (kMaxGroup + 1),
-                                    cudaMemcpyDeviceToHost, c->stream));
-            DGNN_CK(cudaMemcpyAsync(h_cbs, g.hop_cbase, sizeof(int64_t) * H * (kMaxGroup + 1),
-                                    cudaMemcpyDeviceToHost, c->stream));
+            DGNN_TRY(readback_enqueue(c, rb_n, g.n, sizeof(int32_t) * Gc));
+            DGNN_TRY(readback_enqueue(c, rb_hb, g.hop_bound, sizeof(int32_t) * Gc * (H + 2)));
+            DGNN_TRY(readback_enqueue(c, rb_frs, g.hop_fr_off, sizeof(int64_t) * n_frs));
+            DGNN_TRY(readback_enqueue(c, rb_cbs, g.hop_cbase, sizeof(int64_t) * n_frs));
             const auto tg1 = clk::now();
             int flags = 0;
             DGNN_TRY(read_dev_err(c, &flags));  // synchronizes
@@ -1627,8 +1630,7 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
                                      used_edges));
             DGNN_TRY(a_eptr.reserve(used_eptr + eptr_pre[Gc] > a_eptr.cap ? est(used_eptr, eptr_pre[Gc]) : 0,
                                     used_eptr));
-            DGNN_CK(cudaMemcpyAsync(d_plan, h_plan, sizeof(int64_t) * plan_n, cudaMemcpyHostToDevice,
-                                    c->stream));
+            DGNN_TRY(upload_small(c, d_plan, h_plan, sizeof(int64_t) * plan_n));
             CompactPlan p{};
             p.G = Gc;
             p.H = H;
@@ -1676,10 +1678,13 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
         if (trace) {
             const double tot = std::chrono::duration<double, std::milli>(clk::now() - t_start).count();
             t_post = tot - t_enq - t_wait;
-            fprintf(stderr, "[dgnn_sample] groups=%lld G=%lld total %.1f ms: enqueue %.1f, sync-wait %.1f, "
-                    "post-sync host+compaction enqueue %.1f; table 2^%d (bound 2^%d), %lld groups redone\n",
-                    (long long)((nb + G - 1) / G), (long long)G, tot, t_enq, t_wait, t_post, tlog_cur, tlog_safe,
-                    (long long)redone);
+            const double ms_sync0 = std::chrono::duration<double, std::milli>(t_synced - t_entry).count();
+            const double ms_setup = std::chrono::duration<double, std::milli>(t_start - t_synced).count();
+            fprintf(stderr, "[dgnn_sample] groups=%lld G=%lld first sync %.1f ms, setup %.1f ms, then total %.1f ms: "
+                    "enqueue %.1f, sync-wait %.1f, post-sync host+compaction enqueue %.1f; table 2^%d (bound 2^%d), "
+                    "%lld groups redone\n",
+                    (long long)((nb + G - 1) / G), (long long)G, ms_sync0, ms_setup, tot, t_enq, t_wait, t_post,
+                    tlog_cur, tlog_safe, (long long)redone);
         }
         S->cap_nodes = a_nodes.cap;
         S->nodes = a_nodes.release();
@@ -1700,15 +1705,10 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
         set_error("dgnn_sample: offset allocation failed");
         return DGNN_ENOMEM;
     }
-    DGNN_CK(cudaMemcpyAsync(S->node_off, S->node_off_h.data(), sizeof(int64_t) * (nb + 1), cudaMemcpyHostToDevice,
-                            c->stream));
-    DGNN_CK(cudaMemcpyAsync(S->edge_off, S->edge_off_h.data(), sizeof(int64_t) * (nb + 1), cudaMemcpyHostToDevice,
-                            c->stream));
-    DGNN_CK(cudaMemcpyAsync(S->eptr_off, S->eptr_off_h.data(), sizeof(int64_t) * (nb + 1), cudaMemcpyHostToDevice,
-                            c->stream));
-    if (nb)
-        DGNN_CK(cudaMemcpyAsync(S->hop_off, S->hop_off_h.data(), sizeof(int32_t) * nb * (H + 2),
-                                cudaMemcpyHostToDevice, c->stream));
+    DGNN_TRY(upload_small(c, S->node_off, S->node_off_h.data(), sizeof(int64_t) * (nb + 1)));
+    DGNN_TRY(upload_small(c, S->edge_off, S->edge_off_h.data(), sizeof(int64_t) * (nb + 1)));
+    DGNN_TRY(upload_small(c, S->eptr_off, S->eptr_off_h.data(), sizeof(int64_t) * (nb + 1)));
+    if (nb) DGNN_TRY(upload_small(c, S->hop_off, S->hop_off_h.data(), sizeof(int32_t) * nb * (H + 2)));
     if (counts && nb && S->total_nodes && range_count) {
         // a4, range-major over the epoch (see k_cnt_ranges); DGNN_SAMPLE_COUNT=group counted per group
         const int64_t P = (N + (1 << kCntBits) - 1) >> kCntBits;

@@ -59,6 +59,25 @@ class Workspace:
     def __init__(self):
         self._host = {}
         self._dev = {}
+        # buffer name -> (ctx, stage ticket) of the last side-stream copy reading it: the next pass
+        # that rewrites the buffer waits for exactly that copy (wait_reader / set_reader)
+        self._readers = {}
+
+    def wait_reader(self, ctx: A.Ctx, name: str):
+        """Make ``ctx``'s stream wait until the side-stream copies that last read buffer ``name``
+        are done."""
+        r = self._readers.get(name)
+        if r is None:
+            return
+        rctx, ticket = r
+        if rctx is ctx:
+            A.dgnn_stage_wait(ctx, ticket)
+        else:  # another ctx's side stream: wait for all of it
+            ctx.stream.wait_stream(torch.cuda.ExternalStream(rctx.side_stream_ptr, device=ctx.device))
+
+    def set_reader(self, ctx: A.Ctx, name: str, ticket):
+        if ticket is not None:
+            self._readers[name] = (ctx, ticket)
 
     def host(self, name: str, nbytes: int) -> "HostBuffer":
         b = self._host.get(name)
@@ -214,6 +233,9 @@ class Layout:
             gctx.stream.wait_event(self.host_w0_event)
         for ev in after:
             gctx.stream.wait_event(ev)
+        if os.environ.get("DGNN_ASM_TRACE") == "1":  # (measurement only) the copy's own start
+            self._early_start = torch.cuda.Event(enable_timing=True)
+            self._early_start.record(gctx.stream)
         A.dgnn_copy_ranges(gctx, arena, self.host_tier.ptr, ho.copies[0], self.row_bytes)
         ev = torch.cuda.Event()
         ev.record(gctx.stream)
@@ -298,11 +320,10 @@ class Layout:
                 dpre = np.concatenate([[0], np.cumsum(self.batch_tiers[b0:b1, 2])])
                 tabs.append(np.concatenate([no[b0:b1 + 1] - no[b0], dpre * self.row_bytes, dpre, chunk_off]))
             spans.append((int(no[b0]), int(no[b1]), c_lo, c_hi))
+        # kernel-parameter upload (dgnn_upload): the host never waits for the layout's stream, and
+        # the tables do not queue on a copy engine behind the window / stage copies in flight
+        flat = A.dgnn_upload(self.ctx, np.concatenate(tabs).astype(np.int64))
         with torch.cuda.stream(self.ctx.stream):
-            # pinned source + async copy: the host never waits for the layout's stream here
-            src = torch.from_numpy(np.concatenate(tabs).astype(np.int64)).pin_memory()
-            flat = src.to(self.ctx.device, non_blocking=True)
-            self._pinned_srcs.append(src)  # alive as long as the layout (the copy reads it later)
             ready = torch.cuda.Event()
             ready.record(self.ctx.stream)  # tiers, address tables and these tables are in place
         offs = np.concatenate([[0], np.cumsum([len(t) for t in tabs])])
@@ -664,6 +685,12 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
         stats["_events"].append((name, e))
         stats["_host"].append((name, _time.perf_counter()))
 
+    fine_marks = os.environ.get("DGNN_LAYOUT_TRACE") == "1"
+
+    def fine(name):  # (DGNN_LAYOUT_TRACE=1) finer marks inside the classify phase
+        if fine_marks:
+            mark(name)
+
     mark("start")
     if counts is None:
         counts = torch.zeros(N, dtype=torch.int32, device=dev)
@@ -708,8 +735,8 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
     total_nodes = samples.total_nodes
     addr = buf("addr", total_nodes, torch.int32)
     if scratch_ws is not None:
-        # the previous pass on this ctx may still be copying its group buffer out
-        ctx.stream.wait_stream(torch.cuda.ExternalStream(ctx.side_stream_ptr, device=dev))
+        # (the scratch buffers a side-stream copy of the previous pass still reads -- the host-fill
+        # staging and the pack group buffers -- are waited for right before they are rewritten)
         nbytes = max(int(total_nodes), 1) * 4
         packed_ids = scratch_ws.dev("packed_ids", nbytes, dev)[:nbytes].view(torch.int32)
     else:
@@ -717,6 +744,7 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
     packed_off = torch.empty(nb + 1, dtype=torch.int64, device=dev)
     po = A.dgnn_classify(ctx, plan, samples, 0, nb, addr, packed_ids, packed_off) if nb else np.zeros(1, np.int64)
     batch_tiers = A.dgnn_batch_tier_counts(ctx, samples, 0, nb, addr) if nb else np.zeros((0, 3), np.int64)
+    fine("c_classify")
     dplan = None
     if disk_budget_frac is not None and nb:
         disk_budget = int(disk_budget_frac * int(((np.diff(po) * row_bytes + 4095) // 4096).sum())) * 4096
@@ -770,6 +798,7 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
         disk = A.DiskFile(file_path, max(arena_off, 4096), direct=direct_io)
     else:
         raise ValueError(stage)
+    fine("c_arena")
     L = Layout(ctx, samples, plan, counts, row_bytes, dim, features.dtype, addr, gpu_tier, host_tier, arena,
                arena_dev, groups, batch_chunk, stats)
     L.batch_tiers = batch_tiers
@@ -797,17 +826,20 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
                     ho = A.HostOrder(ctx, addr, wo, plan.host_ids, plan.k_host)
                 except A.DgnnError:  # too many distinct window masks: keep the slot order
                     ho = None
+        fine("c_hostorder")
         if ho is not None:
             L.host_order, L.host_order_key = ho, (int(host_order), int(asm_out_budget))
             # window 0's rows first (one contiguous range of the physical order), then the rest: the
             # assembler may stage window 0 as soon as its part is filled (Layout.early_host_prefetch)
             kh, rb = plan.k_host, row_bytes
             first = ho.ranges[0].reshape(-1, 3)[:, :2] if len(ho.ranges[0]) else np.zeros((0, 2), np.int64)
-            done = np.zeros(kh + 1, np.int8)
-            for lo, hi in first:
-                done[int(lo):int(hi)] = 1
-            edges = np.flatnonzero(np.diff(np.concatenate([[1], done[:kh], [1]])))  # runs of unfilled rows
-            rest = list(zip(edges[0::2], edges[1::2]))
+            rest, cur = [], 0  # the complement of window 0's ranges in [0, kh): the runs of unfilled rows
+            for lo, hi in sorted((int(a), int(b)) for a, b in first):
+                if lo > cur:
+                    rest.append((cur, lo))
+                cur = max(cur, hi)
+            if cur < kh:
+                rest.append((cur, kh))
             fws = scratch_ws if scratch_ws is not None else ws
             if fws is not None and not isinstance(features, A.ShardedFeatures):
                 # through HBM: the rows gathered in physical order on the layout's stream (HBM-bound,
@@ -817,6 +849,7 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
                 # stream (the wait before classify)
                 with torch.cuda.stream(ctx.stream):
                     hbuf = fws.dev("host_fill", kh * rb, dev)[:kh * rb]
+                fws.wait_reader(ctx, "host_fill")  # the previous pass's fill copies read it
                 A.dgnn_gather_rows(ctx, features, ho.phys_ids[:kh], hbuf)
                 t = None
                 for lo, hi in first:
@@ -827,6 +860,7 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
                     t = A.dgnn_stage_copy(ctx, host_tier.ptr + int(lo) * rb, hbuf.data_ptr() + int(lo) * rb,
                                           (int(hi) - int(lo)) * rb, 0)
                 L.host_fill_ticket = t
+                fws.set_reader(ctx, "host_fill", t)
             else:  # SM stores into the pinned tier, window 0's range first
                 for lo, hi in first:
                     A.dgnn_gather_rows(ctx, features, ho.phys_ids[int(lo):int(hi)], host_tier.ptr + int(lo) * rb)
@@ -840,23 +874,21 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
                                    "rows_copied": ho.copy_rows, "arena_rows": ho.capacity}
         else:
             A.dgnn_gather_rows(ctx, features, plan.host_ids, host_tier.ptr)
+    fine("c_fill")
     if nb:
         L.assembly_plan(int(asm_out_budget))  # a9's per-run tables, uploaded here on the layout's stream
+    fine("c_asmplan")
     # a7's tables go up before the pack's wait (before_pack): an H2D copy queued between that wait
     # and the pack would sit behind whatever the copy engines are moving for the assembly then
-    with torch.cuda.stream(ctx.stream):
-        rel_all = torch.from_numpy(np.concatenate(
-            [np.concatenate([po[g.b_lo:g.b_hi + 1] - po[g.b_lo], g.chunk_off]) for g in groups]
-            or [np.zeros(0, np.int64)]).astype(np.int64)).pin_memory()
-        # async: a blocking copy would hold the host until this stream passes the wait for the
-        # previous pass's assembly (before_pack), delaying the enqueue of the next assembly
-        rel_src, rel_all = rel_all, rel_all.to(dev, non_blocking=True)
-        L._pinned_srcs.append(rel_src)
-        sec_dev = None
-        if embed_graph and nb:  # group-relative graph-section offsets of every batch
-            sec_src = torch.from_numpy(np.concatenate([g.sec_off for g in groups]).astype(np.int64)).pin_memory()
-            sec_dev = sec_src.to(dev, non_blocking=True)
-            L._pinned_srcs.append(sec_src)
+    # (kernel-parameter uploads, dgnn_upload: a blocking copy would hold the host until this stream
+    # passes the wait for the previous pass's assembly, and an async copy-engine copy would queue
+    # behind the window copies -- and the pack behind it)
+    rel_all = A.dgnn_upload(ctx, np.concatenate(
+        [np.concatenate([po[g.b_lo:g.b_hi + 1] - po[g.b_lo], g.chunk_off]) for g in groups]
+        or [np.zeros(0, np.int64)]).astype(np.int64))
+    sec_dev = None
+    if embed_graph and nb:  # group-relative graph-section offsets of every batch
+        sec_dev = A.dgnn_upload(ctx, np.concatenate([g.sec_off for g in groups]).astype(np.int64))
     mark("classify")
     if before_pack is not None:
         before_pack()
@@ -876,6 +908,8 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
         L.disk = disk
         L._bounce_w = ws.host("bounce_w", FILE_CHUNK) if ws is not None else HostBuffer(FILE_CHUNK)
     bufs = L._group_bufs
+    if bufs and gws is not None:
+        gws.wait_reader(ctx, "group_buf")  # the previous pass's stage-out copies read them
     group_last_ticket = []
     off = 0
     for gi, g in enumerate(groups):
@@ -918,6 +952,8 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
             A.dgnn_pack(ctx, features, ids, rel_po, rel_co, total, g.group_bytes, dst)
             if sec_dev is not None:
                 A.dgnn_pack_graph(ctx, samples, g.b_lo, k, sec_dev[g.b_lo:g.b_hi], dst)
+    if group_last_ticket and gws is not None:
+        gws.set_reader(ctx, "group_buf", group_last_ticket[-1])
     if dplan is not None:
         L._req_pages_host = dplan.req_pages.cpu().numpy() if disk is not None else None
     if dplan is not None and dplan.cache_pages:
