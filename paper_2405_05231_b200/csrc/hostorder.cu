@@ -18,6 +18,7 @@
 //   dgnn_copy_ranges        the copy-engine copies of a window's ranges (H2D)
 //   dgnn_remap_ids_dev      ids[i] = table[ids[i]] (slot -> physical row for the generic gather)
 #include <algorithm>
+#include <cstdlib>
 #include <array>
 #include <utility>
 #include <vector>
@@ -292,7 +293,8 @@ extern "C" dgnn_status dgnn_host_order_schedule(const int64_t* group_start_host,
     }
     // bridging: gap k lies between runs k and k + 1 of the same group; bridged[k] merges them
     std::vector<char> bridged(runs.size(), 0);
-    {
+    const char* nb_env = std::getenv("DGNN_HOST_BRIDGE");  // "0": no bridging (A/B measurement)
+    if (!(nb_env && nb_env[0] == '0')) {
         std::vector<size_t> gaps;
         for (size_t k = 0; k + 1 < runs.size(); ++k)
             if (runs[k].g == runs[k + 1].g) gaps.push_back(k);
