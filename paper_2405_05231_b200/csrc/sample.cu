@@ -472,12 +472,23 @@ __global__ void k_remap(Grp g, int32_t* __restrict__ cand, const int32_t* __rest
 // is redone on the hash-set path (adversarial ID distributions only).  Results are identical
 // by construction: the dedup is a set operation, new nodes are ordered by ID (reading c10), and
 // the remap is per candidate.
-constexpr int kPartThreads = 512;
-constexpr int kPartTableLog = 12;                       // 4096 slots: keys + locals + sort keys = 64 KB
+// (the DGNN_PART_* macros exist for A/B builds, tools/build_variant.sh)
+#ifndef DGNN_PART_THREADS
+#define DGNN_PART_THREADS 512
+#endif
+#ifndef DGNN_PART_TABLE_LOG
+#define DGNN_PART_TABLE_LOG 12
+#endif
+#ifndef DGNN_PART_TARGET
+#define DGNN_PART_TARGET 1024  // distinct IDs a bucket is sized to expect
+#endif
+constexpr int kPartThreads = DGNN_PART_THREADS;
+constexpr int kPartTableLog = DGNN_PART_TABLE_LOG;      // 4096 slots: keys + locals + sort keys = 64 KB
 constexpr int kPartTable = 1 << kPartTableLog;
 constexpr size_t kPartSmem = (size_t)kPartTable * 16;  // dynamic shared memory of k_part_dedup
-constexpr int kRankBits = 10;  // sub-ranges of a bucket's ID range in the counting order
-constexpr int kRankMax = 2048; // new IDs a bucket ranks by counting (above: bitonic sort)
+constexpr int kRankBits = kPartTableLog - 2;  // sub-ranges of a bucket's ID range in the counting order
+constexpr int kRankMax = kPartTable / 2;      // new IDs a bucket ranks by counting (above: bitonic sort)
+constexpr int kPartTarget = DGNN_PART_TARGET;
 static_assert((kPartTable - kRankMax) * 2 >= (1 << kRankBits) + 1 + kRankMax, "rank scratch in s_new");
 
 constexpr int kSeedSortMax = 4096;                      // batch_size limit of the partitioned path
@@ -1271,7 +1282,7 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
             int64_t est = after_bound[h];
             if (after_seen[h] > 0) est = std::min(est, after_seen[h] + after_seen[h] / 4);
             else if (c->sample_n_hint > 0) est = std::min(est, c->sample_n_hint + c->sample_n_hint / 4);
-            return std::min(pbits_max, std::max(0, ceil_log2((est + 1023) / 1024)));
+            return std::min(pbits_max, std::max(0, ceil_log2((est + kPartTarget - 1) / kPartTarget)));
         };
         const int64_t Pmax = (int64_t)1 << pbits_max;
 
