@@ -655,7 +655,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default=os.environ.get("DGNN_BENCH_CONFIG", "papers"))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-batches", type=int, default=32)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-mode", default="host-features", choices=["host-features", "copy-all"],
