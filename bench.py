@@ -1024,6 +1024,9 @@ def main():
         e1.record(R.sA)
         torch.cuda.synchronize()
         R.before_layout = None
+        if os.environ.get("DGNN_E2E_TRACE") == "1":  # (measurement only) the e2e passes' device timeline
+            for t in R.timeline_ms():
+                log(f"[e2e-trace] {t}")
         if host_feats:
             R.inp, R.pack_alone = saved_inp, True
         barrier(ws)
