@@ -477,10 +477,19 @@ class Layout:
                     gctx.stream.wait_event(early)
                 else:
                     A.dgnn_copy_ranges(gctx, staging[s], self.host_tier.ptr, ho.copies[w], self.row_bytes)
-                if wspan:  # and the window's chunks, once their stage-out pieces are in the arena
-                    self.wait_chunks(gctx.stream, groups[w1 - 1][1], waited_g)
+                if wspan:  # and the window's chunks: each stage-out piece of the span is copied in as
+                    # soon as that piece is in the arena (the round trip pipelines piece by piece)
                     lo, hi = wspan[w]
-                    A.dgnn_copy_ranges(gctx, wchunk[w % 2], self.arena.ptr, [lo, hi, 0], 1)
+                    for pi, (pb, pe, ticket) in enumerate(self.stage_pieces):
+                        plo = int(self.batch_chunk[pb, 0])
+                        phi = int(self.batch_chunk[pe, 0]) if pe < nb else int(self.stats["chunk_bytes"])
+                        a, z = max(lo, plo), min(hi, phi)
+                        if a >= z:
+                            continue
+                        if pi not in waited_g:
+                            A.dgnn_stage_wait_stream(self.ctx, ticket, gctx.stream)
+                            waited_g.add(pi)
+                        A.dgnn_copy_ranges(gctx, wchunk[w % 2], self.arena.ptr, [a, z, a - lo], 1)
                 if pcie_rows is not None:
                     with torch.cuda.stream(gctx.stream):
                         pcie_rows.add_(ho.copy_rows[w])
@@ -937,10 +946,13 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
                 A.dgnn_pack_graph(ctx, samples, g.b_lo, k, sec_dev[g.b_lo:g.b_hi], dst)
             # stage-out in pieces of <= stage_piece bytes on batch boundaries, so the assembler
             # can start on the first batches while the rest is still crossing PCIe
+            # (at least 8 pieces per group, >= 64 MB each: the assembly stages each window's chunks in
+            # piece by piece, so smaller groups need finer pieces to pipeline the round trip)
+            piece = stage_piece if stage_piece >= (1 << 40) else min(stage_piece, max(64 << 20, g.group_bytes // 8))
             b = g.b_lo
             while b < g.b_hi:
                 e = b + 1
-                while e < g.b_hi and g.chunk_off[e + 1 - g.b_lo] - g.chunk_off[b - g.b_lo] <= stage_piece:
+                while e < g.b_hi and g.chunk_off[e + 1 - g.b_lo] - g.chunk_off[b - g.b_lo] <= piece:
                     e += 1
                 lo, hi = int(g.chunk_off[b - g.b_lo]), int(g.chunk_off[e - g.b_lo])
                 t = A.dgnn_stage_copy(ctx, arena.ptr + g.arena_off + lo, dst.data_ptr() + lo, hi - lo, 0)
