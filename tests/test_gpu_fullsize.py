@@ -116,15 +116,90 @@ def _oracle_ref(papers):
         cfg = papers["cfg"]
         counts = np.zeros(cfg["num_nodes"], np.uint32)
         samples, want = [], set(SAMPLED)
+        S = papers["L"].samples
+        mismatched, all_nodes = [], []
         for t0 in range(0, 1172, 200):  # bounded host memory: stream the oracle's samples
+            t1 = min(1172, t0 + 200)
             part = oracle.sample(papers["indptr"], papers["indices"], papers["seeds"], cfg["batch_size"],
-                                 list(cfg["fanout"]), RNG_SEED, batches=range(t0, min(1172, t0 + 200)), threads=16)
+                                 list(cfg["fanout"]), RNG_SEED, batches=range(t0, t1), threads=16)
             oracle.count_frequencies(part, cfg["num_nodes"], counts)
             samples += [r for r in part if r.bid in want]
-            del part
+            # every batch of the part against the GPU's samples (one device read per array and part)
+            n0, e0, p0 = S.node_off_host[t0], S.edge_off_host[t0], S.eptr_off_host[t0]
+            g_nodes = S.nodes[n0:S.node_off_host[t1]].cpu().numpy()
+            g_src = S.src_local[e0:S.edge_off_host[t1]].cpu().numpy()
+            g_eptr = S.eptr[p0:S.eptr_off_host[t1]].cpu().numpy()
+            for r in part:
+                b = r.bid
+                ok = (np.array_equal(g_nodes[S.node_off_host[b] - n0:S.node_off_host[b + 1] - n0], r.nodes) and
+                      np.array_equal(g_src[S.edge_off_host[b] - e0:S.edge_off_host[b + 1] - e0], r.src_local) and
+                      np.array_equal(g_eptr[S.eptr_off_host[b] - p0:S.eptr_off_host[b + 1] - p0], r.eptr) and
+                      np.array_equal(S.hop_off_host[b], r.hop_off))
+                if not ok:
+                    mismatched.append(b)
+                all_nodes.append(r.nodes)
+            del part, g_nodes, g_src, g_eptr
         tm, gpu_ids, host_ids = oracle.select_tiers(counts, papers["gpu_rows"], papers["host_rows"])
-        papers["ref"] = dict(samples=samples, counts=counts, tier_map=tm, gpu_ids=gpu_ids, host_ids=host_ids)
+        papers["ref"] = dict(samples=samples, counts=counts, tier_map=tm, gpu_ids=gpu_ids, host_ids=host_ids,
+                             mismatched=mismatched, all_nodes=all_nodes)
     return papers["ref"]
+
+
+def test_every_batch_sample_bit_exact(papers):
+    """All 1172 batches' samples (nodes, hop offsets, eptr, src_local) equal the oracle's, checked
+    while the oracle streams the epoch for the counts."""
+    ref = _oracle_ref(papers)
+    assert len(ref["all_nodes"]) == 1172
+    assert ref["mismatched"] == []
+
+
+def test_every_batch_address_table_bit_exact(papers):
+    """The address tables of all 1172 batches (503.6 M entries) equal the oracle's classify under
+    the oracle's own tier map."""
+    ref = _oracle_ref(papers)
+    L = papers["L"]
+    S = L.samples
+    got = L.addr[:S.total_nodes].cpu().numpy().view(np.uint32)
+    bad = []
+    for b, nodes in enumerate(ref["all_nodes"]):
+        addr, _ = oracle.classify(nodes, ref["tier_map"])
+        if not np.array_equal(got[S.node_off_host[b]:S.node_off_host[b + 1]], addr):
+            bad.append(b)
+    assert bad == []
+
+
+def test_every_batch_chunk_and_assembly(papers):
+    """All 1172 batches: the packed chunk holds the source rows of the oracle's packed list P_b
+    (7.66 M rows) followed by a zero tail, and every assembled batch equals the source rows of
+    its nodes (503.6 M rows) -- the source rows by the generator's closed form, evaluated on the
+    GPU batch by batch (the table itself was released after the layout)."""
+    from workload import feature_rows
+    ref = _oracle_ref(papers)
+    L, cfg = papers["L"], papers["cfg"]
+    dim, rb = cfg["dim"], cfg["dim"] * 4
+    S = L.samples
+    dev = torch.device("cuda", 0)
+    arena = L.arena.tensor
+    bad_chunks = []
+    for b, nodes in enumerate(ref["all_nodes"]):
+        _, P = oracle.classify(nodes, ref["tier_map"])
+        off, rows = (int(x) for x in L.batch_chunk[b])
+        end = int(L.batch_chunk[b + 1, 0]) if b + 1 < S.num_batches else int(L.stats["arena_bytes"])
+        got = arena[off:end].to(dev)
+        exp = feature_rows(torch.from_numpy(P.astype(np.int64)).to(dev), dim, 1)
+        if rows != len(P) or not torch.equal(got[:rows * rb].view(torch.int32), exp.reshape(-1).view(torch.int32)) \
+                or bool(got[rows * rb:].any()):
+            bad_chunks.append(b)
+    assert bad_chunks == []
+    bad_out, seen = [], 0
+    for b, out in L.assemble_epoch():
+        n0, n1 = int(S.node_off_host[b]), int(S.node_off_host[b + 1])
+        exp = feature_rows(S.nodes[n0:n1].to(torch.int64), dim, 1)
+        if not torch.equal(out.reshape(-1).view(torch.int32), exp.reshape(-1).view(torch.int32)):
+            bad_out.append(b)
+        seen += 1
+    papers["ctx"].sync()
+    assert seen == 1172 and bad_out == []
 
 
 def test_epoch_counts_and_tier_plan_bit_exact(papers):
