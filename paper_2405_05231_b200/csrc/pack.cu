@@ -103,23 +103,37 @@ __global__ void __launch_bounds__(256) k_gather(Src src, int64_t row_bytes, cons
 
 bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
-__global__ void k_classify_min(const uint32_t* __restrict__ addr, int64_t n, const int64_t* __restrict__ seg,
-                               int nseg, int64_t n0, int64_t* __restrict__ packed_off) {
-    __shared__ int64_t s_seg[kMaxSmemSeg + 1];
-    const bool in_smem = nseg <= kMaxSmemSeg;
-    if (in_smem)
-        for (int i = threadIdx.x; i <= nseg; i += blockDim.x) s_seg[i] = seg[i];
-    __syncthreads();
-    const int64_t* sg = in_smem ? s_seg : seg;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t a = addr[i];
-        if ((a >> DGNN_TIER_SHIFT) == DGNN_TIER_DISK) {
-            const int b = segment_of(sg, nseg + 1, n0 + i);
-            // only the batch's first DISK node can hold the minimum: skip the atomic otherwise
-            if (i == 0 || n0 + i == sg[b] || (addr[i - 1] >> DGNN_TIER_SHIFT) != DGNN_TIER_DISK ||
-                ((addr[i - 1] & DGNN_SLOT_MASK) + 1 != (a & DGNN_SLOT_MASK)))
-                atomicMin((unsigned long long*)&packed_off[b], (unsigned long long)(a & DGNN_SLOT_MASK));
+// a6's second pass, one CTA per batch (grid-stride over batches): the batch's first DISK node
+// holds its smallest packed index (DISK slots are the scan's running count, ascending in node
+// order), so packed_off[b] = the minimum DISK slot of the batch (block-wide min; batches without
+// DISK nodes keep the memset's sentinel for k_classify_fill), then the batch's DISK addresses are
+// made relative to it.  Two coalesced passes over the batch's addresses, no per-node batch search
+// and no atomics across batches.
+__global__ void k_classify_batches(uint32_t* __restrict__ addr, const int64_t* __restrict__ seg, int nseg,
+                                   int64_t n0, int64_t* __restrict__ packed_off) {
+    __shared__ unsigned long long s_min;
+    for (int b = blockIdx.x; b < nseg; b += gridDim.x) {
+        if (threadIdx.x == 0) s_min = ~0ull;
+        __syncthreads();
+        const int64_t lo = seg[b] - n0, hi = seg[b + 1] - n0;
+        unsigned long long m = ~0ull;
+        for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+            const uint32_t a = addr[i];
+            if ((a >> DGNN_TIER_SHIFT) == DGNN_TIER_DISK) m = min(m, (unsigned long long)(a & DGNN_SLOT_MASK));
         }
+        for (int d = 16; d; d >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, d));
+        if ((threadIdx.x & 31) == 0 && m != ~0ull) atomicMin(&s_min, m);
+        __syncthreads();
+        const unsigned long long first = s_min;
+        if (first != ~0ull) {
+            if (threadIdx.x == 0) packed_off[b] = (int64_t)first;
+            const uint32_t f = (uint32_t)first;
+            for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+                const uint32_t a = addr[i];
+                if ((a >> DGNN_TIER_SHIFT) == DGNN_TIER_DISK) addr[i] = a - f;
+            }
+        }
+        __syncthreads();
     }
 }
 
@@ -151,28 +165,6 @@ __global__ void k_classify_fill(int64_t* packed_off, int nseg) {
     if (threadIdx.x != 0) return;
     for (int b = nseg - 1; b >= 0; --b)
         if (packed_off[b] > packed_off[b + 1]) packed_off[b] = packed_off[b + 1];
-}
-
-__global__ void k_classify_fix(uint32_t* __restrict__ addr, int64_t n, const int64_t* __restrict__ seg, int nseg,
-                               int64_t n0, const int64_t* __restrict__ packed_off) {
-    __shared__ int64_t s_seg[kMaxSmemSeg + 1];
-    __shared__ int64_t s_po[kMaxSmemSeg + 1];
-    const bool in_smem = nseg <= kMaxSmemSeg;
-    if (in_smem)
-        for (int i = threadIdx.x; i <= nseg; i += blockDim.x) {
-            s_seg[i] = seg[i];
-            s_po[i] = packed_off[i];
-        }
-    __syncthreads();
-    const int64_t* sg = in_smem ? s_seg : seg;
-    const int64_t* po = in_smem ? s_po : packed_off;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t a = addr[i];
-        if ((a >> DGNN_TIER_SHIFT) == DGNN_TIER_DISK) {
-            const int b = segment_of(sg, nseg + 1, n0 + i);
-            addr[i] = a - (uint32_t)po[b];
-        }
-    }
 }
 
 }  // namespace
@@ -213,13 +205,10 @@ extern "C" dgnn_status dgnn_classify(dgnn_ctx* c, const dgnn_cache_plan* plan, c
         // pass 2: packed_off[b] = the smallest global packed index of batch b (batches
         // without DISK nodes take their successor's), then DISK slots relative to the batch
         DGNN_TRY(memset_async(c, packed_off, 0x7F, sizeof(int64_t) * nbg));
-        launch(c, DGNN_K_CLASSIFY, 4.0 * n, [&] {
-            k_classify_min<<<grid_for(c, n, 256), 256, 0, c->stream>>>(addr, n, seg, nseg, n0, packed_off);
+        launch(c, DGNN_K_CLASSIFY, 12.0 * n, [&] {
+            k_classify_batches<<<(int)std::min<int64_t>(nbg, (int64_t)c->num_sms * 8), 256, 0, c->stream>>>(
+                addr, seg, nseg, n0, packed_off);
             k_classify_fill<<<1, 32, 0, c->stream>>>(packed_off, nseg);
-        });
-        DGNN_CK_LAUNCH();
-        launch(c, DGNN_K_CLASSIFY, 8.0 * n, [&] {
-            k_classify_fix<<<grid_for(c, n, 256), 256, 0, c->stream>>>(addr, n, seg, nseg, n0, packed_off);
         });
         DGNN_CK_LAUNCH();
     } else {
