@@ -349,6 +349,9 @@ class Runner:
         self.stage = "pinned"  # the disk tier: pinned host arena, or "file" (O_DIRECT on local storage)
         self.disk_dir = os.environ.get("DGNN_DISK_DIR", tempfile.gettempdir())
         self.embed_graph = False  # graph samples kept in the chunks, loaded back for training
+        # the host tier's rows read from a host-resident feature table instead of a copy of their own
+        # (the e2e leg with --e2e-mode host-features)
+        self.host_from_table = False
         # window-ordered host tier: each host-row window is a few contiguous ranges for the copy engine
         self.host_order = os.environ.get("DGNN_HOST_ORDER", "1") == "1"
         # output bytes per assembly run (one launch): fewer, larger runs are fewer host-side calls
@@ -437,7 +440,7 @@ class Runner:
                                       scratch_ws=self.scratch_ws, before_pack=before_pack, gpu_shard=gpu_shard,
                                       stage=self.stage, embed_graph=self.embed_graph,
                                       host_order=self.host_window if self.host_order else None,
-                                      asm_out_budget=self.out_budget,
+                                      asm_out_budget=self.out_budget, host_from_table=self.host_from_table,
                                       file_path=os.path.join(self.disk_dir, f"dgnn_disk_r{self.rank}_s{slot}.bin"))
         L._slot = slot
         return L
@@ -1005,6 +1008,7 @@ def main():
             saved_inp = R.inp
             R.inp = (cfg, indptr, indices, seeds, inp_host[3], gpu_rows, host_rows)
             R.pack_alone = False  # the pack now reads over PCIe: nothing to gain from running alone
+            R.host_from_table = os.environ.get("DGNN_E2E_HOST_TABLE", "1") == "1"
         else:
             h2d = sum(t.numel() * t.element_size() for t in inp_host)
             dev_inputs = (indptr, indices, seeds, feats)
@@ -1013,6 +1017,7 @@ def main():
             # every pass: inputs H2D from pinned host (stream A, before the pass's layout) ...
             for h, d_ in zip(inp_host, dev_inputs):
                 d_.copy_(h, non_blocking=True)
+
 
         R.before_layout = copy_in
         barrier(ws)
@@ -1028,7 +1033,7 @@ def main():
             for t in R.timeline_ms():
                 log(f"[e2e-trace] {t}")
         if host_feats:
-            R.inp, R.pack_alone = saved_inp, True
+            R.inp, R.pack_alone, R.host_from_table = saved_inp, True, False
         barrier(ws)
         ms_e2e = max_over_ranks(e0.elapsed_time(e1), ws)
         result["e2e"] = {"value": round(nb_all * args.e2e_steps / (ms_e2e / 1e3), 2), "unit": "mini-batches/s",

@@ -430,6 +430,19 @@ dgnn_status dgnn_host_order_schedule(const int64_t* group_start_host, const uint
 dgnn_status dgnn_host_window_ranges(dgnn_ctx* ctx, const uint32_t* slot_mask, const int32_t* phys_of_slot,
                                     int64_t k_host, int32_t window, const int64_t* ranges_dev, int64_t nr,
                                     int32_t* smap);
+/* The host tier read from the feature table itself (a host-resident table, bench.py's e2e mode):
+ * instead of copying a window's physical host-tier ranges (dgnn_copy_ranges), gather, for every
+ * triple t of ranges_dev (phys_lo, phys_hi, staging_lo; prefix_dev[nr+1] = rows before each
+ * triple, prefix_dev[nr] = total_rows), the table rows of the nodes at physical rows [phys_lo,
+ * phys_hi) -- ids = the host order's phys_ids (physical row -> node id, device) -- into dst_dev rows
+ * [staging_lo, ...).  table: device or pinned host (UVA) [num_nodes, row_bytes]; row_bytes % 4 == 0.
+ * The staging arena then holds exactly what dgnn_copy_ranges would have put there (the tier's
+ * rows are the table's rows of its nodes).  Enqueued on the ctx stream.
+ * Errors: DGNN_EINVAL. */
+dgnn_status dgnn_gather_ranges(dgnn_ctx* ctx, const void* table, int64_t row_bytes, const int32_t* ids,
+                               const int64_t* ranges_dev, const int64_t* prefix_dev, int64_t nr,
+                               int64_t total_rows, void* dst_dev);
+
 /* Small host -> device table upload (the per-run assembly tables, the pack's offset tables; a
  * scheduling primitive, no arithmetic of the method): `bytes` of src_host (any host memory, read
  * before the call returns) to dst_dev (device, caller-owned), enqueued on the ctx stream as kernels

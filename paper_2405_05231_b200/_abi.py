@@ -51,6 +51,7 @@ EXPORTS = [
     "dgnn_chunk_layout_graph", "dgnn_pack_graph", "dgnn_samples_load", "dgnn_samples_drop_device",
     "dgnn_host_order", "dgnn_host_order_ranges", "dgnn_host_window_ranges", "dgnn_copy_ranges", "dgnn_remap_ids_dev",
     "dgnn_pack_sharded", "dgnn_gather_rows_sharded", "dgnn_host_order_schedule", "dgnn_upload",
+    "dgnn_gather_ranges",
 ]
 
 
@@ -149,6 +150,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "dgnn_host_window_ranges": (i32, [P, P, P, i64, i32, P, i64, P]),
             "dgnn_copy_ranges": (i32, [P, P, P, P, i64, i64]),
             "dgnn_upload": (i32, [P, P, P, i64]),
+            "dgnn_gather_ranges": (i32, [P, P, i64, P, P, P, i64, i64, P]),
             "dgnn_remap_ids_dev": (i32, [P, P, P, i64, P]),
             "dgnn_host_order_schedule": (i32, [P, P, i64, i64, i32, i64, P, i64, P, P, i64, P,
                                                 ctypes.POINTER(i64)]),
@@ -217,6 +219,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
 # entry points that only enqueue work on streams (no synchronization, no host waits); see load_library
 _ENQUEUE_ONLY = frozenset([
     "dgnn_assemble_group", "dgnn_assemble_group_peer", "dgnn_assemble_group_sharded", "dgnn_copy_ranges", "dgnn_upload",
+    "dgnn_gather_ranges",
     "dgnn_host_window_ranges", "dgnn_host_window", "dgnn_remap_ids_dev", "dgnn_stage_wait",
     "dgnn_stage_wait_stream", "dgnn_stage_copy", "dgnn_gather_rows", "dgnn_gather_rows_dev", "dgnn_pack",
     "dgnn_ctx_launches", "dgnn_ctx_stream", "dgnn_ctx_side_stream", "dgnn_last_error", "dgnn_kernel_name",
@@ -558,6 +561,13 @@ def dgnn_upload(ctx: Ctx, src, dtype=torch.int64) -> torch.Tensor:
     return out
 
 
+def dgnn_gather_ranges(ctx: Ctx, table, row_bytes: int, ids: torch.Tensor, ranges_dev: torch.Tensor,
+                       prefix_dev: torch.Tensor, nr: int, total_rows: int, dst):
+    _check(load_library().dgnn_gather_ranges(ctx.handle, _ptr(table), int(row_bytes), _ptr(ids), _ptr(ranges_dev),
+                                             _ptr(prefix_dev), int(nr), int(total_rows), _ptr(dst)),
+           "dgnn_gather_ranges")
+
+
 class HostOrder:
     """The window-ordered host tier of one layout (dgnn_host_order): device slot_mask / phys_of_slot
     / phys_ids, and per window its physical ranges (host triples + device copy)."""
@@ -603,6 +613,7 @@ class HostOrder:
                                                        P(moff.ctypes.data), ctypes.byref(copied)),
                "dgnn_host_order_schedule")
         self.rows_copied = int(copied.value)
+        self._copies_dev = None
         self.copies = [co[3 * coff[w]:3 * coff[w + 1]].copy() for w in range(self.nwin)]
         self.copy_rows = [int((c[1::3] - c[0::3]).sum()) for c in self.copies]
         maps = [mo[3 * moff[w]:3 * moff[w + 1]].copy() for w in range(self.nwin)]
@@ -612,6 +623,25 @@ class HostOrder:
         offs = np.concatenate([[0], np.cumsum([len(r) for r in self.ranges + maps])])
         self.ranges_dev = [flat[int(offs[w]):int(offs[w + 1])] for w in range(self.nwin)]
         self.map_dev = [flat[int(offs[self.nwin + w]):int(offs[self.nwin + w + 1])] for w in range(self.nwin)]
+
+    def copies_dev(self, ctx: Ctx):
+        """Per window: (triples_dev, prefix_dev, n_triples, rows) of its scheduled copy list, for
+        dgnn_gather_ranges (the tier read from the feature table); uploaded once, on ctx's stream."""
+        import numpy as np
+        if self._copies_dev is None:
+            parts, meta = [], []
+            for c in self.copies:
+                c = np.ascontiguousarray(c, dtype=np.int64)
+                pre = np.concatenate([[0], np.cumsum(c[1::3] - c[0::3])]).astype(np.int64)
+                meta.append((len(c), len(pre), len(c) // 3, int(pre[-1])))
+                parts += [c, pre]
+            flat = dgnn_upload(ctx, np.concatenate(parts + [np.zeros(1, np.int64)]))
+            out, o = [], 0
+            for nc, npre, nr, rows in meta:
+                out.append((flat[o:o + nc], flat[o + nc:o + nc + npre], nr, rows))
+                o += nc + npre
+            self._copies_dev = out
+        return self._copies_dev
 
 
 def dgnn_host_window_ranges(ctx: Ctx, ho: HostOrder, window: int, smap: torch.Tensor, scheduled: bool = True):

@@ -24,9 +24,42 @@
 #include <vector>
 
 #include "internal.cuh"
+#include "rowcopy.cuh"
 
 namespace dgnn {
 namespace {
+
+// (host tier read from the feature table itself) one row per staging row of a window's copies:
+// row r of the copy list lies in triple t (prefix[t] <= r < prefix[t+1]); its source is the table
+// row of the node at physical row lo_t + k, its destination staging row st_t + k
+struct RangeRow {
+    const uint8_t* table;
+    int64_t row_bytes;
+    const int32_t* ids;     // physical row -> node id
+    const int64_t* tri;     // (phys_lo, phys_hi, staging_lo) triples
+    const int64_t* prefix;  // [nr + 1] rows before each triple
+    int64_t nr;
+    uint8_t* dst;
+    __device__ __forceinline__ bool operator()(int64_t r, const uint8_t*& s, uint8_t*& d) const {
+        int64_t lo = 0, hi = nr;
+        while (hi - lo > 1) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (prefix[mid] <= r) lo = mid;
+            else hi = mid;
+        }
+        const int64_t k = r - prefix[lo];
+        s = table + (int64_t)ids[tri[3 * lo] + k] * row_bytes;
+        d = dst + (tri[3 * lo + 2] + k) * row_bytes;
+        return true;
+    }
+};
+
+template <class V>
+__global__ void __launch_bounds__(256) k_gather_ranges(RangeRow f, int64_t R) {
+    const int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    copy_rows_warp<8, V>(R, f.row_bytes, f, warp, nwarps);
+}
 
 __global__ void k_host_masks(const uint32_t* __restrict__ addr, int64_t n, uint32_t bit, int64_t kh,
                              uint32_t* __restrict__ mask) {
@@ -224,6 +257,28 @@ extern "C" dgnn_status dgnn_copy_ranges(dgnn_ctx* c, void* dst_dev, const void* 
         DGNN_CK(cudaMemcpyAsync((uint8_t*)dst_dev + st * row_bytes, (const uint8_t*)src_host + lo * row_bytes,
                                 (size_t)((hi - lo) * row_bytes), cudaMemcpyHostToDevice, c->stream));
     }
+    return DGNN_OK;
+}
+
+extern "C" dgnn_status dgnn_gather_ranges(dgnn_ctx* c, const void* table, int64_t row_bytes, const int32_t* ids,
+                                          const int64_t* ranges_dev, const int64_t* prefix_dev, int64_t nr,
+                                          int64_t total_rows, void* dst_dev) {
+    DGNN_REQUIRE(c && row_bytes > 0 && row_bytes % 4 == 0 && nr >= 0 && total_rows >= 0 &&
+                     (total_rows == 0 || (table && ids && ranges_dev && prefix_dev && dst_dev && nr > 0)),
+                 "dgnn_gather_ranges: bad argument");
+    if (total_rows == 0) return DGNN_OK;
+    DGNN_CK(cudaSetDevice(c->device));
+    const RangeRow f{static_cast<const uint8_t*>(table), row_bytes, ids, ranges_dev, prefix_dev, nr,
+                     static_cast<uint8_t*>(dst_dev)};
+    const bool v16 = row_bytes % 16 == 0 && ((uintptr_t)table & 15) == 0 && ((uintptr_t)dst_dev & 15) == 0;
+    const int grid = v16 ? grid_resident(c, k_gather_ranges<uint4>, total_rows * 32 / 8, 256, c->assemble_blocks_per_sm)
+                         : grid_resident(c, k_gather_ranges<uint32_t>, total_rows * 32 / 8, 256,
+                                         c->assemble_blocks_per_sm);
+    launch(c, DGNN_K_HOST_GATHER, (double)total_rows * row_bytes, [&] {
+        if (v16) k_gather_ranges<uint4><<<grid, 256, 0, c->stream>>>(f, total_rows);
+        else k_gather_ranges<uint32_t><<<grid, 256, 0, c->stream>>>(f, total_rows);
+    });
+    DGNN_CK_LAUNCH();
     return DGNN_OK;
 }
 

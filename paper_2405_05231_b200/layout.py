@@ -132,7 +132,7 @@ class Layout:
     dtype: torch.dtype
     addr: torch.Tensor              # uint32 (as int32) address table of every node of every batch
     gpu_tier: torch.Tensor          # [K_g, row_bytes] uint8, HBM
-    host_tier: HostBuffer           # [K_h * row_bytes] pinned
+    host_tier: HostBuffer           # [K_h * row_bytes] pinned (None when read from the table itself)
     arena: HostBuffer | None        # disk tier (pinned), or None when kept in HBM
     arena_dev: torch.Tensor | None  # disk tier kept in HBM (stage="hbm")
     groups: list = field(default_factory=list)
@@ -149,6 +149,7 @@ class Layout:
     host_order: A.HostOrder | None = None  # window-ordered host tier (physical rows permuted)
     host_order_key: tuple = None    # (host_window, out_budget) the ordering was built for
     host_w0_event: object = None    # the layout stream's event once window 0's host rows are filled
+    host_table: object = None       # (host_from_table) the host-resident feature table the tier's rows are read from
     host_w0_ticket: int = None      # (fill through HBM) the side-stream ticket of window 0's rows
     host_fill_ticket: int = None    # (fill through HBM) the ticket after which the whole tier is filled
 
@@ -182,6 +183,9 @@ class Layout:
         """Assemble batch b into ``out`` ([n_b, dim]) reading the chunk from ``chunk_dev`` if given
         (already staged to HBM), else directly from the arena (UVA over PCIe).  With a disk cache
         the batch's partial input (chunk rows + its cache pages) is built first."""
+        if self.host_tier is None:
+            raise ValueError("the host tier is read from the feature table (host_from_table): assemble through "
+                             "assemble_epoch with the layout's host windows")
         n0, n1 = int(self.samples.node_off_host[b]), int(self.samples.node_off_host[b + 1])
         off, rows = int(self.batch_chunk[b, 0]), int(self.batch_chunk[b, 1])
         if chunk_dev is not None:
@@ -236,10 +240,20 @@ class Layout:
         if os.environ.get("DGNN_ASM_TRACE") == "1":  # (measurement only) the copy's own start
             self._early_start = torch.cuda.Event(enable_timing=True)
             self._early_start.record(gctx.stream)
-        A.dgnn_copy_ranges(gctx, arena, self.host_tier.ptr, ho.copies[0], self.row_bytes)
+        self._stage_window(gctx, arena, 0)
         ev = torch.cuda.Event()
         ev.record(gctx.stream)
         return ev
+
+    def _stage_window(self, gctx: A.Ctx, dst, w: int):
+        """Window w's scheduled host rows into the staging arena ``dst``: the copy engine's ranges of the
+        pinned tier, or (host_from_table) the same rows gathered from the host-resident table."""
+        ho = self.host_order
+        if self.host_table is None:
+            A.dgnn_copy_ranges(gctx, dst, self.host_tier.ptr, ho.copies[w], self.row_bytes)
+            return
+        tri, pre, nr, rows = ho.copies_dev(self.ctx)[w]
+        A.dgnn_gather_ranges(gctx, self.host_table, self.row_bytes, ho.phys_ids, tri, pre, nr, rows, dst)
 
     def host_windows(self, host_window: int, out_budget: int = 1 << 30):
         """The assembler's host-row windows: (first run, last run + 1) over assembly_groups(out_budget),
@@ -392,6 +406,9 @@ class Layout:
         windows = self.host_windows(host_window, out_budget)[1]  # (first run, last run + 1)
         ho = self.host_order
         ordered = ho is not None and bool(windows) and self.host_order_key == (host_window, int(out_budget))
+        if self.host_tier is None and not ordered and kh > 0:
+            raise ValueError("the host tier is read from the feature table (host_from_table): assemble with the "
+                             "layout's host windows (host_window and out_budget of offline_layout's host_order)")
         def buf(name, n, dtype=torch.uint8, shape=None):
             """n elements of dtype, from the workspace when there is one (grow-only, >= 16 bytes)."""
             esz = torch.empty(0, dtype=dtype).element_size()
@@ -476,7 +493,7 @@ class Layout:
                 if w == 0 and early is not None:  # (staged ahead: early_host_prefetch)
                     gctx.stream.wait_event(early)
                 else:
-                    A.dgnn_copy_ranges(gctx, staging[s], self.host_tier.ptr, ho.copies[w], self.row_bytes)
+                    self._stage_window(gctx, staging[s], w)
                 if wspan:  # and the window's chunks: each stage-out piece of the span is copied in as
                     # soon as that piece is in the arena (the round trip pipelines piece by piece)
                     lo, hi = wspan[w]
@@ -644,7 +661,7 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
                    disk_k: int = 4, disk_budget_frac: float | None = None, after_sample=None,
                    scratch_ws: Workspace | None = None, before_pack=None, gpu_shard=None,
                    embed_graph: bool = False, host_order: int | None = None,
-                   asm_out_budget: int = 1 << 30) -> Layout:
+                   asm_out_budget: int = 1 << 30, host_from_table: bool = False) -> Layout:
     """Run a1-a8 on this rank's batches.
 
     ``seeds`` are this rank's seeds (batch t of them gets bid = batch_id_base + t).
@@ -734,8 +751,12 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
         gpu_tier = shard_buf[:ids.numel()]
         if ids.numel():
             A.dgnn_gather_rows(ctx, features, ids, gpu_tier)
-    host_tier = ws.host("host_tier", plan.k_host * row_bytes) if ws is not None else \
-        HostBuffer(plan.k_host * row_bytes)
+    # host_from_table: the feature table is host-resident (pinned), so the tier's rows need no copy of
+    # their own -- the assembler's window staging gathers them from the table (dgnn_gather_ranges)
+    table_host = bool(host_from_table and host_order and plan.k_host > 0 and
+                      not isinstance(features, A.ShardedFeatures) and not features.is_cuda)
+    host_tier = None if table_host else (ws.host("host_tier", plan.k_host * row_bytes) if ws is not None else
+                                         HostBuffer(plan.k_host * row_bytes))
     if not host_order:
         A.dgnn_gather_rows(ctx, features, plan.host_ids, host_tier.ptr)
     mark("tiers")
@@ -836,7 +857,21 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
                 except A.DgnnError:  # too many distinct window masks: keep the slot order
                     ho = None
         fine("c_hostorder")
-        if ho is not None:
+        if ho is None and table_host:  # no window ordering after all: the tier is materialized
+            host_tier = L.host_tier = ws.host("host_tier", plan.k_host * row_bytes) if ws is not None else \
+                HostBuffer(plan.k_host * row_bytes)
+            table_host = False
+        if ho is not None and table_host:
+            L.host_order, L.host_order_key = ho, (int(host_order), int(asm_out_budget))
+            L.host_table = features
+            ho.copies_dev(ctx)  # every window's copy list on the device (uploaded on the layout's stream)
+            ev = torch.cuda.Event()
+            ev.record(ctx.stream)  # phys_ids and the lists are in place: window 0 may be staged
+            L.host_w0_event = ev
+            stats["host_order"] = {"windows": ho.nwin, "groups": ho.n_groups, "source": "feature table",
+                                   "ranges_per_window": [len(r) // 3 for r in ho.ranges], "rows": ho.rows,
+                                   "rows_copied": ho.copy_rows, "arena_rows": ho.capacity}
+        elif ho is not None:
             L.host_order, L.host_order_key = ho, (int(host_order), int(asm_out_budget))
             # window 0's rows first (one contiguous range of the physical order), then the rest: the
             # assembler may stage window 0 as soon as its part is filled (Layout.early_host_prefetch)

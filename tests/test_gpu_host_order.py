@@ -95,3 +95,41 @@ def test_window_ordered_host_tier(dg, tiny, ref, W, budget, group):
         assert np.array_equal(out.view(torch.uint8).reshape(n_b, -1).cpu().numpy(), oracle.assemble(feats, nodes[b].nodes))
     ctx.sync()
     gctx.sync()
+
+
+@pytest.mark.parametrize("W,budget,group,early", [(2, 1 << 30, 8, False), (3, 600_000, 3, True)])
+def test_host_tier_read_from_the_table(dg, tiny, ref, W, budget, group, early):
+    """host_from_table (the feature table in pinned host memory, bench.py's e2e mode): no host-tier
+    copy is built; the windows' scheduled rows are gathered from the table (dgnn_gather_ranges) into
+    the same staging positions, so every assembled batch still equals the direct gather -- also with
+    window 0 staged ahead through early_host_prefetch."""
+    from paper_2405_05231_b200.layout import Workspace
+    ctx = dg.Ctx(device=0)
+    dev = torch.device("cuda", 0)
+    gctx = dg.Ctx(device=0, stream=torch.cuda.Stream())
+    hb = dg.HostBuffer(tiny.features.numel() * tiny.features.element_size())
+    f_host = hb.tensor.view(tiny.features.dtype).view(tiny.features.shape)
+    f_host.copy_(tiny.features)
+    L = dg.offline_layout(ctx, tiny.indptr.to(dev), tiny.indices.to(dev), f_host, tiny.seeds.to(dev), FAN, B,
+                          GPU_ROWS, HOST_ROWS, RNG_SEED, group_size=group, host_order=W, asm_out_budget=budget,
+                          host_from_table=True)
+    ctx.sync()
+    assert L.host_tier is None and L.host_table is not None and L.host_order is not None
+    feats = tiny.features.numpy()
+    nodes = ref["samples"]
+    ws = Workspace()
+    ev = L.early_host_prefetch(gctx, ws, W, budget, "_t") if early else None
+    assert (ev is not None) == early
+    n = 0
+    for b, out in L.assemble_epoch(host_window=W, gather_ctx=gctx, out_budget=budget, ws=ws, arena_tag="_t",
+                                   early=ev):
+        got = out.view(torch.uint8).reshape(out.shape[0], -1).cpu().numpy()
+        assert np.array_equal(got, oracle.assemble(feats, nodes[b].nodes)), f"batch {b}"
+        n += 1
+    assert n == len(nodes)
+    with pytest.raises(ValueError):  # no host-tier copy: other windows cannot read it
+        for _ in L.assemble_epoch(host_window=W + 3, gather_ctx=gctx, out_budget=budget):
+            pass
+    ctx.sync()
+    gctx.sync()
+    del hb
