@@ -133,3 +133,46 @@ def test_host_tier_read_from_the_table(dg, tiny, ref, W, budget, group, early):
     ctx.sync()
     gctx.sync()
     del hb
+
+
+@pytest.mark.slow
+def test_host_tier_read_from_the_table_products_scale(dg):
+    """The e2e leg's layout at products scale (192 batches, 2.4 M nodes, 400-byte rows, two windows
+    of 128 batches, 64 MB stage pieces, window 0 staged early): the table in pinned host memory,
+    the host tier read from it; every assembled batch equals the source rows of its nodes (the
+    generator's closed form on the GPU)."""
+    from paper_2405_05231_b200.layout import Workspace
+    from workload import CONFIGS, config_rows, feature_rows, make_features, make_graph, make_seeds
+    dev = torch.device("cuda", 0)
+    cfg = dict(CONFIGS["products"])
+    indptr, indices = make_graph(cfg["num_nodes"], cfg["num_edges"], cfg["degree"], cfg["skew"], 0, dev)
+    seeds = make_seeds(cfg["num_nodes"], cfg["num_seeds"], 0, dev)
+    feats = make_features(cfg["num_nodes"], cfg["dim"], dev, fseed=1)
+    hb = dg.HostBuffer(feats.numel() * 4)
+    f_host = hb.tensor.view(torch.float32).view(feats.shape)
+    f_host.copy_(feats.cpu())
+    del feats
+    gpu_rows, host_rows = config_rows(cfg)
+    ctx = dg.Ctx(device=0)
+    gctx = dg.Ctx(device=0, stream=torch.cuda.Stream())
+    budget = 256 << 20
+    L = dg.offline_layout(ctx, indptr, indices, f_host, seeds, cfg["fanout"], cfg["batch_size"], gpu_rows, host_rows,
+                          RNG_SEED, group_size=0, host_order=128, asm_out_budget=budget, host_from_table=True,
+                          stage_piece=64 << 20)
+    assert L.host_tier is None and L.host_order is not None and L.host_order.nwin == 2
+    ws = Workspace()
+    ev = L.early_host_prefetch(gctx, ws, 128, budget, "_p")
+    assert ev is not None
+    S = L.samples
+    n, bad = 0, []
+    for b, out in L.assemble_epoch(host_window=128, gather_ctx=gctx, out_budget=budget, ws=ws, arena_tag="_p",
+                                   early=ev):
+        n0, n1 = int(S.node_off_host[b]), int(S.node_off_host[b + 1])
+        exp = feature_rows(S.nodes[n0:n1].to(torch.int64), cfg["dim"], 1)
+        if not torch.equal(out.reshape(-1).view(torch.int32), exp.reshape(-1).view(torch.int32)):
+            bad.append(b)
+        n += 1
+    ctx.sync()
+    gctx.sync()
+    assert n == S.num_batches and bad == []
+    del hb
