@@ -338,6 +338,7 @@ class Runner:
             # it every 0.5 ms instead of the default 5 ms
             sys.setswitchinterval(float(os.environ.get("DGNN_SWITCH_INTERVAL", "0.0005")))
         self.asm_traces = []  # DGNN_ASM_TRACE=1: (assembly start event, per-window events)
+        self.side_traces = []  # DGNN_LAYOUT_TRACE=1: the layouts' side-stream (D2H) progress events
         self.observe = None  # test hook: observe(pass, batch, rows) for every assembled batch
         self.asm_host_ms = []  # host time of each assembly's enqueue (measurement only)
         self.asm_trace_on = os.environ.get("DGNN_ASM_TRACE") == "1"
@@ -510,6 +511,8 @@ class Runner:
         if getattr(L, "_asm_trace", None):
             self.asm_traces.append((a0, L._asm_trace))
         self.timeline.append(((L.stats.get("_events", []), L.stats.get("_host", [])), a0, ev_a))
+        if L.stats.get("_side"):
+            self.side_traces.append(L.stats["_side"])
         return ev_a
 
     def run(self, K: int, keep_last=False):
@@ -795,6 +798,7 @@ def main():
     gathered_rows = int(R.pcie_rows.item())
     timeline = R.timeline_ms()
     timed_trace = (list(R.asm_traces), list(R.timeline), list(R.early_trace))  # DGNN_ASM_TRACE: timed passes
+    side_traces = list(R.side_traces)
     # every kernel family, over extra instrumented passes (not part of the timed value)
     stat_steps = max(1, args.stat_steps)
     for c in R.ctxs():
@@ -1066,6 +1070,8 @@ def main():
         for (evs, _), a0_, a1_ in tl[-4:]:
             d = {name: round(t0.elapsed_time(ev), 1) for name, ev in evs}
             log(f"[asm-trace] layout {d} assembly {round(t0.elapsed_time(a0_), 1)}-{round(t0.elapsed_time(a1_), 1)}")
+        for sd in side_traces[-4:]:
+            log(f"[asm-trace] side stream {dict((n, round(t0.elapsed_time(e), 1)) for n, e in sd)}")
         for x, y, z in early[-4:]:
             log(f"[asm-trace] early copy issued {round(t0.elapsed_time(x), 1)} started "
                 f"{round(t0.elapsed_time(z), 1) if z is not None else None} done {round(t0.elapsed_time(y), 1)}")

@@ -717,6 +717,12 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
         if fine_marks:
             mark(name)
 
+    def side_mark(name):  # (DGNN_LAYOUT_TRACE=1) where the side stream's copies have got to
+        if fine_marks:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(torch.cuda.ExternalStream(ctx.side_stream_ptr, device=dev))
+            stats.setdefault("_side", []).append((name, e))
+
     mark("start")
     if counts is None:
         counts = torch.zeros(N, dtype=torch.int32, device=dev)
@@ -900,10 +906,12 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
                     t = A.dgnn_stage_copy(ctx, host_tier.ptr + int(lo) * rb, hbuf.data_ptr() + int(lo) * rb,
                                           (int(hi) - int(lo)) * rb, 0)
                 L.host_w0_ticket = t
+                side_mark("fill_w0_done")
                 for lo, hi in rest:
                     t = A.dgnn_stage_copy(ctx, host_tier.ptr + int(lo) * rb, hbuf.data_ptr() + int(lo) * rb,
                                           (int(hi) - int(lo)) * rb, 0)
                 L.host_fill_ticket = t
+                side_mark("fill_done")
                 fws.set_reader(ctx, "host_fill", t)
             else:  # SM stores into the pinned tier, window 0's range first
                 for lo, hi in first:
@@ -994,6 +1002,7 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
                 L.stage_pieces.append((b, e, t))
                 b = e
             group_last_ticket.append(L.stage_pieces[-1][2])
+            side_mark(f"stage_out_g{gi}_done")
         else:
             dst = arena_dev[g.arena_off:g.arena_off + max(g.group_bytes, 0)]
             A.dgnn_pack(ctx, features, ids, rel_po, rel_co, total, g.group_bytes, dst)
