@@ -1045,7 +1045,8 @@ def main():
                          "steps": args.e2e_steps,
                          "mode": args.e2e_mode,
                          "note": ("CSR and seeds copied from pinned host every step; the feature table stays in "
-                                  "pinned host memory (the paper's setting) and the tier fill and pack read the "
+                                  "pinned host memory (the paper's setting) and the GPU-tier fill, the host-tier "
+                                  "window staging (the host tier read from the table) and the pack read the "
                                   "rows they need from it in place (counted in h2d_bytes_per_step)"
                                   if host_feats else
                                   "inputs (CSR, features, seeds) copied from pinned host every step") +
