@@ -364,7 +364,7 @@ class Runner:
         self.slots = None  # shard.PeerSlots in the partitioned modes
         self.ws_n, self.slot_asm_ev = 1, [None, None]
         self.pack_alone = True  # pipelined: the HBM-bound pack waits for the previous assembly
-        self.host_window = 128
+        self.host_window = 256
         self.stage_piece = (512 << 20) if pipelined else (1 << 40)  # stage-out granularity (bytes)
         self.disk_budget_frac = None  # segmented disk cache off (unlimited disk budget, reading c18)
         self.train = False  # trainer stub after assembly (the training pipeline)
@@ -673,7 +673,7 @@ def main():
                     help="extra passes after the timed region with every kernel family timed (the kernels table)")
     ap.add_argument("--sequential", action="store_true",
                     help="no epoch pipelining: the layout of pass e+1 starts after the assembly of pass e")
-    ap.add_argument("--host-window", type=int, default=128,
+    ap.add_argument("--host-window", type=int, default=256,
                     help="batches per host-row merging window in a9 (1 = per-batch UVA reads, the paper's)")
     ap.add_argument("--blocks", action="store_true",
                     help="DGL-block sampling variant (reading c27): every node so far resamples at each hop")

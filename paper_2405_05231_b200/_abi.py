@@ -600,9 +600,11 @@ class HostOrder:
                                                          ctypes.byref(rows)), "dgnn_host_order_ranges")
             self.ranges.append(rg[:3 * int(nr.value)].copy())
             self.rows.append(int(rows.value))
-        # the staging schedule: one arena of two windows' rows; rows shared by consecutive windows
-        # are copied once (dgnn_host_order_schedule)
-        self.capacity = 2 * max(self.rows) if self.rows else 0
+        # the staging schedule: one arena of two windows' rows, but never more than the tier (the
+        # rows resident at a prefetch are those windows w-1 and w need, each group once, so k_host
+        # always fits); rows shared by consecutive windows are copied once, and spare room bridges the
+        # gaps between a group's runs (dgnn_host_order_schedule)
+        self.capacity = min(2 * max(self.rows), self.k_host) if self.rows else 0
         cap_t = 4 * cap * (self.nwin + 1) + 16
         co, mo = np.zeros(3 * cap_t, np.int64), np.zeros(3 * cap_t, np.int64)
         coff, moff = np.zeros(self.nwin + 1, np.int64), np.zeros(self.nwin + 1, np.int64)
