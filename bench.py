@@ -673,8 +673,9 @@ def main():
                     help="extra passes after the timed region with every kernel family timed (the kernels table)")
     ap.add_argument("--sequential", action="store_true",
                     help="no epoch pipelining: the layout of pass e+1 starts after the assembly of pass e")
-    ap.add_argument("--host-window", type=int, default=256,
-                    help="batches per host-row merging window in a9 (1 = per-batch UVA reads, the paper's)")
+    ap.add_argument("--host-window", type=int, default=None,
+                    help="batches per host-row merging window in a9 (1 = per-batch UVA reads, the paper's); "
+                         "default 256 on papers-shaped (5 windows), 128 elsewhere (measured: DESIGN.md §8)")
     ap.add_argument("--blocks", action="store_true",
                     help="DGL-block sampling variant (reading c27): every node so far resamples at each hop")
     ap.add_argument("--train", action="store_true",
@@ -733,6 +734,8 @@ def main():
     R = Runner(dg, inp, rank, dev, pipelined=not args.sequential)
     R.bid_base = bid_base
     R.setup_gpu_tier(args.gpu_tier, ws)
+    if args.host_window is None:
+        args.host_window = 256 if args.config == "papers" else 128
     R.host_window = args.host_window
     R.disk_budget_frac = args.disk_budget
     R.train = args.train or args.embed_graph
