@@ -507,8 +507,8 @@ struct Part {
     int64_t* bstart;  // [G * P + 1] bucket starts (exclusive scan of the counts), total at the end
     int64_t* bcur;    // [G * P] scatter cursors
     int32_t* bcnt;    // [G * P] candidates per bucket
-    int32_t* pu;      // [C] bucketed candidate IDs
-    int32_t* pi;      // [C] their candidate indices
+    int2* pui;        // [C] bucketed (candidate ID, candidate index) pairs: one 8-byte store per
+                      // candidate in the scatter, so a bin's run of pairs fills whole sectors
     unsigned long long* status;  // [G * P] look-back words of k_part_dedup
     unsigned int* ticket;        // bucket ticket counter
     int32_t B;        // batch size (seed slice stride)
@@ -650,8 +650,7 @@ __global__ void __launch_bounds__(kPartTileThreads) k_part_tile(Grp g, Part pt, 
                     atomicAdd(&pt.bcnt[b], 1);
                 } else {
                     const int64_t pos = atomicAdd((unsigned long long*)&pt.bcur[b], 1ull);
-                    pt.pu[pos] = u[it];
-                    pt.pi[pos] = (int32_t)i;
+                    pt.pui[pos] = make_int2(u[it], (int32_t)i);
                 }
             }
         }
@@ -671,8 +670,7 @@ __global__ void __launch_bounds__(kPartTileThreads) k_part_tile(Grp g, Part pt, 
                 for (int it = 0; it < kIt; ++it) {
                     if (bin[it] < 0) continue;
                     const int64_t pos = s_base[bin[it]] + rk[it];
-                    pt.pu[pos] = u[it];
-                    pt.pi[pos] = (int32_t)(t0 + it * kPartTileThreads + threadIdx.x);
+                    pt.pui[pos] = make_int2(u[it], (int32_t)(t0 + it * kPartTileThreads + threadIdx.x));
                 }
             }
             __syncthreads();
@@ -764,7 +762,7 @@ __global__ void __launch_bounds__(kPartThreads) k_part_dedup(Grp g, Part pt, int
             __syncthreads();
             // candidates: the first insert of an ID is a new node
             for (int64_t j = c0 + threadIdx.x; j < c1; j += blockDim.x) {
-                const int32_t u = pt.pu[j];
+                const int32_t u = pt.pui[j].x;
                 uint32_t q = part_hash(u, tlog);
                 for (int probes = 0;; ++probes) {
                     if (probes >= tsize) {  // unreachable below the limit; never spin
@@ -880,10 +878,10 @@ __global__ void __launch_bounds__(kPartThreads) k_part_dedup(Grp g, Part pt, int
             __syncthreads();
             // remap: every candidate of the bucket to its local ID
             for (int64_t j = c0 + threadIdx.x; j < c1; j += blockDim.x) {
-                const int32_t u = pt.pu[j];
-                uint32_t q = part_hash(u, tlog);
-                while (s_key[q] != u) q = (q + 1) & tmask;
-                cand[pt.pi[j]] = s_loc[q];
+                const int2 ui = pt.pui[j];
+                uint32_t q = part_hash(ui.x, tlog);
+                while (s_key[q] != ui.x) q = (q + 1) & tmask;
+                cand[ui.y] = s_loc[q];
             }
         }
         __syncthreads();
@@ -1032,27 +1030,24 @@ struct CompactPlan {
     int blocks;
 };
 
+// blockIdx.y = batch slot s: its nodes are one contiguous run in the slot's scratch and one in the
+// arena, so each CTA row copies its slot's run (no per-element search for the slot)
 __global__ void k_compact_nodes(CompactPlan p, const int32_t* __restrict__ gnodes, int32_t* __restrict__ out) {
-    __shared__ int64_t s_pre[kMaxGroup + 1];
-    for (int i = threadIdx.x; i <= p.G; i += blockDim.x) s_pre[i] = p.node_pre[i];
-    __syncthreads();
-    const int64_t T = s_pre[p.G];
-    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < T; q += (int64_t)gridDim.x * blockDim.x) {
-        const int s = segment_of(s_pre, p.G + 1, q);
-        out[q] = gnodes[(int64_t)s * p.cap_n + (q - s_pre[s])];
-    }
+    const int s = blockIdx.y;
+    const int64_t pre = p.node_pre[s], n = p.node_pre[s + 1] - pre;
+    const int32_t* src = gnodes + (int64_t)s * p.cap_n;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+        out[pre + j] = src[j];
 }
 
+// blockIdx.y = batch slot s: hop h's candidates of slot s are one contiguous run of cand
 __global__ void k_compact_edges(CompactPlan p, int h, const int32_t* __restrict__ cand, int32_t* __restrict__ out) {
-    __shared__ int64_t s_cb[kMaxGroup + 1];
+    const int s = blockIdx.y;
     const int64_t* cb = p.hop_cbase + h * (kMaxGroup + 1);
-    for (int i = threadIdx.x; i <= p.G; i += blockDim.x) s_cb[i] = cb[i];
-    __syncthreads();
-    const int64_t C = s_cb[p.G];
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < C; i += (int64_t)gridDim.x * blockDim.x) {
-        const int s = segment_of(s_cb, p.G + 1, i);
-        out[p.edge_pre[s] + p.edges_before[h * p.G + s] + (i - s_cb[s])] = cand[i];
-    }
+    const int64_t c0 = cb[s], n = cb[s + 1] - c0;
+    int32_t* dst = out + p.edge_pre[s] + p.edges_before[h * p.G + s];
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+        dst[j] = cand[c0 + j];
 }
 
 __global__ void k_compact_eptr(CompactPlan p, int32_t* __restrict__ out) {
@@ -1332,8 +1327,7 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
             sl.base = d_slab.p;
             carve(sl);
         }
-        pt.pu = d_npos;
-        pt.pi = d_ntab;
+        pt.pui = reinterpret_cast<int2*>(d_npos);  // spans d_npos and d_ntab (the hash-set path's pair)
         // hash-set path scratch (bucket sort arrays + the hash sets), taken when that path runs
         DevBuf<uint8_t> d_legacy;
         DevBuf<int32_t> d_tabs;
@@ -1656,8 +1650,8 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
             p.cptr = d_cptr_list;
             p.blocks = g.blocks;
             launch(c, DGNN_K_SAMPLE_COMPACT, 8.0 * node_pre[Gc], [&] {
-                k_compact_nodes<<<grid_for(c, node_pre[Gc], 256), 256, 0, c->stream>>>(p, g.nodes,
-                                                                                        a_nodes.p + used_nodes);
+                const int gx = std::max(1, grid_for(c, node_pre[Gc], 256) / Gc);
+                k_compact_nodes<<<dim3(gx, Gc), 256, 0, c->stream>>>(p, g.nodes, a_nodes.p + used_nodes);
             });
             DGNN_CK_LAUNCH();
             if (counts && node_pre[Gc] && !range_count) {  // one count per batch containing the node
@@ -1671,8 +1665,8 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
                 const int64_t Ch = h_cbs[h * (kMaxGroup + 1) + Gc];
                 if (Ch == 0) continue;
                 launch(c, DGNN_K_SAMPLE_COMPACT, 8.0 * Ch, [&] {
-                    k_compact_edges<<<grid_for(c, Ch, 256), 256, 0, c->stream>>>(p, h, d_cand[h],
-                                                                                 a_edges.p + used_edges);
+                    const int gx = std::max(1, grid_for(c, Ch, 256) / Gc);
+                    k_compact_edges<<<dim3(gx, Gc), 256, 0, c->stream>>>(p, h, d_cand[h], a_edges.p + used_edges);
                 });
                 DGNN_CK_LAUNCH();
             }
