@@ -129,27 +129,41 @@ __global__ void k_seed_range(const int32_t* __restrict__ seeds, int64_t n, int64
 }
 
 // ------------------------------------------------------ per-hop bookkeeping
+// frontier offsets of the group's slots: an exclusive scan over G <= kMaxGroup frontier sizes, one
+// thread per slot and one for the total (launched with kSlotThreads threads)
+constexpr int kSlotThreads = kMaxGroup + 32;
 __global__ void k_hop_begin(Grp g, int h) {
-    if (threadIdx.x != 0) return;
-    int64_t acc = 0;
-    for (int s = 0; s < g.G; ++s) {
-        g.fr_off[s] = acc;
-        g.hop_fr_off[h * (kMaxGroup + 1) + s] = acc;
-        acc += g.fr_hi[s] - g.fr_lo[s];
+    static_assert(kSlotThreads <= 1024 && kMaxGroup % 32 == 0, "one thread per slot");
+    __shared__ int64_t s_warp[kSlotThreads / 32];
+    const int s = threadIdx.x, lane = s & 31, w = s >> 5;
+    const int64_t len = s < g.G ? (int64_t)(g.fr_hi[s] - g.fr_lo[s]) : 0;
+    int64_t x = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
     }
-    g.fr_off[g.G] = acc;
-    g.hop_fr_off[h * (kMaxGroup + 1) + g.G] = acc;
+    if (lane == 31) s_warp[w] = x;
+    __syncthreads();
+    int64_t pre = x - len;
+    for (int k = 0; k < w; ++k) pre += s_warp[k];
+    if (s <= g.G) {  // s == G: the total (len 0 there)
+        g.fr_off[s] = pre;
+        g.hop_fr_off[h * (kMaxGroup + 1) + s] = pre;
+    }
 }
 
+// candidate bases of the group's slots (one thread per slot and one for the total, kSlotThreads)
 __global__ void k_hop_cands(Grp g, int h, int64_t* cptr) {
-    if (threadIdx.x != 0) return;
+    const int s = threadIdx.x;
     const int64_t F = g.fr_off[g.G];
-    cptr[F] = *g.cand_total;
-    for (int s = 0; s <= g.G; ++s) {
-        const int64_t c = cptr[g.fr_off[s]];
-        g.cand_base[s] = c;
-        g.hop_cbase[h * (kMaxGroup + 1) + s] = c;
-    }
+    if (s > g.G) return;
+    // (slots whose frontier offset is F -- the total, and empty trailing slots -- take the total)
+    const int64_t o = g.fr_off[s];
+    const int64_t c = o == F ? *g.cand_total : cptr[o];
+    if (s == g.G) cptr[F] = c;
+    g.cand_base[s] = c;
+    g.hop_cbase[h * (kMaxGroup + 1) + s] = c;
 }
 
 // new_off[s] = start of slot s's new nodes in the flattened bucket order
@@ -1441,13 +1455,13 @@ extern "C" dgnn_status dgnn_sample(dgnn_ctx* c, const dgnn_csr* csr, const int32
             for (int h = 0; h < H; ++h) {
                 const int k = fanout[h];
                 const int64_t fmax = Gc * fr_bound[h], cmax = Gc * cand_bound[h];
-                launch(c, DGNN_K_SAMPLE_SETUP, 0.0, [&] { k_hop_begin<<<1, 32, 0, c->stream>>>(g, h); });
+                launch(c, DGNN_K_SAMPLE_SETUP, 0.0, [&] { k_hop_begin<<<1, kSlotThreads, 0, c->stream>>>(g, h); });
                 DGNN_CK_LAUNCH();
                 // a2: candidate offsets (and the frontier's (v, start, deg) records)
                 DGNN_TRY(scan::run(c, fmax, g.fr_off + Gc, DegIn{g, csr->indptr, k, c->dev_err},
                                    StoreExcl{d_cptr[h]}, g.cand_total));
                 launch(c, DGNN_K_SAMPLE_SETUP, 0.0,
-                       [&] { k_hop_cands<<<1, 32, 0, c->stream>>>(g, h, d_cptr[h]); });
+                       [&] { k_hop_cands<<<1, kSlotThreads, 0, c->stream>>>(g, h, d_cptr[h]); });
                 DGNN_CK_LAUNCH();
                 // a2: draws + gather
                 if (k > 0) {
