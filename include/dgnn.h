@@ -277,6 +277,21 @@ dgnn_status dgnn_batch_tier_counts(dgnn_ctx* ctx, const dgnn_samples* samples, i
 dgnn_status dgnn_chunk_layout(const int64_t* packed_off_host, int64_t nb, int64_t row_bytes,
                               int64_t* chunk_off_host);
 
+/* Host arithmetic of the packing groups (the analogue of P:439's "C - 4N" partition sizing):
+ * consecutive batches, each group at most group_size batches (<= 0: unbounded) whose packed rows
+ * plus one 4 KiB page of padding per batch fit group_budget bytes (a group always holds at least one
+ * batch).  packed_off_host [nb+1] as from dgnn_classify; group_lo_host [nb+1] receives the first batch
+ * of every group followed by nb; *n_groups their count.  Errors: DGNN_EINVAL. */
+dgnn_status dgnn_packing_groups(const int64_t* packed_off_host, int64_t nb, int64_t row_bytes, int64_t group_size,
+                                int64_t group_budget, int64_t* group_lo_host, int64_t* n_groups);
+
+/* Host arithmetic of the assembler's runs (a9, one dgnn_assemble_group launch each): consecutive
+ * batches whose assembled rows fit max_rows (a run holds at least one batch, at most max_batches).
+ * node_off_host [nb+1] (the samples' node offsets); run_lo_host [nb+1] receives the first batch of
+ * every run followed by nb; *n_runs their count.  Errors: DGNN_EINVAL. */
+dgnn_status dgnn_assembly_runs(const int64_t* node_off_host, int64_t nb, int64_t max_rows, int64_t max_batches,
+                               int64_t* run_lo_host, int64_t* n_runs);
+
 /* The graph sample kept in the chunk ("the graph sample of the mini-batch is also kept in
  * the chunk"; reading c22b, opt-in).  Chunk i then holds its |P_i| packed rows at offset 0, and
  * at sec_off[i] = roundup(|P_i| * row_bytes, 16) a graph section of int32 words:

@@ -51,7 +51,7 @@ EXPORTS = [
     "dgnn_chunk_layout_graph", "dgnn_pack_graph", "dgnn_samples_load", "dgnn_samples_drop_device",
     "dgnn_host_order", "dgnn_host_order_ranges", "dgnn_host_window_ranges", "dgnn_copy_ranges", "dgnn_remap_ids_dev",
     "dgnn_pack_sharded", "dgnn_gather_rows_sharded", "dgnn_host_order_schedule", "dgnn_upload",
-    "dgnn_gather_ranges",
+    "dgnn_gather_ranges", "dgnn_packing_groups", "dgnn_assembly_runs",
 ]
 
 
@@ -150,6 +150,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "dgnn_host_window_ranges": (i32, [P, P, P, i64, i32, P, i64, P]),
             "dgnn_copy_ranges": (i32, [P, P, P, P, i64, i64]),
             "dgnn_upload": (i32, [P, P, P, i64]),
+            "dgnn_packing_groups": (i32, [P, i64, i64, i64, i64, P, ctypes.POINTER(i64)]),
+            "dgnn_assembly_runs": (i32, [P, i64, i64, i64, P, ctypes.POINTER(i64)]),
             "dgnn_gather_ranges": (i32, [P, P, i64, P, P, P, i64, i64, P]),
             "dgnn_remap_ids_dev": (i32, [P, P, P, i64, P]),
             "dgnn_host_order_schedule": (i32, [P, P, i64, i64, i32, i64, P, i64, P, P, i64, P,
@@ -512,6 +514,33 @@ def dgnn_batch_tier_counts(ctx: Ctx, samples: Samples, b_lo: int, b_hi: int, add
     _check(load_library().dgnn_batch_tier_counts(ctx.handle, samples.handle, int(b_lo), int(b_hi), _ptr(addr),
                                                  P(out.ctypes.data) if out.size else P(0)), "dgnn_batch_tier_counts")
     return out
+
+
+def dgnn_packing_groups(packed_off_host, row_bytes: int, group_size: int, group_budget: int):
+    """-> [(b_lo, b_hi)] packing groups of consecutive batches (host arithmetic in the library)."""
+    import numpy as np
+    po = np.ascontiguousarray(packed_off_host, dtype=np.int64)
+    nb = len(po) - 1
+    lo = np.zeros(nb + 1, np.int64)
+    n = i64()
+    _check(load_library().dgnn_packing_groups(P(po.ctypes.data), nb, int(row_bytes), int(group_size),
+                                              int(group_budget), P(lo.ctypes.data), ctypes.byref(n)),
+           "dgnn_packing_groups")
+    k = int(n.value)
+    return [(int(lo[i]), int(lo[i + 1]) if i + 1 < k else nb) for i in range(k)]
+
+
+def dgnn_assembly_runs(node_off_host, max_rows: int, max_batches: int = 1024):
+    """-> [(b_lo, b_hi)] assembler runs of consecutive batches (host arithmetic in the library)."""
+    import numpy as np
+    no = np.ascontiguousarray(node_off_host, dtype=np.int64)
+    nb = len(no) - 1
+    lo = np.zeros(nb + 1, np.int64)
+    n = i64()
+    _check(load_library().dgnn_assembly_runs(P(no.ctypes.data), nb, int(max_rows), int(max_batches),
+                                             P(lo.ctypes.data), ctypes.byref(n)), "dgnn_assembly_runs")
+    k = int(n.value)
+    return [(int(lo[i]), int(lo[i + 1]) if i + 1 < k else nb) for i in range(k)]
 
 
 def dgnn_chunk_layout(packed_off_host, row_bytes: int):

@@ -238,6 +238,42 @@ extern "C" dgnn_status dgnn_batch_tier_counts(dgnn_ctx* c, const dgnn_samples* S
     return DGNN_OK;
 }
 
+extern "C" dgnn_status dgnn_packing_groups(const int64_t* po, int64_t nb, int64_t row_bytes, int64_t group_size,
+                                           int64_t group_budget, int64_t* group_lo, int64_t* n_groups) {
+    DGNN_REQUIRE(po && group_lo && n_groups && nb >= 0 && row_bytes > 0, "dgnn_packing_groups: bad argument");
+    int64_t n = 0, g0 = 0;
+    while (g0 < nb) {
+        int64_t g1 = g0 + 1;
+        while (g1 < nb && (group_size <= 0 || g1 - g0 < group_size) &&
+               (po[g1 + 1] - po[g0]) * row_bytes + 4096 * (g1 + 1 - g0) <= group_budget)
+            ++g1;
+        group_lo[n++] = g0;
+        g0 = g1;
+    }
+    group_lo[n] = nb;
+    *n_groups = n;
+    return DGNN_OK;
+}
+
+extern "C" dgnn_status dgnn_assembly_runs(const int64_t* no, int64_t nb, int64_t max_rows, int64_t max_batches,
+                                          int64_t* run_lo, int64_t* n_runs) {
+    DGNN_REQUIRE(no && run_lo && n_runs && nb >= 0 && max_rows >= 1 && max_batches >= 1,
+                 "dgnn_assembly_runs: bad argument");
+    int64_t n = 0, b0 = 0;
+    while (b0 < nb) {
+        // the last b1 with no[b1] - no[b0] <= max_rows (upper bound in the non-decreasing offsets),
+        // then at least one batch, at most max_batches
+        const int64_t* it = std::upper_bound(no, no + nb + 1, no[b0] + max_rows);
+        int64_t b1 = (int64_t)(it - no) - 1;
+        b1 = std::min(std::max(b1, b0 + 1), std::min(b0 + max_batches, nb));
+        run_lo[n++] = b0;
+        b0 = b1;
+    }
+    run_lo[n] = nb;
+    *n_runs = n;
+    return DGNN_OK;
+}
+
 extern "C" dgnn_status dgnn_chunk_layout(const int64_t* packed_off_host, int64_t nb, int64_t row_bytes,
                                          int64_t* chunk_off_host) {
     DGNN_REQUIRE(packed_off_host && chunk_off_host && nb >= 0 && row_bytes > 0, "dgnn_chunk_layout: bad argument");

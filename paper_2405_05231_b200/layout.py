@@ -297,18 +297,14 @@ class Layout:
     def assembly_groups(self, out_budget: int = 1 << 30):
         """Runs of consecutive batches assembled per launch: the output of a run fits
         ``out_budget`` bytes and its chunks are one contiguous span of the disk tier."""
-        no = self.samples.node_off_host
-        groups = []
-        b0 = 0
-        nb = self.num_batches
-        max_rows = max(1, out_budget // self.row_bytes)
-        while b0 < nb:
-            # the last b1 with no[b1] - no[b0] <= max_rows, at least one batch, at most 1024
-            b1 = int(np.searchsorted(no, no[b0] + max_rows, side="right")) - 1
-            b1 = min(max(b1, b0 + 1), b0 + 1024, nb)
-            groups.append((b0, b1))
-            b0 = b1
-        return groups
+        # (dgnn_assembly_runs: the last b1 with no[b1] - no[b0] <= max_rows, at least one batch, at
+        # most 1024, cached per budget)
+        key = ("runs", int(out_budget))
+        runs = self._asm_plans.get(key)
+        if runs is None:
+            runs = A.dgnn_assembly_runs(self.samples.node_off_host, max(1, out_budget // self.row_bytes), 1024)
+            self._asm_plans[key] = runs
+        return runs
 
     def assembly_plan(self, out_budget: int = 1 << 30):
         """Per-run device tables (node offsets, chunk byte offsets, packed-row prefix, all
@@ -798,16 +794,11 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
     groups = []
     batch_chunk = np.zeros((nb, 2), np.int64)
     arena_off = 0
-    g0 = 0
     if embed_graph and (disk_budget is not None or dplan is not None):
         raise ValueError("embed_graph with the segmented disk cache is not supported")
-    while g0 < nb:
-        # a packing group: at most `group_size` batches (0 = unbounded) whose chunks fit the
-        # group-buffer budget (the analogue of P:439's "C - 4N" partition sizing)
-        g1 = g0 + 1
-        while g1 < nb and (group_size <= 0 or g1 - g0 < group_size) and \
-                (po[g1 + 1] - po[g0]) * row_bytes + 4096 * (g1 + 1 - g0) <= group_budget:
-            g1 += 1
+    # packing groups: at most `group_size` batches (0 = unbounded) whose chunks fit the group-buffer
+    # budget (the analogue of P:439's "C - 4N" partition sizing; dgnn_packing_groups)
+    for g0, g1 in (A.dgnn_packing_groups(po, row_bytes, group_size, group_budget) if nb else []):
         rel = po[g0:g1 + 1] - po[g0]
         so = None
         if embed_graph:
@@ -818,7 +809,6 @@ def offline_layout(ctx: A.Ctx, indptr: torch.Tensor, indices: torch.Tensor, feat
         batch_chunk[g0:g1, 0] = arena_off + co[:-1]
         batch_chunk[g0:g1, 1] = rows[g0:g1]
         arena_off += int(co[-1])
-        g0 = g1
     chunk_bytes = arena_off
     cache_off = arena_off
     if dplan is not None:
