@@ -285,7 +285,7 @@ dgnn_status dgnn_chunk_layout(const int64_t* packed_off_host, int64_t nb, int64_
 dgnn_status dgnn_packing_groups(const int64_t* packed_off_host, int64_t nb, int64_t row_bytes, int64_t group_size,
                                 int64_t group_budget, int64_t* group_lo_host, int64_t* n_groups);
 
-/* Host arithmetic of the assembler's runs (a9, one dgnn_assemble_group launch each): consecutive
+/* Host arithmetic of the assembler's runs (a9; one dgnn_assemble_group launch each): consecutive
  * batches whose assembled rows fit max_rows (a run holds at least one batch, at most max_batches).
  * node_off_host [nb+1] (the samples' node offsets); run_lo_host [nb+1] receives the first batch of
  * every run followed by nb; *n_runs their count.  Errors: DGNN_EINVAL. */
