@@ -292,6 +292,22 @@ dgnn_status dgnn_packing_groups(const int64_t* packed_off_host, int64_t nb, int6
 dgnn_status dgnn_assembly_runs(const int64_t* node_off_host, int64_t nb, int64_t max_rows, int64_t max_batches,
                                int64_t* run_lo_host, int64_t* n_runs);
 
+/* Host arithmetic of the per-run tables the run-level assembly reads (dgnn_assemble_group*), all
+ * relative to the run [b0, b1) = [run_lo[r], run_lo[r+1]), k = b1 - b0:
+ *   packed-only layout (disk_rows == NULL): node offsets no[b0..b1] - no[b0] (k+1), chunk byte
+ *     offsets chunk_start[b0..b1) - c_lo then c_hi - c_lo (k+1), packed-row prefix from b0 (k+1),
+ *     and with sec_abs (graph samples in the chunks) sec_abs[b0..b1) - c_lo (k);
+ *   segmented disk cache (disk_rows = DISK rows per batch): node offsets (k+1), dense partial-input
+ *     byte offsets dpre * row_bytes (k+1), dpre (k+1), chunk byte offsets (k+1);
+ * with c_lo = chunk_start[b0], c_hi = chunk_start[b1] (chunk_bytes past the last batch).  All host
+ * int64: node_off [nb+1], chunk_start / chunk_rows / disk_rows / sec_abs [nb]; tab receives the tables
+ * back to back (tab_off [n_runs+1] their starts; EINVAL past tab_cap); spans [4*n_runs] = (no[b0],
+ * no[b1], c_lo, c_hi) per run. */
+dgnn_status dgnn_assembly_tables(const int64_t* node_off, const int64_t* chunk_start, const int64_t* chunk_rows,
+                                 const int64_t* disk_rows, const int64_t* sec_abs, int64_t nb, int64_t chunk_bytes,
+                                 int64_t row_bytes, const int64_t* run_lo, int64_t n_runs, int64_t* tab,
+                                 int64_t tab_cap, int64_t* tab_off, int64_t* spans);
+
 /* The graph sample kept in the chunk ("the graph sample of the mini-batch is also kept in
  * the chunk"; reading c22b, opt-in).  Chunk i then holds its |P_i| packed rows at offset 0, and
  * at sec_off[i] = roundup(|P_i| * row_bytes, 16) a graph section of int32 words:

@@ -51,7 +51,7 @@ EXPORTS = [
     "dgnn_chunk_layout_graph", "dgnn_pack_graph", "dgnn_samples_load", "dgnn_samples_drop_device",
     "dgnn_host_order", "dgnn_host_order_ranges", "dgnn_host_window_ranges", "dgnn_copy_ranges", "dgnn_remap_ids_dev",
     "dgnn_pack_sharded", "dgnn_gather_rows_sharded", "dgnn_host_order_schedule", "dgnn_upload",
-    "dgnn_gather_ranges", "dgnn_packing_groups", "dgnn_assembly_runs",
+    "dgnn_gather_ranges", "dgnn_packing_groups", "dgnn_assembly_runs", "dgnn_assembly_tables",
 ]
 
 
@@ -152,6 +152,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "dgnn_upload": (i32, [P, P, P, i64]),
             "dgnn_packing_groups": (i32, [P, i64, i64, i64, i64, P, ctypes.POINTER(i64)]),
             "dgnn_assembly_runs": (i32, [P, i64, i64, i64, P, ctypes.POINTER(i64)]),
+            "dgnn_assembly_tables": (i32, [P, P, P, P, P, i64, i64, i64, P, i64, P, i64, P, P]),
             "dgnn_gather_ranges": (i32, [P, P, i64, P, P, P, i64, i64, P]),
             "dgnn_remap_ids_dev": (i32, [P, P, P, i64, P]),
             "dgnn_host_order_schedule": (i32, [P, P, i64, i64, i32, i64, P, i64, P, P, i64, P,
@@ -541,6 +542,29 @@ def dgnn_assembly_runs(node_off_host, max_rows: int, max_batches: int = 1024):
                                              P(lo.ctypes.data), ctypes.byref(n)), "dgnn_assembly_runs")
     k = int(n.value)
     return [(int(lo[i]), int(lo[i + 1]) if i + 1 < k else nb) for i in range(k)]
+
+
+def dgnn_assembly_tables(node_off, chunk_start, chunk_rows, disk_rows, sec_abs, chunk_bytes: int, row_bytes: int,
+                         runs):
+    """-> (flat int64 tables back to back, their offsets [n_runs+1], spans [(n0, n1, c_lo, c_hi)]) of
+    the assembler's runs (host arithmetic in the library; see dgnn.h)."""
+    import numpy as np
+
+    def arr(x):
+        return None if x is None else np.ascontiguousarray(x, dtype=np.int64)
+    no, cs, cr, dr, sc = arr(node_off), arr(chunk_start), arr(chunk_rows), arr(disk_rows), arr(sec_abs)
+    nb = len(no) - 1
+    lo = np.array([r[0] for r in runs] + ([runs[-1][1]] if runs else [0]), np.int64)
+    k_tot = sum(b1 - b0 for b0, b1 in runs)
+    cap = 4 * (k_tot + len(runs)) + 16
+    tab = np.zeros(cap, np.int64)
+    offs = np.zeros(len(runs) + 1, np.int64)
+    spans = np.zeros(4 * max(len(runs), 1), np.int64)
+    p = lambda a: P(a.ctypes.data) if a is not None else P(0)
+    _check(load_library().dgnn_assembly_tables(p(no), p(cs), p(cr), p(dr), p(sc), nb, int(chunk_bytes),
+                                               int(row_bytes), P(lo.ctypes.data), len(runs), P(tab.ctypes.data), cap,
+                                               P(offs.ctypes.data), P(spans.ctypes.data)), "dgnn_assembly_tables")
+    return tab[:int(offs[-1])].copy(), offs, [tuple(int(v) for v in spans[4 * r:4 * r + 4]) for r in range(len(runs))]
 
 
 def dgnn_chunk_layout(packed_off_host, row_bytes: int):

@@ -274,6 +274,55 @@ extern "C" dgnn_status dgnn_assembly_runs(const int64_t* no, int64_t nb, int64_t
     return DGNN_OK;
 }
 
+extern "C" dgnn_status dgnn_assembly_tables(const int64_t* no, const int64_t* cst, const int64_t* crows,
+                                            const int64_t* drows, const int64_t* sec, int64_t nb, int64_t chunk_bytes,
+                                            int64_t row_bytes, const int64_t* run_lo, int64_t n_runs, int64_t* tab,
+                                            int64_t tab_cap, int64_t* tab_off, int64_t* spans) {
+    DGNN_REQUIRE(no && cst && crows && run_lo && tab_off && spans && nb >= 0 && n_runs >= 0 && row_bytes > 0 &&
+                     (tab || tab_cap == 0),
+                 "dgnn_assembly_tables: bad argument");
+    int64_t o = 0;
+    auto put = [&](int64_t v) -> bool {
+        if (o >= tab_cap) return false;
+        tab[o++] = v;
+        return true;
+    };
+    for (int64_t r = 0; r < n_runs; ++r) {
+        const int64_t b0 = run_lo[r], b1 = run_lo[r + 1];
+        DGNN_REQUIRE(0 <= b0 && b0 < b1 && b1 <= nb, "dgnn_assembly_tables: bad run [%lld, %lld)", (long long)b0,
+                     (long long)b1);
+        const int64_t c_lo = cst[b0], c_hi = b1 < nb ? cst[b1] : chunk_bytes;
+        tab_off[r] = o;
+        bool ok = true;
+        for (int64_t b = b0; b <= b1; ++b) ok = ok && put(no[b] - no[b0]);
+        if (!drows) {
+            for (int64_t b = b0; b < b1; ++b) ok = ok && put(cst[b] - c_lo);
+            ok = ok && put(c_hi - c_lo);
+            int64_t acc = 0;
+            ok = ok && put(0);
+            for (int64_t b = b0; b < b1; ++b) ok = ok && put(acc += crows[b]);
+            if (sec)
+                for (int64_t b = b0; b < b1; ++b) ok = ok && put(sec[b] - c_lo);
+        } else {
+            int64_t acc = 0;
+            ok = ok && put(0);
+            for (int64_t b = b0; b < b1; ++b) ok = ok && put((acc += drows[b]) * row_bytes);
+            acc = 0;
+            ok = ok && put(0);
+            for (int64_t b = b0; b < b1; ++b) ok = ok && put(acc += drows[b]);
+            for (int64_t b = b0; b < b1; ++b) ok = ok && put(cst[b] - c_lo);
+            ok = ok && put(c_hi - c_lo);
+        }
+        DGNN_REQUIRE(ok, "dgnn_assembly_tables: tab_cap %lld too small", (long long)tab_cap);
+        spans[4 * r] = no[b0];
+        spans[4 * r + 1] = no[b1];
+        spans[4 * r + 2] = c_lo;
+        spans[4 * r + 3] = c_hi;
+    }
+    tab_off[n_runs] = o;
+    return DGNN_OK;
+}
+
 extern "C" dgnn_status dgnn_chunk_layout(const int64_t* packed_off_host, int64_t nb, int64_t row_bytes,
                                          int64_t* chunk_off_host) {
     DGNN_REQUIRE(packed_off_host && chunk_off_host && nb >= 0 && row_bytes > 0, "dgnn_chunk_layout: bad argument");

@@ -313,30 +313,20 @@ class Layout:
         plan = self._asm_plans.get(key)
         if plan is not None:
             return plan
-        nb = self.num_batches
         groups = self.assembly_groups(out_budget)
-        no = self.samples.node_off_host
-        rows_pre = np.concatenate([[0], np.cumsum(self.batch_chunk[:, 1])])
-        tabs, spans = [], []
-        for (b0, b1) in groups:
-            c_lo = int(self.batch_chunk[b0, 0])
-            # chunks of consecutive batches are contiguous (4 KiB-aligned) in the disk tier
-            c_hi = int(self.batch_chunk[b1, 0]) if b1 < nb else int(self.stats["chunk_bytes"])
-            chunk_off = np.concatenate([self.batch_chunk[b0:b1, 0] - c_lo, [c_hi - c_lo]])
-            if self.disk_plan is None:
-                tabs.append(np.concatenate([no[b0:b1 + 1] - no[b0], chunk_off, rows_pre[b0:b1 + 1] - rows_pre[b0]] +
-                                           ([self.sec_abs[b0:b1] - c_lo] if self.sec_abs is not None else [])))
-            else:  # a9 reads the partial input: dense DISK rows of the run in local order
-                dpre = np.concatenate([[0], np.cumsum(self.batch_tiers[b0:b1, 2])])
-                tabs.append(np.concatenate([no[b0:b1 + 1] - no[b0], dpre * self.row_bytes, dpre, chunk_off]))
-            spans.append((int(no[b0]), int(no[b1]), c_lo, c_hi))
+        # node offsets, chunk byte offsets and packed-row prefix of every run, relative to the run
+        # (chunks of consecutive batches are contiguous, 4 KiB-aligned, in the disk tier); with the
+        # segmented disk cache the dense partial-input offsets instead (dgnn_assembly_tables)
+        tab, offs, spans = A.dgnn_assembly_tables(
+            self.samples.node_off_host, self.batch_chunk[:, 0], self.batch_chunk[:, 1],
+            self.batch_tiers[:, 2] if self.disk_plan is not None else None,
+            self.sec_abs if self.disk_plan is None else None, int(self.stats["chunk_bytes"]), self.row_bytes, groups)
         # kernel-parameter upload (dgnn_upload): the host never waits for the layout's stream, and
         # the tables do not queue on a copy engine behind the window / stage copies in flight
-        flat = A.dgnn_upload(self.ctx, np.concatenate(tabs).astype(np.int64))
+        flat = A.dgnn_upload(self.ctx, tab)
         with torch.cuda.stream(self.ctx.stream):
             ready = torch.cuda.Event()
             ready.record(self.ctx.stream)  # tiers, address tables and these tables are in place
-        offs = np.concatenate([[0], np.cumsum([len(t) for t in tabs])])
         plan = (groups, spans, flat, offs, ready)
         self._asm_plans[key] = plan
         return plan

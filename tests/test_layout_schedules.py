@@ -50,3 +50,40 @@ def test_packing_groups_and_runs_match_their_definitions(trial):
 def test_bad_arguments():
     with pytest.raises(A.DgnnError):
         A.dgnn_assembly_runs(np.array([0, 5], np.int64), 0)
+
+
+def _tables_ref(no, cst, crows, drows, sec, chunk_bytes, rb, runs):
+    nb = len(no) - 1
+    rows_pre = np.concatenate([[0], np.cumsum(crows)])
+    tabs, spans = [], []
+    for b0, b1 in runs:
+        c_lo = int(cst[b0])
+        c_hi = int(cst[b1]) if b1 < nb else int(chunk_bytes)
+        chunk_off = np.concatenate([cst[b0:b1] - c_lo, [c_hi - c_lo]])
+        if drows is None:
+            tabs.append(np.concatenate([no[b0:b1 + 1] - no[b0], chunk_off, rows_pre[b0:b1 + 1] - rows_pre[b0]] +
+                                       ([sec[b0:b1] - c_lo] if sec is not None else [])))
+        else:
+            dpre = np.concatenate([[0], np.cumsum(drows[b0:b1])])
+            tabs.append(np.concatenate([no[b0:b1 + 1] - no[b0], dpre * rb, dpre, chunk_off]))
+        spans.append((int(no[b0]), int(no[b1]), c_lo, c_hi))
+    flat = np.concatenate(tabs).astype(np.int64) if tabs else np.zeros(0, np.int64)
+    offs = np.concatenate([[0], np.cumsum([len(t) for t in tabs])]).astype(np.int64)
+    return flat, offs, spans
+
+
+@pytest.mark.parametrize("trial", range(30))
+def test_assembly_tables_match_their_definition(trial):
+    rng = np.random.default_rng(1000 + trial)
+    nb = int(rng.integers(1, 300))
+    no = np.concatenate([[0], np.cumsum(rng.integers(1, 5000, nb))]).astype(np.int64)
+    rb = int(rng.choice([400, 512, 4096]))
+    crows = rng.integers(0, 3000, nb).astype(np.int64)
+    cst = np.concatenate([[0], np.cumsum((crows * rb + 4095) // 4096 * 4096)])[:nb].astype(np.int64) + 4096
+    chunk_bytes = int(cst[-1] + ((crows[-1] * rb + 4095) // 4096) * 4096) + 4096
+    drows = rng.integers(0, 3000, nb).astype(np.int64) if trial % 3 == 0 else None
+    sec = (cst + rng.integers(0, 4096, nb)).astype(np.int64) if (drows is None and trial % 2) else None
+    runs = A.dgnn_assembly_runs(no, int(rng.choice([1000, 50_000, 1 << 30])), int(rng.choice([1, 5, 1024])))
+    got = A.dgnn_assembly_tables(no, cst, crows, drows, sec, chunk_bytes, rb, runs)
+    want = _tables_ref(no, cst, crows, drows, sec, chunk_bytes, rb, runs)
+    assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1]) and got[2] == want[2]
