@@ -468,21 +468,21 @@ extern "C" dgnn_status dgnn_shard_requests(dgnn_ctx* c, const uint32_t* addr, in
         });
         DGNN_CK_LAUNCH();
     }
+    // the per-owner counts are the host's (the exchange sizes its all-to-all with them): the one
+    // synchronization of the call; the cursors go back in kernel parameters (no second wait)
     std::vector<unsigned long long> h(world);
-    DGNN_CK(cudaMemcpyAsync(h.data(), cnt.p, sizeof(unsigned long long) * world, cudaMemcpyDeviceToHost, c->stream));
-    DGNN_CK(cudaStreamSynchronize(c->stream));
+    DGNN_TRY(read_small(c, h.data(), cnt.p, sizeof(unsigned long long) * world));
     req_off_host[0] = 0;
     for (int o = 0; o < world; ++o) req_off_host[o + 1] = req_off_host[o] + (int64_t)h[o];
     if (req_off_host[world] == 0) return DGNN_OK;
     std::vector<unsigned long long> cur(world);
     for (int o = 0; o < world; ++o) cur[o] = (unsigned long long)req_off_host[o];
-    DGNN_CK(cudaMemcpyAsync(cnt.p, cur.data(), sizeof(unsigned long long) * world, cudaMemcpyHostToDevice, c->stream));
+    DGNN_TRY(upload_small(c, cnt.p, cur.data(), sizeof(unsigned long long) * world));
     launch(c, DGNN_K_ASSEMBLE, 0.0, [&] {
         k_owner_scatter<<<grid_for(c, n, 256, 4), 256, 0, c->stream>>>(addr, n, k_gpu, rank, world, cnt.p, req_slot,
                                                                         req_pos);
     });
     DGNN_CK_LAUNCH();
-    DGNN_CK(cudaStreamSynchronize(c->stream));  // `cur` (host) was a copy source
     return DGNN_OK;
 }
 
