@@ -966,6 +966,7 @@ __global__ void __launch_bounds__(kCntThreads) k_cnt_ranges(CntPlan c, uint32_t*
     extern __shared__ __align__(16) unsigned char s_dyn[];
     uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_dyn);
     __shared__ int64_t s_pre[kCntChunk + 1];
+    __shared__ int64_t s_base[kCntChunk];  // per slice of the chunk: node position of its run's entry 0 minus s_pre
     __shared__ int64_t s_wsum[kCntThreads / 32];
     const int64_t NS = c.nb * c.H;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -999,7 +1000,13 @@ __global__ void __launch_bounds__(kCntThreads) k_cnt_ranges(CntPlan c, uint32_t*
 #pragma unroll
             for (int k = 0; k < kPer; ++k) {
                 const int i = threadIdx.x * kPer + k;
-                if (i < ns) s_pre[i] = acc;
+                if (i < ns) {
+                    s_pre[i] = acc;
+                    const int64_t sl = s0 + i;
+                    const int64_t b = sl / c.H;
+                    const int x = (int)(sl - b * c.H) + 1;
+                    s_base[i] = c.node_off[b] + c.hop_off[b * (c.H + 2) + x] + lo_row[sl] - acc;
+                }
                 acc += len[k];
             }
             if (threadIdx.x == kCntThreads - 1) s_pre[ns] = acc;  // chunk total
@@ -1013,11 +1020,7 @@ __global__ void __launch_bounds__(kCntThreads) k_cnt_ranges(CntPlan c, uint32_t*
                     if (s_pre[mid] <= t) lo = mid;
                     else hi = mid;
                 }
-                const int64_t sl = s0 + lo;
-                const int64_t b = sl / c.H;
-                const int x = (int)(sl - b * c.H) + 1;
-                const int64_t pos = c.node_off[b] + c.hop_off[b * (c.H + 2) + x] + lo_row[sl] + (t - s_pre[lo]);
-                atomicAdd(&s_cnt[c.nodes[pos] - (p << kCntBits)], 1u);
+                atomicAdd(&s_cnt[c.nodes[s_base[lo] + t] - (p << kCntBits)], 1u);
             }
         }
         __syncthreads();
